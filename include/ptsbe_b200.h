@@ -1,0 +1,198 @@
+/*
+ * ptsbe_b200.h -- C ABI of libptsbe_b200.so, the B200 (sm_100a) drop-in for the
+ * PTSBE proportional hot path of the reference package `ptsbe`.
+ *
+ * The reference has no FFI seam (pure Python); the entry points below are what
+ * a ctypes binding inside the reference would call in place of the Python
+ * functions cited next to each of them (paths relative to
+ * /root/reference/pkg/src/ptsbe/).  INTEGRATION.md shows that binding.
+ *
+ * Conventions
+ *   - every function returns a ptsbe_status (0 = ok); the message of the last
+ *     failure on the calling thread is ptsbe_last_error();
+ *   - all pointers are HOST pointers unless the name ends in _dev;
+ *   - inputs are caller-owned and only read; variable-length outputs are
+ *     allocated by the library and released with ptsbe_free();
+ *   - a plan is immutable after creation and may be shared by threads; calls
+ *     that run kernels serialise on the plan's own CUDA stream;
+ *   - there is no CPU fallback: without a CUDA device every compute entry point
+ *     fails with PTSBE_EDEVICE.
+ */
+#ifndef PTSBE_B200_H
+#define PTSBE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PTSBE_OK = 0,
+  PTSBE_EINVAL = 1,      /* ValueError                                    */
+  PTSBE_ESTRUCT = 2,     /* errors.py: NetworkStructureError              */
+  PTSBE_ERESOURCE = 3,   /* errors.py: ResourceLimitError (ceiling/deadline) */
+  PTSBE_ENUMERIC = 4,    /* errors.py: NumericalError (engine.py:447-448) */
+  PTSBE_EIMPOSSIBLE = 5, /* errors.py: ImpossiblePrefixError (engine.py:475-476) */
+  PTSBE_EDEVICE = 6,     /* CUDA missing / runtime failure                */
+  PTSBE_ECAPACITY = 7    /* errors.py: CapacityError                      */
+} ptsbe_status;
+
+enum { PTSBE_C64 = 0, PTSBE_C128 = 1 };
+
+/* ---- compiled stage program (produced by paper_2604_08467_b200/compiler.py) ----
+ *
+ * A program is the stored contraction path of one (stage, pass) with every
+ * index map precomputed (replaces tensor.py:219-268 execute_path +
+ * tensor.py:190-216 contract_pair + engine.py:361-407 marginal_network).
+ *
+ * leaves : n_leaves x 4 words  {pool_off, size, sel_kind, sel_arg}
+ *          sel_kind 0: constant            data = pool[pool_off .. +size)
+ *          sel_kind 1: Kraus variant       data = pool[pool_off + kraus_idx[e][sel_arg]*size ..)
+ *                      (UPV merge, engine.py:284-313, done once on the host per variant)
+ *          sel_kind 2: prefix bit          data = pool[pool_off + bit(sel_arg)*size ..)
+ *                      (basis vectors of engine.py:395-399)
+ * steps  : n_steps x 12 words {a_kind, a_ref, b_kind, b_ref, o_kind, o_ref,
+ *                              out_n, k_n, lo_n, hi_n, tab_off, reserved}
+ *          operand kind 0: arena offset (elements), 1: leaf index,
+ *                       2 + p: record of pass p of the same stage, a_ref = offset in record
+ *          output  kind 0: arena offset, 1: offset in this pass's output record
+ * tables : u32 offsets; for a step: loA[lo_n] loB[lo_n] hiA[hi_n] hiB[hi_n] kA[k_n] kB[k_n]
+ *          out[c] = sum_k A[loA[c%lo_n]+hiA[c/lo_n]+kA[k]] * B[loB[..]+hiB[..]+kB[k]]
+ */
+typedef struct {
+  uint32_t n_leaves;
+  uint32_t n_steps;
+  uint32_t n_table_words;
+  uint32_t arena_fast_elems;  /* per-item shared-memory arena, in complex elements   */
+  uint32_t arena_spill_elems; /* per-item global spill arena (offsets >= arena_fast) */
+  uint32_t out_elems;         /* complex elements per output record                  */
+  uint32_t threads_per_item;  /* 32 (warp per item) or a CTA size up to 1024         */
+  uint32_t level;             /* 1-based item level this pass iterates over          */
+  uint32_t result_kind;       /* where the finished record lives: 0 arena, 1 leaf, 2 record */
+  uint32_t result_ref;
+  const uint32_t* leaves;
+  const uint32_t* steps;
+  const uint32_t* tables;
+} ptsbe_program_desc;
+
+typedef struct {
+  uint32_t dtype;     /* PTSBE_C64 | PTSBE_C128 */
+  uint32_t n_qubits;
+  uint32_t n_sites;   /* g: gate sites = columns of kraus_idx */
+  uint32_t n_stages;  /* f */
+  const uint32_t* stage_sizes; /* b_1..b_f (engine.py:76-142 BatchPlan.sizes) */
+  const void* pool;   /* operand values: interleaved re,im of dtype precision */
+  uint64_t pool_elems;
+  /* stage j (1-based) owns passes 0..j-1; pass p iterates over the unique
+   * prefixes entering stage p+1 (p = j-1 is the marginal pass itself) */
+  const ptsbe_program_desc* programs; /* stage-major, f*(f+1)/2 entries */
+  uint64_t max_intermediate;          /* ceiling, informational (checked at compile time) */
+} ptsbe_plan_desc;
+
+typedef struct ptsbe_plan ptsbe_plan;
+
+/* per-run statistics (mirrors engine.py:155-181 EngineStats + RunResult counters) */
+#define PTSBE_MAX_STAGES 64
+typedef struct {
+  uint64_t stage_events[PTSBE_MAX_STAGES]; /* U_j = unique prefixes contracted in stage j */
+  float stage_ms[PTSBE_MAX_STAGES];        /* device time per stage (CUDA events)          */
+  uint64_t gpu_launches;                   /* kernels launched by this call               */
+  uint64_t total_shots;
+  uint64_t n_records;
+  float loop_ms;      /* contraction + sampling + local histogram, device timed */
+  float h2d_ms;
+  float d2h_ms;
+  uint64_t h2d_bytes;
+  uint64_t d2h_bytes;
+  uint32_t n_chunks;
+  uint32_t flagged_sets; /* error sets with vanishing mass / negative diagonal */
+  int64_t first_flagged_id;
+  uint32_t first_flag_kind; /* PTSBE_ENUMERIC or PTSBE_EIMPOSSIBLE */
+  uint32_t first_flag_stage;
+} ptsbe_run_stats;
+
+const char* ptsbe_last_error(void);
+int ptsbe_device_count(void);
+const char* ptsbe_version(void);
+
+/* replaces: building + caching the stage networks and paths once per run
+ * (engine.py:864-879 warm loop; planner.py:343-442 PathCache) */
+int ptsbe_plan_create(const ptsbe_plan_desc* desc, int device, ptsbe_plan** out);
+void ptsbe_plan_destroy(ptsbe_plan* plan);
+
+/* replaces: conditional_marginal / _contract_marginal for a batch of W work
+ * items of one stage (engine.py:417-477).
+ *   kraus_idx [W][g] variant index per site, prefixes [W][words] packed bits
+ *   (qubit q -> word q/64, bit 63-(q%64)), words = ceil(n_qubits/64) (>=1).
+ *   out_probs [W][2^b] UNNORMALISED clamped populations, float64;
+ *   out_mass[W], out_min[W] = sum and minimum before clamping (guards are the
+ *   caller's: engine.py:445-450, 475-476). */
+int ptsbe_marginals(ptsbe_plan* plan, uint32_t stage, const uint8_t* kraus_idx,
+                    const uint64_t* prefixes, uint64_t n_items, double* out_probs,
+                    double* out_mass, double* out_min);
+
+/* replaces: execute_path / contract_pair on one constant network
+ * (tensor.py:190-268): runs the single program of a 1-stage plan for one item
+ * and returns the complex result (out_elems values of the plan's dtype). */
+int ptsbe_execute_raw(ptsbe_plan* plan, void* out_complex);
+
+/* replaces: the multinomial split of one stage (engine.py:519-522) on given
+ * float64 marginals, for sampler parity tests.  item w draws mult[w] outcomes
+ * from probs[w][0..2^b) with Philox-4x32-10 counters
+ * (draw, rank[w], stage, eset_id[w]) and key = seed.  Outputs: child_item[],
+ * child_index[], child_count[] in item-major, index-ascending order. */
+int ptsbe_sample_stage(uint32_t b, uint32_t stage, uint64_t seed, uint64_t n_items,
+                       const double* probs, const uint32_t* mult, const uint32_t* eset_id,
+                       const uint32_t* rank, uint32_t** child_item, uint32_t** child_index,
+                       uint32_t** child_count, uint64_t* n_children, int device);
+
+/* replaces: the fan-out over error sets + merge_records
+ * (engine.py:885-906, sample_proportional engine.py:493-524, merge_records 815-829).
+ *   kraus_idx [E][g], shots [E] (>=1), eset_ids [E] global ids used for the RNG
+ *   streams (results do not depend on how error sets are split across calls).
+ *   merged != 0: one histogram over all error sets, records sorted by key;
+ *   merged == 0: per-error-set records, sorted by (position in this call, key),
+ *                rec_eset[] filled with the position.
+ *   keys [n_records][words]. */
+int ptsbe_sample(ptsbe_plan* plan, const uint8_t* kraus_idx, const uint32_t* shots,
+                 const uint32_t* eset_ids, uint64_t n_sets, uint64_t seed, int merged,
+                 uint64_t** keys, uint32_t** rec_eset, uint64_t** counts,
+                 uint64_t* n_records, ptsbe_run_stats* stats);
+
+/* resident variant for device-timed throughput: inputs are uploaded once,
+ * every run leaves its histogram on the device and returns only its length. */
+typedef struct ptsbe_batch ptsbe_batch;
+int ptsbe_batch_upload(ptsbe_plan* plan, const uint8_t* kraus_idx, const uint32_t* shots,
+                       const uint32_t* eset_ids, uint64_t n_sets, ptsbe_batch** out);
+int ptsbe_batch_run(ptsbe_batch* batch, uint64_t seed, uint64_t* n_records,
+                    ptsbe_run_stats* stats);
+/* copy the histogram of the last run to the host (library-allocated) */
+int ptsbe_batch_fetch(ptsbe_batch* batch, uint64_t** keys, uint64_t** counts,
+                      uint64_t* n_records);
+void ptsbe_batch_destroy(ptsbe_batch* batch);
+
+/* replaces: merge_records across ranks after the gather (engine.py:815-829):
+ * sums counts of equal keys, output sorted by key. keys [n][words]. */
+int ptsbe_histogram_merge(const uint64_t* keys, const uint64_t* counts, uint64_t n,
+                          uint32_t words, uint64_t** out_keys, uint64_t** out_counts,
+                          uint64_t* n_out, int device);
+
+/* replaces: find_path_greedy (planner.py:121-251), host code.
+ *   operands are given as CSR lists of (label, dim); op_class / class_weight
+ *   (optional, may be NULL) weight a step by the number of distinct instances
+ *   of its result across the batch (error-independent hoisting).
+ *   merges_out [2*(n_ops-1)] stable-id pairs (result keeps the smaller id). */
+int ptsbe_plan_greedy(uint32_t n_ops, const uint32_t* op_ptr, const int64_t* labels,
+                      const uint32_t* dims, const uint32_t* op_class,
+                      const double* class_weight, uint32_t n_classes, uint32_t hypersamples,
+                      uint64_t seed, double size_cap_log2, uint32_t* merges_out,
+                      double* cost_out, double* flops_out);
+
+void ptsbe_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PTSBE_B200_H */

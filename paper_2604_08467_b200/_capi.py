@@ -1,0 +1,279 @@
+"""ctypes binding of libptsbe_b200.so (include/ptsbe_b200.h).
+
+This is the whole Python<->CUDA boundary: plain pointers and sizes, no torch
+types.  The library is built in-tree by `__graft_entry__.build()` (or
+`make -C paper_2604_08467_b200/csrc`).  There is no CPU fallback: if the
+library is missing or no CUDA device is present, compute calls raise
+`DeviceError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+from .compiler import CompiledPlan, ConstantProgram, PlanDesc
+from .errors import STATUS_TO_ERROR, DeviceError
+
+LIB_NAME = "libptsbe_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+MAX_STAGES = 64
+
+EXPORTS = (
+    "ptsbe_last_error", "ptsbe_device_count", "ptsbe_version", "ptsbe_plan_create",
+    "ptsbe_plan_destroy", "ptsbe_marginals", "ptsbe_execute_raw", "ptsbe_sample_stage",
+    "ptsbe_sample", "ptsbe_batch_upload", "ptsbe_batch_run", "ptsbe_batch_fetch",
+    "ptsbe_batch_destroy", "ptsbe_histogram_merge", "ptsbe_plan_greedy", "ptsbe_free",
+)
+
+
+class RunStats(ctypes.Structure):
+    _fields_ = [
+        ("stage_events", ctypes.c_uint64 * MAX_STAGES),
+        ("stage_ms", ctypes.c_float * MAX_STAGES),
+        ("gpu_launches", ctypes.c_uint64),
+        ("total_shots", ctypes.c_uint64),
+        ("n_records", ctypes.c_uint64),
+        ("loop_ms", ctypes.c_float),
+        ("h2d_ms", ctypes.c_float),
+        ("d2h_ms", ctypes.c_float),
+        ("h2d_bytes", ctypes.c_uint64),
+        ("d2h_bytes", ctypes.c_uint64),
+        ("n_chunks", ctypes.c_uint32),
+        ("flagged_sets", ctypes.c_uint32),
+        ("first_flagged_id", ctypes.c_int64),
+        ("first_flag_kind", ctypes.c_uint32),
+        ("first_flag_stage", ctypes.c_uint32),
+    ]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """dlopen the in-tree library; loud failure when it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise DeviceError(
+            f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)"
+        )
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+    except OSError as exc:  # pragma: no cover - depends on the box
+        raise DeviceError(f"cannot load {LIB_PATH}: {exc}") from exc
+    P, U64, U32, I = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
+    lib.ptsbe_last_error.restype = ctypes.c_char_p
+    lib.ptsbe_version.restype = ctypes.c_char_p
+    lib.ptsbe_device_count.restype = I
+    lib.ptsbe_plan_create.argtypes = [ctypes.POINTER(PlanDesc), I, ctypes.POINTER(P)]
+    lib.ptsbe_plan_destroy.argtypes = [P]
+    lib.ptsbe_plan_destroy.restype = None
+    lib.ptsbe_marginals.argtypes = [P, U32, P, P, U64, P, P, P]
+    lib.ptsbe_execute_raw.argtypes = [P, P]
+    lib.ptsbe_sample_stage.argtypes = [U32, U32, U64, U64, P, P, P, P,
+                                       ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P),
+                                       ctypes.POINTER(U64), I]
+    lib.ptsbe_sample.argtypes = [P, P, P, P, U64, U64, I, ctypes.POINTER(P), ctypes.POINTER(P),
+                                 ctypes.POINTER(P), ctypes.POINTER(U64), ctypes.POINTER(RunStats)]
+    lib.ptsbe_batch_upload.argtypes = [P, P, P, P, U64, ctypes.POINTER(P)]
+    lib.ptsbe_batch_run.argtypes = [P, U64, ctypes.POINTER(U64), ctypes.POINTER(RunStats)]
+    lib.ptsbe_batch_fetch.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(U64)]
+    lib.ptsbe_batch_destroy.argtypes = [P]
+    lib.ptsbe_batch_destroy.restype = None
+    lib.ptsbe_histogram_merge.argtypes = [P, P, U64, U32, ctypes.POINTER(P), ctypes.POINTER(P),
+                                          ctypes.POINTER(U64), I]
+    lib.ptsbe_plan_greedy.argtypes = [U32, P, P, P, P, P, U32, U32, U64, ctypes.c_double, P,
+                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    lib.ptsbe_free.argtypes = [P]
+    lib.ptsbe_free.restype = None
+    _lib = lib
+    return lib
+
+
+def device_count() -> int:
+    return int(load().ptsbe_device_count())
+
+
+def check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = load().ptsbe_last_error().decode("utf-8", "replace")
+    raise STATUS_TO_ERROR.get(rc, DeviceError)(msg)
+
+
+def _take(ptr: ctypes.c_void_p, count: int, dtype) -> np.ndarray:
+    """Copy a library-allocated array into numpy and release it."""
+    lib = load()
+    if not ptr.value:
+        return np.zeros(0, dtype=dtype)
+    n = int(count)
+    buf = (ctypes.c_char * (n * np.dtype(dtype).itemsize)).from_address(ptr.value)
+    out = np.frombuffer(buf, dtype=dtype, count=n).copy()
+    lib.ptsbe_free(ptr)
+    return out
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+class ResidentBatch:
+    """Error sets uploaded once; each `run` leaves its histogram in HBM."""
+
+    def __init__(self, plan: "DevicePlan", kraus_idx, shots, eset_ids):
+        self.plan = plan
+        self._h = ctypes.c_void_p()
+        kraus_idx = np.ascontiguousarray(kraus_idx, dtype=np.uint8)
+        shots = np.ascontiguousarray(shots, dtype=np.uint32)
+        ids = None if eset_ids is None else np.ascontiguousarray(eset_ids, dtype=np.uint32)
+        check(load().ptsbe_batch_upload(plan._h, _ptr(kraus_idx), _ptr(shots), _ptr(ids),
+                                        shots.size, ctypes.byref(self._h)))
+
+    def run(self, seed: int) -> tuple[int, RunStats]:
+        st = RunStats()
+        n = ctypes.c_uint64()
+        check(load().ptsbe_batch_run(self._h, seed & (2**64 - 1), ctypes.byref(n), ctypes.byref(st)))
+        return int(n.value), st
+
+    def fetch(self) -> tuple[np.ndarray, np.ndarray]:
+        k, c, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
+        check(load().ptsbe_batch_fetch(self._h, ctypes.byref(k), ctypes.byref(c), ctypes.byref(n)))
+        w = self.plan.words
+        return _take(k, n.value * w, np.uint64).reshape(-1, w), _take(c, n.value, np.uint64)
+
+    def close(self):
+        if self._h:
+            load().ptsbe_batch_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DevicePlan:
+    """Owner of a `ptsbe_plan*`."""
+
+    def __init__(self, compiled: CompiledPlan, device: int = 0):
+        lib = load()
+        self.compiled = compiled
+        self.words = max(1, (compiled.n_qubits + 63) // 64)
+        self.n_sites = compiled.n_sites
+        self._h = ctypes.c_void_p()
+        desc = compiled.descriptor()
+        check(lib.ptsbe_plan_create(ctypes.byref(desc), device, ctypes.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            load().ptsbe_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def marginals(self, stage: int, kraus_idx: np.ndarray, prefixes: np.ndarray):
+        """(probs [W, 2^b] float64 unnormalised+clamped, mass [W], min [W])."""
+        kraus_idx = np.ascontiguousarray(kraus_idx, dtype=np.uint8)
+        w = kraus_idx.shape[0]
+        prefixes = np.ascontiguousarray(prefixes, dtype=np.uint64).reshape(w, self.words)
+        nb = 1 << self.compiled.sizes[stage - 1]
+        probs = np.empty((w, nb), dtype=np.float64)
+        mass = np.empty(w, dtype=np.float64)
+        mn = np.empty(w, dtype=np.float64)
+        check(load().ptsbe_marginals(self._h, stage, _ptr(kraus_idx), _ptr(prefixes), w,
+                                     _ptr(probs), _ptr(mass), _ptr(mn)))
+        return probs, mass, mn
+
+    def execute_raw(self, out: np.ndarray) -> None:
+        check(load().ptsbe_execute_raw(self._h, _ptr(out)))
+
+    def sample(self, kraus_idx, shots, eset_ids, seed: int, merged: bool = True):
+        """Host-buffer entry point: returns (keys [R, words] u64, eset [R] or None,
+        counts [R] u64, RunStats)."""
+        kraus_idx = np.ascontiguousarray(kraus_idx, dtype=np.uint8)
+        shots = np.ascontiguousarray(shots, dtype=np.uint32)
+        ids = None if eset_ids is None else np.ascontiguousarray(eset_ids, dtype=np.uint32)
+        k, e, c, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
+        st = RunStats()
+        check(load().ptsbe_sample(self._h, _ptr(kraus_idx), _ptr(shots), _ptr(ids), shots.size,
+                                  seed & (2**64 - 1), 1 if merged else 0, ctypes.byref(k),
+                                  ctypes.byref(e), ctypes.byref(c), ctypes.byref(n), ctypes.byref(st)))
+        keys = _take(k, n.value * self.words, np.uint64).reshape(-1, self.words)
+        counts = _take(c, n.value, np.uint64)
+        esets = None if merged else _take(e, n.value, np.uint32)
+        return keys, esets, counts, st
+
+    def upload(self, kraus_idx, shots, eset_ids=None) -> ResidentBatch:
+        return ResidentBatch(self, kraus_idx, shots, eset_ids)
+
+
+def run_constant_program(cp: ConstantProgram) -> np.ndarray:
+    """Execute a constant one-item program (tensor.execute_path on the device)."""
+    compiled = CompiledPlan(dtype="complex128", n_qubits=1, n_sites=0, sizes=(1,), pool=cp.pool,
+                            programs=[cp.program], max_intermediate=0)
+    plan = DevicePlan(compiled)
+    try:
+        out = np.empty(max(cp.program.out_elems, 1), dtype=np.complex128)
+        plan.execute_raw(out)
+    finally:
+        plan.close()
+    return out[: cp.program.out_elems].reshape(cp.out_shape)
+
+
+def sample_stage(b: int, stage: int, seed: int, probs, mult, eset_id, rank, device: int = 0):
+    """Sampler-only probe (ptsbe_sample_stage): children as (item, index, count)."""
+    probs = np.ascontiguousarray(probs, dtype=np.float64).reshape(-1, 1 << b)
+    w = probs.shape[0]
+    mult = np.ascontiguousarray(mult, dtype=np.uint32)
+    eset_id = np.ascontiguousarray(eset_id, dtype=np.uint32)
+    rank = np.ascontiguousarray(rank, dtype=np.uint32)
+    ci, cx, cc, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
+    check(load().ptsbe_sample_stage(b, stage, seed & (2**64 - 1), w, _ptr(probs), _ptr(mult),
+                                    _ptr(eset_id), _ptr(rank), ctypes.byref(ci), ctypes.byref(cx),
+                                    ctypes.byref(cc), ctypes.byref(n), device))
+    return _take(ci, n.value, np.uint32), _take(cx, n.value, np.uint32), _take(cc, n.value, np.uint32)
+
+
+def histogram_merge(keys, counts, device: int = 0):
+    """Device sort + reduce-by-key of (key, count) records (merge_records)."""
+    keys = np.ascontiguousarray(keys, dtype=np.uint64)
+    if keys.ndim == 1:
+        keys = keys.reshape(-1, 1)
+    counts = np.ascontiguousarray(counts, dtype=np.uint64)
+    ok, oc, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
+    check(load().ptsbe_histogram_merge(_ptr(keys), _ptr(counts), counts.size, keys.shape[1],
+                                       ctypes.byref(ok), ctypes.byref(oc), ctypes.byref(n), device))
+    w = keys.shape[1]
+    return _take(ok, n.value * w, np.uint64).reshape(-1, w), _take(oc, n.value, np.uint64)
+
+
+def plan_greedy(op_labels, op_dims, op_class=None, class_weight=None, hypersamples=100,
+                seed=0, size_cap_log2=0.0):
+    """Host planner core (csrc/planner.cpp).  Returns (merges [(x, y)...] over
+    stable operand ids, weighted cost, reference flop estimate)."""
+    n = len(op_labels)
+    ptr = np.zeros(n + 1, dtype=np.uint32)
+    for k, lb in enumerate(op_labels):
+        ptr[k + 1] = ptr[k] + len(lb)
+    labels = np.asarray([l for lb in op_labels for l in lb], dtype=np.int64)
+    dims = np.asarray([d for ds in op_dims for d in ds], dtype=np.uint32)
+    cls = None if op_class is None else np.ascontiguousarray(op_class, dtype=np.uint32)
+    cw = None if class_weight is None else np.ascontiguousarray(class_weight, dtype=np.float64)
+    merges = np.zeros(2 * max(n - 1, 1), dtype=np.uint32)
+    cost, flops = ctypes.c_double(), ctypes.c_double()
+    check(load().ptsbe_plan_greedy(n, _ptr(ptr), _ptr(labels), _ptr(dims), _ptr(cls), _ptr(cw),
+                                   0 if cw is None else cw.size, hypersamples, seed & (2**64 - 1),
+                                   float(size_cap_log2), _ptr(merges), ctypes.byref(cost),
+                                   ctypes.byref(flops)))
+    return merges[: 2 * (n - 1)].reshape(-1, 2), cost.value, flops.value

@@ -1,0 +1,487 @@
+"""Stage-program compiler: (stage network structure, stored path) -> flat device
+programs for `csrc/executor.cuh`.
+
+What the reference does per contraction at run time -- rebuild the sandwich
+network (engine.py:361-407), conjugate every operand (tensor.py:87-88), look
+the path up and validate it (planner.py:416-442), dispatch one np.tensordot
+per step (tensor.py:236-259) and transpose the result (engine.py:442) -- is
+done here ONCE per (circuit structure, batch plan): every step gets
+precomputed gather tables, every intermediate gets an arena offset from a
+liveness analysis, the bra half is stored pre-conjugated in the operand pool
+and the output permutation is folded into the last step.
+
+Error-independent hoisting (north-star subsystem 1): every node of the
+contraction tree is tagged with the newest thing its value depends on --
+class 0: the error set only; class s: also prefix bits measured in stage s.
+Nodes of class p are evaluated in "pass p", once per unique prefix entering
+stage p+1, and handed to later passes as records in HBM.  Only the nodes
+whose class is j-1 are recomputed for every stage-j work item.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from .errors import CapacityError, IncompletePathError, NetworkStructureError, ResourceLimitError
+
+SEL_CONST, SEL_KRAUS, SEL_PREFIX = 0, 1, 2
+STEP_WORDS, LEAF_WORDS = 12, 4
+LO_TABLE_MAX = 1024          # entries in the per-lane (low) gather table of a step
+SMEM_BYTES = 200 * 1024      # shared memory a single work item may claim
+WARP_ARENA_BYTES = 6 * 1024  # beyond this a warp-per-item mapping starves occupancy
+
+
+@dataclass
+class Operand:
+    """One leaf of a stage network.  `data` is [variants, size] complex128,
+    row-major over `labels`; the variant is chosen per work item by the Kraus
+    index of gate site `sel_arg` (SEL_KRAUS) or by prefix bit `sel_arg`
+    (SEL_PREFIX)."""
+
+    labels: tuple
+    dims: tuple
+    data: np.ndarray
+    sel_kind: int = SEL_CONST
+    sel_arg: int = 0
+    cls: int = 0
+
+
+class Pool:
+    """Operand value pool shared by all programs of a plan; identical blocks
+    (kets, basis vectors, copy tensors) are stored once."""
+
+    def __init__(self):
+        self.blocks: list[np.ndarray] = []
+        self.size = 0
+        self._seen: dict[bytes, int] = {}
+
+    def add(self, block: np.ndarray) -> int:
+        flat = np.ascontiguousarray(block, dtype=np.complex128).reshape(-1)
+        key = flat.tobytes()
+        at = self._seen.get(key)
+        if at is None:
+            at = self.size
+            self._seen[key] = at
+            self.blocks.append(flat)
+            self.size += flat.size
+        return at
+
+    def finish(self, dtype: str) -> np.ndarray:
+        allv = np.concatenate(self.blocks) if self.blocks else np.zeros(0, np.complex128)
+        return allv.astype(np.complex64 if dtype == "complex64" else np.complex128)
+
+
+@dataclass
+class Program:
+    leaves: np.ndarray
+    steps: np.ndarray
+    tables: np.ndarray
+    arena_fast: int
+    arena_spill: int
+    out_elems: int
+    threads: int
+    level: int
+    result_kind: int = 0
+    result_ref: int = 0
+    flops: float = 0.0          # complex multiply-adds of one execution of this pass
+    peak_elems: int = 0
+    max_out: int = 0
+
+
+class _Arena:
+    """First-fit allocator over element offsets, used for liveness-based
+    placement of intermediates."""
+
+    def __init__(self):
+        self.free: list[list[int]] = []  # sorted [start, end)
+        self.top = 0
+
+    def alloc(self, n: int, cap: Optional[int] = None) -> Optional[int]:
+        """Offset of a free run of n elements; None (state untouched) when the
+        run would end beyond `cap`."""
+        for k, (s, e) in enumerate(self.free):
+            if e - s >= n:
+                if e - s == n:
+                    del self.free[k]
+                else:
+                    self.free[k][0] = s + n
+                return s
+        # grow; a trailing free block that touches the top is extended
+        tail = bool(self.free) and self.free[-1][1] == self.top
+        s = self.free[-1][0] if tail else self.top
+        if cap is not None and s + n > cap:
+            return None
+        if tail:
+            del self.free[-1]
+        self.top = s + n
+        return s
+
+    def release(self, s: int, n: int) -> None:
+        self.free.append([s, s + n])
+        self.free.sort()
+        merged = []
+        for blk in self.free:
+            if merged and merged[-1][1] == blk[0]:
+                merged[-1][1] = blk[1]
+            else:
+                merged.append(blk)
+        self.free = merged
+
+
+def _offsets(dims: Sequence[int], strides: Sequence[int]) -> np.ndarray:
+    """Row-major enumeration of a multi-index -> linear offset with the given
+    strides (0 stride = label absent from that operand)."""
+    out = np.zeros(1, dtype=np.int64)
+    for d, s in zip(dims, strides):
+        out = (out[:, None] + (np.arange(d, dtype=np.int64) * s)[None, :]).reshape(-1)
+    return out
+
+
+def _row_major_strides(dims: Sequence[int]) -> list[int]:
+    st = [1] * len(dims)
+    for k in range(len(dims) - 2, -1, -1):
+        st[k] = st[k + 1] * dims[k + 1]
+    return st
+
+
+@dataclass
+class _Node:
+    labels: tuple
+    dims: tuple
+    cls: int
+    a: int = -1
+    b: int = -1
+    parent: int = -1
+    pass_: int = 0
+    size: int = 1
+
+
+def build_tree(operands: Sequence[Operand], steps, ceiling: Optional[int] = None):
+    """Replay slot steps into a binary tree.  Result legs: a's survivors then
+    b's (tensor.py:193-195).  Raises like the reference's execute_path."""
+    nodes = [
+        _Node(tuple(o.labels), tuple(o.dims), o.cls, size=int(np.prod(o.dims, dtype=np.int64)) if o.dims else 1)
+        for o in operands
+    ]
+    slots = list(range(len(operands)))
+    flops = 0.0
+    for step in steps:
+        i, j = int(step[0]), int(step[1])
+        if i > j:
+            i, j = j, i
+        if i == j or i < 0 or j >= len(slots):
+            raise NetworkStructureError(f"invalid step {tuple(step)} with {len(slots)} slots")
+        na, nb = nodes[slots[i]], nodes[slots[j]]
+        bd = dict(zip(nb.labels, nb.dims))
+        shared = set()
+        for lb, d in zip(na.labels, na.dims):
+            if lb in bd:
+                if bd[lb] != d:
+                    raise NetworkStructureError(f"shared label {lb} has dims {d} vs {bd[lb]}")
+                shared.add(lb)
+        labels = [lb for lb in na.labels if lb not in shared] + [lb for lb in nb.labels if lb not in shared]
+        dims = [d for lb, d in zip(na.labels, na.dims) if lb not in shared] + [
+            d for lb, d in zip(nb.labels, nb.dims) if lb not in shared
+        ]
+        size = int(np.prod(dims, dtype=object)) if dims else 1
+        if ceiling is not None and size > ceiling:
+            raise ResourceLimitError(f"intermediate of {size} entries exceeds ceiling {ceiling}")
+        k = 1
+        for lb, d in zip(na.labels, na.dims):
+            if lb in shared:
+                k *= d
+        flops += float(size) * k
+        nid = len(nodes)
+        nodes.append(_Node(tuple(labels), tuple(dims), max(na.cls, nb.cls), slots[i], slots[j], size=size))
+        na.parent = nb.parent = nid
+        slots[i] = nid
+        del slots[j]
+    if len(slots) != 1:
+        raise IncompletePathError(f"path left {len(slots)} operands, expected 1")
+    return nodes, slots[0], flops
+
+
+def compile_stage(
+    operands: Sequence[Operand],
+    steps,
+    open_order: Optional[Sequence[int]],
+    n_passes: int,
+    pool: Pool,
+    elem_bytes: int,
+    ceiling: Optional[int] = None,
+) -> tuple[list[Program], tuple]:
+    """Compile one stage network + stored path into `n_passes` programs.
+    Returns (programs, result label order)."""
+    nodes, root, _ = build_tree(operands, steps, ceiling)
+    n_leaves = len(operands)
+    top = n_passes - 1
+    rootn = nodes[root]
+    if open_order is None:
+        open_order = rootn.labels
+    if sorted(open_order) != sorted(rootn.labels):
+        raise NetworkStructureError(
+            f"result labels {sorted(rootn.labels)} != open indices {sorted(open_order)}"
+        )
+    for nd in nodes:
+        nd.pass_ = min(nd.cls, top)
+    if root >= n_leaves:
+        rootn.pass_ = top  # the finished record is always produced by the marginal pass
+
+    # storage decisions ------------------------------------------------------
+    # frontier = computed node consumed by a later pass -> lives in its pass's record
+    rec_off: dict[int, int] = {}
+    rec_size = [0] * n_passes
+    for nid in range(n_leaves, len(nodes)):
+        nd = nodes[nid]
+        if nd.parent >= 0 and nodes[nd.parent].pass_ > nd.pass_:
+            rec_off[nid] = rec_size[nd.pass_]
+            rec_size[nd.pass_] += nd.size
+
+    programs: list[Program] = []
+    result_kind, result_ref = 0, 0
+    for p in range(n_passes):
+        mine = [nid for nid in range(n_leaves, len(nodes)) if nodes[nid].pass_ == p]
+        # sizing of the on-chip arena: try everything on chip, spill the big buffers otherwise
+        max_out = max([nodes[nid].size for nid in mine], default=1)
+        peak = _place(nodes, mine, rec_off, root, fast_cap=None)[1]
+        if max_out <= 128 and peak * elem_bytes <= WARP_ARENA_BYTES:
+            threads, fast_cap = 32, peak
+        else:
+            threads = 64
+            while threads < 512 and threads * 4 < max_out:
+                threads *= 2
+            fast_cap = min(peak, SMEM_BYTES // elem_bytes)
+        where, peak_fast, peak_spill = _place(nodes, mine, rec_off, root, fast_cap=fast_cap)
+
+        step_rows, tables = [], []
+        tab_off = 0
+        flops = 0.0
+        prog_leaves: list[list[int]] = []
+        prog_leaf_index: dict[int, int] = {}
+
+        def ref_of(nid: int):
+            if nid < n_leaves:
+                at = prog_leaf_index.get(nid)
+                if at is None:
+                    o = operands[nid]
+                    blk = np.asarray(o.data, dtype=np.complex128).reshape(o.data.shape[0], -1)
+                    size = blk.shape[1]
+                    at = len(prog_leaves)
+                    prog_leaf_index[nid] = at
+                    prog_leaves.append([pool.add(blk), size, o.sel_kind, o.sel_arg])
+                return 1, at
+            if nid in rec_off and nodes[nid].pass_ != p:
+                return 2 + nodes[nid].pass_, rec_off[nid]
+            if nid in rec_off:
+                raise AssertionError("frontier node consumed inside its own pass")
+            return 0, where[nid]
+
+        for nid in mine:
+            nd = nodes[nid]
+            na, nb = nodes[nd.a], nodes[nd.b]
+            a_kind, a_ref = ref_of(nd.a)
+            b_kind, b_ref = ref_of(nd.b)
+            if nid in rec_off:
+                o_kind, o_ref = 1, rec_off[nid]
+            else:
+                o_kind, o_ref = 0, where[nid]
+            out_labels = list(open_order) if nid == root else list(nd.labels)
+            dim_of = dict(zip(na.labels, na.dims))
+            dim_of.update(zip(nb.labels, nb.dims))
+            sa = dict(zip(na.labels, _row_major_strides(na.dims)))
+            sb = dict(zip(nb.labels, _row_major_strides(nb.dims)))
+            shared = [lb for lb in na.labels if lb in sb]
+            odims = [dim_of[lb] for lb in out_labels]
+            # split the output index into a high part and a <= LO_TABLE_MAX low part
+            cut, lo_n = len(out_labels), 1
+            while cut > 0 and lo_n * odims[cut - 1] <= LO_TABLE_MAX:
+                cut -= 1
+                lo_n *= odims[cut]
+            hi_lab, lo_lab = out_labels[:cut], out_labels[cut:]
+            hi_n = int(np.prod([dim_of[lb] for lb in hi_lab], dtype=np.int64)) if hi_lab else 1
+            lo_a = _offsets([dim_of[lb] for lb in lo_lab], [sa.get(lb, 0) for lb in lo_lab])
+            lo_b = _offsets([dim_of[lb] for lb in lo_lab], [sb.get(lb, 0) for lb in lo_lab])
+            hi_a = _offsets([dim_of[lb] for lb in hi_lab], [sa.get(lb, 0) for lb in hi_lab])
+            hi_b = _offsets([dim_of[lb] for lb in hi_lab], [sb.get(lb, 0) for lb in hi_lab])
+            k_a = _offsets([dim_of[lb] for lb in shared], [sa[lb] for lb in shared])
+            k_b = _offsets([dim_of[lb] for lb in shared], [sb[lb] for lb in shared])
+            k_n = k_a.size
+            words = np.concatenate([lo_a, lo_b, hi_a, hi_b, k_a, k_b]).astype(np.uint32)
+            tables.append(words)
+            step_rows.append(
+                [a_kind, a_ref, b_kind, b_ref, o_kind, o_ref, nd.size, k_n, lo_n, hi_n, tab_off, 0]
+            )
+            tab_off += words.size
+            flops += float(nd.size) * k_n
+            if nid == root:
+                result_kind, result_ref = (2 + p, o_ref) if o_kind == 1 else (0, o_ref)
+        if p == top and root < n_leaves:
+            # single-operand network: the "result" is the leaf itself
+            result_kind, result_ref = ref_of(root)
+            if tuple(open_order) != tuple(rootn.labels):
+                raise CapacityError("single-operand network with permuted open legs")
+        programs.append(
+            Program(
+                leaves=np.asarray(prog_leaves, dtype=np.uint32).reshape(-1, LEAF_WORDS),
+                steps=np.asarray(step_rows, dtype=np.uint32).reshape(-1, STEP_WORDS),
+                tables=np.concatenate(tables).astype(np.uint32) if tables else np.zeros(0, np.uint32),
+                arena_fast=int(peak_fast),
+                arena_spill=int(peak_spill),
+                out_elems=int(rec_size[p]) if p < top else int(rootn.size),
+                threads=threads,
+                level=p + 1,
+                result_kind=result_kind if p == top else 0,
+                result_ref=result_ref if p == top else 0,
+                flops=flops,
+                peak_elems=int(peak_fast + peak_spill),
+                max_out=int(max_out),
+            )
+        )
+    return programs, tuple(open_order)
+
+
+def _place(nodes, mine, rec_off, root, fast_cap):
+    """Liveness-based placement of the intermediates of one pass.  Buffers go to
+    the fast (shared-memory) arena while they fit under `fast_cap`, otherwise to
+    the spill arena whose offsets start at fast_cap.  Returns
+    (offset per node, fast peak, spill peak)."""
+    fast, spill = _Arena(), _Arena()
+    where: dict[int, int] = {}
+    in_spill: set[int] = set()
+    mine_set = set(mine)
+    for nid in mine:
+        nd = nodes[nid]
+        if nid not in rec_off:
+            off = fast.alloc(nd.size, fast_cap)
+            if off is None:
+                off = spill.alloc(nd.size)
+                in_spill.add(nid)
+            where[nid] = off
+        for ch in (nd.a, nd.b):
+            if ch in where and ch in mine_set:
+                (spill if ch in in_spill else fast).release(where[ch], nodes[ch].size)
+    if fast_cap is None:
+        return where, fast.top, 0
+    for nid in in_spill:
+        where[nid] += fast_cap
+    return where, (fast_cap if in_spill else fast.top), spill.top
+
+
+# ---------------------------------------------------------------------------
+# constant networks: execute_path / contract_pair on the device
+# ---------------------------------------------------------------------------
+
+@dataclass
+class ConstantProgram:
+    program: Program
+    pool: np.ndarray
+    out_shape: tuple
+
+
+def compile_constant_network(net, steps):
+    from .tensor import Index
+
+    ops = [
+        Operand(labels=t.labels, dims=tuple(ix.dim for ix in t.indices), data=t.data.reshape(1, -1))
+        for t in net.operands
+    ]
+    pool = Pool()
+    progs, order = compile_stage(ops, steps, None, 1, pool, 16)
+    dims = {}
+    for t in net.operands:
+        for ix in t.indices:
+            dims[ix.label] = ix.dim
+    out_indices = [Index(lb, dims[lb]) for lb in order]
+    return ConstantProgram(progs[0], pool.finish("complex128"), tuple(ix.dim for ix in out_indices)), out_indices
+
+
+def compile_pair(a, b):
+    from .tensor import TensorNetwork
+
+    class _Loose:  # contract_pair accepts any two tensors; no open/closed bookkeeping needed
+        operands = (a, b)
+
+    return compile_constant_network(_Loose, [(0, 1)])
+
+
+# ---------------------------------------------------------------------------
+# ctypes view of a compiled plan
+# ---------------------------------------------------------------------------
+
+class ProgramDesc(ctypes.Structure):
+    _fields_ = [
+        ("n_leaves", ctypes.c_uint32),
+        ("n_steps", ctypes.c_uint32),
+        ("n_table_words", ctypes.c_uint32),
+        ("arena_fast_elems", ctypes.c_uint32),
+        ("arena_spill_elems", ctypes.c_uint32),
+        ("out_elems", ctypes.c_uint32),
+        ("threads_per_item", ctypes.c_uint32),
+        ("level", ctypes.c_uint32),
+        ("result_kind", ctypes.c_uint32),
+        ("result_ref", ctypes.c_uint32),
+        ("leaves", ctypes.c_void_p),
+        ("steps", ctypes.c_void_p),
+        ("tables", ctypes.c_void_p),
+    ]
+
+
+class PlanDesc(ctypes.Structure):
+    _fields_ = [
+        ("dtype", ctypes.c_uint32),
+        ("n_qubits", ctypes.c_uint32),
+        ("n_sites", ctypes.c_uint32),
+        ("n_stages", ctypes.c_uint32),
+        ("stage_sizes", ctypes.c_void_p),
+        ("pool", ctypes.c_void_p),
+        ("pool_elems", ctypes.c_uint64),
+        ("programs", ctypes.c_void_p),
+        ("max_intermediate", ctypes.c_uint64),
+    ]
+
+
+@dataclass
+class CompiledPlan:
+    """Everything `ptsbe_plan_create` needs, kept alive on the Python side."""
+
+    dtype: str
+    n_qubits: int
+    n_sites: int
+    sizes: tuple
+    pool: np.ndarray
+    programs: list  # stage-major flat list of Program
+    max_intermediate: int
+    _keep: list = field(default_factory=list)
+
+    def descriptor(self) -> PlanDesc:
+        arr = (ProgramDesc * len(self.programs))()
+        keep = []
+        for k, pr in enumerate(self.programs):
+            lv = np.ascontiguousarray(pr.leaves, dtype=np.uint32)
+            st = np.ascontiguousarray(pr.steps, dtype=np.uint32)
+            tb = np.ascontiguousarray(pr.tables, dtype=np.uint32)
+            keep += [lv, st, tb]
+            arr[k] = ProgramDesc(
+                lv.shape[0], st.shape[0], tb.size, pr.arena_fast, pr.arena_spill, pr.out_elems,
+                pr.threads, pr.level, pr.result_kind, pr.result_ref,
+                lv.ctypes.data, st.ctypes.data, tb.ctypes.data,
+            )
+        sizes = np.asarray(self.sizes, dtype=np.uint32)
+        pool = np.ascontiguousarray(self.pool)
+        keep += [arr, sizes, pool]
+        self._keep = keep
+        return PlanDesc(
+            0 if self.dtype == "complex64" else 1,
+            self.n_qubits,
+            self.n_sites,
+            len(self.sizes),
+            sizes.ctypes.data,
+            pool.ctypes.data,
+            pool.size,
+            ctypes.addressof(arr),
+            self.max_intermediate,
+        )

@@ -1,0 +1,939 @@
+// C-ABI of libptsbe_b200.so (include/ptsbe_b200.h) and the host-side run
+// driver: per-stage hoist passes, marginal pass, sampler, order-preserving
+// compaction into the next stage's work list, final histogram.
+//
+// Replaces the fan-out loop of run_ptsbe (engine.py:885-906) and
+// sample_proportional (engine.py:493-524): the loop over error sets and the
+// loop over sorted prefixes become the batch axis of every launch.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <memory>
+#include <mutex>
+
+#include "common.cuh"
+#include "executor.cuh"
+#include "histogram.cuh"
+#include "sampler.cuh"
+#include "scan.cuh"
+
+namespace ptsbe {
+
+thread_local std::string g_last_error;
+thread_local uint64_t g_launches = 0;
+
+struct Program {
+  ptsbe_program_desc d;
+  DevBuf leaves, steps, tables;
+  int blocks_per_sm = 0;  // resolved lazily per (program, item_bytes)
+};
+
+}  // namespace ptsbe
+
+using namespace ptsbe;
+
+struct ptsbe_plan {
+  int device = 0;
+  uint32_t dtype = 0, n = 0, g = 0, f = 0, words = 1;
+  std::vector<uint32_t> sizes, offsets;        // offsets[j] = qubits measured before stage j+1
+  std::vector<std::vector<Program>> programs;  // [stage-1][pass]
+  DevBuf pool;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  size_t elem = 8;
+  std::mutex mu;
+  // tunables (environment overrides for experiments)
+  size_t probs_budget = 256ull << 20;  // bytes of marginal buffer per sub-batch
+  uint64_t chunk_shots = 1ull << 26;
+  size_t ext_budget = 48ull << 30;
+  double vanish = 1e-12, neg_abs = -1e-12, neg_rel = 0.0;
+};
+
+namespace ptsbe {
+
+static size_t env_size(const char* name, size_t dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  return (size_t)strtoull(v, nullptr, 10);
+}
+
+struct ExecLaunch {
+  unsigned grid, block;
+  size_t smem;
+  uint32_t item_bytes;
+  uint32_t groups_per_block;
+};
+
+template <typename R>
+static ExecLaunch configure_exec(ptsbe_plan* pl, Program& pr, uint32_t n_items) {
+  using C = typename CxT<R>::type;
+  ExecLaunch L;
+  const ptsbe_program_desc& d = pr.d;
+  size_t ib = (size_t)d.arena_fast_elems * sizeof(C) + (size_t)pl->words * 8 +
+              4ull * (d.level + 1) + pl->g;
+  ib = (ib + 15) & ~size_t(15);
+  L.item_bytes = (uint32_t)ib;
+  const bool warp = d.threads_per_item <= 32;
+  if (warp) {
+    uint32_t gpb = 8;
+    while (gpb > 1 && ib * gpb + 1024 > 227 * 1024) gpb >>= 1;
+    L.groups_per_block = gpb;
+    L.block = 32 * gpb;
+  } else {
+    L.groups_per_block = 1;
+    L.block = d.threads_per_item;
+  }
+  L.smem = ib * L.groups_per_block + 1024;
+  if (L.smem > 227 * 1024)
+    throw Failure(PTSBE_ERESOURCE, "stage program needs more shared memory than one SM has");
+  auto kern = warp ? exec_kernel<R, true> : exec_kernel<R, false>;
+  if (pr.blocks_per_sm == 0) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    int nb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, (int)L.block, L.smem));
+    pr.blocks_per_sm = std::max(nb, 1);
+  }
+  const uint64_t need = (n_items + L.groups_per_block - 1) / L.groups_per_block;
+  const uint64_t cap = (uint64_t)pl->sm_count * pr.blocks_per_sm;
+  L.grid = (unsigned)std::max<uint64_t>(1, std::min(need, cap));
+  return L;
+}
+
+template <typename R>
+static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelDev* levels_dev,
+                        const uint8_t* kraus_dev, uint32_t first, uint32_t n_items, void* out,
+                        double* mass, double* minv) {
+  using C = typename CxT<R>::type;
+  if (n_items == 0) return;
+  ExecLaunch L = configure_exec<R>(pl, pr, n_items);
+  DevBuf spill;
+  if (pr.d.arena_spill_elems)
+    spill.alloc((size_t)L.grid * L.groups_per_block * pr.d.arena_spill_elems * sizeof(C),
+                pl->stream);
+  ExecArgs a;
+  a.leaves = pr.leaves.as<uint32_t>();
+  a.steps = pr.steps.as<uint32_t>();
+  a.tables = pr.tables.as<uint32_t>();
+  a.pool = pl->pool.p;
+  a.kraus = kraus_dev;
+  a.levels = levels_dev;
+  a.spill = spill.p;
+  a.out = out;
+  a.out_mass = mass;
+  a.out_min = minv;
+  a.n_steps = pr.d.n_steps;
+  a.arena_fast = pr.d.arena_fast_elems;
+  a.arena_spill = pr.d.arena_spill_elems;
+  a.out_elems = pr.d.out_elems;
+  a.result_kind = pr.d.result_kind;
+  a.result_ref = pr.d.result_ref;
+  a.level = pr.d.level;
+  a.first_item = first;
+  a.n_items = n_items;
+  a.g = pl->g;
+  a.words = pl->words;
+  a.item_bytes = L.item_bytes;
+  a.mode = mode;
+  if (pr.d.threads_per_item <= 32)
+    exec_kernel<R, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  else
+    exec_kernel<R, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  g_launches++;
+  CK(cudaGetLastError());
+}
+
+static void launch_exec_any(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelDev* lv,
+                            const uint8_t* kraus, uint32_t first, uint32_t n, void* out,
+                            double* mass, double* minv) {
+  if (pl->dtype == PTSBE_C64) launch_exec<float>(pl, pr, mode, lv, kraus, first, n, out, mass, minv);
+  else launch_exec<double>(pl, pr, mode, lv, kraus, first, n, out, mass, minv);
+}
+
+static void launch_sampler(cudaStream_t st, SampleArgs& a, int sm_count) {
+  if (a.n_items == 0) return;
+  const size_t nb = 1ull << a.b;
+  const size_t smem = nb * 12;
+  if (a.b > 14) throw Failure(PTSBE_ECAPACITY, "sampler supports stage batches of at most 14 qubits");
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_set = true;
+  }
+  const uint64_t cap = (uint64_t)sm_count * 16;
+  const unsigned grid = (unsigned)std::min<uint64_t>(a.n_items, cap);
+  sample_kernel<<<grid, SAMPLE_THREADS, smem, st>>>(a);
+  g_launches++;
+  CK(cudaGetLastError());
+}
+
+// Work-item list of one level, device resident.
+struct Level {
+  uint32_t n = 0;
+  DevBuf eset, parent, prefix, mult, slot_off, rank, gid;
+};
+
+struct RunOutput {
+  // final records of one chunk, device resident (level f+1): eset rows, keys, counts
+  DevBuf eset, keys, counts;
+  uint64_t n = 0;
+};
+
+// Runs error sets [e0, e0+ne) of a resident batch through all stages.
+static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* shots_dev,
+                      const uint32_t* ids_dev, uint32_t ne, uint64_t chunk_shots, uint64_t seed,
+                      RunOutput& out, ptsbe_run_stats* stats, unsigned long long* flag_dev,
+                      uint32_t* flag_count_dev) {
+  cudaStream_t st = pl->stream;
+  const uint32_t f = pl->f, words = pl->words;
+  const unsigned T = 256;
+  std::vector<Level> lv(f + 2);
+  std::vector<LevelDev> table(f + 2);
+  memset(table.data(), 0, sizeof(LevelDev) * table.size());
+  DevBuf table_dev((f + 2) * sizeof(LevelDev), st);
+  DevBuf seg_start((size_t)ne * 4, st);
+  DevBuf slot_index(chunk_shots * 4, st), slot_count(chunk_shots * 4, st);
+  DevBuf scal(16, st);
+
+  // level 1: one item per error set, empty prefix
+  {
+    Level& l = lv[1];
+    l.n = ne;
+    l.eset.alloc((size_t)ne * 4, st);
+    l.parent.alloc((size_t)ne * 4, st);
+    l.prefix.alloc((size_t)ne * 8 * words, st);
+    l.mult.alloc((size_t)ne * 4, st);
+    l.slot_off.alloc((size_t)ne * 4, st);
+    l.rank.alloc((size_t)ne * 4, st);
+    l.gid.alloc((size_t)ne * 4, st);
+    iota_kernel<<<cdiv(ne, T), T, 0, st>>>(l.eset.as<uint32_t>(), ne, 0);
+    g_launches++;
+    CK(cudaMemsetAsync(l.parent.p, 0, (size_t)ne * 4, st));
+    CK(cudaMemsetAsync(l.prefix.p, 0, (size_t)ne * 8 * words, st));
+    CK(cudaMemsetAsync(l.rank.p, 0, (size_t)ne * 4, st));
+    CK(cudaMemcpyAsync(l.mult.p, shots_dev, (size_t)ne * 4, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(l.gid.p, ids_dev, (size_t)ne * 4, cudaMemcpyDeviceToDevice, st));
+    exclusive_scan<uint32_t, uint32_t>(l.mult.as<uint32_t>(), l.slot_off.as<uint32_t>(), ne,
+                                       nullptr, st);
+  }
+
+  std::vector<cudaEvent_t> ev(f + 1);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  CK(cudaEventRecord(ev[0], st));
+
+  for (uint32_t j = 1; j <= f; ++j) {
+    Level& cur = lv[j];
+    const uint32_t U = cur.n, b = pl->sizes[j - 1], nb = 1u << b;
+    stats->stage_events[j - 1] += U;
+    auto& progs = pl->programs[j - 1];
+    // level table for this stage
+    std::vector<DevBuf> ext(j);
+    for (uint32_t l = 1; l <= j; ++l) {
+      table[l].eset = lv[l].eset.as<uint32_t>();
+      table[l].parent = lv[l].parent.as<uint32_t>();
+      table[l].prefix = lv[l].prefix.as<uint64_t>();
+      table[l].n = lv[l].n;
+      table[l].ext = nullptr;
+      table[l].ext_rec = 0;
+      if (l < j && progs[l - 1].d.out_elems && progs[l - 1].d.n_steps) {
+        ext[l - 1].alloc((size_t)lv[l].n * progs[l - 1].d.out_elems * pl->elem, st);
+        table[l].ext = ext[l - 1].p;
+        table[l].ext_rec = progs[l - 1].d.out_elems;
+      }
+    }
+    CK(cudaMemcpyAsync(table_dev.p, table.data(), sizeof(LevelDev) * (f + 2),
+                       cudaMemcpyHostToDevice, st));
+    // hoist passes: everything that does not depend on the newest prefix bits
+    for (uint32_t p = 0; p + 1 < j; ++p) {
+      if (!progs[p].d.n_steps) continue;
+      launch_exec_any(pl, progs[p], EXEC_HOIST, table_dev.as<LevelDev>(), kraus_dev, 0,
+                      lv[p + 1].n, ext[p].p, nullptr, nullptr);
+    }
+    // marginal pass + sampler, in sub-batches sized to the probs buffer
+    const size_t real = pl->dtype == PTSBE_C64 ? 4 : 8;
+    uint32_t B = (uint32_t)std::max<size_t>(1, std::min<size_t>(U, pl->probs_budget / (nb * real)));
+    DevBuf probs((size_t)B * nb * real, st), mass((size_t)B * 8, st), minv((size_t)B * 8, st);
+    DevBuf nnz((size_t)U * 4, st);
+    for (uint32_t s0 = 0; s0 < U; s0 += B) {
+      const uint32_t nbatch = std::min(B, U - s0);
+      launch_exec_any(pl, progs[j - 1], EXEC_MARGINAL, table_dev.as<LevelDev>(), kraus_dev, s0,
+                      nbatch, probs.p, mass.as<double>(), minv.as<double>());
+      SampleArgs sa;
+      sa.probs = probs.p;
+      sa.mult = cur.mult.as<uint32_t>();
+      sa.slot_off = cur.slot_off.as<uint32_t>();
+      sa.eset_id = cur.gid.as<uint32_t>();
+      sa.rank = cur.rank.as<uint32_t>();
+      sa.mass = mass.as<double>();
+      sa.minv = minv.as<double>();
+      sa.slot_index = slot_index.as<uint32_t>();
+      sa.slot_count = slot_count.as<uint32_t>();
+      sa.nnz = nnz.as<uint32_t>();
+      sa.flag = flag_dev;
+      sa.flag_count = flag_count_dev;
+      sa.n_items = nbatch;
+      sa.first_item = s0;
+      sa.b = b;
+      sa.stage = j;
+      sa.k0 = (uint32_t)seed;
+      sa.k1 = (uint32_t)(seed >> 32);
+      sa.is_f32 = pl->dtype == PTSBE_C64;
+      sa.vanish = pl->vanish;
+      sa.neg_abs = pl->neg_abs;
+      sa.neg_rel = pl->neg_rel;
+      launch_sampler(st, sa, pl->sm_count);
+    }
+    // compaction into level j+1
+    DevBuf child_base((size_t)U * 4, st);
+    exclusive_scan<uint32_t, uint32_t>(nnz.as<uint32_t>(), child_base.as<uint32_t>(), U,
+                                       scal.as<uint32_t>(), st);
+    uint32_t Un = 0;
+    CK(cudaMemcpyAsync(&Un, scal.p, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    Level& nx = lv[j + 1];
+    nx.n = Un;
+    nx.eset.alloc((size_t)Un * 4, st);
+    nx.parent.alloc((size_t)Un * 4, st);
+    nx.prefix.alloc((size_t)Un * 8 * words, st);
+    nx.mult.alloc((size_t)Un * 4, st);
+    if (Un) {
+      ExpandArgs ea;
+      ea.p_eset = cur.eset.as<uint32_t>();
+      ea.p_prefix = cur.prefix.as<uint64_t>();
+      ea.p_n = U;
+      ea.p_slot_off = cur.slot_off.as<uint32_t>();
+      ea.child_base = child_base.as<uint32_t>();
+      ea.slot_index = slot_index.as<uint32_t>();
+      ea.slot_count = slot_count.as<uint32_t>();
+      ea.c_eset = nx.eset.as<uint32_t>();
+      ea.c_parent = nx.parent.as<uint32_t>();
+      ea.c_prefix = nx.prefix.as<uint64_t>();
+      ea.c_mult = nx.mult.as<uint32_t>();
+      ea.c_n = Un;
+      ea.words = words;
+      ea.offset = pl->offsets[j - 1];
+      ea.b = b;
+      expand_kernel<<<cdiv(Un, T), T, 0, st>>>(ea);
+      g_launches++;
+      if (j < f) {
+        nx.slot_off.alloc((size_t)Un * 4, st);
+        nx.rank.alloc((size_t)Un * 4, st);
+        nx.gid.alloc((size_t)Un * 4, st);
+        exclusive_scan<uint32_t, uint32_t>(nx.mult.as<uint32_t>(), nx.slot_off.as<uint32_t>(), Un,
+                                           nullptr, st);
+        segment_start_kernel<<<cdiv(Un, T), T, 0, st>>>(nx.eset.as<uint32_t>(), Un,
+                                                        seg_start.as<uint32_t>());
+        rank_kernel<<<cdiv(Un, T), T, 0, st>>>(nx.eset.as<uint32_t>(), seg_start.as<uint32_t>(),
+                                               ids_dev, Un, nx.rank.as<uint32_t>(),
+                                               nx.gid.as<uint32_t>());
+        g_launches += 2;
+      }
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ev[j], st));
+    // parents' per-stage arrays are no longer needed (lists stay for ancestor lookups)
+    cur.mult.release();
+    cur.slot_off.release();
+    cur.rank.release();
+    cur.gid.release();
+  }
+  CK(cudaStreamSynchronize(st));
+  for (uint32_t j = 1; j <= f; ++j) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev[j - 1], ev[j]));
+    stats->stage_ms[j - 1] += ms;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  Level& fin = lv[f + 1];
+  out.n = fin.n;
+  out.eset = std::move(fin.eset);
+  out.keys = std::move(fin.prefix);
+  out.counts = std::move(fin.mult);
+}
+
+}  // namespace ptsbe
+
+// ---------------------------------------------------------------------------
+// resident batch
+// ---------------------------------------------------------------------------
+struct ptsbe_batch {
+  ptsbe_plan* plan = nullptr;
+  uint64_t n_sets = 0, total_shots = 0;
+  std::vector<uint32_t> shots_host;
+  DevBuf kraus, shots, ids;
+  // last run
+  Histogram merged;
+  RunOutput per_set;  // when merged == 0 (single chunk only)
+  bool have_per_set = false;
+};
+
+namespace ptsbe {
+
+static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stats* stats) {
+  ptsbe_plan* pl = bt->plan;
+  cudaStream_t st = pl->stream;
+  CK(cudaSetDevice(pl->device));
+  memset(stats, 0, sizeof *stats);
+  stats->first_flagged_id = -1;
+  stats->total_shots = bt->total_shots;
+  g_launches = 0;
+  DevBuf flag(16, st);
+  CK(cudaMemsetAsync(flag.p, 0xff, 8, st));
+  CK(cudaMemsetAsync(flag.as<unsigned char>() + 8, 0, 8, st));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+
+  // chunk the error sets: bounded shots (slot arrays) and bounded hoist records
+  std::vector<std::pair<uint64_t, uint64_t>> chunks;  // (first set, count)
+  {
+    uint64_t e = 0;
+    while (e < bt->n_sets) {
+      uint64_t cnt = 0, sh = 0;
+      while (e + cnt < bt->n_sets) {
+        const uint64_t s = bt->shots_host[e + cnt];
+        if (cnt && sh + s > pl->chunk_shots) break;
+        // hoist-record bound: records of pass p exist for every level-(p+1) item
+        size_t ext_bytes = 0;
+        for (uint32_t j = 1; j <= pl->f; ++j) {
+          size_t here = 0;
+          for (uint32_t p = 0; p + 1 < j; ++p) {
+            const double cap_items = std::min<double>(
+                (double)(sh + s),
+                (double)(cnt + 1) * std::pow(2.0, std::min<uint32_t>(pl->offsets[p], 60)));
+            here += (size_t)(cap_items * pl->programs[j - 1][p].d.out_elems * pl->elem);
+          }
+          ext_bytes = std::max(ext_bytes, here);
+        }
+        if (cnt && ext_bytes > pl->ext_budget) break;
+        sh += s;
+        ++cnt;
+      }
+      if (sh >= (1ull << 32)) throw Failure(PTSBE_ECAPACITY, "one error set with >= 2^32 shots");
+      chunks.push_back({e, cnt});
+      e += cnt;
+    }
+  }
+  stats->n_chunks = (uint32_t)chunks.size();
+  const uint32_t words = pl->words;
+  std::vector<RunOutput> outs(chunks.size());
+  uint64_t total_rec = 0;
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    const uint64_t e = chunks[c].first, cnt = chunks[c].second;
+    uint64_t sh = 0;
+    for (uint64_t i = 0; i < cnt; ++i) sh += bt->shots_host[e + i];
+    run_chunk(pl, bt->kraus.as<uint8_t>() + e * pl->g, bt->shots.as<uint32_t>() + e,
+              bt->ids.as<uint32_t>() + e, (uint32_t)cnt, sh, seed, outs[c], stats,
+              flag.as<unsigned long long>(), flag.as<uint32_t>() + 2);
+    total_rec += outs[c].n;
+  }
+  // flags
+  struct { unsigned long long first; uint32_t count; uint32_t pad; } fl;
+  CK(cudaMemcpyAsync(&fl, flag.p, 16, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  stats->flagged_sets = fl.count;
+  if (fl.count) {
+    stats->first_flag_kind = (uint32_t)(fl.first & 0xff);
+    stats->first_flag_stage = (uint32_t)((fl.first >> 8) & 0xff);
+    stats->first_flagged_id = (int64_t)(fl.first >> 16);
+  }
+  bt->have_per_set = false;
+  if (merged) {
+    if (chunks.size() == 1) {
+      reduce_by_key(outs[0].keys.as<uint64_t>(), outs[0].n, words, outs[0].counts.as<uint32_t>(),
+                    nullptr, outs[0].n, pl->n, bt->merged, st);
+    } else {
+      // concatenate chunk records (SoA with common stride), then reduce
+      DevBuf keys(total_rec * 8 * words, st), counts(total_rec * 4, st);
+      uint64_t off = 0;
+      for (auto& o : outs) {
+        for (uint32_t w = 0; w < words; ++w)
+          CK(cudaMemcpyAsync(keys.as<uint64_t>() + (uint64_t)w * total_rec + off,
+                             o.keys.as<uint64_t>() + (uint64_t)w * o.n, o.n * 8,
+                             cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(counts.as<uint32_t>() + off, o.counts.p, o.n * 4,
+                           cudaMemcpyDeviceToDevice, st));
+        off += o.n;
+      }
+      reduce_by_key(keys.as<uint64_t>(), total_rec, words, counts.as<uint32_t>(), nullptr,
+                    total_rec, pl->n, bt->merged, st);
+    }
+    stats->n_records = bt->merged.n;
+  } else {
+    if (chunks.size() != 1)
+      throw Failure(PTSBE_ECAPACITY, "per-error-set output needs the batch to fit one chunk");
+    bt->per_set = std::move(outs[0]);
+    bt->have_per_set = true;
+    stats->n_records = bt->per_set.n;
+  }
+  CK(cudaEventRecord(e1, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaEventElapsedTime(&stats->loop_ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  stats->gpu_launches = g_launches;
+}
+
+template <typename F>
+static int guarded(F&& fn) {
+  try {
+    fn();
+    return PTSBE_OK;
+  } catch (const Failure& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return PTSBE_EDEVICE;
+  }
+}
+
+}  // namespace ptsbe
+
+extern "C" {
+
+const char* ptsbe_last_error(void) { return g_last_error.c_str(); }
+const char* ptsbe_version(void) { return "ptsbe_b200 0.1 (sm_100a)"; }
+
+int ptsbe_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+void ptsbe_free(void* p) { free(p); }
+
+int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
+  return guarded([&] {
+    if (!d || !out) throw Failure(PTSBE_EINVAL, "null plan descriptor");
+    if (d->dtype > 1) throw Failure(PTSBE_EINVAL, "dtype must be PTSBE_C64 or PTSBE_C128");
+    if (d->n_stages < 1 || d->n_stages > PTSBE_MAX_STAGES)
+      throw Failure(PTSBE_ECAPACITY, "stage count outside 1..PTSBE_MAX_STAGES");
+    if (ptsbe_device_count() <= device)
+      throw Failure(PTSBE_EDEVICE, "no CUDA device: libptsbe_b200 has no CPU fallback");
+    CK(cudaSetDevice(device));
+    std::unique_ptr<ptsbe_plan> pl(new ptsbe_plan);
+    pl->device = device;
+    pl->dtype = d->dtype;
+    pl->n = d->n_qubits;
+    pl->g = d->n_sites;
+    pl->f = d->n_stages;
+    pl->words = std::max<uint32_t>(1, (d->n_qubits + 63) / 64);
+    pl->elem = d->dtype == PTSBE_C64 ? 8 : 16;
+    uint32_t off = 0;
+    for (uint32_t j = 0; j < d->n_stages; ++j) {
+      pl->sizes.push_back(d->stage_sizes[j]);
+      pl->offsets.push_back(off);
+      off += d->stage_sizes[j];
+    }
+    if (off != d->n_qubits) throw Failure(PTSBE_EINVAL, "stage sizes do not sum to n_qubits");
+    if (d->dtype == PTSBE_C64) { pl->neg_abs = -1e-12; pl->neg_rel = 1e-4; }
+    CK(cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    pl->sm_count = prop.multiProcessorCount;
+    cudaMemPool_t mp;
+    CK(cudaDeviceGetDefaultMemPool(&mp, device));
+    uint64_t thr = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr));
+    pl->probs_budget = env_size("PTSBE_PROBS_BYTES", pl->probs_budget);
+    pl->chunk_shots = env_size("PTSBE_CHUNK_SHOTS", pl->chunk_shots);
+    pl->ext_budget = env_size("PTSBE_EXT_BYTES", pl->ext_budget);
+    cudaStream_t st = pl->stream;
+    pl->pool.alloc(std::max<size_t>(16, d->pool_elems * pl->elem), st);
+    if (d->pool_elems)
+      CK(cudaMemcpyAsync(pl->pool.p, d->pool, d->pool_elems * pl->elem, cudaMemcpyHostToDevice, st));
+    size_t k = 0;
+    pl->programs.resize(d->n_stages);
+    for (uint32_t j = 1; j <= d->n_stages; ++j) {
+      pl->programs[j - 1].resize(j);
+      for (uint32_t p = 0; p < j; ++p, ++k) {
+        Program& pr = pl->programs[j - 1][p];
+        pr.d = d->programs[k];
+        if (pr.d.level != p + 1) throw Failure(PTSBE_EINVAL, "program level does not match its pass");
+        if (pr.d.threads_per_item > 1024 || (pr.d.threads_per_item & 31))
+          throw Failure(PTSBE_EINVAL, "threads_per_item must be a multiple of 32 up to 1024");
+        pr.leaves.alloc(std::max<size_t>(16, (size_t)pr.d.n_leaves * LEAF_WORDS * 4), st);
+        pr.steps.alloc(std::max<size_t>(16, (size_t)pr.d.n_steps * STEP_WORDS * 4), st);
+        pr.tables.alloc(std::max<size_t>(16, (size_t)pr.d.n_table_words * 4), st);
+        if (pr.d.n_leaves)
+          CK(cudaMemcpyAsync(pr.leaves.p, pr.d.leaves, (size_t)pr.d.n_leaves * LEAF_WORDS * 4,
+                             cudaMemcpyHostToDevice, st));
+        if (pr.d.n_steps)
+          CK(cudaMemcpyAsync(pr.steps.p, pr.d.steps, (size_t)pr.d.n_steps * STEP_WORDS * 4,
+                             cudaMemcpyHostToDevice, st));
+        if (pr.d.n_table_words)
+          CK(cudaMemcpyAsync(pr.tables.p, pr.d.tables, (size_t)pr.d.n_table_words * 4,
+                             cudaMemcpyHostToDevice, st));
+        pr.d.leaves = pr.d.steps = pr.d.tables = nullptr;
+      }
+    }
+    CK(cudaStreamSynchronize(st));
+    *out = pl.release();
+  });
+}
+
+void ptsbe_plan_destroy(ptsbe_plan* pl) {
+  if (!pl) return;
+  cudaSetDevice(pl->device);
+  cudaStreamSynchronize(pl->stream);
+  pl->pool.release();
+  for (auto& s : pl->programs)
+    for (auto& p : s) { p.leaves.release(); p.steps.release(); p.tables.release(); }
+  cudaStreamSynchronize(pl->stream);
+  cudaStreamDestroy(pl->stream);
+  delete pl;
+}
+
+int ptsbe_marginals(ptsbe_plan* pl, uint32_t stage, const uint8_t* kraus_idx,
+                    const uint64_t* prefixes, uint64_t n_items, double* out_probs,
+                    double* out_mass, double* out_min) {
+  return guarded([&] {
+    if (!pl) throw Failure(PTSBE_EINVAL, "null plan");
+    if (stage < 1 || stage > pl->f) throw Failure(PTSBE_EINVAL, "stage outside 1..f");
+    std::lock_guard<std::mutex> lock(pl->mu);
+    CK(cudaSetDevice(pl->device));
+    g_launches = 0;
+    cudaStream_t st = pl->stream;
+    const uint32_t j = stage, words = pl->words, f = pl->f;
+    auto& progs = pl->programs[j - 1];
+    const uint32_t nb = progs[j - 1].d.out_elems;
+    const size_t real = pl->dtype == PTSBE_C64 ? 4 : 8;
+    size_t per_item = (size_t)nb * real;
+    for (uint32_t p = 0; p + 1 < j; ++p) per_item += (size_t)progs[p].d.out_elems * pl->elem;
+    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(65536, (1ull << 30) / per_item));
+    std::vector<LevelDev> table(f + 2);
+    DevBuf table_dev((f + 2) * sizeof(LevelDev), st);
+    std::vector<unsigned char> host(chunk * nb * real);
+    for (uint64_t c0 = 0; c0 < n_items; c0 += chunk) {
+      const uint32_t W = (uint32_t)std::min<uint64_t>(chunk, n_items - c0);
+      DevBuf kraus((size_t)W * std::max<uint32_t>(pl->g, 1), st), ident((size_t)W * 4, st),
+          pfx((size_t)W * 8 * words, st);
+      if (pl->g)
+        CK(cudaMemcpyAsync(kraus.p, kraus_idx + c0 * pl->g, (size_t)W * pl->g,
+                           cudaMemcpyHostToDevice, st));
+      // prefixes arrive item-major [W][words]; the device wants [words][W]
+      std::vector<uint64_t> soa((size_t)W * words);
+      for (uint32_t i = 0; i < W; ++i)
+        for (uint32_t w = 0; w < words; ++w)
+          soa[(size_t)w * W + i] = prefixes ? prefixes[(c0 + i) * words + w] : 0;
+      CK(cudaMemcpyAsync(pfx.p, soa.data(), soa.size() * 8, cudaMemcpyHostToDevice, st));
+      iota_kernel<<<cdiv(W, 256), 256, 0, st>>>(ident.as<uint32_t>(), W, 0);
+      g_launches++;
+      memset(table.data(), 0, sizeof(LevelDev) * table.size());
+      std::vector<DevBuf> ext(j);
+      for (uint32_t l = 1; l <= j; ++l) {
+        table[l].eset = ident.as<uint32_t>();
+        table[l].parent = ident.as<uint32_t>();
+        table[l].prefix = pfx.as<uint64_t>();
+        table[l].n = W;
+        if (l < j && progs[l - 1].d.out_elems && progs[l - 1].d.n_steps) {
+          ext[l - 1].alloc((size_t)W * progs[l - 1].d.out_elems * pl->elem, st);
+          table[l].ext = ext[l - 1].p;
+          table[l].ext_rec = progs[l - 1].d.out_elems;
+        }
+      }
+      CK(cudaMemcpyAsync(table_dev.p, table.data(), sizeof(LevelDev) * (f + 2),
+                         cudaMemcpyHostToDevice, st));
+      for (uint32_t p = 0; p + 1 < j; ++p)
+        if (progs[p].d.n_steps)
+          launch_exec_any(pl, progs[p], EXEC_HOIST, table_dev.as<LevelDev>(), kraus.as<uint8_t>(),
+                          0, W, ext[p].p, nullptr, nullptr);
+      DevBuf probs((size_t)W * nb * real, st), mass((size_t)W * 8, st), minv((size_t)W * 8, st);
+      launch_exec_any(pl, progs[j - 1], EXEC_MARGINAL, table_dev.as<LevelDev>(),
+                      kraus.as<uint8_t>(), 0, W, probs.p, mass.as<double>(), minv.as<double>());
+      CK(cudaMemcpyAsync(host.data(), probs.p, (size_t)W * nb * real, cudaMemcpyDeviceToHost, st));
+      if (out_mass) CK(cudaMemcpyAsync(out_mass + c0, mass.p, (size_t)W * 8, cudaMemcpyDeviceToHost, st));
+      if (out_min) CK(cudaMemcpyAsync(out_min + c0, minv.p, (size_t)W * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      double* o = out_probs + c0 * nb;
+      if (pl->dtype == PTSBE_C64) {
+        const float* h = reinterpret_cast<const float*>(host.data());
+        for (size_t i = 0; i < (size_t)W * nb; ++i) o[i] = (double)h[i];
+      } else {
+        memcpy(o, host.data(), (size_t)W * nb * 8);
+      }
+    }
+  });
+}
+
+// Runs pass 0 of stage 1 of a plan in RAW mode for one item: complex result of a
+// constant network (tensor.py execute_path / contract_pair on the device).
+int ptsbe_execute_raw(ptsbe_plan* pl, void* out_complex) {
+  return guarded([&] {
+    if (!pl) throw Failure(PTSBE_EINVAL, "null plan");
+    std::lock_guard<std::mutex> lock(pl->mu);
+    CK(cudaSetDevice(pl->device));
+    cudaStream_t st = pl->stream;
+    Program& pr = pl->programs[0][0];
+    std::vector<LevelDev> table(pl->f + 2);
+    memset(table.data(), 0, sizeof(LevelDev) * table.size());
+    DevBuf table_dev(table.size() * sizeof(LevelDev), st), ident(16, st), pfx(8 * pl->words, st),
+        kraus(16, st), res((size_t)pr.d.out_elems * pl->elem, st);
+    CK(cudaMemsetAsync(ident.p, 0, 16, st));
+    CK(cudaMemsetAsync(pfx.p, 0, 8 * pl->words, st));
+    CK(cudaMemsetAsync(kraus.p, 0, 16, st));
+    table[1].eset = ident.as<uint32_t>();
+    table[1].parent = ident.as<uint32_t>();
+    table[1].prefix = pfx.as<uint64_t>();
+    table[1].n = 1;
+    CK(cudaMemcpyAsync(table_dev.p, table.data(), table.size() * sizeof(LevelDev),
+                       cudaMemcpyHostToDevice, st));
+    launch_exec_any(pl, pr, EXEC_RAW, table_dev.as<LevelDev>(), kraus.as<uint8_t>(), 0, 1, res.p,
+                    nullptr, nullptr);
+    CK(cudaMemcpyAsync(out_complex, res.p, (size_t)pr.d.out_elems * pl->elem,
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int ptsbe_sample_stage(uint32_t b, uint32_t stage, uint64_t seed, uint64_t n_items,
+                       const double* probs, const uint32_t* mult, const uint32_t* eset_id,
+                       const uint32_t* rank, uint32_t** child_item, uint32_t** child_index,
+                       uint32_t** child_count, uint64_t* n_children, int device) {
+  return guarded([&] {
+    if (ptsbe_device_count() <= device)
+      throw Failure(PTSBE_EDEVICE, "no CUDA device: libptsbe_b200 has no CPU fallback");
+    if (b > 14) throw Failure(PTSBE_ECAPACITY, "sampler supports stage batches of at most 14 qubits");
+    CK(cudaSetDevice(device));
+    g_launches = 0;
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    {
+      const uint64_t nb = 1ull << b;
+      uint64_t shots = 0;
+      for (uint64_t i = 0; i < n_items; ++i) shots += mult[i];
+      DevBuf dp(n_items * nb * 8, st), dm(n_items * 4, st), de(n_items * 4, st), dr(n_items * 4, st),
+          so(n_items * 4, st), si(std::max<uint64_t>(shots, 1) * 4, st),
+          sc(std::max<uint64_t>(shots, 1) * 4, st), nnz(n_items * 4, st), flag(16, st),
+          base(n_items * 4, st);
+      CK(cudaMemcpyAsync(dp.p, probs, n_items * nb * 8, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(dm.p, mult, n_items * 4, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(de.p, eset_id, n_items * 4, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(dr.p, rank, n_items * 4, cudaMemcpyHostToDevice, st));
+      CK(cudaMemsetAsync(flag.p, 0xff, 8, st));
+      CK(cudaMemsetAsync(flag.as<unsigned char>() + 8, 0, 8, st));
+      exclusive_scan<uint32_t, uint32_t>(dm.as<uint32_t>(), so.as<uint32_t>(), n_items, nullptr, st);
+      SampleArgs sa;
+      memset(&sa, 0, sizeof sa);
+      sa.probs = dp.p;
+      sa.mult = dm.as<uint32_t>();
+      sa.slot_off = so.as<uint32_t>();
+      sa.eset_id = de.as<uint32_t>();
+      sa.rank = dr.as<uint32_t>();
+      sa.slot_index = si.as<uint32_t>();
+      sa.slot_count = sc.as<uint32_t>();
+      sa.nnz = nnz.as<uint32_t>();
+      sa.flag = flag.as<unsigned long long>();
+      sa.flag_count = flag.as<uint32_t>() + 2;
+      sa.n_items = n_items;
+      sa.b = b;
+      sa.stage = stage;
+      sa.k0 = (uint32_t)seed;
+      sa.k1 = (uint32_t)(seed >> 32);
+      sa.is_f32 = 0;
+      cudaDeviceProp prop;
+      CK(cudaGetDeviceProperties(&prop, device));
+      launch_sampler(st, sa, prop.multiProcessorCount);
+      std::vector<uint32_t> h_nnz(n_items), h_so(n_items), h_si(shots), h_sc(shots);
+      CK(cudaMemcpyAsync(h_nnz.data(), nnz.p, n_items * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_so.data(), so.p, n_items * 4, cudaMemcpyDeviceToHost, st));
+      if (shots) {
+        CK(cudaMemcpyAsync(h_si.data(), si.p, shots * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(h_sc.data(), sc.p, shots * 4, cudaMemcpyDeviceToHost, st));
+      }
+      CK(cudaStreamSynchronize(st));
+      uint64_t total = 0;
+      for (uint64_t i = 0; i < n_items; ++i) total += h_nnz[i];
+      uint32_t* ci = (uint32_t*)malloc(std::max<uint64_t>(total, 1) * 4);
+      uint32_t* cx = (uint32_t*)malloc(std::max<uint64_t>(total, 1) * 4);
+      uint32_t* cc = (uint32_t*)malloc(std::max<uint64_t>(total, 1) * 4);
+      uint64_t k = 0;
+      for (uint64_t i = 0; i < n_items; ++i)
+        for (uint32_t c = 0; c < h_nnz[i]; ++c, ++k) {
+          ci[k] = (uint32_t)i;
+          cx[k] = h_si[h_so[i] + c];
+          cc[k] = h_sc[h_so[i] + c];
+        }
+      *child_item = ci;
+      *child_index = cx;
+      *child_count = cc;
+      *n_children = total;
+    }
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  });
+}
+
+int ptsbe_batch_upload(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t* shots,
+                       const uint32_t* eset_ids, uint64_t n_sets, ptsbe_batch** out) {
+  return guarded([&] {
+    if (!pl || !out) throw Failure(PTSBE_EINVAL, "null plan");
+    if (n_sets < 1) throw Failure(PTSBE_EINVAL, "need at least one error set");
+    if (n_sets >= (1ull << 32)) throw Failure(PTSBE_ECAPACITY, "more than 2^32 error sets");
+    CK(cudaSetDevice(pl->device));
+    std::unique_ptr<ptsbe_batch> bt(new ptsbe_batch);
+    bt->plan = pl;
+    bt->n_sets = n_sets;
+    bt->shots_host.assign(shots, shots + n_sets);
+    for (uint64_t i = 0; i < n_sets; ++i) {
+      if (shots[i] < 1) throw Failure(PTSBE_EINVAL, "proportional sampling needs m >= 1");
+      bt->total_shots += shots[i];
+    }
+    cudaStream_t st = pl->stream;
+    bt->kraus.alloc(std::max<size_t>(16, n_sets * pl->g), st);
+    bt->shots.alloc(n_sets * 4, st);
+    bt->ids.alloc(n_sets * 4, st);
+    if (pl->g) CK(cudaMemcpyAsync(bt->kraus.p, kraus_idx, n_sets * pl->g, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(bt->shots.p, shots, n_sets * 4, cudaMemcpyHostToDevice, st));
+    if (eset_ids) {
+      CK(cudaMemcpyAsync(bt->ids.p, eset_ids, n_sets * 4, cudaMemcpyHostToDevice, st));
+    } else {
+      iota_kernel<<<cdiv(n_sets, 256), 256, 0, st>>>(bt->ids.as<uint32_t>(), (uint32_t)n_sets, 0);
+    }
+    CK(cudaStreamSynchronize(st));
+    *out = bt.release();
+  });
+}
+
+int ptsbe_batch_run(ptsbe_batch* bt, uint64_t seed, uint64_t* n_records, ptsbe_run_stats* stats) {
+  return guarded([&] {
+    if (!bt) throw Failure(PTSBE_EINVAL, "null batch");
+    ptsbe_run_stats local;
+    std::lock_guard<std::mutex> lock(bt->plan->mu);
+    run_batch(bt, seed, 1, stats ? stats : &local);
+    if (n_records) *n_records = bt->merged.n;
+  });
+}
+
+static void fetch_merged(ptsbe_batch* bt, uint64_t** keys, uint64_t** counts, uint64_t* n) {
+  ptsbe_plan* pl = bt->plan;
+  const uint64_t nr = bt->merged.n;
+  uint64_t* k = (uint64_t*)malloc(std::max<uint64_t>(nr, 1) * 8 * pl->words);
+  uint64_t* c = (uint64_t*)malloc(std::max<uint64_t>(nr, 1) * 8);
+  if (nr) {
+    CK(cudaMemcpyAsync(k, bt->merged.keys.p, nr * 8 * pl->words, cudaMemcpyDeviceToHost, pl->stream));
+    CK(cudaMemcpyAsync(c, bt->merged.counts.p, nr * 8, cudaMemcpyDeviceToHost, pl->stream));
+    CK(cudaStreamSynchronize(pl->stream));
+  }
+  *keys = k;
+  *counts = c;
+  *n = nr;
+}
+
+int ptsbe_batch_fetch(ptsbe_batch* bt, uint64_t** keys, uint64_t** counts, uint64_t* n_records) {
+  return guarded([&] {
+    if (!bt) throw Failure(PTSBE_EINVAL, "null batch");
+    std::lock_guard<std::mutex> lock(bt->plan->mu);
+    CK(cudaSetDevice(bt->plan->device));
+    fetch_merged(bt, keys, counts, n_records);
+  });
+}
+
+void ptsbe_batch_destroy(ptsbe_batch* bt) {
+  if (!bt) return;
+  cudaSetDevice(bt->plan->device);
+  cudaStreamSynchronize(bt->plan->stream);
+  delete bt;
+}
+
+int ptsbe_sample(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t* shots,
+                 const uint32_t* eset_ids, uint64_t n_sets, uint64_t seed, int merged,
+                 uint64_t** keys, uint32_t** rec_eset, uint64_t** counts, uint64_t* n_records,
+                 ptsbe_run_stats* stats) {
+  ptsbe_batch* bt = nullptr;
+  ptsbe_run_stats local;
+  if (!stats) stats = &local;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
+  int rc = guarded([&] {
+    if (!pl) throw Failure(PTSBE_EINVAL, "null plan");
+    CK(cudaSetDevice(pl->device));
+    CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+    CK(cudaEventCreate(&e2)); CK(cudaEventCreate(&e3));
+    CK(cudaEventRecord(e0, pl->stream));
+  });
+  if (rc) return rc;
+  rc = ptsbe_batch_upload(pl, kraus_idx, shots, eset_ids, n_sets, &bt);
+  if (rc) return rc;
+  rc = guarded([&] {
+    std::lock_guard<std::mutex> lock(pl->mu);
+    CK(cudaEventRecord(e1, pl->stream));
+    run_batch(bt, seed, merged, stats);
+    CK(cudaEventRecord(e2, pl->stream));
+    const uint32_t words = pl->words;
+    if (merged) {
+      fetch_merged(bt, keys, counts, n_records);
+      if (rec_eset) *rec_eset = nullptr;
+    } else {
+      const uint64_t nr = bt->per_set.n;
+      std::vector<uint64_t> soa(std::max<uint64_t>(nr, 1) * words);
+      std::vector<uint32_t> c32(std::max<uint64_t>(nr, 1));
+      uint64_t* k = (uint64_t*)malloc(std::max<uint64_t>(nr, 1) * 8 * words);
+      uint64_t* c = (uint64_t*)malloc(std::max<uint64_t>(nr, 1) * 8);
+      uint32_t* es = (uint32_t*)malloc(std::max<uint64_t>(nr, 1) * 4);
+      if (nr) {
+        CK(cudaMemcpyAsync(soa.data(), bt->per_set.keys.p, nr * 8 * words, cudaMemcpyDeviceToHost, pl->stream));
+        CK(cudaMemcpyAsync(c32.data(), bt->per_set.counts.p, nr * 4, cudaMemcpyDeviceToHost, pl->stream));
+        CK(cudaMemcpyAsync(es, bt->per_set.eset.p, nr * 4, cudaMemcpyDeviceToHost, pl->stream));
+        CK(cudaStreamSynchronize(pl->stream));
+      }
+      for (uint64_t i = 0; i < nr; ++i) {
+        for (uint32_t w = 0; w < words; ++w) k[i * words + w] = soa[(uint64_t)w * nr + i];
+        c[i] = c32[i];
+      }
+      *keys = k; *counts = c; *n_records = nr;
+      if (rec_eset) *rec_eset = es; else free(es);
+    }
+    CK(cudaEventRecord(e3, pl->stream));
+    CK(cudaStreamSynchronize(pl->stream));
+    CK(cudaEventElapsedTime(&stats->h2d_ms, e0, e1));
+    CK(cudaEventElapsedTime(&stats->d2h_ms, e2, e3));
+    stats->h2d_bytes = n_sets * pl->g + n_sets * 4 * (eset_ids ? 2 : 1);
+    stats->d2h_bytes = *n_records * (8ull * words + (merged ? 8 : 8));
+  });
+  ptsbe_batch_destroy(bt);
+  if (e0) { cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2); cudaEventDestroy(e3); }
+  return rc;
+}
+
+int ptsbe_histogram_merge(const uint64_t* keys, const uint64_t* counts, uint64_t n,
+                          uint32_t words, uint64_t** out_keys, uint64_t** out_counts,
+                          uint64_t* n_out, int device) {
+  return guarded([&] {
+    if (ptsbe_device_count() <= device)
+      throw Failure(PTSBE_EDEVICE, "no CUDA device: libptsbe_b200 has no CPU fallback");
+    if (words < 1) throw Failure(PTSBE_EINVAL, "words must be >= 1");
+    CK(cudaSetDevice(device));
+    g_launches = 0;
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    {
+      // item-major host keys -> SoA device keys
+      std::vector<uint64_t> soa(std::max<uint64_t>(n, 1) * words);
+      for (uint64_t i = 0; i < n; ++i)
+        for (uint32_t w = 0; w < words; ++w) soa[(uint64_t)w * n + i] = keys[i * words + w];
+      DevBuf dk(std::max<uint64_t>(n, 1) * 8 * words, st), dc(std::max<uint64_t>(n, 1) * 8, st);
+      if (n) {
+        CK(cudaMemcpyAsync(dk.p, soa.data(), n * 8 * words, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dc.p, counts, n * 8, cudaMemcpyHostToDevice, st));
+      }
+      Histogram h;
+      reduce_by_key(dk.as<uint64_t>(), n, words, nullptr, dc.as<uint64_t>(), n, 64 * words, h, st);
+      uint64_t* k = (uint64_t*)malloc(std::max<uint64_t>(h.n, 1) * 8 * words);
+      uint64_t* c = (uint64_t*)malloc(std::max<uint64_t>(h.n, 1) * 8);
+      if (h.n) {
+        CK(cudaMemcpyAsync(k, h.keys.p, h.n * 8 * words, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(c, h.counts.p, h.n * 8, cudaMemcpyDeviceToHost, st));
+      }
+      CK(cudaStreamSynchronize(st));
+      *out_keys = k; *out_counts = c; *n_out = h.n;
+    }
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,224 @@
+// Host-side contraction-path search (north-star subsystem 1): randomized greedy
+// descents over the error-free template network, scored with a batch-aware
+// cost.  A path is found once per stage and stored; every error set and every
+// prefix replays it (engine.py:864-879, planner.py:416-442).
+//
+// Differences from the reference planner (planner.py:121-251) are deliberate:
+//   * native code, so hundreds of descents on 1000-operand networks cost
+//     milliseconds instead of minutes;
+//   * every operand carries a dependency class (0 = depends on the error set
+//     only, k = also on prefix bits measured up to stage k).  A step's cost is
+//     flops x (number of distinct instances of its result in the batch), which
+//     is what the executor really pays once error-independent subtrees are
+//     hoisted and computed once per error set / per earlier-stage prefix;
+//   * a soft cap keeps intermediates inside the on-chip arena.
+// The flop model itself is the reference's: product of the dims of the union of
+// both operands' labels (planner.py:61-103), reported next to the weighted cost.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <queue>
+#include <vector>
+
+#include "../../include/ptsbe_b200.h"
+
+namespace {
+
+struct Rng {  // splitmix64
+  uint64_t s;
+  explicit Rng(uint64_t seed) : s(seed) {}
+  uint64_t next() {
+    uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  double uniform() { return ((next() >> 11) + 0.5) * (1.0 / 9007199254740992.0); }
+};
+
+struct Cand {
+  double key, tie;
+  uint32_t x, y, vx, vy;
+  bool operator<(const Cand& o) const {  // min-heap through std::priority_queue
+    if (key != o.key) return key > o.key;
+    return tie > o.tie;
+  }
+};
+
+struct Problem {
+  uint32_t n;
+  std::vector<std::vector<int32_t>> labels;  // dense label ids, sorted
+  std::vector<double> log2dim;               // per label
+  std::vector<uint32_t> cls;
+  std::vector<double> logw;  // log class weight
+  uint32_t n_labels;
+  double cap_log2;
+};
+
+struct Descent {
+  std::vector<uint32_t> merges;
+  double weighted = 0, flops = 0;
+};
+
+static Descent descend(const Problem& P, Rng& rng, double temperature) {
+  const uint32_t n = P.n;
+  std::vector<std::vector<int32_t>> lab = P.labels;
+  std::vector<uint32_t> cls = P.cls, version(n, 0);
+  std::vector<char> alive(n, 1);
+  std::vector<double> lsize(n, 0.0);
+  std::vector<int32_t> own(2 * (size_t)P.n_labels, -1);
+  for (uint32_t t = 0; t < n; ++t)
+    for (int32_t l : lab[t]) {
+      lsize[t] += P.log2dim[l];
+      if (own[2 * l] < 0) own[2 * l] = (int32_t)t; else own[2 * l + 1] = (int32_t)t;
+    }
+  auto other = [&](int32_t l, uint32_t t) -> int32_t {
+    return own[2 * l] == (int32_t)t ? own[2 * l + 1] : own[2 * l];
+  };
+  std::priority_queue<Cand> heap;
+  auto measure = [&](uint32_t x, uint32_t y, double& lunion, double& lshared, double& lout) {
+    lshared = 0;
+    const auto &a = lab[x], &b = lab[y];
+    size_t i = 0, j = 0;
+    while (i < a.size() && j < b.size()) {
+      if (a[i] < b[j]) ++i;
+      else if (a[i] > b[j]) ++j;
+      else { lshared += P.log2dim[a[i]]; ++i; ++j; }
+    }
+    lunion = lsize[x] + lsize[y] - lshared;
+    lout = lunion - lshared;
+  };
+  auto push = [&](uint32_t x, uint32_t y) {
+    if (x > y) std::swap(x, y);
+    double lu, ls, lo;
+    measure(x, y, lu, ls, lo);
+    // reference score: flops(step) - prod(shared dims), compared in log space
+    const double score = std::max(0.0, std::exp2(std::min(lu, 1000.0)) - std::exp2(ls));
+    double key = std::log1p(score) + P.logw[std::max(cls[x], cls[y])];
+    if (lo > P.cap_log2) key += 50.0 * (lo - P.cap_log2) + 100.0;
+    if (temperature > 0.0) {
+      const double u = rng.uniform();
+      key += temperature * -std::log(-std::log(u));
+    }
+    heap.push(Cand{key, rng.uniform(), x, y, version[x], version[y]});
+  };
+  for (uint32_t t = 0; t < n; ++t)
+    for (int32_t l : lab[t]) {
+      const int32_t o = other(l, t);
+      if (o > (int32_t)t) push(t, (uint32_t)o);
+    }
+  Descent D;
+  D.merges.reserve(2 * (size_t)n);
+  uint32_t remaining = n;
+  std::vector<int32_t> merged;
+  while (remaining > 1) {
+    uint32_t x = 0, y = 0;
+    bool found = false;
+    while (!heap.empty()) {
+      const Cand c = heap.top();
+      heap.pop();
+      if (alive[c.x] && alive[c.y] && version[c.x] == c.vx && version[c.y] == c.vy) {
+        x = c.x; y = c.y; found = true;
+        break;
+      }
+    }
+    if (!found) {  // disconnected pieces: outer product of the two smallest
+      int64_t s1 = -1, s2 = -1;
+      for (uint32_t t = 0; t < n; ++t) {
+        if (!alive[t]) continue;
+        if (s1 < 0 || lsize[t] < lsize[s1]) { s2 = s1; s1 = t; }
+        else if (s2 < 0 || lsize[t] < lsize[s2]) s2 = t;
+      }
+      x = (uint32_t)std::min(s1, s2);
+      y = (uint32_t)std::max(s1, s2);
+    }
+    double lu, ls, lo;
+    measure(x, y, lu, ls, lo);
+    const uint32_t c = std::max(cls[x], cls[y]);
+    const double fl = std::exp2(std::min(lu, 1000.0));
+    D.flops += fl;
+    D.weighted += fl * std::exp(P.logw[c]);
+    merged.clear();
+    std::set_symmetric_difference(lab[x].begin(), lab[x].end(), lab[y].begin(), lab[y].end(),
+                                  std::back_inserter(merged));
+    for (int32_t l : lab[y]) {  // y's labels now live on x; labels shared with x vanish
+      if (other(l, y) == (int32_t)x) {
+        own[2 * l] = own[2 * l + 1] = -1;
+      } else if (own[2 * l] == (int32_t)y) {
+        own[2 * l] = (int32_t)x;
+      } else {
+        own[2 * l + 1] = (int32_t)x;
+      }
+    }
+    lab[x] = merged;
+    lab[y].clear();
+    lab[y].shrink_to_fit();
+    alive[y] = 0;
+    cls[x] = c;
+    lsize[x] = lo;
+    version[x]++;
+    D.merges.push_back(x);
+    D.merges.push_back(y);
+    --remaining;
+    // re-score the neighbourhood of the merged tensor (each neighbour once)
+    std::vector<uint32_t> nb;
+    for (int32_t l : lab[x]) {
+      const int32_t o = other(l, x);
+      if (o >= 0 && o != (int32_t)x && alive[o]) nb.push_back((uint32_t)o);
+    }
+    std::sort(nb.begin(), nb.end());
+    nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+    for (uint32_t z : nb) push(x, z);
+  }
+  return D;
+}
+
+}  // namespace
+
+extern "C" int ptsbe_plan_greedy(uint32_t n_ops, const uint32_t* op_ptr, const int64_t* labels,
+                                 const uint32_t* dims, const uint32_t* op_class,
+                                 const double* class_weight, uint32_t n_classes,
+                                 uint32_t hypersamples, uint64_t seed, double size_cap_log2,
+                                 uint32_t* merges_out, double* cost_out, double* flops_out) {
+  if (n_ops < 1 || hypersamples < 1 || !op_ptr || !merges_out) return PTSBE_EINVAL;
+  Problem P;
+  P.n = n_ops;
+  P.labels.resize(n_ops);
+  P.cls.assign(n_ops, 0);
+  P.cap_log2 = size_cap_log2 > 0 ? size_cap_log2 : 1e9;
+  // densify labels
+  std::vector<int64_t> uniq(labels, labels + op_ptr[n_ops]);
+  std::sort(uniq.begin(), uniq.end());
+  uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+  P.n_labels = (uint32_t)uniq.size();
+  P.log2dim.assign(P.n_labels, 0.0);
+  std::vector<uint8_t> uses(P.n_labels, 0);
+  for (uint32_t t = 0; t < n_ops; ++t) {
+    for (uint32_t k = op_ptr[t]; k < op_ptr[t + 1]; ++k) {
+      const int32_t id = (int32_t)(std::lower_bound(uniq.begin(), uniq.end(), labels[k]) - uniq.begin());
+      P.labels[t].push_back(id);
+      P.log2dim[id] = std::log2((double)dims[k]);
+      if (++uses[id] > 2) return PTSBE_ESTRUCT;
+    }
+    std::sort(P.labels[t].begin(), P.labels[t].end());
+    if (op_class) P.cls[t] = op_class[t];
+  }
+  uint32_t nc = std::max<uint32_t>(1, n_classes);
+  P.logw.assign(nc, 0.0);
+  for (uint32_t c = 0; c < nc; ++c)
+    if (class_weight) P.logw[c] = std::log(std::max(class_weight[c], 1e-300));
+  for (uint32_t t = 0; t < n_ops; ++t)
+    if (P.cls[t] >= nc) return PTSBE_EINVAL;
+  Rng rng(seed * 0x9E3779B97F4A7C15ull + 0x1234567ull);
+  Descent best;
+  bool have = false;
+  for (uint32_t h = 0; h < hypersamples; ++h) {
+    const double temperature = h == 0 ? 0.0 : (h % 3 == 0 ? 0.5 : 1.0);
+    Descent d = descend(P, rng, temperature);
+    if (!have || d.weighted < best.weighted) { best = std::move(d); have = true; }
+  }
+  std::copy(best.merges.begin(), best.merges.end(), merges_out);
+  if (cost_out) *cost_out = best.weighted;
+  if (flops_out) *flops_out = best.flops;
+  return PTSBE_OK;
+}

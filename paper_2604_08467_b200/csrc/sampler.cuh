@@ -1,0 +1,234 @@
+// Non-degenerate batched sampler (north-star subsystem 3).
+//
+// For every unique (error set, prefix) work item of a stage: turn the
+// unnormalised marginal into an exact fixed-point CDF, draw the item's shot
+// multiplicity from counter-based Philox uniforms, and emit the non-empty
+// outcomes in ascending order.  The next stage's work list is then built by an
+// order-preserving compaction (scan.cuh), so children of one error set stay in
+// lexicographic prefix order -- the same order the reference iterates in
+// (engine.py:513-523 `for prefix in sorted(groups)`), which is what makes the
+// RNG stream of a work item (error-set id, stage, rank) reproducible on any
+// number of GPUs.
+//
+// Replaces rng.multinomial + flatnonzero + dict insert (engine.py:519-522).
+// Every operation that decides a count is integer arithmetic, so the CPU oracle
+// (oracle/ptsbe_oracle.py: fixed_point_weights / multinomial_counts) reproduces
+// the counts bit for bit from the same float64 marginals.
+#pragma once
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace ptsbe {
+
+// ---- Philox-4x32-10 (Salmon et al. 2011), counter = (c0,c1,c2,c3), key = (k0,k1) ----
+struct Philox4 { uint32_t v[4]; };
+
+__host__ __device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2,
+                                                          uint32_t c3, uint32_t k0, uint32_t k1) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)M0 * c0, p1 = (uint64_t)M1 * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+    const uint32_t n1 = (uint32_t)p1;
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    const uint32_t n3 = (uint32_t)p0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    k0 += W0; k1 += W1;
+  }
+  Philox4 o; o.v[0] = c0; o.v[1] = c1; o.v[2] = c2; o.v[3] = c3;
+  return o;
+}
+
+struct SampleArgs {
+  const void* probs;        // [items][nb] real, float (is_f32) or double
+  const uint32_t* mult;     // [items] shots to split
+  const uint32_t* slot_off; // [items] first output slot of the item (exclusive scan of mult)
+  const uint32_t* eset_id;  // [items] GLOBAL error-set id (RNG stream)
+  const uint32_t* rank;     // [items] rank of the prefix inside its error set (sorted order)
+  const double* mass;       // [items] or null
+  const double* minv;       // [items] or null
+  uint32_t* slot_index;     // [total shots] outcome index of each non-empty child
+  uint32_t* slot_count;     // [total shots] its count
+  uint32_t* nnz;            // [items] number of non-empty children
+  unsigned long long* flag; // [1] min over flagged items of (eset id << 16 | stage << 8 | kind)
+  uint32_t* flag_count;     // [1]
+  uint64_t n_items;
+  uint32_t first_item;      // probs/mass/minv are indexed by (item - first_item)
+  uint32_t b;               // nb = 2^b
+  uint32_t stage;
+  uint32_t k0, k1;          // Philox key = seed
+  uint32_t is_f32;
+  double vanish;            // engine.py:54 VANISHING_MASS
+  double neg_abs, neg_rel;  // engine.py:53 NEGATIVE_DIAG_TOLERANCE (+ relative term for c64)
+};
+
+constexpr int SAMPLE_THREADS = 128;
+
+// One CTA per work item.  Shared memory: u64 cdf[nb] + u32 cnt[nb] + scan scratch.
+__global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(const SampleArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const uint32_t nb = 1u << a.b;
+  uint64_t* cdf = reinterpret_cast<uint64_t*>(sm);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(cdf + nb);
+  __shared__ uint64_t ws64[33];
+  __shared__ uint32_t ws32[33];
+  __shared__ double redmax[SAMPLE_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t per = (nb + SAMPLE_THREADS - 1) / SAMPLE_THREADS;
+
+  for (uint64_t it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+    const uint64_t item = a.first_item + it;
+    const uint32_t m = a.mult[item];
+    // ---- load (coalesced), clamp, max ----
+    double* pd = reinterpret_cast<double*>(cdf);
+    double mx = 0.0;
+    if (a.is_f32) {
+      const float* p = reinterpret_cast<const float*>(a.probs) + it * nb;
+      for (uint32_t k = tid; k < nb; k += SAMPLE_THREADS) {
+        double v = (double)p[k]; v = v > 0.0 ? v : 0.0; pd[k] = v; mx = fmax(mx, v);
+      }
+    } else {
+      const double* p = reinterpret_cast<const double*>(a.probs) + it * nb;
+      for (uint32_t k = tid; k < nb; k += SAMPLE_THREADS) {
+        double v = p[k]; v = v > 0.0 ? v : 0.0; pd[k] = v; mx = fmax(mx, v);
+      }
+    }
+    for (uint32_t k = tid; k < nb; k += SAMPLE_THREADS) cnt[k] = 0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+    if (lane == 0) redmax[wid] = mx;
+    __syncthreads();
+    mx = redmax[0];
+#pragma unroll
+    for (int w = 1; w < SAMPLE_THREADS / 32; ++w) mx = fmax(mx, redmax[w]);
+
+    // ---- guards (engine.py:447-448, 475-476, 484-485) ----
+    uint32_t bad = 0;
+    if (a.mass) {
+      const double ms = a.mass[it], mn = a.minv[it];
+      if (mn < a.neg_abs - a.neg_rel * ms) bad = PTSBE_ENUMERIC;
+      else if (ms < a.vanish) bad = PTSBE_EIMPOSSIBLE;
+    }
+    if (!bad && !(mx > 0.0)) bad = PTSBE_EIMPOSSIBLE;
+    if (bad) {
+      if (tid == 0) {
+        a.nnz[item] = 0;
+        atomicMin(a.flag, ((unsigned long long)a.eset_id[item] << 16) |
+                              ((unsigned long long)(a.stage & 0xff) << 8) | bad);
+        atomicAdd(a.flag_count, 1u);
+      }
+      __syncthreads();
+      continue;
+    }
+
+    // ---- exact fixed-point weights: w_k = floor(p_k * 2^shift), shift from max only ----
+    int ex;
+    frexp(mx, &ex);                       // mx = f * 2^ex, f in [0.5, 1)
+    const int shift = (62 - (int)a.b) - ex;  // p_k * 2^shift < 2^(62-b)
+    const uint32_t k0 = tid * per;
+    uint64_t local = 0;
+    for (uint32_t k = k0; k < k0 + per && k < nb; ++k) {
+      const uint64_t w = (uint64_t)ldexp(pd[k], shift);
+      local += w;
+      cdf[k] = w;  // same 8-byte slot as pd[k]; only this thread touches it
+    }
+    uint64_t total;
+    uint64_t run = block_exclusive<uint64_t>(local, ws64, &total);
+    for (uint32_t k = k0; k < k0 + per && k < nb; ++k) {
+      run += cdf[k];
+      cdf[k] = run;  // inclusive
+    }
+    __syncthreads();
+
+    // ---- draws: outcome = #{k : cdf[k] <= r}, r = floor(x * W / 2^64) ----
+    const uint32_t rk = a.rank[item], es = a.eset_id[item];
+    for (uint32_t t = tid; t < m; t += SAMPLE_THREADS) {
+      const Philox4 x = philox4x32_10(t, rk, a.stage, es, a.k0, a.k1);
+      const uint64_t x64 = ((uint64_t)x.v[1] << 32) | x.v[0];
+      const uint64_t r = __umul64hi(x64, total);
+      uint32_t lo = 0, hi = nb;  // first index with cdf > r
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (cdf[mid] <= r) lo = mid + 1; else hi = mid;
+      }
+      atomicAdd(&cnt[lo], 1u);
+    }
+    __syncthreads();
+
+    // ---- ordered emission of non-empty outcomes ----
+    uint32_t mine = 0;
+    for (uint32_t k = k0; k < k0 + per && k < nb; ++k) mine += cnt[k] != 0;
+    uint32_t tot32;
+    uint32_t pos = block_exclusive<uint32_t>(mine, ws32, &tot32);
+    const uint32_t base = a.slot_off[item];
+    for (uint32_t k = k0; k < k0 + per && k < nb; ++k) {
+      const uint32_t c = cnt[k];
+      if (c) { a.slot_index[base + pos] = k; a.slot_count[base + pos] = c; ++pos; }
+    }
+    if (tid == 0) a.nnz[item] = tot32;
+    __syncthreads();
+  }
+}
+
+// ---- next-level construction ----------------------------------------------
+
+struct ExpandArgs {
+  // parent level
+  const uint32_t* p_eset; const uint64_t* p_prefix; uint32_t p_n;
+  const uint32_t* p_slot_off; const uint32_t* child_base;  // [p_n] exclusive scan of nnz
+  const uint32_t* slot_index; const uint32_t* slot_count;
+  // child level
+  uint32_t* c_eset; uint32_t* c_parent; uint64_t* c_prefix; uint32_t* c_mult; uint32_t c_n;
+  uint32_t words, offset, b;  // child prefix = parent prefix with b bits appended at qubit `offset`
+};
+
+__global__ void expand_kernel(const ExpandArgs a) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.c_n) return;
+  uint32_t lo = 0, hi = a.p_n;  // last parent with child_base <= c
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a.child_base[mid] <= c) lo = mid; else hi = mid;
+  }
+  const uint32_t w = lo, pos = c - a.child_base[w];
+  const uint32_t slot = a.p_slot_off[w] + pos;
+  const uint32_t idx = a.slot_index[slot];
+  a.c_eset[c] = a.p_eset[w];
+  a.c_parent[c] = w;
+  a.c_mult[c] = a.slot_count[slot];
+  // qubit q -> word q/64, bit 63-(q%64); first batch qubit = MSB of idx (engine.py:489-490)
+  for (uint32_t wd = 0; wd < a.words; ++wd) {
+    uint64_t v = a.p_prefix[(size_t)wd * a.p_n + w];
+    const int q0 = (int)wd * 64, q1 = q0 + 64;
+    const int s = max(q0, (int)a.offset), e = min(q1, (int)(a.offset + a.b));
+    for (int q = s; q < e; ++q) {
+      const uint64_t bit = (idx >> (a.b - 1 - (q - a.offset))) & 1u;
+      v |= bit << (63 - (q - q0));
+    }
+    a.c_prefix[(size_t)wd * a.c_n + c] = v;
+  }
+}
+
+// rank of an item inside its error set = index - first index of that error set
+__global__ void segment_start_kernel(const uint32_t* eset, uint32_t n, uint32_t* seg_start) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i == 0 || eset[i] != eset[i - 1]) seg_start[eset[i]] = i;
+}
+__global__ void rank_kernel(const uint32_t* eset, const uint32_t* seg_start,
+                            const uint32_t* global_id, uint32_t n, uint32_t* rank,
+                            uint32_t* gid) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t e = eset[i];
+  rank[i] = i - seg_start[e];
+  gid[i] = global_id[e];
+}
+
+__global__ void iota_kernel(uint32_t* p, uint32_t n, uint32_t add) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = i + add;
+}
+
+}  // namespace ptsbe

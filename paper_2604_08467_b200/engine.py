@@ -1,0 +1,942 @@
+"""Trajectory engine of the drop-in host API, running on the B200 path.
+
+Same public names, argument meaning and error behaviour as the reference
+engine for the proportional PTSBE path
+(/root/reference/pkg/src/ptsbe/engine.py:57-524, 664-929); the arithmetic is
+done by libptsbe_b200.so:
+
+  merge_errors (UPV, engine.py:284-313)      -> per-site variant tables, gathered on device
+  marginal_network (engine.py:361-407)       -> static operand table built once per stage
+  _contract_marginal (engine.py:417-450)     -> exec_kernel + fused epilogue
+  sample_proportional (engine.py:493-524)    -> sample_kernel + order-preserving compaction
+  merge_records (engine.py:815-829)          -> device sort + reduce-by-key
+  run_ptsbe fan-out (engine.py:885-906)      -> one batched run over all error sets
+
+New, batch-granular entry points:
+`conditional_marginals_batched` and `sample_proportional_batched`.
+
+Out of scope (SURVEY.md sections 2 and 8f): the non-proportional sampler and the
+deliberately slow comparison modes.  Their names are exported for import
+compatibility and raise NotImplementedError when called.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import time
+from dataclasses import dataclass, field
+from typing import NamedTuple, Optional, Sequence
+
+import numpy as np
+
+from . import compiler
+from .circuits import (
+    PAULI_KINDS,
+    TWO_QUBIT_PAULIS,
+    Circuit,
+    build_network,
+    final_qubit_labels,
+    gate_matrix,
+    is_identity_label,
+    pauli_matrix,
+)
+from .compiler import SEL_CONST, SEL_KRAUS, SEL_PREFIX, CompiledPlan, Operand, Pool
+from .errors import (
+    STATUS_TO_ERROR,
+    ImpossiblePrefixError,
+    NetworkStructureError,
+    NumericalError,
+    ResourceLimitError,
+    SimulationError,
+)
+from .planner import PathCache, cache_lookup_or_plan
+from .tensor import DEFAULT_INTERMEDIATE_CEILING, Index, Tensor, TensorNetwork
+
+NEGATIVE_DIAG_TOLERANCE = -1e-12
+VANISHING_MASS = 1e-12
+
+_BASIS = np.eye(2, dtype=np.complex128)
+_COPY3 = np.zeros((2, 2, 2), dtype=np.complex128)
+_COPY3[0, 0, 0] = _COPY3[1, 1, 1] = 1.0
+
+_KEY_PRESAMPLE, _KEY_SAMPLER, _KEY_BASELINE, _KEY_PLANNER = 0, 1, 2, 3
+
+
+def spawn_rng(seed: int, *key: int) -> np.random.Generator:
+    """Independent generator per key path (engine.py:57-59)."""
+    return np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=key))
+
+
+@dataclass(frozen=True)
+class ErrorSet:
+    """One pre-sampled realization: operator label per gate site plus its shot
+    allocation (engine.py:62-73)."""
+
+    id: int
+    realized: tuple
+    m: int
+
+    def __post_init__(self):
+        if self.m < 0:
+            raise ValueError("shot allocation must be non-negative")
+
+
+@dataclass(frozen=True)
+class BatchPlan:
+    """Ordered qubit batches for staged sampling (engine.py:76-142).  The
+    non-proportional knobs are carried for API compatibility only."""
+
+    sizes: tuple
+    nonfinal_shots: int = 1
+    final_mode: str = "exhaustive"
+    direct_count: int = 1
+    threshold: float = 1e-6
+
+    def __post_init__(self):
+        object.__setattr__(self, "sizes", tuple(int(b) for b in self.sizes))
+        if not self.sizes or min(self.sizes) < 1:
+            raise ValueError(f"batch sizes must be positive, got {self.sizes}")
+        if self.final_mode not in ("direct", "exhaustive"):
+            raise ValueError(f"unknown final mode {self.final_mode!r}")
+        if self.direct_count < 1:
+            raise ValueError("direct count must be >= 1")
+        if self.threshold <= 0.0:
+            raise ValueError("exhaustive threshold must be positive")
+        if self.nonfinal_shots < 1:
+            raise ValueError("nonfinal_shots must be >= 1")
+
+    @property
+    def f(self) -> int:
+        return len(self.sizes)
+
+    @property
+    def n(self) -> int:
+        return sum(self.sizes)
+
+    def offset(self, j: int) -> int:
+        return sum(self.sizes[: j - 1])
+
+    def stage_qubits(self, j: int) -> range:
+        lo = self.offset(j)
+        return range(lo, lo + self.sizes[j - 1])
+
+    def stage_of_qubit(self, q: int) -> int:
+        acc = 0
+        for j, b in enumerate(self.sizes, start=1):
+            acc += b
+            if q < acc:
+                return j
+        raise ValueError(f"qubit {q} outside the plan")
+
+    @classmethod
+    def fixed(cls, n: int, b: int, **kw) -> "BatchPlan":
+        if b < 1:
+            raise ValueError("batch size must be >= 1")
+        f = max(1, math.ceil(n / b))
+        return cls(sizes=tuple([b] * (f - 1) + [n - b * (f - 1)]), **kw)
+
+    @classmethod
+    def with_final(cls, n: int, nonfinal: int = 10, final: int = 28, **kw) -> "BatchPlan":
+        last = min(final, n)
+        k, r = divmod(n - last, nonfinal)
+        return cls(sizes=tuple([nonfinal] * k + ([r] if r else []) + [last]), **kw)
+
+
+@dataclass
+class ShotRecord:
+    bitstring: str
+    count: int
+    prob: Optional[float] = None
+
+
+@dataclass
+class EngineStats:
+    """Plan/contraction counters and times per stage (engine.py:155-181).
+    On this path `contract_seconds` / `stage_seconds` are device times."""
+
+    plan_events: int = 0
+    contract_events: int = 0
+    path_seconds: float = 0.0
+    contract_seconds: float = 0.0
+    stage_events: dict = field(default_factory=dict)
+    stage_seconds: dict = field(default_factory=dict)
+
+    def record_contraction(self, stage: int, seconds: float, events: int = 1) -> None:
+        self.contract_events += events
+        self.contract_seconds += seconds
+        self.stage_events[stage] = self.stage_events.get(stage, 0) + events
+        self.stage_seconds[stage] = self.stage_seconds.get(stage, 0.0) + seconds
+
+    def merge(self, other: "EngineStats") -> None:
+        self.plan_events += other.plan_events
+        self.contract_events += other.contract_events
+        self.path_seconds += other.path_seconds
+        self.contract_seconds += other.contract_seconds
+        for k, v in other.stage_events.items():
+            self.stage_events[k] = self.stage_events.get(k, 0) + v
+        for k, v in other.stage_seconds.items():
+            self.stage_seconds[k] = self.stage_seconds.get(k, 0.0) + v
+
+
+@dataclass
+class SamplerContext:
+    """Cache, counters, planner settings and guards of one run
+    (engine.py:184-209) plus the device knobs."""
+
+    cache: PathCache = field(default_factory=PathCache)
+    stats: EngineStats = field(default_factory=EngineStats)
+    hypersamples: int = 100
+    planner_seed: int = 0
+    max_intermediate: int = DEFAULT_INTERMEDIATE_CEILING
+    deadline: Optional[float] = None
+    dtype: str = "complex128"
+    device: int = 0
+
+    def check_deadline(self) -> None:
+        if self.deadline is not None and time.perf_counter() > self.deadline:
+            raise ResourceLimitError("wall-clock deadline exceeded")
+
+    def fork(self) -> "SamplerContext":
+        return SamplerContext(
+            cache=self.cache, stats=EngineStats(), hypersamples=self.hypersamples,
+            planner_seed=self.planner_seed, max_intermediate=self.max_intermediate,
+            deadline=self.deadline, dtype=self.dtype, device=self.device,
+        )
+
+
+@dataclass(frozen=True)
+class CircuitNetwork:
+    """Uncontracted network + per-qubit final labels (engine.py:212-229).
+    `channels` (one NoiseChannel or None per gate site) lets non-Pauli
+    operator labels such as "K1" be resolved; Pauli labels need nothing."""
+
+    net: TensorNetwork
+    final_labels: tuple
+    channels: Optional[tuple] = None
+
+    @classmethod
+    def from_circuit(cls, c: Circuit) -> "CircuitNetwork":
+        return cls(net=build_network(c), final_labels=final_qubit_labels(c),
+                   channels=tuple(g.noise for g in c.gates))
+
+    @property
+    def n(self) -> int:
+        return len(self.final_labels)
+
+    def operator(self, site: int, label: str) -> np.ndarray:
+        if self.channels is not None and self.channels[site] is not None:
+            return self.channels[site].operator(label)
+        return pauli_matrix(label)
+
+    def merged(self, k: ErrorSet) -> "CircuitNetwork":
+        return CircuitNetwork(net=merge_errors(self.net, k, self), final_labels=self.final_labels)
+
+
+def draw_realization(c: Circuit, rng: np.random.Generator) -> tuple:
+    """One realized label per gate site.  The rng call order for the
+    reference's channel kinds is the reference's (engine.py:232-244), so a
+    seed produces the same realization in both packages."""
+    out = []
+    for g in c.gates:
+        ch = g.noise
+        if rng.random() < ch.p:
+            if ch.kind == "depolarizing":
+                out.append(TWO_QUBIT_PAULIS[int(rng.integers(15))])
+            elif ch.kind == "depolarizing1":
+                out.append(PAULI_KINDS[int(rng.integers(3))])
+            elif ch.kind == "amplitude_damping":
+                out.append("K1")
+            else:
+                out.append(ch.kind)
+        else:
+            out.append(ch.identity_label())
+    return tuple(out)
+
+
+def _allocate(e: int, rule: str, total_shots: int, shots_per_set) -> list:
+    if e < 1:
+        raise ValueError("need at least one error set")
+    if rule == "proportional":
+        if total_shots < e:
+            raise ValueError("proportional rule needs total_shots >= number of sets")
+        base, rem = divmod(total_shots, e)
+        return [base + 1 if i < rem else base for i in range(e)]
+    if rule == "uniform":
+        if shots_per_set is None:
+            raise ValueError("uniform rule needs shots_per_set")
+        if isinstance(shots_per_set, (int, np.integer)):
+            return [int(shots_per_set)] * e
+        alloc = [int(v) for v in shots_per_set]
+        if len(alloc) != e:
+            raise ValueError("shots_per_set length must equal number of sets")
+        return alloc
+    raise ValueError(f"unknown allocation rule {rule!r}")
+
+
+def presample_errors(c: Circuit, e: int, rule: str = "proportional", total_shots: int = 0,
+                     rng: Optional[np.random.Generator] = None, shots_per_set=None) -> list:
+    """Draw `e` realizations and allot shots (engine.py:247-281)."""
+    alloc = _allocate(e, rule, total_shots, shots_per_set)
+    if rng is None:
+        rng = np.random.default_rng()
+    return [ErrorSet(id=i, realized=draw_realization(c, rng), m=alloc[i]) for i in range(e)]
+
+
+def merge_errors(template: TensorNetwork, k: ErrorSet, owner: Optional[CircuitNetwork] = None) -> TensorNetwork:
+    """UPV on the host carriers: error operator left-multiplied into its gate
+    tensor, structure untouched (engine.py:284-313).  The device path never
+    calls this per error set -- it gathers from variant tables -- but the
+    single-network API (`CircuitNetwork.merged`) keeps the reference meaning."""
+    g = len(k.realized)
+    n = len(template.operands) - g
+    if n < 1:
+        raise NetworkStructureError(
+            f"realization has {g} sites but network has {len(template.operands)} operands"
+        )
+    ops = list(template.operands)
+    for site, label in enumerate(k.realized):
+        if is_identity_label(label):
+            continue
+        old = ops[n + site]
+        op = owner.operator(site, label) if owner is not None else pauli_matrix(label)
+        arity = int(round(math.log2(op.shape[0])))
+        if old.data.ndim != 2 * arity:
+            raise NetworkStructureError(
+                f"site {site}: {arity}-qubit error on {old.data.ndim // 2}-qubit gate"
+            )
+        side = 1 << arity
+        ops[n + site] = Tensor(old.indices, (op @ old.data.reshape(side, side)).reshape(old.data.shape))
+    return TensorNetwork(ops, template.open_indices)
+
+
+class MarginalNetwork(NamedTuple):
+    net: TensorNetwork
+    open_labels: tuple
+
+
+def _stage_layout(cnet: CircuitNetwork, plan: BatchPlan, j: int):
+    """Label bookkeeping of the stage-j sandwich (engine.py:373-406): returns
+    (bra label map, list of (qubit, ket leg, bra leg) for prefix qubits, list of
+    (qubit, ket leg, bra leg, open leg) for batch qubits)."""
+    n = cnet.n
+    if not 1 <= j <= plan.f:
+        raise ValueError(f"stage {j} outside 1..{plan.f}")
+    offset = plan.offset(j)
+    batch = plan.stage_qubits(j)
+    fresh = 1 + max((ix.label for t in cnet.net.operands for ix in t.indices), default=0)
+    bra = {}
+    for t in cnet.net.operands:
+        for ix in t.indices:
+            if ix.label not in bra:
+                bra[ix.label] = fresh
+                fresh += 1
+    for q in range(batch.stop, n):  # traced qubits: bra leg joins the ket leg
+        bra[cnet.final_labels[q]] = cnet.final_labels[q]
+    fixed = [(q, cnet.final_labels[q], bra[cnet.final_labels[q]]) for q in range(offset)]
+    opened = []
+    for q in batch:
+        opened.append((q, cnet.final_labels[q], bra[cnet.final_labels[q]], fresh))
+        fresh += 1
+    return bra, fixed, opened
+
+
+def marginal_network(cnet: CircuitNetwork, plan: BatchPlan, j: int, prefix: str) -> MarginalNetwork:
+    """Host carrier of the stage-j sandwich for one prefix, operand order as in
+    the reference (engine.py:361-407) so signatures -- and therefore cached
+    paths -- are interchangeable between the two packages."""
+    bra, fixed, opened = _stage_layout(cnet, plan, j)
+    if len(prefix) != len(fixed):
+        raise ValueError(f"stage {j} expects a {len(fixed)}-bit prefix, got {len(prefix)}")
+    ops = list(cnet.net.operands)
+    ops.extend(t.conj().relabeled(bra) for t in cnet.net.operands)
+    for q, ket_leg, bra_leg in fixed:
+        vec = _BASIS[1] if prefix[q] == "1" else _BASIS[0]
+        ops.append(Tensor([Index(ket_leg, 2)], vec))
+        ops.append(Tensor([Index(bra_leg, 2)], vec))
+    for _, ket_leg, bra_leg, open_leg in opened:
+        ops.append(Tensor([Index(ket_leg, 2), Index(bra_leg, 2), Index(open_leg, 2)], _COPY3))
+    opens = tuple(o[3] for o in opened)
+    return MarginalNetwork(net=TensorNetwork(ops, opens), open_labels=opens)
+
+
+# ---------------------------------------------------------------------------
+# device pipeline
+# ---------------------------------------------------------------------------
+
+class VariantTables:
+    """Per gate site: the distinct realized labels of a batch of error sets and
+    the merged tensors `operator @ gate` (UPV, engine.py:300-312).  Error sets
+    become rows of a uint8 index matrix."""
+
+    def __init__(self, cnet: CircuitNetwork, n_sites: int, labels_per_site: Sequence[Sequence[str]]):
+        self.n_sites = n_sites
+        self.labels = [list(lbs) for lbs in labels_per_site]
+        self.index = [{lb: k for k, lb in enumerate(lbs)} for lbs in self.labels]
+        n_kets = len(cnet.net.operands) - n_sites
+        self.data = []
+        for site, lbs in enumerate(self.labels):
+            base = cnet.net.operands[n_kets + site]
+            side = int(round(math.sqrt(base.data.size)))
+            rows = []
+            for lb in lbs:
+                if is_identity_label(lb):
+                    rows.append(base.data.reshape(-1))
+                    continue
+                op = cnet.operator(site, lb)
+                if op.shape[0] != side:
+                    arity = int(round(math.log2(op.shape[0])))
+                    raise NetworkStructureError(
+                        f"site {site}: {arity}-qubit error on {base.data.ndim // 2}-qubit gate"
+                    )
+                rows.append((op @ base.data.reshape(side, side)).reshape(-1))
+            if len(rows) > 255:
+                raise ValueError(f"site {site}: more than 255 distinct operators")
+            self.data.append(np.asarray(rows, dtype=np.complex128))
+
+    @classmethod
+    def from_errorsets(cls, cnet: CircuitNetwork, errorsets: Sequence[ErrorSet]) -> "VariantTables":
+        if not errorsets:
+            raise ValueError("need at least one error set")
+        g = len(errorsets[0].realized)
+        if len(cnet.net.operands) - g < 1:
+            raise NetworkStructureError(
+                f"realization has {g} sites but network has {len(cnet.net.operands)} operands"
+            )
+        seen = [dict() for _ in range(g)]
+        for k in errorsets:
+            if len(k.realized) != g:
+                raise NetworkStructureError("realization length does not match gate count")
+            for site, lb in enumerate(k.realized):
+                seen[site].setdefault(lb, None)
+        return cls(cnet, g, [list(d) for d in seen])
+
+    @classmethod
+    def from_channels(cls, cnet: CircuitNetwork) -> "VariantTables":
+        """Full tables from the circuit's channels (index = position in
+        `NoiseChannel.outcomes()`)."""
+        if cnet.channels is None:
+            raise ValueError("network carries no channels")
+        return cls(cnet, len(cnet.channels), [[lb for lb, _ in ch.outcomes()] for ch in cnet.channels])
+
+    @classmethod
+    def none(cls, cnet: CircuitNetwork) -> "VariantTables":
+        return cls(cnet, 0, [])
+
+    def encode(self, errorsets: Sequence[ErrorSet]) -> np.ndarray:
+        out = np.zeros((len(errorsets), max(self.n_sites, 0)), dtype=np.uint8)
+        for r, k in enumerate(errorsets):
+            for site, lb in enumerate(k.realized):
+                out[r, site] = self.index[site][lb]
+        return out
+
+
+def stage_operands(cnet: CircuitNetwork, plan: BatchPlan, j: int, tables: VariantTables):
+    """Static operand table of the stage-j sandwich, same operand order as
+    `marginal_network`.  Returns (operands, open label order)."""
+    bra, fixed, opened = _stage_layout(cnet, plan, j)
+    n_kets = len(cnet.net.operands) - tables.n_sites
+    ops = []
+    for conj in (False, True):
+        for slot, t in enumerate(cnet.net.operands):
+            labels = tuple(bra.get(lb, lb) for lb in t.labels) if conj else t.labels
+            dims = tuple(ix.dim for ix in t.indices)
+            site = slot - n_kets
+            if site >= 0:
+                data, kind, arg = tables.data[site], SEL_KRAUS, site
+                if data.shape[0] == 1:
+                    kind = SEL_CONST
+            else:
+                data, kind, arg = t.data.reshape(1, -1), SEL_CONST, 0
+            ops.append(Operand(labels, dims, np.conj(data) if conj else data, kind, arg, 0))
+    for q, ket_leg, bra_leg in fixed:
+        s = plan.stage_of_qubit(q)
+        ops.append(Operand((ket_leg,), (2,), _BASIS, SEL_PREFIX, q, s))
+        ops.append(Operand((bra_leg,), (2,), _BASIS, SEL_PREFIX, q, s))
+    for _, ket_leg, bra_leg, open_leg in opened:
+        ops.append(Operand((ket_leg, bra_leg, open_leg), (2, 2, 2), _COPY3.reshape(1, -1)))
+    return ops, tuple(o[3] for o in opened)
+
+
+def _size_cap_log2(dtype: str) -> float:
+    return 13.0 if dtype == "complex64" else 12.0
+
+
+class DevicePipeline:
+    """Plans (once), compiles and owns the device plan of one
+    (circuit structure, batch plan, variant tables) triple."""
+
+    def __init__(self, cnet: CircuitNetwork, plan: BatchPlan, tables: VariantTables,
+                 ctx: SamplerContext, stages: Optional[Sequence[int]] = None,
+                 shots_per_set: float = 1.0):
+        from . import _capi
+
+        if plan.n != cnet.n:
+            raise ValueError(f"plan covers {plan.n} qubits, circuit has {cnet.n}")
+        self.cnet, self.plan, self.tables, self.ctx = cnet, plan, tables, ctx
+        elem = 8 if ctx.dtype == "complex64" else 16
+        pool = Pool()
+        programs = []
+        self.paths = {}
+        self.stage_flops = {}
+        want = set(range(1, plan.f + 1)) if stages is None else set(stages)
+        for j in range(1, plan.f + 1):
+            if j not in want:
+                programs += [_empty_program(p + 1, 1 << plan.sizes[j - 1] if p == j - 1 else 0) for p in range(j)]
+                continue
+            ops, opens = stage_operands(cnet, plan, j, tables)
+            mnet = marginal_network(cnet, plan, j, "0" * plan.offset(j))
+            # distinct instances of a class-k result: unique prefixes entering stage k+1
+            weights = [float(min(shots_per_set, 2.0 ** min(plan.offset(k + 1), 60))) for k in range(j)]
+            t0 = time.perf_counter()
+            path, hit = cache_lookup_or_plan(
+                ctx.cache, mnet.net, stage=j, hypersamples=ctx.hypersamples,
+                rng=spawn_rng(ctx.planner_seed, _KEY_PLANNER, j),
+                op_class=[o.cls for o in ops], class_weight=weights,
+                size_cap_log2=_size_cap_log2(ctx.dtype),
+            )
+            if not hit:
+                ctx.stats.plan_events += 1
+                ctx.stats.path_seconds += time.perf_counter() - t0
+            self.paths[j] = path
+            progs, _ = compiler.compile_stage(ops, path.steps, opens, j, pool, elem,
+                                              ceiling=ctx.max_intermediate)
+            self.stage_flops[j] = [p.flops for p in progs]
+            programs += progs
+        self.compiled = CompiledPlan(
+            dtype=ctx.dtype, n_qubits=plan.n, n_sites=tables.n_sites, sizes=plan.sizes,
+            pool=pool.finish(ctx.dtype), programs=programs, max_intermediate=ctx.max_intermediate,
+        )
+        self.device_plan = _capi.DevicePlan(self.compiled, ctx.device)
+
+    def close(self):
+        self.device_plan.close()
+
+    def programs_of(self, j: int):
+        base = j * (j - 1) // 2
+        return self.compiled.programs[base: base + j]
+
+
+def _empty_program(level: int, out_elems: int) -> compiler.Program:
+    return compiler.Program(
+        leaves=np.zeros((0, compiler.LEAF_WORDS), np.uint32), steps=np.zeros((0, compiler.STEP_WORDS), np.uint32),
+        tables=np.zeros(0, np.uint32), arena_fast=0, arena_spill=0, out_elems=out_elems, threads=32, level=level,
+    )
+
+
+def pack_prefixes(prefixes: Sequence[str], n_qubits: int) -> np.ndarray:
+    """Bitstrings -> [W, words] u64; qubit q sits at word q//64, bit 63-(q%64)."""
+    words = max(1, (n_qubits + 63) // 64)
+    out = np.zeros((len(prefixes), words), dtype=np.uint64)
+    for r, s in enumerate(prefixes):
+        for q, ch in enumerate(s):
+            if ch == "1":
+                out[r, q >> 6] |= np.uint64(1) << np.uint64(63 - (q & 63))
+            elif ch != "0":
+                raise ValueError(f"prefix {s!r} is not a bitstring")
+    return out
+
+
+def unpack_keys(keys: np.ndarray, n_qubits: int) -> list:
+    """[R, words] u64 -> list of n-character bitstrings (qubit 0 leftmost)."""
+    if keys.shape[0] == 0:
+        return []
+    be = np.ascontiguousarray(keys.astype(">u8"))
+    bits = np.unpackbits(be.view(np.uint8).reshape(keys.shape[0], -1), axis=1)[:, :n_qubits]
+    chars = (bits + ord("0")).astype(np.uint8)
+    return [row.tobytes().decode("ascii") for row in chars]
+
+
+def conditional_marginals_batched(
+    template: CircuitNetwork,
+    errorsets: Sequence[ErrorSet],
+    plan: BatchPlan,
+    j: int,
+    prefixes: Sequence[str],
+    ctx: Optional[SamplerContext] = None,
+    *,
+    normalize: bool = True,
+    return_mass: bool = False,
+):
+    """Conditional distributions of stage j for W work items
+    (error set w, prefix w) in one batched device call.  Row w equals the
+    reference's `conditional_marginal(template.merged(errorsets[w]), ...,
+    j, prefixes[w])` (engine.py:453-477) up to the dtype's tolerance."""
+    if ctx is None:
+        ctx = SamplerContext()
+    if len(errorsets) != len(prefixes):
+        raise ValueError("one prefix per error set expected")
+    if not 1 <= j <= plan.f:
+        raise ValueError(f"stage {j} outside 1..{plan.f}")
+    for s in prefixes:
+        if len(s) != plan.offset(j):
+            raise ValueError(f"stage {j} expects a {plan.offset(j)}-bit prefix, got {len(s)}")
+    ctx.check_deadline()
+    tables = VariantTables.from_errorsets(template, errorsets)
+    pipe = DevicePipeline(template, plan, tables, ctx, stages=[j])
+    try:
+        probs, mass, mn = pipe.device_plan.marginals(j, tables.encode(errorsets), pack_prefixes(prefixes, plan.n))
+    finally:
+        pipe.close()
+    ctx.stats.record_contraction(j, 0.0, events=len(prefixes))
+    _guard(mn, mass, ctx.dtype, [f"error set {k.id}: " for k in errorsets], prefixes, check_mass=normalize)
+    if normalize:
+        probs = probs / mass[:, None]
+    return (probs, mass) if return_mass else probs
+
+
+def _guard(mn, mass, dtype, who, prefixes, check_mass=True):
+    """Numerical guards of engine.py:445-450 and 475-476.  complex64 cannot
+    resolve -1e-12, so its negative tolerance scales with the mass."""
+    rel = 1e-4 if dtype == "complex64" else 0.0
+    for w in range(len(mass)):
+        if mn[w] < NEGATIVE_DIAG_TOLERANCE - rel * mass[w]:
+            raise NumericalError(f"{who[w]}marginal diagonal entry {mn[w]} below {NEGATIVE_DIAG_TOLERANCE}")
+        if check_mass and mass[w] < VANISHING_MASS:
+            raise ImpossiblePrefixError(f"{who[w]}prefix {prefixes[w]!r} has vanishing mass {mass[w]}")
+
+
+def _contract_marginal(mnet: MarginalNetwork, ctx: SamplerContext, j: int, path=None):
+    """(clamped unnormalised population vector, mass) of one stage network on
+    the device (engine.py:417-450)."""
+    from . import _capi
+
+    ctx.check_deadline()
+    net = mnet.net
+    if path is None:
+        t0 = time.perf_counter()
+        path, hit = cache_lookup_or_plan(ctx.cache, net, stage=j, hypersamples=ctx.hypersamples,
+                                         rng=spawn_rng(ctx.planner_seed, _KEY_PLANNER, j))
+        if not hit:
+            ctx.stats.plan_events += 1
+            ctx.stats.path_seconds += time.perf_counter() - t0
+    ops = [Operand(t.labels, tuple(ix.dim for ix in t.indices), t.data.reshape(1, -1)) for t in net.operands]
+    pool = Pool()
+    steps = getattr(path, "steps", path)
+    progs, _ = compiler.compile_stage(ops, steps, mnet.open_labels, 1, pool, 16 if ctx.dtype != "complex64" else 8,
+                                      ceiling=ctx.max_intermediate)
+    out_elems = progs[0].out_elems
+    nbits = out_elems.bit_length() - 1
+    if nbits < 1 or (1 << nbits) != out_elems:
+        raise NetworkStructureError("a marginal network must leave 2^b (b >= 1) open entries")
+    compiled = CompiledPlan(dtype=ctx.dtype, n_qubits=nbits, n_sites=0, sizes=(nbits,), pool=pool.finish(ctx.dtype),
+                            programs=progs, max_intermediate=ctx.max_intermediate)
+    dp = _capi.DevicePlan(compiled, ctx.device)
+    t0 = time.perf_counter()
+    try:
+        probs, mass, mn = dp.marginals(1, np.zeros((1, 0), np.uint8), np.zeros((1, dp.words), np.uint64))
+    finally:
+        dp.close()
+    ctx.stats.record_contraction(j, time.perf_counter() - t0)
+    _guard(mn, mass, ctx.dtype, [""], [""], check_mass=False)
+    return probs[0], float(mass[0])
+
+
+def conditional_marginal(cnet: CircuitNetwork, cache: PathCache, plan: BatchPlan, j: int, prefix: str, *,
+                         hypersamples: int = 100, planner_seed: int = 0, stats: Optional[EngineStats] = None,
+                         max_intermediate: int = DEFAULT_INTERMEDIATE_CEILING, dtype: str = "complex128") -> np.ndarray:
+    """Normalised conditional distribution over the 2^{b_j} outcomes of stage j
+    given `prefix` (engine.py:453-477), one work item on the device."""
+    ctx = SamplerContext(cache=cache, stats=stats if stats is not None else EngineStats(),
+                         hypersamples=hypersamples, planner_seed=planner_seed,
+                         max_intermediate=max_intermediate, dtype=dtype)
+    probs, mass = _contract_marginal(marginal_network(cnet, plan, j, prefix), ctx, j)
+    if mass < VANISHING_MASS:
+        raise ImpossiblePrefixError(f"prefix {prefix!r} has vanishing mass {mass}")
+    return probs / mass
+
+
+def _bits(idx: int, width: int) -> str:
+    return format(idx, f"0{width}b")
+
+
+def _raise_flagged(stats, errorsets_by_id=None):
+    if not stats.flagged_sets:
+        return
+    exc = STATUS_TO_ERROR.get(int(stats.first_flag_kind), SimulationError)
+    what = ("marginal diagonal entry below tolerance" if exc is NumericalError
+            else "prefix has vanishing mass")
+    raise exc(f"error set {int(stats.first_flagged_id)}: stage {int(stats.first_flag_stage)}: {what} "
+              f"({int(stats.flagged_sets)} work item(s) flagged)")
+
+
+def sample_proportional_batched(
+    template: CircuitNetwork,
+    errorsets: Sequence[ErrorSet],
+    plan: BatchPlan,
+    seed: int,
+    ctx: Optional[SamplerContext] = None,
+) -> list:
+    """Born-rule sampling of every error set's shots in one batched device run.
+    Returns one sorted `list[ShotRecord]` per error set -- what the reference's
+    `sample_proportional` (engine.py:493-524) returns for each of them.  The
+    RNG stream of a work item is Philox(seed; error-set id, stage, prefix rank),
+    so results do not depend on how error sets are grouped into calls."""
+    if ctx is None:
+        ctx = SamplerContext()
+    for k in errorsets:
+        if k.m < 1:
+            raise ValueError("proportional sampling needs m >= 1")
+    ctx.check_deadline()
+    tables = VariantTables.from_errorsets(template, errorsets)
+    shots = np.asarray([k.m for k in errorsets], dtype=np.uint32)
+    pipe = DevicePipeline(template, plan, tables, ctx, shots_per_set=float(shots.mean()))
+    try:
+        keys, esets, counts, st = pipe.device_plan.sample(
+            tables.encode(errorsets), shots, np.asarray([k.id for k in errorsets], dtype=np.uint32),
+            seed, merged=False)
+    finally:
+        pipe.close()
+    _account(ctx.stats, st, plan.f)
+    _raise_flagged(st)
+    strings = unpack_keys(keys, plan.n)
+    out = [[] for _ in errorsets]
+    for s, e, c in zip(strings, esets.tolist(), counts.tolist()):
+        out[e].append(ShotRecord(bitstring=s, count=int(c)))
+    return out
+
+
+def _account(stats: EngineStats, st, f: int) -> None:
+    for j in range(1, f + 1):
+        stats.record_contraction(j, st.stage_ms[j - 1] * 1e-3, events=int(st.stage_events[j - 1]))
+
+
+def sample_proportional(template: CircuitNetwork, k: ErrorSet, plan: BatchPlan, rng,
+                        ctx: Optional[SamplerContext] = None) -> list:
+    """Single-error-set form of the reference signature (engine.py:493-499).
+    `rng` only seeds the device's counter-based streams (one 63-bit draw); a
+    NumPy generator cannot be replayed on the device."""
+    if k.m < 1:
+        raise ValueError("proportional sampling needs m >= 1")
+    seed = int(rng.integers(0, 2**63 - 1)) if hasattr(rng, "integers") else int(rng)
+    return sample_proportional_batched(template, [k], plan, seed, ctx)[0]
+
+
+def merge_records(per_set: Sequence[Sequence[ShotRecord]]) -> list:
+    """Counts summed per bitstring on the device (sort + reduce-by-key); the
+    `prob` tag survives only if all contributors agree (engine.py:815-829)."""
+    from . import _capi
+
+    rows = [r for recs in per_set for r in recs]
+    if not rows:
+        return []
+    width = len(rows[0].bitstring)
+    keys, counts = _capi.histogram_merge(pack_prefixes([r.bitstring for r in rows], width),
+                                         np.asarray([r.count for r in rows], dtype=np.uint64))
+    tags: dict = {}
+    for r in rows:
+        if r.bitstring not in tags:
+            tags[r.bitstring] = r.prob
+        elif tags[r.bitstring] != r.prob:
+            tags[r.bitstring] = None
+    return [ShotRecord(bitstring=s, count=int(c), prob=tags[s])
+            for s, c in zip(unpack_keys(keys, width), counts.tolist())]
+
+
+MODES = ("ptsbe-proportional", "ptsbe-nonproportional", "unoptimized-ptsbe", "baseline")
+
+
+@dataclass
+class RunConfig:
+    """Run description, echoed into results (engine.py:667-747).  `dtype` and
+    `device` are the only additions; defaults keep reference numerics."""
+
+    n: int
+    g: int
+    mode: str = "ptsbe-proportional"
+    two_qubit_fraction: float = 0.2
+    p_range: tuple = (0.02, 0.2)
+    error_sets: int = 4
+    total_shots: int = 64
+    batch_sizes: Optional[tuple] = None
+    nonfinal_batch: int = 10
+    final_batch: int = 28
+    nonfinal_shots: int = 1
+    final_mode: str = "exhaustive"
+    tau: float = 1e-6
+    direct_count: int = 1
+    hypersamples: int = 100
+    baseline_batch: int = 24
+    baseline_hypersamples: int = 1
+    seed: int = 0
+    workers: int = 1
+    max_intermediate: int = DEFAULT_INTERMEDIATE_CEILING
+    timeout_s: Optional[float] = 120.0
+    dtype: str = "complex128"
+    device: int = 0
+
+    def __post_init__(self):
+        if self.mode not in MODES:
+            raise ValueError(f"mode must be one of {MODES}, got {self.mode!r}")
+        if self.dtype not in ("complex64", "complex128"):
+            raise ValueError(f"dtype must be complex64 or complex128, got {self.dtype!r}")
+        if self.batch_sizes is not None:
+            self.batch_sizes = tuple(int(b) for b in self.batch_sizes)
+            if sum(self.batch_sizes) != self.n:
+                raise ValueError(f"batch sizes {self.batch_sizes} must sum to n={self.n}")
+
+    def plan(self) -> BatchPlan:
+        kw = dict(nonfinal_shots=self.nonfinal_shots, final_mode=self.final_mode,
+                  direct_count=self.direct_count, threshold=self.tau)
+        if self.batch_sizes is not None:
+            return BatchPlan(sizes=self.batch_sizes, **kw)
+        return BatchPlan.with_final(self.n, self.nonfinal_batch, self.final_batch, **kw)
+
+    def to_dict(self) -> dict:
+        doc = {k: getattr(self, k) for k in (
+            "n", "g", "mode", "two_qubit_fraction", "p_range", "error_sets", "total_shots",
+            "batch_sizes", "nonfinal_batch", "final_batch", "nonfinal_shots", "final_mode", "tau",
+            "direct_count", "hypersamples", "baseline_batch", "baseline_hypersamples", "seed",
+            "workers", "max_intermediate", "timeout_s", "dtype", "device")}
+        doc["p_range"] = list(self.p_range)
+        doc["batch_sizes"] = list(self.batch_sizes) if self.batch_sizes else None
+        return doc
+
+    @classmethod
+    def from_dict(cls, doc: dict) -> "RunConfig":
+        doc = dict(doc)
+        for key in ("p_range", "batch_sizes"):
+            if doc.get(key) is not None:
+                doc[key] = tuple(doc[key])
+        return cls(**doc)
+
+
+@dataclass
+class RunResult:
+    """Aggregated records + instrumentation (engine.py:750-812)."""
+
+    mode: str
+    records: list
+    unique_shots: int
+    total_count: int
+    timings: dict
+    plan_events: int
+    contract_events: int
+    stage_events: dict
+    stage_seconds: dict
+    config: dict
+    seed: int
+    shot_allocations: list
+
+    @property
+    def loop_seconds(self) -> float:
+        return self.timings["loop_s"]
+
+    def to_json(self) -> str:
+        return json.dumps({
+            "mode": self.mode,
+            "records": [{"bitstring": r.bitstring, "count": r.count, "prob": r.prob} for r in self.records],
+            "unique_shots": self.unique_shots,
+            "total_count": self.total_count,
+            "timings": self.timings,
+            "plan_events": self.plan_events,
+            "contract_events": self.contract_events,
+            "stage_events": {str(k): v for k, v in self.stage_events.items()},
+            "stage_seconds": {str(k): v for k, v in self.stage_seconds.items()},
+            "config": self.config,
+            "seed": self.seed,
+            "shot_allocations": self.shot_allocations,
+        })
+
+    @classmethod
+    def from_json(cls, text: str) -> "RunResult":
+        doc = json.loads(text)
+        return cls(
+            mode=doc["mode"],
+            records=[ShotRecord(r["bitstring"], r["count"], r.get("prob")) for r in doc["records"]],
+            unique_shots=doc["unique_shots"], total_count=doc["total_count"], timings=doc["timings"],
+            plan_events=doc["plan_events"], contract_events=doc["contract_events"],
+            stage_events={int(k): v for k, v in doc["stage_events"].items()},
+            stage_seconds={int(k): v for k, v in doc["stage_seconds"].items()},
+            config=doc["config"], seed=doc["seed"], shot_allocations=doc["shot_allocations"],
+        )
+
+
+def run_ptsbe(c: Circuit, config: RunConfig, cache: Optional[PathCache] = None,
+              errorsets: Optional[Sequence[ErrorSet]] = None) -> RunResult:
+    """Optimised proportional pipeline on the device (engine.py:832-929):
+    pre-sample error sets on the host (same rng stream as the reference), plan
+    one path per stage on the error-free template (plan events = f, or 0 with a
+    warm cache), then ONE batched device run over all error sets, histogram
+    merged on the device.  `errorsets` overrides the pre-sampling (the
+    north-star API: pre-sampled error sets in, histogram out)."""
+    if config.mode == "ptsbe-nonproportional":
+        raise NotImplementedError("non-proportional sampling is out of scope of the B200 path (SURVEY.md 8f)")
+    if config.mode != "ptsbe-proportional":
+        raise ValueError(f"run_ptsbe handles optimized modes only, got {config.mode!r}")
+    plan = config.plan()
+    if plan.n != c.n:
+        raise ValueError(f"plan covers {plan.n} qubits, circuit has {c.n}")
+    ctx = SamplerContext(
+        cache=cache if cache is not None else PathCache(), hypersamples=config.hypersamples,
+        planner_seed=config.seed, max_intermediate=config.max_intermediate,
+        deadline=(time.perf_counter() + config.timeout_s) if config.timeout_s else None,
+        dtype=config.dtype, device=config.device,
+    )
+    t0 = time.perf_counter()
+    template = CircuitNetwork.from_circuit(c)
+    if errorsets is None:
+        errorsets = presample_errors(c, config.error_sets, rule="proportional",
+                                     total_shots=config.total_shots,
+                                     rng=spawn_rng(config.seed, _KEY_PRESAMPLE))
+    generate_s = time.perf_counter() - t0
+
+    t0 = time.perf_counter()
+    tables = VariantTables.from_errorsets(template, errorsets)
+    shots = np.asarray([k.m for k in errorsets], dtype=np.uint32)
+    if shots.min() < 1:
+        raise ValueError("proportional sampling needs m >= 1")
+    pipe = DevicePipeline(template, plan, tables, ctx, shots_per_set=float(shots.mean()))
+    plan_s = time.perf_counter() - t0
+    try:
+        ctx.check_deadline()
+        kraus_idx = tables.encode(errorsets)
+        ids = np.asarray([k.id for k in errorsets], dtype=np.uint32)
+        t0 = time.perf_counter()
+        keys, _, counts, st = pipe.device_plan.sample(kraus_idx, shots, ids, config.seed, merged=True)
+        loop_s = time.perf_counter() - t0
+    finally:
+        pipe.close()
+    _account(ctx.stats, st, plan.f)
+    _raise_flagged(st)
+    t0 = time.perf_counter()
+    records = [ShotRecord(bitstring=s, count=int(n)) for s, n in zip(unpack_keys(keys, plan.n), counts.tolist())]
+    aggregate_s = time.perf_counter() - t0
+    return RunResult(
+        mode=config.mode, records=records, unique_shots=len(records),
+        total_count=sum(r.count for r in records),
+        timings={
+            "generate_s": generate_s, "plan_s": plan_s, "loop_s": loop_s, "aggregate_s": aggregate_s,
+            "path_s": ctx.stats.path_seconds, "contract_s": ctx.stats.contract_seconds,
+            "device_loop_s": st.loop_ms * 1e-3, "h2d_s": st.h2d_ms * 1e-3, "d2h_s": st.d2h_ms * 1e-3,
+            "gpu_launches": int(st.gpu_launches),
+        },
+        plan_events=ctx.stats.plan_events, contract_events=ctx.stats.contract_events,
+        stage_events=dict(sorted(ctx.stats.stage_events.items())),
+        stage_seconds=dict(sorted(ctx.stats.stage_seconds.items())),
+        config=config.to_dict(), seed=config.seed, shot_allocations=[int(k.m) for k in errorsets],
+    )
+
+
+def run_mode(c: Circuit, config: RunConfig, cache: Optional[PathCache] = None) -> RunResult:
+    """Dispatch by mode (engine.py:932-941).  Only the proportional PTSBE mode
+    runs on the device; the comparison modes stay with the CPU reference."""
+    if config.mode == "ptsbe-proportional":
+        return run_ptsbe(c, config, cache=cache)
+    raise NotImplementedError(
+        f"mode {config.mode!r} is a CPU comparison mode of the reference and is out of scope here"
+    )
+
+
+def _out_of_scope(name: str):
+    def stub(*_a, **_k):
+        raise NotImplementedError(f"{name} is outside the B200 hot path (SURVEY.md sections 2, 8f); "
+                                  "use the CPU reference for it")
+    stub.__name__ = name
+    return stub
+
+
+insert_errors = _out_of_scope("insert_errors")
+sample_nonproportional = _out_of_scope("sample_nonproportional")
+sample_baseline = _out_of_scope("sample_baseline")
+sample_unoptimized_ptsbe = _out_of_scope("sample_unoptimized_ptsbe")

@@ -1,0 +1,278 @@
+"""Path planner front end and the signature-keyed path cache.
+
+Public surface of the reference planner (planner.py:34-442): `ContractionPath`
+(JSON wire-compatible), `path_cost`, `find_path_greedy`, `find_path_optimal`,
+`PathCache` (same JSON persistence format, planner.py:372-413) and
+`cache_lookup_or_plan`.  The search itself runs in native code
+(`csrc/planner.cpp`, entry point `ptsbe_plan_greedy`); it is seeded
+deterministically from the caller's `rng` but does not reproduce the
+reference's descent order -- paths are interchangeable (same step convention,
+validated by structural replay), not identical.
+
+Batch-aware extension: `op_class` / `class_weight` make the search minimise
+sum(step flops x number of distinct instances of the step's result in the
+batch) instead of plain flops, which is what the hoisting executor pays.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import threading
+from dataclasses import dataclass
+from typing import Hashable, Optional, Sequence
+
+import numpy as np
+
+from .errors import CapacityError, NetworkStructureError, PathCacheError
+from .tensor import NetworkSignature, TensorNetwork, network_signature, replay_shapes
+
+
+@dataclass(frozen=True)
+class ContractionPath:
+    """Slot-pair schedule: step (i, j), i < j, contracts slots i and j into
+    slot i and deletes slot j (planner.py:34-54)."""
+
+    steps: tuple
+    est_cost: float
+
+    def to_json(self) -> str:
+        return json.dumps({"steps": [list(s) for s in self.steps], "est_cost": self.est_cost})
+
+    @classmethod
+    def from_json(cls, text: str) -> "ContractionPath":
+        doc = json.loads(text)
+        return cls(tuple((int(i), int(j)) for i, j in doc["steps"]), float(doc["est_cost"]))
+
+
+def path_cost(net: TensorNetwork, path) -> float:
+    """Sum over steps of prod(dims of the union of both operands' labels)
+    (planner.py:61-103)."""
+    from .errors import IncompletePathError
+
+    steps = getattr(path, "steps", path)
+    cost, _, slots = replay_shapes(net, steps)
+    if len(slots) != 1:
+        raise IncompletePathError(f"path left {len(slots)} operands, expected 1")
+    if set(slots[0]) != set(net.open_indices):
+        raise NetworkStructureError("replayed path does not produce the open indices")
+    return cost
+
+
+def merges_to_steps(n: int, merges) -> tuple:
+    """Stable-id merges (result keeps the smaller id) -> slot steps under the
+    replace-lower / shift-down convention (planner.py:106-118).  Uses a Fenwick
+    tree so 1000-operand paths convert in O(n log n)."""
+    tree = [0] * (n + 1)
+
+    def add(i, v):
+        i += 1
+        while i <= n:
+            tree[i] += v
+            i += i & -i
+
+    def before(i):  # number of alive ids < i
+        s = 0
+        while i > 0:
+            s += tree[i]
+            i -= i & -i
+        return s
+
+    for k in range(n):
+        add(k, 1)
+    out = []
+    for x, y in merges:
+        x, y = int(x), int(y)
+        if x > y:
+            x, y = y, x
+        out.append((before(x), before(y)))
+        add(y, -1)
+    return tuple(out)
+
+
+def find_path_greedy(
+    net: TensorNetwork,
+    hypersamples: int = 100,
+    rng: Optional[np.random.Generator] = None,
+    *,
+    op_class: Optional[Sequence[int]] = None,
+    class_weight: Optional[Sequence[float]] = None,
+    size_cap_log2: float = 0.0,
+) -> ContractionPath:
+    """Best of `hypersamples` randomized greedy descents (planner.py:212-251).
+    `est_cost` is the reference flop estimate of the chosen path."""
+    from . import _capi
+
+    if hypersamples < 1:
+        raise ValueError("hypersamples must be >= 1")
+    n = len(net.operands)
+    if n == 0:
+        raise NetworkStructureError("network has no operands")
+    if n == 1:
+        return ContractionPath(steps=(), est_cost=0.0)
+    if rng is None:
+        rng = np.random.default_rng()
+    seed = int(rng.integers(0, 2**63 - 1))
+    merges, _, flops = _capi.plan_greedy(
+        [t.labels for t in net.operands],
+        [[ix.dim for ix in t.indices] for t in net.operands],
+        op_class=op_class,
+        class_weight=class_weight,
+        hypersamples=hypersamples,
+        seed=seed,
+        size_cap_log2=size_cap_log2,
+    )
+    return ContractionPath(steps=merges_to_steps(n, merges), est_cost=float(flops))
+
+
+MAX_OPTIMAL_OPERANDS = 14
+
+
+def find_path_optimal(net: TensorNetwork) -> ContractionPath:
+    """Minimum-flop path by DP over operand subsets, <= 14 operands
+    (planner.py:257-340).  Verification oracle only; host code."""
+    n = len(net.operands)
+    if n == 0:
+        raise NetworkStructureError("network has no operands")
+    if n > MAX_OPTIMAL_OPERANDS:
+        raise CapacityError(f"optimal planner capped at {MAX_OPTIMAL_OPERANDS} operands, got {n}")
+    if n == 1:
+        return ContractionPath(steps=(), est_cost=0.0)
+    # label -> (dim, occupancy mask)
+    occ: dict[int, int] = {}
+    dim: dict[int, int] = {}
+    for k, t in enumerate(net.operands):
+        for ix in t.indices:
+            occ[ix.label] = occ.get(ix.label, 0) | (1 << k)
+            dim[ix.label] = ix.dim
+    labels = list(occ)
+    full = (1 << n) - 1
+
+    def union_size(m1: int, m2: int) -> float:
+        s = 1.0
+        for lb in labels:
+            i1, i2 = occ[lb] & m1, occ[lb] & m2
+            if (i1 and i1 & (i1 - 1) == 0) or (i2 and i2 & (i2 - 1) == 0):
+                s *= dim[lb]
+        return s
+
+    best = {1 << k: (0.0, None) for k in range(n)}
+    by_pop = sorted(range(1, full + 1), key=lambda m: bin(m).count("1"))
+    for mask in by_pop:
+        if mask & (mask - 1) == 0:
+            continue
+        low = mask & -mask
+        top_cost, top_split = math.inf, None
+        sub = (mask - 1) & mask
+        while sub:
+            if sub & low:
+                rest = mask ^ sub
+                c = best[sub][0] + best[rest][0] + union_size(sub, rest)
+                if c < top_cost:
+                    top_cost, top_split = c, (sub, rest)
+            sub = (sub - 1) & mask
+        best[mask] = (top_cost, top_split)
+    merges = []
+
+    def emit(mask: int) -> int:
+        if mask & (mask - 1) == 0:
+            return mask.bit_length() - 1
+        s1, s2 = best[mask][1]
+        a, b = emit(s1), emit(s2)
+        merges.append((min(a, b), max(a, b)))
+        return min(a, b)
+
+    emit(full)
+    return ContractionPath(steps=merges_to_steps(n, merges), est_cost=best[full][0])
+
+
+class PathCache:
+    """(NetworkSignature, stage descriptor) -> ContractionPath.  Readers are
+    lock-free, writers take a lock, planning the same key twice is idempotent
+    (planner.py:343-413).  The JSON format is the reference's, so a cache file
+    written by either package warms the other."""
+
+    def __init__(self):
+        self._store: dict = {}
+        self._lock = threading.Lock()
+        self.hits = 0
+        self.misses = 0
+
+    def __len__(self):
+        return len(self._store)
+
+    def get(self, sig: NetworkSignature, stage: Hashable):
+        return self._store.get((sig, stage))
+
+    def put(self, sig: NetworkSignature, stage: Hashable, path: ContractionPath) -> None:
+        with self._lock:
+            self._store[(sig, stage)] = path
+
+    def clear(self) -> None:
+        with self._lock:
+            self._store.clear()
+            self.hits = self.misses = 0
+
+    def save(self, fp) -> None:
+        rows = []
+        for (sig, stage), path in self._store.items():
+            rows.append(
+                {
+                    "signature": {
+                        "num_operands": sig.num_operands,
+                        "shapes": [list(s) for s in sig.shapes],
+                        "bonds": [[list(p) for p in b] for b in sig.bonds],
+                        "open_legs": [list(o) for o in sig.open_legs],
+                    },
+                    "stage": stage,
+                    "steps": [list(s) for s in path.steps],
+                    "est_cost": path.est_cost,
+                }
+            )
+        json.dump({"entries": rows}, fp)
+
+    @classmethod
+    def load(cls, fp) -> "PathCache":
+        cache = cls()
+        for row in json.load(fp)["entries"]:
+            s = row["signature"]
+            sig = NetworkSignature(
+                num_operands=int(s["num_operands"]),
+                shapes=tuple(tuple(int(d) for d in shape) for shape in s["shapes"]),
+                bonds=tuple(tuple(tuple(int(v) for v in p) for p in b) for b in s["bonds"]),
+                open_legs=tuple(tuple(int(v) for v in o) for o in s["open_legs"]),
+            )
+            stage = row["stage"]
+            if isinstance(stage, list):
+                stage = tuple(stage)
+            cache.put(
+                sig,
+                stage,
+                ContractionPath(tuple((int(i), int(j)) for i, j in row["steps"]), float(row["est_cost"])),
+            )
+        return cache
+
+
+def cache_lookup_or_plan(
+    cache: PathCache,
+    net: TensorNetwork,
+    stage: Hashable,
+    hypersamples: int = 100,
+    rng: Optional[np.random.Generator] = None,
+    **plan_kw,
+) -> tuple:
+    """(path, hit).  A hit is validated by structural replay; a stored path
+    that does not replay means the cache is corrupt (planner.py:416-442)."""
+    sig = network_signature(net)
+    path = cache.get(sig, stage)
+    if path is not None:
+        try:
+            path_cost(net, path)
+        except NetworkStructureError as exc:
+            raise PathCacheError(f"cached path for stage {stage!r} does not replay: {exc}") from exc
+        cache.hits += 1
+        return path, True
+    path = find_path_greedy(net, hypersamples=hypersamples, rng=rng, **plan_kw)
+    cache.put(sig, stage, path)
+    cache.misses += 1
+    return path, False
