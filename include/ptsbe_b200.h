@@ -190,6 +190,22 @@ int ptsbe_plan_greedy(uint32_t n_ops, const uint32_t* op_ptr, const int64_t* lab
                       uint64_t seed, double size_cap_log2, uint32_t* merges_out,
                       double* cost_out, double* flops_out);
 
+/* ---- device-pointer variants for the multi-GPU gather (one process per GPU;
+ * the caller moves the buffers with NCCL and must synchronise its own stream
+ * before handing pointers to the library) ---------------------------------- */
+
+/* histogram of the last ptsbe_batch_run, left in HBM: keys_dev [n][words] u64,
+ * counts_dev [n] u64.  Valid until the next run or ptsbe_batch_destroy. */
+int ptsbe_batch_histogram_dev(ptsbe_batch* batch, const uint64_t** keys_dev,
+                              const uint64_t** counts_dev, uint64_t* n_records);
+
+/* ptsbe_histogram_merge on device buffers (merge_records after the NCCL gather,
+ * engine.py:815-829).  Outputs are device buffers released with ptsbe_free_dev. */
+int ptsbe_histogram_merge_dev(const uint64_t* keys_dev, const uint64_t* counts_dev, uint64_t n,
+                              uint32_t words, int device, uint64_t** out_keys_dev,
+                              uint64_t** out_counts_dev, uint64_t* n_out);
+void ptsbe_free_dev(void* p_dev);
+
 void ptsbe_free(void* p);
 
 #ifdef __cplusplus

@@ -27,6 +27,7 @@ EXPORTS = (
     "ptsbe_plan_destroy", "ptsbe_marginals", "ptsbe_execute_raw", "ptsbe_sample_stage",
     "ptsbe_sample", "ptsbe_batch_upload", "ptsbe_batch_run", "ptsbe_batch_fetch",
     "ptsbe_batch_destroy", "ptsbe_histogram_merge", "ptsbe_plan_greedy", "ptsbe_free",
+    "ptsbe_batch_histogram_dev", "ptsbe_histogram_merge_dev", "ptsbe_free_dev",
 )
 
 
@@ -92,6 +93,11 @@ def load() -> ctypes.CDLL:
                                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
     lib.ptsbe_free.argtypes = [P]
     lib.ptsbe_free.restype = None
+    lib.ptsbe_batch_histogram_dev.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(U64)]
+    lib.ptsbe_histogram_merge_dev.argtypes = [P, P, U64, U32, I, ctypes.POINTER(P), ctypes.POINTER(P),
+                                              ctypes.POINTER(U64)]
+    lib.ptsbe_free_dev.argtypes = [P]
+    lib.ptsbe_free_dev.restype = None
     _lib = lib
     return lib
 
@@ -123,6 +129,30 @@ def _ptr(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes.data
 
 
+class DeviceArray:
+    """A u64 device buffer owned by the library (or borrowed from a batch),
+    exported through `__cuda_array_interface__` so torch can wrap it without a
+    copy: `torch.as_tensor(arr, device="cuda")`."""
+
+    def __init__(self, ptr: int, shape: tuple, owner=None, owned: bool = False):
+        self.ptr, self.shape, self._owner, self._owned = int(ptr or 0), tuple(shape), owner, owned
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": self.shape, "typestr": "<u8", "data": (self.ptr, False), "version": 2}
+
+    def free(self):
+        if self._owned and self.ptr:
+            load().ptsbe_free_dev(self.ptr)
+        self.ptr, self._owned = 0, False
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 class ResidentBatch:
     """Error sets uploaded once; each `run` leaves its histogram in HBM."""
 
@@ -146,6 +176,14 @@ class ResidentBatch:
         check(load().ptsbe_batch_fetch(self._h, ctypes.byref(k), ctypes.byref(c), ctypes.byref(n)))
         w = self.plan.words
         return _take(k, n.value * w, np.uint64).reshape(-1, w), _take(c, n.value, np.uint64)
+
+    def histogram_dev(self) -> tuple["DeviceArray", "DeviceArray"]:
+        """Histogram of the last run as borrowed device buffers (keys [R, words],
+        counts [R]); valid until the next run or close()."""
+        k, c, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
+        check(load().ptsbe_batch_histogram_dev(self._h, ctypes.byref(k), ctypes.byref(c), ctypes.byref(n)))
+        return (DeviceArray(k.value, (n.value, self.plan.words), owner=self),
+                DeviceArray(c.value, (n.value,), owner=self))
 
     def close(self):
         if self._h:
@@ -256,6 +294,14 @@ def histogram_merge(keys, counts, device: int = 0):
                                        ctypes.byref(ok), ctypes.byref(oc), ctypes.byref(n), device))
     w = keys.shape[1]
     return _take(ok, n.value * w, np.uint64).reshape(-1, w), _take(oc, n.value, np.uint64)
+
+
+def histogram_merge_dev(keys_ptr: int, counts_ptr: int, n: int, words: int, device: int = 0):
+    """Device-pointer form of `histogram_merge`: returns owned DeviceArrays."""
+    ok, oc, m = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
+    check(load().ptsbe_histogram_merge_dev(keys_ptr, counts_ptr, n, words, device, ctypes.byref(ok),
+                                           ctypes.byref(oc), ctypes.byref(m)))
+    return (DeviceArray(ok.value, (m.value, words), owned=True), DeviceArray(oc.value, (m.value,), owned=True))
 
 
 def plan_greedy(op_labels, op_dims, op_class=None, class_weight=None, hypersamples=100,

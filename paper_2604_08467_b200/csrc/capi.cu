@@ -899,6 +899,57 @@ int ptsbe_sample(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t* shots
   return rc;
 }
 
+int ptsbe_batch_histogram_dev(ptsbe_batch* bt, const uint64_t** keys_dev,
+                              const uint64_t** counts_dev, uint64_t* n_records) {
+  return guarded([&] {
+    if (!bt || !keys_dev || !counts_dev || !n_records) throw Failure(PTSBE_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lock(bt->plan->mu);
+    *keys_dev = bt->merged.keys.as<uint64_t>();
+    *counts_dev = bt->merged.counts.as<uint64_t>();
+    *n_records = bt->merged.n;
+  });
+}
+
+int ptsbe_histogram_merge_dev(const uint64_t* keys_dev, const uint64_t* counts_dev, uint64_t n,
+                              uint32_t words, int device, uint64_t** out_keys_dev,
+                              uint64_t** out_counts_dev, uint64_t* n_out) {
+  return guarded([&] {
+    if (ptsbe_device_count() <= device)
+      throw Failure(PTSBE_EDEVICE, "no CUDA device: libptsbe_b200 has no CPU fallback");
+    if (words < 1) throw Failure(PTSBE_EINVAL, "words must be >= 1");
+    CK(cudaSetDevice(device));
+    g_launches = 0;
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    {
+      const uint64_t m = std::max<uint64_t>(n, 1);
+      DevBuf soa;
+      const uint64_t* kin = keys_dev;
+      if (words > 1 && n) {  // row-major [n][words] -> SoA [words][n]
+        soa.alloc(m * 8 * words, st);
+        transpose_keys_kernel<<<cdiv(n * words, 256), 256, 0, st>>>(keys_dev, soa.as<uint64_t>(), n, words);
+        g_launches++;
+        kin = soa.as<uint64_t>();
+      }
+      Histogram h;
+      reduce_by_key(kin, n, words, nullptr, counts_dev, n, 64 * words, h, st);
+      CK(cudaStreamSynchronize(st));
+      *n_out = h.n;
+      // hand the buffers over: detach them from their RAII owners
+      *out_keys_dev = h.keys.as<uint64_t>();
+      *out_counts_dev = h.counts.as<uint64_t>();
+      h.keys.p = nullptr;
+      h.counts.p = nullptr;
+    }
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  });
+}
+
+void ptsbe_free_dev(void* p) {
+  if (p) cudaFree(p);
+}
+
 int ptsbe_histogram_merge(const uint64_t* keys, const uint64_t* counts, uint64_t n,
                           uint32_t words, uint64_t** out_keys, uint64_t** out_counts,
                           uint64_t* n_out, int device) {

@@ -68,6 +68,14 @@ __global__ void segment_counts_kernel(const uint64_t* seg_begin_scan, uint64_t t
   out_counts[r] = end - seg_begin_scan[r];
 }
 
+// row-major [n][words] -> SoA [words][n]
+__global__ void transpose_keys_kernel(const uint64_t* in, uint64_t* out, uint64_t n, uint32_t words) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * words) return;
+  const uint64_t r = i / words, w = i - r * words;
+  out[w * n + r] = in[i];
+}
+
 struct Histogram {
   DevBuf keys;    // [n][words] row-major
   DevBuf counts;  // [n] u64

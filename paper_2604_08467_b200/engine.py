@@ -468,7 +468,7 @@ class DevicePipeline:
 
     def __init__(self, cnet: CircuitNetwork, plan: BatchPlan, tables: VariantTables,
                  ctx: SamplerContext, stages: Optional[Sequence[int]] = None,
-                 shots_per_set: float = 1.0):
+                 shots_per_set: float = 1.0, upload: bool = True):
         from . import _capi
 
         if plan.n != cnet.n:
@@ -507,10 +507,12 @@ class DevicePipeline:
             dtype=ctx.dtype, n_qubits=plan.n, n_sites=tables.n_sites, sizes=plan.sizes,
             pool=pool.finish(ctx.dtype), programs=programs, max_intermediate=ctx.max_intermediate,
         )
-        self.device_plan = _capi.DevicePlan(self.compiled, ctx.device)
+        # upload=False: compile only (plan inspection; CPU-side tests of the compiler)
+        self.device_plan = _capi.DevicePlan(self.compiled, ctx.device) if upload else None
 
     def close(self):
-        self.device_plan.close()
+        if self.device_plan is not None:
+            self.device_plan.close()
 
     def programs_of(self, j: int):
         base = j * (j - 1) // 2
@@ -817,6 +819,10 @@ class RunResult:
     config: dict
     seed: int
     shot_allocations: list
+    # packed device-format histogram ([R, words] u64 keys, [R] u64 counts); kept only
+    # for the multi-GPU gather (partition.py), never serialised
+    packed_keys: Optional[np.ndarray] = field(default=None, repr=False, compare=False)
+    packed_counts: Optional[np.ndarray] = field(default=None, repr=False, compare=False)
 
     @property
     def loop_seconds(self) -> float:
@@ -853,7 +859,7 @@ class RunResult:
 
 
 def run_ptsbe(c: Circuit, config: RunConfig, cache: Optional[PathCache] = None,
-              errorsets: Optional[Sequence[ErrorSet]] = None) -> RunResult:
+              errorsets: Optional[Sequence[ErrorSet]] = None, _keep_packed: bool = False) -> RunResult:
     """Optimised proportional pipeline on the device (engine.py:832-929):
     pre-sample error sets on the host (same rng stream as the reference), plan
     one path per stage on the error-free template (plan events = f, or 0 with a
@@ -915,6 +921,7 @@ def run_ptsbe(c: Circuit, config: RunConfig, cache: Optional[PathCache] = None,
         stage_events=dict(sorted(ctx.stats.stage_events.items())),
         stage_seconds=dict(sorted(ctx.stats.stage_seconds.items())),
         config=config.to_dict(), seed=config.seed, shot_allocations=[int(k.m) for k in errorsets],
+        packed_keys=keys if _keep_packed else None, packed_counts=counts if _keep_packed else None,
     )
 
 

@@ -1,0 +1,124 @@
+"""Plan compiler vs oracle, on the CPU: the flat device programs (gather
+tables, arena placement, hoist passes, Kraus/prefix selectors, folded output
+permutation) are interpreted by tests/emulator.py and must reproduce the
+golden marginals of the unmodified reference."""
+
+import numpy as np
+import pytest
+
+import emulator
+from conftest import case_objects
+from paper_2604_08467_b200 import compiler
+from paper_2604_08467_b200.engine import (
+    BatchPlan, CircuitNetwork, DevicePipeline, SamplerContext, VariantTables, marginal_network,
+)
+from paper_2604_08467_b200.planner import PathCache, find_path_greedy, path_cost
+from paper_2604_08467_b200.tensor import network_signature
+
+
+def _pipeline(case, dtype="complex128", hypersamples=4):
+    c, sizes, es = case_objects(case)
+    tpl = CircuitNetwork.from_circuit(c)
+    tables = VariantTables.from_errorsets(tpl, es)
+    ctx = SamplerContext(hypersamples=hypersamples, planner_seed=5, dtype=dtype)
+    pipe = DevicePipeline(tpl, BatchPlan(sizes), tables, ctx, shots_per_set=100.0, upload=False)
+    return pipe, tables, es
+
+
+@pytest.mark.parametrize("name", ["ghz12", "ghz6_per_qubit", "random_0", "random_4", "hea8", "qaoa8",
+                                  "surface_d3_r1", "random10x40"])
+def test_compiled_programs_reproduce_golden_marginals(golden_cases, name):
+    case = golden_cases[name]
+    pipe, tables, es = _pipeline(case)
+    idx = tables.encode(es)
+    for row in case["marginals"]:
+        j = row["stage"]
+        bits = [int(ch) for ch in row["prefix"]] + [0] * (pipe.plan.n - len(row["prefix"]))
+        rec = emulator.run_stage(pipe.programs_of(j), pipe.compiled.pool, idx[row["eset"]], bits)
+        probs = np.clip(rec.real, 0, None)
+        assert np.max(np.abs(rec.imag)) < 1e-12
+        np.testing.assert_allclose(probs / probs.sum(), np.asarray(row["probs"]), rtol=0, atol=1e-11)
+
+
+def test_complex64_pool_within_tolerance(golden_cases):
+    case = golden_cases["hea8"]
+    pipe, tables, es = _pipeline(case, dtype="complex64")
+    assert pipe.compiled.pool.dtype == np.complex64
+    idx = tables.encode(es)
+    for row in case["marginals"][:12]:
+        bits = [int(ch) for ch in row["prefix"]] + [0] * (pipe.plan.n - len(row["prefix"]))
+        rec = emulator.run_stage(pipe.programs_of(row["stage"]), pipe.compiled.pool, idx[row["eset"]], bits,
+                                 dtype=np.complex64)
+        probs = np.clip(rec.real, 0, None)
+        want = np.asarray(row["probs"])
+        assert np.max(np.abs(probs / probs.sum() - want)) <= 1e-5 * want.max()
+
+
+def test_hoisting_moves_work_out_of_the_marginal_pass(golden_cases):
+    """Error-independent unified path: in stage j >= 2 part of the tree depends
+    on the error set only (pass 0) and is not recomputed per prefix."""
+    pipe, _, _ = _pipeline(golden_cases["random10x40"], hypersamples=16)
+    for j in range(2, pipe.plan.f + 1):
+        flops = pipe.stage_flops[j]
+        assert len(flops) == j
+        assert flops[0] > 0
+        assert flops[-1] < sum(flops)
+    # one plan event per stage, paths shared by every error set (engine.py:864-879)
+    assert pipe.ctx.stats.plan_events == pipe.plan.f
+
+
+def test_one_stored_path_per_stage_and_cache_reuse(golden_cases):
+    case = golden_cases["ghz12"]
+    c, sizes, es = case_objects(case)
+    tpl = CircuitNetwork.from_circuit(c)
+    tables = VariantTables.from_errorsets(tpl, es)
+    cache = PathCache()
+    ctx = SamplerContext(cache=cache, hypersamples=2)
+    DevicePipeline(tpl, BatchPlan(sizes), tables, ctx, upload=False)
+    assert ctx.stats.plan_events == 3 and len(cache) == 3
+    ctx2 = SamplerContext(cache=cache, hypersamples=2)
+    DevicePipeline(tpl, BatchPlan(sizes), tables, ctx2, upload=False)
+    assert ctx2.stats.plan_events == 0 and cache.hits == 3
+
+
+def test_signature_is_prefix_and_error_independent(golden_cases):
+    c, sizes, es = case_objects(golden_cases["random_4"])
+    tpl = CircuitNetwork.from_circuit(c)
+    plan = BatchPlan(sizes)
+    a = network_signature(marginal_network(tpl, plan, 2, "000").net)
+    b = network_signature(marginal_network(tpl.merged(es[0]), plan, 2, "101").net)
+    assert a == b
+
+
+def test_planner_path_is_valid_and_cost_matches(golden_cases):
+    c, sizes, _ = case_objects(golden_cases["random10x40"])
+    tpl = CircuitNetwork.from_circuit(c)
+    net = marginal_network(tpl, BatchPlan(sizes), 2, "0000").net
+    one = find_path_greedy(net, hypersamples=1, rng=np.random.default_rng(0))
+    many = find_path_greedy(net, hypersamples=32, rng=np.random.default_rng(0))
+    assert len(one.steps) == len(net.operands) - 1
+    assert path_cost(net, one) == pytest.approx(one.est_cost)
+    assert path_cost(net, many) == pytest.approx(many.est_cost)
+    assert many.est_cost <= one.est_cost * 1.0000001
+    again = find_path_greedy(net, hypersamples=32, rng=np.random.default_rng(0))
+    assert again.steps == many.steps
+
+
+def test_arena_buffers_never_overlap_live_values(golden_cases):
+    """Liveness placement: an output buffer must not alias an operand that is
+    still to be read (checked structurally on every step)."""
+    pipe, _, _ = _pipeline(golden_cases["surface_d3_r1"])
+    for pr in pipe.compiled.programs:
+        live = {}
+        for st in pr.steps:
+            ak, ar, bk, br, ok, orf, out_n = (int(v) for v in st[:7])
+            if ok == 0:
+                for off, n in live.items():
+                    reads = [(k, r) for k, r in ((ak, ar), (bk, br)) if k == 0]
+                    if any(r == off for _, r in reads):
+                        continue
+                    assert orf + out_n <= off or off + n <= orf, "output overlaps a live intermediate"
+                live[orf] = out_n
+            for k, r in ((ak, ar), (bk, br)):
+                if k == 0:
+                    live.pop(r, None)

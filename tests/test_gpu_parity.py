@@ -1,0 +1,227 @@
+"""Parity of the CUDA path (through the C-ABI of libptsbe_b200.so) against the
+oracle and the golden vectors of the unmodified reference.
+
+Tolerances (BASELINE.json north_star): marginals within 1e-11 (complex128) and
+1e-5 relative (complex64); sampler counts bit-exact given the same float64
+marginals and the same uniforms; complex128 end-to-end histograms bit-exact
+against the reference-with-shim goldens; complex64 end-to-end by TVD."""
+
+import numpy as np
+import pytest
+
+from conftest import case_objects
+from oracle import bridge
+from oracle import ptsbe_oracle as O
+from paper_2604_08467_b200 import _capi, workloads
+from paper_2604_08467_b200.engine import (
+    BatchPlan, CircuitNetwork, ErrorSet, RunConfig, SamplerContext, conditional_marginal,
+    conditional_marginals_batched, merge_records, run_ptsbe, sample_proportional,
+    sample_proportional_batched, ShotRecord, presample_errors,
+)
+from paper_2604_08467_b200.errors import ImpossiblePrefixError
+from paper_2604_08467_b200.planner import PathCache
+from paper_2604_08467_b200.tensor import Index, Tensor, TensorNetwork, contract_pair, execute_path
+from paper_2604_08467_b200.circuits import Circuit, Gate, NoiseChannel
+
+pytestmark = pytest.mark.gpu
+
+ALL = ["ghz12", "ghz6_per_qubit", "random_0", "random_1", "random_2", "random_3", "random_4", "random_5",
+       "hea8", "qaoa8", "surface_d3_r1", "random10x40"]
+
+
+def _marginal_rows(case):
+    c, sizes, es = case_objects(case)
+    by_stage = {}
+    for row in case["marginals"]:
+        by_stage.setdefault(row["stage"], []).append(row)
+    return c, sizes, es, by_stage
+
+
+@pytest.mark.parametrize("name", ALL)
+@pytest.mark.parametrize("dtype,tol", [("complex128", 1e-11), ("complex64", 1e-5)])
+def test_marginals_match_reference_goldens(golden_cases, name, dtype, tol):
+    c, sizes, es, by_stage = _marginal_rows(golden_cases[name])
+    tpl = CircuitNetwork.from_circuit(c)
+    for j, rows in by_stage.items():
+        ctx = SamplerContext(hypersamples=4, dtype=dtype)
+        got = conditional_marginals_batched(tpl, [es[r["eset"]] for r in rows], BatchPlan(sizes), j,
+                                            [r["prefix"] for r in rows], ctx)
+        want = np.asarray([r["probs"] for r in rows])
+        assert got.shape == want.shape
+        err = np.max(np.abs(got - want), axis=1) / np.max(want, axis=1)
+        assert err.max() <= tol, (name, j, err.max())
+
+
+def test_single_item_conditional_marginal_signature(golden_cases):
+    """Reference signature conditional_marginal(cnet, cache, plan, j, prefix)."""
+    case = golden_cases["random_4"]
+    c, sizes, es = case_objects(case)
+    tpl = CircuitNetwork.from_circuit(c)
+    for row in case["marginals"][:4]:
+        got = conditional_marginal(tpl.merged(es[row["eset"]]), PathCache(), BatchPlan(sizes), row["stage"],
+                                   row["prefix"], hypersamples=2)
+        np.testing.assert_allclose(got, row["probs"], atol=1e-11, rtol=0)
+
+
+def test_bell_kats():
+    c = Circuit(2, (Gate("H", (0,)), Gate("CX", (0, 1), None, NoiseChannel("depolarizing", 0.0))))
+    tpl = CircuitNetwork.from_circuit(c)
+    cache = PathCache()
+    np.testing.assert_allclose(conditional_marginal(tpl, cache, BatchPlan((2,)), 1, ""), [0.5, 0, 0, 0.5], atol=1e-12)
+    np.testing.assert_allclose(conditional_marginal(tpl, cache, BatchPlan((1, 1)), 2, "1"), [0, 1], atol=1e-12)
+
+
+def test_sampler_bit_exact_against_oracle_draws():
+    """Same float64 marginals + same Philox uniforms -> identical counts."""
+    rng = np.random.default_rng(3)
+    for b in (1, 2, 5, 10):
+        w = 37
+        probs = rng.random((w, 1 << b)) ** 3
+        probs[rng.random(probs.shape) < 0.3] = 0.0
+        probs[:, 0] += 1e-3
+        mult = rng.integers(1, 5000, size=w).astype(np.uint32)
+        mult[0] = 1
+        eset = rng.integers(0, 1000, size=w).astype(np.uint32)
+        rank = rng.integers(0, 50, size=w).astype(np.uint32)
+        item, index, count = _capi.sample_stage(b, 3, 0xDEADBEEFCAFE, probs, mult, eset, rank)
+        pos = 0
+        for i in range(w):
+            want = O.multinomial_counts(probs[i], int(mult[i]), 0xDEADBEEFCAFE, int(eset[i]), 3, int(rank[i]))
+            nz = np.flatnonzero(want)
+            sl = slice(pos, pos + nz.size)
+            assert np.all(item[sl] == i)
+            assert index[sl].tolist() == nz.tolist()
+            assert count[sl].tolist() == want[nz].tolist()
+            pos += nz.size
+        assert pos == item.size
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_complex128_histograms_bit_exact_vs_reference(golden_cases, name):
+    """Reference sample_proportional (with the counter-based RNG shim) vs the
+    device run, per error set, records and stage events."""
+    case = golden_cases[name]
+    c, sizes, es = case_objects(case)
+    tpl = CircuitNetwork.from_circuit(c)
+    ctx = SamplerContext(hypersamples=4, dtype="complex128")
+    per_set = sample_proportional_batched(tpl, es, BatchPlan(sizes), case["seed"], ctx)
+    got = [[[r.bitstring, r.count] for r in recs] for recs in per_set]
+    assert got == case["histograms"]
+    assert {str(k): v for k, v in ctx.stats.stage_events.items()} == case["stage_events"]
+    assert ctx.stats.plan_events == len(sizes)
+
+
+def test_run_ptsbe_merged_histogram_and_counters(golden_cases):
+    case = golden_cases["hea8"]
+    c, sizes, es = case_objects(case)
+    cfg = RunConfig(n=c.n, g=len(c.gates), batch_sizes=sizes, seed=case["seed"], hypersamples=4,
+                    error_sets=len(es), total_shots=sum(k.m for k in es))
+    res = run_ptsbe(c, cfg, errorsets=es)
+    want = O.merge_histograms([[tuple(r) for r in h] for h in case["histograms"]])
+    assert [(r.bitstring, r.count) for r in res.records] == want
+    assert res.total_count == sum(k.m for k in es)
+    assert res.plan_events == len(sizes)
+    assert res.contract_events == sum(case["stage_events"].values())
+    assert {str(k): v for k, v in res.stage_events.items()} == case["stage_events"]
+    assert res.timings["gpu_launches"] > 0
+    again = run_ptsbe(c, cfg, errorsets=es)
+    assert [(r.bitstring, r.count) for r in again.records] == want  # repeat runs identical
+
+
+def test_results_do_not_depend_on_grouping(golden_cases):
+    """Determinism under sharding (reference tests/test_engine.py:455-463):
+    splitting the error sets over calls does not change any record."""
+    case = golden_cases["random10x40"]
+    c, sizes, es = case_objects(case)
+    tpl = CircuitNetwork.from_circuit(c)
+    whole = sample_proportional_batched(tpl, es, BatchPlan(sizes), 77, SamplerContext(hypersamples=4))
+    parts = []
+    for lo, hi in ((0, 1), (1, 3), (3, 4)):
+        parts += sample_proportional_batched(tpl, es[lo:hi], BatchPlan(sizes), 77, SamplerContext(hypersamples=4))
+    assert [[(r.bitstring, r.count) for r in recs] for recs in whole] == \
+           [[(r.bitstring, r.count) for r in recs] for recs in parts]
+
+
+def test_complex64_end_to_end_tvd():
+    c, _ = workloads.ghz(12, p=0.05)
+    sizes = (4, 4, 4)
+    es = presample_errors(c, 8, "uniform", shots_per_set=20000, rng=np.random.default_rng(5))
+    tpl = CircuitNetwork.from_circuit(c)
+    per_set = sample_proportional_batched(tpl, es, BatchPlan(sizes), 11, SamplerContext(hypersamples=4, dtype="complex64"))
+    for k, recs in zip(es, per_set):
+        ops, finals = bridge.merged_ops(c, k.realized)
+        exact = O.conditional_marginal(ops, finals, (12,), 1, "")
+        emp = np.zeros(1 << 12)
+        for r in recs:
+            emp[int(r.bitstring, 2)] = r.count / k.m
+        assert sum(r.count for r in recs) == k.m
+        assert 0.5 * np.abs(emp - exact).sum() <= 0.02
+
+
+def test_deterministic_circuit_and_single_set_signature():
+    c = Circuit(3, tuple(Gate("X", (q,)) for q in range(3)))
+    tpl = CircuitNetwork.from_circuit(c)
+    recs = sample_proportional(tpl, ErrorSet(0, ("I", "I", "I"), 10), BatchPlan((1, 1, 1)), np.random.default_rng(0))
+    assert [(r.bitstring, r.count) for r in recs] == [("111", 10)]
+
+
+def test_impossible_trajectory_is_flagged_with_its_id():
+    """Amplitude damping K1 on |0> annihilates the state: the error set is
+    reported (ImpossiblePrefixError, engine.py:475-476) instead of crashing the batch."""
+    c = Circuit(2, (Gate("Rz", (0,), 0.3, NoiseChannel("amplitude_damping", 0.2)), Gate("H", (1,))))
+    tpl = CircuitNetwork.from_circuit(c)
+    es = [ErrorSet(0, ("K0", "I"), 5), ErrorSet(7, ("K1", "I"), 5)]
+    with pytest.raises(ImpossiblePrefixError, match="error set 7"):
+        sample_proportional_batched(tpl, es, BatchPlan((1, 1)), 1)
+
+
+def test_tensor_core_api_on_device():
+    """contract_pair / execute_path known answers (reference tests/test_tensor.py:25-62)."""
+    a = Tensor([Index(0, 2), Index(1, 3)], np.ones((2, 3)))
+    b = Tensor([Index(1, 3), Index(2, 2)], np.ones((3, 2)))
+    out = contract_pair(a, b)
+    assert out.labels == (0, 2) and np.allclose(out.data, 3)
+    v = Tensor([Index(5, 2)], [1, 2])
+    w = Tensor([Index(6, 2)], [3, 4])
+    out = contract_pair(v, w)
+    assert out.labels == (5, 6) and np.allclose(out.data, [[3, 4], [6, 8]])
+    rng = np.random.default_rng(1)
+    ts = [Tensor([Index(0, 2), Index(1, 3)], rng.normal(size=(2, 3)) + 1j * rng.normal(size=(2, 3))),
+          Tensor([Index(1, 3), Index(2, 4)], rng.normal(size=(3, 4)) + 1j * rng.normal(size=(3, 4))),
+          Tensor([Index(2, 4), Index(3, 2)], rng.normal(size=(4, 2)) + 1j * rng.normal(size=(4, 2)))]
+    net = TensorNetwork(ts, [0, 3])
+    got = execute_path(net, [(0, 1), (0, 1)])
+    want = ts[0].data @ ts[1].data @ ts[2].data
+    assert got.labels == (0, 3)
+    np.testing.assert_allclose(got.data, want, atol=1e-12)
+
+
+def test_merge_records_on_device_wide_keys():
+    """Two-word keys (n > 64 qubits, surface code d=5 x 3 rounds = 97 bits)."""
+    rng = np.random.default_rng(2)
+    strings = ["".join(rng.choice(["0", "1"], size=97)) for _ in range(40)]
+    per_set = [[ShotRecord(s, int(rng.integers(1, 9))) for s in rng.choice(strings, size=25)] for _ in range(6)]
+    got = merge_records(per_set)
+    want = O.merge_histograms([[(r.bitstring, r.count) for r in recs] for recs in per_set])
+    assert [(r.bitstring, r.count) for r in got] == want
+
+
+def test_full_size_properties_cfg1():
+    """BASELINE config 1 at full size: 64 error sets x 1000 shots, complex64;
+    size-independent properties (shot conservation, sortedness, sharding idempotence)."""
+    c, sizes = workloads.ghz(12, p=0.01)
+    idx = workloads.presample_matrix(c, 64, np.random.default_rng(1))
+    es = workloads.errorsets_from_matrix(c, idx, 1000)
+    cfg = RunConfig(n=12, g=12, batch_sizes=sizes, seed=4, hypersamples=8, dtype="complex64",
+                    error_sets=64, total_shots=64000)
+    res = run_ptsbe(c, cfg, errorsets=es)
+    assert res.total_count == 64000
+    keys = [r.bitstring for r in res.records]
+    assert keys == sorted(keys) and len(set(keys)) == len(keys)
+    a = run_ptsbe(c, cfg, errorsets=es[:20])
+    b = run_ptsbe(c, cfg, errorsets=es[20:])
+    merged = merge_records([a.records, b.records])
+    assert [(r.bitstring, r.count) for r in merged] == [(r.bitstring, r.count) for r in res.records]
+    # GHZ with weak noise: the two GHZ strings dominate
+    top = {r.bitstring: r.count for r in res.records}
+    assert top["0" * 12] + top["1" * 12] > 0.8 * 64000
