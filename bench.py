@@ -1,0 +1,472 @@
+#!/usr/bin/env python
+"""Throughput of the PTSBE proportional hot path (BASELINE.json metric:
+shots/sec, device-timed, max over ranks) on synthetic circuits of the named
+shapes.
+
+  python bench.py --gpus N --steps K --warmup W            # this repo's CUDA path
+  python bench.py --impl reference --gpus N --steps K ...  # the reference algorithm on the host cores
+
+A step = one pass of the hot path (stored-path contraction + non-degenerate
+sampling + local histogram) over one batch of pre-sampled error sets.  Weak
+scaling: every GPU gets `--sets` error sets; with N > 1 each step ends with
+the NCCL gather + merge of the per-rank histograms.  Planning/compilation is
+excluded from the timed region, as the reference excludes path planning from
+its loop time (reference bench.py:5-8, engine.py:895-901).
+
+`value`    inputs resident in HBM (ptsbe_batch_run), device-timed.
+`e2e`      ptsbe_sample() with HOST buffers: pinned Kraus-index matrix and shot
+           counts copied H2D, histogram copied D2H, inside the timed region.
+`roofline` the dominant kernel (stored-path executor, marginal pass of the
+           busiest stage): algorithmic bytes and flops per launch over the
+           CUDA-event time of those launches.
+`cpu_baseline` / `--impl reference`: oracle/ptsbe_oracle.py (numpy port of the
+           reference algorithm; the reference itself is pure Python and cannot
+           travel to the GPU box) on a bounded sample of the same workload,
+           one process per host core.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "shots/sec (device-timed, max over ranks)"
+
+
+# --------------------------------------------------------------------------
+# workloads
+# --------------------------------------------------------------------------
+
+def build_workload(name: str, args):
+    from paper_2604_08467_b200 import workloads
+
+    if name == "cfg2":
+        c, sizes = workloads.hea(30, 6, gamma=0.01, p=0.01, seed=2)
+        dflt = dict(sets=4096, shots=10_000, dtype="complex64",
+                    label="cfg2: 30-qubit HEA depth 6, amplitude damping 0.01 + 2q depolarizing 0.01")
+    elif name == "cfg1":
+        c, sizes = workloads.ghz(12, p=0.01)
+        dflt = dict(sets=64, shots=1000, dtype="complex64", label="cfg1: 12-qubit GHZ, depolarizing 0.01")
+    elif name == "cfg3":
+        c, sizes = workloads.surface_code(5, 3, p=1e-3)
+        dflt = dict(sets=100_000, shots=1, dtype="complex64", label="cfg3: surface code d=5, 3 rounds, p=1e-3")
+    elif name == "cfg4":
+        c, sizes = workloads.qaoa(50, 2, p=1e-3, seed=4)
+        dflt = dict(sets=10_000, shots=10_000, dtype="complex128", label="cfg4: 50-qubit QAOA p=2, 3-regular")
+    elif name == "cfg5":
+        c, sizes = workloads.random40(40, 400, seed=5)
+        dflt = dict(sets=100_000, shots=100, dtype="complex64", label="cfg5: random_circuit(40, 400)")
+    else:
+        raise SystemExit(f"unknown workload {name!r}")
+    if args.plan:
+        sizes = tuple(int(v) for v in args.plan.split(","))
+        if sum(sizes) != c.n:
+            raise SystemExit(f"--plan must sum to {c.n}")
+    sets = args.sets or dflt["sets"]
+    shots = args.shots or dflt["shots"]
+    dtype = args.dtype or dflt["dtype"]
+    return c, sizes, sets, shots, dtype, dflt["label"]
+
+
+def error_matrix(c, sets: int, first_id: int, seed: int) -> np.ndarray:
+    """Kraus-index rows of global error sets [first_id, first_id + sets): the
+    stream is keyed by the block of 4096 ids, so any rank layout sees the same
+    error set under the same global id."""
+    from paper_2604_08467_b200 import workloads
+
+    blk = 4096
+    out = np.empty((sets, len(c.gates)), dtype=np.uint8)
+    b0, b1 = first_id // blk, (first_id + sets - 1) // blk
+    for b in range(b0, b1 + 1):
+        rows = workloads.presample_matrix(c, blk, np.random.default_rng([seed, b]))
+        lo, hi = max(first_id, b * blk), min(first_id + sets, (b + 1) * blk)
+        out[lo - first_id: hi - first_id] = rows[lo - b * blk: hi - b * blk]
+    return out
+
+
+# --------------------------------------------------------------------------
+# CPU legs (oracle port of the reference algorithm, process-parallel over error sets)
+# --------------------------------------------------------------------------
+
+def _cpu_worker(job):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import bridge
+    from oracle import ptsbe_oracle as O
+    from paper_2604_08467_b200 import workloads
+
+    c, sizes, rows, ids, shots, seed, paths = job
+    ops, finals = bridge.template_of(c)
+    es = workloads.errorsets_from_matrix(c, rows, shots)
+    t0 = time.perf_counter()
+    done = 0
+    for k, gid in zip(es, ids):
+        merged = O.merge_errors(ops, bridge.realized_operators(c, k.realized))
+        try:
+            O.sample_proportional(merged, finals, sizes, k.m, seed, int(gid), paths)
+        except O.ImpossiblePrefix:
+            pass
+        done += k.m
+    return done, time.perf_counter() - t0
+
+
+def cpu_leg(c, sizes, seed: int, sets: int, shots: int, procs: int):
+    """Times the reference algorithm (oracle port) on `sets` error sets x `shots`
+    shots of the workload, one process per core; planning excluded (one stored
+    path per stage, planned once on the template -- engine.py:864-879)."""
+    import multiprocessing as mp
+
+    from oracle import bridge
+    from oracle import ptsbe_oracle as O
+
+    ops, finals = bridge.template_of(c)
+    # one stored path per stage, searched like the reference does (100 randomized greedy
+    # descents on the plain flop model, planner.py:212-251) with the product's native planner
+    from paper_2604_08467_b200.engine import BatchPlan, CircuitNetwork, marginal_network
+    from paper_2604_08467_b200.planner import find_path_greedy
+
+    tpl, bp = CircuitNetwork.from_circuit(c), BatchPlan(sizes)
+    paths = [list(find_path_greedy(marginal_network(tpl, bp, j, "0" * bp.offset(j)).net, hypersamples=100,
+                                   rng=np.random.default_rng([seed, j])).steps) for j in range(1, bp.f + 1)]
+    rows = error_matrix(c, sets, 0, seed)
+    procs = max(1, min(procs, sets))
+    jobs = []
+    for r in range(procs):
+        sl = slice(r * sets // procs, (r + 1) * sets // procs)
+        jobs.append((c, sizes, rows[sl], np.arange(sets)[sl], shots, seed, paths))
+    t0 = time.perf_counter()
+    if procs == 1:
+        res = [_cpu_worker(jobs[0])]
+    else:
+        with mp.get_context("fork").Pool(procs) as pool:
+            res = pool.map(_cpu_worker, jobs)
+    wall = time.perf_counter() - t0
+    done = sum(r[0] for r in res)
+    return done / wall, wall, procs
+
+
+def cpu_sample_size(name: str):
+    """(error sets, shots per set) of the bounded CPU sample: about 10-30 s of
+    host work for the whole pool."""
+    return {"cfg1": (64, 1000), "cfg2": (None, 24), "cfg3": (None, 1), "cfg4": (None, 8),
+            "cfg5": (None, 20)}[name]
+
+
+# --------------------------------------------------------------------------
+# clocks
+# --------------------------------------------------------------------------
+
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.rows, self.proc = [], None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100", "-i", str(index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.perf_counter(), line.strip()))
+
+    def stop(self, t0: float, t1: float) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        for t, line in self.rows:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7 or not (t0 <= t <= t1):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+# main
+# --------------------------------------------------------------------------
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        doc = json.load(open(path))
+        return float(doc["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    c, sizes, sets, shots, dtype, label = build_workload(args.workload, args)
+    cores = os.cpu_count() or 1
+    s_sets, s_shots = cpu_sample_size(args.workload)
+    s_sets = s_sets or cores
+    if args.cpu_sets:
+        s_sets = args.cpu_sets
+    if args.cpu_shots:
+        s_shots = args.cpu_shots
+    for _ in range(min(args.warmup, 1)):
+        cpu_leg(c, sizes, args.seed, min(s_sets, cores), max(1, s_shots // 4), cores)
+    vals, walls = [], []
+    for _ in range(args.steps):
+        v, wall, procs = cpu_leg(c, sizes, args.seed, s_sets, s_shots, cores)
+        vals.append(v)
+        walls.append(wall)
+    value = float(np.mean(vals))
+    sample = f"{s_sets} error sets x {s_shots} shots per step of the same circuit/plan, {procs} processes"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "shots/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(walls)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "complex128 (f64)",
+        "data": "synthetic",
+        "config": {"workload": label, "plan": list(sizes), "error_sets": s_sets, "shots_per_set": s_shots,
+                   "full_size": f"{sets} error sets x {shots} shots per GPU"},
+        "cpu_baseline": {"value": value, "unit": "shots/s", "cores": procs, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "shots/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--sets", type=int, default=0, help="error sets PER GPU")
+    ap.add_argument("--shots", type=int, default=0, help="shots per error set")
+    ap.add_argument("--plan", default="", help="comma-separated batch sizes")
+    ap.add_argument("--dtype", default="", choices=["", "complex64", "complex128"])
+    ap.add_argument("--hypersamples", type=int, default=64)
+    ap.add_argument("--seed", type=int, default=20260408)
+    ap.add_argument("--cpu-sets", type=int, default=0)
+    ap.add_argument("--cpu-shots", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    c, sizes, sets, shots, dtype, label = build_workload(args.workload, args)
+
+    # ---- cpu_baseline leg first (rank 0, N = 1 only), before CUDA is touched ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        s_sets, s_shots = cpu_sample_size(args.workload)
+        s_sets = args.cpu_sets or s_sets or cores
+        s_shots = args.cpu_shots or s_shots
+        v, wall, procs = cpu_leg(c, sizes, args.seed, s_sets, s_shots, cores)
+        cpu = {"value": v, "unit": "shots/s", "cores": procs, "kind": "port",
+               "sample": f"{s_sets} error sets x {s_shots} shots of the same circuit/plan, {wall:.1f} s wall"}
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_08467_b200 import _capi
+    from paper_2604_08467_b200.engine import BatchPlan, CircuitNetwork, DevicePipeline, SamplerContext, VariantTables
+    from paper_2604_08467_b200.partition import gather_histograms, merge_on_device
+
+    if _capi.device_count() < 1:
+        raise SystemExit("bench.py needs a CUDA device: libptsbe_b200 has no CPU fallback")
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+
+    # ---- inputs: weak scaling, `sets` error sets per GPU, global ids ----
+    first = rank * sets
+    kraus = error_matrix(c, sets, first, args.seed)
+    shots_arr = np.full(sets, shots, dtype=np.uint32)
+    ids = np.arange(first, first + sets, dtype=np.uint32)
+    total_shots_local = int(shots_arr.sum())
+
+    # ---- plan once (excluded from timing) ----
+    t0 = time.perf_counter()
+    tpl = CircuitNetwork.from_circuit(c)
+    tables = VariantTables.from_channels(tpl)
+    ctx = SamplerContext(hypersamples=args.hypersamples, planner_seed=args.seed, dtype=dtype, device=local_rank)
+    pipe = DevicePipeline(tpl, BatchPlan(sizes), tables, ctx, shots_per_set=float(shots))
+    plan_s = time.perf_counter() - t0
+    dp = pipe.device_plan
+    batch = dp.upload(kraus, shots_arr, ids)
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def step(i):
+        """One pass over the batch; returns (device ms of this rank, stats)."""
+        n_rec, st = batch.run(args.seed + i)
+        ms = float(st.loop_ms)
+        if world > 1:
+            k, cnt = batch.histogram_dev()
+            kt = torch.as_tensor(k, device=f"cuda:{local_rank}").view(torch.int64) if n_rec else \
+                torch.zeros((0, dp.words), dtype=torch.int64, device=f"cuda:{local_rank}")
+            ct = torch.as_tensor(cnt, device=f"cuda:{local_rank}").view(torch.int64) if n_rec else \
+                torch.zeros(0, dtype=torch.int64, device=f"cuda:{local_rank}")
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            gather_histograms(kt, ct, merge=lambda a, b: merge_on_device(a, b, local_rank))
+            e1.record()
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+        return ms, st
+
+    for i in range(args.warmup):
+        step(-1 - i)
+    sync_all()
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    time.sleep(0.15 if sampler else 0.0)
+    wall0 = time.perf_counter()
+    dev_ms, stats = 0.0, []
+    for i in range(args.steps):
+        ms, st = step(i)
+        dev_ms += ms
+        stats.append(st)
+    sync_all()
+    wall1 = time.perf_counter()
+    clocks = sampler.stop(wall0, wall1) if sampler else None
+
+    t = torch.tensor([dev_ms, (wall1 - wall0) * 1e3], dtype=torch.float64, device=f"cuda:{local_rank}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms_max, wall_ms_max = float(t[0]), float(t[1])
+    total_shots = total_shots_local * world
+    value = total_shots * args.steps / (dev_ms_max * 1e-3)
+
+    # ---- e2e through the host-buffer C-ABI call (pinned inputs) ----
+    e2e = None
+    if not args.no_e2e:
+        pin_k = torch.empty(kraus.shape, dtype=torch.uint8, pin_memory=True)
+        pin_s = torch.empty(sets, dtype=torch.int32, pin_memory=True)
+        pin_i = torch.empty(sets, dtype=torch.int32, pin_memory=True)
+        pin_k.numpy()[:] = kraus
+        pin_s.numpy().view(np.uint32)[:] = shots_arr
+        pin_i.numpy().view(np.uint32)[:] = ids
+        e_steps = max(1, min(args.steps, 3))
+        dp.sample(pin_k.numpy(), pin_s.numpy().view(np.uint32), pin_i.numpy().view(np.uint32), args.seed - 1)
+        sync_all()
+        w0 = time.perf_counter()
+        h2d = d2h = 0
+        for i in range(e_steps):
+            keys, _, counts, st = dp.sample(pin_k.numpy(), pin_s.numpy().view(np.uint32),
+                                            pin_i.numpy().view(np.uint32), args.seed + i)
+            h2d, d2h = int(st.h2d_bytes), int(st.d2h_bytes)
+            if world > 1:
+                kt = torch.from_numpy(keys.view(np.int64)).to(f"cuda:{local_rank}")
+                ct = torch.from_numpy(counts.view(np.int64)).to(f"cuda:{local_rank}")
+                kk, cc = gather_histograms(kt, ct, merge=lambda a, b: merge_on_device(a, b, local_rank))
+                cc.cpu()
+        sync_all()
+        te = torch.tensor([(time.perf_counter() - w0)], dtype=torch.float64, device=f"cuda:{local_rank}")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": total_shots * e_steps / float(te[0]), "unit": "shots/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e_steps,
+               "timing": "host wall clock around ptsbe_sample(), streams drained on both sides"}
+
+    if rank == 0:
+        f = len(sizes)
+        st = stats[-1]
+        elem = 8 if dtype == "complex64" else 16
+        real = elem // 2
+        marg = [sum(float(s.marg_ms[j]) for s in stats) for j in range(f)]
+        hoist = [sum(float(s.hoist_ms[j]) for s in stats) for j in range(f)]
+        samp = [sum(float(s.sampler_ms[j]) for s in stats) for j in range(f)]
+        comp = [sum(float(s.compact_ms[j]) for s in stats) for j in range(f)]
+        hist_ms = sum(float(s.histogram_ms) for s in stats)
+        jtop = int(np.argmax(marg))
+        prog = pipe.programs_of(jtop + 1)[-1]
+        items = sum(int(s.stage_events[jtop]) for s in stats)
+        launches = sum(int(s.marg_launches[jtop]) for s in stats)
+        words = dp.words
+        # algorithmic bytes of one work item of the marginal pass:
+        # records of earlier passes it reads + its list entry (error set, parent, prefix words)
+        # + the population vector, mass and minimum it writes
+        item_bytes = prog.ext_read_elems * elem + 8 + 8 * words + prog.out_elems * real + 16
+        item_flops = 8.0 * prog.flops
+        hbm_peak, peak_src = peaks()
+        t_s = marg[jtop] * 1e-3
+        achieved = items * item_bytes / t_s / 1e9 if t_s > 0 else 0.0
+        fp32_peak, fp64_peak = _capi.measure_fma_peak(local_rank)
+        fma_peak = fp32_peak if dtype == "complex64" else fp64_peak
+        tflops = items * item_flops / t_s / 1e12 if t_s > 0 else 0.0
+        timed_ms = sum(float(s.loop_ms) for s in stats)
+        out = {
+            "metric": METRIC, "value": value, "unit": "shots/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "c64 (f32 FMA)" if dtype == "complex64" else "c128 (f64 FMA)", "data": "synthetic",
+            "config": {"workload": label, "plan": list(sizes), "error_sets_per_gpu": sets, "shots_per_set": shots,
+                       "gates": len(c.gates), "hypersamples": args.hypersamples, "plan_s": round(plan_s, 3),
+                       "l2": "per-step working set (work lists, hoisted records, population vectors) exceeds the 126 MB L2"
+                             if total_shots_local * 8 > 126e6 else "working set below L2 size (small workload)",
+                       "parallelism": f"error sets sharded over {world} GPU(s), weak scaling"},
+            "clocks": clocks,
+            "e2e": e2e,
+            "gpu_launches": int(sum(int(s.gpu_launches) for s in stats)),
+            "wall_ms_per_step": wall_ms_max / args.steps,
+            "unique_bitstrings": int(st.n_records),
+            "stage_events": [int(st.stage_events[j]) for j in range(f)],
+            "kernel_ms_per_step": {
+                "exec_marginal": [m / args.steps for m in marg], "exec_hoist": [h / args.steps for h in hoist],
+                "sampler": [s / args.steps for s in samp], "compaction": [x / args.steps for x in comp],
+                "histogram": hist_ms / args.steps, "stage_total": [sum(float(s.stage_ms[j]) for s in stats) / args.steps for j in range(f)],
+            },
+            "roofline": {
+                "kernel": f"exec_kernel<{ 'float' if dtype == 'complex64' else 'double'}> marginal pass, stage {jtop + 1}",
+                "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
+                "bytes_per_item": item_bytes, "items_per_launch": items / max(launches, 1),
+                "launch_ms": marg[jtop] / max(launches, 1), "share_of_step": marg[jtop] / max(timed_ms, 1e-9),
+                "fma": {"achieved_tflops": tflops, "peak_tflops": fma_peak, "frac": tflops / fma_peak if fma_peak else None,
+                        "flops_per_item": item_flops, "peak_source": "ptsbe_measure_fma_peak (independent FMA chains, this run)"},
+            },
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out))
+    batch.close()
+    pipe.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -111,6 +111,13 @@ typedef struct {
   int64_t first_flagged_id;
   uint32_t first_flag_kind; /* PTSBE_ENUMERIC or PTSBE_EIMPOSSIBLE */
   uint32_t first_flag_stage;
+  /* per-kernel device time inside each stage (CUDA events on the plan's stream) */
+  float hoist_ms[PTSBE_MAX_STAGES];   /* exec_kernel, hoist passes 0..j-2          */
+  float marg_ms[PTSBE_MAX_STAGES];    /* exec_kernel, marginal pass                */
+  float sampler_ms[PTSBE_MAX_STAGES]; /* sample_kernel                             */
+  float compact_ms[PTSBE_MAX_STAGES]; /* scans + expand + rank (next work list)    */
+  float histogram_ms;                 /* final sort + reduce-by-key                */
+  uint32_t marg_launches[PTSBE_MAX_STAGES];
 } ptsbe_run_stats;
 
 const char* ptsbe_last_error(void);
@@ -205,6 +212,10 @@ int ptsbe_histogram_merge_dev(const uint64_t* keys_dev, const uint64_t* counts_d
                               uint32_t words, int device, uint64_t** out_keys_dev,
                               uint64_t** out_counts_dev, uint64_t* n_out);
 void ptsbe_free_dev(void* p_dev);
+
+/* measurement helper for bench.py's roofline denominators: sustained
+ * non-tensor FMA throughput of the device (independent FFMA / DFMA chains). */
+int ptsbe_measure_fma_peak(int device, double* fp32_tflops, double* fp64_tflops);
 
 void ptsbe_free(void* p);
 

@@ -28,6 +28,7 @@ EXPORTS = (
     "ptsbe_sample", "ptsbe_batch_upload", "ptsbe_batch_run", "ptsbe_batch_fetch",
     "ptsbe_batch_destroy", "ptsbe_histogram_merge", "ptsbe_plan_greedy", "ptsbe_free",
     "ptsbe_batch_histogram_dev", "ptsbe_histogram_merge_dev", "ptsbe_free_dev",
+    "ptsbe_measure_fma_peak",
 )
 
 
@@ -48,6 +49,12 @@ class RunStats(ctypes.Structure):
         ("first_flagged_id", ctypes.c_int64),
         ("first_flag_kind", ctypes.c_uint32),
         ("first_flag_stage", ctypes.c_uint32),
+        ("hoist_ms", ctypes.c_float * MAX_STAGES),
+        ("marg_ms", ctypes.c_float * MAX_STAGES),
+        ("sampler_ms", ctypes.c_float * MAX_STAGES),
+        ("compact_ms", ctypes.c_float * MAX_STAGES),
+        ("histogram_ms", ctypes.c_float),
+        ("marg_launches", ctypes.c_uint32 * MAX_STAGES),
     ]
 
 
@@ -98,6 +105,7 @@ def load() -> ctypes.CDLL:
                                               ctypes.POINTER(U64)]
     lib.ptsbe_free_dev.argtypes = [P]
     lib.ptsbe_free_dev.restype = None
+    lib.ptsbe_measure_fma_peak.argtypes = [I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
     _lib = lib
     return lib
 
@@ -302,6 +310,13 @@ def histogram_merge_dev(keys_ptr: int, counts_ptr: int, n: int, words: int, devi
     check(load().ptsbe_histogram_merge_dev(keys_ptr, counts_ptr, n, words, device, ctypes.byref(ok),
                                            ctypes.byref(oc), ctypes.byref(m)))
     return (DeviceArray(ok.value, (m.value, words), owned=True), DeviceArray(oc.value, (m.value,), owned=True))
+
+
+def measure_fma_peak(device: int = 0) -> tuple:
+    """(fp32, fp64) sustained non-tensor FMA TFLOP/s of the device."""
+    a, b = ctypes.c_double(), ctypes.c_double()
+    check(load().ptsbe_measure_fma_peak(device, ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
 
 
 def plan_greedy(op_labels, op_dims, op_class=None, class_weight=None, hypersamples=100,

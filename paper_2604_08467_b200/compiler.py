@@ -90,6 +90,8 @@ class Program:
     flops: float = 0.0          # complex multiply-adds of one execution of this pass
     peak_elems: int = 0
     max_out: int = 0
+    ext_read_elems: int = 0     # elements of earlier passes' records one execution reads (HBM/L2)
+    leaf_read_elems: int = 0    # elements of operand-pool leaves one execution reads (L1/L2 resident)
 
 
 class _Arena:
@@ -262,6 +264,7 @@ def compile_stage(
         flops = 0.0
         prog_leaves: list[list[int]] = []
         prog_leaf_index: dict[int, int] = {}
+        ext_reads: dict[int, int] = {}
 
         def ref_of(nid: int):
             if nid < n_leaves:
@@ -275,6 +278,7 @@ def compile_stage(
                     prog_leaves.append([pool.add(blk), size, o.sel_kind, o.sel_arg])
                 return 1, at
             if nid in rec_off and nodes[nid].pass_ != p:
+                ext_reads[nid] = nodes[nid].size
                 return 2 + nodes[nid].pass_, rec_off[nid]
             if nid in rec_off:
                 raise AssertionError("frontier node consumed inside its own pass")
@@ -339,6 +343,8 @@ def compile_stage(
                 flops=flops,
                 peak_elems=int(peak_fast + peak_spill),
                 max_out=int(max_out),
+                ext_read_elems=int(sum(ext_reads.values())),
+                leaf_read_elems=int(sum(lf[1] for lf in prog_leaves)),
             )
         )
     return programs, tuple(open_order)

@@ -219,6 +219,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
   std::vector<cudaEvent_t> ev(f + 1);
   for (auto& e : ev) CK(cudaEventCreate(&e));
   CK(cudaEventRecord(ev[0], st));
+  EventLog log(st);
 
   for (uint32_t j = 1; j <= f; ++j) {
     Level& cur = lv[j];
@@ -245,8 +246,10 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     // hoist passes: everything that does not depend on the newest prefix bits
     for (uint32_t p = 0; p + 1 < j; ++p) {
       if (!progs[p].d.n_steps) continue;
+      log.begin(&stats->hoist_ms[j - 1]);
       launch_exec_any(pl, progs[p], EXEC_HOIST, table_dev.as<LevelDev>(), kraus_dev, 0,
                       lv[p + 1].n, ext[p].p, nullptr, nullptr);
+      log.end();
     }
     // marginal pass + sampler, in sub-batches sized to the probs buffer
     const size_t real = pl->dtype == PTSBE_C64 ? 4 : 8;
@@ -255,8 +258,11 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     DevBuf nnz((size_t)U * 4, st);
     for (uint32_t s0 = 0; s0 < U; s0 += B) {
       const uint32_t nbatch = std::min(B, U - s0);
+      log.begin(&stats->marg_ms[j - 1]);
       launch_exec_any(pl, progs[j - 1], EXEC_MARGINAL, table_dev.as<LevelDev>(), kraus_dev, s0,
                       nbatch, probs.p, mass.as<double>(), minv.as<double>());
+      log.end();
+      stats->marg_launches[j - 1]++;
       SampleArgs sa;
       sa.probs = probs.p;
       sa.mult = cur.mult.as<uint32_t>();
@@ -280,9 +286,12 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       sa.vanish = pl->vanish;
       sa.neg_abs = pl->neg_abs;
       sa.neg_rel = pl->neg_rel;
+      log.begin(&stats->sampler_ms[j - 1]);
       launch_sampler(st, sa, pl->sm_count);
+      log.end();
     }
     // compaction into level j+1
+    log.begin(&stats->compact_ms[j - 1]);
     DevBuf child_base((size_t)U * 4, st);
     exclusive_scan<uint32_t, uint32_t>(nnz.as<uint32_t>(), child_base.as<uint32_t>(), U,
                                        scal.as<uint32_t>(), st);
@@ -329,6 +338,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       }
     }
     CK(cudaGetLastError());
+    log.end();
     CK(cudaEventRecord(ev[j], st));
     // parents' per-stage arrays are no longer needed (lists stay for ancestor lookups)
     cur.mult.release();
@@ -337,6 +347,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     cur.gid.release();
   }
   CK(cudaStreamSynchronize(st));
+  log.flush();
   for (uint32_t j = 1; j <= f; ++j) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, ev[j - 1], ev[j]));
@@ -438,6 +449,8 @@ static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stat
     stats->first_flagged_id = (int64_t)(fl.first >> 16);
   }
   bt->have_per_set = false;
+  EventLog hlog(st);
+  hlog.begin(&stats->histogram_ms);
   if (merged) {
     if (chunks.size() == 1) {
       reduce_by_key(outs[0].keys.as<uint64_t>(), outs[0].n, words, outs[0].counts.as<uint32_t>(),
@@ -466,8 +479,10 @@ static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stat
     bt->have_per_set = true;
     stats->n_records = bt->per_set.n;
   }
+  hlog.end();
   CK(cudaEventRecord(e1, st));
   CK(cudaStreamSynchronize(st));
+  hlog.flush();
   CK(cudaEventElapsedTime(&stats->loop_ms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
@@ -488,6 +503,43 @@ static int guarded(F&& fn) {
   }
 }
 
+}  // namespace ptsbe
+
+namespace ptsbe {
+template <typename T>
+__global__ void fma_peak_kernel(T* out, int iters) {
+  T a0 = threadIdx.x * T(1e-3), a1 = a0 + T(1), a2 = a0 + T(2), a3 = a0 + T(3);
+  T a4 = a0 + T(4), a5 = a0 + T(5), a6 = a0 + T(6), a7 = a0 + T(7);
+  const T m = T(0.999), c = T(1e-4);
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+    a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+template <typename T>
+static double fma_peak(int sm_count, int iters) {
+  const int blocks = sm_count * 8, threads = 256;
+  DevBuf out((size_t)blocks * threads * sizeof(T), nullptr);
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  fma_peak_kernel<T><<<blocks, threads>>>(out.as<T>(), iters / 8);
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    CK(cudaEventRecord(a));
+    fma_peak_kernel<T><<<blocks, threads>>>(out.as<T>(), iters);
+    CK(cudaEventRecord(b));
+    CK(cudaEventSynchronize(b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    best = std::min(best, ms);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  CK(cudaDeviceSynchronize());
+  return 2.0 * 8.0 * iters * (double)blocks * threads / (best * 1e-3) / 1e12;
+}
 }  // namespace ptsbe
 
 extern "C" {
@@ -943,6 +995,18 @@ int ptsbe_histogram_merge_dev(const uint64_t* keys_dev, const uint64_t* counts_d
     }
     cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
+  });
+}
+
+int ptsbe_measure_fma_peak(int device, double* fp32_tflops, double* fp64_tflops) {
+  return guarded([&] {
+    if (ptsbe_device_count() <= device)
+      throw Failure(PTSBE_EDEVICE, "no CUDA device: libptsbe_b200 has no CPU fallback");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (fp32_tflops) *fp32_tflops = fma_peak<float>(prop.multiProcessorCount, 1 << 16);
+    if (fp64_tflops) *fp64_tflops = fma_peak<double>(prop.multiProcessorCount, 1 << 12);
   });
 }
 

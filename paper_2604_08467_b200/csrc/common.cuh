@@ -68,6 +68,35 @@ struct DevBuf {
   template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
 };
 
+// Deferred CUDA-event timing of spans on one stream: spans are recorded while the
+// work is enqueued and read back after the next synchronisation point.
+struct EventLog {
+  struct Span { cudaEvent_t a, b; float* acc; };
+  std::vector<Span> spans;
+  cudaStream_t st = nullptr;
+  explicit EventLog(cudaStream_t s) : st(s) {}
+  void begin(float* acc) {
+    Span sp;
+    sp.acc = acc;
+    CK(cudaEventCreate(&sp.a));
+    CK(cudaEventCreate(&sp.b));
+    CK(cudaEventRecord(sp.a, st));
+    spans.push_back(sp);
+  }
+  void end() { CK(cudaEventRecord(spans.back().b, st)); }
+  // call after the stream has been synchronised
+  void flush() {
+    for (auto& sp : spans) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, sp.a, sp.b) == cudaSuccess && sp.acc) *sp.acc += ms;
+      cudaEventDestroy(sp.a);
+      cudaEventDestroy(sp.b);
+    }
+    spans.clear();
+  }
+  ~EventLog() { for (auto& sp : spans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); } }
+};
+
 inline unsigned cdiv(uint64_t a, uint64_t b) { return (unsigned)((a + b - 1) / b); }
 
 }  // namespace ptsbe
