@@ -70,8 +70,15 @@ typedef struct {
   uint32_t out_elems;         /* complex elements per output record                  */
   uint32_t threads_per_item;  /* 32 (warp per item) or a CTA size up to 1024         */
   uint32_t level;             /* 1-based item level this pass iterates over          */
-  uint32_t result_kind;       /* where the finished record lives: 0 arena, 1 leaf, 2 record */
+  uint32_t result_kind;       /* where the finished record lives: 0 arena, 1 leaf, 2+p record of
+                                 pass p, 3 projection form (marginal pass only)               */
   uint32_t result_ref;
+  uint32_t proj_d;            /* projection form: the steps leave a vector v[proj_d] in the pass's
+                                 output record; the stage result is Re(sum_d v[d] * M[d][c]) with
+                                 M[proj_d][out_elems] at offset result_ref of pass 0's record (one
+                                 per error set) -- run as a dense product over all work items of
+                                 an error set (csrc/project.cuh)                                 */
+  uint32_t reserved;
   const uint32_t* leaves;
   const uint32_t* steps;
   const uint32_t* tables;
@@ -113,7 +120,8 @@ typedef struct {
   uint32_t first_flag_stage;
   /* per-kernel device time inside each stage (CUDA events on the plan's stream) */
   float hoist_ms[PTSBE_MAX_STAGES];   /* exec_kernel, hoist passes 0..j-2          */
-  float marg_ms[PTSBE_MAX_STAGES];    /* exec_kernel, marginal pass                */
+  float marg_ms[PTSBE_MAX_STAGES];    /* exec_kernel, marginal pass (per-item steps) */
+  float project_ms[PTSBE_MAX_STAGES]; /* project_kernel, dense root step           */
   float sampler_ms[PTSBE_MAX_STAGES]; /* sample_kernel                             */
   float compact_ms[PTSBE_MAX_STAGES]; /* scans + expand + rank (next work list)    */
   float histogram_ms;                 /* final sort + reduce-by-key                */
@@ -189,11 +197,15 @@ int ptsbe_histogram_merge(const uint64_t* keys, const uint64_t* counts, uint64_t
 /* replaces: find_path_greedy (planner.py:121-251), host code.
  *   operands are given as CSR lists of (label, dim); op_class / class_weight
  *   (optional, may be NULL) weight a step by the number of distinct instances
- *   of its result across the batch (error-independent hoisting).
+ *   of its result across the batch (error-independent hoisting);
+ *   class_cap_log2 (optional) is a soft cap on log2(result entries) per class
+ *   (records of hoisted classes may be larger than per-item on-chip buffers),
+ *   size_cap_log2 the default for classes without one (0 = none).
  *   merges_out [2*(n_ops-1)] stable-id pairs (result keeps the smaller id). */
 int ptsbe_plan_greedy(uint32_t n_ops, const uint32_t* op_ptr, const int64_t* labels,
                       const uint32_t* dims, const uint32_t* op_class,
-                      const double* class_weight, uint32_t n_classes, uint32_t hypersamples,
+                      const double* class_weight, const double* class_cap_log2,
+                      uint32_t n_classes, uint32_t hypersamples,
                       uint64_t seed, double size_cap_log2, uint32_t* merges_out,
                       double* cost_out, double* flops_out);
 

@@ -92,6 +92,8 @@ class Program:
     max_out: int = 0
     ext_read_elems: int = 0     # elements of earlier passes' records one execution reads (HBM/L2)
     leaf_read_elems: int = 0    # elements of operand-pool leaves one execution reads (L1/L2 resident)
+    proj_d: int = 0             # > 0: projection form, the steps produce a vector v[proj_d] and the
+                                # stage result is Re(v . M), M[proj_d, out_elems] at result_ref in pass 0's record
 
 
 class _Arena:
@@ -233,6 +235,19 @@ def compile_stage(
     if root >= n_leaves:
         rootn.pass_ = top  # the finished record is always produced by the marginal pass
 
+    # projection form: root = (per-item vector v) x (error-set record M[v legs, open legs]).
+    # The root step is not interpreted per item; it runs as one dense product over all
+    # items that share M (csrc/project.cuh).  M is stored as [v's leg order, open order].
+    proj = None
+    if top >= 1 and root >= n_leaves:
+        for v, m in ((rootn.a, rootn.b), (rootn.b, rootn.a)):
+            nv, nm = nodes[v], nodes[m]
+            if (v >= n_leaves and m >= n_leaves and nm.cls == 0 and nv.pass_ == top
+                    and set(nv.labels) <= set(nm.labels)
+                    and set(nm.labels) - set(nv.labels) == set(open_order)):
+                proj = (v, m)
+                break
+
     # storage decisions ------------------------------------------------------
     # frontier = computed node consumed by a later pass -> lives in its pass's record
     rec_off: dict[int, int] = {}
@@ -242,11 +257,16 @@ def compile_stage(
         if nd.parent >= 0 and nodes[nd.parent].pass_ > nd.pass_:
             rec_off[nid] = rec_size[nd.pass_]
             rec_size[nd.pass_] += nd.size
+    if proj is not None:
+        rec_off[proj[0]] = 0  # v is the output record of the marginal pass
+        rec_size[top] = nodes[proj[0]].size
 
     programs: list[Program] = []
     result_kind, result_ref = 0, 0
     for p in range(n_passes):
         mine = [nid for nid in range(n_leaves, len(nodes)) if nodes[nid].pass_ == p]
+        if proj is not None and p == top:
+            mine = [nid for nid in mine if nid != root]
         # sizing of the on-chip arena: try everything on chip, spill the big buffers otherwise
         max_out = max([nodes[nid].size for nid in mine], default=1)
         peak = _place(nodes, mine, rec_off, root, fast_cap=None)[1]
@@ -294,6 +314,8 @@ def compile_stage(
             else:
                 o_kind, o_ref = 0, where[nid]
             out_labels = list(open_order) if nid == root else list(nd.labels)
+            if proj is not None and nid == proj[1]:
+                out_labels = list(nodes[proj[0]].labels) + list(open_order)
             dim_of = dict(zip(na.labels, na.dims))
             dim_of.update(zip(nb.labels, nb.dims))
             sa = dict(zip(na.labels, _row_major_strides(na.dims)))
@@ -323,6 +345,8 @@ def compile_stage(
             flops += float(nd.size) * k_n
             if nid == root:
                 result_kind, result_ref = (2 + p, o_ref) if o_kind == 1 else (0, o_ref)
+        if p == top and proj is not None:
+            result_kind, result_ref = 3, rec_off[proj[1]]
         if p == top and root < n_leaves:
             # single-operand network: the "result" is the leaf itself
             result_kind, result_ref = ref_of(root)
@@ -345,6 +369,7 @@ def compile_stage(
                 max_out=int(max_out),
                 ext_read_elems=int(sum(ext_reads.values())),
                 leaf_read_elems=int(sum(lf[1] for lf in prog_leaves)),
+                proj_d=int(nodes[proj[0]].size) if (proj is not None and p == top) else 0,
             )
         )
     return programs, tuple(open_order)
@@ -430,6 +455,8 @@ class ProgramDesc(ctypes.Structure):
         ("level", ctypes.c_uint32),
         ("result_kind", ctypes.c_uint32),
         ("result_ref", ctypes.c_uint32),
+        ("proj_d", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
         ("leaves", ctypes.c_void_p),
         ("steps", ctypes.c_void_p),
         ("tables", ctypes.c_void_p),
@@ -473,7 +500,7 @@ class CompiledPlan:
             keep += [lv, st, tb]
             arr[k] = ProgramDesc(
                 lv.shape[0], st.shape[0], tb.size, pr.arena_fast, pr.arena_spill, pr.out_elems,
-                pr.threads, pr.level, pr.result_kind, pr.result_ref,
+                pr.threads, pr.level, pr.result_kind, pr.result_ref, pr.proj_d, 0,
                 lv.ctypes.data, st.ctypes.data, tb.ctypes.data,
             )
         sizes = np.asarray(self.sizes, dtype=np.uint32)

@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "executor.cuh"
 #include "histogram.cuh"
+#include "project.cuh"
 #include "sampler.cuh"
 #include "scan.cuh"
 
@@ -124,7 +125,7 @@ static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelD
   a.n_steps = pr.d.n_steps;
   a.arena_fast = pr.d.arena_fast_elems;
   a.arena_spill = pr.d.arena_spill_elems;
-  a.out_elems = pr.d.out_elems;
+  a.out_elems = mode == EXEC_VECTOR ? pr.d.proj_d : pr.d.out_elems;
   a.result_kind = pr.d.result_kind;
   a.result_ref = pr.d.result_ref;
   a.level = pr.d.level;
@@ -147,6 +148,41 @@ static void launch_exec_any(ptsbe_plan* pl, Program& pr, uint32_t mode, const Le
                             double* mass, double* minv) {
   if (pl->dtype == PTSBE_C64) launch_exec<float>(pl, pr, mode, lv, kraus, first, n, out, mass, minv);
   else launch_exec<double>(pl, pr, mode, lv, kraus, first, n, out, mass, minv);
+}
+
+// P = Re(V . M) for the work items [first, first + n) of a level (project.cuh)
+static void launch_project(ptsbe_plan* pl, const Program& pr, const void* v, const void* rec0,
+                           uint32_t rec_stride, const uint32_t* eset, uint32_t first, uint32_t n,
+                           void* out) {
+  if (n == 0) return;
+  ProjectArgs a;
+  a.v = v;
+  a.rec0 = rec0;
+  a.eset = eset;
+  a.out = out;
+  a.first_item = first;
+  a.n_items = n;
+  a.D = pr.d.proj_d;
+  a.N = pr.d.out_elems;
+  a.rec_stride = rec_stride;
+  a.m_off = pr.d.result_ref;
+  const uint64_t tiles = (uint64_t)cdiv(n, PJ_TI) * cdiv(a.N, PJ_TN);
+  const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)pl->sm_count * 2);
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(project_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    CK(cudaFuncSetAttribute(project_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    attr_set = true;
+  }
+  if (pl->dtype == PTSBE_C64) {
+    const size_t smem = (size_t)ProjK<float>::KC * (PJ_TIP + PJ_TN) * sizeof(float2);
+    project_kernel<float><<<grid, PJ_THREADS, smem, pl->stream>>>(a);
+  } else {
+    const size_t smem = (size_t)ProjK<double>::KC * (PJ_TIP + PJ_TN) * sizeof(double2);
+    project_kernel<double><<<grid, PJ_THREADS, smem, pl->stream>>>(a);
+  }
+  g_launches++;
+  CK(cudaGetLastError());
 }
 
 static void launch_sampler(cudaStream_t st, SampleArgs& a, int sm_count) {
@@ -256,11 +292,23 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     uint32_t B = (uint32_t)std::max<size_t>(1, std::min<size_t>(U, pl->probs_budget / (nb * real)));
     DevBuf probs((size_t)B * nb * real, st), mass((size_t)B * 8, st), minv((size_t)B * 8, st);
     DevBuf nnz((size_t)U * 4, st);
+    const bool proj = progs[j - 1].d.result_kind == 3;
+    DevBuf vbuf;
+    if (proj) vbuf.alloc((size_t)B * progs[j - 1].d.proj_d * pl->elem, st);
     for (uint32_t s0 = 0; s0 < U; s0 += B) {
       const uint32_t nbatch = std::min(B, U - s0);
       log.begin(&stats->marg_ms[j - 1]);
-      launch_exec_any(pl, progs[j - 1], EXEC_MARGINAL, table_dev.as<LevelDev>(), kraus_dev, s0,
-                      nbatch, probs.p, mass.as<double>(), minv.as<double>());
+      if (proj) {
+        launch_exec_any(pl, progs[j - 1], EXEC_VECTOR, table_dev.as<LevelDev>(), kraus_dev, s0,
+                        nbatch, vbuf.p, nullptr, nullptr);
+        log.end();
+        log.begin(&stats->project_ms[j - 1]);
+        launch_project(pl, progs[j - 1], vbuf.p, table[1].ext, table[1].ext_rec,
+                       cur.eset.as<uint32_t>(), s0, nbatch, probs.p);
+      } else {
+        launch_exec_any(pl, progs[j - 1], EXEC_MARGINAL, table_dev.as<LevelDev>(), kraus_dev, s0,
+                        nbatch, probs.p, mass.as<double>(), minv.as<double>());
+      }
       log.end();
       stats->marg_launches[j - 1]++;
       SampleArgs sa;
@@ -269,8 +317,8 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       sa.slot_off = cur.slot_off.as<uint32_t>();
       sa.eset_id = cur.gid.as<uint32_t>();
       sa.rank = cur.rank.as<uint32_t>();
-      sa.mass = mass.as<double>();
-      sa.minv = minv.as<double>();
+      sa.mass = proj ? nullptr : mass.as<double>();
+      sa.minv = proj ? nullptr : minv.as<double>();
       sa.slot_index = slot_index.as<uint32_t>();
       sa.slot_count = slot_count.as<uint32_t>();
       sa.nnz = nnz.as<uint32_t>();
@@ -606,6 +654,8 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
         Program& pr = pl->programs[j - 1][p];
         pr.d = d->programs[k];
         if (pr.d.level != p + 1) throw Failure(PTSBE_EINVAL, "program level does not match its pass");
+        if (pr.d.result_kind == 3 && (p + 1 != j || j < 2 || pr.d.proj_d < 1))
+          throw Failure(PTSBE_EINVAL, "projection form is only valid for the marginal pass of a stage >= 2");
         if (pr.d.threads_per_item > 1024 || (pr.d.threads_per_item & 31))
           throw Failure(PTSBE_EINVAL, "threads_per_item must be a multiple of 32 up to 1024");
         pr.leaves.alloc(std::max<size_t>(16, (size_t)pr.d.n_leaves * LEAF_WORDS * 4), st);
@@ -695,8 +745,23 @@ int ptsbe_marginals(ptsbe_plan* pl, uint32_t stage, const uint8_t* kraus_idx,
           launch_exec_any(pl, progs[p], EXEC_HOIST, table_dev.as<LevelDev>(), kraus.as<uint8_t>(),
                           0, W, ext[p].p, nullptr, nullptr);
       DevBuf probs((size_t)W * nb * real, st), mass((size_t)W * 8, st), minv((size_t)W * 8, st);
-      launch_exec_any(pl, progs[j - 1], EXEC_MARGINAL, table_dev.as<LevelDev>(),
-                      kraus.as<uint8_t>(), 0, W, probs.p, mass.as<double>(), minv.as<double>());
+      if (progs[j - 1].d.result_kind == 3) {
+        DevBuf vbuf((size_t)W * progs[j - 1].d.proj_d * pl->elem, st);
+        launch_exec_any(pl, progs[j - 1], EXEC_VECTOR, table_dev.as<LevelDev>(), kraus.as<uint8_t>(),
+                        0, W, vbuf.p, nullptr, nullptr);
+        launch_project(pl, progs[j - 1], vbuf.p, table[1].ext, table[1].ext_rec, ident.as<uint32_t>(),
+                       0, W, probs.p);
+        if (pl->dtype == PTSBE_C64)
+          row_stats_kernel<float><<<cdiv((uint64_t)W * 32, 256), 256, 0, st>>>(
+              probs.as<float>(), W, nb, mass.as<double>(), minv.as<double>());
+        else
+          row_stats_kernel<double><<<cdiv((uint64_t)W * 32, 256), 256, 0, st>>>(
+              probs.as<double>(), W, nb, mass.as<double>(), minv.as<double>());
+        g_launches++;
+      } else {
+        launch_exec_any(pl, progs[j - 1], EXEC_MARGINAL, table_dev.as<LevelDev>(),
+                        kraus.as<uint8_t>(), 0, W, probs.p, mass.as<double>(), minv.as<double>());
+      }
       CK(cudaMemcpyAsync(host.data(), probs.p, (size_t)W * nb * real, cudaMemcpyDeviceToHost, st));
       if (out_mass) CK(cudaMemcpyAsync(out_mass + c0, mass.p, (size_t)W * 8, cudaMemcpyDeviceToHost, st));
       if (out_min) CK(cudaMemcpyAsync(out_min + c0, minv.p, (size_t)W * 8, cudaMemcpyDeviceToHost, st));
@@ -787,6 +852,7 @@ int ptsbe_sample_stage(uint32_t b, uint32_t stage, uint64_t seed, uint64_t n_ite
       sa.k0 = (uint32_t)seed;
       sa.k1 = (uint32_t)(seed >> 32);
       sa.is_f32 = 0;
+      sa.neg_abs = -1e-12;
       cudaDeviceProp prop;
       CK(cudaGetDeviceProperties(&prop, device));
       launch_sampler(st, sa, prop.multiProcessorCount);

@@ -31,7 +31,7 @@ struct LevelDev {
   uint32_t ext_rec;
 };
 
-enum ExecMode { EXEC_HOIST = 0, EXEC_MARGINAL = 1, EXEC_RAW = 2 };
+enum ExecMode { EXEC_HOIST = 0, EXEC_MARGINAL = 1, EXEC_RAW = 2, EXEC_VECTOR = 3 };
 
 struct ExecArgs {
   const uint32_t* leaves;
@@ -42,7 +42,7 @@ struct ExecArgs {
   const LevelDev* levels;
   void* spill;   // [resident groups][arena_spill]
   void* out;     // HOIST: records [level n][out_elems] ; MARGINAL: real probs [items][out_elems]
-                 // RAW: complex [items][out_elems]
+                 // RAW: complex [items][out_elems] ; VECTOR: complex [items of this launch][out_elems]
   double* out_mass;  // MARGINAL: [items]
   double* out_min;   // MARGINAL: [items]
   uint32_t n_steps;
@@ -140,7 +140,7 @@ __global__ void exec_kernel(const ExecArgs a) {
       const C* B = resolve(st[2], st[3]);
       C* O;
       if (st[4] == 0) O = st[5] < a.arena_fast ? arena + st[5] : spill + (st[5] - a.arena_fast);
-      else O = reinterpret_cast<C*>(a.out) + (size_t)item * a.out_elems + st[5];
+      else O = reinterpret_cast<C*>(a.out) + (size_t)(a.mode == EXEC_VECTOR ? it : item) * a.out_elems + st[5];
       const uint32_t out_n = st[6], kn = st[7], lo_n = st[8], hi_n = st[9];
       const uint32_t* loA = a.tables + st[10];
       const uint32_t* loB = loA + lo_n;
@@ -168,7 +168,7 @@ __global__ void exec_kernel(const ExecArgs a) {
     }
 
     // ---- epilogue ----
-    if (a.mode != EXEC_HOIST) {
+    if (a.mode == EXEC_MARGINAL || a.mode == EXEC_RAW) {
       const C* res = resolve(a.result_kind, a.result_ref);
       if (a.mode == EXEC_RAW) {
         C* o = reinterpret_cast<C*>(a.out) + (size_t)it * a.out_elems;

@@ -52,7 +52,7 @@ struct Problem {
   std::vector<uint32_t> cls;
   std::vector<double> logw;  // log class weight
   uint32_t n_labels;
-  double cap_log2;
+  std::vector<double> cap_log2;  // per class
 };
 
 struct Descent {
@@ -95,7 +95,8 @@ static Descent descend(const Problem& P, Rng& rng, double temperature) {
     // reference score: flops(step) - prod(shared dims), compared in log space
     const double score = std::max(0.0, std::exp2(std::min(lu, 1000.0)) - std::exp2(ls));
     double key = std::log1p(score) + P.logw[std::max(cls[x], cls[y])];
-    if (lo > P.cap_log2) key += 50.0 * (lo - P.cap_log2) + 100.0;
+    const double cap = P.cap_log2[std::max(cls[x], cls[y])];
+    if (lo > cap) key += 50.0 * (lo - cap) + 100.0;
     if (temperature > 0.0) {
       const double u = rng.uniform();
       key += temperature * -std::log(-std::log(u));
@@ -177,15 +178,15 @@ static Descent descend(const Problem& P, Rng& rng, double temperature) {
 
 extern "C" int ptsbe_plan_greedy(uint32_t n_ops, const uint32_t* op_ptr, const int64_t* labels,
                                  const uint32_t* dims, const uint32_t* op_class,
-                                 const double* class_weight, uint32_t n_classes,
-                                 uint32_t hypersamples, uint64_t seed, double size_cap_log2,
+                                 const double* class_weight, const double* class_cap_log2,
+                                 uint32_t n_classes, uint32_t hypersamples, uint64_t seed,
+                                 double size_cap_log2,
                                  uint32_t* merges_out, double* cost_out, double* flops_out) {
   if (n_ops < 1 || hypersamples < 1 || !op_ptr || !merges_out) return PTSBE_EINVAL;
   Problem P;
   P.n = n_ops;
   P.labels.resize(n_ops);
   P.cls.assign(n_ops, 0);
-  P.cap_log2 = size_cap_log2 > 0 ? size_cap_log2 : 1e9;
   // densify labels
   std::vector<int64_t> uniq(labels, labels + op_ptr[n_ops]);
   std::sort(uniq.begin(), uniq.end());
@@ -205,8 +206,11 @@ extern "C" int ptsbe_plan_greedy(uint32_t n_ops, const uint32_t* op_ptr, const i
   }
   uint32_t nc = std::max<uint32_t>(1, n_classes);
   P.logw.assign(nc, 0.0);
-  for (uint32_t c = 0; c < nc; ++c)
+  P.cap_log2.assign(nc, size_cap_log2 > 0 ? size_cap_log2 : 1e9);
+  for (uint32_t c = 0; c < nc; ++c) {
     if (class_weight) P.logw[c] = std::log(std::max(class_weight[c], 1e-300));
+    if (class_cap_log2 && class_cap_log2[c] > 0) P.cap_log2[c] = class_cap_log2[c];
+  }
   for (uint32_t t = 0; t < n_ops; ++t)
     if (P.cls[t] >= nc) return PTSBE_EINVAL;
   Rng rng(seed * 0x9E3779B97F4A7C15ull + 0x1234567ull);

@@ -46,7 +46,7 @@ struct SampleArgs {
   const uint32_t* slot_off; // [items] first output slot of the item (exclusive scan of mult)
   const uint32_t* eset_id;  // [items] GLOBAL error-set id (RNG stream)
   const uint32_t* rank;     // [items] rank of the prefix inside its error set (sorted order)
-  const double* mass;       // [items] or null
+  const double* mass;       // [items] or null: then sum / minimum are taken from the raw row here
   const double* minv;       // [items] or null
   uint32_t* slot_index;     // [total shots] outcome index of each non-empty child
   uint32_t* slot_count;     // [total shots] its count
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(const SampleArgs
   uint32_t* cnt = reinterpret_cast<uint32_t*>(cdf + nb);
   __shared__ uint64_t ws64[33];
   __shared__ uint32_t ws32[33];
-  __shared__ double redmax[SAMPLE_THREADS / 32];
+  __shared__ double redmax[SAMPLE_THREADS / 32], redmin[SAMPLE_THREADS / 32], redsum[SAMPLE_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t per = (nb + SAMPLE_THREADS - 1) / SAMPLE_THREADS;
 
@@ -82,31 +82,39 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(const SampleArgs
     const uint32_t m = a.mult[item];
     // ---- load (coalesced), clamp, max ----
     double* pd = reinterpret_cast<double*>(cdf);
-    double mx = 0.0;
+    double mx = 0.0, rawmin = 1e300, csum = 0.0;
     if (a.is_f32) {
       const float* p = reinterpret_cast<const float*>(a.probs) + it * nb;
       for (uint32_t k = tid; k < nb; k += SAMPLE_THREADS) {
-        double v = (double)p[k]; v = v > 0.0 ? v : 0.0; pd[k] = v; mx = fmax(mx, v);
+        double v = (double)p[k]; rawmin = fmin(rawmin, v);
+        v = v > 0.0 ? v : 0.0; pd[k] = v; mx = fmax(mx, v); csum += v;
       }
     } else {
       const double* p = reinterpret_cast<const double*>(a.probs) + it * nb;
       for (uint32_t k = tid; k < nb; k += SAMPLE_THREADS) {
-        double v = p[k]; v = v > 0.0 ? v : 0.0; pd[k] = v; mx = fmax(mx, v);
+        double v = p[k]; rawmin = fmin(rawmin, v);
+        v = v > 0.0 ? v : 0.0; pd[k] = v; mx = fmax(mx, v); csum += v;
       }
     }
     for (uint32_t k = tid; k < nb; k += SAMPLE_THREADS) cnt[k] = 0;
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
-    if (lane == 0) redmax[wid] = mx;
+    for (int d = 16; d > 0; d >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+      rawmin = fmin(rawmin, __shfl_xor_sync(0xffffffffu, rawmin, d));
+      csum += __shfl_xor_sync(0xffffffffu, csum, d);
+    }
+    if (lane == 0) { redmax[wid] = mx; redmin[wid] = rawmin; redsum[wid] = csum; }
     __syncthreads();
-    mx = redmax[0];
+    mx = redmax[0]; rawmin = redmin[0]; csum = redsum[0];
 #pragma unroll
-    for (int w = 1; w < SAMPLE_THREADS / 32; ++w) mx = fmax(mx, redmax[w]);
+    for (int w = 1; w < SAMPLE_THREADS / 32; ++w) {
+      mx = fmax(mx, redmax[w]); rawmin = fmin(rawmin, redmin[w]); csum += redsum[w];
+    }
 
     // ---- guards (engine.py:447-448, 475-476, 484-485) ----
     uint32_t bad = 0;
-    if (a.mass) {
-      const double ms = a.mass[it], mn = a.minv[it];
+    {
+      const double ms = a.mass ? a.mass[it] : csum, mn = a.minv ? a.minv[it] : rawmin;
       if (mn < a.neg_abs - a.neg_rel * ms) bad = PTSBE_ENUMERIC;
       else if (ms < a.vanish) bad = PTSBE_EIMPOSSIBLE;
     }

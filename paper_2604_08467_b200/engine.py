@@ -50,8 +50,8 @@ from .errors import (
     ResourceLimitError,
     SimulationError,
 )
-from .planner import PathCache, cache_lookup_or_plan
-from .tensor import DEFAULT_INTERMEDIATE_CEILING, Index, Tensor, TensorNetwork
+from .planner import PathCache, cache_lookup_or_plan, plan_stage
+from .tensor import DEFAULT_INTERMEDIATE_CEILING, Index, NetworkSignature, Tensor, TensorNetwork
 
 NEGATIVE_DIAG_TOLERANCE = -1e-12
 VANISHING_MASS = 1e-12
@@ -431,17 +431,69 @@ class VariantTables:
         return out
 
 
-def stage_operands(cnet: CircuitNetwork, plan: BatchPlan, j: int, tables: VariantTables):
-    """Static operand table of the stage-j sandwich, same operand order as
-    `marginal_network`.  Returns (operands, open label order)."""
+def _schmidt_split(data: np.ndarray, tol: float = 1e-12):
+    """Operator-Schmidt split of the variants of one two-qubit site.  `data` is
+    [variants, 16] over legs (out_c, out_t, in_c, in_t).  Returns
+    (A [variants, 4r] over (out_c, in_c, k), B [variants, 4r] over (k, out_t, in_t), r)
+    with r the largest Schmidt rank over the variants, or None when r == 4
+    (nothing to gain).  Controlled gates and RZZ have r = 2, and a Pauli (or
+    any product) error folded in by UPV does not raise it."""
+    nv = data.shape[0]
+    parts, rank = [], 1
+    for v in range(nv):
+        m = data[v].reshape(2, 2, 2, 2).transpose(0, 2, 1, 3).reshape(4, 4)
+        u, sv, vh = np.linalg.svd(m)
+        r = int(np.sum(sv > tol * max(sv[0], 1e-300)))
+        rank = max(rank, r)
+        parts.append((u, sv, vh))
+    if rank >= 4:
+        return None
+    a = np.zeros((nv, 4 * rank), dtype=np.complex128)
+    b = np.zeros((nv, 4 * rank), dtype=np.complex128)
+    for v, (u, sv, vh) in enumerate(parts):
+        root = np.sqrt(sv[:rank])
+        a[v] = (u[:, :rank] * root[None, :]).reshape(-1)        # (oc, ic, k)
+        b[v] = (root[:, None] * vh[:rank, :]).reshape(-1)       # (k, ot, it)
+    return a, b, rank
+
+
+def stage_operands(cnet: CircuitNetwork, plan: BatchPlan, j: int, tables: VariantTables,
+                   split: bool = False):
+    """Static operand table of the stage-j sandwich.  With split=False the
+    operand order is that of `marginal_network` (reference engine.py:392-406).
+    With split=True every two-qubit site whose variants all have operator-
+    Schmidt rank < 4 becomes two rank-3 operands joined by a bond of that rank
+    (both selected by the site's Kraus index): same values, but the network
+    exposes the true entanglement cut of controlled gates, which is what the
+    cut-based planner (planner.plan_stage) needs.  Returns (operands, open
+    label order)."""
     bra, fixed, opened = _stage_layout(cnet, plan, j)
     n_kets = len(cnet.net.operands) - tables.n_sites
+    fresh = 1 + max([lb for t in cnet.net.operands for lb in t.labels] + list(bra.values())
+                    + [o[3] for o in opened])
+    halves = {}
+    if split:
+        for site in range(tables.n_sites):
+            t = cnet.net.operands[n_kets + site]
+            if len(t.labels) == 4:
+                res = _schmidt_split(tables.data[site])
+                if res is not None:
+                    halves[site] = res + (fresh, fresh + 1)
+                    fresh += 2
     ops = []
     for conj in (False, True):
         for slot, t in enumerate(cnet.net.operands):
             labels = tuple(bra.get(lb, lb) for lb in t.labels) if conj else t.labels
             dims = tuple(ix.dim for ix in t.indices)
             site = slot - n_kets
+            if site >= 0 and site in halves:
+                a, b, r, k_ket, k_bra = halves[site]
+                kind = SEL_KRAUS if a.shape[0] > 1 else SEL_CONST
+                kl = k_bra if conj else k_ket
+                oc, ot, ic, it = labels
+                ops.append(Operand((oc, ic, kl), (2, 2, r), np.conj(a) if conj else a, kind, site, 0))
+                ops.append(Operand((kl, ot, it), (r, 2, 2), np.conj(b) if conj else b, kind, site, 0))
+                continue
             if site >= 0:
                 data, kind, arg = tables.data[site], SEL_KRAUS, site
                 if data.shape[0] == 1:
@@ -456,6 +508,23 @@ def stage_operands(cnet: CircuitNetwork, plan: BatchPlan, j: int, tables: Varian
     for _, ket_leg, bra_leg, open_leg in opened:
         ops.append(Operand((ket_leg, bra_leg, open_leg), (2, 2, 2), _COPY3.reshape(1, -1)))
     return ops, tuple(o[3] for o in opened)
+
+
+RECORD_CAP_LOG2 = 18.0  # entries of one hoisted record (per error set / per earlier-stage prefix)
+
+
+def _ops_signature(ops, opens) -> NetworkSignature:
+    """Value-independent fingerprint of a stage operand table, same fields as
+    the reference's network signature (tensor.py:155-187), so stored paths go
+    through the same PathCache and its JSON format."""
+    where: dict = {}
+    for slot, o in enumerate(ops):
+        for axis, lb in enumerate(o.labels):
+            where.setdefault(lb, []).append((slot, axis))
+    bonds = sorted(tuple(sorted(p)) for p in where.values() if len(p) == 2)
+    open_legs = sorted(p[0] for p in where.values() if len(p) == 1)
+    return NetworkSignature(num_operands=len(ops), shapes=tuple(tuple(o.dims) for o in ops),
+                            bonds=tuple(bonds), open_legs=tuple(open_legs))
 
 
 def _size_cap_log2(dtype: str) -> float:
@@ -484,18 +553,23 @@ class DevicePipeline:
             if j not in want:
                 programs += [_empty_program(p + 1, 1 << plan.sizes[j - 1] if p == j - 1 else 0) for p in range(j)]
                 continue
-            ops, opens = stage_operands(cnet, plan, j, tables)
-            mnet = marginal_network(cnet, plan, j, "0" * plan.offset(j))
+            ops, opens = stage_operands(cnet, plan, j, tables, split=True)
             # distinct instances of a class-k result: unique prefixes entering stage k+1
             weights = [float(min(shots_per_set, 2.0 ** min(plan.offset(k + 1), 60))) for k in range(j)]
+            sig = _ops_signature(ops, opens)
+            key = ("b200", j, round(math.log2(max(shots_per_set, 1.0))))
             t0 = time.perf_counter()
-            path, hit = cache_lookup_or_plan(
-                ctx.cache, mnet.net, stage=j, hypersamples=ctx.hypersamples,
-                rng=spawn_rng(ctx.planner_seed, _KEY_PLANNER, j),
-                op_class=[o.cls for o in ops], class_weight=weights,
-                size_cap_log2=_size_cap_log2(ctx.dtype),
-            )
-            if not hit:
+            path = ctx.cache.get(sig, key)
+            if path is not None:
+                ctx.cache.hits += 1
+            else:
+                path = plan_stage(
+                    [o.labels for o in ops], [o.dims for o in ops], [o.cls for o in ops],
+                    [o.sel_kind == SEL_PREFIX for o in ops], opens, weights,
+                    item_cap_log2=_size_cap_log2(ctx.dtype), record_cap_log2=RECORD_CAP_LOG2,
+                    hypersamples=ctx.hypersamples, rng=spawn_rng(ctx.planner_seed, _KEY_PLANNER, j))
+                ctx.cache.put(sig, key, path)
+                ctx.cache.misses += 1
                 ctx.stats.plan_events += 1
                 ctx.stats.path_seconds += time.perf_counter() - t0
             self.paths[j] = path

@@ -98,6 +98,7 @@ def find_path_greedy(
     op_class: Optional[Sequence[int]] = None,
     class_weight: Optional[Sequence[float]] = None,
     size_cap_log2: float = 0.0,
+    class_cap_log2: Optional[Sequence[float]] = None,
 ) -> ContractionPath:
     """Best of `hypersamples` randomized greedy descents (planner.py:212-251).
     `est_cost` is the reference flop estimate of the chosen path."""
@@ -121,8 +122,153 @@ def find_path_greedy(
         hypersamples=hypersamples,
         seed=seed,
         size_cap_log2=size_cap_log2,
+        class_cap_log2=class_cap_log2,
     )
     return ContractionPath(steps=merges_to_steps(n, merges), est_cost=float(flops))
+
+
+def _min_cut_source_side(n: int, edges, sources, sinks) -> tuple:
+    """Dinic max-flow on an undirected capacity graph; returns (cut value, set
+    of nodes on the source side of the min cut closest to the sources)."""
+    from collections import deque
+
+    src, dst = n, n + 1
+    graph = [[] for _ in range(n + 2)]
+
+    def add(u, v, c_uv, c_vu):
+        graph[u].append([v, c_uv, len(graph[v])])
+        graph[v].append([u, c_vu, len(graph[u]) - 1])
+
+    inf = 1 << 40
+    for u, v, c in edges:
+        add(u, v, c, c)
+    for x in sources:
+        add(src, x, inf, 0)
+    for x in sinks:
+        add(x, dst, inf, 0)
+    flow = 0
+    while True:
+        level = [-1] * (n + 2)
+        level[src] = 0
+        dq = deque([src])
+        while dq:
+            u = dq.popleft()
+            for v, c, _ in graph[u]:
+                if c > 0 and level[v] < 0:
+                    level[v] = level[u] + 1
+                    dq.append(v)
+        if level[dst] < 0:
+            break
+        it = [0] * (n + 2)
+        while True:  # iterative DFS for one augmenting path in the level graph
+            stack, found = [src], False
+            while stack:
+                u = stack[-1]
+                if u == dst:
+                    found = True
+                    break
+                adv = False
+                while it[u] < len(graph[u]):
+                    v, c, _ = graph[u][it[u]]
+                    if c > 0 and level[v] == level[u] + 1:
+                        stack.append(v)
+                        adv = True
+                        break
+                    it[u] += 1
+                if not adv:
+                    stack.pop()
+                    if stack:
+                        it[stack[-1]] += 1
+            if not found:
+                break
+            push = inf
+            for u in stack[:-1]:
+                push = min(push, graph[u][it[u]][1])
+            for u in stack[:-1]:
+                e = graph[u][it[u]]
+                e[1] -= push
+                graph[e[0]][e[2]][1] += push
+            flow += push
+            if flow >= inf:
+                return flow, set()
+    seen = {src}
+    dq = deque([src])
+    while dq:
+        u = dq.popleft()
+        for v, c, _ in graph[u]:
+            if c > 0 and v not in seen:
+                seen.add(v)
+                dq.append(v)
+    return flow, {u for u in seen if u < n}
+
+
+def plan_stage(op_labels, op_dims, op_class, op_is_prefix, open_labels, class_weight,
+               item_cap_log2: float, record_cap_log2: float, hypersamples: int = 100,
+               rng: Optional[np.random.Generator] = None) -> ContractionPath:
+    """Path for one stage network of the batched executor (north-star
+    subsystem 1: found once on the template, stored, replayed for every error
+    set and prefix).  Two candidates, the cheaper batch-weighted cost wins:
+
+    generic   class-weighted randomized greedy over the whole network
+              (csrc/planner.cpp);
+    cut       the operands are split by a minimum cut between the prefix
+              projectors (everything that varies per work item) and the open
+              batch legs.  The far side holds no projector, so it contracts
+              ONCE PER ERROR SET into a record M[cut legs, open legs]; the near
+              side contracts per work item into a vector v[cut legs]; the root
+              step P = v . M is a dense matrix product over all items of an
+              error set, which the executor runs as a GEMM (csrc/project.cuh).
+
+    Returns the path in the reference's slot-step convention (planner.py:34-54)
+    over the given operand order; est_cost is the plain flop estimate."""
+    from . import _capi
+
+    n = len(op_labels)
+    if n == 1:
+        return ContractionPath(steps=(), est_cost=0.0)
+    if rng is None:
+        rng = np.random.default_rng()
+    seed = int(rng.integers(0, 2**63 - 1))
+    n_cls = len(class_weight)
+    caps = [record_cap_log2] * (n_cls - 1) + [item_cap_log2]
+    if n_cls == 1:
+        caps = [record_cap_log2]
+    merges, wcost, flops = _capi.plan_greedy(op_labels, op_dims, op_class=op_class, class_weight=class_weight,
+                                             hypersamples=hypersamples, seed=seed, class_cap_log2=caps)
+    best = (wcost, merges, flops)
+    sources = [k for k in range(n) if op_is_prefix[k]]
+    opens = set(open_labels)
+    sinks = [k for k in range(n) if any(lb in opens for lb in op_labels[k])]
+    if sources and sinks and n_cls > 1:
+        owner: dict = {}
+        for k in range(n):
+            for lb, d in zip(op_labels[k], op_dims[k]):
+                owner.setdefault(lb, []).append((k, d))
+        # capacities in units of 1/64 bit so non-power-of-two bonds keep their order
+        edges = [(v[0][0], v[1][0], max(1, int(round(64 * math.log2(v[0][1])))))
+                 for v in owner.values() if len(v) == 2 and v[0][1] > 1]
+        cut, near = _min_cut_source_side(n, edges, sources, sinks)
+        log2_n = sum(math.log2(d) for k in range(n) for lb, d in zip(op_labels[k], op_dims[k]) if lb in opens)
+        far = [k for k in range(n) if k not in near]
+        if near and far and cut / 64.0 + log2_n <= record_cap_log2 and cut / 64.0 <= item_cap_log2:
+            gv = sorted(near)
+
+            def sub(ids, cw, cc):
+                if len(ids) == 1:
+                    return [], 0.0, 0.0
+                m, wc, fl = _capi.plan_greedy([op_labels[k] for k in ids], [op_dims[k] for k in ids],
+                                              op_class=[op_class[k] for k in ids], class_weight=cw,
+                                              hypersamples=hypersamples, seed=seed + 1, class_cap_log2=cc)
+                return [(ids[int(a)], ids[int(b)]) for a, b in m], wc, fl
+
+            mv, wv, fv = sub(gv, class_weight, caps)
+            mm, wm, fm = sub(far, class_weight, [record_cap_log2] * n_cls)
+            root = 2.0 ** (cut / 64.0 + log2_n)
+            total = wv + wm + root * class_weight[-1]
+            if total < best[0]:
+                joined = list(mv) + list(mm) + [(min(gv[0], far[0]), max(gv[0], far[0]))]
+                best = (total, np.asarray(joined, dtype=np.int64).reshape(-1, 2), fv + fm + root)
+    return ContractionPath(steps=merges_to_steps(n, best[1]), est_cost=float(best[2]))
 
 
 MAX_OPTIMAL_OPERANDS = 14

@@ -15,7 +15,7 @@ def run_stage(programs, pool, kraus_row, prefix_bits, dtype=np.complex128):
     result = None
     for p, pr in enumerate(programs):
         arena = np.zeros(pr.arena_fast + pr.arena_spill + 1, dtype=dtype)
-        rec = np.zeros(max(pr.out_elems, 1), dtype=dtype)
+        rec = np.zeros(max(pr.out_elems, pr.proj_d, 1), dtype=dtype)
 
         def resolve(kind, ref):
             if kind == 0:
@@ -52,6 +52,11 @@ def run_stage(programs, pool, kraus_row, prefix_bits, dtype=np.complex128):
                 rec[orf: orf + out_n] = val
         records[p] = rec
         if p == len(programs) - 1:
-            src, base = resolve(pr.result_kind, pr.result_ref)
-            result = np.array(src[base: base + pr.out_elems])
+            if pr.result_kind == 3:  # projection form: result = v . M, M in pass 0's record
+                d, n = pr.proj_d, pr.out_elems
+                m = records[0][pr.result_ref: pr.result_ref + d * n].reshape(d, n)
+                result = rec[:d] @ m
+            else:
+                src, base = resolve(pr.result_kind, pr.result_ref)
+                result = np.array(src[base: base + pr.out_elems])
     return result
