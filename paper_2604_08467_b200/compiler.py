@@ -270,7 +270,7 @@ def compile_stage(
         # sizing of the on-chip arena: try everything on chip, spill the big buffers otherwise
         max_out = max([nodes[nid].size for nid in mine], default=1)
         peak = _place(nodes, mine, rec_off, root, fast_cap=None)[1]
-        if max_out <= 128 and peak * elem_bytes <= WARP_ARENA_BYTES:
+        if max_out <= 512 and peak * elem_bytes <= WARP_ARENA_BYTES:
             threads, fast_cap = 32, peak
         else:
             threads = 64

@@ -36,6 +36,8 @@ struct Rng {  // splitmix64
   double uniform() { return ((next() >> 11) + 0.5) * (1.0 / 9007199254740992.0); }
 };
 
+constexpr double kStepOverheadMacs = 48.0;
+
 struct Cand {
   double key, tie;
   uint32_t x, y, vx, vy;
@@ -60,7 +62,7 @@ struct Descent {
   double weighted = 0, flops = 0;
 };
 
-static Descent descend(const Problem& P, Rng& rng, double temperature) {
+static Descent descend(const Problem& P, Rng& rng, double temperature, double gamma) {
   const uint32_t n = P.n;
   std::vector<std::vector<int32_t>> lab = P.labels;
   std::vector<uint32_t> cls = P.cls, version(n, 0);
@@ -94,7 +96,7 @@ static Descent descend(const Problem& P, Rng& rng, double temperature) {
     measure(x, y, lu, ls, lo);
     // reference score: flops(step) - prod(shared dims), compared in log space
     const double score = std::max(0.0, std::exp2(std::min(lu, 1000.0)) - std::exp2(ls));
-    double key = std::log1p(score) + P.logw[std::max(cls[x], cls[y])];
+    double key = std::log1p(score) + gamma * P.logw[std::max(cls[x], cls[y])];
     const double cap = P.cap_log2[std::max(cls[x], cls[y])];
     if (lo > cap) key += 50.0 * (lo - cap) + 100.0;
     if (temperature > 0.0) {
@@ -138,7 +140,9 @@ static Descent descend(const Problem& P, Rng& rng, double temperature) {
     const uint32_t c = std::max(cls[x], cls[y]);
     const double fl = std::exp2(std::min(lu, 1000.0));
     D.flops += fl;
-    D.weighted += fl * std::exp(P.logw[c]);
+    // every interpreted step costs the executor a fixed dispatch (table fetch, sync) on top of
+    // its multiply-adds
+    D.weighted += (fl + kStepOverheadMacs) * std::exp(P.logw[c]);
     merged.clear();
     std::set_symmetric_difference(lab[x].begin(), lab[x].end(), lab[y].begin(), lab[y].end(),
                                   std::back_inserter(merged));
@@ -216,9 +220,16 @@ extern "C" int ptsbe_plan_greedy(uint32_t n_ops, const uint32_t* op_ptr, const i
   Rng rng(seed * 0x9E3779B97F4A7C15ull + 0x1234567ull);
   Descent best;
   bool have = false;
+  // The search score is flops x weight^gamma.  gamma = 1 hoists as much as possible out of
+  // the per-item classes but lets nearly-free low-class merges run ahead and build blobs the
+  // per-item steps then have to chew through; gamma = 0 is the reference's plain greedy, which
+  // absorbs the rank-1 prefix projectors first and keeps per-item tensors tiny.  Every descent
+  // is judged by the true batch-weighted cost (gamma = 1), so the mix costs nothing.
+  static const double gammas[3] = {1.0, 0.5, 0.0};
   for (uint32_t h = 0; h < hypersamples; ++h) {
-    const double temperature = h == 0 ? 0.0 : (h % 3 == 0 ? 0.5 : 1.0);
-    Descent d = descend(P, rng, temperature);
+    const double gamma = gammas[h % 3];
+    const double temperature = h < 3 ? 0.0 : ((h / 3) % 2 ? 1.0 : 0.5);
+    Descent d = descend(P, rng, temperature, gamma);
     if (!have || d.weighted < best.weighted) { best = std::move(d); have = true; }
   }
   std::copy(best.merges.begin(), best.merges.end(), merges_out);
