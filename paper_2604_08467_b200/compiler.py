@@ -256,7 +256,7 @@ def compile_stage(
         nd = nodes[nid]
         if nd.parent >= 0 and nodes[nd.parent].pass_ > nd.pass_:
             rec_off[nid] = rec_size[nd.pass_]
-            rec_size[nd.pass_] += nd.size
+            rec_size[nd.pass_] += (nd.size + 3) & ~3  # 4-element granules keep vector loads aligned
     if proj is not None:
         rec_off[proj[0]] = 0  # v is the output record of the marginal pass
         rec_size[top] = nodes[proj[0]].size
@@ -271,7 +271,22 @@ def compile_stage(
         max_out = max([nodes[nid].size for nid in mine], default=1)
         peak = _place(nodes, mine, rec_off, root, fast_cap=None)[1]
         if max_out <= 512 and peak * elem_bytes <= WARP_ARENA_BYTES:
-            threads, fast_cap = 32, peak
+            # sub-warp groups: GS lanes per item, 32 / GS items per warp in lockstep.  Pick the
+            # group size with the fewest issued warp-instructions per item (rough model of
+            # csrc/executor.cuh: per step ~80, per output ~10, per multiply-add ~8).
+            def per_item(gs):
+                total = 0.0
+                for nid in mine:
+                    nd = nodes[nid]
+                    kn = 1
+                    la = set(nodes[nd.a].labels)
+                    for lb, d in zip(nodes[nd.b].labels, nodes[nd.b].dims):
+                        if lb in la:
+                            kn *= d
+                    total += 80 + -(-nd.size // gs) * (10 + 8 * kn)
+                return total * gs / 32.0
+            threads = min((8, 16, 32), key=per_item)
+            fast_cap = peak
         else:
             threads = 64
             while threads < 512 and threads * 4 < max_out:

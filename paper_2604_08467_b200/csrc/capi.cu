@@ -70,24 +70,27 @@ static ExecLaunch configure_exec(ptsbe_plan* pl, Program& pr, uint32_t n_items) 
   using C = typename CxT<R>::type;
   ExecLaunch L;
   const ptsbe_program_desc& d = pr.d;
-  size_t ib = (size_t)d.arena_fast_elems * sizeof(C) + (size_t)pl->words * 8 +
-              4ull * (d.level + 1) + pl->g;
+  size_t ib = (size_t)d.arena_fast_elems * sizeof(C) + (size_t)pl->words * 8 + 4ull * (d.level + 1);
   ib = (ib + 15) & ~size_t(15);
   L.item_bytes = (uint32_t)ib;
-  const bool warp = d.threads_per_item <= 32;
+  const uint32_t gs = d.threads_per_item;  // 8 / 16 / 32: sub-warp groups; larger: one CTA per item
+  const bool warp = gs <= 32;
   if (warp) {
-    uint32_t gpb = 8;
-    while (gpb > 1 && ib * gpb + 1024 > 227 * 1024) gpb >>= 1;
-    L.groups_per_block = gpb;
-    L.block = 32 * gpb;
+    uint32_t block = 256;
+    while (block > 32 && ib * (block / gs) + 1024 > 200 * 1024) block >>= 1;
+    L.groups_per_block = block / gs;
+    L.block = block;
   } else {
     L.groups_per_block = 1;
-    L.block = d.threads_per_item;
+    L.block = gs;
   }
   L.smem = ib * L.groups_per_block + 1024;
   if (L.smem > 227 * 1024)
     throw Failure(PTSBE_ERESOURCE, "stage program needs more shared memory than one SM has");
-  auto kern = warp ? exec_kernel<R, true> : exec_kernel<R, false>;
+  void (*kern)(ExecArgs) = gs == 8    ? exec_kernel<R, 8>
+                           : gs == 16 ? exec_kernel<R, 16>
+                           : gs == 32 ? exec_kernel<R, 32>
+                                      : exec_kernel<R, 0>;
   if (pr.blocks_per_sm == 0) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     int nb = 0;
@@ -103,7 +106,7 @@ static ExecLaunch configure_exec(ptsbe_plan* pl, Program& pr, uint32_t n_items) 
 template <typename R>
 static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelDev* levels_dev,
                         const uint8_t* kraus_dev, uint32_t first, uint32_t n_items, void* out,
-                        double* mass, double* minv) {
+                        double* mass, double* minv, uint32_t vec_stride) {
   using C = typename CxT<R>::type;
   if (n_items == 0) return;
   ExecLaunch L = configure_exec<R>(pl, pr, n_items);
@@ -135,28 +138,35 @@ static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelD
   a.words = pl->words;
   a.item_bytes = L.item_bytes;
   a.mode = mode;
-  if (pr.d.threads_per_item <= 32)
-    exec_kernel<R, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
-  else
-    exec_kernel<R, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  a.vec_stride = vec_stride;
+  const uint32_t gs = pr.d.threads_per_item;
+  if (gs == 8) exec_kernel<R, 8><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  else if (gs == 16) exec_kernel<R, 16><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  else if (gs == 32) exec_kernel<R, 32><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  else exec_kernel<R, 0><<<L.grid, L.block, L.smem, pl->stream>>>(a);
   g_launches++;
   CK(cudaGetLastError());
 }
 
 static void launch_exec_any(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelDev* lv,
                             const uint8_t* kraus, uint32_t first, uint32_t n, void* out,
-                            double* mass, double* minv) {
-  if (pl->dtype == PTSBE_C64) launch_exec<float>(pl, pr, mode, lv, kraus, first, n, out, mass, minv);
-  else launch_exec<double>(pl, pr, mode, lv, kraus, first, n, out, mass, minv);
+                            double* mass, double* minv, uint32_t vec_stride = 0) {
+  if (pl->dtype == PTSBE_C64)
+    launch_exec<float>(pl, pr, mode, lv, kraus, first, n, out, mass, minv, vec_stride);
+  else
+    launch_exec<double>(pl, pr, mode, lv, kraus, first, n, out, mass, minv, vec_stride);
 }
 
+static inline uint32_t vec_pitch(uint32_t n) { return (n + PJ_TI - 1) / PJ_TI * PJ_TI; }
+
 // P = Re(V . M) for the work items [first, first + n) of a level (project.cuh)
-static void launch_project(ptsbe_plan* pl, const Program& pr, const void* v, const void* rec0,
-                           uint32_t rec_stride, const uint32_t* eset, uint32_t first, uint32_t n,
-                           void* out) {
+static void launch_project(ptsbe_plan* pl, const Program& pr, const void* v, uint32_t v_stride,
+                           const void* rec0, uint32_t rec_stride, const uint32_t* eset,
+                           uint32_t first, uint32_t n, void* out) {
   if (n == 0) return;
   ProjectArgs a;
-  a.v = v;
+  a.vt = v;
+  a.v_stride = v_stride;
   a.rec0 = rec0;
   a.eset = eset;
   a.out = out;
@@ -175,10 +185,10 @@ static void launch_project(ptsbe_plan* pl, const Program& pr, const void* v, con
     attr_set = true;
   }
   if (pl->dtype == PTSBE_C64) {
-    const size_t smem = (size_t)ProjK<float>::KC * (PJ_TIP + PJ_TN) * sizeof(float2);
+    const size_t smem = (size_t)ProjK<float>::KC * (PJ_TI + PJ_TN) * sizeof(float2);
     project_kernel<float><<<grid, PJ_THREADS, smem, pl->stream>>>(a);
   } else {
-    const size_t smem = (size_t)ProjK<double>::KC * (PJ_TIP + PJ_TN) * sizeof(double2);
+    const size_t smem = (size_t)ProjK<double>::KC * (PJ_TI + PJ_TN) * sizeof(double2);
     project_kernel<double><<<grid, PJ_THREADS, smem, pl->stream>>>(a);
   }
   g_launches++;
@@ -294,16 +304,16 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     DevBuf nnz((size_t)U * 4, st);
     const bool proj = progs[j - 1].d.result_kind == 3;
     DevBuf vbuf;
-    if (proj) vbuf.alloc((size_t)B * progs[j - 1].d.proj_d * pl->elem, st);
+    if (proj) vbuf.alloc((size_t)vec_pitch(B) * progs[j - 1].d.proj_d * pl->elem, st);
     for (uint32_t s0 = 0; s0 < U; s0 += B) {
       const uint32_t nbatch = std::min(B, U - s0);
       log.begin(&stats->marg_ms[j - 1]);
       if (proj) {
         launch_exec_any(pl, progs[j - 1], EXEC_VECTOR, table_dev.as<LevelDev>(), kraus_dev, s0,
-                        nbatch, vbuf.p, nullptr, nullptr);
+                        nbatch, vbuf.p, nullptr, nullptr, vec_pitch(nbatch));
         log.end();
         log.begin(&stats->project_ms[j - 1]);
-        launch_project(pl, progs[j - 1], vbuf.p, table[1].ext, table[1].ext_rec,
+        launch_project(pl, progs[j - 1], vbuf.p, vec_pitch(nbatch), table[1].ext, table[1].ext_rec,
                        cur.eset.as<uint32_t>(), s0, nbatch, probs.p);
       } else {
         launch_exec_any(pl, progs[j - 1], EXEC_MARGINAL, table_dev.as<LevelDev>(), kraus_dev, s0,
@@ -656,8 +666,9 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
         if (pr.d.level != p + 1) throw Failure(PTSBE_EINVAL, "program level does not match its pass");
         if (pr.d.result_kind == 3 && (p + 1 != j || j < 2 || pr.d.proj_d < 1))
           throw Failure(PTSBE_EINVAL, "projection form is only valid for the marginal pass of a stage >= 2");
-        if (pr.d.threads_per_item > 1024 || (pr.d.threads_per_item & 31))
-          throw Failure(PTSBE_EINVAL, "threads_per_item must be a multiple of 32 up to 1024");
+        if (pr.d.threads_per_item > 1024 ||
+            ((pr.d.threads_per_item & 31) && pr.d.threads_per_item != 8 && pr.d.threads_per_item != 16))
+          throw Failure(PTSBE_EINVAL, "threads_per_item must be 8, 16 or a multiple of 32 up to 1024");
         pr.leaves.alloc(std::max<size_t>(16, (size_t)pr.d.n_leaves * LEAF_WORDS * 4), st);
         pr.steps.alloc(std::max<size_t>(16, (size_t)pr.d.n_steps * STEP_WORDS * 4), st);
         pr.tables.alloc(std::max<size_t>(16, (size_t)pr.d.n_table_words * 4), st);
@@ -746,11 +757,12 @@ int ptsbe_marginals(ptsbe_plan* pl, uint32_t stage, const uint8_t* kraus_idx,
                           0, W, ext[p].p, nullptr, nullptr);
       DevBuf probs((size_t)W * nb * real, st), mass((size_t)W * 8, st), minv((size_t)W * 8, st);
       if (progs[j - 1].d.result_kind == 3) {
-        DevBuf vbuf((size_t)W * progs[j - 1].d.proj_d * pl->elem, st);
+        DevBuf vbuf((size_t)vec_pitch(W) * progs[j - 1].d.proj_d * pl->elem, st);
+        CK(cudaMemsetAsync(vbuf.p, 0, vbuf.bytes, st));
         launch_exec_any(pl, progs[j - 1], EXEC_VECTOR, table_dev.as<LevelDev>(), kraus.as<uint8_t>(),
-                        0, W, vbuf.p, nullptr, nullptr);
-        launch_project(pl, progs[j - 1], vbuf.p, table[1].ext, table[1].ext_rec, ident.as<uint32_t>(),
-                       0, W, probs.p);
+                        0, W, vbuf.p, nullptr, nullptr, vec_pitch(W));
+        launch_project(pl, progs[j - 1], vbuf.p, vec_pitch(W), table[1].ext, table[1].ext_rec,
+                       ident.as<uint32_t>(), 0, W, probs.p);
         if (pl->dtype == PTSBE_C64)
           row_stats_kernel<float><<<cdiv((uint64_t)W * 32, 256), 256, 0, st>>>(
               probs.as<float>(), W, nb, mass.as<double>(), minv.as<double>());

@@ -2,11 +2,13 @@
 //
 // One launch runs ONE compiled pass program (see include/ptsbe_b200.h) for a
 // batch of work items (error set x measured prefix).  A work item is handled
-// by one warp (small programs) or one CTA; every intermediate tensor of the
-// path lives in that group's shared-memory arena, so the only HBM traffic of a
-// work item is its Kraus-index row, its prefix words, the (L1/L2-resident)
-// program tables and operand pool, and the final record.  Buffers that the
-// compiler could not fit on chip are placed in a per-group global spill arena.
+// by a group of GS lanes (GS = 8, 16 or 32: 4, 2 or 1 items per warp, all
+// running the same step list in lockstep) or by one CTA; every intermediate
+// tensor of the path lives in that group's shared-memory arena, so the only
+// HBM traffic of a work item is its Kraus-index row, its prefix words, the
+// (L1/L2-resident) program tables and operand pool, records of earlier passes
+// and the final record.  Buffers that the compiler could not fit on chip are
+// placed in a per-group global spill arena.
 //
 // Replaces, per work item: merge_errors (engine.py:284-313, as a table
 // gather), marginal_network (engine.py:361-407, static operand table),
@@ -42,7 +44,8 @@ struct ExecArgs {
   const LevelDev* levels;
   void* spill;   // [resident groups][arena_spill]
   void* out;     // HOIST: records [level n][out_elems] ; MARGINAL: real probs [items][out_elems]
-                 // RAW: complex [items][out_elems] ; VECTOR: complex [items of this launch][out_elems]
+                 // RAW: complex [items][out_elems]
+                 // VECTOR: complex, TRANSPOSED [out_elems][vec_stride] (column = item of this launch)
   double* out_mass;  // MARGINAL: [items]
   double* out_min;   // MARGINAL: [items]
   uint32_t n_steps;
@@ -57,6 +60,7 @@ struct ExecArgs {
   uint32_t words;
   uint32_t item_bytes;  // shared-memory footprint of one group
   uint32_t mode;
+  uint32_t vec_stride;  // VECTOR: row pitch (items, padded) of the transposed output
 };
 
 template <typename R> struct CxT;
@@ -71,17 +75,47 @@ __device__ __forceinline__ void cmac(C& acc, const C a, const C b) {
   acc.y = fma(a.y, b.x, acc.y);
 }
 
-// WARP = true : blockDim.x = 32 * groups, one warp per item, __syncwarp between steps
-// WARP = false: one CTA per item, __syncthreads between steps
-template <typename R, bool WARP>
+struct StepTables {
+  const uint32_t *loA, *loB, *hiA, *hiB, *kA, *kB;
+  uint32_t out_n, lo_n, hi_n;
+};
+
+// inner product over KN shared labels with the k-offsets held in registers
+template <typename C, int KN>
+__device__ __forceinline__ void step_fixed_k(const C* __restrict__ A, const C* __restrict__ B, C* O,
+                                             size_t o_stride, const StepTables& t, int tid,
+                                             int gsize, bool store) {
+  uint32_t ka[KN], kb[KN];
+#pragma unroll
+  for (int k = 0; k < KN; ++k) { ka[k] = __ldg(t.kA + k); kb[k] = __ldg(t.kB + k); }
+  const int sh = 31 - __clz(t.lo_n);
+  const bool pow2 = (t.lo_n & (t.lo_n - 1)) == 0;
+  for (uint32_t c = tid; c < t.out_n; c += gsize) {
+    uint32_t cl, ch;
+    if (pow2) { cl = c & (t.lo_n - 1); ch = c >> sh; }
+    else { ch = c / t.lo_n; cl = c - ch * t.lo_n; }
+    uint32_t a0 = __ldg(t.loA + cl), b0 = __ldg(t.loB + cl);
+    if (t.hi_n > 1) { a0 += __ldg(t.hiA + ch); b0 += __ldg(t.hiB + ch); }
+    C acc; acc.x = 0; acc.y = 0;
+#pragma unroll
+    for (int k = 0; k < KN; ++k) cmac(acc, A[a0 + ka[k]], B[b0 + kb[k]]);
+    if (store) O[(size_t)c * o_stride] = acc;
+  }
+}
+
+// GS > 0 : sub-warp mapping, GS lanes per item, 32 / GS items per warp, __syncwarp between steps
+// GS == 0: one CTA per item, __syncthreads between steps
+template <typename R, int GS>
 __global__ void exec_kernel(const ExecArgs a) {
   using C = typename CxT<R>::type;
+  constexpr bool WARP = GS > 0;
+  constexpr int GSD = GS > 0 ? GS : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
 
-  const int gsize = WARP ? 32 : blockDim.x;
-  const int tid = WARP ? (threadIdx.x & 31) : threadIdx.x;
-  const int group_in_block = WARP ? (threadIdx.x >> 5) : 0;
-  const int groups_per_block = WARP ? (blockDim.x >> 5) : 1;
+  const int gsize = WARP ? GS : blockDim.x;
+  const int tid = WARP ? (threadIdx.x & (GSD - 1)) : threadIdx.x;
+  const int group_in_block = WARP ? (threadIdx.x / GSD) : 0;
+  const int groups_per_block = WARP ? (blockDim.x / GSD) : 1;
   const uint32_t group_global = blockIdx.x * groups_per_block + group_in_block;
   const uint32_t n_groups = gridDim.x * groups_per_block;
 
@@ -89,7 +123,6 @@ __global__ void exec_kernel(const ExecArgs a) {
   C* arena = reinterpret_cast<C*>(my);
   uint64_t* pfx = reinterpret_cast<uint64_t*>(my + (size_t)a.arena_fast * sizeof(C));
   uint32_t* anc = reinterpret_cast<uint32_t*>(pfx + a.words);
-  uint8_t* sel = reinterpret_cast<uint8_t*>(anc + (a.level + 1));
   C* spill = reinterpret_cast<C*>(a.spill) + (size_t)group_global * a.arena_spill;
   const C* pool = reinterpret_cast<const C*>(a.pool);
   // scratch for CTA-wide reductions (marginal epilogue), placed after the groups
@@ -99,7 +132,13 @@ __global__ void exec_kernel(const ExecArgs a) {
     if (WARP) __syncwarp(); else __syncthreads();
   };
 
-  for (uint32_t it = group_global; it < a.n_items; it += n_groups) {
+  // every group of a warp runs the same number of rounds (lockstep __syncwarp): groups past
+  // the end redo the last item with their stores to global memory masked off
+  const uint32_t rounds = (a.n_items + n_groups - 1) / n_groups;
+  for (uint32_t r = 0; r < rounds; ++r) {
+    uint32_t it = r * n_groups + group_global;
+    const bool live = it < a.n_items;
+    if (!live) it = a.n_items - 1;
     const uint32_t item = a.first_item + it;
     // ---- item context: ancestors, prefix words, Kraus-index row ----
     if (tid == 0) {
@@ -113,20 +152,17 @@ __global__ void exec_kernel(const ExecArgs a) {
     const LevelDev lv = a.levels[a.level];
     const uint32_t e = lv.eset[item];
     for (uint32_t w = tid; w < a.words; w += gsize) pfx[w] = lv.prefix[(size_t)w * lv.n + item];
-    {
-      const uint8_t* row = a.kraus + (size_t)e * a.g;
-      for (uint32_t s = tid; s < a.g; s += gsize) sel[s] = row[s];
-    }
+    const uint8_t* sel = a.kraus + (size_t)e * a.g;  // Kraus-index row: shared by all items of the error set (L1/L2)
     group_sync();
 
     auto resolve = [&](uint32_t kind, uint32_t ref) -> const C* {
       if (kind == 0) return ref < a.arena_fast ? arena + ref : spill + (ref - a.arena_fast);
       if (kind == 1) {
-        const uint32_t* lf = a.leaves + (size_t)ref * LEAF_WORDS;
+        const uint4 lf = __ldg(reinterpret_cast<const uint4*>(a.leaves) + ref);
         uint32_t v = 0;
-        if (lf[2] == 1) v = sel[lf[3]];
-        else if (lf[2] == 2) v = (uint32_t)((pfx[lf[3] >> 6] >> (63 - (lf[3] & 63))) & 1ull);
-        return pool + lf[0] + (size_t)v * lf[1];
+        if (lf.z == 1) v = __ldg(sel + lf.w);
+        else if (lf.z == 2) v = (uint32_t)((pfx[lf.w >> 6] >> (63 - (lf.w & 63))) & 1ull);
+        return pool + lf.x + (size_t)v * lf.y;
       }
       const uint32_t l = kind - 1;  // pass p = kind-2 iterates level p+1
       const LevelDev el = a.levels[l];
@@ -135,34 +171,54 @@ __global__ void exec_kernel(const ExecArgs a) {
 
     // ---- replay the stored path ----
     for (uint32_t s = 0; s < a.n_steps; ++s) {
-      const uint32_t* st = a.steps + (size_t)s * STEP_WORDS;
-      const C* A = resolve(st[0], st[1]);
-      const C* B = resolve(st[2], st[3]);
+      const uint4* st4 = reinterpret_cast<const uint4*>(a.steps + (size_t)s * STEP_WORDS);
+      // s0 = {a_kind, a_ref, b_kind, b_ref}, s1 = {o_kind, o_ref, out_n, k_n}, s2 = {lo_n, hi_n, tab_off, -}
+      const uint4 s0 = __ldg(st4), s1 = __ldg(st4 + 1), s2 = __ldg(st4 + 2);
+      const C* A = resolve(s0.x, s0.y);
+      const C* B = resolve(s0.z, s0.w);
       C* O;
-      if (st[4] == 0) O = st[5] < a.arena_fast ? arena + st[5] : spill + (st[5] - a.arena_fast);
-      else O = reinterpret_cast<C*>(a.out) + (size_t)(a.mode == EXEC_VECTOR ? it : item) * a.out_elems + st[5];
-      const uint32_t out_n = st[6], kn = st[7], lo_n = st[8], hi_n = st[9];
-      const uint32_t* loA = a.tables + st[10];
-      const uint32_t* loB = loA + lo_n;
-      const uint32_t* hiA = loB + lo_n;
-      const uint32_t* hiB = hiA + hi_n;
-      const uint32_t* kA = hiB + hi_n;
-      const uint32_t* kB = kA + kn;
-      const bool pow2 = (lo_n & (lo_n - 1)) == 0;
-      const int sh = 31 - __clz(lo_n);
-      for (uint32_t c = tid; c < out_n; c += gsize) {
-        uint32_t cl, ch;
-        if (pow2) { cl = c & (lo_n - 1); ch = c >> sh; }
-        else { ch = c / lo_n; cl = c - ch * lo_n; }
-        uint32_t a0 = __ldg(loA + cl), b0 = __ldg(loB + cl);
-        if (hi_n > 1) { a0 += __ldg(hiA + ch); b0 += __ldg(hiB + ch); }
-        C acc; acc.x = 0; acc.y = 0;
-        if (kn == 1) {
-          cmac(acc, A[a0], B[b0]);
-        } else {
-          for (uint32_t k = 0; k < kn; ++k) cmac(acc, A[a0 + __ldg(kA + k)], B[b0 + __ldg(kB + k)]);
+      size_t o_stride = 1;
+      bool store = true;
+      if (s1.x == 0) {
+        O = s1.y < a.arena_fast ? arena + s1.y : spill + (s1.y - a.arena_fast);
+      } else if (a.mode == EXEC_VECTOR) {
+        O = reinterpret_cast<C*>(a.out) + (size_t)s1.y * a.vec_stride + it;
+        o_stride = a.vec_stride;
+        store = live;
+      } else {
+        O = reinterpret_cast<C*>(a.out) + (size_t)item * a.out_elems + s1.y;
+        store = live;
+      }
+      StepTables t;
+      t.out_n = s1.z;
+      t.lo_n = s2.x;
+      t.hi_n = s2.y;
+      const uint32_t kn = s1.w;
+      t.loA = a.tables + s2.z;
+      t.loB = t.loA + t.lo_n;
+      t.hiA = t.loB + t.lo_n;
+      t.hiB = t.hiA + t.hi_n;
+      t.kA = t.hiB + t.hi_n;
+      t.kB = t.kA + kn;
+      switch (kn) {
+        case 1: step_fixed_k<C, 1>(A, B, O, o_stride, t, tid, gsize, store); break;
+        case 2: step_fixed_k<C, 2>(A, B, O, o_stride, t, tid, gsize, store); break;
+        case 4: step_fixed_k<C, 4>(A, B, O, o_stride, t, tid, gsize, store); break;
+        case 8: step_fixed_k<C, 8>(A, B, O, o_stride, t, tid, gsize, store); break;
+        default: {
+          const bool pow2 = (t.lo_n & (t.lo_n - 1)) == 0;
+          const int sh = 31 - __clz(t.lo_n);
+          for (uint32_t c = tid; c < t.out_n; c += gsize) {
+            uint32_t cl, ch;
+            if (pow2) { cl = c & (t.lo_n - 1); ch = c >> sh; }
+            else { ch = c / t.lo_n; cl = c - ch * t.lo_n; }
+            uint32_t a0 = __ldg(t.loA + cl), b0 = __ldg(t.loB + cl);
+            if (t.hi_n > 1) { a0 += __ldg(t.hiA + ch); b0 += __ldg(t.hiB + ch); }
+            C acc; acc.x = 0; acc.y = 0;
+            for (uint32_t k = 0; k < kn; ++k) cmac(acc, A[a0 + __ldg(t.kA + k)], B[b0 + __ldg(t.kB + k)]);
+            if (store) O[(size_t)c * o_stride] = acc;
+          }
         }
-        O[c] = acc;
       }
       group_sync();
     }
@@ -172,7 +228,8 @@ __global__ void exec_kernel(const ExecArgs a) {
       const C* res = resolve(a.result_kind, a.result_ref);
       if (a.mode == EXEC_RAW) {
         C* o = reinterpret_cast<C*>(a.out) + (size_t)it * a.out_elems;
-        for (uint32_t c = tid; c < a.out_elems; c += gsize) o[c] = res[c];
+        if (live)
+          for (uint32_t c = tid; c < a.out_elems; c += gsize) o[c] = res[c];
       } else {
         // real part, minimum before clamping, clamp, mass (engine.py:445-450)
         R* o = reinterpret_cast<R*>(a.out) + (size_t)it * a.out_elems;
@@ -182,20 +239,21 @@ __global__ void exec_kernel(const ExecArgs a) {
           mn = fmin(mn, (double)v);
           v = v > R(0) ? v : R(0);
           sum += (double)v;
-          o[c] = v;
+          if (live) o[c] = v;
         }
+        constexpr int RED = WARP ? GSD : 32;
 #pragma unroll
-        for (int d = 16; d > 0; d >>= 1) {
+        for (int d = RED / 2; d > 0; d >>= 1) {
           mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, d));
           sum += __shfl_xor_sync(0xffffffffu, sum, d);
         }
         if (WARP) {
-          if (tid == 0) { a.out_mass[it] = sum; a.out_min[it] = mn; }
+          if (tid == 0 && live) { a.out_mass[it] = sum; a.out_min[it] = mn; }
         } else {
           const int wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
           if ((threadIdx.x & 31) == 0) { red[2 * wid] = mn; red[2 * wid + 1] = sum; }
           __syncthreads();
-          if (threadIdx.x == 0) {
+          if (threadIdx.x == 0 && live) {
             for (int w = 1; w < nw; ++w) { mn = fmin(mn, red[2 * w]); sum += red[2 * w + 1]; }
             a.out_mass[it] = sum;
             a.out_min[it] = mn;

@@ -25,49 +25,57 @@
 namespace ptsbe {
 
 struct ProjectArgs {
-  const void* v;          // [n_items][D] complex, indexed by item - first_item
+  const void* vt;         // [D][v_stride] complex, TRANSPOSED: column = item - first_item
   const void* rec0;       // pass-0 records: [error sets][rec_stride] complex
   const uint32_t* eset;   // [level n] error-set row of every item
   void* out;              // [n_items][N] real, raw (unclamped)
   uint32_t first_item, n_items;
   uint32_t D, N;
+  uint32_t v_stride;      // row pitch of vt in elements (multiple of 2)
   uint32_t rec_stride;    // elements per error-set record
   uint32_t m_off;         // offset of M inside the record
 };
 
 constexpr int PJ_TI = 64;    // items per tile
-constexpr int PJ_TIP = PJ_TI + 1;  // padded row of the transposed V chunk (bank-conflict-free stores)
 constexpr int PJ_TN = 128;   // columns per tile
 constexpr int PJ_THREADS = 256;
-constexpr int PJ_RI = 4;     // items per thread
-constexpr int PJ_RN = 8;     // columns per thread
+constexpr int PJ_RI = 4;     // items per thread (consecutive)
+constexpr int PJ_RN = 8;     // columns per thread: 4 pairs, pair p at columns 2 * (p * 16 + tn) + {0, 1}
 
 template <typename R> struct ProjK { static constexpr int KC = 32; };
 template <> struct ProjK<double> { static constexpr int KC = 16; };
 
-// smem: Vs[KC][TI] complex (k-major), Ms[KC][TN] complex
+template <typename R> struct Cx2;  // two complex numbers, one 16/32-byte load
+template <> struct Cx2<float> { using type = float4; };
+template <> struct Cx2<double> { using type = double4; };
+
+// Both operands are k-major (vt[d][item], M[d][c]), so the tiles go to shared memory with
+// straight, coalesced, conflict-free vector copies: Vs[KC][TI], Ms[KC][TN].  A warp is
+// 2 (item groups) x 16 (column groups): the V reads of a k are two broadcasts, the M reads
+// are 16 consecutive pairs -> no bank conflicts on either side.
 template <typename R>
 __global__ void __launch_bounds__(PJ_THREADS) project_kernel(const ProjectArgs a) {
   using C = typename CxT<R>::type;
+  using C2 = typename Cx2<R>::type;
   constexpr int KC = ProjK<R>::KC;
-  extern __shared__ __align__(16) unsigned char pj_smem[];
+  extern __shared__ __align__(32) unsigned char pj_smem[];
   C* Vs = reinterpret_cast<C*>(pj_smem);
-  C* Ms = Vs + KC * PJ_TIP;
+  C* Ms = Vs + KC * PJ_TI;
   const int tid = threadIdx.x;
   const int tn = tid & 15, ti = tid >> 4;  // 16 x 16 thread grid
   const uint32_t n_tiles_i = (a.n_items + PJ_TI - 1) / PJ_TI;
   const uint32_t n_tiles_n = (a.N + PJ_TN - 1) / PJ_TN;
-  const C* V = reinterpret_cast<const C*>(a.v);
+  const C* VT = reinterpret_cast<const C*>(a.vt);
   const C* REC = reinterpret_cast<const C*>(a.rec0);
   R* OUT = reinterpret_cast<R*>(a.out);
 
   for (uint32_t tile = blockIdx.x; tile < n_tiles_i * n_tiles_n; tile += gridDim.x) {
-    // column tiles of one item tile are adjacent in the schedule: V stays in L1/L2
+    // column tiles of one item tile are adjacent in the schedule: its V columns stay in L1/L2
     const uint32_t it0 = (tile / n_tiles_n) * PJ_TI, c0 = (tile % n_tiles_n) * PJ_TN;
     const uint32_t ni = min((uint32_t)PJ_TI, a.n_items - it0);
     const uint32_t e_first = a.eset[a.first_item + it0], e_last = a.eset[a.first_item + it0 + ni - 1];
     if (e_first == e_last) {
-      // ---- uniform tile: one M for all items, tiles staged in shared memory ----
+      // ---- uniform tile: one M for all items ----
       const C* M = REC + (size_t)e_first * a.rec_stride + a.m_off;
       R acc[PJ_RI][PJ_RN];
 #pragma unroll
@@ -76,28 +84,44 @@ __global__ void __launch_bounds__(PJ_THREADS) project_kernel(const ProjectArgs a
         for (int j = 0; j < PJ_RN; ++j) acc[i][j] = R(0);
       for (uint32_t k0 = 0; k0 < a.D; k0 += KC) {
         __syncthreads();
-        // V chunk: global [item][d] -> smem [k][item]
-        for (int x = tid; x < KC * PJ_TI; x += PJ_THREADS) {
-          const int k = x % KC, i = x / KC;
-          C val; val.x = 0; val.y = 0;
-          if ((uint32_t)i < ni && k0 + k < a.D) val = V[(size_t)(it0 + i) * a.D + k0 + k];
-          Vs[k * PJ_TIP + i] = val;
+        // V chunk: rows k0.., columns it0.. (v_stride is padded, so the tail columns exist)
+        for (int x = tid; x < KC * PJ_TI / 2; x += PJ_THREADS) {
+          const int k = x / (PJ_TI / 2), i2 = x % (PJ_TI / 2);
+          C2 val = {};
+          if (k0 + k < a.D)
+            val = *reinterpret_cast<const C2*>(VT + (size_t)(k0 + k) * a.v_stride + it0 + 2 * i2);
+          *reinterpret_cast<C2*>(Vs + k * PJ_TI + 2 * i2) = val;
         }
-        // M chunk: global [d][c] -> smem [k][c]
-        for (int x = tid; x < KC * PJ_TN; x += PJ_THREADS) {
-          const int c = x % PJ_TN, k = x / PJ_TN;
-          C val; val.x = 0; val.y = 0;
-          if (c0 + c < a.N && k0 + k < a.D) val = M[(size_t)(k0 + k) * a.N + c0 + c];
-          Ms[k * PJ_TN + c] = val;
+        // M chunk
+        if (c0 + PJ_TN <= a.N && (a.N & 1) == 0 && (((size_t)e_first * a.rec_stride + a.m_off) & 1) == 0) {
+          for (int x = tid; x < KC * PJ_TN / 2; x += PJ_THREADS) {
+            const int k = x / (PJ_TN / 2), c2 = x % (PJ_TN / 2);
+            C2 val = {};
+            if (k0 + k < a.D) val = *reinterpret_cast<const C2*>(M + (size_t)(k0 + k) * a.N + c0 + 2 * c2);
+            *reinterpret_cast<C2*>(Ms + k * PJ_TN + 2 * c2) = val;
+          }
+        } else {
+          for (int x = tid; x < KC * PJ_TN; x += PJ_THREADS) {
+            const int k = x / PJ_TN, c = x % PJ_TN;
+            C val; val.x = 0; val.y = 0;
+            if (c0 + c < a.N && k0 + k < a.D) val = M[(size_t)(k0 + k) * a.N + c0 + c];
+            Ms[k * PJ_TN + c] = val;
+          }
         }
         __syncthreads();
 #pragma unroll 4
         for (int k = 0; k < KC; ++k) {
           C vr[PJ_RI], mr[PJ_RN];
 #pragma unroll
-          for (int i = 0; i < PJ_RI; ++i) vr[i] = Vs[k * PJ_TIP + ti * PJ_RI + i];
+          for (int i = 0; i < PJ_RI; i += 2) {
+            const C2 v2 = *reinterpret_cast<const C2*>(Vs + k * PJ_TI + ti * PJ_RI + i);
+            vr[i].x = v2.x; vr[i].y = v2.y; vr[i + 1].x = v2.z; vr[i + 1].y = v2.w;
+          }
 #pragma unroll
-          for (int j = 0; j < PJ_RN; ++j) mr[j] = Ms[k * PJ_TN + tn * PJ_RN + j];
+          for (int p = 0; p < PJ_RN / 2; ++p) {
+            const C2 m2 = *reinterpret_cast<const C2*>(Ms + k * PJ_TN + 2 * (p * 16 + tn));
+            mr[2 * p].x = m2.x; mr[2 * p].y = m2.y; mr[2 * p + 1].x = m2.z; mr[2 * p + 1].y = m2.w;
+          }
 #pragma unroll
           for (int i = 0; i < PJ_RI; ++i)
 #pragma unroll
@@ -112,9 +136,11 @@ __global__ void __launch_bounds__(PJ_THREADS) project_kernel(const ProjectArgs a
         const uint32_t item = it0 + ti * PJ_RI + i;
         if (item >= a.n_items) continue;
 #pragma unroll
-        for (int j = 0; j < PJ_RN; ++j) {
-          const uint32_t c = c0 + tn * PJ_RN + j;
-          if (c < a.N) OUT[(size_t)item * a.N + c] = acc[i][j];
+        for (int p = 0; p < PJ_RN / 2; ++p) {
+          const uint32_t c = c0 + 2 * (p * 16 + tn);
+          R* o = OUT + (size_t)item * a.N + c;
+          if (c + 1 < a.N) { o[0] = acc[i][2 * p]; o[1] = acc[i][2 * p + 1]; }
+          else if (c < a.N) o[0] = acc[i][2 * p];
         }
       }
     } else {
@@ -124,10 +150,9 @@ __global__ void __launch_bounds__(PJ_THREADS) project_kernel(const ProjectArgs a
         if (c >= a.N) continue;
         const uint32_t item = it0 + i;
         const C* M = REC + (size_t)a.eset[a.first_item + item] * a.rec_stride + a.m_off;
-        const C* vi = V + (size_t)item * a.D;
         R s = R(0);
         for (uint32_t d = 0; d < a.D; ++d) {
-          const C v = vi[d], m = M[(size_t)d * a.N + c];
+          const C v = VT[(size_t)d * a.v_stride + item], m = M[(size_t)d * a.N + c];
           s = fma(v.x, m.x, s);
           s = fma(-v.y, m.y, s);
         }
