@@ -31,7 +31,7 @@ from .errors import CapacityError, IncompletePathError, NetworkStructureError, R
 SEL_CONST, SEL_KRAUS, SEL_PREFIX = 0, 1, 2
 STEP_WORDS, LEAF_WORDS = 12, 4
 LO_TABLE_MAX = 1024          # entries in the per-lane (low) gather table of a step
-SMEM_BYTES = 200 * 1024      # shared memory a single work item may claim
+SMEM_BYTES = 52 * 1024       # shared-memory arena of a CTA-per-item program: 4 CTAs per SM stay resident
 WARP_ARENA_BYTES = 6 * 1024  # beyond this a warp-per-item mapping starves occupancy
 
 

@@ -22,6 +22,7 @@ namespace ptsbe {
 
 thread_local std::string g_last_error;
 thread_local uint64_t g_launches = 0;
+thread_local Workspace* g_ws = nullptr;
 
 struct Program {
   ptsbe_program_desc d;
@@ -228,7 +229,7 @@ struct RunOutput {
 static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* shots_dev,
                       const uint32_t* ids_dev, uint32_t ne, uint64_t chunk_shots, uint64_t seed,
                       RunOutput& out, ptsbe_run_stats* stats, unsigned long long* flag_dev,
-                      uint32_t* flag_count_dev) {
+                      uint32_t* flag_count_dev, Workspace& ws_out) {
   cudaStream_t st = pl->stream;
   const uint32_t f = pl->f, words = pl->words;
   const unsigned T = 256;
@@ -358,10 +359,16 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     CK(cudaStreamSynchronize(st));
     Level& nx = lv[j + 1];
     nx.n = Un;
-    nx.eset.alloc((size_t)Un * 4, st);
+    if (j == f) {  // the final level is the chunk's output: it outlives the chunk's temporaries
+      nx.eset.alloc((size_t)Un * 4, ws_out);
+      nx.prefix.alloc((size_t)Un * 8 * words, ws_out);
+      nx.mult.alloc((size_t)Un * 4, ws_out);
+    } else {
+      nx.eset.alloc((size_t)Un * 4, st);
+      nx.prefix.alloc((size_t)Un * 8 * words, st);
+      nx.mult.alloc((size_t)Un * 4, st);
+    }
     nx.parent.alloc((size_t)Un * 4, st);
-    nx.prefix.alloc((size_t)Un * 8 * words, st);
-    nx.mult.alloc((size_t)Un * 4, st);
     if (Un) {
       ExpandArgs ea;
       ea.p_eset = cur.eset.as<uint32_t>();
@@ -429,6 +436,8 @@ struct ptsbe_batch {
   uint64_t n_sets = 0, total_shots = 0;
   std::vector<uint32_t> shots_host;
   DevBuf kraus, shots, ids;
+  Workspace ws_tmp;  // temporaries of one chunk (rewound after every chunk)
+  Workspace ws_out;  // chunk outputs and the merged histogram (reset at the start of a run)
   // last run
   Histogram merged;
   RunOutput per_set;  // when merged == 0 (single chunk only)
@@ -445,6 +454,11 @@ static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stat
   stats->first_flagged_id = -1;
   stats->total_shots = bt->total_shots;
   g_launches = 0;
+  bt->ws_tmp.reset();
+  bt->ws_out.reset();
+  bt->merged = Histogram();
+  bt->per_set = RunOutput();
+  WorkspaceScope scope(&bt->ws_out);  // flags, concatenation and the histogram live in ws_out
   DevBuf flag(16, st);
   CK(cudaMemsetAsync(flag.p, 0xff, 8, st));
   CK(cudaMemsetAsync(flag.as<unsigned char>() + 8, 0, 8, st));
@@ -491,9 +505,14 @@ static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stat
     const uint64_t e = chunks[c].first, cnt = chunks[c].second;
     uint64_t sh = 0;
     for (uint64_t i = 0; i < cnt; ++i) sh += bt->shots_host[e + i];
-    run_chunk(pl, bt->kraus.as<uint8_t>() + e * pl->g, bt->shots.as<uint32_t>() + e,
-              bt->ids.as<uint32_t>() + e, (uint32_t)cnt, sh, seed, outs[c], stats,
-              flag.as<unsigned long long>(), flag.as<uint32_t>() + 2);
+    {
+      WorkspaceScope chunk_scope(&bt->ws_tmp);
+      const Workspace::Mark mark = bt->ws_tmp.mark();
+      run_chunk(pl, bt->kraus.as<uint8_t>() + e * pl->g, bt->shots.as<uint32_t>() + e,
+                bt->ids.as<uint32_t>() + e, (uint32_t)cnt, sh, seed, outs[c], stats,
+                flag.as<unsigned long long>(), flag.as<uint32_t>() + 2, bt->ws_out);
+      bt->ws_tmp.rewind(mark);  // run_chunk returns with the stream drained
+    }
     total_rec += outs[c].n;
   }
   // flags
@@ -509,6 +528,7 @@ static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stat
   bt->have_per_set = false;
   EventLog hlog(st);
   hlog.begin(&stats->histogram_ms);
+  WorkspaceScope hist_scope(&bt->ws_tmp);  // sort/scan temporaries and the histogram: until the next run
   if (merged) {
     if (chunks.size() == 1) {
       reduce_by_key(outs[0].keys.as<uint64_t>(), outs[0].n, words, outs[0].counts.as<uint32_t>(),

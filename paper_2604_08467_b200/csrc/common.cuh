@@ -32,22 +32,67 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 extern thread_local std::string g_last_error;
 extern thread_local uint64_t g_launches;  // kernels launched on this thread since reset
 
-// Stream-ordered device buffer.  Allocation goes through the device's default
-// memory pool (release threshold raised at plan creation), so repeated runs
-// reuse the same HBM without cudaMalloc latency.
+// Run-scoped device workspace: a bump allocator over a few big cudaMalloc'ed slabs that are
+// kept between runs.  Every temporary of a sampling run (work lists, hoisted records,
+// population vectors, sort buffers) comes from here, so the timed loop performs no device
+// allocation at all once the slabs exist -- growing the stream-ordered pool by hundreds of
+// MB inside the loop stalls the GPU for as long as the kernels themselves take.
+struct Workspace {
+  struct Slab { char* p; size_t size; };
+  std::vector<Slab> slabs;
+  size_t cur = 0, off = 0;
+  static constexpr size_t kSlab = 1ull << 30;
+  void* alloc(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes == 0) bytes = 256;
+    for (; cur < slabs.size(); ++cur, off = 0)
+      if (off + bytes <= slabs[cur].size) {
+        void* r = slabs[cur].p + off;
+        off += bytes;
+        return r;
+      }
+    size_t want = bytes <= kSlab ? kSlab : ((bytes + bytes / 4 + (kSlab >> 2) - 1) / (kSlab >> 2)) * (kSlab >> 2);
+    Slab sl;
+    sl.size = want;
+    if (cudaMalloc(reinterpret_cast<void**>(&sl.p), want) != cudaSuccess) {
+      cudaGetLastError();
+      sl.size = want = bytes;  // exact fit as a last resort
+      cuda_check(cudaMalloc(reinterpret_cast<void**>(&sl.p), want), "cudaMalloc(workspace slab)", __FILE__, __LINE__);
+    }
+    slabs.push_back(sl);
+    cur = slabs.size() - 1;
+    off = bytes;
+    return sl.p;
+  }
+  struct Mark { size_t cur, off; };
+  Mark mark() const { return Mark{cur, off}; }
+  void rewind(Mark m) { cur = m.cur; off = m.off; }
+  void reset() { cur = 0; off = 0; }
+  size_t reserved() const { size_t t = 0; for (auto& s : slabs) t += s.size; return t; }
+  void destroy() { for (auto& s : slabs) cudaFree(s.p); slabs.clear(); reset(); }
+  ~Workspace() { destroy(); }
+};
+
+// workspace that DevBuf allocations of the calling thread are served from (null: stream-ordered pool)
+extern thread_local Workspace* g_ws;
+
+// Device buffer.  Inside a sampling run (g_ws set) it is a view into the run's workspace and
+// releasing it is free; elsewhere it is a stream-ordered allocation from the device's default
+// memory pool (release threshold raised at plan creation).
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   cudaStream_t s = nullptr;
+  bool owned = true;
   DevBuf() {}
   DevBuf(size_t n, cudaStream_t st) { alloc(n, st); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s) { o.p = nullptr; o.bytes = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s), owned(o.owned) { o.p = nullptr; o.bytes = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       release();
-      p = o.p; bytes = o.bytes; s = o.s;
+      p = o.p; bytes = o.bytes; s = o.s; owned = o.owned;
       o.p = nullptr; o.bytes = 0;
     }
     return *this;
@@ -57,15 +102,29 @@ struct DevBuf {
     s = st;
     bytes = n;
     if (n == 0) return;
+    if (g_ws) { p = g_ws->alloc(n); owned = false; return; }
+    owned = true;
     CK(cudaMallocAsync(&p, n, st));
   }
+  void alloc(size_t n, Workspace& ws) {
+    release();
+    bytes = n;
+    owned = false;
+    if (n) p = ws.alloc(n);
+  }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p && owned) cudaFreeAsync(p, s);
     p = nullptr;
     bytes = 0;
   }
   ~DevBuf() { release(); }
   template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct WorkspaceScope {  // installs a workspace for DevBuf allocations of this thread
+  Workspace* prev;
+  explicit WorkspaceScope(Workspace* ws) : prev(g_ws) { g_ws = ws; }
+  ~WorkspaceScope() { g_ws = prev; }
 };
 
 // Deferred CUDA-event timing of spans on one stream: spans are recorded while the
