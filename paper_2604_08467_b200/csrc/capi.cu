@@ -199,16 +199,27 @@ static void launch_project(ptsbe_plan* pl, const Program& pr, const void* v, uin
 static void launch_sampler(cudaStream_t st, SampleArgs& a, int sm_count) {
   if (a.n_items == 0) return;
   const size_t nb = 1ull << a.b;
-  const size_t smem = nb * 12;
   if (a.b > 14) throw Failure(PTSBE_ECAPACITY, "sampler supports stage batches of at most 14 qubits");
   static bool attr_set = false;
   if (!attr_set) {
     CK(cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(sample_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
     attr_set = true;
   }
-  const uint64_t cap = (uint64_t)sm_count * 16;
-  const unsigned grid = (unsigned)std::min<uint64_t>(a.n_items, cap);
-  sample_kernel<<<grid, SAMPLE_THREADS, smem, st>>>(a);
+  // Many items with few shots each: one warp per item.  Few items with many shots (stage 1):
+  // one CTA per item so the draws spread over 128 threads.
+  if (a.b <= 11 && a.n_items >= (uint64_t)sm_count * 16) {
+    const size_t padded = nb + (nb >> 5) + 1;
+    const size_t smem = (size_t)SW_WARPS * padded * 12;
+    const uint64_t cap = (uint64_t)sm_count * std::max<size_t>(1, std::min<size_t>(16, (200 * 1024) / smem));
+    const unsigned grid = (unsigned)std::min<uint64_t>((a.n_items + SW_WARPS - 1) / SW_WARPS, cap);
+    sample_warp_kernel<<<grid, SW_WARPS * 32, smem, st>>>(a);
+  } else {
+    const size_t smem = nb * 12;
+    const uint64_t cap = (uint64_t)sm_count * 16;
+    const unsigned grid = (unsigned)std::min<uint64_t>(a.n_items, cap);
+    sample_kernel<<<grid, SAMPLE_THREADS, smem, st>>>(a);
+  }
   g_launches++;
   CK(cudaGetLastError());
 }

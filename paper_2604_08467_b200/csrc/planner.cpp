@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <queue>
 #include <vector>
 
@@ -36,7 +37,7 @@ struct Rng {  // splitmix64
   double uniform() { return ((next() >> 11) + 0.5) * (1.0 / 9007199254740992.0); }
 };
 
-constexpr double kStepOverheadMacs = 48.0;
+static double kStepOverheadMacs = 48.0;  // PTSBE_STEP_OVERHEAD overrides (experiments)
 
 struct Cand {
   double key, tie;
@@ -187,6 +188,7 @@ extern "C" int ptsbe_plan_greedy(uint32_t n_ops, const uint32_t* op_ptr, const i
                                  double size_cap_log2,
                                  uint32_t* merges_out, double* cost_out, double* flops_out) {
   if (n_ops < 1 || hypersamples < 1 || !op_ptr || !merges_out) return PTSBE_EINVAL;
+  if (const char* ov = getenv("PTSBE_STEP_OVERHEAD")) kStepOverheadMacs = atof(ov);
   Problem P;
   P.n = n_ops;
   P.labels.resize(n_ops);

@@ -179,6 +179,133 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(const SampleArgs
   }
 }
 
+// Warp-per-item variant for nb <= 2048 (b <= 11): same arithmetic, same results as
+// sample_kernel, but no block-wide barriers.  Each lane owns the nb/32 CONSECUTIVE outcomes
+// [lane*per, lane*per+per); the row is staged through shared memory (padded by one slot per
+// 32 so the strided per-lane reads are conflict-free), scanned serially in registers, and the
+// lane totals are combined with one shuffle scan.  Most work items of the late stages draw one
+// or two shots, so latency per item -- not throughput of the draws -- is what matters.
+constexpr int SW_WARPS = 4;
+
+__device__ __forceinline__ uint32_t sw_pad(uint32_t k) { return k + (k >> 5); }
+
+__global__ void __launch_bounds__(SW_WARPS * 32) sample_warp_kernel(const SampleArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const uint32_t nb = 1u << a.b;
+  const uint32_t padded = nb + (nb >> 5) + 1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t* cdf = reinterpret_cast<uint64_t*>(sm) + (size_t)wid * padded;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(reinterpret_cast<uint64_t*>(sm) + (size_t)SW_WARPS * padded) +
+                  (size_t)wid * padded;
+  double* pd = reinterpret_cast<double*>(cdf);
+  const uint32_t per = nb >= 32 ? nb >> 5 : 1;           // outcomes per lane
+  const uint32_t lanes_used = nb >= 32 ? 32 : nb;
+  const uint64_t n_warps = (uint64_t)gridDim.x * SW_WARPS;
+
+  for (uint64_t it = (uint64_t)blockIdx.x * SW_WARPS + wid; it < a.n_items; it += n_warps) {
+    const uint64_t item = a.first_item + it;
+    const uint32_t m = a.mult[item];
+    // ---- load (coalesced), clamp, max / min / sum ----
+    double mx = 0.0, rawmin = 1e300, csum = 0.0;
+    if (a.is_f32) {
+      const float* p = reinterpret_cast<const float*>(a.probs) + it * nb;
+      for (uint32_t k = lane; k < nb; k += 32) {
+        double v = (double)p[k]; rawmin = fmin(rawmin, v);
+        v = v > 0.0 ? v : 0.0; pd[sw_pad(k)] = v; mx = fmax(mx, v); csum += v;
+        cnt[sw_pad(k)] = 0;
+      }
+    } else {
+      const double* p = reinterpret_cast<const double*>(a.probs) + it * nb;
+      for (uint32_t k = lane; k < nb; k += 32) {
+        double v = p[k]; rawmin = fmin(rawmin, v);
+        v = v > 0.0 ? v : 0.0; pd[sw_pad(k)] = v; mx = fmax(mx, v); csum += v;
+        cnt[sw_pad(k)] = 0;
+      }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+      rawmin = fmin(rawmin, __shfl_xor_sync(0xffffffffu, rawmin, d));
+      csum += __shfl_xor_sync(0xffffffffu, csum, d);
+    }
+    // ---- guards (engine.py:447-448, 475-476, 484-485) ----
+    uint32_t bad = 0;
+    {
+      const double ms = a.mass ? a.mass[it] : csum, mn = a.minv ? a.minv[it] : rawmin;
+      if (mn < a.neg_abs - a.neg_rel * ms) bad = PTSBE_ENUMERIC;
+      else if (ms < a.vanish) bad = PTSBE_EIMPOSSIBLE;
+    }
+    if (!bad && !(mx > 0.0)) bad = PTSBE_EIMPOSSIBLE;
+    if (bad) {
+      if (lane == 0) {
+        a.nnz[item] = 0;
+        atomicMin(a.flag, ((unsigned long long)a.eset_id[item] << 16) |
+                              ((unsigned long long)(a.stage & 0xff) << 8) | bad);
+        atomicAdd(a.flag_count, 1u);
+      }
+      __syncwarp();
+      continue;
+    }
+    __syncwarp();
+    // ---- exact fixed-point weights and their inclusive scan ----
+    int ex;
+    frexp(mx, &ex);
+    const int shift = (62 - (int)a.b) - ex;
+    const uint32_t k0 = lane * per;
+    uint64_t run = 0;
+    if (lane < (int)lanes_used)
+      for (uint32_t k = k0; k < k0 + per; ++k) {
+        run += (uint64_t)ldexp(pd[sw_pad(k)], shift);
+        cdf[sw_pad(k)] = run;  // same 8-byte slot as pd: lane-local inclusive sums
+      }
+    uint64_t incl = run;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += o;
+    }
+    const uint64_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint64_t base = incl - run;
+    if (lane < (int)lanes_used)
+      for (uint32_t k = k0; k < k0 + per; ++k) cdf[sw_pad(k)] += base;
+    __syncwarp();
+    // ---- draws: outcome = #{k : cdf[k] <= r}, r = floor(x * W / 2^64) ----
+    const uint32_t rk = a.rank[item], es = a.eset_id[item];
+    for (uint32_t t = lane; t < m; t += 32) {
+      const Philox4 x = philox4x32_10(t, rk, a.stage, es, a.k0, a.k1);
+      const uint64_t x64 = ((uint64_t)x.v[1] << 32) | x.v[0];
+      const uint64_t r = __umul64hi(x64, total);
+      uint32_t lo = 0, hi = nb;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (cdf[sw_pad(mid)] <= r) lo = mid + 1; else hi = mid;
+      }
+      atomicAdd(&cnt[sw_pad(lo)], 1u);
+    }
+    __syncwarp();
+    // ---- ordered emission of the non-empty outcomes ----
+    uint32_t mine = 0;
+    if (lane < (int)lanes_used)
+      for (uint32_t k = k0; k < k0 + per; ++k) mine += cnt[sw_pad(k)] != 0;
+    uint32_t pos = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, pos, d);
+      if (lane >= d) pos += o;
+    }
+    const uint32_t tot32 = __shfl_sync(0xffffffffu, pos, 31);
+    pos -= mine;
+    const uint32_t slot0 = a.slot_off[item];
+    if (mine)
+      for (uint32_t k = k0; k < k0 + per; ++k) {
+        const uint32_t c = cnt[sw_pad(k)];
+        if (c) { a.slot_index[slot0 + pos] = k; a.slot_count[slot0 + pos] = c; ++pos; }
+      }
+    if (lane == 0) a.nnz[item] = tot32;
+    __syncwarp();
+  }
+}
+
 // ---- next-level construction ----------------------------------------------
 
 struct ExpandArgs {

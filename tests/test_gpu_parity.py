@@ -96,6 +96,33 @@ def test_sampler_bit_exact_against_oracle_draws():
         assert pos == item.size
 
 
+def test_warp_sampler_bit_exact_on_large_batches():
+    """Many work items with few shots each take the warp-per-item sampler
+    (sample_warp_kernel); its counts must equal the oracle's as well."""
+    rng = np.random.default_rng(8)
+    for b in (1, 3, 5, 8, 10, 11):
+        w = 4000
+        probs = rng.random((w, 1 << b)) ** 4
+        probs[rng.random(probs.shape) < 0.4] = 0.0
+        probs[np.arange(w), rng.integers(0, 1 << b, size=w)] += 0.05
+        mult = rng.integers(1, 4, size=w).astype(np.uint32)
+        mult[:50] = rng.integers(40, 400, size=50)
+        eset = rng.integers(0, 5000, size=w).astype(np.uint32)
+        rank = rng.integers(0, 900, size=w).astype(np.uint32)
+        item, index, count = _capi.sample_stage(b, 2, 0x1234ABCD5678, probs, mult, eset, rank)
+        assert int(count.sum()) == int(mult.sum())
+        pos = 0
+        for i in list(range(120)) + list(range(w - 40, w)):
+            while item[pos] < i:
+                pos += 1
+            want = O.multinomial_counts(probs[i], int(mult[i]), 0x1234ABCD5678, int(eset[i]), 2, int(rank[i]))
+            nz = np.flatnonzero(want)
+            sl = slice(pos, pos + nz.size)
+            assert np.all(item[sl] == i)
+            assert index[sl].tolist() == nz.tolist()
+            assert count[sl].tolist() == want[nz].tolist()
+
+
 @pytest.mark.parametrize("name", ALL)
 def test_complex128_histograms_bit_exact_vs_reference(golden_cases, name):
     """Reference sample_proportional (with the counter-based RNG shim) vs the
