@@ -261,7 +261,16 @@ def plan_stage(op_labels, op_dims, op_class, op_is_prefix, open_labels, class_we
                                               hypersamples=hypersamples, seed=seed + 1, class_cap_log2=cc)
                 return [(ids[int(a)], ids[int(b)]) for a, b in m], wc, fl
 
-            mv, wv, fv = sub(gv, class_weight, caps)
+            # near side: the hoisted classes are searched under several record caps.  Hoisted
+            # merges are nearly free in the batch-weighted cost, so an uncapped greedy keeps
+            # merging them into blobs that the per-item steps then have to slice; a small cap
+            # stops at "site tensor" size.  Every candidate is judged by the same weighted cost.
+            mv, wv, fv = None, math.inf, 0.0
+            for rec_cap in (4.0, 5.0, 6.0, 7.0, 8.0, 10.0, 13.0, record_cap_log2):
+                cc = [min(rec_cap, record_cap_log2)] * (n_cls - 1) + [item_cap_log2]
+                m_, w_, f_ = sub(gv, class_weight, cc)
+                if w_ < wv:
+                    mv, wv, fv = m_, w_, f_
             mm, wm, fm = sub(far, class_weight, [record_cap_log2] * n_cls)
             root = 2.0 ** (cut / 64.0 + log2_n)
             total = wv + wm + root * class_weight[-1]
