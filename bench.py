@@ -364,11 +364,22 @@ def main():
     wall1 = time.perf_counter()
     clocks = sampler.stop(wall0, wall1) if sampler else None
 
+    # shots actually sampled in the last step (histogram total); error sets whose trajectory has zero
+    # weight (e.g. amplitude-damping K1 on |0>) are flagged by the device and contribute none
+    _, last_counts = batch.fetch()
+    sampled_local = int(last_counts.sum())
+    flagged_local = int(stats[-1].flagged_sets)
+    if sampled_local != total_shots_local and flagged_local == 0:
+        raise SystemExit(f"histogram holds {sampled_local} shots, expected {total_shots_local}, and nothing was flagged")
     t = torch.tensor([dev_ms, (wall1 - wall0) * 1e3], dtype=torch.float64, device=f"cuda:{local_rank}")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dev_ms_max, wall_ms_max = float(t[0]), float(t[1])
-    total_shots = total_shots_local * world
+    cnt = torch.tensor([sampled_local, flagged_local], dtype=torch.int64, device=f"cuda:{local_rank}")
+    if world > 1:
+        dist.all_reduce(cnt)
+    total_shots = int(cnt[0])
+    flagged_total = int(cnt[1])
     value = total_shots * args.steps / (dev_ms_max * 1e-3)
 
     # ---- e2e through the host-buffer C-ABI call (pinned inputs) ----
@@ -455,6 +466,8 @@ def main():
             "gpu_launches": int(sum(int(s.gpu_launches) for s in stats)),
             "wall_ms_per_step": wall_ms_max / args.steps,
             "unique_bitstrings": int(st.n_records),
+            "sampled_shots_per_step": total_shots, "requested_shots_per_step": total_shots_local * world,
+            "flagged_work_items": flagged_total,
             "stage_events": [int(st.stage_events[j]) for j in range(f)],
             "kernel_ms_per_step": {
                 "exec_marginal": [m / args.steps for m in marg], "project": [m / args.steps for m in projm], "exec_hoist": [h / args.steps for h in hoist],

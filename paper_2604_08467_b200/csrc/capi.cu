@@ -48,7 +48,7 @@ struct ptsbe_plan {
   size_t probs_budget = 256ull << 20;  // bytes of marginal buffer per sub-batch
   uint64_t chunk_shots = 1ull << 26;
   size_t ext_budget = 48ull << 30;
-  double vanish = 1e-12, neg_abs = -1e-12, neg_rel = 0.0;
+  double vanish = 1e-12, neg_abs = -1e-12, neg_rel = 0.0, vanish_stage1 = 1e-30;
 };
 
 namespace ptsbe {
@@ -251,6 +251,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
   DevBuf seg_start((size_t)ne * 4, st);
   DevBuf slot_index(chunk_shots * 4, st), slot_count(chunk_shots * 4, st);
   DevBuf scal(16, st);
+  DevBuf set_mass((size_t)ne * 8, st);  // stage-1 mass (trajectory weight) of every error set
 
   // level 1: one item per error set, empty prefix
   {
@@ -354,6 +355,9 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       sa.k1 = (uint32_t)(seed >> 32);
       sa.is_f32 = pl->dtype == PTSBE_C64;
       sa.vanish = pl->vanish;
+      sa.set_mass = set_mass.as<double>();
+      sa.eset_row = cur.eset.as<uint32_t>();
+      sa.vanish_stage1 = pl->vanish_stage1;
       sa.neg_abs = pl->neg_abs;
       sa.neg_rel = pl->neg_rel;
       log.begin(&stats->sampler_ms[j - 1]);

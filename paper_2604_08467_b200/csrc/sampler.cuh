@@ -61,6 +61,13 @@ struct SampleArgs {
   uint32_t is_f32;
   double vanish;            // engine.py:54 VANISHING_MASS
   double neg_abs, neg_rel;  // engine.py:53 NEGATIVE_DIAG_TOLERANCE (+ relative term for c64)
+  // Non-unitary Kraus operators (amplitude damping) give a trajectory a weight < 1, and every
+  // unnormalised mass of that error set carries it.  The vanishing-mass guard is therefore
+  // taken relative to the error set's stage-1 mass (== 1 for the reference's unitary errors, so
+  // the reference behaviour is unchanged): stage 1 records it, later stages compare against it.
+  double* set_mass;         // [error-set rows] or null (absolute guard)
+  const uint32_t* eset_row; // [items] row of the item's error set in set_mass
+  double vanish_stage1;     // absolute floor for the stage-1 mass itself
 };
 
 constexpr int SAMPLE_THREADS = 128;
@@ -115,8 +122,13 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(const SampleArgs
     uint32_t bad = 0;
     {
       const double ms = a.mass ? a.mass[it] : csum, mn = a.minv ? a.minv[it] : rawmin;
+      double floor_mass = a.vanish;
+      if (a.set_mass) {
+        if (a.stage == 1) { floor_mass = a.vanish_stage1; if (tid == 0) a.set_mass[a.eset_row[item]] = ms; }
+        else floor_mass = a.vanish * a.set_mass[a.eset_row[item]];
+      }
       if (mn < a.neg_abs - a.neg_rel * ms) bad = PTSBE_ENUMERIC;
-      else if (ms < a.vanish) bad = PTSBE_EIMPOSSIBLE;
+      else if (ms < floor_mass) bad = PTSBE_EIMPOSSIBLE;
     }
     if (!bad && !(mx > 0.0)) bad = PTSBE_EIMPOSSIBLE;
     if (bad) {
@@ -232,8 +244,13 @@ __global__ void __launch_bounds__(SW_WARPS * 32) sample_warp_kernel(const Sample
     uint32_t bad = 0;
     {
       const double ms = a.mass ? a.mass[it] : csum, mn = a.minv ? a.minv[it] : rawmin;
+      double floor_mass = a.vanish;
+      if (a.set_mass) {
+        if (a.stage == 1) { floor_mass = a.vanish_stage1; if (lane == 0) a.set_mass[a.eset_row[item]] = ms; }
+        else floor_mass = a.vanish * a.set_mass[a.eset_row[item]];
+      }
       if (mn < a.neg_abs - a.neg_rel * ms) bad = PTSBE_ENUMERIC;
-      else if (ms < a.vanish) bad = PTSBE_EIMPOSSIBLE;
+      else if (ms < floor_mass) bad = PTSBE_EIMPOSSIBLE;
     }
     if (!bad && !(mx > 0.0)) bad = PTSBE_EIMPOSSIBLE;
     if (bad) {

@@ -202,6 +202,30 @@ def test_impossible_trajectory_is_flagged_with_its_id():
         sample_proportional_batched(tpl, es, BatchPlan((1, 1)), 1)
 
 
+def test_low_weight_trajectories_are_sampled_not_dropped():
+    """Non-unitary Kraus operators give a trajectory a weight far below the
+    reference's absolute 1e-12 mass floor (which was written for unitary
+    errors); the device guard is relative to the error set's stage-1 mass, so
+    such error sets are sampled from their normalised distribution."""
+    c, _ = workloads.hea(8, 3, gamma=1e-4, p=0.0, seed=9)
+    labels = [g.noise.identity_label() for g in c.gates]
+    hit = [s for s, g in enumerate(c.gates) if g.noise.kind == "amplitude_damping"][20:25]
+    for s in hit:
+        labels[s] = "K1"
+    es = [ErrorSet(3, tuple(labels), 30000)]
+    tpl = CircuitNetwork.from_circuit(c)
+    for sizes in ((8,), (3, 3, 2)):
+        recs = sample_proportional_batched(tpl, es, BatchPlan(sizes), 21, SamplerContext(hypersamples=4))[0]
+        assert sum(r.count for r in recs) == 30000
+        ops, finals = bridge.merged_ops(c, es[0].realized)
+        probs, mass = O.stage_marginal(ops, finals, (8,), 1, "")
+        assert 0 < mass < 1e-12
+        emp = np.zeros(256)
+        for r in recs:
+            emp[int(r.bitstring, 2)] = r.count / 30000
+        assert 0.5 * np.abs(emp - probs / mass).sum() <= 0.03
+
+
 def test_tensor_core_api_on_device():
     """contract_pair / execute_path known answers (reference tests/test_tensor.py:25-62)."""
     a = Tensor([Index(0, 2), Index(1, 3)], np.ones((2, 3)))
