@@ -54,7 +54,9 @@ enum { PTSBE_C64 = 0, PTSBE_C128 = 1 };
  *          sel_kind 2: prefix bit          data = pool[pool_off + bit(sel_arg)*size ..)
  *                      (basis vectors of engine.py:395-399)
  * steps  : n_steps x 12 words {a_kind, a_ref, b_kind, b_ref, o_kind, o_ref,
- *                              out_n, k_n, lo_n, hi_n, tab_off, reserved}
+ *                              out_n, k_n, lo_n, hi_n, tab_off, conj}
+ *          conj bit 0 / 1: operand A / B is read complex-conjugated (its node is the
+ *          conjugate twin -- bra copy -- of the node that was actually computed)
  *          operand kind 0: arena offset (elements), 1: leaf index,
  *                       2 + p: record of pass p of the same stage, a_ref = offset in record
  *          output  kind 0: arena offset, 1: offset in this pass's output record

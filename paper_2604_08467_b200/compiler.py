@@ -217,9 +217,17 @@ def compile_stage(
     pool: Pool,
     elem_bytes: int,
     ceiling: Optional[int] = None,
+    mirror: Optional[Sequence[int]] = None,
 ) -> tuple[list[Program], tuple]:
     """Compile one stage network + stored path into `n_passes` programs.
-    Returns (programs, result label order)."""
+    Returns (programs, result label order).
+
+    `mirror[k]` (optional) names the operand whose value is the complex
+    conjugate of operand k under a relabelling (the bra copy of a ket operand,
+    engine.py:393 of the reference).  A subtree built only from mirror
+    operands of an already computed subtree, in the same shape, is its
+    conjugate: it is not computed at all, its consumers read the original
+    with a conjugation flag (step word 11: bit 0 = conj A, bit 1 = conj B)."""
     nodes, root, _ = build_tree(operands, steps, ceiling)
     n_leaves = len(operands)
     top = n_passes - 1
@@ -248,13 +256,46 @@ def compile_stage(
                 proj = (v, m)
                 break
 
+    # conjugate subtrees --------------------------------------------------------
+    virt: dict[int, int] = {}          # virtual node -> the computed node it is the conjugate of
+    if mirror is not None:
+        node_mirror: dict[int, int] = {k: int(m) for k, m in enumerate(mirror) if m is not None and m >= 0}
+        by_children: dict[tuple, int] = {}
+        for nid in range(n_leaves, len(nodes)):
+            nd = nodes[nid]
+            ma, mb = node_mirror.get(nd.a), node_mirror.get(nd.b)
+            twin = by_children.get((ma, mb)) if (ma is not None and mb is not None) else None
+            if (twin is not None and twin != nid and twin not in virt and nid != root
+                    and nodes[twin].cls == nd.cls and nodes[twin].dims == nd.dims
+                    and (proj is None or nid not in proj)):
+                virt[nid] = twin
+                node_mirror[nid] = twin
+                node_mirror[twin] = nid
+            else:
+                by_children[(nd.a, nd.b)] = nid
+
+    def real_of(nid: int) -> int:
+        return virt.get(nid, nid)
+
+    # consumers of a computed node: its own parent plus the parents of its virtual twins
+    consumers: dict[int, list[int]] = {}
+    for nid in range(len(nodes)):
+        if nid in virt:
+            continue
+        nd = nodes[nid]
+        if nid >= n_leaves:
+            for ch in (nd.a, nd.b):
+                consumers.setdefault(real_of(ch), []).append(nid)
+
     # storage decisions ------------------------------------------------------
     # frontier = computed node consumed by a later pass -> lives in its pass's record
     rec_off: dict[int, int] = {}
     rec_size = [0] * n_passes
     for nid in range(n_leaves, len(nodes)):
         nd = nodes[nid]
-        if nd.parent >= 0 and nodes[nd.parent].pass_ > nd.pass_:
+        if nid in virt:
+            continue
+        if any(nodes[c].pass_ > nd.pass_ for c in consumers.get(nid, ())):
             rec_off[nid] = rec_size[nd.pass_]
             rec_size[nd.pass_] += (nd.size + 3) & ~3  # 4-element granules keep vector loads aligned
     if proj is not None:
@@ -264,12 +305,12 @@ def compile_stage(
     programs: list[Program] = []
     result_kind, result_ref = 0, 0
     for p in range(n_passes):
-        mine = [nid for nid in range(n_leaves, len(nodes)) if nodes[nid].pass_ == p]
+        mine = [nid for nid in range(n_leaves, len(nodes)) if nodes[nid].pass_ == p and nid not in virt]
         if proj is not None and p == top:
             mine = [nid for nid in mine if nid != root]
         # sizing of the on-chip arena: try everything on chip, spill the big buffers otherwise
         max_out = max([nodes[nid].size for nid in mine], default=1)
-        peak = _place(nodes, mine, rec_off, root, fast_cap=None)[1]
+        peak = _place(nodes, mine, rec_off, real_of, fast_cap=None)[1]
         if max_out <= 512 and peak * elem_bytes <= WARP_ARENA_BYTES:
             # sub-warp groups: GS lanes per item, 32 / GS items per warp in lockstep.  Pick the
             # group size with the fewest issued warp-instructions per item (rough model of
@@ -292,7 +333,7 @@ def compile_stage(
             while threads < 512 and threads * 4 < max_out:
                 threads *= 2
             fast_cap = min(peak, SMEM_BYTES // elem_bytes)
-        where, peak_fast, peak_spill = _place(nodes, mine, rec_off, root, fast_cap=fast_cap)
+        where, peak_fast, peak_spill = _place(nodes, mine, rec_off, real_of, fast_cap=fast_cap)
 
         step_rows, tables = [], []
         tab_off = 0
@@ -302,6 +343,7 @@ def compile_stage(
         ext_reads: dict[int, int] = {}
 
         def ref_of(nid: int):
+            nid = real_of(nid)
             if nid < n_leaves:
                 at = prog_leaf_index.get(nid)
                 if at is None:
@@ -312,11 +354,14 @@ def compile_stage(
                     prog_leaf_index[nid] = at
                     prog_leaves.append([pool.add(blk), size, o.sel_kind, o.sel_arg])
                 return 1, at
-            if nid in rec_off and nodes[nid].pass_ != p:
-                ext_reads[nid] = nodes[nid].size
-                return 2 + nodes[nid].pass_, rec_off[nid]
             if nid in rec_off:
-                raise AssertionError("frontier node consumed inside its own pass")
+                # lives in a record: of an earlier pass, or of this very pass (a node that also
+                # feeds a later pass; the group wrote it before the barrier that precedes this step)
+                if nodes[nid].pass_ != p:
+                    ext_reads[nid] = nodes[nid].size
+                elif p == top:
+                    raise AssertionError("the projection vector is consumed by the projection kernel only")
+                return 2 + nodes[nid].pass_, rec_off[nid]
             return 0, where[nid]
 
         for nid in mine:
@@ -324,6 +369,7 @@ def compile_stage(
             na, nb = nodes[nd.a], nodes[nd.b]
             a_kind, a_ref = ref_of(nd.a)
             b_kind, b_ref = ref_of(nd.b)
+            conj_flags = (1 if nd.a in virt else 0) | (2 if nd.b in virt else 0)
             if nid in rec_off:
                 o_kind, o_ref = 1, rec_off[nid]
             else:
@@ -354,7 +400,7 @@ def compile_stage(
             words = np.concatenate([lo_a, lo_b, hi_a, hi_b, k_a, k_b]).astype(np.uint32)
             tables.append(words)
             step_rows.append(
-                [a_kind, a_ref, b_kind, b_ref, o_kind, o_ref, nd.size, k_n, lo_n, hi_n, tab_off, 0]
+                [a_kind, a_ref, b_kind, b_ref, o_kind, o_ref, nd.size, k_n, lo_n, hi_n, tab_off, conj_flags]
             )
             tab_off += words.size
             flops += float(nd.size) * k_n
@@ -390,15 +436,22 @@ def compile_stage(
     return programs, tuple(open_order)
 
 
-def _place(nodes, mine, rec_off, root, fast_cap):
+def _place(nodes, mine, rec_off, real_of, fast_cap):
     """Liveness-based placement of the intermediates of one pass.  Buffers go to
     the fast (shared-memory) arena while they fit under `fast_cap`, otherwise to
-    the spill arena whose offsets start at fast_cap.  Returns
-    (offset per node, fast peak, spill peak)."""
+    the spill arena whose offsets start at fast_cap.  A buffer is released after
+    its last consumer inside the pass (a node can feed its parent and, through a
+    conjugate twin, the twin's parent).  Returns (offset per node, fast peak,
+    spill peak)."""
     fast, spill = _Arena(), _Arena()
     where: dict[int, int] = {}
     in_spill: set[int] = set()
     mine_set = set(mine)
+    uses: dict[int, int] = {}
+    for nid in mine:
+        for ch in (nodes[nid].a, nodes[nid].b):
+            ch = real_of(ch)
+            uses[ch] = uses.get(ch, 0) + 1
     for nid in mine:
         nd = nodes[nid]
         if nid not in rec_off:
@@ -408,7 +461,9 @@ def _place(nodes, mine, rec_off, root, fast_cap):
                 in_spill.add(nid)
             where[nid] = off
         for ch in (nd.a, nd.b):
-            if ch in where and ch in mine_set:
+            ch = real_of(ch)
+            uses[ch] -= 1
+            if uses[ch] == 0 and ch in where and ch in mine_set:
                 (spill if ch in in_spill else fast).release(where[ch], nodes[ch].size)
     if fast_cap is None:
         return where, fast.top, 0

@@ -78,7 +78,15 @@ __device__ __forceinline__ void cmac(C& acc, const C a, const C b) {
 struct StepTables {
   const uint32_t *loA, *loB, *hiA, *hiB, *kA, *kB;
   uint32_t out_n, lo_n, hi_n;
+  uint32_t conj;  // bit 0: use conj(A), bit 1: use conj(B) -- operand is the conjugate twin of a computed node
 };
+
+template <typename C>
+__device__ __forceinline__ C ld_conj(const C* p, bool flip) {
+  C v = *p;
+  if (flip) v.y = -v.y;
+  return v;
+}
 
 // inner product over KN shared labels with the k-offsets held in registers
 template <typename C, int KN>
@@ -90,6 +98,7 @@ __device__ __forceinline__ void step_fixed_k(const C* __restrict__ A, const C* _
   for (int k = 0; k < KN; ++k) { ka[k] = __ldg(t.kA + k); kb[k] = __ldg(t.kB + k); }
   const int sh = 31 - __clz(t.lo_n);
   const bool pow2 = (t.lo_n & (t.lo_n - 1)) == 0;
+  const bool fa = t.conj & 1, fb = t.conj & 2;
   for (uint32_t c = tid; c < t.out_n; c += gsize) {
     uint32_t cl, ch;
     if (pow2) { cl = c & (t.lo_n - 1); ch = c >> sh; }
@@ -98,7 +107,7 @@ __device__ __forceinline__ void step_fixed_k(const C* __restrict__ A, const C* _
     if (t.hi_n > 1) { a0 += __ldg(t.hiA + ch); b0 += __ldg(t.hiB + ch); }
     C acc; acc.x = 0; acc.y = 0;
 #pragma unroll
-    for (int k = 0; k < KN; ++k) cmac(acc, A[a0 + ka[k]], B[b0 + kb[k]]);
+    for (int k = 0; k < KN; ++k) cmac(acc, ld_conj(A + a0 + ka[k], fa), ld_conj(B + b0 + kb[k], fb));
     if (store) O[(size_t)c * o_stride] = acc;
   }
 }
@@ -193,6 +202,7 @@ __global__ void exec_kernel(const ExecArgs a) {
       t.out_n = s1.z;
       t.lo_n = s2.x;
       t.hi_n = s2.y;
+      t.conj = s2.w;
       const uint32_t kn = s1.w;
       t.loA = a.tables + s2.z;
       t.loB = t.loA + t.lo_n;
@@ -208,6 +218,7 @@ __global__ void exec_kernel(const ExecArgs a) {
         default: {
           const bool pow2 = (t.lo_n & (t.lo_n - 1)) == 0;
           const int sh = 31 - __clz(t.lo_n);
+          const bool fa = t.conj & 1, fb = t.conj & 2;
           for (uint32_t c = tid; c < t.out_n; c += gsize) {
             uint32_t cl, ch;
             if (pow2) { cl = c & (t.lo_n - 1); ch = c >> sh; }
@@ -215,7 +226,8 @@ __global__ void exec_kernel(const ExecArgs a) {
             uint32_t a0 = __ldg(t.loA + cl), b0 = __ldg(t.loB + cl);
             if (t.hi_n > 1) { a0 += __ldg(t.hiA + ch); b0 += __ldg(t.hiB + ch); }
             C acc; acc.x = 0; acc.y = 0;
-            for (uint32_t k = 0; k < kn; ++k) cmac(acc, A[a0 + __ldg(t.kA + k)], B[b0 + __ldg(t.kB + k)]);
+            for (uint32_t k = 0; k < kn; ++k)
+              cmac(acc, ld_conj(A + a0 + __ldg(t.kA + k), fa), ld_conj(B + b0 + __ldg(t.kB + k), fb));
             if (store) O[(size_t)c * o_stride] = acc;
           }
         }

@@ -466,7 +466,8 @@ def stage_operands(cnet: CircuitNetwork, plan: BatchPlan, j: int, tables: Varian
     (both selected by the site's Kraus index): same values, but the network
     exposes the true entanglement cut of controlled gates, which is what the
     cut-based planner (planner.plan_stage) needs.  Returns (operands, open
-    label order)."""
+    label order, mirror) where mirror[k] is the operand that is the conjugate
+    (bra / ket) copy of operand k, -1 for the copy tensors."""
     bra, fixed, opened = _stage_layout(cnet, plan, j)
     n_kets = len(cnet.net.operands) - tables.n_sites
     fresh = 1 + max([lb for t in cnet.net.operands for lb in t.labels] + list(bra.values())
@@ -501,13 +502,17 @@ def stage_operands(cnet: CircuitNetwork, plan: BatchPlan, j: int, tables: Varian
             else:
                 data, kind, arg = t.data.reshape(1, -1), SEL_CONST, 0
             ops.append(Operand(labels, dims, np.conj(data) if conj else data, kind, arg, 0))
+    half = len(ops) // 2
+    mirror = [k + half for k in range(half)] + [k for k in range(half)]
     for q, ket_leg, bra_leg in fixed:
         s = plan.stage_of_qubit(q)
         ops.append(Operand((ket_leg,), (2,), _BASIS, SEL_PREFIX, q, s))
         ops.append(Operand((bra_leg,), (2,), _BASIS, SEL_PREFIX, q, s))
+        mirror += [len(ops) - 1, len(ops) - 2]
     for _, ket_leg, bra_leg, open_leg in opened:
         ops.append(Operand((ket_leg, bra_leg, open_leg), (2, 2, 2), _COPY3.reshape(1, -1)))
-    return ops, tuple(o[3] for o in opened)
+        mirror.append(-1)
+    return ops, tuple(o[3] for o in opened), mirror
 
 
 RECORD_CAP_LOG2 = 18.0  # entries of one hoisted record (per error set / per earlier-stage prefix)
@@ -553,7 +558,7 @@ class DevicePipeline:
             if j not in want:
                 programs += [_empty_program(p + 1, 1 << plan.sizes[j - 1] if p == j - 1 else 0) for p in range(j)]
                 continue
-            ops, opens = stage_operands(cnet, plan, j, tables, split=True)
+            ops, opens, mirror = stage_operands(cnet, plan, j, tables, split=True)
             # distinct instances of a class-k result: unique prefixes entering stage k+1
             weights = [float(min(shots_per_set, 2.0 ** min(plan.offset(k + 1), 60))) for k in range(j)]
             sig = _ops_signature(ops, opens)
@@ -565,7 +570,7 @@ class DevicePipeline:
             else:
                 path = plan_stage(
                     [o.labels for o in ops], [o.dims for o in ops], [o.cls for o in ops],
-                    [o.sel_kind == SEL_PREFIX for o in ops], opens, weights,
+                    [o.sel_kind == SEL_PREFIX for o in ops], opens, weights, op_mirror=mirror,
                     item_cap_log2=_size_cap_log2(ctx.dtype), record_cap_log2=RECORD_CAP_LOG2,
                     hypersamples=ctx.hypersamples, rng=spawn_rng(ctx.planner_seed, _KEY_PLANNER, j))
                 ctx.cache.put(sig, key, path)
@@ -574,7 +579,7 @@ class DevicePipeline:
                 ctx.stats.path_seconds += time.perf_counter() - t0
             self.paths[j] = path
             progs, _ = compiler.compile_stage(ops, path.steps, opens, j, pool, elem,
-                                              ceiling=ctx.max_intermediate)
+                                              ceiling=ctx.max_intermediate, mirror=mirror)
             self.stage_flops[j] = [p.flops for p in progs]
             programs += progs
         self.compiled = CompiledPlan(

@@ -204,7 +204,8 @@ def _min_cut_source_side(n: int, edges, sources, sinks) -> tuple:
 
 def plan_stage(op_labels, op_dims, op_class, op_is_prefix, open_labels, class_weight,
                item_cap_log2: float, record_cap_log2: float, hypersamples: int = 100,
-               rng: Optional[np.random.Generator] = None) -> ContractionPath:
+               rng: Optional[np.random.Generator] = None,
+               op_mirror: Optional[Sequence[int]] = None) -> ContractionPath:
     """Path for one stage network of the batched executor (north-star
     subsystem 1: found once on the template, stored, replayed for every error
     set and prefix).  Two candidates, the cheaper batch-weighted cost wins:
@@ -218,6 +219,11 @@ def plan_stage(op_labels, op_dims, op_class, op_is_prefix, open_labels, class_we
               side contracts per work item into a vector v[cut legs]; the root
               step P = v . M is a dense matrix product over all items of an
               error set, which the executor runs as a GEMM (csrc/project.cuh).
+
+    With `op_mirror` (ket <-> bra twin of every operand) the near side is
+    searched on its ket half only when the two halves are disconnected: the
+    bra half is contracted in the mirrored order, which lets the compiler
+    recognise every bra subtree as the conjugate of a ket subtree and skip it.
 
     Returns the path in the reference's slot-step convention (planner.py:34-54)
     over the given operand order; est_cost is the plain flop estimate."""
@@ -261,6 +267,17 @@ def plan_stage(op_labels, op_dims, op_class, op_is_prefix, open_labels, class_we
                                               hypersamples=hypersamples, seed=seed + 1, class_cap_log2=cc)
                 return [(ids[int(a)], ids[int(b)]) for a, b in m], wc, fl
 
+            # ket / bra halves of the near side: disconnected and mirror images of each other?
+            half = None
+            if op_mirror is not None and all(op_mirror[k] >= 0 and op_mirror[k] in near for k in gv):
+                ket = [k for k in gv if k < op_mirror[k]]
+                ket_set = set(ket)
+                ket_labels = {lb for k in ket for lb in op_labels[k]}
+                bra_labels = {lb for k in gv if k not in ket_set for lb in op_labels[k]}
+                order_ok = all(op_mirror[a] < op_mirror[b] for a, b in zip(ket, ket[1:]))
+                if len(ket) * 2 == len(gv) and not (ket_labels & bra_labels) and order_ok:
+                    half = ket
+            search = half if half is not None else gv
             # near side: the hoisted classes are searched under several record caps.  Hoisted
             # merges are nearly free in the batch-weighted cost, so an uncapped greedy keeps
             # merging them into blobs that the per-item steps then have to slice; a small cap
@@ -268,9 +285,16 @@ def plan_stage(op_labels, op_dims, op_class, op_is_prefix, open_labels, class_we
             mv, wv, fv = None, math.inf, 0.0
             for rec_cap in (4.0, 5.0, 6.0, 7.0, 8.0, 10.0, 13.0, record_cap_log2):
                 cc = [min(rec_cap, record_cap_log2)] * (n_cls - 1) + [item_cap_log2]
-                m_, w_, f_ = sub(gv, class_weight, cc)
+                m_, w_, f_ = sub(search, class_weight, cc)
                 if w_ < wv:
                     mv, wv, fv = m_, w_, f_
+            if half is not None:
+                # mirrored merges for the bra half (its subtrees are conjugate twins: free), then
+                # the outer product of the two halves
+                mv = list(mv) + [(op_mirror[a], op_mirror[b]) for a, b in mv] + \
+                    [(min(half[0], op_mirror[half[0]]), max(half[0], op_mirror[half[0]]))]
+                wv += (2.0 ** (cut / 64.0) + kStepOverheadMacs) * class_weight[-1]
+                fv = 2 * fv + 2.0 ** (cut / 64.0)
             mm, wm, fm = sub(far, class_weight, [record_cap_log2] * n_cls)
             root = 2.0 ** (cut / 64.0 + log2_n)
             total = wv + wm + root * class_weight[-1]
@@ -281,6 +305,7 @@ def plan_stage(op_labels, op_dims, op_class, op_is_prefix, open_labels, class_we
 
 
 MAX_OPTIMAL_OPERANDS = 14
+kStepOverheadMacs = 48.0  # same constant as csrc/planner.cpp
 
 
 def find_path_optimal(net: TensorNetwork) -> ContractionPath:

@@ -16,6 +16,7 @@ def run_stage(programs, pool, kraus_row, prefix_bits, dtype=np.complex128):
     for p, pr in enumerate(programs):
         arena = np.zeros(pr.arena_fast + pr.arena_spill + 1, dtype=dtype)
         rec = np.zeros(max(pr.out_elems, pr.proj_d, 1), dtype=dtype)
+        records[p] = rec  # a pass may read back what it already wrote to its own record
 
         def resolve(kind, ref):
             if kind == 0:
@@ -31,7 +32,7 @@ def run_stage(programs, pool, kraus_row, prefix_bits, dtype=np.complex128):
             return records[kind - 2], ref
 
         for st in pr.steps:
-            ak, ar, bk, br, ok, orf, out_n, kn, lo_n, hi_n, tab, _ = (int(v) for v in st)
+            ak, ar, bk, br, ok, orf, out_n, kn, lo_n, hi_n, tab, flags = (int(v) for v in st)
             t = pr.tables
             loA = t[tab: tab + lo_n].astype(np.int64)
             loB = t[tab + lo_n: tab + 2 * lo_n].astype(np.int64)
@@ -44,7 +45,12 @@ def run_stage(programs, pool, kraus_row, prefix_bits, dtype=np.complex128):
             B, b_base = resolve(bk, br)
             ia = a_base + (hiA[:, None] + loA[None, :]).reshape(-1)[:, None] + kA[None, :]
             ib = b_base + (hiB[:, None] + loB[None, :]).reshape(-1)[:, None] + kB[None, :]
-            val = np.sum(A[ia] * B[ib], axis=1)
+            va, vb = A[ia], B[ib]
+            if flags & 1:
+                va = np.conj(va)
+            if flags & 2:
+                vb = np.conj(vb)
+            val = np.sum(va * vb, axis=1)
             if ok == 0:
                 assert orf + out_n <= pr.arena_fast + pr.arena_spill
                 arena[orf: orf + out_n] = val

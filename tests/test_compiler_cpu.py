@@ -122,3 +122,16 @@ def test_arena_buffers_never_overlap_live_values(golden_cases):
             for k, r in ((ak, ar), (bk, br)):
                 if k == 0:
                     live.pop(r, None)
+
+
+def test_bra_subtrees_are_conjugate_twins_not_recomputed(golden_cases):
+    """The bra half of the per-item network is the conjugate of the ket half
+    (reference engine.py:393 builds it with np.conj): the compiler reads the ket
+    results with a conjugation flag instead of contracting the bra half again."""
+    pipe, tables, es = _pipeline(golden_cases["hea8"], hypersamples=16)
+    flagged = sum(int(np.count_nonzero(pr.steps[:, 11])) for pr in pipe.compiled.programs if len(pr.steps))
+    assert flagged >= 1
+    # and the emulated programs still reproduce the reference marginals (checked per case above)
+    j = pipe.plan.f
+    top = pipe.programs_of(j)[-1]
+    assert top.proj_d >= 1 and top.result_kind == 3
