@@ -209,7 +209,7 @@ def test_low_weight_trajectories_are_sampled_not_dropped():
     such error sets are sampled from their normalised distribution."""
     c, _ = workloads.hea(8, 3, gamma=1e-4, p=0.0, seed=9)
     labels = [g.noise.identity_label() for g in c.gates]
-    hit = [s for s, g in enumerate(c.gates) if g.noise.kind == "amplitude_damping"][20:25]
+    hit = [s for s, g in enumerate(c.gates) if g.noise.kind == "amplitude_damping" and g.kind == "Ry"][10:15]  # distinct qubits
     for s in hit:
         labels[s] = "K1"
     es = [ErrorSet(3, tuple(labels), 30000)]
