@@ -56,7 +56,9 @@ enum { PTSBE_C64 = 0, PTSBE_C128 = 1 };
  * steps  : n_steps x 12 words {a_kind, a_ref, b_kind, b_ref, o_kind, o_ref,
  *                              out_n, k_n, lo_n, hi_n, tab_off, conj}
  *          conj bit 0 / 1: operand A / B is read complex-conjugated (its node is the
- *          conjugate twin -- bra copy -- of the node that was actually computed)
+ *          conjugate twin -- bra copy -- of the node that was actually computed);
+ *          bit 2: B is a prefix-bit basis vector e_x contracted over its only label, so the
+ *          step is the slice out[c] = A[.. + kA[x]] (no multiply-adds)
  *          operand kind 0: arena offset (elements), 1: leaf index,
  *                       2 + p: record of pass p of the same stage, a_ref = offset in record
  *          output  kind 0: arena offset, 1: offset in this pass's output record
@@ -202,12 +204,14 @@ int ptsbe_histogram_merge(const uint64_t* keys, const uint64_t* counts, uint64_t
  *   of its result across the batch (error-independent hoisting);
  *   class_cap_log2 (optional) is a soft cap on log2(result entries) per class
  *   (records of hoisted classes may be larger than per-item on-chip buffers),
- *   size_cap_log2 the default for classes without one (0 = none).
+ *   size_cap_log2 the default for classes without one (0 = none);
+ *   op_unit (optional) marks rank-1 basis-vector operands (prefix projectors):
+ *   contracting one selects a slice of the other operand and is costed as such.
  *   merges_out [2*(n_ops-1)] stable-id pairs (result keeps the smaller id). */
 int ptsbe_plan_greedy(uint32_t n_ops, const uint32_t* op_ptr, const int64_t* labels,
                       const uint32_t* dims, const uint32_t* op_class,
                       const double* class_weight, const double* class_cap_log2,
-                      uint32_t n_classes, uint32_t hypersamples,
+                      const uint8_t* op_unit, uint32_t n_classes, uint32_t hypersamples,
                       uint64_t seed, double size_cap_log2, uint32_t* merges_out,
                       double* cost_out, double* flops_out);
 

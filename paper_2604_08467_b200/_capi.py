@@ -97,7 +97,7 @@ def load() -> ctypes.CDLL:
     lib.ptsbe_batch_destroy.restype = None
     lib.ptsbe_histogram_merge.argtypes = [P, P, U64, U32, ctypes.POINTER(P), ctypes.POINTER(P),
                                           ctypes.POINTER(U64), I]
-    lib.ptsbe_plan_greedy.argtypes = [U32, P, P, P, P, P, P, U32, U32, U64, ctypes.c_double, P,
+    lib.ptsbe_plan_greedy.argtypes = [U32, P, P, P, P, P, P, P, U32, U32, U64, ctypes.c_double, P,
                                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
     lib.ptsbe_free.argtypes = [P]
     lib.ptsbe_free.restype = None
@@ -321,7 +321,7 @@ def measure_fma_peak(device: int = 0) -> tuple:
 
 
 def plan_greedy(op_labels, op_dims, op_class=None, class_weight=None, hypersamples=100,
-                seed=0, size_cap_log2=0.0, class_cap_log2=None):
+                seed=0, size_cap_log2=0.0, class_cap_log2=None, op_unit=None):
     """Host planner core (csrc/planner.cpp).  Returns (merges [(x, y)...] over
     stable operand ids, weighted cost, reference flop estimate)."""
     n = len(op_labels)
@@ -335,9 +335,10 @@ def plan_greedy(op_labels, op_dims, op_class=None, class_weight=None, hypersampl
     cc = None if class_cap_log2 is None else np.ascontiguousarray(class_cap_log2, dtype=np.float64)
     if cc is not None and (cw is None or cc.size != cw.size):
         raise ValueError("class_cap_log2 needs class_weight of the same length")
+    un = None if op_unit is None else np.ascontiguousarray(op_unit, dtype=np.uint8)
     merges = np.zeros(2 * max(n - 1, 1), dtype=np.uint32)
     cost, flops = ctypes.c_double(), ctypes.c_double()
-    check(load().ptsbe_plan_greedy(n, _ptr(ptr), _ptr(labels), _ptr(dims), _ptr(cls), _ptr(cw), _ptr(cc),
+    check(load().ptsbe_plan_greedy(n, _ptr(ptr), _ptr(labels), _ptr(dims), _ptr(cls), _ptr(cw), _ptr(cc), _ptr(un),
                                    0 if cw is None else cw.size, hypersamples, seed & (2**64 - 1),
                                    float(size_cap_log2), _ptr(merges), ctypes.byref(cost),
                                    ctypes.byref(flops)))

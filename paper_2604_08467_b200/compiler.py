@@ -366,10 +366,23 @@ def compile_stage(
 
         for nid in mine:
             nd = nodes[nid]
-            na, nb = nodes[nd.a], nodes[nd.b]
-            a_kind, a_ref = ref_of(nd.a)
-            b_kind, b_ref = ref_of(nd.b)
-            conj_flags = (1 if nd.a in virt else 0) | (2 if nd.b in virt else 0)
+            ca, cb = nd.a, nd.b
+            # a prefix-bit basis vector contracted over its only label selects a slice of the
+            # other operand: make it operand B and flag the step (bit 2), the executor then
+            # gathers instead of multiplying
+            def is_selector(x, other):
+                return (x < n_leaves and operands[x].sel_kind == SEL_PREFIX and len(nodes[x].labels) == 1
+                        and nodes[x].labels[0] in nodes[other].labels)
+            select = False
+            if is_selector(ca, cb):
+                ca, cb = cb, ca
+                select = True
+            elif is_selector(cb, ca):
+                select = True
+            na, nb = nodes[ca], nodes[cb]
+            a_kind, a_ref = ref_of(ca)
+            b_kind, b_ref = ref_of(cb)
+            conj_flags = (1 if ca in virt else 0) | (2 if cb in virt else 0) | (4 if select else 0)
             if nid in rec_off:
                 o_kind, o_ref = 1, rec_off[nid]
             else:
@@ -403,7 +416,7 @@ def compile_stage(
                 [a_kind, a_ref, b_kind, b_ref, o_kind, o_ref, nd.size, k_n, lo_n, hi_n, tab_off, conj_flags]
             )
             tab_off += words.size
-            flops += float(nd.size) * k_n
+            flops += 0.5 * float(nd.size) if select else float(nd.size) * k_n
             if nid == root:
                 result_kind, result_ref = (2 + p, o_ref) if o_kind == 1 else (0, o_ref)
         if p == top and proj is not None:

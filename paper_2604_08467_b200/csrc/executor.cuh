@@ -210,6 +210,24 @@ __global__ void exec_kernel(const ExecArgs a) {
       t.hiB = t.hiA + t.hi_n;
       t.kA = t.hiB + t.hi_n;
       t.kB = t.kA + kn;
+      if (t.conj & 4) {
+        // B is the basis vector e_x of a measured bit, contracted over its only label:
+        // out[c] = A[a0(c) + kA[x]] -- a gather, no multiply-adds
+        const uint32_t x = (B[__ldg(t.kB)].x == R(0)) ? 1u : 0u;
+        const uint32_t off = __ldg(t.kA + x);
+        const bool pow2 = (t.lo_n & (t.lo_n - 1)) == 0;
+        const int sh = 31 - __clz(t.lo_n);
+        const bool fa = t.conj & 1;
+        for (uint32_t c = tid; c < t.out_n; c += gsize) {
+          uint32_t cl, ch;
+          if (pow2) { cl = c & (t.lo_n - 1); ch = c >> sh; }
+          else { ch = c / t.lo_n; cl = c - ch * t.lo_n; }
+          uint32_t a0 = __ldg(t.loA + cl);
+          if (t.hi_n > 1) a0 += __ldg(t.hiA + ch);
+          const C v = ld_conj(A + a0 + off, fa);
+          if (store) O[(size_t)c * o_stride] = v;
+        }
+      } else
       switch (kn) {
         case 1: step_fixed_k<C, 1>(A, B, O, o_stride, t, tid, gsize, store); break;
         case 2: step_fixed_k<C, 2>(A, B, O, o_stride, t, tid, gsize, store); break;

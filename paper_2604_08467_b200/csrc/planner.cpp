@@ -53,6 +53,7 @@ struct Problem {
   std::vector<std::vector<int32_t>> labels;  // dense label ids, sorted
   std::vector<double> log2dim;               // per label
   std::vector<uint32_t> cls;
+  std::vector<uint8_t> unit;  // 1: rank-1 basis vector (prefix projector): merging it is a gather, not a contraction
   std::vector<double> logw;  // log class weight
   uint32_t n_labels;
   std::vector<double> cap_log2;  // per class
@@ -67,6 +68,7 @@ static Descent descend(const Problem& P, Rng& rng, double temperature, double ga
   const uint32_t n = P.n;
   std::vector<std::vector<int32_t>> lab = P.labels;
   std::vector<uint32_t> cls = P.cls, version(n, 0);
+  std::vector<uint8_t> unit = P.unit;
   std::vector<char> alive(n, 1);
   std::vector<double> lsize(n, 0.0);
   std::vector<int32_t> own(2 * (size_t)P.n_labels, -1);
@@ -95,8 +97,11 @@ static Descent descend(const Problem& P, Rng& rng, double temperature, double ga
     if (x > y) std::swap(x, y);
     double lu, ls, lo;
     measure(x, y, lu, ls, lo);
-    // reference score: flops(step) - prod(shared dims), compared in log space
-    const double score = std::max(0.0, std::exp2(std::min(lu, 1000.0)) - std::exp2(ls));
+    // reference score: flops(step) - prod(shared dims), compared in log space; absorbing a basis
+    // vector only selects a slice of the other operand (half a multiply-add per output entry)
+    const bool slice = unit[x] || unit[y];
+    const double score = slice ? 0.5 * std::exp2(lo)
+                               : std::max(0.0, std::exp2(std::min(lu, 1000.0)) - std::exp2(ls));
     double key = std::log1p(score) + gamma * P.logw[std::max(cls[x], cls[y])];
     const double cap = P.cap_log2[std::max(cls[x], cls[y])];
     if (lo > cap) key += 50.0 * (lo - cap) + 100.0;
@@ -139,7 +144,7 @@ static Descent descend(const Problem& P, Rng& rng, double temperature, double ga
     double lu, ls, lo;
     measure(x, y, lu, ls, lo);
     const uint32_t c = std::max(cls[x], cls[y]);
-    const double fl = std::exp2(std::min(lu, 1000.0));
+    const double fl = (unit[x] || unit[y]) ? 0.5 * std::exp2(lo) : std::exp2(std::min(lu, 1000.0));
     D.flops += fl;
     // every interpreted step costs the executor a fixed dispatch (table fetch, sync) on top of
     // its multiply-adds
@@ -161,6 +166,7 @@ static Descent descend(const Problem& P, Rng& rng, double temperature, double ga
     lab[y].shrink_to_fit();
     alive[y] = 0;
     cls[x] = c;
+    unit[x] = 0;
     lsize[x] = lo;
     version[x]++;
     D.merges.push_back(x);
@@ -184,8 +190,8 @@ static Descent descend(const Problem& P, Rng& rng, double temperature, double ga
 extern "C" int ptsbe_plan_greedy(uint32_t n_ops, const uint32_t* op_ptr, const int64_t* labels,
                                  const uint32_t* dims, const uint32_t* op_class,
                                  const double* class_weight, const double* class_cap_log2,
-                                 uint32_t n_classes, uint32_t hypersamples, uint64_t seed,
-                                 double size_cap_log2,
+                                 const uint8_t* op_unit, uint32_t n_classes, uint32_t hypersamples,
+                                 uint64_t seed, double size_cap_log2,
                                  uint32_t* merges_out, double* cost_out, double* flops_out) {
   if (n_ops < 1 || hypersamples < 1 || !op_ptr || !merges_out) return PTSBE_EINVAL;
   if (const char* ov = getenv("PTSBE_STEP_OVERHEAD")) kStepOverheadMacs = atof(ov);
@@ -193,6 +199,7 @@ extern "C" int ptsbe_plan_greedy(uint32_t n_ops, const uint32_t* op_ptr, const i
   P.n = n_ops;
   P.labels.resize(n_ops);
   P.cls.assign(n_ops, 0);
+  P.unit.assign(n_ops, 0);
   // densify labels
   std::vector<int64_t> uniq(labels, labels + op_ptr[n_ops]);
   std::sort(uniq.begin(), uniq.end());
@@ -209,6 +216,7 @@ extern "C" int ptsbe_plan_greedy(uint32_t n_ops, const uint32_t* op_ptr, const i
     }
     std::sort(P.labels[t].begin(), P.labels[t].end());
     if (op_class) P.cls[t] = op_class[t];
+    if (op_unit && op_unit[t] && op_ptr[t + 1] - op_ptr[t] == 1) P.unit[t] = 1;
   }
   uint32_t nc = std::max<uint32_t>(1, n_classes);
   P.logw.assign(nc, 0.0);

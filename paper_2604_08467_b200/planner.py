@@ -239,8 +239,10 @@ def plan_stage(op_labels, op_dims, op_class, op_is_prefix, open_labels, class_we
     caps = [record_cap_log2] * (n_cls - 1) + [item_cap_log2]
     if n_cls == 1:
         caps = [record_cap_log2]
+    unit = [1 if u else 0 for u in op_is_prefix]
     merges, wcost, flops = _capi.plan_greedy(op_labels, op_dims, op_class=op_class, class_weight=class_weight,
-                                             hypersamples=hypersamples, seed=seed, class_cap_log2=caps)
+                                             hypersamples=hypersamples, seed=seed, class_cap_log2=caps,
+                                             op_unit=unit)
     best = (wcost, merges, flops)
     sources = [k for k in range(n) if op_is_prefix[k]]
     opens = set(open_labels)
@@ -264,7 +266,8 @@ def plan_stage(op_labels, op_dims, op_class, op_is_prefix, open_labels, class_we
                     return [], 0.0, 0.0
                 m, wc, fl = _capi.plan_greedy([op_labels[k] for k in ids], [op_dims[k] for k in ids],
                                               op_class=[op_class[k] for k in ids], class_weight=cw,
-                                              hypersamples=hypersamples, seed=seed + 1, class_cap_log2=cc)
+                                              hypersamples=hypersamples, seed=seed + 1, class_cap_log2=cc,
+                                              op_unit=[unit[k] for k in ids])
                 return [(ids[int(a)], ids[int(b)]) for a, b in m], wc, fl
 
             # ket / bra halves of the near side: disconnected and mirror images of each other?
