@@ -416,7 +416,7 @@ def compile_stage(
                 [a_kind, a_ref, b_kind, b_ref, o_kind, o_ref, nd.size, k_n, lo_n, hi_n, tab_off, conj_flags]
             )
             tab_off += words.size
-            flops += 0.5 * float(nd.size) if select else float(nd.size) * k_n
+            flops += float(nd.size) if select else float(nd.size) * k_n
             if nid == root:
                 result_kind, result_ref = (2 + p, o_ref) if o_kind == 1 else (0, o_ref)
         if p == top and proj is not None:

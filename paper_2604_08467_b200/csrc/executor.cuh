@@ -164,6 +164,11 @@ __global__ void exec_kernel(const ExecArgs a) {
     const uint8_t* sel = a.kraus + (size_t)e * a.g;  // Kraus-index row: shared by all items of the error set (L1/L2)
     group_sync();
 
+    // measured bit selected by a prefix-projector leaf (slice steps read the bit, not the vector)
+    auto leaf_bit = [&](uint32_t ref) -> uint32_t {
+      const uint4 lf = __ldg(reinterpret_cast<const uint4*>(a.leaves) + ref);
+      return (uint32_t)((pfx[lf.w >> 6] >> (63 - (lf.w & 63))) & 1ull);
+    };
     auto resolve = [&](uint32_t kind, uint32_t ref) -> const C* {
       if (kind == 0) return ref < a.arena_fast ? arena + ref : spill + (ref - a.arena_fast);
       if (kind == 1) {
@@ -183,8 +188,9 @@ __global__ void exec_kernel(const ExecArgs a) {
       const uint4* st4 = reinterpret_cast<const uint4*>(a.steps + (size_t)s * STEP_WORDS);
       // s0 = {a_kind, a_ref, b_kind, b_ref}, s1 = {o_kind, o_ref, out_n, k_n}, s2 = {lo_n, hi_n, tab_off, -}
       const uint4 s0 = __ldg(st4), s1 = __ldg(st4 + 1), s2 = __ldg(st4 + 2);
+      const bool slice = (s2.w & 4u) != 0;
       const C* A = resolve(s0.x, s0.y);
-      const C* B = resolve(s0.z, s0.w);
+      const C* B = slice ? nullptr : resolve(s0.z, s0.w);
       C* O;
       size_t o_stride = 1;
       bool store = true;
@@ -210,11 +216,11 @@ __global__ void exec_kernel(const ExecArgs a) {
       t.hiB = t.hiA + t.hi_n;
       t.kA = t.hiB + t.hi_n;
       t.kB = t.kA + kn;
-      if (t.conj & 4) {
+      if (slice) {
         // B is the basis vector e_x of a measured bit, contracted over its only label:
         // out[c] = A[a0(c) + kA[x]] -- a gather, no multiply-adds
-        const uint32_t x = (B[__ldg(t.kB)].x == R(0)) ? 1u : 0u;
-        const uint32_t off = __ldg(t.kA + x);
+        const uint32_t k0 = __ldg(t.kA), k1 = __ldg(t.kA + 1);
+        const uint32_t off = leaf_bit(s0.w) ? k1 : k0;
         const bool pow2 = (t.lo_n & (t.lo_n - 1)) == 0;
         const int sh = 31 - __clz(t.lo_n);
         const bool fa = t.conj & 1;

@@ -98,9 +98,9 @@ static Descent descend(const Problem& P, Rng& rng, double temperature, double ga
     double lu, ls, lo;
     measure(x, y, lu, ls, lo);
     // reference score: flops(step) - prod(shared dims), compared in log space; absorbing a basis
-    // vector only selects a slice of the other operand (half a multiply-add per output entry)
+    // vector only selects a slice of the other operand (one load and one store per output entry, about a multiply-add)
     const bool slice = unit[x] || unit[y];
-    const double score = slice ? 0.5 * std::exp2(lo)
+    const double score = slice ? std::exp2(lo)
                                : std::max(0.0, std::exp2(std::min(lu, 1000.0)) - std::exp2(ls));
     double key = std::log1p(score) + gamma * P.logw[std::max(cls[x], cls[y])];
     const double cap = P.cap_log2[std::max(cls[x], cls[y])];
@@ -144,7 +144,7 @@ static Descent descend(const Problem& P, Rng& rng, double temperature, double ga
     double lu, ls, lo;
     measure(x, y, lu, ls, lo);
     const uint32_t c = std::max(cls[x], cls[y]);
-    const double fl = (unit[x] || unit[y]) ? 0.5 * std::exp2(lo) : std::exp2(std::min(lu, 1000.0));
+    const double fl = (unit[x] || unit[y]) ? std::exp2(lo) : std::exp2(std::min(lu, 1000.0));
     D.flops += fl;
     // every interpreted step costs the executor a fixed dispatch (table fetch, sync) on top of
     // its multiply-adds

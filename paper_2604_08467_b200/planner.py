@@ -261,12 +261,12 @@ def plan_stage(op_labels, op_dims, op_class, op_is_prefix, open_labels, class_we
         if near and far and cut / 64.0 + log2_n <= record_cap_log2 and cut / 64.0 <= item_cap_log2:
             gv = sorted(near)
 
-            def sub(ids, cw, cc):
+            def sub(ids, cw, cc, hs=hypersamples):
                 if len(ids) == 1:
                     return [], 0.0, 0.0
                 m, wc, fl = _capi.plan_greedy([op_labels[k] for k in ids], [op_dims[k] for k in ids],
                                               op_class=[op_class[k] for k in ids], class_weight=cw,
-                                              hypersamples=hypersamples, seed=seed + 1, class_cap_log2=cc,
+                                              hypersamples=hs, seed=seed + 1, class_cap_log2=cc,
                                               op_unit=[unit[k] for k in ids])
                 return [(ids[int(a)], ids[int(b)]) for a, b in m], wc, fl
 
@@ -288,7 +288,9 @@ def plan_stage(op_labels, op_dims, op_class, op_is_prefix, open_labels, class_we
             mv, wv, fv = None, math.inf, 0.0
             for rec_cap in (4.0, 5.0, 6.0, 7.0, 8.0, 10.0, 13.0, record_cap_log2):
                 cc = [min(rec_cap, record_cap_log2)] * (n_cls - 1) + [item_cap_log2]
-                m_, w_, f_ = sub(search, class_weight, cc)
+                # the near side is small (a few hundred operands) and decides the per-item cost:
+                # it gets many more descents than the rest
+                m_, w_, f_ = sub(search, class_weight, cc, hs=NEAR_SIDE_DESCENTS * hypersamples)
                 if w_ < wv:
                     mv, wv, fv = m_, w_, f_
             if half is not None:
@@ -309,6 +311,7 @@ def plan_stage(op_labels, op_dims, op_class, op_is_prefix, open_labels, class_we
 
 MAX_OPTIMAL_OPERANDS = 14
 kStepOverheadMacs = 48.0  # same constant as csrc/planner.cpp
+NEAR_SIDE_DESCENTS = 8    # multiplier on hypersamples for the near-side search
 
 
 def find_path_optimal(net: TensorNetwork) -> ContractionPath:
