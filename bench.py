@@ -437,7 +437,7 @@ def main():
                 cands.append((marg[j], f"exec_kernel (per-item steps -> v[{pr.proj_d}]), stage {j + 1}", n_items, launches_j,
                               pr.ext_read_elems * elem + 8 + 8 * words + pr.proj_d * elem, 8.0 * pr.flops))
                 # projection: v read, population vector written, M read once per error set and launch
-                m_bytes = pr.proj_d * pr.out_elems * elem * sets * launches_j / max(n_items, 1)
+                m_bytes = pr.proj_d * pr.out_elems * elem * (sets * args.steps + launches_j) / max(n_items, 1)
                 cands.append((projm[j], f"project_kernel (P = Re(v.M), D={pr.proj_d}, N={pr.out_elems}), stage {j + 1}",
                               n_items, launches_j, pr.proj_d * elem + pr.out_elems * real + m_bytes,
                               4.0 * pr.proj_d * pr.out_elems))
@@ -475,6 +475,9 @@ def main():
                 "sampler": [s / args.steps for s in samp], "compaction": [x / args.steps for x in comp],
                 "histogram": hist_ms / args.steps, "stage_total": [sum(float(s.stage_ms[j]) for s in stats) / args.steps for j in range(f)],
             },
+            "programs": [[{"steps": int(len(pr.steps)), "macs": float(pr.flops), "arena": int(pr.arena_fast),
+                           "lanes": int(pr.threads), "proj_d": int(pr.proj_d), "record": int(pr.out_elems)}
+                          for pr in pipe.programs_of(j + 1)] for j in range(f)],
             "roofline": {
                 "kernel": top_name + (" <float>" if dtype == "complex64" else " <double>"),
                 "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",

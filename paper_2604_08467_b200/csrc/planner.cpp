@@ -19,6 +19,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <queue>
+#include <thread>
 #include <vector>
 
 #include "../../include/ptsbe_b200.h"
@@ -37,7 +38,7 @@ struct Rng {  // splitmix64
   double uniform() { return ((next() >> 11) + 0.5) * (1.0 / 9007199254740992.0); }
 };
 
-static double kStepOverheadMacs = 48.0;  // PTSBE_STEP_OVERHEAD overrides (experiments)
+static double kStepOverheadMacs = 20.0;  // PTSBE_STEP_OVERHEAD overrides (experiments)
 
 struct Cand {
   double key, tie;
@@ -227,20 +228,48 @@ extern "C" int ptsbe_plan_greedy(uint32_t n_ops, const uint32_t* op_ptr, const i
   }
   for (uint32_t t = 0; t < n_ops; ++t)
     if (P.cls[t] >= nc) return PTSBE_EINVAL;
-  Rng rng(seed * 0x9E3779B97F4A7C15ull + 0x1234567ull);
-  Descent best;
-  bool have = false;
   // The search score is flops x weight^gamma.  gamma = 1 hoists as much as possible out of
   // the per-item classes but lets nearly-free low-class merges run ahead and build blobs the
   // per-item steps then have to chew through; gamma = 0 is the reference's plain greedy, which
   // absorbs the rank-1 prefix projectors first and keeps per-item tensors tiny.  Every descent
   // is judged by the true batch-weighted cost (gamma = 1), so the mix costs nothing.
+  // Descents are independent: they run on host threads, descent h always uses the stream
+  // seeded by (seed, h), so the result does not depend on the thread count.
   static const double gammas[3] = {1.0, 0.5, 0.0};
-  for (uint32_t h = 0; h < hypersamples; ++h) {
-    const double gamma = gammas[h % 3];
-    const double temperature = h < 3 ? 0.0 : ((h / 3) % 2 ? 1.0 : 0.5);
-    Descent d = descend(P, rng, temperature, gamma);
-    if (!have || d.weighted < best.weighted) { best = std::move(d); have = true; }
+  unsigned n_threads = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32u));
+  if (const char* tv = getenv("PTSBE_PLANNER_THREADS")) n_threads = std::max(1, atoi(tv));
+  n_threads = std::min<unsigned>(n_threads, hypersamples);
+  std::vector<Descent> bests(n_threads);
+  std::vector<uint32_t> best_h(n_threads, UINT32_MAX);
+  auto worker = [&](unsigned tix) {
+    for (uint32_t h = tix; h < hypersamples; h += n_threads) {
+      Rng rng((seed + 0x632BE59BD9B4E019ull * (h + 1)) * 0x9E3779B97F4A7C15ull + 0x1234567ull);
+      const double gamma = gammas[h % 3];
+      const double temperature = h < 3 ? 0.0 : ((h / 3) % 2 ? 1.0 : 0.5);
+      Descent d = descend(P, rng, temperature, gamma);
+      if (best_h[tix] == UINT32_MAX || d.weighted < bests[tix].weighted) {
+        bests[tix] = std::move(d);
+        best_h[tix] = h;
+      }
+    }
+  };
+  if (n_threads == 1) {
+    worker(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < n_threads; ++t) pool.emplace_back(worker, t);
+    for (auto& th : pool) th.join();
+  }
+  Descent best;
+  uint32_t bh = UINT32_MAX;
+  for (unsigned t = 0; t < n_threads; ++t) {
+    if (best_h[t] == UINT32_MAX) continue;
+    // ties go to the lowest descent index: same answer for any thread count
+    if (bh == UINT32_MAX || bests[t].weighted < best.weighted ||
+        (bests[t].weighted == best.weighted && best_h[t] < bh)) {
+      best = std::move(bests[t]);
+      bh = best_h[t];
+    }
   }
   std::copy(best.merges.begin(), best.merges.end(), merges_out);
   if (cost_out) *cost_out = best.weighted;
