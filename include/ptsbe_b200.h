@@ -58,7 +58,10 @@ enum { PTSBE_C64 = 0, PTSBE_C128 = 1 };
  *          conj bit 0 / 1: operand A / B is read complex-conjugated (its node is the
  *          conjugate twin -- bra copy -- of the node that was actually computed);
  *          bit 2: B is a prefix-bit basis vector e_x contracted over its only label, so the
- *          step is the slice out[c] = A[.. + kA[x]] (no multiply-adds)
+ *          step is the slice out[c] = A[.. + kA[x]] (no multiply-adds);
+ *          bit 3: slice views -- the step's table block ends with [nA, (qubit, stride) x nA,
+ *          nB, (qubit, stride) x nB]: operand bases advance by stride when the measured bit
+ *          of that qubit is 1 (the operand is a slice of a stored tensor, never materialised)
  *          operand kind 0: arena offset (elements), 1: leaf index,
  *                       2 + p: record of pass p of the same stage, a_ref = offset in record
  *          output  kind 0: arena offset, 1: offset in this pass's output record

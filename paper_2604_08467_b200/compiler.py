@@ -277,15 +277,61 @@ def compile_stage(
     def real_of(nid: int) -> int:
         return virt.get(nid, nid)
 
-    # consumers of a computed node: its own parent plus the parents of its virtual twins
+    # slice views --------------------------------------------------------------
+    # Contracting a prefix-bit basis vector e_x over its only label selects the slice
+    # T[.., x, ..] of the other operand.  Such a node is never materialised: it is a VIEW of
+    # T's storage (T's strides minus that label, base offset + bit(q) * stride), and its
+    # consumers gather straight from T.  Exceptions (materialised by a gather step): views
+    # that must live in a record -- consumed by a later pass than the one holding T's buffer,
+    # the projection vector, the root.
+    def selector_of(nid: int):
+        """(selector leaf, other child) when node nid is a slice, else None."""
+        nd = nodes[nid]
+        for x, other in ((nd.a, nd.b), (nd.b, nd.a)):
+            if (x < n_leaves and operands[x].sel_kind == SEL_PREFIX and len(nodes[x].labels) == 1
+                    and nodes[x].labels[0] in nodes[other].labels):
+                return x, other
+        return None
+
+    view: dict[int, tuple] = {}  # view node -> (child it slices, label, qubit)
+
+    def storage_of(nid: int):
+        """(materialised node or leaf, conj?, [(qubit, label)...]) behind a node."""
+        conj, terms = False, []
+        while True:
+            if nid in virt:
+                nid = virt[nid]
+                conj = not conj
+                continue
+            if nid in view:
+                child, lb, q = view[nid]
+                terms.append((q, lb))
+                nid = child
+                continue
+            return nid, conj, terms
+
+    for nid in range(n_leaves, len(nodes)):
+        if nid in virt or nid == root or (proj is not None and nid in proj):
+            continue
+        sel = selector_of(nid)
+        if sel is None:
+            continue
+        base, _, _ = storage_of(sel[1])
+        # the buffer behind the view must be readable where the view is consumed: a leaf, or a
+        # node of the same pass as the view's own pass, or of an earlier pass (then it is a record)
+        if base >= n_leaves and nodes[base].pass_ > nodes[nid].pass_:
+            continue
+        view[nid] = (sel[1], nodes[sel[0]].labels[0], operands[sel[0]].sel_arg)
+
+    # consumers of a materialised node: every computed step that reads its storage, directly,
+    # through a conjugate twin or through slice views
     consumers: dict[int, list[int]] = {}
-    for nid in range(len(nodes)):
-        if nid in virt:
+    for nid in range(n_leaves, len(nodes)):
+        if nid in virt or nid in view:
             continue
         nd = nodes[nid]
-        if nid >= n_leaves:
-            for ch in (nd.a, nd.b):
-                consumers.setdefault(real_of(ch), []).append(nid)
+        for ch in (nd.a, nd.b):
+            consumers.setdefault(storage_of(ch)[0], []).append(nid)
 
     # storage decisions ------------------------------------------------------
     # frontier = computed node consumed by a later pass -> lives in its pass's record
@@ -293,7 +339,7 @@ def compile_stage(
     rec_size = [0] * n_passes
     for nid in range(n_leaves, len(nodes)):
         nd = nodes[nid]
-        if nid in virt:
+        if nid in virt or nid in view:
             continue
         if any(nodes[c].pass_ > nd.pass_ for c in consumers.get(nid, ())):
             rec_off[nid] = rec_size[nd.pass_]
@@ -305,12 +351,12 @@ def compile_stage(
     programs: list[Program] = []
     result_kind, result_ref = 0, 0
     for p in range(n_passes):
-        mine = [nid for nid in range(n_leaves, len(nodes)) if nodes[nid].pass_ == p and nid not in virt]
+        mine = [nid for nid in range(n_leaves, len(nodes)) if nodes[nid].pass_ == p and nid not in virt and nid not in view]
         if proj is not None and p == top:
             mine = [nid for nid in mine if nid != root]
         # sizing of the on-chip arena: try everything on chip, spill the big buffers otherwise
         max_out = max([nodes[nid].size for nid in mine], default=1)
-        peak = _place(nodes, mine, rec_off, real_of, fast_cap=None)[1]
+        peak = _place(nodes, mine, rec_off, lambda x: storage_of(x)[0], fast_cap=None)[1]
         if max_out <= 512 and peak * elem_bytes <= WARP_ARENA_BYTES:
             # sub-warp groups: GS lanes per item, 32 / GS items per warp in lockstep.  Pick the
             # group size with the fewest issued warp-instructions per item (rough model of
@@ -333,7 +379,7 @@ def compile_stage(
             while threads < 512 and threads * 4 < max_out:
                 threads *= 2
             fast_cap = min(peak, SMEM_BYTES // elem_bytes)
-        where, peak_fast, peak_spill = _place(nodes, mine, rec_off, real_of, fast_cap=fast_cap)
+        where, peak_fast, peak_spill = _place(nodes, mine, rec_off, lambda x: storage_of(x)[0], fast_cap=fast_cap)
 
         step_rows, tables = [], []
         tab_off = 0
@@ -342,8 +388,8 @@ def compile_stage(
         prog_leaf_index: dict[int, int] = {}
         ext_reads: dict[int, int] = {}
 
-        def ref_of(nid: int):
-            nid = real_of(nid)
+        def ref_of(nid: int, sliced: int = 0):
+            """(kind, ref) of a MATERIALISED node or leaf."""
             if nid < n_leaves:
                 at = prog_leaf_index.get(nid)
                 if at is None:
@@ -358,31 +404,42 @@ def compile_stage(
                 # lives in a record: of an earlier pass, or of this very pass (a node that also
                 # feeds a later pass; the group wrote it before the barrier that precedes this step)
                 if nodes[nid].pass_ != p:
-                    ext_reads[nid] = nodes[nid].size
+                    ext_reads[nid] = max(ext_reads.get(nid, 0), nodes[nid].size >> sliced)
                 elif p == top:
                     raise AssertionError("the projection vector is consumed by the projection kernel only")
                 return 2 + nodes[nid].pass_, rec_off[nid]
             return 0, where[nid]
 
+        def layout(nid: int):
+            """(materialised base, conj?, strides aligned with nodes[nid].labels,
+            [(qubit, stride)] dynamic offset terms) of an operand."""
+            if nid in virt:
+                b, cj, st, tm = layout(virt[nid])
+                return b, not cj, st, tm
+            if nid in view:
+                child, lb, q = view[nid]
+                b, cj, st, tm = layout(child)
+                pos = nodes[child].labels.index(lb)
+                return b, cj, st[:pos] + st[pos + 1:], tm + [(q, st[pos])]
+            return nid, False, _row_major_strides(nodes[nid].dims), []
+
         for nid in mine:
             nd = nodes[nid]
             ca, cb = nd.a, nd.b
-            # a prefix-bit basis vector contracted over its only label selects a slice of the
-            # other operand: make it operand B and flag the step (bit 2), the executor then
-            # gathers instead of multiplying
-            def is_selector(x, other):
-                return (x < n_leaves and operands[x].sel_kind == SEL_PREFIX and len(nodes[x].labels) == 1
-                        and nodes[x].labels[0] in nodes[other].labels)
+            # a slice that has to be materialised (it feeds a record): the basis vector becomes
+            # operand B and the step is flagged (bit 2), the executor gathers instead of multiplying
             select = False
-            if is_selector(ca, cb):
-                ca, cb = cb, ca
-                select = True
-            elif is_selector(cb, ca):
+            sel = selector_of(nid)
+            if sel is not None:
+                ca, cb = sel[1], sel[0]
                 select = True
             na, nb = nodes[ca], nodes[cb]
-            a_kind, a_ref = ref_of(ca)
-            b_kind, b_ref = ref_of(cb)
-            conj_flags = (1 if ca in virt else 0) | (2 if cb in virt else 0) | (4 if select else 0)
+            base_a, conj_a, st_a, terms_a = layout(ca)
+            base_b, conj_b, st_b, terms_b = layout(cb)
+            a_kind, a_ref = ref_of(base_a, len(terms_a))
+            b_kind, b_ref = ref_of(base_b, len(terms_b))
+            dyn = bool(terms_a or terms_b)
+            conj_flags = (1 if conj_a else 0) | (2 if conj_b else 0) | (4 if select else 0) | (8 if dyn else 0)
             if nid in rec_off:
                 o_kind, o_ref = 1, rec_off[nid]
             else:
@@ -392,8 +449,8 @@ def compile_stage(
                 out_labels = list(nodes[proj[0]].labels) + list(open_order)
             dim_of = dict(zip(na.labels, na.dims))
             dim_of.update(zip(nb.labels, nb.dims))
-            sa = dict(zip(na.labels, _row_major_strides(na.dims)))
-            sb = dict(zip(nb.labels, _row_major_strides(nb.dims)))
+            sa = dict(zip(na.labels, st_a))
+            sb = dict(zip(nb.labels, st_b))
             shared = [lb for lb in na.labels if lb in sb]
             odims = [dim_of[lb] for lb in out_labels]
             # split the output index into a high part and a <= LO_TABLE_MAX low part
@@ -410,7 +467,12 @@ def compile_stage(
             k_a = _offsets([dim_of[lb] for lb in shared], [sa[lb] for lb in shared])
             k_b = _offsets([dim_of[lb] for lb in shared], [sb[lb] for lb in shared])
             k_n = k_a.size
-            words = np.concatenate([lo_a, lo_b, hi_a, hi_b, k_a, k_b]).astype(np.uint32)
+            parts = [lo_a, lo_b, hi_a, hi_b, k_a, k_b]
+            if dyn:  # [nA, (qubit, stride) * nA, nB, (qubit, stride) * nB]
+                dyn_words = [len(terms_a)] + [w for t in terms_a for w in t] + \
+                            [len(terms_b)] + [w for t in terms_b for w in t]
+                parts.append(np.asarray(dyn_words, dtype=np.int64))
+            words = np.concatenate(parts).astype(np.uint32)
             tables.append(words)
             step_rows.append(
                 [a_kind, a_ref, b_kind, b_ref, o_kind, o_ref, nd.size, k_n, lo_n, hi_n, tab_off, conj_flags]

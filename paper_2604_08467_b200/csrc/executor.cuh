@@ -216,6 +216,22 @@ __global__ void exec_kernel(const ExecArgs a) {
       t.hiB = t.hiA + t.hi_n;
       t.kA = t.hiB + t.hi_n;
       t.kB = t.kA + kn;
+      if (t.conj & 8u) {
+        // slice views: the operand is T[.., bit(q), ..] of a stored tensor -- add bit * stride
+        // per sliced leg to the base instead of materialising the slice
+        const uint32_t* dt = t.kB + kn;
+        const uint32_t na = __ldg(dt);
+        for (uint32_t i = 0; i < na; ++i) {
+          const uint32_t q = __ldg(dt + 1 + 2 * i);
+          if ((pfx[q >> 6] >> (63 - (q & 63))) & 1ull) A += __ldg(dt + 2 + 2 * i);
+        }
+        dt += 1 + 2 * na;
+        const uint32_t nb = __ldg(dt);
+        for (uint32_t i = 0; i < nb; ++i) {
+          const uint32_t q = __ldg(dt + 1 + 2 * i);
+          if ((pfx[q >> 6] >> (63 - (q & 63))) & 1ull) B += __ldg(dt + 2 + 2 * i);
+        }
+      }
       if (slice) {
         // B is the basis vector e_x of a measured bit, contracted over its only label:
         // out[c] = A[a0(c) + kA[x]] -- a gather, no multiply-adds

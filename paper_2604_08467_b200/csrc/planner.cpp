@@ -99,9 +99,9 @@ static Descent descend(const Problem& P, Rng& rng, double temperature, double ga
     double lu, ls, lo;
     measure(x, y, lu, ls, lo);
     // reference score: flops(step) - prod(shared dims), compared in log space; absorbing a basis
-    // vector only selects a slice of the other operand (one load and one store per output entry, about a multiply-add)
+    // vector only selects a slice of the other operand (a view of the other operand: the executor only adds bit * stride to its base)
     const bool slice = unit[x] || unit[y];
-    const double score = slice ? std::exp2(lo)
+    const double score = slice ? 0.05 * std::exp2(lo)
                                : std::max(0.0, std::exp2(std::min(lu, 1000.0)) - std::exp2(ls));
     double key = std::log1p(score) + gamma * P.logw[std::max(cls[x], cls[y])];
     const double cap = P.cap_log2[std::max(cls[x], cls[y])];
@@ -145,11 +145,12 @@ static Descent descend(const Problem& P, Rng& rng, double temperature, double ga
     double lu, ls, lo;
     measure(x, y, lu, ls, lo);
     const uint32_t c = std::max(cls[x], cls[y]);
-    const double fl = (unit[x] || unit[y]) ? std::exp2(lo) : std::exp2(std::min(lu, 1000.0));
+    const bool is_slice = unit[x] || unit[y];
+    const double fl = is_slice ? 0.05 * std::exp2(lo) : std::exp2(std::min(lu, 1000.0));
     D.flops += fl;
     // every interpreted step costs the executor a fixed dispatch (table fetch, sync) on top of
     // its multiply-adds
-    D.weighted += (fl + kStepOverheadMacs) * std::exp(P.logw[c]);
+    D.weighted += (fl + (is_slice ? 0.0 : kStepOverheadMacs)) * std::exp(P.logw[c]);
     merged.clear();
     std::set_symmetric_difference(lab[x].begin(), lab[x].end(), lab[y].begin(), lab[y].end(),
                                   std::back_inserter(merged));

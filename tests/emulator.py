@@ -43,6 +43,15 @@ def run_stage(programs, pool, kraus_row, prefix_bits, dtype=np.complex128):
             assert out_n == lo_n * hi_n
             A, a_base = resolve(ak, ar)
             B, b_base = resolve(bk, br)
+            if flags & 8:  # slice views: base offsets depend on measured bits
+                at = tab + 2 * lo_n + 2 * hi_n + 2 * kn
+                na = int(t[at])
+                for i in range(na):
+                    a_base += int(prefix_bits[int(t[at + 1 + 2 * i])]) * int(t[at + 2 + 2 * i])
+                at += 1 + 2 * na
+                nb_ = int(t[at])
+                for i in range(nb_):
+                    b_base += int(prefix_bits[int(t[at + 1 + 2 * i])]) * int(t[at + 2 + 2 * i])
             ia = a_base + (hiA[:, None] + loA[None, :]).reshape(-1)[:, None] + kA[None, :]
             ib = b_base + (hiB[:, None] + loB[None, :]).reshape(-1)[:, None] + kB[None, :]
             va, vb = A[ia], B[ib]
