@@ -203,17 +203,23 @@ static void launch_sampler(cudaStream_t st, SampleArgs& a, int sm_count) {
   static bool attr_set = false;
   if (!attr_set) {
     CK(cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(sample_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    CK(cudaFuncSetAttribute(sample_group_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(sample_group_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(sample_group_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_set = true;
   }
-  // Many items with few shots each: one warp per item.  Few items with many shots (stage 1):
-  // one CTA per item so the draws spread over 128 threads.
+  // Many items with few shots each: a group of 8/16/32 lanes per item.  Few items with many
+  // shots (stage 1): one CTA per item so the draws spread over 128 threads.
   if (a.b <= 11 && a.n_items >= (uint64_t)sm_count * 16) {
+    const int gs = nb <= 128 ? 8 : (nb <= 256 ? 16 : 32);  // ~50 KB of staging per block
     const size_t padded = nb + (nb >> 5) + 1;
-    const size_t smem = (size_t)SW_WARPS * padded * 12;
-    const uint64_t cap = (uint64_t)sm_count * std::max<size_t>(1, std::min<size_t>(16, (200 * 1024) / smem));
-    const unsigned grid = (unsigned)std::min<uint64_t>((a.n_items + SW_WARPS - 1) / SW_WARPS, cap);
-    sample_warp_kernel<<<grid, SW_WARPS * 32, smem, st>>>(a);
+    const size_t smem = (size_t)(SG_THREADS / gs) * padded * 12;
+    const uint64_t per_sm = std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / smem));
+    const uint64_t groups = SG_THREADS / gs;
+    const unsigned grid = (unsigned)std::min<uint64_t>((a.n_items + groups - 1) / groups, (uint64_t)sm_count * per_sm);
+    if (gs == 8) sample_group_kernel<8><<<grid, SG_THREADS, smem, st>>>(a);
+    else if (gs == 16) sample_group_kernel<16><<<grid, SG_THREADS, smem, st>>>(a);
+    else sample_group_kernel<32><<<grid, SG_THREADS, smem, st>>>(a);
   } else {
     const size_t smem = nb * 12;
     const uint64_t cap = (uint64_t)sm_count * 16;

@@ -191,51 +191,60 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(const SampleArgs
   }
 }
 
-// Warp-per-item variant for nb <= 2048 (b <= 11): same arithmetic, same results as
-// sample_kernel, but no block-wide barriers.  Each lane owns the nb/32 CONSECUTIVE outcomes
+// Group-per-item variant for nb <= 2048 (b <= 11): same arithmetic, same results as
+// sample_kernel, but no block-wide barriers.  GS lanes (8, 16 or 32) serve one item, 32 / GS
+// items per warp in lockstep.  Each lane owns the nb/GS CONSECUTIVE outcomes
 // [lane*per, lane*per+per); the row is staged through shared memory (padded by one slot per
 // 32 so the strided per-lane reads are conflict-free), scanned serially in registers, and the
 // lane totals are combined with one shuffle scan.  Most work items of the late stages draw one
-// or two shots, so latency per item -- not throughput of the draws -- is what matters.
-constexpr int SW_WARPS = 4;
+// or two shots, so issue slots and latency per item -- not throughput of the draws -- matter.
+constexpr int SG_THREADS = 256;
 
 __device__ __forceinline__ uint32_t sw_pad(uint32_t k) { return k + (k >> 5); }
 
-__global__ void __launch_bounds__(SW_WARPS * 32) sample_warp_kernel(const SampleArgs a) {
+template <int GS>
+__global__ void __launch_bounds__(SG_THREADS) sample_group_kernel(const SampleArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
+  constexpr int GROUPS = SG_THREADS / GS;
   const uint32_t nb = 1u << a.b;
   const uint32_t padded = nb + (nb >> 5) + 1;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint64_t* cdf = reinterpret_cast<uint64_t*>(sm) + (size_t)wid * padded;
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(reinterpret_cast<uint64_t*>(sm) + (size_t)SW_WARPS * padded) +
-                  (size_t)wid * padded;
+  const int lane = threadIdx.x & (GS - 1), grp = threadIdx.x / GS;
+  uint64_t* cdf = reinterpret_cast<uint64_t*>(sm) + (size_t)grp * padded;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(reinterpret_cast<uint64_t*>(sm) + (size_t)GROUPS * padded) +
+                  (size_t)grp * padded;
   double* pd = reinterpret_cast<double*>(cdf);
-  const uint32_t per = nb >= 32 ? nb >> 5 : 1;           // outcomes per lane
-  const uint32_t lanes_used = nb >= 32 ? 32 : nb;
-  const uint64_t n_warps = (uint64_t)gridDim.x * SW_WARPS;
+  const uint32_t per = nb >= GS ? nb / GS : 1;           // outcomes per lane
+  const int lanes_used = nb >= GS ? GS : (int)nb;
+  const uint64_t n_groups = (uint64_t)gridDim.x * GROUPS;
+  const uint64_t rounds = (a.n_items + n_groups - 1) / n_groups;
 
-  for (uint64_t it = (uint64_t)blockIdx.x * SW_WARPS + wid; it < a.n_items; it += n_warps) {
+  // all groups of a warp run the same number of rounds (lockstep __syncwarp); a group past the
+  // end redoes the last item with every global store masked off
+  for (uint64_t r = 0; r < rounds; ++r) {
+    uint64_t it = r * n_groups + (uint64_t)blockIdx.x * GROUPS + grp;
+    const bool live = it < a.n_items;
+    if (!live) it = a.n_items - 1;
     const uint64_t item = a.first_item + it;
-    const uint32_t m = a.mult[item];
-    // ---- load (coalesced), clamp, max / min / sum ----
+    uint32_t m = a.mult[item];
+    // ---- load, clamp, max / min / sum ----
     double mx = 0.0, rawmin = 1e300, csum = 0.0;
     if (a.is_f32) {
       const float* p = reinterpret_cast<const float*>(a.probs) + it * nb;
-      for (uint32_t k = lane; k < nb; k += 32) {
+      for (uint32_t k = lane; k < nb; k += GS) {
         double v = (double)p[k]; rawmin = fmin(rawmin, v);
         v = v > 0.0 ? v : 0.0; pd[sw_pad(k)] = v; mx = fmax(mx, v); csum += v;
         cnt[sw_pad(k)] = 0;
       }
     } else {
       const double* p = reinterpret_cast<const double*>(a.probs) + it * nb;
-      for (uint32_t k = lane; k < nb; k += 32) {
+      for (uint32_t k = lane; k < nb; k += GS) {
         double v = p[k]; rawmin = fmin(rawmin, v);
         v = v > 0.0 ? v : 0.0; pd[sw_pad(k)] = v; mx = fmax(mx, v); csum += v;
         cnt[sw_pad(k)] = 0;
       }
     }
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
+    for (int d = GS / 2; d > 0; d >>= 1) {
       mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
       rawmin = fmin(rawmin, __shfl_xor_sync(0xffffffffu, rawmin, d));
       csum += __shfl_xor_sync(0xffffffffu, csum, d);
@@ -246,7 +255,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32) sample_warp_kernel(const Sample
       const double ms = a.mass ? a.mass[it] : csum, mn = a.minv ? a.minv[it] : rawmin;
       double floor_mass = a.vanish;
       if (a.set_mass) {
-        if (a.stage == 1) { floor_mass = a.vanish_stage1; if (lane == 0) a.set_mass[a.eset_row[item]] = ms; }
+        if (a.stage == 1) { floor_mass = a.vanish_stage1; if (lane == 0 && live) a.set_mass[a.eset_row[item]] = ms; }
         else floor_mass = a.vanish * a.set_mass[a.eset_row[item]];
       }
       if (mn < a.neg_abs - a.neg_rel * ms) bad = PTSBE_ENUMERIC;
@@ -254,14 +263,13 @@ __global__ void __launch_bounds__(SW_WARPS * 32) sample_warp_kernel(const Sample
     }
     if (!bad && !(mx > 0.0)) bad = PTSBE_EIMPOSSIBLE;
     if (bad) {
-      if (lane == 0) {
-        a.nnz[item] = 0;
+      if (lane == 0 && live) {
         atomicMin(a.flag, ((unsigned long long)a.eset_id[item] << 16) |
                               ((unsigned long long)(a.stage & 0xff) << 8) | bad);
         atomicAdd(a.flag_count, 1u);
       }
-      __syncwarp();
-      continue;
+      m = 0;      // no draws, no children; the group keeps in step with its warp
+      mx = 1.0;
     }
     __syncwarp();
     // ---- exact fixed-point weights and their inclusive scan ----
@@ -270,55 +278,55 @@ __global__ void __launch_bounds__(SW_WARPS * 32) sample_warp_kernel(const Sample
     const int shift = (62 - (int)a.b) - ex;
     const uint32_t k0 = lane * per;
     uint64_t run = 0;
-    if (lane < (int)lanes_used)
+    if (lane < lanes_used)
       for (uint32_t k = k0; k < k0 + per; ++k) {
         run += (uint64_t)ldexp(pd[sw_pad(k)], shift);
         cdf[sw_pad(k)] = run;  // same 8-byte slot as pd: lane-local inclusive sums
       }
     uint64_t incl = run;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
+    for (int d = 1; d < GS; d <<= 1) {
+      const uint64_t o = __shfl_up_sync(0xffffffffu, incl, d, GS);
       if (lane >= d) incl += o;
     }
-    const uint64_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint64_t total = __shfl_sync(0xffffffffu, incl, GS - 1, GS);
     const uint64_t base = incl - run;
-    if (lane < (int)lanes_used)
+    if (lane < lanes_used)
       for (uint32_t k = k0; k < k0 + per; ++k) cdf[sw_pad(k)] += base;
     __syncwarp();
     // ---- draws: outcome = #{k : cdf[k] <= r}, r = floor(x * W / 2^64) ----
     const uint32_t rk = a.rank[item], es = a.eset_id[item];
-    for (uint32_t t = lane; t < m; t += 32) {
+    for (uint32_t t = lane; t < m; t += GS) {
       const Philox4 x = philox4x32_10(t, rk, a.stage, es, a.k0, a.k1);
       const uint64_t x64 = ((uint64_t)x.v[1] << 32) | x.v[0];
-      const uint64_t r = __umul64hi(x64, total);
+      const uint64_t rr = __umul64hi(x64, total);
       uint32_t lo = 0, hi = nb;
       while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (cdf[sw_pad(mid)] <= r) lo = mid + 1; else hi = mid;
+        if (cdf[sw_pad(mid)] <= rr) lo = mid + 1; else hi = mid;
       }
       atomicAdd(&cnt[sw_pad(lo)], 1u);
     }
     __syncwarp();
     // ---- ordered emission of the non-empty outcomes ----
     uint32_t mine = 0;
-    if (lane < (int)lanes_used)
+    if (lane < lanes_used && m)
       for (uint32_t k = k0; k < k0 + per; ++k) mine += cnt[sw_pad(k)] != 0;
     uint32_t pos = mine;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t o = __shfl_up_sync(0xffffffffu, pos, d);
+    for (int d = 1; d < GS; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, pos, d, GS);
       if (lane >= d) pos += o;
     }
-    const uint32_t tot32 = __shfl_sync(0xffffffffu, pos, 31);
+    const uint32_t tot32 = __shfl_sync(0xffffffffu, pos, GS - 1, GS);
     pos -= mine;
     const uint32_t slot0 = a.slot_off[item];
-    if (mine)
+    if (mine && live)
       for (uint32_t k = k0; k < k0 + per; ++k) {
         const uint32_t c = cnt[sw_pad(k)];
         if (c) { a.slot_index[slot0 + pos] = k; a.slot_count[slot0 + pos] = c; ++pos; }
       }
-    if (lane == 0) a.nnz[item] = tot32;
+    if (lane == 0 && live) a.nnz[item] = tot32;
     __syncwarp();
   }
 }
