@@ -178,19 +178,23 @@ static void launch_project(ptsbe_plan* pl, const Program& pr, const void* v, uin
   a.rec_stride = rec_stride;
   a.m_off = pr.d.result_ref;
   const uint64_t tiles = (uint64_t)cdiv(n, PJ_TI) * cdiv(a.N, PJ_TN);
-  const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)pl->sm_count * 2);
-  static bool attr_set = false;
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(project_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-    CK(cudaFuncSetAttribute(project_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-    attr_set = true;
+  const size_t smem_f = 2 * (size_t)ProjK<float>::KC * (PJ_TI + PJ_TN) * sizeof(float2);    // two-deep ring
+  const size_t smem_d = 2 * (size_t)ProjK<double>::KC * (PJ_TI + PJ_TN) * sizeof(double2);
+  static int per_sm_f = 0, per_sm_d = 0;
+  if (!per_sm_f) {
+    CK(cudaFuncSetAttribute(project_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+    CK(cudaFuncSetAttribute(project_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_d, project_kernel<double>, PJ_THREADS, smem_d));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_f, project_kernel<float>, PJ_THREADS, smem_f));
+    per_sm_f = std::max(per_sm_f, 1);
+    per_sm_d = std::max(per_sm_d, 1);
   }
   if (pl->dtype == PTSBE_C64) {
-    const size_t smem = (size_t)ProjK<float>::KC * (PJ_TI + PJ_TN) * sizeof(float2);
-    project_kernel<float><<<grid, PJ_THREADS, smem, pl->stream>>>(a);
+    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)pl->sm_count * per_sm_f);
+    project_kernel<float><<<grid, PJ_THREADS, smem_f, pl->stream>>>(a);
   } else {
-    const size_t smem = (size_t)ProjK<double>::KC * (PJ_TI + PJ_TN) * sizeof(double2);
-    project_kernel<double><<<grid, PJ_THREADS, smem, pl->stream>>>(a);
+    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)pl->sm_count * per_sm_d);
+    project_kernel<double><<<grid, PJ_THREADS, smem_d, pl->stream>>>(a);
   }
   g_launches++;
   CK(cudaGetLastError());
