@@ -122,16 +122,37 @@ def check(rc: int) -> None:
     raise STATUS_TO_ERROR.get(rc, DeviceError)(msg)
 
 
+def _release_owned(self):
+    addr = ctypes.addressof(self)
+    if addr and _lib is not None:
+        _lib.ptsbe_free(ctypes.c_void_p(addr))
+
+
+def _owned_buffer(addr: int, nbytes: int):
+    """ctypes view of one library-allocated host array that calls ptsbe_free()
+    when its last numpy view goes away (large histograms are page-locked
+    buffers the library recycles, so they are wrapped, not copied)."""
+    cls = type("_LibBuffer", (ctypes.c_char * nbytes,), {"__del__": _release_owned})
+    return cls.from_address(addr)
+
+
+_COPY_BELOW = 1 << 20
+
+
 def _take(ptr: ctypes.c_void_p, count: int, dtype) -> np.ndarray:
-    """Copy a library-allocated array into numpy and release it."""
+    """Library-allocated array -> numpy: small arrays are copied and released,
+    large ones are wrapped zero-copy and released with their last view."""
     lib = load()
     if not ptr.value:
         return np.zeros(0, dtype=dtype)
     n = int(count)
-    buf = (ctypes.c_char * (n * np.dtype(dtype).itemsize)).from_address(ptr.value)
-    out = np.frombuffer(buf, dtype=dtype, count=n).copy()
-    lib.ptsbe_free(ptr)
-    return out
+    nbytes = n * np.dtype(dtype).itemsize
+    if nbytes < _COPY_BELOW:
+        buf = (ctypes.c_char * nbytes).from_address(ptr.value)
+        out = np.frombuffer(buf, dtype=dtype, count=n).copy()
+        lib.ptsbe_free(ptr)
+        return out
+    return np.frombuffer(_owned_buffer(ptr.value, nbytes), dtype=dtype, count=n)
 
 
 def _ptr(a: Optional[np.ndarray]):

@@ -49,9 +49,72 @@ struct ptsbe_plan {
   uint64_t chunk_shots = 1ull << 26;
   size_t ext_budget = 48ull << 30;
   double vanish = 1e-12, neg_abs = -1e-12, neg_rel = 0.0, vanish_stage1 = 1e-30;
+  // workspaces of destroyed batches: ptsbe_sample() creates a batch per call, and re-creating
+  // multi-GB slabs (cudaMalloc / cudaFree) per call would dominate its wall time
+  std::vector<std::unique_ptr<Workspace>> ws_cache;
+  std::unique_ptr<Workspace> take_workspace() {
+    if (ws_cache.empty()) return std::unique_ptr<Workspace>(new Workspace);
+    // hand out the largest first: ws_tmp is requested before ws_out and needs more
+    size_t best = 0;
+    for (size_t i = 1; i < ws_cache.size(); ++i)
+      if (ws_cache[i]->reserved() > ws_cache[best]->reserved()) best = i;
+    std::unique_ptr<Workspace> w = std::move(ws_cache[best]);
+    ws_cache.erase(ws_cache.begin() + best);
+    w->reset();
+    return w;
+  }
+  void give_workspace(std::unique_ptr<Workspace> w) {
+    if (!w) return;
+    if (ws_cache.size() < 4) ws_cache.push_back(std::move(w));
+  }
 };
 
 namespace ptsbe {
+
+// Host buffers handed to the caller (histograms).  Large ones are page-locked, so the
+// device->host copy runs at PCIe rate instead of through the driver's bounce buffers, and
+// are recycled between calls (pinning hundreds of MB costs as much as the copy): ptsbe_free()
+// puts them back here.  Small ones are plain malloc.
+struct HostPool {
+  struct Ent { void* p; size_t cap; bool busy; };
+  std::mutex mu;
+  std::vector<Ent> ents;
+  static constexpr size_t kMinPinned = 1ull << 20, kKeepBytes = 8ull << 30;
+  void* get(size_t bytes) {
+    if (bytes < kMinPinned) return malloc(std::max<size_t>(bytes, 8));
+    std::lock_guard<std::mutex> lock(mu);
+    int best = -1;
+    for (size_t i = 0; i < ents.size(); ++i)
+      if (!ents[i].busy && ents[i].cap >= bytes && (best < 0 || ents[i].cap < ents[best].cap)) best = (int)i;
+    if (best >= 0) { ents[best].busy = true; return ents[best].p; }
+    const size_t cap = (bytes + bytes / 8 + (1ull << 21) - 1) & ~((1ull << 21) - 1);
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, cap, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      return malloc(bytes);  // not pinned: slower copy, same result
+    }
+    ents.push_back(Ent{p, cap, true});
+    return p;
+  }
+  bool put(void* p) {  // false: not one of ours
+    std::lock_guard<std::mutex> lock(mu);
+    size_t idle = 0;
+    int hit = -1;
+    for (size_t i = 0; i < ents.size(); ++i) {
+      if (ents[i].p == p) hit = (int)i;
+      else if (!ents[i].busy) idle += ents[i].cap;
+    }
+    if (hit < 0) return false;
+    if (idle + ents[hit].cap > kKeepBytes) {
+      cudaFreeHost(p);
+      ents.erase(ents.begin() + hit);
+    } else {
+      ents[hit].busy = false;
+    }
+    return true;
+  }
+};
+static HostPool g_host_pool;
 
 static size_t env_size(const char* name, size_t dflt) {
   const char* v = getenv(name);
@@ -461,8 +524,10 @@ struct ptsbe_batch {
   uint64_t n_sets = 0, total_shots = 0;
   std::vector<uint32_t> shots_host;
   DevBuf kraus, shots, ids;
-  Workspace ws_tmp;  // temporaries of one chunk (rewound after every chunk)
-  Workspace ws_out;  // chunk outputs and the merged histogram (reset at the start of a run)
+  std::unique_ptr<Workspace> ws_tmp_own;  // temporaries of one chunk (rewound after every chunk)
+  std::unique_ptr<Workspace> ws_out_own;  // chunk outputs and the merged histogram (reset at the start of a run)
+  Workspace& ws_tmp() { return *ws_tmp_own; }
+  Workspace& ws_out() { return *ws_out_own; }
   // last run
   Histogram merged;
   RunOutput per_set;  // when merged == 0 (single chunk only)
@@ -479,11 +544,11 @@ static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stat
   stats->first_flagged_id = -1;
   stats->total_shots = bt->total_shots;
   g_launches = 0;
-  bt->ws_tmp.reset();
-  bt->ws_out.reset();
+  bt->ws_tmp().reset();
+  bt->ws_out().reset();
   bt->merged = Histogram();
   bt->per_set = RunOutput();
-  WorkspaceScope scope(&bt->ws_out);  // flags, concatenation and the histogram live in ws_out
+  WorkspaceScope scope(&bt->ws_out());  // flags, concatenation and the histogram live in ws_out
   DevBuf flag(16, st);
   CK(cudaMemsetAsync(flag.p, 0xff, 8, st));
   CK(cudaMemsetAsync(flag.as<unsigned char>() + 8, 0, 8, st));
@@ -531,12 +596,12 @@ static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stat
     uint64_t sh = 0;
     for (uint64_t i = 0; i < cnt; ++i) sh += bt->shots_host[e + i];
     {
-      WorkspaceScope chunk_scope(&bt->ws_tmp);
-      const Workspace::Mark mark = bt->ws_tmp.mark();
+      WorkspaceScope chunk_scope(&bt->ws_tmp());
+      const Workspace::Mark mark = bt->ws_tmp().mark();
       run_chunk(pl, bt->kraus.as<uint8_t>() + e * pl->g, bt->shots.as<uint32_t>() + e,
                 bt->ids.as<uint32_t>() + e, (uint32_t)cnt, sh, seed, outs[c], stats,
-                flag.as<unsigned long long>(), flag.as<uint32_t>() + 2, bt->ws_out);
-      bt->ws_tmp.rewind(mark);  // run_chunk returns with the stream drained
+                flag.as<unsigned long long>(), flag.as<uint32_t>() + 2, bt->ws_out());
+      bt->ws_tmp().rewind(mark);  // run_chunk returns with the stream drained
     }
     total_rec += outs[c].n;
   }
@@ -553,7 +618,7 @@ static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stat
   bt->have_per_set = false;
   EventLog hlog(st);
   hlog.begin(&stats->histogram_ms);
-  WorkspaceScope hist_scope(&bt->ws_tmp);  // sort/scan temporaries and the histogram: until the next run
+  WorkspaceScope hist_scope(&bt->ws_tmp());  // sort/scan temporaries and the histogram: until the next run
   if (merged) {
     if (chunks.size() == 1) {
       reduce_by_key(outs[0].keys.as<uint64_t>(), outs[0].n, words, outs[0].counts.as<uint32_t>(),
@@ -659,7 +724,9 @@ int ptsbe_device_count(void) {
   return n;
 }
 
-void ptsbe_free(void* p) { free(p); }
+void ptsbe_free(void* p) {
+  if (p && !g_host_pool.put(p)) free(p);
+}
 
 int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
   return guarded([&] {
@@ -738,6 +805,7 @@ void ptsbe_plan_destroy(ptsbe_plan* pl) {
   if (!pl) return;
   cudaSetDevice(pl->device);
   cudaStreamSynchronize(pl->stream);
+  pl->ws_cache.clear();
   pl->pool.release();
   for (auto& s : pl->programs)
     for (auto& p : s) { p.leaves.release(); p.steps.release(); p.tables.release(); }
@@ -953,6 +1021,11 @@ int ptsbe_batch_upload(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t*
     std::unique_ptr<ptsbe_batch> bt(new ptsbe_batch);
     bt->plan = pl;
     bt->n_sets = n_sets;
+    {
+      std::lock_guard<std::mutex> lock(pl->mu);
+      bt->ws_tmp_own = pl->take_workspace();
+      bt->ws_out_own = pl->take_workspace();
+    }
     bt->shots_host.assign(shots, shots + n_sets);
     for (uint64_t i = 0; i < n_sets; ++i) {
       if (shots[i] < 1) throw Failure(PTSBE_EINVAL, "proportional sampling needs m >= 1");
@@ -987,8 +1060,9 @@ int ptsbe_batch_run(ptsbe_batch* bt, uint64_t seed, uint64_t* n_records, ptsbe_r
 static void fetch_merged(ptsbe_batch* bt, uint64_t** keys, uint64_t** counts, uint64_t* n) {
   ptsbe_plan* pl = bt->plan;
   const uint64_t nr = bt->merged.n;
-  uint64_t* k = (uint64_t*)malloc(std::max<uint64_t>(nr, 1) * 8 * pl->words);
-  uint64_t* c = (uint64_t*)malloc(std::max<uint64_t>(nr, 1) * 8);
+  uint64_t* k = (uint64_t*)g_host_pool.get(std::max<uint64_t>(nr, 1) * 8 * pl->words);
+  uint64_t* c = (uint64_t*)g_host_pool.get(std::max<uint64_t>(nr, 1) * 8);
+  if (!k || !c) throw Failure(PTSBE_ECAPACITY, "host allocation of the histogram failed");
   if (nr) {
     CK(cudaMemcpyAsync(k, bt->merged.keys.p, nr * 8 * pl->words, cudaMemcpyDeviceToHost, pl->stream));
     CK(cudaMemcpyAsync(c, bt->merged.counts.p, nr * 8, cudaMemcpyDeviceToHost, pl->stream));
@@ -1012,6 +1086,11 @@ void ptsbe_batch_destroy(ptsbe_batch* bt) {
   if (!bt) return;
   cudaSetDevice(bt->plan->device);
   cudaStreamSynchronize(bt->plan->stream);
+  {
+    std::lock_guard<std::mutex> lock(bt->plan->mu);
+    bt->plan->give_workspace(std::move(bt->ws_tmp_own));
+    bt->plan->give_workspace(std::move(bt->ws_out_own));
+  }
   delete bt;
 }
 
