@@ -425,6 +425,7 @@ def main():
         comp = [sum(float(s.compact_ms[j]) for s in stats) for j in range(f)]
         hist_ms = sum(float(s.histogram_ms) for s in stats)
         projm = [sum(float(s.project_ms[j]) for s in stats) for j in range(f)]
+        desc = [sum(float(s.descent_ms[j]) for s in stats) for j in range(f)]
         words = dp.words
         # candidates for "the dominant kernel": per stage, the per-item executor pass and the dense projection
         cands = []
@@ -432,7 +433,20 @@ def main():
             pr = pipe.programs_of(j + 1)[-1]
             n_items = sum(int(s.stage_events[j]) for s in stats)
             launches_j = sum(int(s.marg_launches[j]) for s in stats)
-            if pr.proj_d:
+            d_items = sum(int(s.descent_items[j]) for s in stats)
+            if pr.proj_d and d_items:
+                # per-item steps, vector written as one row per item
+                cands.append((marg[j], f"exec_kernel (per-item steps -> v[{pr.proj_d}]), stage {j + 1}", n_items, launches_j,
+                              pr.ext_read_elems * elem + 8 + 8 * words + pr.proj_d * elem, 8.0 * pr.flops))
+                # descent: v read, list entry (eset, mult, slot_off, rank, id), one (index, count) per child,
+                # tree columns re-read once per 512-item tile; (b + 1) dot products of D terms per draw
+                b_j = sizes[j]
+                shots_j = total_shots_local * args.steps
+                cands.append((desc[j], f"descent_kernel (per-qubit descent, D={pr.proj_d}, b={b_j}), stage {j + 1}",
+                              d_items, launches_j,
+                              pr.proj_d * elem + 20 + 8 + pr.proj_d * elem * (1 << b_j) / 512.0,
+                              4.0 * pr.proj_d * (b_j + 1) * shots_j / max(d_items, 1)))
+            elif pr.proj_d:
                 # per-item steps: records read + list entry + Kraus row amortised + vector written
                 cands.append((marg[j], f"exec_kernel (per-item steps -> v[{pr.proj_d}]), stage {j + 1}", n_items, launches_j,
                               pr.ext_read_elems * elem + 8 + 8 * words + pr.proj_d * elem, 8.0 * pr.flops))
@@ -472,6 +486,7 @@ def main():
             "stage_events": [int(st.stage_events[j]) for j in range(f)],
             "kernel_ms_per_step": {
                 "exec_marginal": [m / args.steps for m in marg], "project": [m / args.steps for m in projm], "exec_hoist": [h / args.steps for h in hoist],
+                "descent": [x / args.steps for x in desc],
                 "sampler": [s / args.steps for s in samp], "compaction": [x / args.steps for x in comp],
                 "histogram": hist_ms / args.steps, "stage_total": [sum(float(s.stage_ms[j]) for s in stats) / args.steps for j in range(f)],
             },

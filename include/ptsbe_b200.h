@@ -133,6 +133,8 @@ typedef struct {
   float compact_ms[PTSBE_MAX_STAGES]; /* scans + expand + rank (next work list)    */
   float histogram_ms;                 /* final sort + reduce-by-key                */
   uint32_t marg_launches[PTSBE_MAX_STAGES];
+  float descent_ms[PTSBE_MAX_STAGES]; /* tree_build_kernel + descent_kernel (per-qubit descent sampler) */
+  uint64_t descent_items[PTSBE_MAX_STAGES]; /* work items sampled by descent instead of project + sample */
 } ptsbe_run_stats;
 
 const char* ptsbe_last_error(void);

@@ -56,6 +56,8 @@ class RunStats(ctypes.Structure):
         ("compact_ms", ctypes.c_float * MAX_STAGES),
         ("histogram_ms", ctypes.c_float),
         ("marg_launches", ctypes.c_uint32 * MAX_STAGES),
+        ("descent_ms", ctypes.c_float * MAX_STAGES),
+        ("descent_items", ctypes.c_uint64 * MAX_STAGES),
     ]
 
 

@@ -12,6 +12,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "descent.cuh"
 #include "executor.cuh"
 #include "histogram.cuh"
 #include "project.cuh"
@@ -46,6 +47,9 @@ struct ptsbe_plan {
   std::mutex mu;
   // tunables (environment overrides for experiments)
   size_t probs_budget = 256ull << 20;  // bytes of marginal buffer per sub-batch
+  size_t vec_budget = 512ull << 20;    // bytes of per-item vectors per sub-batch (descent stages)
+  uint32_t descent = 1;                // per-qubit descent sampler for low-multiplicity stages
+  double descent_mult = 4.0;           // ... used when shots / unique prefixes of the stage <= this
   uint64_t chunk_shots = 1ull << 26;
   size_t ext_budget = 48ull << 30;
   double vanish = 1e-12, neg_abs = -1e-12, neg_rel = 0.0, vanish_stage1 = 1e-30;
@@ -170,7 +174,7 @@ static ExecLaunch configure_exec(ptsbe_plan* pl, Program& pr, uint32_t n_items) 
 template <typename R>
 static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelDev* levels_dev,
                         const uint8_t* kraus_dev, uint32_t first, uint32_t n_items, void* out,
-                        double* mass, double* minv, uint32_t vec_stride) {
+                        double* mass, double* minv, uint32_t vec_stride, uint32_t vec_row) {
   using C = typename CxT<R>::type;
   if (n_items == 0) return;
   ExecLaunch L = configure_exec<R>(pl, pr, n_items);
@@ -203,6 +207,7 @@ static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelD
   a.item_bytes = L.item_bytes;
   a.mode = mode;
   a.vec_stride = vec_stride;
+  a.vec_row = vec_row;
   const uint32_t gs = pr.d.threads_per_item;
   if (gs == 8) exec_kernel<R, 8><<<L.grid, L.block, L.smem, pl->stream>>>(a);
   else if (gs == 16) exec_kernel<R, 16><<<L.grid, L.block, L.smem, pl->stream>>>(a);
@@ -214,11 +219,74 @@ static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelD
 
 static void launch_exec_any(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelDev* lv,
                             const uint8_t* kraus, uint32_t first, uint32_t n, void* out,
-                            double* mass, double* minv, uint32_t vec_stride = 0) {
+                            double* mass, double* minv, uint32_t vec_stride = 0,
+                            uint32_t vec_row = 0) {
   if (pl->dtype == PTSBE_C64)
-    launch_exec<float>(pl, pr, mode, lv, kraus, first, n, out, mass, minv, vec_stride);
+    launch_exec<float>(pl, pr, mode, lv, kraus, first, n, out, mass, minv, vec_stride, vec_row);
   else
-    launch_exec<double>(pl, pr, mode, lv, kraus, first, n, out, mass, minv, vec_stride);
+    launch_exec<double>(pl, pr, mode, lv, kraus, first, n, out, mass, minv, vec_stride, vec_row);
+}
+
+// ---- per-qubit descent sampler (descent.cuh) ----
+struct DescentShape { uint32_t nch = 0, dpad = 0; size_t smem = 0; };
+
+static DescentShape descent_shape(const ptsbe_plan* pl, uint32_t D, uint32_t b) {
+  DescentShape s;
+  const uint32_t cpc = pl->dtype == PTSBE_C64 ? 2 : 1;
+  for (uint32_t nch = 1; nch <= 8; nch <<= 1)
+    if (DS_GS * nch * cpc >= D) { s.nch = nch; break; }
+  if (!s.nch || b > 12) { s.nch = 0; return s; }
+  s.dpad = DS_GS * s.nch * cpc;
+  s.smem = ((size_t)s.dpad * pl->elem + (size_t)DS_GROUPS * 4) << b;
+  if (s.smem > 160 * 1024) s.nch = 0;
+  return s;
+}
+
+template <typename R, int NCH>
+static void launch_descent_t(ptsbe_plan* pl, const DescentArgs& a, size_t smem) {
+  static int per_sm = 0;
+  static size_t per_sm_smem = 0;
+  if (!per_sm || per_sm_smem != smem) {
+    CK(cudaFuncSetAttribute(descent_kernel<R, NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, descent_kernel<R, NCH>, DS_THREADS, smem));
+    per_sm = std::max(per_sm, 1);
+    per_sm_smem = smem;
+  }
+  const uint64_t tiles = cdiv(a.n_items, DS_TILE);
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)pl->sm_count * per_sm));
+  descent_kernel<R, NCH><<<grid, DS_THREADS, smem, pl->stream>>>(a);
+  g_launches++;
+  CK(cudaGetLastError());
+}
+
+static void launch_descent(ptsbe_plan* pl, const DescentArgs& a, const DescentShape& sh) {
+  if (a.n_items == 0) return;
+  const bool f32 = pl->dtype == PTSBE_C64;
+  switch (sh.nch) {
+    case 1: f32 ? launch_descent_t<float, 1>(pl, a, sh.smem) : launch_descent_t<double, 1>(pl, a, sh.smem); break;
+    case 2: f32 ? launch_descent_t<float, 2>(pl, a, sh.smem) : launch_descent_t<double, 2>(pl, a, sh.smem); break;
+    case 4: f32 ? launch_descent_t<float, 4>(pl, a, sh.smem) : launch_descent_t<double, 4>(pl, a, sh.smem); break;
+    case 8: f32 ? launch_descent_t<float, 8>(pl, a, sh.smem) : launch_descent_t<double, 8>(pl, a, sh.smem); break;
+    default: throw Failure(PTSBE_EINVAL, "descent sampler: unsupported vector length");
+  }
+}
+
+static void launch_tree_build(ptsbe_plan* pl, const Program& pr, const void* rec0, uint32_t rec_stride,
+                              uint32_t n_sets, uint32_t b, uint32_t dpad, void* tree) {
+  TreeArgs t;
+  t.rec0 = rec0;
+  t.tree = tree;
+  t.rec_stride = rec_stride;
+  t.m_off = pr.d.result_ref;
+  t.D = pr.d.proj_d;
+  t.b = b;
+  t.dpad = dpad;
+  t.n_sets = n_sets;
+  const dim3 grid(cdiv(((uint64_t)dpad) << b, 256), n_sets);
+  if (pl->dtype == PTSBE_C64) tree_build_kernel<float><<<grid, 256, 0, pl->stream>>>(t);
+  else tree_build_kernel<double><<<grid, 256, 0, pl->stream>>>(t);
+  g_launches++;
+  CK(cudaGetLastError());
 }
 
 static inline uint32_t vec_pitch(uint32_t n) { return (n + PJ_TI - 1) / PJ_TI * PJ_TI; }
@@ -385,10 +453,61 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     }
     // marginal pass + sampler, in sub-batches sized to the probs buffer
     const size_t real = pl->dtype == PTSBE_C64 ? 4 : 8;
+    const bool proj = progs[j - 1].d.result_kind == 3;
+    DevBuf nnz((size_t)U * 4, st);
+    // Stages whose work items carry few shots each are sampled by per-qubit descent over the
+    // error set's conditional-marginal tree (descent.cuh) instead of project + sample.
+    DescentShape dsh;
+    if (proj && pl->descent && j > 1 && U && (double)chunk_shots <= pl->descent_mult * (double)U)
+      dsh = descent_shape(pl, progs[j - 1].d.proj_d, b);
+    if (dsh.nch) {
+      const Program& pr = progs[j - 1];
+      DevBuf tree(((size_t)ne * dsh.dpad * pl->elem) << b, st);
+      log.begin(&stats->descent_ms[j - 1]);
+      launch_tree_build(pl, pr, table[1].ext, table[1].ext_rec, ne, b, dsh.dpad, tree.p);
+      log.end();
+      const size_t row = (size_t)dsh.dpad * pl->elem;
+      const uint32_t B = (uint32_t)std::max<size_t>(DS_TILE, std::min<size_t>(U, pl->vec_budget / row));
+      DevBuf vbuf((size_t)B * row, st);
+      if (dsh.dpad != pr.d.proj_d) CK(cudaMemsetAsync(vbuf.p, 0, (size_t)B * row, st));
+      for (uint32_t s0 = 0; s0 < U; s0 += B) {
+        const uint32_t nbatch = std::min(B, U - s0);
+        log.begin(&stats->marg_ms[j - 1]);
+        launch_exec_any(pl, progs[j - 1], EXEC_VECTOR, table_dev.as<LevelDev>(), kraus_dev, s0,
+                        nbatch, vbuf.p, nullptr, nullptr, 0, dsh.dpad);
+        log.end();
+        stats->marg_launches[j - 1]++;
+        DescentArgs da;
+        da.v = vbuf.p;
+        da.tree = tree.p;
+        da.eset = cur.eset.as<uint32_t>();
+        da.mult = cur.mult.as<uint32_t>();
+        da.slot_off = cur.slot_off.as<uint32_t>();
+        da.eset_id = cur.gid.as<uint32_t>();
+        da.rank = cur.rank.as<uint32_t>();
+        da.slot_index = slot_index.as<uint32_t>();
+        da.slot_count = slot_count.as<uint32_t>();
+        da.nnz = nnz.as<uint32_t>();
+        da.flag = flag_dev;
+        da.flag_count = flag_count_dev;
+        da.set_mass = set_mass.as<double>();
+        da.first_item = s0;
+        da.n_items = nbatch;
+        da.b = b;
+        da.stage = j;
+        da.k0 = (uint32_t)seed;
+        da.k1 = (uint32_t)(seed >> 32);
+        da.vanish = pl->vanish;
+        da.neg_abs = pl->neg_abs;
+        da.neg_rel = pl->neg_rel;
+        log.begin(&stats->descent_ms[j - 1]);
+        launch_descent(pl, da, dsh);
+        log.end();
+      }
+      stats->descent_items[j - 1] += U;
+    } else {
     uint32_t B = (uint32_t)std::max<size_t>(1, std::min<size_t>(U, pl->probs_budget / (nb * real)));
     DevBuf probs((size_t)B * nb * real, st), mass((size_t)B * 8, st), minv((size_t)B * 8, st);
-    DevBuf nnz((size_t)U * 4, st);
-    const bool proj = progs[j - 1].d.result_kind == 3;
     DevBuf vbuf;
     if (proj) vbuf.alloc((size_t)vec_pitch(B) * progs[j - 1].d.proj_d * pl->elem, st);
     for (uint32_t s0 = 0; s0 < U; s0 += B) {
@@ -436,6 +555,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       log.begin(&stats->sampler_ms[j - 1]);
       launch_sampler(st, sa, pl->sm_count);
       log.end();
+    }
     }
     // compaction into level j+1
     log.begin(&stats->compact_ms[j - 1]);
@@ -762,6 +882,9 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     uint64_t thr = UINT64_MAX;
     CK(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr));
     pl->probs_budget = env_size("PTSBE_PROBS_BYTES", pl->probs_budget);
+    pl->vec_budget = env_size("PTSBE_VEC_BYTES", pl->vec_budget);
+    pl->descent = (uint32_t)env_size("PTSBE_DESCENT", pl->descent);
+    if (const char* dm = getenv("PTSBE_DESCENT_MULT")) if (*dm) pl->descent_mult = atof(dm);
     pl->chunk_shots = env_size("PTSBE_CHUNK_SHOTS", pl->chunk_shots);
     pl->ext_budget = env_size("PTSBE_EXT_BYTES", pl->ext_budget);
     cudaStream_t st = pl->stream;

@@ -61,6 +61,7 @@ struct ExecArgs {
   uint32_t item_bytes;  // shared-memory footprint of one group
   uint32_t mode;
   uint32_t vec_stride;  // VECTOR: row pitch (items, padded) of the transposed output
+  uint32_t vec_row;     // VECTOR: non-zero -> one row of vec_row elements per item instead (descent.cuh)
 };
 
 template <typename R> struct CxT;
@@ -197,8 +198,12 @@ __global__ void exec_kernel(const ExecArgs a) {
       if (s1.x == 0) {
         O = s1.y < a.arena_fast ? arena + s1.y : spill + (s1.y - a.arena_fast);
       } else if (a.mode == EXEC_VECTOR) {
-        O = reinterpret_cast<C*>(a.out) + (size_t)s1.y * a.vec_stride + it;
-        o_stride = a.vec_stride;
+        if (a.vec_row) {
+          O = reinterpret_cast<C*>(a.out) + (size_t)it * a.vec_row + s1.y;
+        } else {
+          O = reinterpret_cast<C*>(a.out) + (size_t)s1.y * a.vec_stride + it;
+          o_stride = a.vec_stride;
+        }
         store = live;
       } else {
         O = reinterpret_cast<C*>(a.out) + (size_t)item * a.out_elems + s1.y;

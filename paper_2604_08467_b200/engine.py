@@ -161,6 +161,8 @@ class EngineStats:
     contract_seconds: float = 0.0
     stage_events: dict = field(default_factory=dict)
     stage_seconds: dict = field(default_factory=dict)
+    # device-only: work items of a stage sampled by per-qubit descent (csrc/descent.cuh)
+    descent_events: dict = field(default_factory=dict)
 
     def record_contraction(self, stage: int, seconds: float, events: int = 1) -> None:
         self.contract_events += events
@@ -177,6 +179,8 @@ class EngineStats:
             self.stage_events[k] = self.stage_events.get(k, 0) + v
         for k, v in other.stage_seconds.items():
             self.stage_seconds[k] = self.stage_seconds.get(k, 0.0) + v
+        for k, v in other.descent_events.items():
+            self.descent_events[k] = self.descent_events.get(k, 0) + v
 
 
 @dataclass
@@ -780,6 +784,8 @@ def sample_proportional_batched(
 def _account(stats: EngineStats, st, f: int) -> None:
     for j in range(1, f + 1):
         stats.record_contraction(j, st.stage_ms[j - 1] * 1e-3, events=int(st.stage_events[j - 1]))
+        if st.descent_items[j - 1]:
+            stats.descent_events[j] = stats.descent_events.get(j, 0) + int(st.descent_items[j - 1])
 
 
 def sample_proportional(template: CircuitNetwork, k: ErrorSet, plan: BatchPlan, rng,

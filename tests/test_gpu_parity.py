@@ -185,6 +185,56 @@ def test_complex64_end_to_end_tvd():
         assert 0.5 * np.abs(emp - exact).sum() <= 0.02
 
 
+def _hea_case(n, depth, sets, shots, seed, gamma=0.01):
+    c, _ = workloads.hea(n, depth, gamma=gamma, p=0.01, seed=2)
+    es = presample_errors(c, sets, "uniform", shots_per_set=shots, rng=np.random.default_rng(seed))
+    return c, CircuitNetwork.from_circuit(c), es
+
+
+def test_descent_sampler_bit_exact_vs_oracle_complex128(monkeypatch):
+    """Per-qubit descent (csrc/descent.cuh) forced on for every projection-form
+    stage: same uniforms, float64 marginals within 1e-11 -> the records equal the
+    oracle's flat multinomial split (reference engine.py:513-523)."""
+    monkeypatch.setenv("PTSBE_DESCENT_MULT", "1e18")
+    c, tpl, es = _hea_case(12, 4, 4, 600, 9)
+    sizes = (4, 4, 4)
+    ctx = SamplerContext(hypersamples=8, dtype="complex128")
+    per_set = sample_proportional_batched(tpl, es, BatchPlan(sizes), 31, ctx)
+    assert sum(ctx.stats.descent_events.values()) > 0, "descent path was not exercised"
+    ops, finals = bridge.template_of(c)
+    _, want, events = O.run_proportional(ops, finals, sizes, bridge.oracle_errorsets(c, es), 31)
+    assert [[(r.bitstring, r.count) for r in recs] for recs in per_set] == want
+    assert dict(ctx.stats.stage_events) == events
+
+
+@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+def test_descent_sampler_agrees_with_flat_sampler(monkeypatch, dtype):
+    """Descent on vs off on a 16-qubit HEA (D = 64 cut): identical records in
+    complex128, TVD <= 0.02 per error set in complex64 (different rounding of the
+    same conditional marginals)."""
+    c, tpl, es = _hea_case(16, 5, 24, 4000, 4, gamma=0.0)
+    sizes = (6, 5, 5)
+
+    def run(descent):
+        monkeypatch.setenv("PTSBE_DESCENT", "1" if descent else "0")
+        monkeypatch.setenv("PTSBE_DESCENT_MULT", "1e18")
+        ctx = SamplerContext(hypersamples=8, dtype=dtype)
+        out = sample_proportional_batched(tpl, es, BatchPlan(sizes), 5, ctx)
+        return out, ctx.stats
+
+    flat, st0 = run(False)
+    desc, st1 = run(True)
+    assert not st0.descent_events and sum(st1.descent_events.values()) > 0
+    for k, a, b in zip(es, flat, desc):
+        assert sum(r.count for r in b) == k.m
+        if dtype == "complex128":
+            assert [(r.bitstring, r.count) for r in a] == [(r.bitstring, r.count) for r in b]
+        else:
+            da, db = {r.bitstring: r.count for r in a}, {r.bitstring: r.count for r in b}
+            tvd = 0.5 * sum(abs(da.get(s, 0) - db.get(s, 0)) for s in set(da) | set(db)) / k.m
+            assert tvd <= 0.02
+
+
 def test_deterministic_circuit_and_single_set_signature():
     c = Circuit(3, tuple(Gate("X", (q,)) for q in range(3)))
     tpl = CircuitNetwork.from_circuit(c)
