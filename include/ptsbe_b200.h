@@ -53,8 +53,9 @@ enum { PTSBE_C64 = 0, PTSBE_C128 = 1 };
  *                      (UPV merge, engine.py:284-313, done once on the host per variant)
  *          sel_kind 2: prefix bit          data = pool[pool_off + bit(sel_arg)*size ..)
  *                      (basis vectors of engine.py:395-399)
- * steps  : n_steps x 12 words {a_kind, a_ref, b_kind, b_ref, o_kind, o_ref,
- *                              out_n, k_n, lo_n, hi_n, tab_off, conj}
+ * steps  : n_steps x 16 words {a_kind, a_ref, b_kind, b_ref, o_kind, o_ref,
+ *                              out_n, k_n, lo_n, hi_n, tab_off, conj,
+ *                              a_memo, b_memo, a_prod | b_prod << 16, own_memo}
  *          conj bit 0 / 1: operand A / B is read complex-conjugated (its node is the
  *          conjugate twin -- bra copy -- of the node that was actually computed);
  *          bit 2: B is a prefix-bit basis vector e_x contracted over its only label, so the
@@ -62,6 +63,10 @@ enum { PTSBE_C64 = 0, PTSBE_C128 = 1 };
  *          bit 3: slice views -- the step's table block ends with [nA, (qubit, stride) x nA,
  *          nB, (qubit, stride) x nB]: operand bases advance by stride when the measured bit
  *          of that qubit is 1 (the operand is a slice of a stored tensor, never materialised)
+ *          bit 4: the step always runs (it writes a record or the result);
+ *          a_prod / b_prod: index of the step of this program that produces operand A / B
+ *          (0xFFFF: a leaf or an earlier pass), a_memo / b_memo / own_memo: offsets of the
+ *          operands' and the step's own variant-0 value in the program's memo (memo_elems > 0)
  *          operand kind 0: arena offset (elements), 1: leaf index,
  *                       2 + p: record of pass p of the same stage, a_ref = offset in record
  *          output  kind 0: arena offset, 1: offset in this pass's output record
@@ -85,10 +90,19 @@ typedef struct {
                                  M[proj_d][out_elems] at offset result_ref of pass 0's record (one
                                  per error set) -- run as a dense product over all work items of
                                  an error set (csrc/project.cuh)                                 */
-  uint32_t reserved;
+  uint32_t memo_elems;        /* > 0: class-0 program with a variant-0 memo.  The value of every
+                                 step under Kraus index 0 at every site is computed once per plan;
+                                 a work item re-executes only the steps that depend on a site with
+                                 a non-zero index (the UPV merge of engine.py:284-313 leaves all
+                                 other tensors of the template untouched) plus the always-run ones */
   const uint32_t* leaves;
   const uint32_t* steps;
   const uint32_t* tables;
+  const uint32_t* memo_ptr;   /* [n_memo_sites + 2] CSR row starts into memo_idx; row s = steps that
+                                 depend on gate site s, row n_memo_sites = always-run steps        */
+  const uint32_t* memo_idx;   /* [n_memo_idx] step indices                                          */
+  uint32_t n_memo_idx;
+  uint32_t n_memo_sites;
 } ptsbe_program_desc;
 
 typedef struct {

@@ -29,7 +29,9 @@ import numpy as np
 from .errors import CapacityError, IncompletePathError, NetworkStructureError, ResourceLimitError
 
 SEL_CONST, SEL_KRAUS, SEL_PREFIX = 0, 1, 2
-STEP_WORDS, LEAF_WORDS = 12, 4
+STEP_WORDS, LEAF_WORDS = 16, 4
+MEMO_NONE = 0xFFFF         # "operand is not produced by a step of this program"
+MEMO_MIN_STEPS = 48        # class-0 programs at least this long get a variant-0 memo
 LO_TABLE_MAX = 1024          # entries in the per-lane (low) gather table of a step
 SMEM_BYTES = 52 * 1024       # shared-memory arena of a CTA-per-item program: 4 CTAs per SM stay resident
 WARP_ARENA_BYTES = 6 * 1024  # beyond this a warp-per-item mapping starves occupancy
@@ -94,6 +96,13 @@ class Program:
     leaf_read_elems: int = 0    # elements of operand-pool leaves one execution reads (L1/L2 resident)
     proj_d: int = 0             # > 0: projection form, the steps produce a vector v[proj_d] and the
                                 # stage result is Re(v . M), M[proj_d, out_elems] at result_ref in pass 0's record
+    # variant-0 memo (class-0 programs): the value of every step under "no error anywhere" is
+    # computed once per plan; a work item re-executes only the steps above a site whose Kraus
+    # index is non-zero (memo_idx[memo_ptr[s]:memo_ptr[s+1]] = steps depending on site s; row
+    # n_sites = steps that always run: record outputs and the result)
+    memo_elems: int = 0
+    memo_ptr: Optional[np.ndarray] = None
+    memo_idx: Optional[np.ndarray] = None
 
 
 class _Arena:
@@ -384,6 +393,12 @@ def compile_stage(
         step_rows, tables = [], []
         tab_off = 0
         flops = 0.0
+        step_index: dict[int, int] = {}   # node -> index of the step of this program that computes it
+        memo_off: dict[int, int] = {}
+        memo_top = 0
+        step_sites: list[int] = []        # per step: bitset of the gate sites its value depends on
+        always_steps: list[int] = []
+        n_sites = 1 + max([o.sel_arg for o in operands if o.sel_kind == SEL_KRAUS], default=-1)
         prog_leaves: list[list[int]] = []
         prog_leaf_index: dict[int, int] = {}
         ext_reads: dict[int, int] = {}
@@ -474,9 +489,29 @@ def compile_stage(
                 parts.append(np.asarray(dyn_words, dtype=np.int64))
             words = np.concatenate(parts).astype(np.uint32)
             tables.append(words)
+            # memo words: where the operands' variant-0 values live and which steps produce them
+            deps = 0
+            memo_words = []
+            for base in (base_a, base_b):
+                if base in step_index:
+                    memo_words.append((memo_off[base], step_index[base]))
+                    deps |= step_sites[step_index[base]]
+                else:
+                    memo_words.append((0, MEMO_NONE))
+                    if base < n_leaves and operands[base].sel_kind == SEL_KRAUS:
+                        deps |= 1 << operands[base].sel_arg
+            is_always = o_kind == 1 or nid == root
+            if is_always:
+                conj_flags |= 16
+                always_steps.append(len(step_rows))
+            step_index[nid] = len(step_rows)
+            memo_off[nid] = memo_top
+            step_sites.append(deps)
             step_rows.append(
-                [a_kind, a_ref, b_kind, b_ref, o_kind, o_ref, nd.size, k_n, lo_n, hi_n, tab_off, conj_flags]
+                [a_kind, a_ref, b_kind, b_ref, o_kind, o_ref, nd.size, k_n, lo_n, hi_n, tab_off, conj_flags,
+                 memo_words[0][0], memo_words[1][0], memo_words[0][1] | (memo_words[1][1] << 16), memo_top]
             )
+            memo_top += (nd.size + 3) & ~3
             tab_off += words.size
             flops += float(nd.size) if select else float(nd.size) * k_n
             if nid == root:
@@ -488,8 +523,24 @@ def compile_stage(
             result_kind, result_ref = ref_of(root)
             if tuple(open_order) != tuple(rootn.labels):
                 raise CapacityError("single-operand network with permuted open legs")
+        memo_elems, memo_ptr, memo_idx = 0, None, None
+        uses_prefix = any(row[11] & (4 | 8) for row in step_rows) or any(lf[2] == SEL_PREFIX for lf in prog_leaves)
+        if (p == 0 and threads > 32 and MEMO_MIN_STEPS <= len(step_rows) < MEMO_NONE and n_sites > 0
+                and not uses_prefix):
+            rows_per_site: list[list[int]] = [[] for _ in range(n_sites + 1)]
+            for k, deps in enumerate(step_sites):
+                while deps:
+                    low = deps & -deps
+                    rows_per_site[low.bit_length() - 1].append(k)
+                    deps ^= low
+            rows_per_site[n_sites] = always_steps
+            memo_ptr = np.zeros(n_sites + 2, dtype=np.uint32)
+            memo_ptr[1:] = np.cumsum([len(r) for r in rows_per_site])
+            memo_idx = np.asarray([k for r in rows_per_site for k in r], dtype=np.uint32)
+            memo_elems = memo_top
         programs.append(
             Program(
+                memo_elems=int(memo_elems), memo_ptr=memo_ptr, memo_idx=memo_idx,
                 leaves=np.asarray(prog_leaves, dtype=np.uint32).reshape(-1, LEAF_WORDS),
                 steps=np.asarray(step_rows, dtype=np.uint32).reshape(-1, STEP_WORDS),
                 tables=np.concatenate(tables).astype(np.uint32) if tables else np.zeros(0, np.uint32),
@@ -601,10 +652,14 @@ class ProgramDesc(ctypes.Structure):
         ("result_kind", ctypes.c_uint32),
         ("result_ref", ctypes.c_uint32),
         ("proj_d", ctypes.c_uint32),
-        ("reserved", ctypes.c_uint32),
+        ("memo_elems", ctypes.c_uint32),
         ("leaves", ctypes.c_void_p),
         ("steps", ctypes.c_void_p),
         ("tables", ctypes.c_void_p),
+        ("memo_ptr", ctypes.c_void_p),
+        ("memo_idx", ctypes.c_void_p),
+        ("n_memo_idx", ctypes.c_uint32),
+        ("n_memo_sites", ctypes.c_uint32),
     ]
 
 
@@ -643,10 +698,17 @@ class CompiledPlan:
             st = np.ascontiguousarray(pr.steps, dtype=np.uint32)
             tb = np.ascontiguousarray(pr.tables, dtype=np.uint32)
             keep += [lv, st, tb]
+            mp = mi = None
+            if pr.memo_elems:
+                mp = np.ascontiguousarray(pr.memo_ptr, dtype=np.uint32)
+                mi = np.ascontiguousarray(pr.memo_idx, dtype=np.uint32)
+                keep += [mp, mi]
             arr[k] = ProgramDesc(
                 lv.shape[0], st.shape[0], tb.size, pr.arena_fast, pr.arena_spill, pr.out_elems,
-                pr.threads, pr.level, pr.result_kind, pr.result_ref, pr.proj_d, 0,
+                pr.threads, pr.level, pr.result_kind, pr.result_ref, pr.proj_d, pr.memo_elems,
                 lv.ctypes.data, st.ctypes.data, tb.ctypes.data,
+                mp.ctypes.data if mp is not None else None, mi.ctypes.data if mi is not None else None,
+                mi.size if mi is not None else 0, (mp.size - 2) if mp is not None else 0,
             )
         sizes = np.asarray(self.sizes, dtype=np.uint32)
         pool = np.ascontiguousarray(self.pool)

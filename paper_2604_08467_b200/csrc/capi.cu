@@ -28,6 +28,8 @@ thread_local Workspace* g_ws = nullptr;
 struct Program {
   ptsbe_program_desc d;
   DevBuf leaves, steps, tables;
+  DevBuf memo_ptr, memo_idx, memo;  // variant-0 memo (class-0 programs): site -> steps CSR, values
+  bool memo_ready = false;
   int blocks_per_sm = 0;  // resolved lazily per (program, item_bytes)
 };
 
@@ -153,12 +155,15 @@ static ExecLaunch configure_exec(ptsbe_plan* pl, Program& pr, uint32_t n_items) 
     L.block = gs;
   }
   L.smem = ib * L.groups_per_block + 1024;
+  const bool memo = !warp && d.memo_elems;
+  if (memo) L.smem += memo_smem_bytes(d.n_steps);
   if (L.smem > 227 * 1024)
     throw Failure(PTSBE_ERESOURCE, "stage program needs more shared memory than one SM has");
-  void (*kern)(ExecArgs) = gs == 8    ? exec_kernel<R, 8>
-                           : gs == 16 ? exec_kernel<R, 16>
-                           : gs == 32 ? exec_kernel<R, 32>
-                                      : exec_kernel<R, 0>;
+  void (*kern)(ExecArgs) = gs == 8    ? exec_kernel<R, 8, false>
+                           : gs == 16 ? exec_kernel<R, 16, false>
+                           : gs == 32 ? exec_kernel<R, 32, false>
+                           : memo     ? exec_kernel<R, 0, true>
+                                      : exec_kernel<R, 0, false>;
   if (pr.blocks_per_sm == 0) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     int nb = 0;
@@ -174,9 +179,40 @@ static ExecLaunch configure_exec(ptsbe_plan* pl, Program& pr, uint32_t n_items) 
 template <typename R>
 static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelDev* levels_dev,
                         const uint8_t* kraus_dev, uint32_t first, uint32_t n_items, void* out,
+                        double* mass, double* minv, uint32_t vec_stride, uint32_t vec_row);
+
+// Variant-0 memo of a class-0 program: one pass of the interpreter over a single pseudo work
+// item whose Kraus-index row is all zeros, every step writing its value to the memo.
+template <typename R>
+static void build_memo(ptsbe_plan* pl, Program& pr) {
+  cudaStream_t st = pl->stream;
+  WorkspaceScope persistent(nullptr);  // the memo outlives the run whose workspace is installed
+  pr.memo.alloc((size_t)pr.d.memo_elems * pl->elem + 64, st);
+  const size_t pfx_at = 64 + (((size_t)pl->g + 7) & ~size_t(7));
+  DevBuf zeros(pfx_at + 8 * pl->words, st), lvl(2 * sizeof(LevelDev), st);
+  CK(cudaMemsetAsync(zeros.p, 0, zeros.bytes, st));
+  LevelDev table[2];
+  memset(table, 0, sizeof table);
+  table[1].eset = zeros.as<uint32_t>();
+  table[1].parent = zeros.as<uint32_t>();
+  table[1].prefix = reinterpret_cast<const uint64_t*>(zeros.as<char>() + pfx_at);
+  table[1].n = 1;
+  CK(cudaMemcpyAsync(lvl.p, table, sizeof table, cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));  // `table` is a stack object
+  launch_exec<R>(pl, pr, EXEC_MEMO_BUILD, lvl.as<LevelDev>(), zeros.as<uint8_t>() + 64, 0, 1, nullptr,
+                 nullptr, nullptr, 0, 0);
+  CK(cudaStreamSynchronize(st));
+  pr.memo_ready = true;
+}
+
+template <typename R>
+static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelDev* levels_dev,
+                        const uint8_t* kraus_dev, uint32_t first, uint32_t n_items, void* out,
                         double* mass, double* minv, uint32_t vec_stride, uint32_t vec_row) {
   using C = typename CxT<R>::type;
   if (n_items == 0) return;
+  const bool memo = pr.d.memo_elems && pr.d.threads_per_item > 32;
+  if (memo && !pr.memo_ready && mode != EXEC_MEMO_BUILD) build_memo<R>(pl, pr);
   ExecLaunch L = configure_exec<R>(pl, pr, n_items);
   DevBuf spill;
   if (pr.d.arena_spill_elems)
@@ -208,11 +244,16 @@ static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelD
   a.mode = mode;
   a.vec_stride = vec_stride;
   a.vec_row = vec_row;
+  a.memo = memo ? pr.memo.p : nullptr;
+  a.memo_ptr = pr.memo_ptr.as<uint32_t>();
+  a.memo_idx = pr.memo_idx.as<uint32_t>();
+  a.n_memo_sites = pr.d.n_memo_sites;
   const uint32_t gs = pr.d.threads_per_item;
-  if (gs == 8) exec_kernel<R, 8><<<L.grid, L.block, L.smem, pl->stream>>>(a);
-  else if (gs == 16) exec_kernel<R, 16><<<L.grid, L.block, L.smem, pl->stream>>>(a);
-  else if (gs == 32) exec_kernel<R, 32><<<L.grid, L.block, L.smem, pl->stream>>>(a);
-  else exec_kernel<R, 0><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  if (gs == 8) exec_kernel<R, 8, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  else if (gs == 16) exec_kernel<R, 16, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  else if (gs == 32) exec_kernel<R, 32, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  else if (memo) exec_kernel<R, 0, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  else exec_kernel<R, 0, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
   g_launches++;
   CK(cudaGetLastError());
 }
@@ -887,6 +928,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     if (const char* dm = getenv("PTSBE_DESCENT_MULT")) if (*dm) pl->descent_mult = atof(dm);
     pl->chunk_shots = env_size("PTSBE_CHUNK_SHOTS", pl->chunk_shots);
     pl->ext_budget = env_size("PTSBE_EXT_BYTES", pl->ext_budget);
+    const bool use_memo = env_size("PTSBE_MEMO", 1) != 0;  // variant-0 memo of class-0 programs
     cudaStream_t st = pl->stream;
     pl->pool.alloc(std::max<size_t>(16, d->pool_elems * pl->elem), st);
     if (d->pool_elems)
@@ -898,6 +940,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
       for (uint32_t p = 0; p < j; ++p, ++k) {
         Program& pr = pl->programs[j - 1][p];
         pr.d = d->programs[k];
+        if (!use_memo) pr.d.memo_elems = 0;
         if (pr.d.level != p + 1) throw Failure(PTSBE_EINVAL, "program level does not match its pass");
         if (pr.d.result_kind == 3 && (p + 1 != j || j < 2 || pr.d.proj_d < 1))
           throw Failure(PTSBE_EINVAL, "projection form is only valid for the marginal pass of a stage >= 2");
@@ -916,7 +959,18 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
         if (pr.d.n_table_words)
           CK(cudaMemcpyAsync(pr.tables.p, pr.d.tables, (size_t)pr.d.n_table_words * 4,
                              cudaMemcpyHostToDevice, st));
-        pr.d.leaves = pr.d.steps = pr.d.tables = nullptr;
+        if (pr.d.memo_elems) {
+          if (!pr.d.memo_ptr || !pr.d.memo_idx || pr.d.n_memo_sites > pl->g || pr.d.n_steps >= 0xFFFF)
+            throw Failure(PTSBE_EINVAL, "memo program without its site -> steps table");
+          const size_t np = (size_t)pr.d.n_memo_sites + 2;
+          pr.memo_ptr.alloc(np * 4, st);
+          pr.memo_idx.alloc(std::max<size_t>(16, (size_t)pr.d.n_memo_idx * 4), st);
+          CK(cudaMemcpyAsync(pr.memo_ptr.p, pr.d.memo_ptr, np * 4, cudaMemcpyHostToDevice, st));
+          if (pr.d.n_memo_idx)
+            CK(cudaMemcpyAsync(pr.memo_idx.p, pr.d.memo_idx, (size_t)pr.d.n_memo_idx * 4,
+                               cudaMemcpyHostToDevice, st));
+        }
+        pr.d.leaves = pr.d.steps = pr.d.tables = pr.d.memo_ptr = pr.d.memo_idx = nullptr;
       }
     }
     CK(cudaStreamSynchronize(st));
@@ -931,7 +985,10 @@ void ptsbe_plan_destroy(ptsbe_plan* pl) {
   pl->ws_cache.clear();
   pl->pool.release();
   for (auto& s : pl->programs)
-    for (auto& p : s) { p.leaves.release(); p.steps.release(); p.tables.release(); }
+    for (auto& p : s) {
+      p.leaves.release(); p.steps.release(); p.tables.release();
+      p.memo_ptr.release(); p.memo_idx.release(); p.memo.release();
+    }
   cudaStreamSynchronize(pl->stream);
   cudaStreamDestroy(pl->stream);
   delete pl;

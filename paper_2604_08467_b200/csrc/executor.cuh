@@ -19,7 +19,8 @@
 
 namespace ptsbe {
 
-constexpr int STEP_WORDS = 12;
+constexpr int STEP_WORDS = 16;
+constexpr uint32_t MEMO_NONE = 0xFFFFu;
 constexpr int LEAF_WORDS = 4;
 
 // Per-level view of the work-item lists (device memory, one entry per level,
@@ -33,7 +34,14 @@ struct LevelDev {
   uint32_t ext_rec;
 };
 
-enum ExecMode { EXEC_HOIST = 0, EXEC_MARGINAL = 1, EXEC_RAW = 2, EXEC_VECTOR = 3 };
+enum ExecMode { EXEC_HOIST = 0, EXEC_MARGINAL = 1, EXEC_RAW = 2, EXEC_VECTOR = 3, EXEC_MEMO_BUILD = 4 };
+
+// shared memory of the variant-0 memo bookkeeping: dirty + run bitmaps, the compacted list of
+// steps to run (u16) and its length
+__host__ __device__ inline uint32_t memo_words(uint32_t n_steps) { return (n_steps + 31) / 32; }
+__host__ __device__ inline uint32_t memo_smem_bytes(uint32_t n_steps) {
+  return (2 * memo_words(n_steps) * 4 + n_steps * 2 + 16 + 15) & ~15u;
+}
 
 struct ExecArgs {
   const uint32_t* leaves;
@@ -62,6 +70,11 @@ struct ExecArgs {
   uint32_t mode;
   uint32_t vec_stride;  // VECTOR: row pitch (items, padded) of the transposed output
   uint32_t vec_row;     // VECTOR: non-zero -> one row of vec_row elements per item instead (descent.cuh)
+  // variant-0 memo (class-0 programs run one CTA per error set)
+  void* memo;                // [memo_elems] value of every step with Kraus index 0 at every site
+  const uint32_t* memo_ptr;  // [n_memo_sites + 2] CSR: steps depending on site s; last row: always-run
+  const uint32_t* memo_idx;
+  uint32_t n_memo_sites;
 };
 
 template <typename R> struct CxT;
@@ -115,7 +128,11 @@ __device__ __forceinline__ void step_fixed_k(const C* __restrict__ A, const C* _
 
 // GS > 0 : sub-warp mapping, GS lanes per item, 32 / GS items per warp, __syncwarp between steps
 // GS == 0: one CTA per item, __syncthreads between steps
-template <typename R, int GS>
+// MEMO    : (GS == 0 only) class-0 program with a variant-0 memo.  UPV leaves every tensor of the
+//           template untouched except at the sites where this error set realised an operator, so
+//           only the steps above those sites are re-executed; everything else is read from the
+//           memo that was computed once per plan.
+template <typename R, int GS, bool MEMO>
 __global__ void exec_kernel(const ExecArgs a) {
   using C = typename CxT<R>::type;
   constexpr bool WARP = GS > 0;
@@ -137,6 +154,14 @@ __global__ void exec_kernel(const ExecArgs a) {
   const C* pool = reinterpret_cast<const C*>(a.pool);
   // scratch for CTA-wide reductions (marginal epilogue), placed after the groups
   double* red = reinterpret_cast<double*>(smem_raw + (size_t)groups_per_block * a.item_bytes);
+  // memo bookkeeping, after the reduction scratch
+  const uint32_t mw = MEMO ? memo_words(a.n_steps) : 0;
+  uint32_t* dirty = reinterpret_cast<uint32_t*>(smem_raw + (size_t)groups_per_block * a.item_bytes + 1024);
+  uint32_t* runb = dirty + mw;
+  uint32_t* n_run_s = runb + mw;
+  uint16_t* run_list = reinterpret_cast<uint16_t*>(n_run_s + 4);
+  const C* memo = reinterpret_cast<const C*>(a.memo);
+  const bool build = MEMO && a.mode == EXEC_MEMO_BUILD;
 
   auto group_sync = [&]() {
     if (WARP) __syncwarp(); else __syncthreads();
@@ -163,7 +188,50 @@ __global__ void exec_kernel(const ExecArgs a) {
     const uint32_t e = lv.eset[item];
     for (uint32_t w = tid; w < a.words; w += gsize) pfx[w] = lv.prefix[(size_t)w * lv.n + item];
     const uint8_t* sel = a.kraus + (size_t)e * a.g;  // Kraus-index row: shared by all items of the error set (L1/L2)
+    if constexpr (MEMO) {
+      for (uint32_t w = tid; w < 2 * mw; w += gsize) dirty[w] = build ? (w >= mw ? 0xffffffffu : 0u) : 0u;
+      __syncthreads();
+      if (!build) {
+        // mark the steps above every site that carries an operator, and the always-run steps
+        for (uint32_t site = tid; site <= a.n_memo_sites; site += gsize) {
+          const bool always = site == a.n_memo_sites;
+          if (!always && __ldg(sel + site) == 0) continue;
+          uint32_t* bits = always ? runb : dirty;
+          const uint32_t k1 = __ldg(a.memo_ptr + site + 1);
+          for (uint32_t k = __ldg(a.memo_ptr + site); k < k1; ++k) {
+            const uint32_t idx = __ldg(a.memo_idx + k);
+            atomicOr(bits + (idx >> 5), 1u << (idx & 31));
+          }
+        }
+        __syncthreads();
+      }
+      // compact (dirty | always) into an ordered list of step indices
+      if (threadIdx.x < 32) {
+        uint32_t base = 0;
+        for (uint32_t w0 = 0; w0 < mw; w0 += 32) {
+          const uint32_t w = w0 + threadIdx.x;
+          uint32_t word = w < mw ? (dirty[w] | runb[w]) : 0u;
+          if (w == mw - 1 && (a.n_steps & 31)) word &= (1u << (a.n_steps & 31)) - 1u;
+          const uint32_t cnt = __popc(word);
+          uint32_t incl = cnt;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+            if ((int)threadIdx.x >= d) incl += o;
+          }
+          uint32_t pos = base + incl - cnt;
+          while (word) {
+            const uint32_t bit = __ffs(word) - 1;
+            run_list[pos++] = (uint16_t)(w * 32 + bit);
+            word &= word - 1;
+          }
+          base += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (threadIdx.x == 0) *n_run_s = base;
+      }
+    }
     group_sync();
+    const uint32_t n_run = MEMO ? *n_run_s : a.n_steps;
 
     // measured bit selected by a prefix-projector leaf (slice steps read the bit, not the vector)
     auto leaf_bit = [&](uint32_t ref) -> uint32_t {
@@ -185,9 +253,11 @@ __global__ void exec_kernel(const ExecArgs a) {
     };
 
     // ---- replay the stored path ----
-    for (uint32_t s = 0; s < a.n_steps; ++s) {
+    for (uint32_t si = 0; si < n_run; ++si) {
+      const uint32_t s = MEMO ? run_list[si] : si;
       const uint4* st4 = reinterpret_cast<const uint4*>(a.steps + (size_t)s * STEP_WORDS);
-      // s0 = {a_kind, a_ref, b_kind, b_ref}, s1 = {o_kind, o_ref, out_n, k_n}, s2 = {lo_n, hi_n, tab_off, -}
+      // s0 = {a_kind, a_ref, b_kind, b_ref}, s1 = {o_kind, o_ref, out_n, k_n}, s2 = {lo_n, hi_n, tab_off, flags}
+      // s3 = {a_memo, b_memo, a_prod | b_prod << 16, own_memo}
       const uint4 s0 = __ldg(st4), s1 = __ldg(st4 + 1), s2 = __ldg(st4 + 2);
       const bool slice = (s2.w & 4u) != 0;
       const C* A = resolve(s0.x, s0.y);
@@ -195,7 +265,20 @@ __global__ void exec_kernel(const ExecArgs a) {
       C* O;
       size_t o_stride = 1;
       bool store = true;
-      if (s1.x == 0) {
+      bool copy_memo = false;
+      uint32_t own_memo = 0;
+      if (MEMO) {
+        const uint4 s3 = __ldg(st4 + 3);
+        const uint32_t pa = s3.z & 0xFFFFu, pb = s3.z >> 16;
+        if (pa != MEMO_NONE && !((dirty[pa >> 5] >> (pa & 31)) & 1u)) A = memo + s3.x;
+        if (pb != MEMO_NONE && !((dirty[pb >> 5] >> (pb & 31)) & 1u)) B = memo + s3.y;
+        own_memo = s3.w;
+        // an always-run step whose inputs are clean: its value is the memo's
+        copy_memo = !build && !((dirty[s >> 5] >> (s & 31)) & 1u);
+      }
+      if (build) {
+        O = const_cast<C*>(memo) + own_memo;
+      } else if (s1.x == 0) {
         O = s1.y < a.arena_fast ? arena + s1.y : spill + (s1.y - a.arena_fast);
       } else if (a.mode == EXEC_VECTOR) {
         if (a.vec_row) {
@@ -237,7 +320,11 @@ __global__ void exec_kernel(const ExecArgs a) {
           if ((pfx[q >> 6] >> (63 - (q & 63))) & 1ull) B += __ldg(dt + 2 + 2 * i);
         }
       }
-      if (slice) {
+      if (MEMO && copy_memo) {
+        const C* src = memo + own_memo;
+        for (uint32_t c = tid; c < t.out_n; c += gsize)
+          if (store) O[(size_t)c * o_stride] = src[c];
+      } else if (slice) {
         // B is the basis vector e_x of a measured bit, contracted over its only label:
         // out[c] = A[a0(c) + kA[x]] -- a gather, no multiply-adds
         const uint32_t k0 = __ldg(t.kA), k1 = __ldg(t.kA + 1);

@@ -129,9 +129,42 @@ def test_bra_subtrees_are_conjugate_twins_not_recomputed(golden_cases):
     (reference engine.py:393 builds it with np.conj): the compiler reads the ket
     results with a conjugation flag instead of contracting the bra half again."""
     pipe, tables, es = _pipeline(golden_cases["hea8"], hypersamples=16)
-    flagged = sum(int(np.count_nonzero(pr.steps[:, 11])) for pr in pipe.compiled.programs if len(pr.steps))
+    flagged = sum(int(np.count_nonzero(pr.steps[:, 11] & 3)) for pr in pipe.compiled.programs if len(pr.steps))
     assert flagged >= 1
     # and the emulated programs still reproduce the reference marginals (checked per case above)
     j = pipe.plan.f
     top = pipe.programs_of(j)[-1]
     assert top.proj_d >= 1 and top.result_kind == 3
+
+
+def test_variant0_memo_skips_clean_steps_and_keeps_values():
+    """Class-0 programs carry a variant-0 memo: steps whose inputs see no error
+    are not re-executed per error set.  Emulated with and without the memo the
+    records must be identical, and most steps must be skipped at low noise."""
+    import dataclasses
+
+    from paper_2604_08467_b200 import workloads
+
+    c, _ = workloads.hea(14, 4, gamma=0.02, p=0.02, seed=7)
+    tpl = CircuitNetwork.from_circuit(c)
+    tables = VariantTables.from_channels(tpl)
+    ctx = SamplerContext(hypersamples=8, planner_seed=3, dtype="complex128")
+    pipe = DevicePipeline(tpl, BatchPlan((7, 7)), tables, ctx, shots_per_set=1000.0, upload=False)
+    rows = workloads.presample_matrix(c, 12, np.random.default_rng(5))
+    rows[0] = 0  # an error-free set: only the always-run steps execute
+    memo_programs = 0
+    for j in (1, 2):
+        progs = pipe.programs_of(j)
+        memo_programs += sum(1 for pr in progs if pr.memo_elems)
+        plain = [dataclasses.replace(pr, memo_elems=0) for pr in progs]
+        for r, row in enumerate(rows):
+            bits = [(r >> k) & 1 for k in range(14)]
+            stats = {}
+            got = emulator.run_stage(progs, pipe.compiled.pool, row, bits, stats=stats)
+            want = emulator.run_stage(plain, pipe.compiled.pool, row, bits)
+            np.testing.assert_array_equal(got, want)
+            if stats:
+                assert stats["executed"] < stats["total"]
+                if r == 0:
+                    assert stats["executed"] <= 0.25 * stats["total"]
+    assert memo_programs >= 1

@@ -326,3 +326,33 @@ def test_full_size_properties_cfg1():
     # GHZ with weak noise: the two GHZ strings dominate
     top = {r.bitstring: r.count for r in res.records}
     assert top["0" * 12] + top["1" * 12] > 0.8 * 64000
+
+
+def test_variant0_memo_bit_exact_vs_oracle_and_vs_full_replay(monkeypatch):
+    """Class-0 programs re-execute only the steps above a site that carries an
+    operator (variant-0 memo, csrc/executor.cuh MEMO).  The arithmetic of the
+    executed steps is unchanged, so complex128 records must equal both the
+    oracle's and those of the full replay (PTSBE_MEMO=0), error-free sets included."""
+    c, tpl, es = _hea_case(14, 4, 6, 400, 21, gamma=0.02)
+    es[0] = ErrorSet(es[0].id, tuple("K0" if len(lb) == 2 and lb[0] == "K" else "I" * len(lb) for lb in es[0].realized), es[0].m)
+    sizes = (7, 7)
+
+    def run(memo):
+        monkeypatch.setenv("PTSBE_MEMO", "1" if memo else "0")
+        ctx = SamplerContext(hypersamples=8, dtype="complex128")
+        out = sample_proportional_batched(tpl, es, BatchPlan(sizes), 77, ctx)
+        return [[(r.bitstring, r.count) for r in recs] for recs in out], dict(ctx.stats.stage_events)
+
+    with_memo, ev1 = run(True)
+    without, ev0 = run(False)
+    assert with_memo == without and ev1 == ev0
+    ops, finals = bridge.template_of(c)
+    _, want, events = O.run_proportional(ops, finals, sizes, bridge.oracle_errorsets(c, es), 77)
+    assert with_memo == want and ev1 == events
+    # marginals through the memo path, complex64 within 1e-5 of the oracle
+    pfx = [recs[0][0][:7] for recs in want]
+    probs = conditional_marginals_batched(tpl, es, BatchPlan(sizes), 2, pfx, SamplerContext(hypersamples=8, dtype="complex64"))
+    for k, p, row in zip(es, pfx, probs):
+        mops, _ = bridge.merged_ops(c, k.realized)
+        ref = O.conditional_marginal(mops, finals, sizes, 2, p)
+        assert np.max(np.abs(row - ref)) <= 1e-5 * ref.max()
