@@ -15,6 +15,7 @@
 #include "descent.cuh"
 #include "executor.cuh"
 #include "histogram.cuh"
+#include "lane.cuh"
 #include "project.cuh"
 #include "sampler.cuh"
 #include "scan.cuh"
@@ -31,6 +32,10 @@ struct Program {
   DevBuf memo_ptr, memo_idx, memo;  // variant-0 memo (class-0 programs): site -> steps CSR, values
   bool memo_ready = false;
   int blocks_per_sm = 0;  // resolved lazily per (program, item_bytes)
+  // lane-per-item interpreter (lane.cuh): program small enough to run one thread per work item;
+  // lane_fused: additionally its last step alone produces the projection vector
+  bool lane_ok = false, lane_fused = false;
+  int lane_blocks_per_sm = 0;
 };
 
 }  // namespace ptsbe
@@ -50,6 +55,7 @@ struct ptsbe_plan {
   // tunables (environment overrides for experiments)
   size_t probs_budget = 256ull << 20;  // bytes of marginal buffer per sub-batch
   size_t vec_budget = 512ull << 20;    // bytes of per-item vectors per sub-batch (descent stages)
+  uint32_t lane = 1;                   // lane-per-item interpreter / fused descent (lane.cuh)
   uint32_t descent = 1;                // per-qubit descent sampler for low-multiplicity stages
   double descent_mult = 4.0;           // ... used when shots / unique prefixes of the stage <= this
   uint64_t chunk_shots = 1ull << 26;
@@ -268,6 +274,94 @@ static void launch_exec_any(ptsbe_plan* pl, Program& pr, uint32_t mode, const Le
     launch_exec<double>(pl, pr, mode, lv, kraus, first, n, out, mass, minv, vec_stride, vec_row);
 }
 
+// ---- lane-per-item interpreter (lane.cuh) ----
+static void classify_lane(const ptsbe_plan* pl, Program& pr) {
+  const ptsbe_program_desc& d = pr.d;
+  pr.lane_ok = pr.lane_fused = false;
+  if (!d.n_steps || !d.steps || d.threads_per_item > 32 || d.arena_spill_elems || d.arena_fast_elems > 48 ||
+      d.memo_elems || d.level + 1 > (uint32_t)LN_MAX_LEVELS || pl->f + 2 > (uint32_t)LN_MAX_LEVELS)
+    return;
+  const size_t image = ((size_t)d.n_steps * STEP_WORDS + (size_t)d.n_leaves * LEAF_WORDS + d.n_table_words) * 4;
+  if (image > 24 * 1024) return;
+  const LaneLayout L = lane_layout(d.n_steps, d.n_leaves, d.n_table_words, pl->f + 2, d.arena_fast_elems,
+                                   pl->words, (uint32_t)pl->elem);
+  if (L.end > 72 * 1024) return;  // keeps at least three CTAs per SM
+  uint64_t serial = 0;
+  bool inner_to_arena = true;
+  for (uint32_t s = 0; s < d.n_steps; ++s) {
+    const uint32_t* st = d.steps + (size_t)s * STEP_WORDS;
+    serial += (uint64_t)st[6] * std::max<uint32_t>(st[7], 1);
+    if (s + 1 < d.n_steps && st[4] != 0) inner_to_arena = false;
+  }
+  if (serial > 16384) return;  // one thread would run too long; the group mapping is better
+  pr.lane_ok = true;
+  const uint32_t* last = d.steps + (size_t)(d.n_steps - 1) * STEP_WORDS;
+  pr.lane_fused = d.proj_d && d.result_kind == 3 && inner_to_arena && last[4] == 1 && last[5] == 0 &&
+                  last[6] == d.proj_d;
+}
+
+template <typename R>
+static LaneArgs lane_args(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelDev* levels_dev,
+                          const uint8_t* kraus_dev, uint32_t first, uint32_t n_items, void* out,
+                          uint32_t vec_row) {
+  LaneArgs a;
+  memset(&a, 0, sizeof a);
+  a.e.leaves = pr.leaves.as<uint32_t>();
+  a.e.steps = pr.steps.as<uint32_t>();
+  a.e.tables = pr.tables.as<uint32_t>();
+  a.e.pool = pl->pool.p;
+  a.e.kraus = kraus_dev;
+  a.e.levels = levels_dev;
+  a.e.out = out;
+  a.e.n_steps = pr.d.n_steps;
+  a.e.arena_fast = pr.d.arena_fast_elems;
+  a.e.out_elems = pr.d.out_elems;
+  a.e.level = pr.d.level;
+  a.e.first_item = first;
+  a.e.n_items = n_items;
+  a.e.g = pl->g;
+  a.e.words = pl->words;
+  a.e.mode = mode;
+  a.e.vec_row = vec_row;
+  a.n_leaves = pr.d.n_leaves;
+  a.n_table_words = pr.d.n_table_words;
+  a.n_levels = pl->f + 2;
+  return a;
+}
+
+template <typename R>
+static void launch_lane(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelDev* levels_dev,
+                        const uint8_t* kraus_dev, uint32_t first, uint32_t n_items, void* out,
+                        uint32_t vec_row) {
+  using C = typename CxT<R>::type;
+  if (n_items == 0) return;
+  const LaneArgs a = lane_args<R>(pl, pr, mode, levels_dev, kraus_dev, first, n_items, out, vec_row);
+  const LaneLayout L = lane_layout(a.e.n_steps, a.n_leaves, a.n_table_words, a.n_levels, a.e.arena_fast,
+                                   a.e.words, (uint32_t)sizeof(C));
+  if (pr.lane_blocks_per_sm == 0) {
+    CK(cudaFuncSetAttribute(exec_lane_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    int nb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, exec_lane_kernel<R>, LN_THREADS, L.end));
+    pr.lane_blocks_per_sm = std::max(nb, 1);
+  }
+  const uint64_t need = cdiv(n_items, LN_THREADS);
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)pl->sm_count * pr.lane_blocks_per_sm));
+  exec_lane_kernel<R><<<grid, LN_THREADS, L.end, pl->stream>>>(a);
+  g_launches++;
+  CK(cudaGetLastError());
+}
+
+// hoist pass of a per-prefix program: lane-per-item when the program qualifies
+static void launch_hoist(ptsbe_plan* pl, Program& pr, const LevelDev* lv, const uint8_t* kraus,
+                         uint32_t n, void* out) {
+  if (pr.lane_ok && pl->lane) {
+    if (pl->dtype == PTSBE_C64) launch_lane<float>(pl, pr, EXEC_HOIST, lv, kraus, 0, n, out, 0);
+    else launch_lane<double>(pl, pr, EXEC_HOIST, lv, kraus, 0, n, out, 0);
+  } else {
+    launch_exec_any(pl, pr, EXEC_HOIST, lv, kraus, 0, n, out, nullptr, nullptr);
+  }
+}
+
 // ---- per-qubit descent sampler (descent.cuh) ----
 struct DescentShape { uint32_t nch = 0, dpad = 0; size_t smem = 0; };
 
@@ -308,6 +402,54 @@ static void launch_descent(ptsbe_plan* pl, const DescentArgs& a, const DescentSh
     case 2: f32 ? launch_descent_t<float, 2>(pl, a, sh.smem) : launch_descent_t<double, 2>(pl, a, sh.smem); break;
     case 4: f32 ? launch_descent_t<float, 4>(pl, a, sh.smem) : launch_descent_t<double, 4>(pl, a, sh.smem); break;
     case 8: f32 ? launch_descent_t<float, 8>(pl, a, sh.smem) : launch_descent_t<double, 8>(pl, a, sh.smem); break;
+    default: throw Failure(PTSBE_EINVAL, "descent sampler: unsupported vector length");
+  }
+}
+
+template <typename R, int NCH>
+static void launch_lane_descent_t(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a) {
+  using C = typename CxT<R>::type;
+  using CH = typename DsChunk<R>::type;
+  const LaneLayout L = lane_layout(a.l.e.n_steps, a.l.n_leaves, a.l.n_table_words, a.l.n_levels,
+                                   a.l.e.arena_fast, a.l.e.words, (uint32_t)sizeof(C));
+  const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 4 * 4) +
+                      (((size_t)DS_GS * NCH * sizeof(CH)) << a.d.b);
+  if (smem > 200 * 1024) throw Failure(PTSBE_ERESOURCE, "fused descent needs more shared memory than one SM has");
+  if (pr.lane_blocks_per_sm == 0) {
+    CK(cudaFuncSetAttribute(lane_descent_kernel<R, NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    int nb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lane_descent_kernel<R, NCH>, LN_THREADS, smem));
+    pr.lane_blocks_per_sm = std::max(nb, 1);
+  }
+  // tiles: long enough to amortise the CTA barriers around an error-set run, short enough that
+  // every resident CTA gets several
+  const uint64_t ctas = (uint64_t)pl->sm_count * pr.lane_blocks_per_sm;
+  uint64_t tile = a.d.n_items / (ctas * 4) / LN_THREADS * LN_THREADS;
+  tile = std::min<uint64_t>(2048, std::max<uint64_t>(LN_THREADS, tile));
+  a.tile = (uint32_t)tile;
+  const uint64_t tiles = cdiv(a.d.n_items, tile);
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, ctas));
+  lane_descent_kernel<R, NCH><<<grid, LN_THREADS, smem, pl->stream>>>(a);
+  g_launches++;
+  CK(cudaGetLastError());
+}
+
+static bool lane_descent_fits(const ptsbe_plan* pl, const Program& pr, const DescentShape& sh, uint32_t b) {
+  const uint32_t elem = (uint32_t)pl->elem;
+  const LaneLayout L = lane_layout(pr.d.n_steps, pr.d.n_leaves, pr.d.n_table_words, pl->f + 2,
+                                   pr.d.arena_fast_elems, pl->words, elem);
+  const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 4 * 4) + (((size_t)DS_GS * sh.nch * 16) << b);
+  return smem <= 200 * 1024;
+}
+
+static void launch_lane_descent(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a, const DescentShape& sh) {
+  if (a.d.n_items == 0) return;
+  const bool f32 = pl->dtype == PTSBE_C64;
+  switch (sh.nch) {
+    case 1: f32 ? launch_lane_descent_t<float, 1>(pl, pr, a) : launch_lane_descent_t<double, 1>(pl, pr, a); break;
+    case 2: f32 ? launch_lane_descent_t<float, 2>(pl, pr, a) : launch_lane_descent_t<double, 2>(pl, pr, a); break;
+    case 4: f32 ? launch_lane_descent_t<float, 4>(pl, pr, a) : launch_lane_descent_t<double, 4>(pl, pr, a); break;
+    case 8: f32 ? launch_lane_descent_t<float, 8>(pl, pr, a) : launch_lane_descent_t<double, 8>(pl, pr, a); break;
     default: throw Failure(PTSBE_EINVAL, "descent sampler: unsupported vector length");
   }
 }
@@ -488,8 +630,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     for (uint32_t p = 0; p + 1 < j; ++p) {
       if (!progs[p].d.n_steps) continue;
       log.begin(&stats->hoist_ms[j - 1]);
-      launch_exec_any(pl, progs[p], EXEC_HOIST, table_dev.as<LevelDev>(), kraus_dev, 0,
-                      lv[p + 1].n, ext[p].p, nullptr, nullptr);
+      launch_hoist(pl, progs[p], table_dev.as<LevelDev>(), kraus_dev, lv[p + 1].n, ext[p].p);
       log.end();
     }
     // marginal pass + sampler, in sub-batches sized to the probs buffer
@@ -507,6 +648,63 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       log.begin(&stats->descent_ms[j - 1]);
       launch_tree_build(pl, pr, table[1].ext, table[1].ext_rec, ne, b, dsh.dpad, tree.p);
       log.end();
+      Program& prj = progs[j - 1];
+      const bool fused = pl->lane && prj.lane_fused && lane_descent_fits(pl, prj, dsh, b);
+      if (fused) {
+        // per-item steps and descent in one kernel: v never leaves the SM; raw per-draw outcomes
+        // are merged into ordered (outcome, count) pairs afterwards
+        DevBuf big_list(((size_t)(chunk_shots / LN_DEDUP_SERIAL) + 1) * 4, st), big_count(16, st);
+        CK(cudaMemsetAsync(big_count.p, 0, 16, st));
+        LaneDescentArgs fa;
+        memset(&fa, 0, sizeof fa);
+        if (pl->dtype == PTSBE_C64)
+          fa.l = lane_args<float>(pl, prj, EXEC_VECTOR, table_dev.as<LevelDev>(), kraus_dev, 0, U, nullptr, 0);
+        else
+          fa.l = lane_args<double>(pl, prj, EXEC_VECTOR, table_dev.as<LevelDev>(), kraus_dev, 0, U, nullptr, 0);
+        DescentArgs& da = fa.d;
+        da.tree = tree.p;
+        da.eset = cur.eset.as<uint32_t>();
+        da.mult = cur.mult.as<uint32_t>();
+        da.slot_off = cur.slot_off.as<uint32_t>();
+        da.eset_id = cur.gid.as<uint32_t>();
+        da.rank = cur.rank.as<uint32_t>();
+        da.slot_index = slot_index.as<uint32_t>();
+        da.slot_count = slot_count.as<uint32_t>();
+        da.nnz = nnz.as<uint32_t>();
+        da.flag = flag_dev;
+        da.flag_count = flag_count_dev;
+        da.set_mass = set_mass.as<double>();
+        da.first_item = 0;
+        da.n_items = U;
+        da.b = b;
+        da.stage = j;
+        da.k0 = (uint32_t)seed;
+        da.k1 = (uint32_t)(seed >> 32);
+        da.vanish = pl->vanish;
+        da.neg_abs = pl->neg_abs;
+        da.neg_rel = pl->neg_rel;
+        fa.big_list = big_list.as<uint32_t>();
+        fa.big_count = big_count.as<uint32_t>();
+        log.begin(&stats->descent_ms[j - 1]);
+        launch_lane_descent(pl, prj, fa, dsh);
+        DedupArgs dd;
+        dd.slot_off = da.slot_off;
+        dd.slot_index = da.slot_index;
+        dd.slot_count = da.slot_count;
+        dd.nnz = da.nnz;
+        dd.big_list = fa.big_list;
+        dd.big_count = fa.big_count;
+        dd.first_item = 0;
+        dd.n_items = U;
+        dd.b = b;
+        dedup_kernel<<<cdiv(U, 256), 256, 0, st>>>(dd);
+        dedup_big_kernel<<<pl->sm_count, 256, sizeof(uint32_t) << b, st>>>(dd);
+        g_launches += 2;
+        CK(cudaGetLastError());
+        log.end();
+        stats->marg_launches[j - 1]++;
+        stats->descent_items[j - 1] += U;
+      } else {
       const size_t row = (size_t)dsh.dpad * pl->elem;
       const uint32_t B = (uint32_t)std::max<size_t>(DS_TILE, std::min<size_t>(U, pl->vec_budget / row));
       DevBuf vbuf((size_t)B * row, st);
@@ -546,6 +744,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
         log.end();
       }
       stats->descent_items[j - 1] += U;
+      }
     } else {
     uint32_t B = (uint32_t)std::max<size_t>(1, std::min<size_t>(U, pl->probs_budget / (nb * real)));
     DevBuf probs((size_t)B * nb * real, st), mass((size_t)B * 8, st), minv((size_t)B * 8, st);
@@ -925,6 +1124,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     pl->probs_budget = env_size("PTSBE_PROBS_BYTES", pl->probs_budget);
     pl->vec_budget = env_size("PTSBE_VEC_BYTES", pl->vec_budget);
     pl->descent = (uint32_t)env_size("PTSBE_DESCENT", pl->descent);
+    pl->lane = (uint32_t)env_size("PTSBE_LANE", pl->lane);
     if (const char* dm = getenv("PTSBE_DESCENT_MULT")) if (*dm) pl->descent_mult = atof(dm);
     pl->chunk_shots = env_size("PTSBE_CHUNK_SHOTS", pl->chunk_shots);
     pl->ext_budget = env_size("PTSBE_EXT_BYTES", pl->ext_budget);
@@ -959,6 +1159,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
         if (pr.d.n_table_words)
           CK(cudaMemcpyAsync(pr.tables.p, pr.d.tables, (size_t)pr.d.n_table_words * 4,
                              cudaMemcpyHostToDevice, st));
+        classify_lane(pl.get(), pr);
         if (pr.d.memo_elems) {
           if (!pr.d.memo_ptr || !pr.d.memo_idx || pr.d.n_memo_sites > pl->g || pr.d.n_steps >= 0xFFFF)
             throw Failure(PTSBE_EINVAL, "memo program without its site -> steps table");

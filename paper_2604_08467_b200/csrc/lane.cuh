@@ -1,0 +1,640 @@
+// Lane-per-item interpreter for the tiny per-prefix programs, and the fused
+// "per-item steps + per-qubit descent" sampler built on it.
+//
+// The per-prefix passes of a stage (class >= 1 nodes of the stored path: the few
+// contractions that depend on measured bits) are 2-20 steps over rank <= 4
+// tensors -- a few hundred multiply-adds per work item, repeated for tens of
+// millions of items.  With a group of lanes per item (executor.cuh) most issued
+// instructions are step decoding replicated in every group.  Here ONE THREAD owns
+// a work item: the step decode and every gather-table entry are warp-uniform
+// (served from the program image in shared memory as broadcasts), only operand
+// loads and the multiply-adds are per-lane work, and the item's intermediates
+// live in a private slice of a warp-interleaved shared-memory arena
+// (element e of lane t at [e * 33 + t]: conflict-free for "same element, all
+// lanes" as well as for "same item, different elements").
+//
+// lane_descent_kernel additionally keeps the item's last intermediate on chip:
+// the final step (the one that produces the projection vector v) is evaluated by
+// the 8-lane group that draws from it, straight into registers, so v never exists
+// in memory.  A draw is the unit of work of the descent phase (no loop over an
+// item's multiplicity, no idle groups next to a high-multiplicity item); the raw
+// per-draw outcomes are merged into ordered (outcome, count) pairs by
+// dedup_kernel afterwards.
+//
+// Same semantics as executor.cuh / descent.cuh (reference engine.py:361-450,
+// 493-524); same Philox counters, so a work item's stream does not depend on the
+// kernel that serves it.
+#pragma once
+#include "common.cuh"
+#include "descent.cuh"
+#include "executor.cuh"
+#include "sampler.cuh"
+
+namespace ptsbe {
+
+constexpr int LN_THREADS = 256;
+constexpr int LN_WARPS = LN_THREADS / 32;
+constexpr int LN_AST = 33;          // arena element stride (in elements) between consecutive indices
+constexpr int LN_MAX_LEVELS = 16;   // ancestors kept per lane
+constexpr uint32_t LN_DEDUP_SERIAL = 48;  // draws per item merged by one thread; more: warp path
+
+// shared-memory layout shared by the two kernels (offsets in bytes from the dynamic base)
+struct LaneLayout {
+  uint32_t steps_off, leaves_off, tables_off, levels_off, arena_off, anc_off, pfx_off, end;
+};
+
+__host__ __device__ inline LaneLayout lane_layout(uint32_t n_steps, uint32_t n_leaves, uint32_t n_table_words,
+                                                  uint32_t n_levels, uint32_t arena_elems, uint32_t words,
+                                                  uint32_t elem_bytes) {
+  LaneLayout L;
+  uint32_t o = 0;
+  L.steps_off = o;  o += n_steps * STEP_WORDS * 4;
+  L.leaves_off = o; o += n_leaves * LEAF_WORDS * 4;
+  L.tables_off = o; o += n_table_words * 4;
+  o = (o + 15) & ~15u;
+  L.levels_off = o; o += n_levels * (uint32_t)sizeof(LevelDev);
+  o = (o + 15) & ~15u;
+  L.arena_off = o;  o += LN_WARPS * (arena_elems ? arena_elems : 1) * LN_AST * elem_bytes;
+  o = (o + 15) & ~15u;
+  L.anc_off = o;    o += n_levels * LN_THREADS * 4;
+  o = (o + 15) & ~15u;
+  L.pfx_off = o;    o += words * LN_THREADS * 8;
+  L.end = (o + 15) & ~15u;
+  return L;
+}
+
+// One operand of a step as seen by one lane: a (generic) pointer and an element stride --
+// LN_AST inside the lane's private arena slice, 1 for a leaf in the operand pool or a record
+// of an earlier pass.  One code path serves both, so the inner loops carry no branch.
+template <typename C>
+struct LaneOp {
+  const C* p;
+  uint32_t stride;
+};
+
+template <typename R>
+struct LaneCtx {
+  using C = typename CxT<R>::type;
+  const uint32_t* steps;
+  const uint32_t* leaves;
+  const uint32_t* tables;
+  const LevelDev* levels;   // shared-memory copy
+  C* arena_w;               // this warp's arena
+  const uint32_t* anc;      // [level][LN_THREADS]
+  const uint64_t* pfx;      // [word][LN_THREADS]
+  const C* pool;
+  const uint8_t* kraus;
+  uint32_t g, arena_fast;
+
+  __device__ __forceinline__ uint32_t bit(uint32_t q, uint32_t slot) const {
+    return (uint32_t)((pfx[(q >> 6) * LN_THREADS + slot] >> (63 - (q & 63))) & 1ull);
+  }
+  // operand (kind, ref) for the work item whose context sits in thread slot `slot`
+  __device__ __forceinline__ LaneOp<C> resolve(uint32_t kind, uint32_t ref, uint32_t slot, uint32_t eset) const {
+    LaneOp<C> o;
+    if (kind == 0) {
+      o.p = arena_w + ref * LN_AST + (slot & 31);
+      o.stride = LN_AST;
+      return o;
+    }
+    o.stride = 1;
+    if (kind == 1) {
+      const uint4 lf = reinterpret_cast<const uint4*>(leaves)[ref];
+      uint32_t v = 0;
+      if (lf.z == 1) v = __ldg(kraus + (size_t)eset * g + lf.w);
+      else if (lf.z == 2) v = bit(lf.w, slot);
+      o.p = pool + lf.x + (size_t)v * lf.y;
+      return o;
+    }
+    const uint32_t l = kind - 1;
+    o.p = reinterpret_cast<const C*>(levels[l].ext) + (size_t)anc[l * LN_THREADS + slot] * levels[l].ext_rec + ref;
+    return o;
+  }
+};
+
+// acc += a' * b' with a' = conj(a) if FA, b' = conj(b) if FB (sign flips fold into the FMAs)
+template <bool FA, bool FB, typename C>
+__device__ __forceinline__ void cmac_s(C& acc, const C a, const C b) {
+  const auto ay = FA ? -a.y : a.y;
+  const auto by = FB ? -b.y : b.y;
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-ay, by, acc.x);
+  acc.y = fma(a.x, by, acc.y);
+  acc.y = fma(ay, b.x, acc.y);
+}
+
+// Decoded step (warp-uniform part)
+struct LaneStep {
+  uint4 s0, s1, s2;
+  const uint32_t *loA, *loB, *hiA, *hiB, *kA, *kB, *dyn;
+  uint32_t out_n, kn, lo_n, hi_n, flags;
+};
+
+__device__ __forceinline__ LaneStep lane_decode(const uint32_t* steps, const uint32_t* tables, uint32_t s) {
+  LaneStep t;
+  const uint4* st4 = reinterpret_cast<const uint4*>(steps + (size_t)s * STEP_WORDS);
+  t.s0 = st4[0]; t.s1 = st4[1]; t.s2 = st4[2];
+  t.out_n = t.s1.z; t.kn = t.s1.w; t.lo_n = t.s2.x; t.hi_n = t.s2.y; t.flags = t.s2.w;
+  t.loA = tables + t.s2.z;
+  t.loB = t.loA + t.lo_n;
+  t.hiA = t.loB + t.lo_n;
+  t.hiB = t.hiA + t.hi_n;
+  t.kA = t.hiB + t.hi_n;
+  t.kB = t.kA + t.kn;
+  t.dyn = t.kB + t.kn;
+  return t;
+}
+
+// Operands of a decoded step for the item in thread slot `slot` (slice views applied; for a
+// slice step B is unused and A already points at the selected slice)
+template <typename R>
+__device__ __forceinline__ void lane_operands(const LaneCtx<R>& cx, const LaneStep& t, uint32_t slot, uint32_t eset,
+                                              LaneOp<typename CxT<R>::type>& A, LaneOp<typename CxT<R>::type>& B) {
+  A = cx.resolve(t.s0.x, t.s0.y, slot, eset);
+  const bool slice = (t.flags & 4u) != 0;
+  if (!slice) {
+    B = cx.resolve(t.s0.z, t.s0.w, slot, eset);
+  } else {
+    // B is the basis vector e_x of a measured bit contracted over its only label: a gather
+    const uint4 lf = reinterpret_cast<const uint4*>(cx.leaves)[t.s0.w];
+    A.p += (cx.bit(lf.w, slot) ? t.kA[1] : t.kA[0]) * A.stride;
+    B = A;
+  }
+  if (t.flags & 8u) {
+    const uint32_t* dt = t.dyn;
+    const uint32_t na = dt[0];
+    uint32_t add = 0;
+    for (uint32_t i = 0; i < na; ++i)
+      if (cx.bit(dt[1 + 2 * i], slot)) add += dt[2 + 2 * i];
+    A.p += add * A.stride;
+    dt += 1 + 2 * na;
+    const uint32_t nb = dt[0];
+    add = 0;
+    for (uint32_t i = 0; i < nb; ++i)
+      if (cx.bit(dt[1 + 2 * i], slot)) add += dt[2 + 2 * i];
+    if (!slice) B.p += add * B.stride;
+  }
+}
+
+// value of output element c of a decoded step (generic form: tables read per element)
+template <typename R>
+__device__ __forceinline__ typename CxT<R>::type lane_element(
+    const LaneStep& t, const LaneOp<typename CxT<R>::type>& A, const LaneOp<typename CxT<R>::type>& B, uint32_t c) {
+  using C = typename CxT<R>::type;
+  uint32_t cl = c, ch = 0;
+  if (t.hi_n > 1) { ch = c / t.lo_n; cl = c - ch * t.lo_n; }
+  uint32_t a0 = t.loA[cl], b0 = t.loB[cl];
+  if (t.hi_n > 1) { a0 += t.hiA[ch]; b0 += t.hiB[ch]; }
+  const bool fa = t.flags & 1u, fb = t.flags & 2u;
+  if (t.flags & 4u) {
+    C v = A.p[a0 * A.stride];
+    if (fa) v.y = -v.y;
+    return v;
+  }
+  C acc; acc.x = 0; acc.y = 0;
+  for (uint32_t k = 0; k < t.kn; ++k) {
+    C x = A.p[(a0 + t.kA[k]) * A.stride], y = B.p[(b0 + t.kB[k]) * B.stride];
+    if (fa) x.y = -x.y;
+    if (fb) y.y = -y.y;
+    cmac(acc, x, y);
+  }
+  return acc;
+}
+
+// all outputs of a step with KN contracted entries: k-offsets in registers, conjugation folded
+template <typename C, int KN, bool FA, bool FB>
+__device__ __forceinline__ void lane_step_fixed(const LaneStep& t, const LaneOp<C>& A, const LaneOp<C>& B, C* O,
+                                                uint32_t o_stride, bool store) {
+  uint32_t ka[KN], kb[KN];
+#pragma unroll
+  for (int k = 0; k < KN; ++k) { ka[k] = t.kA[k] * A.stride; kb[k] = t.kB[k] * B.stride; }
+  for (uint32_t ch = 0, c = 0; ch < t.hi_n; ++ch) {
+    const uint32_t ha = t.hi_n > 1 ? t.hiA[ch] : 0u, hb = t.hi_n > 1 ? t.hiB[ch] : 0u;
+    for (uint32_t cl = 0; cl < t.lo_n; ++cl, ++c) {
+      const C* pa = A.p + (t.loA[cl] + ha) * A.stride;
+      const C* pb = B.p + (t.loB[cl] + hb) * B.stride;
+      C acc; acc.x = 0; acc.y = 0;
+#pragma unroll
+      for (int k = 0; k < KN; ++k) cmac_s<FA, FB>(acc, pa[ka[k]], pb[kb[k]]);
+      if (store) O[c * o_stride] = acc;
+    }
+  }
+}
+
+template <typename C, int KN>
+__device__ __forceinline__ void lane_step_kn(const LaneStep& t, const LaneOp<C>& A, const LaneOp<C>& B, C* O,
+                                             uint32_t o_stride, bool store) {
+  switch (t.flags & 3u) {
+    case 0: lane_step_fixed<C, KN, false, false>(t, A, B, O, o_stride, store); break;
+    case 1: lane_step_fixed<C, KN, true, false>(t, A, B, O, o_stride, store); break;
+    case 2: lane_step_fixed<C, KN, false, true>(t, A, B, O, o_stride, store); break;
+    default: lane_step_fixed<C, KN, true, true>(t, A, B, O, o_stride, store); break;
+  }
+}
+
+struct LaneArgs {
+  ExecArgs e;               // program, lists, output (HOIST record or VECTOR row per item)
+  uint32_t n_leaves, n_table_words, n_levels;
+};
+
+// Loads the program image and the level table into shared memory (all threads), returns the context.
+template <typename R>
+__device__ __forceinline__ LaneCtx<R> lane_setup(const LaneArgs& a, unsigned char* smem, const LaneLayout& L) {
+  using C = typename CxT<R>::type;
+  uint32_t* img = reinterpret_cast<uint32_t*>(smem);
+  const uint32_t ns = a.e.n_steps * STEP_WORDS, nl = a.n_leaves * LEAF_WORDS, nt = a.n_table_words;
+  for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) img[L.steps_off / 4 + i] = __ldg(a.e.steps + i);
+  for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) img[L.leaves_off / 4 + i] = __ldg(a.e.leaves + i);
+  for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) img[L.tables_off / 4 + i] = __ldg(a.e.tables + i);
+  const uint32_t lw = a.n_levels * (uint32_t)(sizeof(LevelDev) / 4);
+  const uint32_t* lsrc = reinterpret_cast<const uint32_t*>(a.e.levels);
+  for (uint32_t i = threadIdx.x; i < lw; i += blockDim.x) img[L.levels_off / 4 + i] = __ldg(lsrc + i);
+  LaneCtx<R> cx;
+  cx.steps = img + L.steps_off / 4;
+  cx.leaves = img + L.leaves_off / 4;
+  cx.tables = img + L.tables_off / 4;
+  cx.levels = reinterpret_cast<const LevelDev*>(smem + L.levels_off);
+  cx.arena_w = reinterpret_cast<C*>(smem + L.arena_off) +
+               (size_t)(threadIdx.x >> 5) * (a.e.arena_fast ? a.e.arena_fast : 1) * LN_AST;
+  cx.anc = reinterpret_cast<const uint32_t*>(smem + L.anc_off);
+  cx.pfx = reinterpret_cast<const uint64_t*>(smem + L.pfx_off);
+  cx.pool = reinterpret_cast<const C*>(a.e.pool);
+  cx.kraus = a.e.kraus;
+  cx.g = a.e.g;
+  cx.arena_fast = a.e.arena_fast;
+  return cx;
+}
+
+// Item context of this thread's slot: ancestors and prefix words -> shared memory.  Returns the
+// error-set row.
+template <typename R>
+__device__ __forceinline__ uint32_t lane_item_context(const LaneArgs& a, const LaneCtx<R>& cx, unsigned char* smem,
+                                                      const LaneLayout& L, uint32_t item) {
+  uint32_t* anc = reinterpret_cast<uint32_t*>(smem + L.anc_off);
+  uint64_t* pfx = reinterpret_cast<uint64_t*>(smem + L.pfx_off);
+  const uint32_t slot = threadIdx.x;
+  uint32_t cur = item;
+  anc[a.e.level * LN_THREADS + slot] = cur;
+  for (int l = (int)a.e.level; l > 1; --l) {
+    cur = __ldg(cx.levels[l].parent + cur);
+    anc[(l - 1) * LN_THREADS + slot] = cur;
+  }
+  const LevelDev& lv = cx.levels[a.e.level];
+  for (uint32_t w = 0; w < a.e.words; ++w) pfx[w * LN_THREADS + slot] = __ldg(lv.prefix + (size_t)w * lv.n + item);
+  return __ldg(lv.eset + item);
+}
+
+// Runs steps [s0, s1) for the item of this thread.  Outputs of kind 0 go to the private arena;
+// outputs of kind 1 to `rec` (this item's record / vector row) when `live`.
+template <typename R>
+__device__ __forceinline__ void lane_run(const LaneCtx<R>& cx, uint32_t s0, uint32_t s1, uint32_t eset,
+                                         typename CxT<R>::type* rec, bool live) {
+  using C = typename CxT<R>::type;
+  const uint32_t slot = threadIdx.x, ls = threadIdx.x & 31;
+  for (uint32_t s = s0; s < s1; ++s) {
+    const LaneStep t = lane_decode(cx.steps, cx.tables, s);
+    LaneOp<C> A, B;
+    lane_operands<R>(cx, t, slot, eset, A, B);
+    const bool to_arena = t.s1.x == 0;
+    C* O = to_arena ? cx.arena_w + t.s1.y * LN_AST + ls : rec + t.s1.y;
+    const uint32_t o_stride = to_arena ? LN_AST : 1u;
+    const bool store = to_arena || live;
+    if (t.flags & 4u) {
+      for (uint32_t c = 0; c < t.out_n; ++c) {
+        const C v = lane_element<R>(t, A, B, c);
+        if (store) O[c * o_stride] = v;
+      }
+    } else {
+      switch (t.kn) {
+        case 1: lane_step_kn<C, 1>(t, A, B, O, o_stride, store); break;
+        case 2: lane_step_kn<C, 2>(t, A, B, O, o_stride, store); break;
+        case 4: lane_step_kn<C, 4>(t, A, B, O, o_stride, store); break;
+        case 8: lane_step_kn<C, 8>(t, A, B, O, o_stride, store); break;
+        case 16: lane_step_kn<C, 16>(t, A, B, O, o_stride, store); break;
+        default:
+          for (uint32_t c = 0; c < t.out_n; ++c) {
+            const C v = lane_element<R>(t, A, B, c);
+            if (store) O[c * o_stride] = v;
+          }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// standalone: hoist passes p >= 1 and vector rows, one thread per work item
+// ---------------------------------------------------------------------------
+template <typename R>
+__global__ void __launch_bounds__(LN_THREADS) exec_lane_kernel(const LaneArgs a) {
+  using C = typename CxT<R>::type;
+  extern __shared__ __align__(16) unsigned char ln_smem[];
+  const LaneLayout L = lane_layout(a.e.n_steps, a.n_leaves, a.n_table_words, a.n_levels, a.e.arena_fast,
+                                   a.e.words, (uint32_t)sizeof(C));
+  const LaneCtx<R> cx = lane_setup<R>(a, ln_smem, L);
+  __syncthreads();
+  const uint32_t per_round = gridDim.x * LN_THREADS;
+  const uint32_t rounds = (a.e.n_items + per_round - 1) / per_round;
+  for (uint32_t r = 0; r < rounds; ++r) {
+    uint32_t it = r * per_round + blockIdx.x * LN_THREADS + threadIdx.x;
+    const bool live = it < a.e.n_items;
+    if (!live) it = a.e.n_items - 1;
+    const uint32_t item = a.e.first_item + it;
+    const uint32_t eset = lane_item_context<R>(a, cx, ln_smem, L, item);
+    __syncwarp();
+    C* rec = a.e.mode == EXEC_VECTOR ? reinterpret_cast<C*>(a.e.out) + (size_t)it * a.e.vec_row
+                                     : reinterpret_cast<C*>(a.e.out) + (size_t)item * a.e.out_elems;
+    lane_run<R>(cx, 0, a.e.n_steps, eset, rec, live);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fused: per-item steps (thread per item) + per-qubit descent (8 lanes per draw)
+// ---------------------------------------------------------------------------
+struct LaneDescentArgs {
+  LaneArgs l;               // l.e.out unused; the last step of the program produces v
+  DescentArgs d;            // d.v unused
+  uint32_t* big_list;       // items with more than LN_DEDUP_SERIAL draws (merged by dedup_big_kernel)
+  uint32_t* big_count;
+  uint32_t tile;            // consecutive items a CTA takes at a time (multiple of LN_THREADS)
+};
+
+template <typename R, int NCH>
+__global__ void __launch_bounds__(LN_THREADS) lane_descent_kernel(const LaneDescentArgs a) {
+  using C = typename CxT<R>::type;
+  using CH = typename DsChunk<R>::type;
+  constexpr int CPC = DsChunk<R>::CPC;
+  constexpr uint32_t COL = DS_GS * NCH;
+  extern __shared__ __align__(16) unsigned char ln_smem[];
+  const ExecArgs& e = a.l.e;
+  const DescentArgs& d = a.d;
+  const LaneLayout L = lane_layout(e.n_steps, a.l.n_leaves, a.l.n_table_words, a.l.n_levels, e.arena_fast, e.words,
+                                   (uint32_t)sizeof(C));
+  const LaneCtx<R> cx = lane_setup<R>(a.l, ln_smem, L);
+  const uint32_t N = 1u << d.b;
+  // after the interpreter's region: per-warp scratch, then the tree table
+  double* mass_s = reinterpret_cast<double*>(ln_smem + L.end);                 // [LN_THREADS]
+  uint32_t* cum_s = reinterpret_cast<uint32_t*>(mass_s + LN_THREADS);          // [LN_THREADS]
+  uint32_t* slot0_s = cum_s + LN_THREADS;                                      // [LN_THREADS]
+  uint32_t* eset_s = slot0_s + LN_THREADS;                                     // [LN_THREADS]
+  uint32_t* bad_s = eset_s + LN_THREADS;                                       // [LN_THREADS]
+  CH* table = reinterpret_cast<CH*>(bad_s + LN_THREADS);                       // [N][COL]
+  __shared__ uint32_t s_end;
+  const int tid = threadIdx.x, lane32 = tid & 31, warp = tid >> 5;
+  const int lane = tid & (DS_GS - 1), grp = lane32 / DS_GS;                    // 8-lane groups: 4 per warp
+  const unsigned gmask = 0xffu << (8 * grp);
+  const uint32_t wbase = warp * 32;
+  const CH* TREE = reinterpret_cast<const CH*>(d.tree);
+  uint32_t loaded = 0xffffffffu;
+  __syncthreads();  // program image complete
+  const LaneStep last = lane_decode(cx.steps, cx.tables, e.n_steps - 1);
+
+  // v of the item in warp slot i, distributed over this group's lanes: lane holds the 16-byte
+  // chunks {k * 8 + lane}, i.e. elements CPC * (k * 8 + lane) + {0, CPC - 1}.
+  // Common case (v = x (x) conj(x): one multiply per element, no slice): the gather offsets of
+  // this lane's elements do not depend on the item -- resolved once per kernel.
+  const bool fast_last = last.kn == 1 && !(last.flags & 4u) && last.hi_n == 1;
+  const uint32_t last_sa = last.s0.x == 0 ? LN_AST : 1u, last_sb = last.s0.z == 0 ? LN_AST : 1u;
+  uint32_t via[NCH * CPC], vib[NCH * CPC];
+#pragma unroll
+  for (int k = 0; k < NCH * CPC; ++k) {
+    const uint32_t c = CPC * ((k / CPC) * DS_GS + lane) + (k % CPC);
+    const bool ok = fast_last && c < last.out_n;
+    via[k] = ok ? (last.loA[c] + last.kA[0]) * last_sa : 0xffffffffu;
+    vib[k] = ok ? (last.loB[c] + last.kB[0]) * last_sb : 0u;
+  }
+  const R sgn_a = (last.flags & 1u) ? R(-1) : R(1), sgn_b = (last.flags & 2u) ? R(-1) : R(1);
+  auto vector_of = [&](uint32_t i, CH (&v)[NCH]) {
+    const uint32_t slot = wbase + i;
+    LaneOp<C> A, B;
+    lane_operands<R>(cx, last, slot, eset_s[slot], A, B);
+    C x[NCH * CPC];
+#pragma unroll
+    for (int k = 0; k < NCH * CPC; ++k) {
+      x[k].x = 0; x[k].y = 0;
+      if (fast_last) {
+        if (via[k] != 0xffffffffu) {
+          C p = A.p[via[k]], q = B.p[vib[k]];
+          p.y *= sgn_a; q.y *= sgn_b;
+          cmac(x[k], p, q);
+        }
+      } else {
+        const uint32_t c = CPC * ((k / CPC) * DS_GS + lane) + (k % CPC);
+        if (c < last.out_n) x[k] = lane_element<R>(last, A, B, c);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      if constexpr (CPC == 2) { v[k].x = x[2 * k].x; v[k].y = x[2 * k].y; v[k].z = x[2 * k + 1].x; v[k].w = x[2 * k + 1].y; }
+      else { v[k].x = x[k].x; v[k].y = x[k].y; }
+    }
+  };
+  auto dot = [&](const CH (&v)[NCH], const CH* col) -> double {
+    R acc = R(0);
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) {
+      const CH m = col[i * DS_GS + lane];
+      if constexpr (CPC == 2) {
+        acc = fma(v[i].x, m.x, acc); acc = fma(-v[i].y, m.y, acc);
+        acc = fma(v[i].z, m.z, acc); acc = fma(-v[i].w, m.w, acc);
+      } else {
+        acc = fma(v[i].x, m.x, acc); acc = fma(-v[i].y, m.y, acc);
+      }
+    }
+#pragma unroll
+    for (int s = DS_GS / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(gmask, acc, s, DS_GS);
+    return (double)acc;
+  };
+
+  const uint32_t n_tiles = (d.n_items + a.tile - 1) / a.tile;
+  const uint32_t tiles_per = (n_tiles + gridDim.x - 1) / gridDim.x;
+  const uint32_t tile_end = min(n_tiles, (blockIdx.x + 1) * tiles_per);
+  __syncthreads();
+  for (uint32_t tile = blockIdx.x * tiles_per; tile < tile_end; ++tile) {
+    const uint32_t t1 = min(d.n_items, (tile + 1) * a.tile);
+    uint32_t pos = tile * a.tile;
+    while (pos < t1) {
+      // ---- the run of items [pos, end) that share error set er ----
+      const uint32_t er = d.eset[d.first_item + pos];
+      if (tid == 0) s_end = t1;
+      __syncthreads();
+      for (uint32_t i = pos + 1 + tid; i < t1; i += LN_THREADS)
+        if (d.eset[d.first_item + i] != er) { atomicMin(&s_end, i); break; }
+      if (er != loaded) {
+        const CH* src = TREE + (size_t)er * N * COL;
+        for (uint32_t x = tid; x < N * COL; x += LN_THREADS) table[x] = __ldg(src + x);
+        loaded = er;
+      }
+      __syncthreads();
+      const uint32_t end = s_end;
+      const double floor_mass = d.vanish * d.set_mass[er];
+
+      for (uint32_t w0 = pos + wbase; w0 < end; w0 += LN_THREADS) {
+        // ---- phase A: this lane's item, every step but the last ----
+        const uint32_t it = w0 + lane32;
+        const bool live = it < end;
+        const uint32_t item = d.first_item + (live ? it : end - 1);
+        const uint32_t es_row = lane_item_context<R>(a.l, cx, ln_smem, L, item);
+        eset_s[tid] = es_row;
+        __syncwarp();
+        lane_run<R>(cx, 0, e.n_steps - 1, es_row, nullptr, false);
+        uint32_t m = live ? d.mult[item] : 0u;
+        slot0_s[tid] = d.slot_off[item];
+        bad_s[tid] = 0;
+        __syncwarp();
+        // ---- mass of every item of the warp (guards as descent.cuh) ----
+        const uint32_t n_live = min(32u, end - w0);
+        for (uint32_t i0 = 0; i0 < n_live; i0 += 4) {
+          const uint32_t i = min(i0 + grp, n_live - 1);
+          CH v[NCH];
+          vector_of(i, v);
+          const double mass = dot(v, table);
+          if (lane == 0 && i0 + grp < n_live) {
+            mass_s[wbase + i] = mass;
+            if (!(mass >= floor_mass) || !(mass > 0.0)) bad_s[wbase + i] = PTSBE_EIMPOSSIBLE;
+          }
+        }
+        __syncwarp();
+        if (bad_s[tid]) m = 0;
+        // inclusive scan of the multiplicities -> draw index ranges of the warp's items
+        uint32_t incl = m;
+#pragma unroll
+        for (int s = 1; s < 32; s <<= 1) {
+          const uint32_t o = __shfl_up_sync(0xffffffffu, incl, s);
+          if (lane32 >= s) incl += o;
+        }
+        cum_s[tid] = incl;
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        __syncwarp();
+        // ---- phase B: one draw per 8-lane group and round ----
+        for (uint32_t d0 = 0; d0 < total; d0 += 4) {
+          const bool active = d0 + grp < total;
+          const uint32_t dr = active ? d0 + grp : total - 1;
+          uint32_t lo = 0, hi = 31;  // smallest i with cum[i] > dr
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (cum_s[wbase + mid] > dr) hi = mid; else lo = mid + 1;
+          }
+          const uint32_t i = lo;
+          const uint32_t before = i ? cum_s[wbase + i - 1] : 0u;
+          const uint32_t t = dr - before;
+          const uint32_t item_i = d.first_item + w0 + i;
+          CH v[NCH];
+          vector_of(i, v);
+          const double mass = mass_s[wbase + i];
+          const double tol = d.neg_abs - d.neg_rel * mass;
+          const uint32_t rk = d.rank[item_i], es = d.eset_id[item_i];
+          const Philox4 x = philox4x32_10(t, rk, d.stage, es, d.k0, d.k1);
+          const uint64_t x64 = ((uint64_t)x.v[1] << 32) | x.v[0];
+          double p = mass;
+          double r = (double)(x64 >> 11) * (1.0 / 9007199254740992.0) * mass;  // u in [0, 1)
+          uint32_t node = 0, bad = 0;
+          for (uint32_t lvl = 1; lvl <= d.b; ++lvl) {
+            double pl = dot(v, table + (size_t)((1u << (lvl - 1)) + node) * COL);
+            if (pl < tol || p - pl < tol) bad = PTSBE_ENUMERIC;
+            pl = fmin(fmax(pl, 0.0), p);
+            if (r < pl) { node = 2 * node; p = pl; }
+            else { node = 2 * node + 1; r -= pl; p -= pl; }
+          }
+          if (active && lane == 0) {
+            const uint32_t sl = slot0_s[wbase + i] + t;
+            d.slot_index[sl] = node;
+            d.slot_count[sl] = 1;
+            if (bad) bad_s[wbase + i] = bad;
+          }
+        }
+        __syncwarp();
+        // ---- per item: number of raw children, flags, hand-over of long draw lists ----
+        if (live) {
+          const uint32_t bad = bad_s[tid];
+          if (bad) {
+            d.nnz[item] = 0;
+            atomicMin(d.flag, ((unsigned long long)d.eset_id[item] << 16) |
+                                  ((unsigned long long)(d.stage & 0xff) << 8) | bad);
+            atomicAdd(d.flag_count, 1u);
+          } else {
+            d.nnz[item] = m;
+            if (m > LN_DEDUP_SERIAL) a.big_list[atomicAdd(a.big_count, 1u)] = item;
+          }
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      pos = end;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// raw per-draw outcomes -> ordered (outcome, count) pairs
+// ---------------------------------------------------------------------------
+struct DedupArgs {
+  const uint32_t* slot_off;
+  uint32_t* slot_index;
+  uint32_t* slot_count;
+  uint32_t* nnz;
+  const uint32_t* big_list;
+  const uint32_t* big_count;
+  uint32_t first_item, n_items, b;
+};
+
+// one thread per item with 2..LN_DEDUP_SERIAL draws: insertion sort + run-length merge in place
+__global__ void dedup_kernel(const DedupArgs a) {
+  const uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= a.n_items) return;
+  const uint32_t item = a.first_item + it;
+  const uint32_t m = a.nnz[item];
+  if (m < 2 || m > LN_DEDUP_SERIAL) return;
+  uint32_t* idx = a.slot_index + a.slot_off[item];
+  uint32_t* cnt = a.slot_count + a.slot_off[item];
+  for (uint32_t i = 1; i < m; ++i) {
+    const uint32_t x = idx[i];
+    uint32_t j = i;
+    while (j > 0 && idx[j - 1] > x) { idx[j] = idx[j - 1]; --j; }
+    idx[j] = x;
+  }
+  uint32_t out = 0, run = 1;
+  for (uint32_t i = 1; i <= m; ++i) {
+    if (i < m && idx[i] == idx[i - 1]) { ++run; continue; }
+    idx[out] = idx[i - 1];
+    cnt[out] = run;
+    ++out;
+    run = 1;
+  }
+  a.nnz[item] = out;
+}
+
+// one CTA per item with more draws than that: shared-memory counters, ordered emission
+__global__ void __launch_bounds__(256) dedup_big_kernel(const DedupArgs a) {
+  extern __shared__ uint32_t dd_cnt[];
+  __shared__ uint32_t s_scan[256];
+  const uint32_t N = 1u << a.b, n_big = *a.big_count;
+  for (uint32_t k = blockIdx.x; k < n_big; k += gridDim.x) {
+    const uint32_t item = a.big_list[k];
+    const uint32_t m = a.nnz[item];
+    uint32_t* idx = a.slot_index + a.slot_off[item];
+    uint32_t* cnt = a.slot_count + a.slot_off[item];
+    for (uint32_t c = threadIdx.x; c < N; c += 256) dd_cnt[c] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < m; i += 256) atomicAdd(&dd_cnt[idx[i]], 1u);
+    __syncthreads();
+    // thread owns the consecutive outcomes [t * per, t * per + per)
+    const uint32_t per = (N + 255) / 256, c0 = threadIdx.x * per;
+    uint32_t mine = 0;
+    for (uint32_t c = c0; c < min(N, c0 + per); ++c) mine += dd_cnt[c] != 0;
+    s_scan[threadIdx.x] = mine;
+    __syncthreads();
+    for (int s = 1; s < 256; s <<= 1) {
+      const uint32_t o = threadIdx.x >= (unsigned)s ? s_scan[threadIdx.x - s] : 0u;
+      __syncthreads();
+      s_scan[threadIdx.x] += o;
+      __syncthreads();
+    }
+    uint32_t posn = s_scan[threadIdx.x] - mine;
+    for (uint32_t c = c0; c < min(N, c0 + per); ++c)
+      if (dd_cnt[c]) { idx[posn] = c; cnt[posn] = dd_cnt[c]; ++posn; }
+    if (threadIdx.x == 255) a.nnz[item] = s_scan[255];
+    __syncthreads();
+  }
+}
+
+}  // namespace ptsbe
