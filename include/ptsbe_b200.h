@@ -53,9 +53,13 @@ enum { PTSBE_C64 = 0, PTSBE_C128 = 1 };
  *                      (UPV merge, engine.py:284-313, done once on the host per variant)
  *          sel_kind 2: prefix bit          data = pool[pool_off + bit(sel_arg)*size ..)
  *                      (basis vectors of engine.py:395-399)
- * steps  : n_steps x 16 words {a_kind, a_ref, b_kind, b_ref, o_kind, o_ref,
+ * steps  : n_steps x 20 words {a_kind, a_ref, b_kind, b_ref, o_kind, o_ref,
  *                              out_n, k_n, lo_n, hi_n, tab_off, conj,
- *                              a_memo, b_memo, a_prod | b_prod << 16, own_memo}
+ *                              a_memo, b_memo, a_prod | b_prod << 16, own_memo,
+ *                              gemm_off, gemm_m, gemm_n, 0}
+ *          gemm_m > 0: the step also carries its separable form at tables[gemm_off]:
+ *          aOff[gemm_m] bOff[gemm_n] oA[gemm_m] oB[gemm_n] with
+ *          out[oA[a] + oB[b]] = sum_k A[aOff[a] + kA[k]] * B[bOff[b] + kB[k]]
  *          conj bit 0 / 1: operand A / B is read complex-conjugated (its node is the
  *          conjugate twin -- bra copy -- of the node that was actually computed);
  *          bit 2: B is a prefix-bit basis vector e_x contracted over its only label, so the
@@ -80,7 +84,7 @@ typedef struct {
   uint32_t arena_fast_elems;  /* per-item shared-memory arena, in complex elements   */
   uint32_t arena_spill_elems; /* per-item global spill arena (offsets >= arena_fast) */
   uint32_t out_elems;         /* complex elements per output record                  */
-  uint32_t threads_per_item;  /* 32 (warp per item) or a CTA size up to 1024         */
+  uint32_t threads_per_item;  /* 8, 16, 32 (lanes per item) or a CTA size up to 256          */
   uint32_t level;             /* 1-based item level this pass iterates over          */
   uint32_t result_kind;       /* where the finished record lives: 0 arena, 1 leaf, 2+p record of
                                  pass p, 3 projection form (marginal pass only)               */

@@ -29,7 +29,8 @@ import numpy as np
 from .errors import CapacityError, IncompletePathError, NetworkStructureError, ResourceLimitError
 
 SEL_CONST, SEL_KRAUS, SEL_PREFIX = 0, 1, 2
-STEP_WORDS, LEAF_WORDS = 16, 4
+STEP_WORDS, LEAF_WORDS = 20, 4
+GEMM_MIN_MACS = 2048       # steps at least this large also get their separable (GEMM) form
 MEMO_NONE = 0xFFFF         # "operand is not produced by a step of this program"
 MEMO_MIN_STEPS = 48        # class-0 programs at least this long get a variant-0 memo
 LO_TABLE_MAX = 1024          # entries in the per-lane (low) gather table of a step
@@ -384,8 +385,10 @@ def compile_stage(
             threads = min((8, 16, 32), key=per_item)
             fast_cap = peak
         else:
+            # CTA per item.  Large steps run as 4 x 4 register tiles (separable form), so 256
+            # threads cover 4096 outputs per sweep and two CTAs fit the register file of an SM
             threads = 64
-            while threads < 512 and threads * 4 < max_out:
+            while threads < 256 and threads * 4 < max_out:
                 threads *= 2
             fast_cap = min(peak, SMEM_BYTES // elem_bytes)
         where, peak_fast, peak_spill = _place(nodes, mine, rec_off, lambda x: storage_of(x)[0], fast_cap=fast_cap)
@@ -487,6 +490,23 @@ def compile_stage(
                 dyn_words = [len(terms_a)] + [w for t in terms_a for w in t] + \
                             [len(terms_b)] + [w for t in terms_b for w in t]
                 parts.append(np.asarray(dyn_words, dtype=np.int64))
+            # separable form of the same step: every output label survives from exactly one
+            # operand, so out[oA[a] + oB[b]] = sum_k A[aOff[a] + kA[k]] * B[bOff[b] + kB[k]] with
+            # a / b enumerating A's / B's surviving labels -- a GEMM the CTA executor runs with
+            # register tiles (csrc/executor.cuh, tiled_step)
+            gemm_off = gemm_m = gemm_n = 0
+            if not select and float(nd.size) * k_n >= GEMM_MIN_MACS:
+                ost = dict(zip(out_labels, _row_major_strides(odims)))
+                lab_a = [lb for lb in out_labels if lb in sa]
+                lab_b = [lb for lb in out_labels if lb not in sa]
+                if all(lb in sb for lb in lab_b) and not any(lb in sb for lb in lab_a):
+                    a_off = _offsets([dim_of[lb] for lb in lab_a], [sa[lb] for lb in lab_a])
+                    b_off = _offsets([dim_of[lb] for lb in lab_b], [sb[lb] for lb in lab_b])
+                    o_a = _offsets([dim_of[lb] for lb in lab_a], [ost[lb] for lb in lab_a])
+                    o_b = _offsets([dim_of[lb] for lb in lab_b], [ost[lb] for lb in lab_b])
+                    gemm_m, gemm_n = a_off.size, b_off.size
+                    gemm_off = tab_off + int(sum(part.size for part in parts))
+                    parts += [a_off, b_off, o_a, o_b]
             words = np.concatenate(parts).astype(np.uint32)
             tables.append(words)
             # memo words: where the operands' variant-0 values live and which steps produce them
@@ -509,7 +529,8 @@ def compile_stage(
             step_sites.append(deps)
             step_rows.append(
                 [a_kind, a_ref, b_kind, b_ref, o_kind, o_ref, nd.size, k_n, lo_n, hi_n, tab_off, conj_flags,
-                 memo_words[0][0], memo_words[1][0], memo_words[0][1] | (memo_words[1][1] << 16), memo_top]
+                 memo_words[0][0], memo_words[1][0], memo_words[0][1] | (memo_words[1][1] << 16), memo_top,
+                 gemm_off, gemm_m, gemm_n, 0]
             )
             memo_top += (nd.size + 3) & ~3
             tab_off += words.size

@@ -36,6 +36,7 @@ struct Program {
   // lane_fused: additionally its last step alone produces the projection vector
   bool lane_ok = false, lane_fused = false;
   int lane_blocks_per_sm = 0;
+  bool tiled = false;  // most multiply-adds sit in large separable steps: register-tiled kernel variant
 };
 
 }  // namespace ptsbe
@@ -135,6 +136,7 @@ static size_t env_size(const char* name, size_t dflt) {
 }
 
 struct ExecLaunch {
+  uint32_t desc_off, desc_cap = 0;
   unsigned grid, block;
   size_t smem;
   uint32_t item_bytes;
@@ -163,12 +165,18 @@ static ExecLaunch configure_exec(ptsbe_plan* pl, Program& pr, uint32_t n_items) 
   L.smem = ib * L.groups_per_block + 1024;
   const bool memo = !warp && d.memo_elems;
   if (memo) L.smem += memo_smem_bytes(d.n_steps);
+  L.desc_off = 0;
+  if (!warp) {  // staged step descriptors
+    L.desc_off = (uint32_t)L.smem;
+    L.desc_cap = std::min<uint32_t>(d.n_steps, (uint32_t)env_size("PTSBE_DESC_CAP", DESC_CAP));
+    L.smem += (size_t)L.desc_cap * STEP_WORDS * 4;
+  }
   if (L.smem > 227 * 1024)
     throw Failure(PTSBE_ERESOURCE, "stage program needs more shared memory than one SM has");
   void (*kern)(ExecArgs) = gs == 8    ? exec_kernel<R, 8, false>
                            : gs == 16 ? exec_kernel<R, 16, false>
                            : gs == 32 ? exec_kernel<R, 32, false>
-                           : memo     ? exec_kernel<R, 0, true>
+                           : memo     ? (pr.tiled ? exec_kernel<R, 0, true, true> : exec_kernel<R, 0, true>)
                                       : exec_kernel<R, 0, false>;
   if (pr.blocks_per_sm == 0) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -250,6 +258,8 @@ static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelD
   a.mode = mode;
   a.vec_stride = vec_stride;
   a.vec_row = vec_row;
+  a.desc_off = L.desc_off;
+  a.desc_cap = L.desc_cap;
   a.memo = memo ? pr.memo.p : nullptr;
   a.memo_ptr = pr.memo_ptr.as<uint32_t>();
   a.memo_idx = pr.memo_idx.as<uint32_t>();
@@ -258,6 +268,7 @@ static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelD
   if (gs == 8) exec_kernel<R, 8, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
   else if (gs == 16) exec_kernel<R, 16, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
   else if (gs == 32) exec_kernel<R, 32, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  else if (memo && pr.tiled) exec_kernel<R, 0, true, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
   else if (memo) exec_kernel<R, 0, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
   else exec_kernel<R, 0, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
   g_launches++;
@@ -1144,9 +1155,9 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
         if (pr.d.level != p + 1) throw Failure(PTSBE_EINVAL, "program level does not match its pass");
         if (pr.d.result_kind == 3 && (p + 1 != j || j < 2 || pr.d.proj_d < 1))
           throw Failure(PTSBE_EINVAL, "projection form is only valid for the marginal pass of a stage >= 2");
-        if (pr.d.threads_per_item > 1024 ||
+        if (pr.d.threads_per_item > 256 ||
             ((pr.d.threads_per_item & 31) && pr.d.threads_per_item != 8 && pr.d.threads_per_item != 16))
-          throw Failure(PTSBE_EINVAL, "threads_per_item must be 8, 16 or a multiple of 32 up to 1024");
+          throw Failure(PTSBE_EINVAL, "threads_per_item must be 8, 16 or a multiple of 32 up to 256");
         pr.leaves.alloc(std::max<size_t>(16, (size_t)pr.d.n_leaves * LEAF_WORDS * 4), st);
         pr.steps.alloc(std::max<size_t>(16, (size_t)pr.d.n_steps * STEP_WORDS * 4), st);
         pr.tables.alloc(std::max<size_t>(16, (size_t)pr.d.n_table_words * 4), st);
@@ -1160,6 +1171,16 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
           CK(cudaMemcpyAsync(pr.tables.p, pr.d.tables, (size_t)pr.d.n_table_words * 4,
                              cudaMemcpyHostToDevice, st));
         classify_lane(pl.get(), pr);
+        {
+          double big = 0, all = 0;
+          for (uint32_t q = 0; q < pr.d.n_steps && pr.d.steps; ++q) {
+            const uint32_t* stw = pr.d.steps + (size_t)q * STEP_WORDS;
+            const double macs = (double)stw[6] * std::max<uint32_t>(stw[7], 1);
+            all += macs;
+            if (stw[17]) big += macs;
+          }
+          pr.tiled = big >= 1.5e5 && big >= 0.5 * all;
+        }
         if (pr.d.memo_elems) {
           if (!pr.d.memo_ptr || !pr.d.memo_idx || pr.d.n_memo_sites > pl->g || pr.d.n_steps >= 0xFFFF)
             throw Failure(PTSBE_EINVAL, "memo program without its site -> steps table");

@@ -19,7 +19,7 @@
 
 namespace ptsbe {
 
-constexpr int STEP_WORDS = 16;
+constexpr int STEP_WORDS = 20;
 constexpr uint32_t MEMO_NONE = 0xFFFFu;
 constexpr int LEAF_WORDS = 4;
 
@@ -75,7 +75,17 @@ struct ExecArgs {
   const uint32_t* memo_ptr;  // [n_memo_sites + 2] CSR: steps depending on site s; last row: always-run
   const uint32_t* memo_idx;
   uint32_t n_memo_sites;
+  // CTA-per-item programs: step descriptors staged in shared memory (the step loop is a chain
+  // of dependent loads otherwise: descriptor -> table -> operand)
+  uint32_t desc_off;   // byte offset of the staging area from the dynamic shared-memory base
+  uint32_t desc_cap;   // steps it holds (0: none)
 };
+
+constexpr uint32_t DESC_CAP = 192;  // staged step descriptors per CTA (x 80 bytes)
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 
 template <typename R> struct CxT;
 template <> struct CxT<float> { using type = float2; };
@@ -126,14 +136,66 @@ __device__ __forceinline__ void step_fixed_k(const C* __restrict__ A, const C* _
   }
 }
 
+// Separable (GEMM) form of a large step, one CTA: out[oA[a] + oB[b]] = sum_k A[aOff[a] + kA[k]] *
+// B[bOff[b] + kB[k]].  A thread owns a TM x TN register tile, so each loaded operand element
+// feeds TN (or TM) multiply-adds instead of one; neighbouring threads share the tile row (their A
+// loads are shared-memory broadcasts).  The k order of every output is that of the plain form,
+// so the values are bit-identical.
+template <typename C, bool FA, bool FB>
+__device__ __forceinline__ void tiled_step(const C* __restrict__ A, const C* __restrict__ B, C* O,
+                                           const uint32_t* __restrict__ g, uint32_t M, uint32_t N,
+                                           const uint32_t* __restrict__ kA, const uint32_t* __restrict__ kB,
+                                           uint32_t kn, int tid, int nthreads, bool store) {
+  constexpr int TM = 4, TN = 4;
+  const uint32_t *aOff = g, *bOff = g + M, *oA = g + M + N, *oB = g + 2 * M + N;
+  const uint32_t tn = (N + TN - 1) / TN, tm = (M + TM - 1) / TM;
+  for (uint32_t tile = tid; tile < tm * tn; tile += nthreads) {
+    const uint32_t ta = tile / tn, tb = tile - ta * tn;
+    uint32_t ao[TM], bo[TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) ao[i] = __ldg(aOff + min(ta * TM + i, M - 1));
+#pragma unroll
+    for (int j = 0; j < TN; ++j) bo[j] = __ldg(bOff + min(tb * TN + j, N - 1));
+    C acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) { acc[i][j].x = 0; acc[i][j].y = 0; }
+    for (uint32_t k = 0; k < kn; ++k) {
+      const uint32_t ka = __ldg(kA + k), kb = __ldg(kB + k);
+      C av[TM], bv[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) { av[i] = A[ao[i] + ka]; if (FA) av[i].y = -av[i].y; }
+#pragma unroll
+      for (int j = 0; j < TN; ++j) { bv[j] = B[bo[j] + kb]; if (FB) bv[j].y = -bv[j].y; }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) cmac(acc[i][j], av[i], bv[j]);
+    }
+    if (store) {
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        if (ta * TM + i >= M) break;
+        const uint32_t oa = __ldg(oA + ta * TM + i);
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+          if (tb * TN + j < N) O[oa + __ldg(oB + tb * TN + j)] = acc[i][j];
+      }
+    }
+  }
+}
+
 // GS > 0 : sub-warp mapping, GS lanes per item, 32 / GS items per warp, __syncwarp between steps
 // GS == 0: one CTA per item, __syncthreads between steps
 // MEMO    : (GS == 0 only) class-0 program with a variant-0 memo.  UPV leaves every tensor of the
 //           template untouched except at the sites where this error set realised an operator, so
 //           only the steps above those sites are re-executed; everything else is read from the
 //           memo that was computed once per plan.
-template <typename R, int GS, bool MEMO>
-__global__ void exec_kernel(const ExecArgs a) {
+// TILED   : (with MEMO) large steps run in their separable form with register tiles; costs
+//           registers, so only programs dominated by such steps use it
+template <typename R, int GS, bool MEMO, bool TILED = false>
+__global__ void __launch_bounds__(TILED ? 512 : 256, TILED ? 1 : 5) exec_kernel(const ExecArgs a) {
   using C = typename CxT<R>::type;
   constexpr bool WARP = GS > 0;
   constexpr int GSD = GS > 0 ? GS : 1;
@@ -162,6 +224,14 @@ __global__ void exec_kernel(const ExecArgs a) {
   uint16_t* run_list = reinterpret_cast<uint16_t*>(n_run_s + 4);
   const C* memo = reinterpret_cast<const C*>(a.memo);
   const bool build = MEMO && a.mode == EXEC_MEMO_BUILD;
+  uint32_t* desc_s = reinterpret_cast<uint32_t*>(smem_raw + a.desc_off);
+  uint32_t n_staged = 0;
+  if (!WARP && !MEMO && a.desc_cap) {
+    // same step list for every item: staged once
+    n_staged = min(a.n_steps, a.desc_cap);
+    for (uint32_t i = threadIdx.x; i < n_staged * STEP_WORDS; i += blockDim.x) desc_s[i] = __ldg(a.steps + i);
+    __syncthreads();
+  }
 
   auto group_sync = [&]() {
     if (WARP) __syncwarp(); else __syncthreads();
@@ -232,6 +302,16 @@ __global__ void exec_kernel(const ExecArgs a) {
     }
     group_sync();
     const uint32_t n_run = MEMO ? *n_run_s : a.n_steps;
+    if constexpr (MEMO) {
+      // descriptors of the steps this item runs: one round of parallel loads instead of one
+      // dependent load chain per step
+      n_staged = min(n_run, a.desc_cap);
+      for (uint32_t i = threadIdx.x; i < n_staged * STEP_WORDS; i += blockDim.x) {
+        const uint32_t si = i / STEP_WORDS, w = i - si * STEP_WORDS;
+        desc_s[i] = __ldg(a.steps + (size_t)run_list[si] * STEP_WORDS + w);
+      }
+      __syncthreads();
+    }
 
     // measured bit selected by a prefix-projector leaf (slice steps read the bit, not the vector)
     auto leaf_bit = [&](uint32_t ref) -> uint32_t {
@@ -255,10 +335,27 @@ __global__ void exec_kernel(const ExecArgs a) {
     // ---- replay the stored path ----
     for (uint32_t si = 0; si < n_run; ++si) {
       const uint32_t s = MEMO ? run_list[si] : si;
-      const uint4* st4 = reinterpret_cast<const uint4*>(a.steps + (size_t)s * STEP_WORDS);
       // s0 = {a_kind, a_ref, b_kind, b_ref}, s1 = {o_kind, o_ref, out_n, k_n}, s2 = {lo_n, hi_n, tab_off, flags}
-      // s3 = {a_memo, b_memo, a_prod | b_prod << 16, own_memo}
-      const uint4 s0 = __ldg(st4), s1 = __ldg(st4 + 1), s2 = __ldg(st4 + 2);
+      // s3 = {a_memo, b_memo, a_prod | b_prod << 16, own_memo}, s4 = {gemm_off, gemm_m, gemm_n, -}
+      uint4 s0, s1, s2, s3, s4;
+      s3 = make_uint4(0, 0, 0, 0); s4 = s3;
+      if (si < n_staged) {
+        const uint4* st4 = reinterpret_cast<const uint4*>(desc_s + (size_t)si * STEP_WORDS);
+        s0 = st4[0]; s1 = st4[1]; s2 = st4[2];
+        if (MEMO) s3 = st4[3];
+        if (TILED) s4 = st4[4];
+        if (threadIdx.x == 0 && si + 1 < n_staged) {
+          // warm L1 with the next step's gather tables while this step computes
+          const uint32_t* nd = desc_s + (size_t)(si + 1) * STEP_WORDS;
+          prefetch_l1(a.tables + nd[10]);
+          if (TILED && nd[17]) prefetch_l1(a.tables + nd[16]);
+        }
+      } else {
+        const uint4* st4 = reinterpret_cast<const uint4*>(a.steps + (size_t)s * STEP_WORDS);
+        s0 = __ldg(st4); s1 = __ldg(st4 + 1); s2 = __ldg(st4 + 2);
+        if (MEMO) s3 = __ldg(st4 + 3);
+        if (TILED) s4 = __ldg(st4 + 4);
+      }
       const bool slice = (s2.w & 4u) != 0;
       const C* A = resolve(s0.x, s0.y);
       const C* B = slice ? nullptr : resolve(s0.z, s0.w);
@@ -268,7 +365,6 @@ __global__ void exec_kernel(const ExecArgs a) {
       bool copy_memo = false;
       uint32_t own_memo = 0;
       if (MEMO) {
-        const uint4 s3 = __ldg(st4 + 3);
         const uint32_t pa = s3.z & 0xFFFFu, pb = s3.z >> 16;
         if (pa != MEMO_NONE && !((dirty[pa >> 5] >> (pa & 31)) & 1u)) A = memo + s3.x;
         if (pb != MEMO_NONE && !((dirty[pb >> 5] >> (pb & 31)) & 1u)) B = memo + s3.y;
@@ -324,6 +420,15 @@ __global__ void exec_kernel(const ExecArgs a) {
         const C* src = memo + own_memo;
         for (uint32_t c = tid; c < t.out_n; c += gsize)
           if (store) O[(size_t)c * o_stride] = src[c];
+      } else if (TILED && o_stride == 1 && s4.y != 0) {
+        // large step: separable form with register tiles
+        const uint32_t* gt = a.tables + s4.x;
+        switch (t.conj & 3u) {
+          case 0: tiled_step<C, false, false>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
+          case 1: tiled_step<C, true, false>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
+          case 2: tiled_step<C, false, true>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
+          default: tiled_step<C, true, true>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
+        }
       } else if (slice) {
         // B is the basis vector e_x of a measured bit, contracted over its only label:
         // out[c] = A[a0(c) + kA[x]] -- a gather, no multiply-adds

@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(LN_THREADS) lane_descent_kernel(const LaneDesc
       else { v[k].x = x[k].x; v[k].y = x[k].y; }
     }
   };
-  auto dot = [&](const CH (&v)[NCH], const CH* col) -> double {
+  auto dot = [&](const CH (&v)[NCH], const CH* col) -> R {
     R acc = R(0);
 #pragma unroll
     for (int i = 0; i < NCH; ++i) {
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(LN_THREADS) lane_descent_kernel(const LaneDesc
     }
 #pragma unroll
     for (int s = DS_GS / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(gmask, acc, s, DS_GS);
-    return (double)acc;
+    return acc;
   };
 
   const uint32_t n_tiles = (d.n_items + a.tile - 1) / a.tile;
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(LN_THREADS) lane_descent_kernel(const LaneDesc
           const uint32_t i = min(i0 + grp, n_live - 1);
           CH v[NCH];
           vector_of(i, v);
-          const double mass = dot(v, table);
+          const double mass = (double)dot(v, table);
           if (lane == 0 && i0 + grp < n_live) {
             mass_s[wbase + i] = mass;
             if (!(mass >= floor_mass) || !(mass > 0.0)) bad_s[wbase + i] = PTSBE_EIMPOSSIBLE;
@@ -520,18 +520,22 @@ __global__ void __launch_bounds__(LN_THREADS) lane_descent_kernel(const LaneDesc
           const uint32_t item_i = d.first_item + w0 + i;
           CH v[NCH];
           vector_of(i, v);
-          const double mass = mass_s[wbase + i];
-          const double tol = d.neg_abs - d.neg_rel * mass;
+          // decisions in the arithmetic type of the path (float for complex64: the conditional
+          // marginals carry 1e-5 relative error anyway; double for complex128, bit-compatible
+          // with the oracle's float64 inverse-CDF walk)
+          const R mass = (R)mass_s[wbase + i];
+          const R tol = (R)(d.neg_abs - d.neg_rel * (double)mass);
           const uint32_t rk = d.rank[item_i], es = d.eset_id[item_i];
           const Philox4 x = philox4x32_10(t, rk, d.stage, es, d.k0, d.k1);
           const uint64_t x64 = ((uint64_t)x.v[1] << 32) | x.v[0];
-          double p = mass;
-          double r = (double)(x64 >> 11) * (1.0 / 9007199254740992.0) * mass;  // u in [0, 1)
+          R p = mass;
+          R r = (R)((double)(x64 >> 11) * (1.0 / 9007199254740992.0)) * mass;  // u in [0, 1)
+          if (sizeof(R) == 4 && !(r < mass)) r = nextafterf((float)mass, 0.0f);  // u rounded up to 1.0f
           uint32_t node = 0, bad = 0;
           for (uint32_t lvl = 1; lvl <= d.b; ++lvl) {
-            double pl = dot(v, table + (size_t)((1u << (lvl - 1)) + node) * COL);
+            R pl = dot(v, table + (size_t)((1u << (lvl - 1)) + node) * COL);
             if (pl < tol || p - pl < tol) bad = PTSBE_ENUMERIC;
-            pl = fmin(fmax(pl, 0.0), p);
+            pl = fmin(fmax(pl, R(0)), p);
             if (r < pl) { node = 2 * node; p = pl; }
             else { node = 2 * node + 1; r -= pl; p -= pl; }
           }
