@@ -434,7 +434,23 @@ def main():
             n_items = sum(int(s.stage_events[j]) for s in stats)
             launches_j = sum(int(s.marg_launches[j]) for s in stats)
             d_items = sum(int(s.descent_items[j]) for s in stats)
-            if pr.proj_d and d_items:
+            if pr.proj_d and d_items and marg[j] == 0.0:
+                # fused lane_descent_kernel (csrc/lane.cuh): per-item steps (thread per item) + per-qubit
+                # descent (8 lanes per draw); v never leaves the SM.  HBM traffic of one work item: its
+                # list entry (eset, parent, mult, slot_off, rank, id, prefix words), one (index, count)
+                # pair per draw, nnz; plus, amortised, every record of an earlier pass and every tree
+                # column once per launch.
+                b_j = sizes[j]
+                progs_j = pipe.programs_of(j + 1)
+                shots_j = total_shots_local * args.steps
+                rec_bytes = sum(float(sum(int(s.stage_events[p]) for s in stats)) * progs_j[p].out_elems * elem
+                                for p in range(1, j))  # pass 0 records: read through the tree only
+                tree_bytes = float(sets * args.steps) * pr.proj_d * elem * (1 << b_j)
+                per_item = 24 + 8 * words + 4 + 8.0 * shots_j / max(d_items, 1) + (rec_bytes + tree_bytes) / max(d_items, 1)
+                flops_item = 8.0 * pr.flops * (1.0 + shots_j / max(d_items, 1)) + 4.0 * pr.proj_d * (b_j + 1) * shots_j / max(d_items, 1)
+                cands.append((desc[j], f"lane_descent_kernel (per-item steps + per-qubit descent fused, D={pr.proj_d}, b={b_j}), stage {j + 1}",
+                              d_items, launches_j, per_item, flops_item))
+            elif pr.proj_d and d_items:
                 # per-item steps, vector written as one row per item
                 cands.append((marg[j], f"exec_kernel (per-item steps -> v[{pr.proj_d}]), stage {j + 1}", n_items, launches_j,
                               pr.ext_read_elems * elem + 8 + 8 * words + pr.proj_d * elem, 8.0 * pr.flops))

@@ -481,22 +481,29 @@ __global__ void __launch_bounds__(LN_THREADS) lane_descent_kernel(const LaneDesc
         slot0_s[tid] = d.slot_off[item];
         bad_s[tid] = 0;
         __syncwarp();
-        // ---- mass of every item of the warp (guards as descent.cuh) ----
-        const uint32_t n_live = min(32u, end - w0);
-        for (uint32_t i0 = 0; i0 < n_live; i0 += 4) {
-          const uint32_t i = min(i0 + grp, n_live - 1);
-          CH v[NCH];
-          vector_of(i, v);
-          const double mass = (double)dot(v, table);
-          if (lane == 0 && i0 + grp < n_live) {
-            mass_s[wbase + i] = mass;
-            if (!(mass >= floor_mass) || !(mass > 0.0)) bad_s[wbase + i] = PTSBE_EIMPOSSIBLE;
+        // one descent from v: decisions in the arithmetic type of the path (float for complex64: the
+        // conditional marginals carry 1e-5 relative error anyway; double for complex128, compatible
+        // with the oracle's float64 inverse-CDF walk)
+        auto descend = [&](const CH (&v)[NCH], R mass, uint32_t t, uint32_t i, uint32_t& bad) -> uint32_t {
+          const R tol = (R)(d.neg_abs - d.neg_rel * (double)mass);
+          const uint32_t item_i = d.first_item + w0 + i;
+          const Philox4 x = philox4x32_10(t, __ldg(d.rank + item_i), d.stage, __ldg(d.eset_id + item_i), d.k0, d.k1);
+          const uint64_t x64 = ((uint64_t)x.v[1] << 32) | x.v[0];
+          R p = mass;
+          R r = (R)((double)(x64 >> 11) * (1.0 / 9007199254740992.0)) * mass;  // u in [0, 1)
+          if (sizeof(R) == 4 && !(r < mass)) r = nextafterf((float)mass, 0.0f);  // u rounded up to 1.0f
+          uint32_t node = 0;
+          for (uint32_t lvl = 1; lvl <= d.b; ++lvl) {
+            R pl = dot(v, table + (size_t)((1u << (lvl - 1)) + node) * COL);
+            if (pl < tol || p - pl < tol) bad = PTSBE_ENUMERIC;
+            pl = fmin(fmax(pl, R(0)), p);
+            if (r < pl) { node = 2 * node; p = pl; }
+            else { node = 2 * node + 1; r -= pl; p -= pl; }
           }
-        }
-        __syncwarp();
-        if (bad_s[tid]) m = 0;
-        // inclusive scan of the multiplicities -> draw index ranges of the warp's items
-        uint32_t incl = m;
+          return node;
+        };
+        // draws 1.. of the items that carry more than one shot: inclusive scan of (m - 1)
+        uint32_t incl = m > 1 ? m - 1 : 0u;
 #pragma unroll
         for (int s = 1; s < 32; s <<= 1) {
           const uint32_t o = __shfl_up_sync(0xffffffffu, incl, s);
@@ -505,46 +512,55 @@ __global__ void __launch_bounds__(LN_THREADS) lane_descent_kernel(const LaneDesc
         cum_s[tid] = incl;
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
         __syncwarp();
-        // ---- phase B: one draw per 8-lane group and round ----
-        for (uint32_t d0 = 0; d0 < total; d0 += 4) {
-          const bool active = d0 + grp < total;
-          const uint32_t dr = active ? d0 + grp : total - 1;
-          uint32_t lo = 0, hi = 31;  // smallest i with cum[i] > dr
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (cum_s[wbase + mid] > dr) hi = mid; else lo = mid + 1;
+        // ---- phase B: one (item, draw) per 8-lane group and round.  Rounds [0, item_rounds): the
+        // warp's items in order -- v, mass (guards as descent.cuh) and draw 0; later rounds: the
+        // remaining draws of multi-shot items, v recomputed, mass from shared memory ----
+        const uint32_t n_live = min(32u, end - w0);
+        const uint32_t item_rounds = (n_live + 3) / 4, rounds = item_rounds + (total + 3) / 4;
+        for (uint32_t rd = 0; rd < rounds; ++rd) {
+          const bool first = rd < item_rounds;  // warp-uniform
+          bool active;
+          uint32_t i, t;
+          if (first) {
+            active = rd * 4 + grp < n_live;
+            i = active ? rd * 4 + grp : n_live - 1;
+            t = 0;
+          } else {
+            const uint32_t d0 = (rd - item_rounds) * 4;
+            active = d0 + grp < total;
+            const uint32_t dr = active ? d0 + grp : total - 1;
+            uint32_t lo = 0, hi = 31;  // smallest i with cum[i] > dr
+            while (lo < hi) {
+              const uint32_t mid = (lo + hi) >> 1;
+              if (cum_s[wbase + mid] > dr) hi = mid; else lo = mid + 1;
+            }
+            i = lo;
+            t = 1 + dr - (i ? cum_s[wbase + i - 1] : 0u);
           }
-          const uint32_t i = lo;
-          const uint32_t before = i ? cum_s[wbase + i - 1] : 0u;
-          const uint32_t t = dr - before;
-          const uint32_t item_i = d.first_item + w0 + i;
           CH v[NCH];
           vector_of(i, v);
-          // decisions in the arithmetic type of the path (float for complex64: the conditional
-          // marginals carry 1e-5 relative error anyway; double for complex128, bit-compatible
-          // with the oracle's float64 inverse-CDF walk)
-          const R mass = (R)mass_s[wbase + i];
-          const R tol = (R)(d.neg_abs - d.neg_rel * (double)mass);
-          const uint32_t rk = d.rank[item_i], es = d.eset_id[item_i];
-          const Philox4 x = philox4x32_10(t, rk, d.stage, es, d.k0, d.k1);
-          const uint64_t x64 = ((uint64_t)x.v[1] << 32) | x.v[0];
-          R p = mass;
-          R r = (R)((double)(x64 >> 11) * (1.0 / 9007199254740992.0)) * mass;  // u in [0, 1)
-          if (sizeof(R) == 4 && !(r < mass)) r = nextafterf((float)mass, 0.0f);  // u rounded up to 1.0f
-          uint32_t node = 0, bad = 0;
-          for (uint32_t lvl = 1; lvl <= d.b; ++lvl) {
-            R pl = dot(v, table + (size_t)((1u << (lvl - 1)) + node) * COL);
-            if (pl < tol || p - pl < tol) bad = PTSBE_ENUMERIC;
-            pl = fmin(fmax(pl, R(0)), p);
-            if (r < pl) { node = 2 * node; p = pl; }
-            else { node = 2 * node + 1; r -= pl; p -= pl; }
+          uint32_t bad = 0;
+          R mass;
+          if (first) {
+            mass = dot(v, table);
+            if (!((double)mass >= floor_mass) || !(mass > R(0))) bad = PTSBE_EIMPOSSIBLE;
+          } else {
+            mass = (R)mass_s[wbase + i];
+            bad = bad_s[wbase + i] == PTSBE_EIMPOSSIBLE ? PTSBE_EIMPOSSIBLE : 0u;
           }
+          uint32_t node = 0;
+          if (!bad) node = descend(v, mass, t, i, bad);  // group-uniform branch
           if (active && lane == 0) {
-            const uint32_t sl = slot0_s[wbase + i] + t;
-            d.slot_index[sl] = node;
-            d.slot_count[sl] = 1;
-            if (bad) bad_s[wbase + i] = bad;
+            if (first) mass_s[wbase + i] = (double)mass;
+            if (bad) {
+              bad_s[wbase + i] = bad;
+            } else {
+              const uint32_t sl = slot0_s[wbase + i] + t;
+              d.slot_index[sl] = node;
+              d.slot_count[sl] = 1;
+            }
           }
+          if (first && rd + 1 == item_rounds) __syncwarp();  // masses and flags visible to the later rounds
         }
         __syncwarp();
         // ---- per item: number of raw children, flags, hand-over of long draw lists ----
