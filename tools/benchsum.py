@@ -8,3 +8,4 @@ for k, v in d["kernel_ms_per_step"].items():
     print("  %-14s %s" % (k, [round(x, 2) for x in v] if isinstance(v, list) else round(v, 2)))
 r = d["roofline"]
 print("  roofline:", r["kernel"], "frac %.4f" % r["frac"], "fma frac %.4f" % r["fma"]["frac"], "share %.2f" % r["share_of_step"])
+print("  e2e:", {k: v for k, v in e2e.items() if k not in ("timing", "unit")})
