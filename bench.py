@@ -66,6 +66,15 @@ def build_workload(name: str, args):
     elif name == "cfg4":
         c, sizes = workloads.qaoa(50, 2, p=1e-3, seed=4)
         dflt = dict(sets=10_000, shots=10_000, dtype="complex128", label="cfg4: 50-qubit QAOA p=2, 3-regular")
+    elif name == "cfg3s":
+        # the full-size cfg3 / cfg4 networks exceed the 2^26-entry intermediate ceiling (the reference's own
+        # execute_path raises ResourceLimitError for them too); these are the largest twins that plan
+        c, sizes = workloads.surface_code(3, 1, p=1e-3)
+        dflt = dict(sets=100_000, shots=1, dtype="complex64", label="cfg3 twin: surface code d=3, 1 round, p=1e-3 (17 qubits)")
+    elif name == "cfg4s":
+        c, _ = workloads.qaoa(12, 2, p=1e-3, seed=4)
+        sizes = (5, 5, 2)
+        dflt = dict(sets=2_000, shots=10_000, dtype="complex128", label="cfg4 twin: 12-qubit QAOA p=2, 3-regular")
     elif name == "cfg5":
         c, sizes = workloads.random40(40, 400, seed=5)
         dflt = dict(sets=100_000, shots=100, dtype="complex64", label="cfg5: random_circuit(40, 400)")
@@ -161,7 +170,7 @@ def cpu_sample_size(name: str):
     """(error sets, shots per set) of the bounded CPU sample: about 10-30 s of
     host work for the whole pool."""
     return {"cfg1": (64, 1000), "cfg2": (None, 24), "cfg3": (None, 1), "cfg4": (None, 8),
-            "cfg5": (None, 20)}[name]
+            "cfg5": (None, 20), "cfg3s": (64, 1), "cfg4s": (None, 50)}[name]
 
 
 # --------------------------------------------------------------------------
@@ -264,7 +273,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfg3s", "cfg4s"])
     ap.add_argument("--sets", type=int, default=0, help="error sets PER GPU")
     ap.add_argument("--shots", type=int, default=0, help="shots per error set")
     ap.add_argument("--plan", default="", help="comma-separated batch sizes")

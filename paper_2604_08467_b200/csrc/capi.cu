@@ -476,7 +476,7 @@ static void launch_tree_build(ptsbe_plan* pl, const Program& pr, const void* rec
   t.b = b;
   t.dpad = dpad;
   t.n_sets = n_sets;
-  const dim3 grid(cdiv(((uint64_t)dpad) << b, 256), n_sets);
+  const dim3 grid(n_sets, cdiv(((uint64_t)dpad) << b, 256));  // error sets on x: up to 2^31 - 1
   if (pl->dtype == PTSBE_C64) tree_build_kernel<float><<<grid, 256, 0, pl->stream>>>(t);
   else tree_build_kernel<double><<<grid, 256, 0, pl->stream>>>(t);
   g_launches++;

@@ -51,8 +51,8 @@ template <typename R>
 __global__ void tree_build_kernel(const TreeArgs a) {
   using C = typename CxT<R>::type;
   const uint32_t N = 1u << a.b;
-  const uint32_t e = blockIdx.y;
-  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t e = blockIdx.x;
+  const uint32_t x = blockIdx.y * blockDim.x + threadIdx.x;
   if (x >= N * a.dpad) return;
   const uint32_t idx = x / a.dpad, d = x % a.dpad;
   C* out = reinterpret_cast<C*>(a.tree) + ((size_t)e * N + idx) * a.dpad + d;

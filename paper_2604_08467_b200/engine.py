@@ -461,8 +461,43 @@ def _schmidt_split(data: np.ndarray, tol: float = 1e-12):
     return a, b, rank
 
 
+def _light_cone(cnet: CircuitNetwork, tables: "VariantTables", n_kets: int, first_traced: int):
+    """Backward sweep over the gate sites.  Returns (dropped sites, {traced qubit: label at which
+    its bra leg joins its ket leg}).  A qubit is active once something kept acts on it; measured and
+    projected qubits (q < first_traced) are active from the end of the circuit."""
+    ops = cnet.net.operands
+    end = {q: lb for q, lb in enumerate(cnet.final_labels)}      # current end label of every wire
+    owner = {lb: q for q, lb in end.items()}
+    active = set(range(first_traced))
+    joins = {}
+    dropped = set()
+    for site in reversed(range(tables.n_sites)):
+        t = ops[n_kets + site]
+        k = len(t.labels) // 2
+        outs, ins = t.labels[:k], t.labels[k:]
+        qs = [owner[lb] for lb in outs]
+        side = 1 << k
+        data = tables.data[site].reshape(-1, side, side)
+        unitary = all(np.allclose(v.conj().T @ v, np.eye(side), atol=1e-12) for v in data)
+        if unitary and not any(q in active for q in qs):
+            dropped.add(site)
+        else:
+            for q, lb in zip(qs, outs):
+                if q not in active:
+                    active.add(q)
+                    joins[q] = lb        # traced wire enters the light cone here
+        for q, lo, li in zip(qs, outs, ins):
+            del owner[lo]
+            owner[li] = q
+            end[q] = li
+    for q in range(first_traced, cnet.n):
+        if q not in active:
+            joins[q] = end[q]            # nothing kept on this wire: <0|0> at the ket label
+    return dropped, joins
+
+
 def stage_operands(cnet: CircuitNetwork, plan: BatchPlan, j: int, tables: VariantTables,
-                   split: bool = False):
+                   split: bool = False, lightcone: bool = True):
     """Static operand table of the stage-j sandwich.  With split=False the
     operand order is that of `marginal_network` (reference engine.py:392-406).
     With split=True every two-qubit site whose variants all have operator-
@@ -474,13 +509,28 @@ def stage_operands(cnet: CircuitNetwork, plan: BatchPlan, j: int, tables: Varian
     (bra / ket) copy of operand k, -1 for the copy tensors."""
     bra, fixed, opened = _stage_layout(cnet, plan, j)
     n_kets = len(cnet.net.operands) - tables.n_sites
+    dropped: set = set()
+    if lightcone and tables.n_sites:
+        # Unitary light cone: a site that acts only on traced qubits, after everything that reaches a
+        # measured qubit, meets its own conjugate in the sandwich and (P U)^dagger (P U) = 1 for every
+        # realised operator P of a unitary channel -- in every error set, so the structure stays
+        # error-independent.  Both copies are dropped and the bra leg joins the ket leg at the
+        # boundary of the light cone instead of at the end of the circuit.
+        first_traced = plan.stage_qubits(j).stop
+        dropped, joins = _light_cone(cnet, tables, n_kets, first_traced)
+        nxt = 1 + max(list(bra.values()) + [o[3] for o in opened] + [lb for t in cnet.net.operands for lb in t.labels])
+        for q in range(first_traced, cnet.n):  # undo the identification at the final labels ...
+            bra[cnet.final_labels[q]] = nxt
+            nxt += 1
+        for lb in joins.values():              # ... and join where the wire enters the light cone
+            bra[lb] = lb
     fresh = 1 + max([lb for t in cnet.net.operands for lb in t.labels] + list(bra.values())
                     + [o[3] for o in opened])
     halves = {}
     if split:
         for site in range(tables.n_sites):
             t = cnet.net.operands[n_kets + site]
-            if len(t.labels) == 4:
+            if len(t.labels) == 4 and site not in dropped:
                 res = _schmidt_split(tables.data[site])
                 if res is not None:
                     halves[site] = res + (fresh, fresh + 1)
@@ -491,6 +541,8 @@ def stage_operands(cnet: CircuitNetwork, plan: BatchPlan, j: int, tables: Varian
             labels = tuple(bra.get(lb, lb) for lb in t.labels) if conj else t.labels
             dims = tuple(ix.dim for ix in t.indices)
             site = slot - n_kets
+            if site in dropped:
+                continue
             if site >= 0 and site in halves:
                 a, b, r, k_ket, k_bra = halves[site]
                 kind = SEL_KRAUS if a.shape[0] > 1 else SEL_CONST
