@@ -76,7 +76,8 @@ def build_workload(name: str, args):
         sizes = (5, 5, 2)
         dflt = dict(sets=2_000, shots=10_000, dtype="complex128", label="cfg4 twin: 12-qubit QAOA p=2, 3-regular")
     elif name == "cfg5":
-        c, sizes = workloads.random40(40, 400, seed=5)
+        c, _ = workloads.random40(40, 400, seed=5)
+        sizes = (10, 6, 6, 6, 6, 6)  # best of a sweep; 6-qubit stages keep the descent tree in shared memory
         dflt = dict(sets=100_000, shots=100, dtype="complex64", label="cfg5: random_circuit(40, 400)")
     else:
         raise SystemExit(f"unknown workload {name!r}")

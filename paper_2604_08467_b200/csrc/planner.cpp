@@ -38,7 +38,11 @@ struct Rng {  // splitmix64
   double uniform() { return ((next() >> 11) + 0.5) * (1.0 / 9007199254740992.0); }
 };
 
-static double kStepOverheadMacs = 20.0;  // PTSBE_STEP_OVERHEAD overrides (experiments)
+// Cost of issuing one step for one work item, in multiply-add equivalents.  Measured on B200
+// (cfg5 stage-3/4 per-item programs, CTA per item): time per item ~ 1.1 ns x steps + 0.0015 ns x MACs,
+// i.e. a barrier-separated step costs as much as ~700 MACs; lane-per-item programs pay ~30.
+// 400 makes the search prefer few-step (cut / projection) forms for the per-item pass.
+static double kStepOverheadMacs = 400.0;  // PTSBE_STEP_OVERHEAD overrides (experiments)
 
 struct Cand {
   double key, tie;

@@ -310,7 +310,7 @@ def plan_stage(op_labels, op_dims, op_class, op_is_prefix, open_labels, class_we
 
 
 MAX_OPTIMAL_OPERANDS = 14
-kStepOverheadMacs = 20.0  # same constant as csrc/planner.cpp
+kStepOverheadMacs = 400.0  # same constant as csrc/planner.cpp
 NEAR_SIDE_DESCENTS = 8    # multiplier on hypersamples for the near-side search
 
 
