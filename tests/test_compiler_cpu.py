@@ -168,3 +168,70 @@ def test_variant0_memo_skips_clean_steps_and_keeps_values():
                 if r == 0:
                     assert stats["executed"] <= 0.25 * stats["total"]
     assert memo_programs >= 1
+
+
+def test_unitary_light_cone_drops_sites_and_keeps_marginals(golden_cases):
+    """Sites that act only on traced qubits behind the measured light cone cancel
+    against their conjugates (Pauli channels: every realised operator is
+    unitary).  Early stages of a unitary-noise circuit lose most of their
+    operands; the emulated marginals still equal the reference goldens, and a
+    non-unitary channel (amplitude damping) blocks the cancellation."""
+    from paper_2604_08467_b200 import workloads
+    from paper_2604_08467_b200.engine import _light_cone, stage_operands
+
+    case = golden_cases["random10x40"]
+    c, sizes, es = case_objects(case)
+    tpl = CircuitNetwork.from_circuit(c)
+    tables = VariantTables.from_errorsets(tpl, es)
+    plan = BatchPlan(sizes)
+    n_kets = len(tpl.net.operands) - tables.n_sites
+    dropped = [len(_light_cone(tpl, tables, n_kets, plan.stage_qubits(j).stop)[0]) for j in range(1, plan.f + 1)]
+    assert dropped[0] > 0 and dropped[-1] == 0 and dropped == sorted(dropped, reverse=True)
+    full, _, _ = stage_operands(tpl, plan, 1, tables, split=True, lightcone=False)
+    cone, _, _ = stage_operands(tpl, plan, 1, tables, split=True, lightcone=True)
+    assert len(cone) < len(full)
+    # values: the golden-marginal test above runs with the light cone on (DevicePipeline default);
+    # here: amplitude damping sites are never dropped
+    ch, _ = workloads.hea(6, 2, gamma=0.05, p=0.0, seed=1)
+    tpl2 = CircuitNetwork.from_circuit(ch)
+    tab2 = VariantTables.from_channels(tpl2)
+    nk2 = len(tpl2.net.operands) - tab2.n_sites
+    gone, _ = _light_cone(tpl2, tab2, nk2, 2)
+    kinds = {type(ch.gates[s].noise).__name__ + ":" + ch.gates[s].noise.kind for s in gone}
+    assert all("amplitude" not in k for k in kinds)
+
+
+def test_separable_form_tables_match_the_gather_tables():
+    """Large steps carry a GEMM form (aOff, bOff, oA, oB); it must address the
+    same operand and output elements as the lo/hi gather tables."""
+    from paper_2604_08467_b200 import workloads
+
+    c, _ = workloads.hea(14, 4, gamma=0.02, p=0.02, seed=7)
+    tpl = CircuitNetwork.from_circuit(c)
+    tables = VariantTables.from_channels(tpl)
+    ctx = SamplerContext(hypersamples=8, planner_seed=3, dtype="complex128")
+    pipe = DevicePipeline(tpl, BatchPlan((7, 7)), tables, ctx, shots_per_set=1000.0, upload=False)
+    checked = 0
+    for pr in pipe.compiled.programs:
+        t = pr.tables.astype(np.int64)
+        for st in pr.steps:
+            out_n, kn, lo_n, hi_n, tab = (int(st[k]) for k in (6, 7, 8, 9, 10))
+            g_off, m, n = int(st[16]), int(st[17]), int(st[18])
+            if not m:
+                continue
+            assert m * n == out_n
+            loA, loB = t[tab: tab + lo_n], t[tab + lo_n: tab + 2 * lo_n]
+            hiA = t[tab + 2 * lo_n: tab + 2 * lo_n + hi_n]
+            hiB = t[tab + 2 * lo_n + hi_n: tab + 2 * lo_n + 2 * hi_n]
+            a_plain = (hiA[:, None] + loA[None, :]).reshape(-1)
+            b_plain = (hiB[:, None] + loB[None, :]).reshape(-1)
+            aOff, bOff = t[g_off: g_off + m], t[g_off + m: g_off + m + n]
+            oA, oB = t[g_off + m + n: g_off + 2 * m + n], t[g_off + 2 * m + n: g_off + 2 * m + 2 * n]
+            out = (oA[:, None] + oB[None, :]).reshape(-1)
+            assert sorted(out.tolist()) == list(range(out_n))
+            a_gemm = np.repeat(aOff, n)
+            b_gemm = np.tile(bOff, m)
+            np.testing.assert_array_equal(a_plain[out], a_gemm)
+            np.testing.assert_array_equal(b_plain[out], b_gemm)
+            checked += 1
+    assert checked >= 1
