@@ -37,6 +37,10 @@ struct Program {
   bool lane_ok = false, lane_fused = false;
   int lane_blocks_per_sm = 0;
   bool tiled = false;  // most multiply-adds sit in large separable steps: register-tiled kernel variant
+  // projection vector is x (x) conj(x): Hermitian-packed tree columns (lane.cuh HERM)
+  bool herm = false;
+  std::vector<uint32_t> herm_map_host;
+  DevBuf herm_map;
 };
 
 }  // namespace ptsbe
@@ -309,6 +313,38 @@ static void classify_lane(const ptsbe_plan* pl, Program& pr) {
   const uint32_t* last = d.steps + (size_t)(d.n_steps - 1) * STEP_WORDS;
   pr.lane_fused = d.proj_d && d.result_kind == 3 && inner_to_arena && last[4] == 1 && last[5] == 0 &&
                   last[6] == d.proj_d;
+  // Hermitian form: last step = outer product of one arena tensor with its own conjugate
+  pr.herm = false;
+  pr.herm_map_host.clear();
+  const uint32_t D = d.proj_d, flags = last[11];
+  if (pr.lane_fused && D <= 4096 && last[7] == 1 && last[9] == 1 && !(flags & (4u | 8u)) &&
+      last[0] == 0 && last[2] == 0 && last[1] == last[3] && ((flags & 3u) == 1u || (flags & 3u) == 2u) && d.tables) {
+    const uint32_t* t = d.tables + last[10];
+    const uint32_t lo_n = last[8];
+    const uint32_t *loA = t, *loB = t + lo_n, *kA = t + 2 * lo_n + 2, *kB = kA + 1;
+    std::vector<std::pair<uint32_t, uint32_t>> ab(D);
+    bool ok = lo_n == D;
+    for (uint32_t c = 0; ok && c < D; ++c) ab[c] = {loA[c] + kA[0], loB[c] + kB[0]};
+    std::vector<uint32_t> partner(D, 0xffffffffu);
+    for (uint32_t c = 0; ok && c < D; ++c) {
+      for (uint32_t c2 = 0; c2 < D; ++c2)
+        if (ab[c2].first == ab[c].second && ab[c2].second == ab[c].first) { partner[c] = c2; break; }
+      if (partner[c] == 0xffffffffu) ok = false;
+    }
+    if (ok) {
+      // slots: diagonal elements first come as they appear, pairs as (Re, Im) of the smaller index
+      for (uint32_t c = 0; c < D; ++c) {
+        const uint32_t c2 = partner[c];
+        if (c2 == c) pr.herm_map_host.push_back(c | (c << 12) | (0u << 24));
+        else if (c < c2) {
+          pr.herm_map_host.push_back(c | (c2 << 12) | (0u << 24));
+          pr.herm_map_host.push_back(c | (c2 << 12) | (1u << 24));
+        }
+      }
+      pr.herm = pr.herm_map_host.size() == D;
+      if (!pr.herm) pr.herm_map_host.clear();
+    }
+  }
 }
 
 template <typename R>
@@ -417,7 +453,7 @@ static void launch_descent(ptsbe_plan* pl, const DescentArgs& a, const DescentSh
   }
 }
 
-template <typename R, int NCH>
+template <typename R, int NCH, bool HERM>
 static void launch_lane_descent_t(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a) {
   using C = typename CxT<R>::type;
   using CH = typename DsChunk<R>::type;
@@ -427,9 +463,9 @@ static void launch_lane_descent_t(ptsbe_plan* pl, Program& pr, LaneDescentArgs& 
                       (((size_t)DS_GS * NCH * sizeof(CH)) << a.d.b);
   if (smem > 200 * 1024) throw Failure(PTSBE_ERESOURCE, "fused descent needs more shared memory than one SM has");
   if (pr.lane_blocks_per_sm == 0) {
-    CK(cudaFuncSetAttribute(lane_descent_kernel<R, NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(lane_descent_kernel<R, NCH, HERM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lane_descent_kernel<R, NCH>, LN_THREADS, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lane_descent_kernel<R, NCH, HERM>, LN_THREADS, smem));
     pr.lane_blocks_per_sm = std::max(nb, 1);
   }
   // tiles: long enough to amortise the CTA barriers around an error-set run, short enough that
@@ -440,7 +476,7 @@ static void launch_lane_descent_t(ptsbe_plan* pl, Program& pr, LaneDescentArgs& 
   a.tile = (uint32_t)tile;
   const uint64_t tiles = cdiv(a.d.n_items, tile);
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, ctas));
-  lane_descent_kernel<R, NCH><<<grid, LN_THREADS, smem, pl->stream>>>(a);
+  lane_descent_kernel<R, NCH, HERM><<<grid, LN_THREADS, smem, pl->stream>>>(a);
   g_launches++;
   CK(cudaGetLastError());
 }
@@ -456,13 +492,33 @@ static bool lane_descent_fits(const ptsbe_plan* pl, const Program& pr, const Des
 static void launch_lane_descent(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a, const DescentShape& sh) {
   if (a.d.n_items == 0) return;
   const bool f32 = pl->dtype == PTSBE_C64;
+  if (a.herm_map) {
+    switch (sh.nch) {
+      case 1: f32 ? launch_lane_descent_t<float, 1, true>(pl, pr, a) : launch_lane_descent_t<double, 1, true>(pl, pr, a); break;
+      case 2: f32 ? launch_lane_descent_t<float, 2, true>(pl, pr, a) : launch_lane_descent_t<double, 2, true>(pl, pr, a); break;
+      case 4: f32 ? launch_lane_descent_t<float, 4, true>(pl, pr, a) : launch_lane_descent_t<double, 4, true>(pl, pr, a); break;
+      case 8: f32 ? launch_lane_descent_t<float, 8, true>(pl, pr, a) : launch_lane_descent_t<double, 8, true>(pl, pr, a); break;
+      default: throw Failure(PTSBE_EINVAL, "descent sampler: unsupported vector length");
+    }
+    return;
+  }
   switch (sh.nch) {
-    case 1: f32 ? launch_lane_descent_t<float, 1>(pl, pr, a) : launch_lane_descent_t<double, 1>(pl, pr, a); break;
-    case 2: f32 ? launch_lane_descent_t<float, 2>(pl, pr, a) : launch_lane_descent_t<double, 2>(pl, pr, a); break;
-    case 4: f32 ? launch_lane_descent_t<float, 4>(pl, pr, a) : launch_lane_descent_t<double, 4>(pl, pr, a); break;
-    case 8: f32 ? launch_lane_descent_t<float, 8>(pl, pr, a) : launch_lane_descent_t<double, 8>(pl, pr, a); break;
+    case 1: f32 ? launch_lane_descent_t<float, 1, false>(pl, pr, a) : launch_lane_descent_t<double, 1, false>(pl, pr, a); break;
+    case 2: f32 ? launch_lane_descent_t<float, 2, false>(pl, pr, a) : launch_lane_descent_t<double, 2, false>(pl, pr, a); break;
+    case 4: f32 ? launch_lane_descent_t<float, 4, false>(pl, pr, a) : launch_lane_descent_t<double, 4, false>(pl, pr, a); break;
+    case 8: f32 ? launch_lane_descent_t<float, 8, false>(pl, pr, a) : launch_lane_descent_t<double, 8, false>(pl, pr, a); break;
     default: throw Failure(PTSBE_EINVAL, "descent sampler: unsupported vector length");
   }
+}
+
+// descent shape of the Hermitian-packed form: D reals per column
+static DescentShape herm_shape(const ptsbe_plan* pl, uint32_t D) {
+  DescentShape s;
+  const uint32_t epc = pl->dtype == PTSBE_C64 ? 4 : 2;  // reals per 16-byte chunk
+  for (uint32_t nch = 1; nch <= 8; nch <<= 1)
+    if (DS_GS * nch * epc >= D) { s.nch = nch; break; }
+  s.dpad = DS_GS * s.nch * epc;
+  return s;
 }
 
 static void launch_tree_build(ptsbe_plan* pl, const Program& pr, const void* rec0, uint32_t rec_stride,
@@ -661,6 +717,31 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       log.end();
       Program& prj = progs[j - 1];
       const bool fused = pl->lane && prj.lane_fused && lane_descent_fits(pl, prj, dsh, b);
+      // Hermitian-packed columns (v = x (x) conj(x)): half the table, half the work per tree level
+      DescentShape hsh;
+      DevBuf htree;
+      if (fused && prj.herm) {
+        hsh = herm_shape(pl, prj.d.proj_d);
+        if (hsh.nch) {
+          const size_t real = pl->elem / 2;
+          htree.alloc(((size_t)ne * hsh.dpad * real) << b, st);
+          HermPackArgs hp;
+          hp.tree = tree.p;
+          hp.packed = htree.p;
+          hp.map = prj.herm_map.as<uint32_t>();
+          hp.D = prj.d.proj_d;
+          hp.dpad_c = dsh.dpad;
+          hp.dpad_r = hsh.dpad;
+          hp.b = b;
+          const dim3 grid(ne, cdiv(((uint64_t)hsh.dpad) << b, 256));
+          log.begin(&stats->descent_ms[j - 1]);
+          if (pl->dtype == PTSBE_C64) herm_pack_kernel<float><<<grid, 256, 0, st>>>(hp);
+          else herm_pack_kernel<double><<<grid, 256, 0, st>>>(hp);
+          g_launches++;
+          CK(cudaGetLastError());
+          log.end();
+        }
+      }
       if (fused) {
         // per-item steps and descent in one kernel: v never leaves the SM; raw per-draw outcomes
         // are merged into ordered (outcome, count) pairs afterwards
@@ -673,7 +754,8 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
         else
           fa.l = lane_args<double>(pl, prj, EXEC_VECTOR, table_dev.as<LevelDev>(), kraus_dev, 0, U, nullptr, 0);
         DescentArgs& da = fa.d;
-        da.tree = tree.p;
+        da.tree = hsh.nch ? htree.p : tree.p;
+        fa.herm_map = hsh.nch ? prj.herm_map.as<uint32_t>() : nullptr;
         da.eset = cur.eset.as<uint32_t>();
         da.mult = cur.mult.as<uint32_t>();
         da.slot_off = cur.slot_off.as<uint32_t>();
@@ -697,7 +779,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
         fa.big_list = big_list.as<uint32_t>();
         fa.big_count = big_count.as<uint32_t>();
         log.begin(&stats->descent_ms[j - 1]);
-        launch_lane_descent(pl, prj, fa, dsh);
+        launch_lane_descent(pl, prj, fa, hsh.nch ? hsh : dsh);
         DedupArgs dd;
         dd.slot_off = da.slot_off;
         dd.slot_index = da.slot_index;
@@ -1171,6 +1253,13 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
           CK(cudaMemcpyAsync(pr.tables.p, pr.d.tables, (size_t)pr.d.n_table_words * 4,
                              cudaMemcpyHostToDevice, st));
         classify_lane(pl.get(), pr);
+        if (pr.herm && env_size("PTSBE_HERM", 1)) {
+          pr.herm_map.alloc(pr.herm_map_host.size() * 4, st);
+          CK(cudaMemcpyAsync(pr.herm_map.p, pr.herm_map_host.data(), pr.herm_map_host.size() * 4,
+                             cudaMemcpyHostToDevice, st));
+        } else {
+          pr.herm = false;
+        }
         {
           double big = 0, all = 0;
           for (uint32_t q = 0; q < pr.d.n_steps && pr.d.steps; ++q) {
@@ -1209,7 +1298,7 @@ void ptsbe_plan_destroy(ptsbe_plan* pl) {
   for (auto& s : pl->programs)
     for (auto& p : s) {
       p.leaves.release(); p.steps.release(); p.tables.release();
-      p.memo_ptr.release(); p.memo_idx.release(); p.memo.release();
+      p.memo_ptr.release(); p.memo_idx.release(); p.memo.release(); p.herm_map.release();
     }
   cudaStreamSynchronize(pl->stream);
   cudaStreamDestroy(pl->stream);

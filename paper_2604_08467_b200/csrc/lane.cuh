@@ -356,13 +356,46 @@ struct LaneDescentArgs {
   uint32_t* big_list;       // items with more than LN_DEDUP_SERIAL draws (merged by dedup_big_kernel)
   uint32_t* big_count;
   uint32_t tile;            // consecutive items a CTA takes at a time (multiple of LN_THREADS)
+  const uint32_t* herm_map; // HERM: [D] real slot -> c | c' << 12 | kind << 24 (kind 0: Re v_c, 1: Im v_c)
 };
 
-template <typename R, int NCH>
-__global__ void __launch_bounds__(LN_THREADS) lane_descent_kernel(const LaneDescentArgs a) {
+// Hermitian packing (HERM).  When the projection vector is v = x (x) conj(x) (the ket / bra halves
+// of the cut are mirror images), v[c'] = conj(v[c]) for the transposed index c', so
+//   Re sum_c v_c C_c = sum_diag v_c Re C_c + sum_{c < c'} Re v_c (Re C_c + Re C_c') - Im v_c (Im C_c - Im C_c'):
+// D REAL products instead of D complex ones.  The tree columns are packed accordingly by
+// herm_pack_kernel, which halves both the table in shared memory and the work of every tree level.
+struct HermPackArgs {
+  const void* tree;         // [sets][N][dpad_c] complex columns (tree_build_kernel)
+  void* packed;             // [sets][N][dpad_r] reals
+  const uint32_t* map;      // [D] c | c' << 12 | kind << 24
+  uint32_t D, dpad_c, dpad_r, b;
+};
+
+template <typename R>
+__global__ void herm_pack_kernel(const HermPackArgs a) {
+  using C = typename CxT<R>::type;
+  const uint32_t N = 1u << a.b;
+  const uint32_t e = blockIdx.x;
+  const uint32_t x = blockIdx.y * blockDim.x + threadIdx.x;
+  if (x >= N * a.dpad_r) return;
+  const uint32_t node = x / a.dpad_r, s = x % a.dpad_r;
+  R out = R(0);
+  if (s < a.D) {
+    const uint32_t m = __ldg(a.map + s);
+    const uint32_t c = m & 0xfffu, c2 = (m >> 12) & 0xfffu, kind = m >> 24;
+    const C* col = reinterpret_cast<const C*>(a.tree) + ((size_t)e * N + node) * a.dpad_c;
+    const C u = col[c], w = col[c2];
+    if (kind == 0) out = (c == c2) ? u.x : u.x + w.x;
+    else if (kind == 1) out = -(u.y - w.y);
+  }
+  reinterpret_cast<R*>(a.packed)[((size_t)e * N + node) * a.dpad_r + s] = out;
+}
+
+template <typename R, int NCH, bool HERM>
+__global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneDescentArgs a) {
   using C = typename CxT<R>::type;
   using CH = typename DsChunk<R>::type;
-  constexpr int CPC = DsChunk<R>::CPC;
+  constexpr int CPC = HERM ? 2 * DsChunk<R>::CPC : DsChunk<R>::CPC;  // vector elements per 16-byte chunk
   constexpr uint32_t COL = DS_GS * NCH;
   extern __shared__ __align__(16) unsigned char ln_smem[];
   const ExecArgs& e = a.l.e;
@@ -392,13 +425,22 @@ __global__ void __launch_bounds__(LN_THREADS) lane_descent_kernel(const LaneDesc
   // chunks {k * 8 + lane}, i.e. elements CPC * (k * 8 + lane) + {0, CPC - 1}.
   // Common case (v = x (x) conj(x): one multiply per element, no slice): the gather offsets of
   // this lane's elements do not depend on the item -- resolved once per kernel.
-  const bool fast_last = last.kn == 1 && !(last.flags & 4u) && last.hi_n == 1;
+  const bool fast_last = HERM || (last.kn == 1 && !(last.flags & 4u) && last.hi_n == 1);
   const uint32_t last_sa = last.s0.x == 0 ? LN_AST : 1u, last_sb = last.s0.z == 0 ? LN_AST : 1u;
   uint32_t via[NCH * CPC], vib[NCH * CPC];
+  uint32_t vim = 0;  // HERM: bit k set -> slot k takes the imaginary part
 #pragma unroll
   for (int k = 0; k < NCH * CPC; ++k) {
-    const uint32_t c = CPC * ((k / CPC) * DS_GS + lane) + (k % CPC);
-    const bool ok = fast_last && c < last.out_n;
+    uint32_t c = CPC * ((k / CPC) * DS_GS + lane) + (k % CPC);
+    bool ok = fast_last && c < last.out_n;
+    if constexpr (HERM) {
+      if (ok) {
+        const uint32_t m = __ldg(a.herm_map + c);  // c | c' << 12 | kind << 24
+        c = m & 0xfffu;
+        if ((m >> 24) == 1u) vim |= 1u << k;
+        ok = (m >> 24) < 2u;
+      }
+    }
     via[k] = ok ? (last.loA[c] + last.kA[0]) * last_sa : 0xffffffffu;
     vib[k] = ok ? (last.loB[c] + last.kB[0]) * last_sb : 0u;
   }
@@ -422,10 +464,22 @@ __global__ void __launch_bounds__(LN_THREADS) lane_descent_kernel(const LaneDesc
         if (c < last.out_n) x[k] = lane_element<R>(last, A, B, c);
       }
     }
+    if constexpr (HERM) {
+      // real slots: Re or Im of the selected element
+      R w[NCH * CPC];
 #pragma unroll
-    for (int k = 0; k < NCH; ++k) {
-      if constexpr (CPC == 2) { v[k].x = x[2 * k].x; v[k].y = x[2 * k].y; v[k].z = x[2 * k + 1].x; v[k].w = x[2 * k + 1].y; }
-      else { v[k].x = x[k].x; v[k].y = x[k].y; }
+      for (int k = 0; k < NCH * CPC; ++k) w[k] = ((vim >> k) & 1u) ? x[k].y : x[k].x;
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) {
+        if constexpr (CPC == 4) { v[k].x = w[4 * k]; v[k].y = w[4 * k + 1]; v[k].z = w[4 * k + 2]; v[k].w = w[4 * k + 3]; }
+        else { v[k].x = w[2 * k]; v[k].y = w[2 * k + 1]; }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < NCH; ++k) {
+        if constexpr (CPC == 2) { v[k].x = x[2 * k].x; v[k].y = x[2 * k].y; v[k].z = x[2 * k + 1].x; v[k].w = x[2 * k + 1].y; }
+        else { v[k].x = x[k].x; v[k].y = x[k].y; }
+      }
     }
   };
   auto dot = [&](const CH (&v)[NCH], const CH* col) -> R {
@@ -433,7 +487,10 @@ __global__ void __launch_bounds__(LN_THREADS) lane_descent_kernel(const LaneDesc
 #pragma unroll
     for (int i = 0; i < NCH; ++i) {
       const CH m = col[i * DS_GS + lane];
-      if constexpr (CPC == 2) {
+      if constexpr (HERM) {
+        acc = fma(v[i].x, m.x, acc); acc = fma(v[i].y, m.y, acc);
+        if constexpr (CPC == 4) { acc = fma(v[i].z, m.z, acc); acc = fma(v[i].w, m.w, acc); }
+      } else if constexpr (CPC == 2) {
         acc = fma(v[i].x, m.x, acc); acc = fma(-v[i].y, m.y, acc);
         acc = fma(v[i].z, m.z, acc); acc = fma(-v[i].w, m.w, acc);
       } else {
