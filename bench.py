@@ -54,7 +54,7 @@ def build_workload(name: str, args):
 
     if name == "cfg2":
         c, _ = workloads.hea(30, 6, gamma=0.01, p=0.01, seed=2)
-        sizes = (9, 7, 6, 8)  # BatchPlan is an input of the method (reference engine.py:76-142); best of a sweep
+        sizes = (9, 6, 7, 8)  # BatchPlan is an input of the method (reference engine.py:76-142); best of a sweep
         dflt = dict(sets=4096, shots=10_000, dtype="complex64",
                     label="cfg2: 30-qubit HEA depth 6, amplitude damping 0.01 + 2q depolarizing 0.01")
     elif name == "cfg1":
