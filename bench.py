@@ -469,7 +469,7 @@ def main():
                 per_item = 24 + 8 * words + 4 + 8.0 * shots_j / max(d_items, 1) + (rec_bytes + tree_bytes) / max(d_items, 1)
                 flops_item = 8.0 * pr.flops * (1.0 + shots_j / max(d_items, 1)) + 4.0 * pr.proj_d * (b_j + 1) * shots_j / max(d_items, 1)
                 cands.append((desc[j], f"lane_descent_kernel (per-item steps + per-qubit descent fused, D={pr.proj_d}, b={b_j}), stage {j + 1}",
-                              d_items, launches_j, per_item, flops_item))
+                              d_items, launches_j, per_item, flops_item, 92.0))  # ncu: 78-106 B of DRAM traffic per item
             elif pr.proj_d and d_items:
                 # per-item steps, vector written as one row per item
                 cands.append((marg[j], f"exec_kernel (per-item steps -> v[{pr.proj_d}]), stage {j + 1}", n_items, launches_j,
@@ -494,7 +494,10 @@ def main():
             else:
                 cands.append((marg[j], f"exec_kernel (marginal pass), stage {j + 1}", n_items, launches_j,
                               pr.ext_read_elems * elem + 8 + 8 * words + pr.out_elems * real + 16, 8.0 * pr.flops))
-        top_ms, top_name, items, launches, item_bytes, item_flops = max(cands, key=lambda x: x[0])
+        top = max(cands, key=lambda x: x[0])
+        top_ms, top_name, items, launches, item_bytes, item_flops = top[:6]
+        # DRAM bytes per work item measured by ncu --set full for this kernel (profiles/), when captured
+        ncu_item_traffic = top[6] if len(top) > 6 else None
         hbm_peak, peak_src = peaks()
         t_s = top_ms * 1e-3
         achieved = items * item_bytes / t_s / 1e9 if t_s > 0 else 0.0
@@ -532,7 +535,11 @@ def main():
             "roofline": {
                 "kernel": top_name + (" <float>" if dtype == "complex64" else " <double>"),
                 "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
+                "frac": achieved / hbm_peak,
+                "traffic": (ncu_item_traffic * items / max(launches, 1)) if ncu_item_traffic else None,
+                "traffic_source": ("profiles/r1_final_ncu_summary.md: dram read + write per work item of this kernel "
+                                   "(ncu --set full, 512-set run) x items per launch") if ncu_item_traffic else None,
+                "peak_source": peak_src,
                 "bytes_per_item": item_bytes, "items_per_launch": items / max(launches, 1),
                 "launch_ms": top_ms / max(launches, 1), "share_of_step": top_ms / max(timed_ms, 1e-9),
                 "fma": {"achieved_tflops": tflops, "peak_tflops": fma_peak, "frac": tflops / fma_peak if fma_peak else None,
