@@ -460,7 +460,7 @@ static void launch_lane_descent_t(ptsbe_plan* pl, Program& pr, LaneDescentArgs& 
   const LaneLayout L = lane_layout(a.l.e.n_steps, a.l.n_leaves, a.l.n_table_words, a.l.n_levels,
                                    a.l.e.arena_fast, a.l.e.words, (uint32_t)sizeof(C));
   const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 4 * 4) +
-                      (((size_t)DS_GS * NCH * sizeof(CH)) << a.d.b);
+                      (((size_t)LN_GS * NCH * sizeof(CH)) << a.d.b);
   if (smem > 200 * 1024) throw Failure(PTSBE_ERESOURCE, "fused descent needs more shared memory than one SM has");
   if (pr.lane_blocks_per_sm == 0) {
     CK(cudaFuncSetAttribute(lane_descent_kernel<R, NCH, HERM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -485,8 +485,10 @@ static bool lane_descent_fits(const ptsbe_plan* pl, const Program& pr, const Des
   const uint32_t elem = (uint32_t)pl->elem;
   const LaneLayout L = lane_layout(pr.d.n_steps, pr.d.n_leaves, pr.d.n_table_words, pl->f + 2,
                                    pr.d.arena_fast_elems, pl->words, elem);
-  const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 4 * 4) + (((size_t)DS_GS * sh.nch * 16) << b);
-  return smem <= 200 * 1024;
+  // sh is the 8-lane shape of descent.cuh; the fused kernel spreads the same padded column over LN_GS lanes
+  const uint32_t nch_f = sh.nch * (DS_GS / LN_GS);
+  const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 4 * 4) + (((size_t)LN_GS * nch_f * 16) << b);
+  return nch_f <= 8 && smem <= 200 * 1024;
 }
 
 static void launch_lane_descent(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a, const DescentShape& sh) {
@@ -516,8 +518,8 @@ static DescentShape herm_shape(const ptsbe_plan* pl, uint32_t D) {
   DescentShape s;
   const uint32_t epc = pl->dtype == PTSBE_C64 ? 4 : 2;  // reals per 16-byte chunk
   for (uint32_t nch = 1; nch <= 8; nch <<= 1)
-    if (DS_GS * nch * epc >= D) { s.nch = nch; break; }
-  s.dpad = DS_GS * s.nch * epc;
+    if (LN_GS * nch * epc >= D) { s.nch = nch; break; }
+  s.dpad = LN_GS * s.nch * epc;
   return s;
 }
 
@@ -779,7 +781,9 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
         fa.big_list = big_list.as<uint32_t>();
         fa.big_count = big_count.as<uint32_t>();
         log.begin(&stats->descent_ms[j - 1]);
-        launch_lane_descent(pl, prj, fa, hsh.nch ? hsh : dsh);
+        DescentShape fsh = dsh;  // chunks per lane of the fused kernel's LN_GS-lane groups
+        fsh.nch = dsh.nch * (DS_GS / LN_GS);
+        launch_lane_descent(pl, prj, fa, hsh.nch ? hsh : fsh);
         DedupArgs dd;
         dd.slot_off = da.slot_off;
         dd.slot_index = da.slot_index;

@@ -36,6 +36,8 @@ constexpr int LN_THREADS = 256;
 constexpr int LN_WARPS = LN_THREADS / 32;
 constexpr int LN_AST = 33;          // arena element stride (in elements) between consecutive indices
 constexpr int LN_MAX_LEVELS = 16;   // ancestors kept per lane
+constexpr int LN_GS = 4;            // lanes per (item, draw) in the descent phase of the fused kernel
+constexpr int LN_NG = 32 / LN_GS;   // such groups per warp
 constexpr uint32_t LN_DEDUP_SERIAL = 48;  // draws per item merged by one thread; more: warp path
 
 // shared-memory layout shared by the two kernels (offsets in bytes from the dynamic base)
@@ -396,7 +398,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
   using C = typename CxT<R>::type;
   using CH = typename DsChunk<R>::type;
   constexpr int CPC = HERM ? 2 * DsChunk<R>::CPC : DsChunk<R>::CPC;  // vector elements per 16-byte chunk
-  constexpr uint32_t COL = DS_GS * NCH;
+  constexpr uint32_t COL = LN_GS * NCH;
   extern __shared__ __align__(16) unsigned char ln_smem[];
   const ExecArgs& e = a.l.e;
   const DescentArgs& d = a.d;
@@ -413,8 +415,8 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
   CH* table = reinterpret_cast<CH*>(bad_s + LN_THREADS);                       // [N][COL]
   __shared__ uint32_t s_end;
   const int tid = threadIdx.x, lane32 = tid & 31, warp = tid >> 5;
-  const int lane = tid & (DS_GS - 1), grp = lane32 / DS_GS;                    // 8-lane groups: 4 per warp
-  const unsigned gmask = 0xffu << (8 * grp);
+  const int lane = tid & (LN_GS - 1), grp = lane32 / LN_GS;                    // LN_GS-lane groups
+  const unsigned gmask = ((1u << LN_GS) - 1u) << (LN_GS * grp);
   const uint32_t wbase = warp * 32;
   const CH* TREE = reinterpret_cast<const CH*>(d.tree);
   uint32_t loaded = 0xffffffffu;
@@ -431,7 +433,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
   uint32_t vim = 0;  // HERM: bit k set -> slot k takes the imaginary part
 #pragma unroll
   for (int k = 0; k < NCH * CPC; ++k) {
-    uint32_t c = CPC * ((k / CPC) * DS_GS + lane) + (k % CPC);
+    uint32_t c = CPC * ((k / CPC) * LN_GS + lane) + (k % CPC);
     bool ok = fast_last && c < last.out_n;
     if constexpr (HERM) {
       if (ok) {
@@ -460,7 +462,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
           cmac(x[k], p, q);
         }
       } else {
-        const uint32_t c = CPC * ((k / CPC) * DS_GS + lane) + (k % CPC);
+        const uint32_t c = CPC * ((k / CPC) * LN_GS + lane) + (k % CPC);
         if (c < last.out_n) x[k] = lane_element<R>(last, A, B, c);
       }
     }
@@ -486,7 +488,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
     R acc = R(0);
 #pragma unroll
     for (int i = 0; i < NCH; ++i) {
-      const CH m = col[i * DS_GS + lane];
+      const CH m = col[i * LN_GS + lane];
       if constexpr (HERM) {
         acc = fma(v[i].x, m.x, acc); acc = fma(v[i].y, m.y, acc);
         if constexpr (CPC == 4) { acc = fma(v[i].z, m.z, acc); acc = fma(v[i].w, m.w, acc); }
@@ -498,7 +500,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
       }
     }
 #pragma unroll
-    for (int s = DS_GS / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(gmask, acc, s, DS_GS);
+    for (int s = LN_GS / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(gmask, acc, s, LN_GS);
     return acc;
   };
 
@@ -573,17 +575,17 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
         // warp's items in order -- v, mass (guards as descent.cuh) and draw 0; later rounds: the
         // remaining draws of multi-shot items, v recomputed, mass from shared memory ----
         const uint32_t n_live = min(32u, end - w0);
-        const uint32_t item_rounds = (n_live + 3) / 4, rounds = item_rounds + (total + 3) / 4;
+        const uint32_t item_rounds = (n_live + LN_NG - 1) / LN_NG, rounds = item_rounds + (total + LN_NG - 1) / LN_NG;
         for (uint32_t rd = 0; rd < rounds; ++rd) {
           const bool first = rd < item_rounds;  // warp-uniform
           bool active;
           uint32_t i, t;
           if (first) {
-            active = rd * 4 + grp < n_live;
-            i = active ? rd * 4 + grp : n_live - 1;
+            active = rd * LN_NG + grp < n_live;
+            i = active ? rd * LN_NG + grp : n_live - 1;
             t = 0;
           } else {
-            const uint32_t d0 = (rd - item_rounds) * 4;
+            const uint32_t d0 = (rd - item_rounds) * LN_NG;
             active = d0 + grp < total;
             const uint32_t dr = active ? d0 + grp : total - 1;
             uint32_t lo = 0, hi = 31;  // smallest i with cum[i] > dr
