@@ -412,7 +412,9 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
   uint32_t* slot0_s = cum_s + LN_THREADS;                                      // [LN_THREADS]
   uint32_t* eset_s = slot0_s + LN_THREADS;                                     // [LN_THREADS]
   uint32_t* bad_s = eset_s + LN_THREADS;                                       // [LN_THREADS]
-  CH* table = reinterpret_cast<CH*>(bad_s + LN_THREADS);                       // [N][COL]
+  uint32_t* rank_s = bad_s + LN_THREADS;                                       // [LN_THREADS]
+  uint32_t* gid_s = rank_s + LN_THREADS;                                       // [LN_THREADS]
+  CH* table = reinterpret_cast<CH*>(gid_s + LN_THREADS);                       // [N][COL]
   __shared__ uint32_t s_end;
   const int tid = threadIdx.x, lane32 = tid & 31, warp = tid >> 5;
   const int lane = tid & (LN_GS - 1), grp = lane32 / LN_GS;                    // LN_GS-lane groups
@@ -538,6 +540,8 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
         lane_run<R>(cx, 0, e.n_steps - 1, es_row, nullptr, false);
         uint32_t m = live ? d.mult[item] : 0u;
         slot0_s[tid] = d.slot_off[item];
+        rank_s[tid] = d.rank[item];     // Philox counter words of this lane's item: staged here so a
+        gid_s[tid] = d.eset_id[item];   // draw does not start with an L2 round trip
         bad_s[tid] = 0;
         __syncwarp();
         // one descent from v: decisions in the arithmetic type of the path (float for complex64: the
@@ -545,8 +549,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
         // with the oracle's float64 inverse-CDF walk)
         auto descend = [&](const CH (&v)[NCH], R mass, uint32_t t, uint32_t i, uint32_t& bad) -> uint32_t {
           const R tol = (R)(d.neg_abs - d.neg_rel * (double)mass);
-          const uint32_t item_i = d.first_item + w0 + i;
-          const Philox4 x = philox4x32_10(t, __ldg(d.rank + item_i), d.stage, __ldg(d.eset_id + item_i), d.k0, d.k1);
+          const Philox4 x = philox4x32_10(t, rank_s[wbase + i], d.stage, gid_s[wbase + i], d.k0, d.k1);
           const uint64_t x64 = ((uint64_t)x.v[1] << 32) | x.v[0];
           R p = mass;
           R r = (R)((double)(x64 >> 11) * (1.0 / 9007199254740992.0)) * mass;  // u in [0, 1)
