@@ -174,6 +174,7 @@ static ExecLaunch configure_exec(ptsbe_plan* pl, Program& pr, uint32_t n_items) 
     L.desc_off = (uint32_t)L.smem;
     L.desc_cap = std::min<uint32_t>(d.n_steps, (uint32_t)env_size("PTSBE_DESC_CAP", DESC_CAP));
     L.smem += (size_t)L.desc_cap * STEP_WORDS * 4;
+    if (memo) L.smem += (size_t)L.desc_cap * 2 * sizeof(void*);  // pre-resolved leaf operands
   }
   if (L.smem > 227 * 1024)
     throw Failure(PTSBE_ERESOURCE, "stage program needs more shared memory than one SM has");

@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(TILED ? 512 : 256, TILED ? 1 : 5) exec_kernel(
   const C* memo = reinterpret_cast<const C*>(a.memo);
   const bool build = MEMO && a.mode == EXEC_MEMO_BUILD;
   uint32_t* desc_s = reinterpret_cast<uint32_t*>(smem_raw + a.desc_off);
+  const C** pre_s = reinterpret_cast<const C**>(smem_raw + a.desc_off + (size_t)a.desc_cap * STEP_WORDS * 4);
   uint32_t n_staged = 0;
   if (!WARP && !MEMO && a.desc_cap) {
     // same step list for every item: staged once
@@ -311,6 +312,18 @@ __global__ void __launch_bounds__(TILED ? 512 : 256, TILED ? 1 : 5) exec_kernel(
         desc_s[i] = __ldg(a.steps + (size_t)run_list[si] * STEP_WORDS + w);
       }
       __syncthreads();
+      // leaf operands of the staged steps resolved in parallel (leaf row -> Kraus index -> pool
+      // address is two dependent loads that would otherwise sit in front of every small step)
+      for (uint32_t i = threadIdx.x; i < n_staged * 2; i += blockDim.x) {
+        const uint32_t* dsc = desc_s + (size_t)(i >> 1) * STEP_WORDS + (i & 1) * 2;
+        const C* ptr = nullptr;
+        if (dsc[0] == 1) {
+          const uint4 lf = __ldg(reinterpret_cast<const uint4*>(a.leaves) + dsc[1]);
+          if (lf.z < 2) ptr = pool + lf.x + (size_t)(lf.z == 1 ? __ldg(sel + lf.w) : 0u) * lf.y;
+        }
+        pre_s[i] = ptr;
+      }
+      __syncthreads();
     }
 
     // measured bit selected by a prefix-projector leaf (slice steps read the bit, not the vector)
@@ -357,8 +370,11 @@ __global__ void __launch_bounds__(TILED ? 512 : 256, TILED ? 1 : 5) exec_kernel(
         if (TILED) s4 = __ldg(st4 + 4);
       }
       const bool slice = (s2.w & 4u) != 0;
-      const C* A = resolve(s0.x, s0.y);
-      const C* B = slice ? nullptr : resolve(s0.z, s0.w);
+      const C* A = nullptr;
+      const C* B = nullptr;
+      if (MEMO && si < n_staged) { A = pre_s[2 * si]; B = pre_s[2 * si + 1]; }
+      if (!A) A = resolve(s0.x, s0.y);
+      if (!B && !slice) B = resolve(s0.z, s0.w);
       C* O;
       size_t o_stride = 1;
       bool store = true;
