@@ -461,7 +461,7 @@ static void launch_lane_descent_t(ptsbe_plan* pl, Program& pr, LaneDescentArgs& 
   const LaneLayout L = lane_layout(a.l.e.n_steps, a.l.n_leaves, a.l.n_table_words, a.l.n_levels,
                                    a.l.e.arena_fast, a.l.e.words, (uint32_t)sizeof(C));
   const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4) +
-                      (((size_t)LN_GS * NCH * sizeof(CH)) << a.d.b);
+                      (((size_t)(LN_GS * NCH + 1) * sizeof(CH)) << a.d.b);
   if (smem > 200 * 1024) throw Failure(PTSBE_ERESOURCE, "fused descent needs more shared memory than one SM has");
   if (pr.lane_blocks_per_sm == 0) {
     CK(cudaFuncSetAttribute(lane_descent_kernel<R, NCH, HERM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -488,7 +488,7 @@ static bool lane_descent_fits(const ptsbe_plan* pl, const Program& pr, const Des
                                    pr.d.arena_fast_elems, pl->words, elem);
   // sh is the 8-lane shape of descent.cuh; the fused kernel spreads the same padded column over LN_GS lanes
   const uint32_t nch_f = sh.nch * (DS_GS / LN_GS);
-  const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4) + (((size_t)LN_GS * nch_f * 16) << b);
+  const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4) + (((size_t)(LN_GS * nch_f + 1) * 16) << b);
   return nch_f <= 8 && smem <= 200 * 1024;
 }
 

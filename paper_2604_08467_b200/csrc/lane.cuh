@@ -399,6 +399,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
   using CH = typename DsChunk<R>::type;
   constexpr int CPC = HERM ? 2 * DsChunk<R>::CPC : DsChunk<R>::CPC;  // vector elements per 16-byte chunk
   constexpr uint32_t COL = LN_GS * NCH;
+  constexpr uint32_t COLP = COL + 1;  // shared-memory row pitch: one chunk of padding staggers the rows over the banks
   extern __shared__ __align__(16) unsigned char ln_smem[];
   const ExecArgs& e = a.l.e;
   const DescentArgs& d = a.d;
@@ -414,7 +415,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
   uint32_t* bad_s = eset_s + LN_THREADS;                                       // [LN_THREADS]
   uint32_t* rank_s = bad_s + LN_THREADS;                                       // [LN_THREADS]
   uint32_t* gid_s = rank_s + LN_THREADS;                                       // [LN_THREADS]
-  CH* table = reinterpret_cast<CH*>(gid_s + LN_THREADS);                       // [N][COL]
+  CH* table = reinterpret_cast<CH*>(gid_s + LN_THREADS);                       // [N][COLP]
   __shared__ uint32_t s_end;
   const int tid = threadIdx.x, lane32 = tid & 31, warp = tid >> 5;
   const int lane = tid & (LN_GS - 1), grp = lane32 / LN_GS;                    // LN_GS-lane groups
@@ -522,7 +523,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
         if (d.eset[d.first_item + i] != er) { atomicMin(&s_end, i); break; }
       if (er != loaded) {
         const CH* src = TREE + (size_t)er * N * COL;
-        for (uint32_t x = tid; x < N * COL; x += LN_THREADS) table[x] = __ldg(src + x);
+        for (uint32_t x = tid; x < N * COL; x += LN_THREADS) table[(x / COL) * COLP + (x % COL)] = __ldg(src + x);
         loaded = er;
       }
       __syncthreads();
@@ -556,7 +557,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
           if (sizeof(R) == 4 && !(r < mass)) r = nextafterf((float)mass, 0.0f);  // u rounded up to 1.0f
           uint32_t node = 0;
           for (uint32_t lvl = 1; lvl <= d.b; ++lvl) {
-            R pl = dot(v, table + (size_t)((1u << (lvl - 1)) + node) * COL);
+            R pl = dot(v, table + (size_t)((1u << (lvl - 1)) + node) * COLP);
             if (pl < tol || p - pl < tol) bad = PTSBE_ENUMERIC;
             pl = fmin(fmax(pl, R(0)), p);
             if (r < pl) { node = 2 * node; p = pl; }
