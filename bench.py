@@ -379,6 +379,10 @@ def main():
     # weight (e.g. amplitude-damping K1 on |0>) are flagged by the device and contribute none
     _, last_counts = batch.fetch()
     sampled_local = int(last_counts.sum())
+    del last_counts
+    # the resident batch hands its workspaces back to the plan before the host-buffer leg creates its
+    # own batch (at E = 10^6 the two would not fit side by side)
+    batch.close()
     flagged_local = int(stats[-1].flagged_sets)
     if sampled_local != total_shots_local and flagged_local == 0:
         raise SystemExit(f"histogram holds {sampled_local} shots, expected {total_shots_local}, and nothing was flagged")
@@ -548,7 +552,6 @@ def main():
             "cpu_baseline": cpu,
         }
         print(json.dumps(out))
-    batch.close()
     pipe.close()
     if world > 1:
         dist.destroy_process_group()

@@ -117,3 +117,36 @@ def test_multinomial_counts_sum_and_distribution():
     # zero-probability outcomes are never drawn
     c = O.multinomial_counts(np.array([0.0, 1.0, 0.0, 0.0]), 1000, 1, 0, 1, 0)
     assert c.tolist() == [0, 1000, 0, 0]
+
+
+def _nonprop_runs():
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_nonproportional.json")
+    with open(path) as fp:
+        return json.load(fp)["runs"]
+
+
+def test_golden_nonproportional_records(golden_cases):
+    """The reference's own sample_nonproportional (engine.py:527-576, driven by
+    the counter-based shim CounterChoice) and the oracle's restatement emit the
+    same records in the same order: chosen prefixes, exhaustive harvest with its
+    probability tags (1e-12), direct multinomial counts."""
+    n_records = 0
+    for run in _nonprop_runs():
+        case = golden_cases[run["case"]]
+        c, sizes, es = case_objects(case)
+        var = run["variant"]
+        for k, want in zip(es, run["records"]):
+            ops, finals = bridge.merged_ops(c, k.realized)
+            got = O.sample_nonproportional(ops, finals, sizes, run["seed"], k.id, nonfinal_shots=var["nonfinal_shots"],
+                                           final_mode=var["final_mode"], threshold=var["threshold"],
+                                           direct_count=var["direct_count"])
+            assert [(s, n) for s, n, _ in got] == [(s, n) for s, n, _ in want]
+            for (_, _, p), (_, _, q) in zip(got, want):
+                assert (p is None) == (q is None)
+                if p is not None:
+                    assert abs(p - q) <= 1e-12
+            n_records += len(got)
+    assert n_records >= 1000

@@ -1,5 +1,6 @@
 """Print the headline fields of a bench.py JSON line (last line of a log)."""
-import json, sys
+import json, signal, sys
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)
 d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
 e2e = d.get("e2e") or {}
 print("value %.4g shots/s  ms/step %.2f  e2e %.4g  flagged %s  events %s" % (
