@@ -203,6 +203,20 @@ int ptsbe_sample(ptsbe_plan* plan, const uint8_t* kraus_idx, const uint32_t* sho
                  uint64_t** keys, uint32_t** rec_eset, uint64_t** counts,
                  uint64_t* n_records, ptsbe_run_stats* stats);
 
+/* replaces: sample_nonproportional per error set (engine.py:527-576), the data-harvesting mode.
+ *   Every non-final stage branches each prefix into up to `nonfinal_shots` DISTINCT children
+ *   (weighted choice without replacement, engine.py:549-556); the final stage emits, per prefix,
+ *   final_mode 0: every outcome whose conditional probability reaches `threshold`, count 1, tagged
+ *                 with that probability in probs[] (engine.py:562-568),
+ *   final_mode 1: a multinomial split of `direct_count` shots, probs[] = -1 (engine.py:569-574).
+ *   Records are per error set, sorted by (position in this call, key): rec_eset[] holds the position.
+ *   Uniforms: Philox counters (draw, prefix rank, stage, global error-set id), key = seed. */
+int ptsbe_sample_nonproportional(ptsbe_plan* plan, const uint8_t* kraus_idx, const uint32_t* eset_ids,
+                                 uint64_t n_sets, uint64_t seed, uint32_t nonfinal_shots,
+                                 uint32_t final_mode, double threshold, uint32_t direct_count,
+                                 uint64_t** keys, uint32_t** rec_eset, uint64_t** counts, double** probs,
+                                 uint64_t* n_records, ptsbe_run_stats* stats);
+
 /* resident variant for device-timed throughput: inputs are uploaded once,
  * every run leaves its histogram on the device and returns only its length. */
 typedef struct ptsbe_batch ptsbe_batch;

@@ -28,7 +28,7 @@ EXPORTS = (
     "ptsbe_sample", "ptsbe_batch_upload", "ptsbe_batch_run", "ptsbe_batch_fetch",
     "ptsbe_batch_destroy", "ptsbe_histogram_merge", "ptsbe_plan_greedy", "ptsbe_free",
     "ptsbe_batch_histogram_dev", "ptsbe_histogram_merge_dev", "ptsbe_free_dev",
-    "ptsbe_measure_fma_peak",
+    "ptsbe_measure_fma_peak", "ptsbe_sample_nonproportional",
 )
 
 
@@ -92,6 +92,9 @@ def load() -> ctypes.CDLL:
                                        ctypes.POINTER(U64), I]
     lib.ptsbe_sample.argtypes = [P, P, P, P, U64, U64, I, ctypes.POINTER(P), ctypes.POINTER(P),
                                  ctypes.POINTER(P), ctypes.POINTER(U64), ctypes.POINTER(RunStats)]
+    lib.ptsbe_sample_nonproportional.argtypes = [P, P, P, U64, U64, U32, U32, ctypes.c_double, U32,
+                                                 ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P),
+                                                 ctypes.POINTER(P), ctypes.POINTER(U64), ctypes.POINTER(RunStats)]
     lib.ptsbe_batch_upload.argtypes = [P, P, P, P, U64, ctypes.POINTER(P)]
     lib.ptsbe_batch_run.argtypes = [P, U64, ctypes.POINTER(U64), ctypes.POINTER(RunStats)]
     lib.ptsbe_batch_fetch.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(U64)]
@@ -283,6 +286,26 @@ class DevicePlan:
         counts = _take(c, n.value, np.uint64)
         esets = None if merged else _take(e, n.value, np.uint32)
         return keys, esets, counts, st
+
+    def sample_nonproportional(self, kraus_idx, eset_ids, seed: int, nonfinal_shots: int, final_mode: str,
+                               threshold: float, direct_count: int):
+        """Non-proportional sampling (engine.py:527-576) of every error set in one device run:
+        returns (keys [R, words] u64, eset position [R], counts [R], probs [R] or None, RunStats)."""
+        kraus_idx = np.ascontiguousarray(kraus_idx, dtype=np.uint8)
+        ids = None if eset_ids is None else np.ascontiguousarray(eset_ids, dtype=np.uint32)
+        if final_mode not in ("exhaustive", "direct"):
+            raise ValueError(f"final_mode must be 'exhaustive' or 'direct', got {final_mode!r}")
+        k, e, c, pr, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
+        st = RunStats()
+        check(load().ptsbe_sample_nonproportional(
+            self._h, _ptr(kraus_idx), _ptr(ids), kraus_idx.shape[0], seed & (2**64 - 1), int(nonfinal_shots),
+            0 if final_mode == "exhaustive" else 1, float(threshold), int(direct_count),
+            ctypes.byref(k), ctypes.byref(e), ctypes.byref(c), ctypes.byref(pr), ctypes.byref(n), ctypes.byref(st)))
+        keys = _take(k, n.value * self.words, np.uint64).reshape(-1, self.words)
+        esets = _take(e, n.value, np.uint32)
+        counts = _take(c, n.value, np.uint64)
+        probs = _take(pr, n.value, np.float64)
+        return keys, esets, counts, (probs if final_mode == "exhaustive" else None), st
 
     def upload(self, kraus_idx, shots, eset_ids=None) -> ResidentBatch:
         return ResidentBatch(self, kraus_idx, shots, eset_ids)

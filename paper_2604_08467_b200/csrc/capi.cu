@@ -596,6 +596,18 @@ static void launch_sampler(cudaStream_t st, SampleArgs& a, int sm_count) {
     CK(cudaFuncSetAttribute(sample_group_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_set = true;
   }
+  if (a.np_mode) {
+    static bool np_attr = false;
+    if (!np_attr) {
+      CK(cudaFuncSetAttribute(nonprop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      np_attr = true;
+    }
+    const unsigned grid = (unsigned)std::min<uint64_t>(a.n_items, (uint64_t)sm_count * 16);
+    nonprop_kernel<<<grid, SAMPLE_THREADS, nb * 12, st>>>(a);
+    g_launches++;
+    CK(cudaGetLastError());
+    return;
+  }
   // Many items with few shots each: a group of 8/16/32 lanes per item.  Few items with many
   // shots (stage 1): one CTA per item so the draws spread over 128 threads.
   if (a.b <= 11 && a.n_items >= (uint64_t)sm_count * 16) {
@@ -624,7 +636,17 @@ struct Level {
   DevBuf eset, parent, prefix, mult, slot_off, rank, gid;
 };
 
+// non-proportional sampling (reference engine.py:527-576): per-stage multiplicities are not shot
+// counts but branching factors
+struct NonpropParams {
+  uint32_t nonfinal_shots;  // children per prefix in every non-final stage (distinct, weighted)
+  uint32_t final_mode;      // 0: exhaustive harvest (threshold), 1: direct multinomial of direct_count
+  uint32_t direct_count;
+  double threshold;
+};
+
 struct RunOutput {
+  DevBuf probs;  // non-proportional exhaustive mode: conditional probability tag of every record
   // final records of one chunk, device resident (level f+1): eset rows, keys, counts
   DevBuf eset, keys, counts;
   uint64_t n = 0;
@@ -634,9 +656,17 @@ struct RunOutput {
 static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* shots_dev,
                       const uint32_t* ids_dev, uint32_t ne, uint64_t chunk_shots, uint64_t seed,
                       RunOutput& out, ptsbe_run_stats* stats, unsigned long long* flag_dev,
-                      uint32_t* flag_count_dev, Workspace& ws_out) {
+                      uint32_t* flag_count_dev, Workspace& ws_out, const NonpropParams* npp = nullptr) {
   cudaStream_t st = pl->stream;
   const uint32_t f = pl->f, words = pl->words;
+  const bool np_exhaustive = npp && npp->final_mode == 0;
+  // multiplicity of the items ENTERING stage j in non-proportional mode
+  auto np_mult = [&](uint32_t j) -> uint32_t {
+    if (j < f) return npp->nonfinal_shots;
+    return np_exhaustive ? (1u << pl->sizes[f - 1]) : npp->direct_count;
+  };
+  DevBuf slot_prob;
+  if (np_exhaustive) slot_prob.alloc(chunk_shots * 8, st);
   const unsigned T = 256;
   std::vector<Level> lv(f + 2);
   std::vector<LevelDev> table(f + 2);
@@ -663,7 +693,12 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     CK(cudaMemsetAsync(l.parent.p, 0, (size_t)ne * 4, st));
     CK(cudaMemsetAsync(l.prefix.p, 0, (size_t)ne * 8 * words, st));
     CK(cudaMemsetAsync(l.rank.p, 0, (size_t)ne * 4, st));
-    CK(cudaMemcpyAsync(l.mult.p, shots_dev, (size_t)ne * 4, cudaMemcpyDeviceToDevice, st));
+    if (npp) {
+      fill_u32_kernel<<<cdiv(ne, T), T, 0, st>>>(l.mult.as<uint32_t>(), ne, np_mult(1));
+      g_launches++;
+    } else {
+      CK(cudaMemcpyAsync(l.mult.p, shots_dev, (size_t)ne * 4, cudaMemcpyDeviceToDevice, st));
+    }
     CK(cudaMemcpyAsync(l.gid.p, ids_dev, (size_t)ne * 4, cudaMemcpyDeviceToDevice, st));
     exclusive_scan<uint32_t, uint32_t>(l.mult.as<uint32_t>(), l.slot_off.as<uint32_t>(), ne,
                                        nullptr, st);
@@ -710,7 +745,8 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     // Stages whose work items carry few shots each are sampled by per-qubit descent over the
     // error set's conditional-marginal tree (descent.cuh) instead of project + sample.
     DescentShape dsh;
-    if (proj && pl->descent && j > 1 && U && (double)chunk_shots <= pl->descent_mult * (double)U)
+    if (proj && pl->descent && j > 1 && U && (double)chunk_shots <= pl->descent_mult * (double)U &&
+        (!npp || (j == f && !np_exhaustive)))  // choice without replacement / harvest need the full vector
       dsh = descent_shape(pl, progs[j - 1].d.proj_d, b);
     if (dsh.nch) {
       const Program& pr = progs[j - 1];
@@ -890,6 +926,19 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       sa.vanish_stage1 = pl->vanish_stage1;
       sa.neg_abs = pl->neg_abs;
       sa.neg_rel = pl->neg_rel;
+      sa.np_mode = 0;
+      sa.child_mult = 0;
+      sa.threshold = 0.0;
+      sa.slot_prob = nullptr;
+      if (npp && j < f) {
+        sa.np_mode = 1;
+        sa.child_mult = np_mult(j + 1);
+      } else if (np_exhaustive && j == f) {
+        sa.np_mode = 2;
+        sa.child_mult = 1;
+        sa.threshold = npp->threshold;
+        sa.slot_prob = slot_prob.as<double>();
+      }
       log.begin(&stats->sampler_ms[j - 1]);
       launch_sampler(st, sa, pl->sm_count);
       log.end();
@@ -934,6 +983,13 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       ea.b = b;
       expand_kernel<<<cdiv(Un, T), T, 0, st>>>(ea);
       g_launches++;
+      if (np_exhaustive && j == f) {
+        out.probs.alloc((size_t)Un * 8, ws_out);
+        gather_prob_kernel<<<cdiv(Un, T), T, 0, st>>>(nx.parent.as<uint32_t>(), child_base.as<uint32_t>(),
+                                                      cur.slot_off.as<uint32_t>(), slot_prob.as<double>(),
+                                                      out.probs.as<double>(), Un);
+        g_launches++;
+      }
       if (j < f) {
         nx.slot_off.alloc((size_t)Un * 4, st);
         nx.rank.alloc((size_t)Un * 4, st);
@@ -1647,6 +1703,97 @@ int ptsbe_sample(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t* shots
   ptsbe_batch_destroy(bt);
   if (e0) { cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2); cudaEventDestroy(e3); }
   return rc;
+}
+
+int ptsbe_sample_nonproportional(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t* eset_ids,
+                                 uint64_t n_sets, uint64_t seed, uint32_t nonfinal_shots,
+                                 uint32_t final_mode, double threshold, uint32_t direct_count,
+                                 uint64_t** keys, uint32_t** rec_eset, uint64_t** counts, double** probs,
+                                 uint64_t* n_records, ptsbe_run_stats* stats) {
+  ptsbe_run_stats local;
+  if (!stats) stats = &local;
+  return guarded([&] {
+    if (!pl || !keys || !rec_eset || !counts || !probs || !n_records) throw Failure(PTSBE_EINVAL, "null argument");
+    if (n_sets < 1 || n_sets >= (1ull << 31)) throw Failure(PTSBE_EINVAL, "need 1 .. 2^31 error sets");
+    if (nonfinal_shots < 1 || final_mode > 1 || (final_mode == 1 && direct_count < 1))
+      throw Failure(PTSBE_EINVAL, "non-proportional sampling needs nonfinal_shots >= 1 and a valid final mode");
+    std::lock_guard<std::mutex> lock(pl->mu);
+    CK(cudaSetDevice(pl->device));
+    cudaStream_t st = pl->stream;
+    const uint32_t f = pl->f, words = pl->words;
+    NonpropParams np{nonfinal_shots, final_mode, direct_count, threshold};
+    // slots any stage can need: items_j <= n_sets * nonfinal^(j-1), each with its multiplicity
+    double bound = 0, items = (double)n_sets;
+    for (uint32_t j = 1; j <= f; ++j) {
+      const double mult = j < f ? nonfinal_shots : (final_mode == 0 ? std::ldexp(1.0, (int)pl->sizes[f - 1]) : direct_count);
+      bound = std::max(bound, items * mult);
+      items *= nonfinal_shots;
+    }
+    if (bound >= 2147483648.0) throw Failure(PTSBE_ECAPACITY, "non-proportional run needs more than 2^31 child slots");
+    memset(stats, 0, sizeof *stats);
+    stats->first_flagged_id = -1;
+    g_launches = 0;
+    std::unique_ptr<Workspace> ws_tmp = pl->take_workspace(), ws_out = pl->take_workspace();
+    ws_tmp->reset();
+    ws_out->reset();
+    {
+      WorkspaceScope scope(ws_out.get());
+      DevBuf kraus(std::max<size_t>(16, n_sets * pl->g), st), ids(n_sets * 4, st), flag(16, st);
+      if (pl->g) CK(cudaMemcpyAsync(kraus.p, kraus_idx, n_sets * pl->g, cudaMemcpyHostToDevice, st));
+      if (eset_ids) CK(cudaMemcpyAsync(ids.p, eset_ids, n_sets * 4, cudaMemcpyHostToDevice, st));
+      else { iota_kernel<<<cdiv(n_sets, 256), 256, 0, st>>>(ids.as<uint32_t>(), (uint32_t)n_sets, 0); g_launches++; }
+      CK(cudaMemsetAsync(flag.p, 0xff, 8, st));
+      CK(cudaMemsetAsync(flag.as<unsigned char>() + 8, 0, 8, st));
+      RunOutput out;
+      cudaEvent_t e0, e1;
+      CK(cudaEventCreate(&e0));
+      CK(cudaEventCreate(&e1));
+      CK(cudaEventRecord(e0, st));
+      {
+        WorkspaceScope chunk_scope(ws_tmp.get());
+        run_chunk(pl, kraus.as<uint8_t>(), nullptr, ids.as<uint32_t>(), (uint32_t)n_sets, (uint64_t)bound, seed, out,
+                  stats, flag.as<unsigned long long>(), flag.as<uint32_t>() + 2, *ws_out, &np);
+      }
+      CK(cudaEventRecord(e1, st));
+      struct { unsigned long long first; uint32_t count; uint32_t pad; } fl;
+      CK(cudaMemcpyAsync(&fl, flag.p, 16, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      CK(cudaEventElapsedTime(&stats->loop_ms, e0, e1));
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      stats->flagged_sets = fl.count;
+      if (fl.count) {
+        stats->first_flag_kind = (uint32_t)(fl.first & 0xff);
+        stats->first_flag_stage = (uint32_t)((fl.first >> 8) & 0xff);
+        stats->first_flagged_id = (int64_t)(fl.first >> 16);
+      }
+      const uint64_t nr = out.n;
+      std::vector<uint64_t> soa(std::max<uint64_t>(nr, 1) * words);
+      std::vector<uint32_t> c32(std::max<uint64_t>(nr, 1));
+      uint64_t* k = (uint64_t*)malloc(std::max<uint64_t>(nr, 1) * 8 * words);
+      uint64_t* c = (uint64_t*)malloc(std::max<uint64_t>(nr, 1) * 8);
+      uint32_t* es = (uint32_t*)malloc(std::max<uint64_t>(nr, 1) * 4);
+      double* pr = (double*)malloc(std::max<uint64_t>(nr, 1) * 8);
+      if (!k || !c || !es || !pr) throw Failure(PTSBE_ECAPACITY, "host allocation of the records failed");
+      if (nr) {
+        CK(cudaMemcpyAsync(soa.data(), out.keys.p, nr * 8 * words, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(c32.data(), out.counts.p, nr * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(es, out.eset.p, nr * 4, cudaMemcpyDeviceToHost, st));
+        if (final_mode == 0) CK(cudaMemcpyAsync(pr, out.probs.p, nr * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      }
+      for (uint64_t i = 0; i < nr; ++i) {
+        for (uint32_t w = 0; w < words; ++w) k[i * words + w] = soa[(uint64_t)w * nr + i];
+        c[i] = c32[i];
+        if (final_mode != 0) pr[i] = -1.0;  // no tag in direct mode
+      }
+      *keys = k; *counts = c; *rec_eset = es; *probs = pr; *n_records = nr;
+      stats->n_records = nr;
+      stats->gpu_launches = g_launches;
+    }
+    pl->give_workspace(std::move(ws_tmp));
+    pl->give_workspace(std::move(ws_out));
+  });
 }
 
 int ptsbe_batch_histogram_dev(ptsbe_batch* bt, const uint64_t** keys_dev,

@@ -68,6 +68,11 @@ struct SampleArgs {
   double* set_mass;         // [error-set rows] or null (absolute guard)
   const uint32_t* eset_row; // [items] row of the item's error set in set_mass
   double vanish_stage1;     // absolute floor for the stage-1 mass itself
+  // non-proportional sampler (nonprop_kernel; reference engine.py:527-576)
+  uint32_t np_mode;         // 1: weighted choice of mult[item] distinct outcomes, 2: exhaustive harvest
+  uint32_t child_mult;      // multiplicity handed to every emitted child (slot_count)
+  double threshold;         // harvest: conditional probability an outcome must reach
+  double* slot_prob;        // harvest: conditional probability of each emitted outcome
 };
 
 constexpr int SAMPLE_THREADS = 128;
@@ -187,6 +192,156 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(const SampleArgs
       if (c) { a.slot_index[base + pos] = k; a.slot_count[base + pos] = c; ++pos; }
     }
     if (tid == 0) a.nnz[item] = tot32;
+    __syncthreads();
+  }
+}
+
+// Non-proportional sampler (reference engine.py:527-576), one CTA per work item.
+//   np_mode 1 (non-final stages): mult[item] DISTINCT outcomes, weighted, without replacement --
+//     the distribution of rng.choice(positive, size, replace=False, p) (engine.py:555) as successive
+//     draws from the remaining integer weights: draw t lands at r = floor(x_t * W_t / 2^64) in the
+//     inclusive CDF, the chosen outcome's weight is then removed from the CDF tail.  Same fixed-point
+//     weights and Philox counters as sample_kernel, so the oracle (wor_choice) reproduces the choice
+//     bit for bit from the same float64 marginals.
+//   np_mode 2 (final stage, exhaustive): every outcome whose conditional probability
+//     clamp(P_k) / mass reaches `threshold`, tagged with it (engine.py:562-568).
+// Children are emitted in ascending outcome order with slot_count = child_mult.
+__global__ void __launch_bounds__(SAMPLE_THREADS) nonprop_kernel(const SampleArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const uint32_t nb = 1u << a.b;
+  uint64_t* cdf = reinterpret_cast<uint64_t*>(sm);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(cdf + nb);
+  __shared__ uint64_t ws64[33];
+  __shared__ uint32_t ws32[33];
+  __shared__ double redmax[SAMPLE_THREADS / 32], redmin[SAMPLE_THREADS / 32], redsum[SAMPLE_THREADS / 32];
+  __shared__ uint32_t s_pick;
+  __shared__ uint64_t s_total;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t per = (nb + SAMPLE_THREADS - 1) / SAMPLE_THREADS;
+
+  for (uint64_t it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+    const uint64_t item = a.first_item + it;
+    const uint32_t m = a.mult[item];
+    double* pd = reinterpret_cast<double*>(cdf);
+    double mx = 0.0, rawmin = 1e300, csum = 0.0;
+    for (uint32_t k = tid; k < nb; k += SAMPLE_THREADS) {
+      double v = a.is_f32 ? (double)(reinterpret_cast<const float*>(a.probs) + it * nb)[k]
+                          : (reinterpret_cast<const double*>(a.probs) + it * nb)[k];
+      rawmin = fmin(rawmin, v);
+      v = v > 0.0 ? v : 0.0; pd[k] = v; mx = fmax(mx, v); csum += v;
+      cnt[k] = 0;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+      rawmin = fmin(rawmin, __shfl_xor_sync(0xffffffffu, rawmin, d));
+      csum += __shfl_xor_sync(0xffffffffu, csum, d);
+    }
+    if (lane == 0) { redmax[wid] = mx; redmin[wid] = rawmin; redsum[wid] = csum; }
+    __syncthreads();
+    mx = redmax[0]; rawmin = redmin[0]; csum = redsum[0];
+#pragma unroll
+    for (int w = 1; w < SAMPLE_THREADS / 32; ++w) {
+      mx = fmax(mx, redmax[w]); rawmin = fmin(rawmin, redmin[w]); csum += redsum[w];
+    }
+    // ---- guards (engine.py:447-448, 475-476, 484-485), as sample_kernel ----
+    uint32_t bad = 0;
+    {
+      const double ms = a.mass ? a.mass[it] : csum, mn = a.minv ? a.minv[it] : rawmin;
+      double floor_mass = a.vanish;
+      if (a.set_mass) {
+        if (a.stage == 1) { floor_mass = a.vanish_stage1; if (tid == 0) a.set_mass[a.eset_row[item]] = ms; }
+        else floor_mass = a.vanish * a.set_mass[a.eset_row[item]];
+      }
+      if (mn < a.neg_abs - a.neg_rel * ms) bad = PTSBE_ENUMERIC;
+      else if (ms < floor_mass) bad = PTSBE_EIMPOSSIBLE;
+    }
+    if (!bad && !(mx > 0.0)) bad = PTSBE_EIMPOSSIBLE;
+    if (bad) {
+      if (tid == 0) {
+        a.nnz[item] = 0;
+        atomicMin(a.flag, ((unsigned long long)a.eset_id[item] << 16) |
+                              ((unsigned long long)(a.stage & 0xff) << 8) | bad);
+        atomicAdd(a.flag_count, 1u);
+      }
+      __syncthreads();
+      continue;
+    }
+    const uint32_t k0 = tid * per;
+    const uint32_t base = a.slot_off[item];
+    if (a.np_mode == 2) {
+      // ---- exhaustive harvest: p_k = clamp(P_k) / mass >= threshold, ascending k ----
+      const double ms = a.mass ? a.mass[it] : csum;
+      uint32_t mine = 0;
+      for (uint32_t k = k0; k < k0 + per && k < nb; ++k) mine += (pd[k] / ms) >= a.threshold;
+      uint32_t tot32;
+      uint32_t pos = block_exclusive<uint32_t>(mine, ws32, &tot32);
+      for (uint32_t k = k0; k < k0 + per && k < nb; ++k) {
+        const double pk = pd[k] / ms;
+        if (pk >= a.threshold) {
+          a.slot_index[base + pos] = k;
+          a.slot_count[base + pos] = a.child_mult;
+          a.slot_prob[base + pos] = pk;
+          ++pos;
+        }
+      }
+      if (tid == 0) a.nnz[item] = tot32;
+      __syncthreads();
+      continue;
+    }
+    // ---- exact fixed-point weights and inclusive CDF, as sample_kernel ----
+    int ex;
+    frexp(mx, &ex);
+    const int shift = (62 - (int)a.b) - ex;
+    uint64_t local = 0;
+    for (uint32_t k = k0; k < k0 + per && k < nb; ++k) {
+      const uint64_t w = (uint64_t)ldexp(pd[k], shift);
+      local += w;
+      cdf[k] = w;
+    }
+    uint64_t total;
+    uint64_t run = block_exclusive<uint64_t>(local, ws64, &total);
+    for (uint32_t k = k0; k < k0 + per && k < nb; ++k) {
+      run += cdf[k];
+      cdf[k] = run;
+    }
+    if (tid == 0) s_total = total;
+    __syncthreads();
+    // ---- successive draws without replacement ----
+    const uint32_t rk = a.rank[item], es = a.eset_id[item];
+    uint32_t taken = 0;
+    for (uint32_t t = 0; t < m; ++t) {
+      const uint64_t tot = s_total;
+      if (tot == 0) break;  // fewer positive outcomes than requested (engine.py:551)
+      if (tid == 0) {
+        const Philox4 x = philox4x32_10(t, rk, a.stage, es, a.k0, a.k1);
+        const uint64_t x64 = ((uint64_t)x.v[1] << 32) | x.v[0];
+        const uint64_t r = __umul64hi(x64, tot);
+        uint32_t lo = 0, hi = nb;  // first index with cdf > r
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (cdf[mid] <= r) lo = mid + 1; else hi = mid;
+        }
+        s_pick = lo;
+      }
+      __syncthreads();
+      const uint32_t pick = s_pick;
+      const uint64_t w = cdf[pick] - (pick ? cdf[pick - 1] : 0ull);
+      __syncthreads();  // everyone has read the weight before the tail moves
+      for (uint32_t k = pick + tid; k < nb; k += SAMPLE_THREADS) cdf[k] -= w;
+      if (tid == 0) { cnt[pick] = 1; s_total = tot - w; }
+      ++taken;
+      __syncthreads();
+    }
+    // ---- ordered emission of the chosen outcomes ----
+    uint32_t mine = 0;
+    for (uint32_t k = k0; k < k0 + per && k < nb; ++k) mine += cnt[k] != 0;
+    uint32_t tot32;
+    uint32_t pos = block_exclusive<uint32_t>(mine, ws32, &tot32);
+    for (uint32_t k = k0; k < k0 + per && k < nb; ++k)
+      if (cnt[k]) { a.slot_index[base + pos] = k; a.slot_count[base + pos] = a.child_mult; ++pos; }
+    if (tid == 0) a.nnz[item] = tot32;
+    (void)taken;
     __syncthreads();
   }
 }

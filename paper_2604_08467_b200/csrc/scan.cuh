@@ -106,4 +106,19 @@ void exclusive_scan(const TI* in, TO* out, uint64_t n, TO* total_dev, cudaStream
   CK(cudaGetLastError());
 }
 
+__global__ void fill_u32_kernel(uint32_t* out, uint32_t n, uint32_t value) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = value;
+}
+
+// probability tag of child c: slot (slot_off[parent] + position of c among its parent's children)
+__global__ void gather_prob_kernel(const uint32_t* c_parent, const uint32_t* child_base,
+                                   const uint32_t* p_slot_off, const double* slot_prob, double* out,
+                                   uint32_t n) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const uint32_t p = c_parent[c];
+  out[c] = slot_prob[p_slot_off[p] + (c - child_base[p])];
+}
+
 }  // namespace ptsbe

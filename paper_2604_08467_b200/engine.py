@@ -833,6 +833,49 @@ def sample_proportional_batched(
     return out
 
 
+def sample_nonproportional_batched(
+    template: CircuitNetwork,
+    errorsets: Sequence[ErrorSet],
+    plan: BatchPlan,
+    seed: int,
+    ctx: Optional[SamplerContext] = None,
+) -> list:
+    """Data-harvesting sampling of every error set in one batched device run
+    (reference `sample_nonproportional`, engine.py:527-576): each non-final stage
+    branches every prefix into up to `plan.nonfinal_shots` distinct children
+    (weighted draw without replacement), the final stage emits every outcome
+    whose conditional probability reaches `plan.threshold` (tagged with it) or a
+    multinomial split of `plan.direct_count` shots.  One list of ShotRecord per
+    error set, in the reference's order (sorted by bitstring)."""
+    if ctx is None:
+        ctx = SamplerContext()
+    ctx.check_deadline()
+    tables = VariantTables.from_errorsets(template, errorsets)
+    pipe = DevicePipeline(template, plan, tables, ctx, shots_per_set=float(max(plan.nonfinal_shots, 1)))
+    try:
+        keys, esets, counts, probs, st = pipe.device_plan.sample_nonproportional(
+            tables.encode(errorsets), np.asarray([k.id for k in errorsets], dtype=np.uint32), seed,
+            plan.nonfinal_shots, plan.final_mode, plan.threshold, plan.direct_count)
+    finally:
+        pipe.close()
+    _account(ctx.stats, st, plan.f)
+    _raise_flagged(st)
+    strings = unpack_keys(keys, plan.n)
+    out = [[] for _ in errorsets]
+    tags = probs.tolist() if probs is not None else [None] * len(strings)
+    for s, e, c, p in zip(strings, esets.tolist(), counts.tolist(), tags):
+        out[e].append(ShotRecord(bitstring=s, count=int(c), prob=p))
+    return out
+
+
+def sample_nonproportional(template: CircuitNetwork, k: ErrorSet, plan: BatchPlan, rng,
+                           ctx: Optional[SamplerContext] = None) -> list:
+    """Single-error-set form of the reference signature (engine.py:527-533).
+    `rng` only seeds the device's counter-based streams."""
+    seed = int(rng.integers(0, 2**63 - 1)) if hasattr(rng, "integers") else int(rng)
+    return sample_nonproportional_batched(template, [k], plan, seed, ctx)[0]
+
+
 def _account(stats: EngineStats, st, f: int) -> None:
     for j in range(1, f + 1):
         stats.record_contraction(j, st.stage_ms[j - 1] * 1e-3, events=int(st.stage_events[j - 1]))
@@ -1003,10 +1046,9 @@ def run_ptsbe(c: Circuit, config: RunConfig, cache: Optional[PathCache] = None,
     warm cache), then ONE batched device run over all error sets, histogram
     merged on the device.  `errorsets` overrides the pre-sampling (the
     north-star API: pre-sampled error sets in, histogram out)."""
-    if config.mode == "ptsbe-nonproportional":
-        raise NotImplementedError("non-proportional sampling is out of scope of the B200 path (SURVEY.md 8f)")
-    if config.mode != "ptsbe-proportional":
+    if config.mode not in ("ptsbe-proportional", "ptsbe-nonproportional"):
         raise ValueError(f"run_ptsbe handles optimized modes only, got {config.mode!r}")
+    nonprop = config.mode == "ptsbe-nonproportional"
     plan = config.plan()
     if plan.n != c.n:
         raise ValueError(f"plan covers {plan.n} qubits, circuit has {c.n}")
@@ -1027,23 +1069,37 @@ def run_ptsbe(c: Circuit, config: RunConfig, cache: Optional[PathCache] = None,
     t0 = time.perf_counter()
     tables = VariantTables.from_errorsets(template, errorsets)
     shots = np.asarray([k.m for k in errorsets], dtype=np.uint32)
-    if shots.min() < 1:
+    if not nonprop and shots.min() < 1:
         raise ValueError("proportional sampling needs m >= 1")
-    pipe = DevicePipeline(template, plan, tables, ctx, shots_per_set=float(shots.mean()))
+    pipe = DevicePipeline(template, plan, tables, ctx,
+                          shots_per_set=float(plan.nonfinal_shots) if nonprop else float(shots.mean()))
     plan_s = time.perf_counter() - t0
     try:
         ctx.check_deadline()
         kraus_idx = tables.encode(errorsets)
         ids = np.asarray([k.id for k in errorsets], dtype=np.uint32)
         t0 = time.perf_counter()
-        keys, _, counts, st = pipe.device_plan.sample(kraus_idx, shots, ids, config.seed, merged=True)
+        if nonprop:
+            keys, esets, counts, probs, st = pipe.device_plan.sample_nonproportional(
+                kraus_idx, ids, config.seed, plan.nonfinal_shots, plan.final_mode, plan.threshold, plan.direct_count)
+        else:
+            keys, _, counts, st = pipe.device_plan.sample(kraus_idx, shots, ids, config.seed, merged=True)
         loop_s = time.perf_counter() - t0
     finally:
         pipe.close()
     _account(ctx.stats, st, plan.f)
     _raise_flagged(st)
     t0 = time.perf_counter()
-    records = [ShotRecord(bitstring=s, count=int(n)) for s, n in zip(unpack_keys(keys, plan.n), counts.tolist())]
+    if nonprop:
+        # per-error-set records -> merge_records (engine.py:815-829): counts summed per bitstring, the
+        # probability tag survives only if every contributor agrees
+        per_set = [[] for _ in errorsets]
+        tags = probs.tolist() if probs is not None else [None] * int(counts.size)
+        for s_, e_, n_, p_ in zip(unpack_keys(keys, plan.n), esets.tolist(), counts.tolist(), tags):
+            per_set[e_].append(ShotRecord(bitstring=s_, count=int(n_), prob=p_))
+        records = merge_records(per_set)
+    else:
+        records = [ShotRecord(bitstring=s, count=int(n)) for s, n in zip(unpack_keys(keys, plan.n), counts.tolist())]
     aggregate_s = time.perf_counter() - t0
     return RunResult(
         mode=config.mode, records=records, unique_shots=len(records),
@@ -1058,14 +1114,15 @@ def run_ptsbe(c: Circuit, config: RunConfig, cache: Optional[PathCache] = None,
         stage_events=dict(sorted(ctx.stats.stage_events.items())),
         stage_seconds=dict(sorted(ctx.stats.stage_seconds.items())),
         config=config.to_dict(), seed=config.seed, shot_allocations=[int(k.m) for k in errorsets],
-        packed_keys=keys if _keep_packed else None, packed_counts=counts if _keep_packed else None,
+        packed_keys=keys if (_keep_packed and not nonprop) else None,
+        packed_counts=counts if (_keep_packed and not nonprop) else None,
     )
 
 
 def run_mode(c: Circuit, config: RunConfig, cache: Optional[PathCache] = None) -> RunResult:
     """Dispatch by mode (engine.py:932-941).  Only the proportional PTSBE mode
     runs on the device; the comparison modes stay with the CPU reference."""
-    if config.mode == "ptsbe-proportional":
+    if config.mode in ("ptsbe-proportional", "ptsbe-nonproportional"):
         return run_ptsbe(c, config, cache=cache)
     raise NotImplementedError(
         f"mode {config.mode!r} is a CPU comparison mode of the reference and is out of scope here"
@@ -1081,6 +1138,5 @@ def _out_of_scope(name: str):
 
 
 insert_errors = _out_of_scope("insert_errors")
-sample_nonproportional = _out_of_scope("sample_nonproportional")
 sample_baseline = _out_of_scope("sample_baseline")
 sample_unoptimized_ptsbe = _out_of_scope("sample_unoptimized_ptsbe")

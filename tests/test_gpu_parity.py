@@ -406,3 +406,80 @@ def test_many_error_sets_single_shot_descent():
         pipe.close()
     assert int(counts.sum()) + 0 == sets - 0 * int(st.flagged_sets)
     assert int(st.flagged_sets) == 0
+
+
+def _nonprop_runs():
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_nonproportional.json")
+    with open(path) as fp:
+        return json.load(fp)["runs"]
+
+
+def test_nonproportional_bit_exact_vs_reference_goldens(golden_cases):
+    """Non-proportional sampler (engine.py:527-576) on the device, complex128,
+    against the records of the UNMODIFIED reference driven by the counter-based
+    shim: same chosen prefixes, same harvested outcomes in the same order,
+    probability tags within 1e-11, direct-mode counts identical."""
+    from paper_2604_08467_b200.engine import sample_nonproportional_batched
+
+    n_records = 0
+    for run in _nonprop_runs():
+        case = golden_cases[run["case"]]
+        c, sizes, es = case_objects(case)
+        var = run["variant"]
+        plan = BatchPlan(sizes, nonfinal_shots=var["nonfinal_shots"], final_mode=var["final_mode"],
+                         threshold=var["threshold"], direct_count=var["direct_count"])
+        tpl = CircuitNetwork.from_circuit(c)
+        got = sample_nonproportional_batched(tpl, es, plan, run["seed"], SamplerContext(hypersamples=4, dtype="complex128"))
+        for recs, want in zip(got, run["records"]):
+            assert [(r.bitstring, r.count) for r in recs] == [(s, n) for s, n, _ in want], (run["case"], var)
+            for r, (_, _, q) in zip(recs, want):
+                assert (r.prob is None) == (q is None)
+                if q is not None:
+                    assert abs(r.prob - q) <= 1e-11
+            n_records += len(recs)
+    assert n_records >= 1000
+
+
+def test_nonproportional_exhaustive_set_equality_complex64(golden_cases):
+    """Reference acceptance criterion 4 (tests/test_acceptance.py:134-153): with a
+    single batch covering the register the exhaustive output equals
+    {s : p(s) >= tau}.  complex64: outcomes within 1e-5 of the threshold may fall
+    on either side; everything else must match, tags within 1e-5."""
+    from paper_2604_08467_b200.engine import sample_nonproportional_batched
+
+    for name in ("random_0", "random_2", "random_4", "hea8", "qaoa8"):
+        c, _, es = case_objects(golden_cases[name])
+        tpl = CircuitNetwork.from_circuit(c)
+        tau = 1e-3
+        plan = BatchPlan((c.n,), final_mode="exhaustive", threshold=tau)
+        got = sample_nonproportional_batched(tpl, es, plan, 5, SamplerContext(hypersamples=4, dtype="complex64"))
+        for k, recs in zip(es, got):
+            mops, finals = bridge.merged_ops(c, k.realized)
+            p = O.conditional_marginal(mops, finals, (c.n,), 1, "")
+            sure = {format(i, f"0{c.n}b") for i in np.flatnonzero(p >= tau * (1 + 1e-4))}
+            maybe = {format(i, f"0{c.n}b") for i in np.flatnonzero(p >= tau * (1 - 1e-4))}
+            have = {r.bitstring for r in recs}
+            assert sure <= have <= maybe
+            for r in recs:
+                assert abs(r.prob - p[int(r.bitstring, 2)]) <= 1e-5 * p.max()
+
+
+def test_run_ptsbe_nonproportional_mode():
+    """run_ptsbe(mode='ptsbe-nonproportional'): records merged over error sets
+    (engine.py:815-829), plan events = f, one contraction per prefix."""
+    c, _ = workloads.hea(8, 3, gamma=0.0, p=0.05, seed=21)
+    cfg = RunConfig(n=8, g=len(c.gates), mode="ptsbe-nonproportional", batch_sizes=(3, 3, 2), error_sets=6,
+                    total_shots=6, nonfinal_shots=2, final_mode="exhaustive", tau=1e-2, seed=3, hypersamples=4)
+    res = run_ptsbe(c, cfg)
+    assert res.plan_events == 3 and res.records
+    assert [r.bitstring for r in res.records] == sorted(r.bitstring for r in res.records)
+    assert res.stage_events[1] == 6 and res.stage_events[2] <= 12 and res.stage_events[3] <= 24
+    again = run_ptsbe(c, cfg)
+    assert [(r.bitstring, r.count, r.prob) for r in again.records] == [(r.bitstring, r.count, r.prob) for r in res.records]
+    direct = run_ptsbe(c, RunConfig(n=8, g=len(c.gates), mode="ptsbe-nonproportional", batch_sizes=(3, 3, 2),
+                                    error_sets=6, total_shots=6, nonfinal_shots=1, final_mode="direct",
+                                    direct_count=7, seed=3, hypersamples=4))
+    assert direct.total_count == 6 * 7
