@@ -268,6 +268,94 @@ def reference_arm(args):
     }))
 
 
+def _np_cpu_worker(job):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import bridge
+    from oracle import ptsbe_oracle as O
+    from paper_2604_08467_b200 import workloads
+
+    c, sizes, rows, ids, seed, nonfinal, tau, paths = job
+    ops, finals = bridge.template_of(c)
+    es = workloads.errorsets_from_matrix(c, rows, 1)
+    n = 0
+    for k, gid in zip(es, ids):
+        merged = O.merge_errors(ops, bridge.realized_operators(c, k.realized))
+        try:
+            n += len(O.sample_nonproportional(merged, finals, sizes, seed, int(gid), nonfinal_shots=nonfinal,
+                                              final_mode="exhaustive", threshold=tau, paths=paths))
+        except O.ImpossiblePrefix:
+            pass
+    return n
+
+
+def nonproportional_bench(args):
+    """Data-harvesting mode (non-proportional NBS, exhaustive final stage): records per second through the
+    host-buffer C-ABI call ptsbe_sample_nonproportional (H2D of the Kraus-index matrix and D2H of the records
+    inside the timed region), next to the oracle port on the host cores.  Throughput is counted the way the
+    reference counts it for this mode: harvested bitstrings / loop seconds (reference bench.py:40-46)."""
+    import multiprocessing as mp
+
+    from paper_2604_08467_b200 import _capi
+    from paper_2604_08467_b200.engine import (BatchPlan, CircuitNetwork, DevicePipeline, SamplerContext,
+                                              VariantTables, marginal_network)
+    from paper_2604_08467_b200.planner import find_path_greedy
+
+    c, sizes, sets, _, dtype, label = build_workload(args.workload, args)
+    cores = os.cpu_count() or 1
+    # CPU leg first (before CUDA is touched): a bounded sample of the same workload
+    cpu = None
+    if not args.no_cpu:
+        tpl, bp = CircuitNetwork.from_circuit(c), BatchPlan(sizes)
+        paths = [list(find_path_greedy(marginal_network(tpl, bp, j, "0" * bp.offset(j)).net, hypersamples=100,
+                                       rng=np.random.default_rng([args.seed, j])).steps) for j in range(1, bp.f + 1)]
+        n_cpu = args.cpu_sets or 8 * cores
+        rows = error_matrix(c, n_cpu, 0, args.seed)
+        jobs = [(c, sizes, rows[r::cores], np.arange(n_cpu)[r::cores], args.seed, args.nonfinal_shots, args.tau, paths)
+                for r in range(min(cores, n_cpu))]
+        t0 = time.perf_counter()
+        with mp.get_context("fork").Pool(len(jobs)) as pool:
+            got = sum(pool.map(_np_cpu_worker, jobs))
+        wall = time.perf_counter() - t0
+        cpu = {"value": got / wall, "unit": "bitstrings/s", "cores": len(jobs), "kind": "port",
+               "sample": f"{n_cpu} error sets of the same circuit/plan, {wall:.1f} s wall"}
+    if _capi.device_count() < 1:
+        raise SystemExit("bench.py needs a CUDA device: libptsbe_b200 has no CPU fallback")
+    tpl = CircuitNetwork.from_circuit(c)
+    tables = VariantTables.from_channels(tpl)
+    ctx = SamplerContext(hypersamples=args.hypersamples, planner_seed=args.seed, dtype=dtype)
+    plan = BatchPlan(sizes, nonfinal_shots=args.nonfinal_shots, final_mode="exhaustive", threshold=args.tau)
+    pipe = DevicePipeline(tpl, plan, tables, ctx, shots_per_set=float(args.nonfinal_shots))
+    dp = pipe.device_plan
+    kraus = error_matrix(c, sets, 0, args.seed)
+    ids = np.arange(sets, dtype=np.uint32)
+    for w in range(max(args.warmup, 1)):
+        dp.sample_nonproportional(kraus, ids, args.seed - 1 - w, args.nonfinal_shots, "exhaustive", args.tau, 1)
+    t0 = time.perf_counter()
+    n_rec, dev_ms, launches = 0, 0.0, 0
+    for i in range(args.steps):
+        keys, _, counts, probs, st = dp.sample_nonproportional(kraus, ids, args.seed + i, args.nonfinal_shots,
+                                                               "exhaustive", args.tau, 1)
+        n_rec += int(counts.size)
+        dev_ms += float(st.loop_ms)
+        launches += int(st.gpu_launches)
+    wall = time.perf_counter() - t0
+    f = len(sizes)
+    print(json.dumps({
+        "metric": "harvested bitstrings/sec (non-proportional NBS, exhaustive final stage)", "mode": "nonproportional",
+        "value": n_rec / (dev_ms * 1e-3), "unit": "bitstrings/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c64 (f32 FMA)" if dtype == "complex64" else "c128 (f64 FMA)", "data": "synthetic",
+        "config": {"workload": label, "plan": list(sizes), "error_sets_per_gpu": sets,
+                   "nonfinal_shots": args.nonfinal_shots, "tau": args.tau},
+        "e2e": {"value": n_rec / wall, "unit": "bitstrings/s", "h2d_bytes_per_step": int(kraus.nbytes + ids.nbytes),
+                "d2h_bytes_per_step": int((n_rec // args.steps) * (8 * dp.words + 8 + 8 + 4))},
+        "gpu_launches": launches, "records_per_step": n_rec // args.steps,
+        "stage_events": [int(st.stage_events[j]) for j in range(f)], "flagged_work_items": int(st.flagged_sets),
+        "cpu_baseline": cpu,
+    }))
+    pipe.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -285,8 +373,14 @@ def main():
     ap.add_argument("--cpu-shots", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="proportional", choices=["proportional", "nonproportional"],
+                    help="nonproportional: data-harvesting mode (reference engine.py:527-576), SURVEY 8f #1")
+    ap.add_argument("--nonfinal-shots", type=int, default=1)
+    ap.add_argument("--tau", type=float, default=1e-4)
     args = ap.parse_args()
 
+    if args.mode == "nonproportional":
+        return nonproportional_bench(args)
     if args.impl == "reference":
         return reference_arm(args)
 
