@@ -15,8 +15,8 @@
 //
 // lane_descent_kernel additionally keeps the item's last intermediate on chip:
 // the final step (the one that produces the projection vector v) is evaluated by
-// the 8-lane group that draws from it, straight into registers, so v never exists
-// in memory.  A draw is the unit of work of the descent phase (no loop over an
+// the LN_GS-lane group that draws from it, straight into registers, so v never
+// exists in memory.  A draw is the unit of work of the descent phase (no loop over an
 // item's multiplicity, no idle groups next to a high-multiplicity item); the raw
 // per-draw outcomes are merged into ordered (outcome, count) pairs by
 // dedup_kernel afterwards.
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(LN_THREADS) exec_lane_kernel(const LaneArgs a)
 }
 
 // ---------------------------------------------------------------------------
-// fused: per-item steps (thread per item) + per-qubit descent (8 lanes per draw)
+// fused: per-item steps (thread per item) + per-qubit descent (LN_GS lanes per draw)
 // ---------------------------------------------------------------------------
 struct LaneDescentArgs {
   LaneArgs l;               // l.e.out unused; the last step of the program produces v
@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
   const LaneStep last = lane_decode(cx.steps, cx.tables, e.n_steps - 1);
 
   // v of the item in warp slot i, distributed over this group's lanes: lane holds the 16-byte
-  // chunks {k * 8 + lane}, i.e. elements CPC * (k * 8 + lane) + {0, CPC - 1}.
+  // chunks {k * LN_GS + lane}, i.e. elements CPC * (k * LN_GS + lane) + {0, CPC - 1}.
   // Common case (v = x (x) conj(x): one multiply per element, no slice): the gather offsets of
   // this lane's elements do not depend on the item -- resolved once per kernel.
   const bool fast_last = HERM || (last.kn == 1 && !(last.flags & 4u) && last.hi_n == 1);
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
         cum_s[tid] = incl;
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
         __syncwarp();
-        // ---- phase B: one (item, draw) per 8-lane group and round.  Rounds [0, item_rounds): the
+        // ---- phase B: one (item, draw) per LN_GS-lane group and round.  Rounds [0, item_rounds): the
         // warp's items in order -- v, mass (guards as descent.cuh) and draw 0; later rounds: the
         // remaining draws of multi-shot items, v recomputed, mass from shared memory ----
         const uint32_t n_live = min(32u, end - w0);
