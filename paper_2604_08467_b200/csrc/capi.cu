@@ -587,6 +587,15 @@ static void launch_project(ptsbe_plan* pl, const Program& pr, const void* v, uin
 static void launch_sampler(cudaStream_t st, SampleArgs& a, int sm_count) {
   if (a.n_items == 0) return;
   const size_t nb = 1ull << a.b;
+  if (a.np_mode == 2 && nb * 12 > 160 * 1024) {
+    // exhaustive harvest of a population vector beyond shared memory: streamed from global memory
+    if (a.b > 30) throw Failure(PTSBE_ECAPACITY, "exhaustive harvest supports final batches of at most 30 qubits");
+    const unsigned grid = (unsigned)std::min<uint64_t>(a.n_items, (uint64_t)sm_count * 8);
+    harvest_big_kernel<<<grid, SAMPLE_THREADS, 0, st>>>(a);
+    g_launches++;
+    CK(cudaGetLastError());
+    return;
+  }
   if (a.b > 14) throw Failure(PTSBE_ECAPACITY, "sampler supports stage batches of at most 14 qubits");
   static bool attr_set = false;
   if (!attr_set) {

@@ -346,6 +346,97 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) nonprop_kernel(const SampleArg
   }
 }
 
+// Exhaustive harvest over a population vector that does not fit shared memory (final batches of
+// 14-26 qubits: the data-harvesting regime of the paper).  One CTA per work item
+// streams the 2^b reals twice: mass / minimum, then ordered threshold compaction in tiles of
+// HB_TILE entries (each thread owns HB_PER consecutive entries of a tile, a block scan gives its
+// output position).  Purely bandwidth-bound: 2 x 2^b x sizeof(real) read, 16 B per harvested record.
+constexpr int HB_PER = 8;
+constexpr int HB_TILE = SAMPLE_THREADS * HB_PER;
+
+__global__ void __launch_bounds__(SAMPLE_THREADS) harvest_big_kernel(const SampleArgs a) {
+  const uint64_t nb = 1ull << a.b;
+  __shared__ uint32_t ws32[33];
+  __shared__ double redmin[SAMPLE_THREADS / 32], redsum[SAMPLE_THREADS / 32];
+  __shared__ uint32_t s_base;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (uint64_t it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+    const uint64_t item = a.first_item + it;
+    const float* pf = reinterpret_cast<const float*>(a.probs) + it * nb;
+    const double* pdb = reinterpret_cast<const double*>(a.probs) + it * nb;
+    auto at = [&](uint64_t k) -> double { return a.is_f32 ? (double)pf[k] : pdb[k]; };
+    double rawmin = 1e300, csum = 0.0;
+    for (uint64_t k = tid; k < nb; k += SAMPLE_THREADS) {
+      double v = at(k);
+      rawmin = fmin(rawmin, v);
+      csum += v > 0.0 ? v : 0.0;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      rawmin = fmin(rawmin, __shfl_xor_sync(0xffffffffu, rawmin, d));
+      csum += __shfl_xor_sync(0xffffffffu, csum, d);
+    }
+    if (lane == 0) { redmin[wid] = rawmin; redsum[wid] = csum; }
+    __syncthreads();
+    rawmin = redmin[0]; csum = redsum[0];
+#pragma unroll
+    for (int w = 1; w < SAMPLE_THREADS / 32; ++w) { rawmin = fmin(rawmin, redmin[w]); csum += redsum[w]; }
+    const double ms = a.mass ? a.mass[it] : csum, mn = a.minv ? a.minv[it] : rawmin;
+    uint32_t bad = 0;
+    {
+      double floor_mass = a.vanish;
+      if (a.set_mass) {
+        if (a.stage == 1) { floor_mass = a.vanish_stage1; if (tid == 0) a.set_mass[a.eset_row[item]] = ms; }
+        else floor_mass = a.vanish * a.set_mass[a.eset_row[item]];
+      }
+      if (mn < a.neg_abs - a.neg_rel * ms) bad = PTSBE_ENUMERIC;
+      else if (ms < floor_mass || !(ms > 0.0)) bad = PTSBE_EIMPOSSIBLE;
+    }
+    if (bad) {
+      if (tid == 0) {
+        a.nnz[item] = 0;
+        atomicMin(a.flag, ((unsigned long long)a.eset_id[item] << 16) |
+                              ((unsigned long long)(a.stage & 0xff) << 8) | bad);
+        atomicAdd(a.flag_count, 1u);
+      }
+      __syncthreads();
+      continue;
+    }
+    if (tid == 0) s_base = 0;
+    __syncthreads();
+    const uint32_t base = a.slot_off[item];
+    for (uint64_t t0 = 0; t0 < nb; t0 += HB_TILE) {
+      const uint64_t k0 = t0 + (uint64_t)tid * HB_PER;
+      double pk[HB_PER];
+      uint32_t mine = 0;
+#pragma unroll
+      for (int i = 0; i < HB_PER; ++i) {
+        const uint64_t k = k0 + i;
+        double v = k < nb ? at(k) : 0.0;
+        v = v > 0.0 ? v / ms : 0.0;
+        pk[i] = v;
+        mine += (k < nb && v >= a.threshold);
+      }
+      uint32_t tot32;
+      uint32_t pos = s_base + block_exclusive<uint32_t>(mine, ws32, &tot32);
+#pragma unroll
+      for (int i = 0; i < HB_PER; ++i) {
+        if (k0 + i < nb && pk[i] >= a.threshold) {
+          a.slot_index[base + pos] = (uint32_t)(k0 + i);
+          a.slot_count[base + pos] = a.child_mult;
+          a.slot_prob[base + pos] = pk[i];
+          ++pos;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) s_base += tot32;
+      __syncthreads();
+    }
+    if (tid == 0) a.nnz[item] = s_base;
+    __syncthreads();
+  }
+}
+
 // Group-per-item variant for nb <= 2048 (b <= 11): same arithmetic, same results as
 // sample_kernel, but no block-wide barriers.  GS lanes (8, 16 or 32) serve one item, 32 / GS
 // items per warp in lockstep.  Each lane owns the nb/GS CONSECUTIVE outcomes

@@ -483,3 +483,32 @@ def test_run_ptsbe_nonproportional_mode():
                                     error_sets=6, total_shots=6, nonfinal_shots=1, final_mode="direct",
                                     direct_count=7, seed=3, hypersamples=4))
     assert direct.total_count == 6 * 7
+
+
+def test_nonproportional_exhaustive_large_final_batch():
+    """Final batch beyond the shared-memory sampler (2^16 outcomes, harvest_big_kernel):
+    the harvested set equals {s : p(s) >= tau} of the oracle's full distribution,
+    tags within 1e-11 (complex128), for a single stage and for a (2, 14) plan."""
+    from paper_2604_08467_b200.engine import sample_nonproportional_batched
+
+    c, _ = workloads.hea(16, 3, gamma=0.0, p=0.03, seed=5)
+    es = presample_errors(c, 3, "uniform", shots_per_set=1, rng=np.random.default_rng(8))
+    tpl = CircuitNetwork.from_circuit(c)
+    tau = 2e-5
+    got = sample_nonproportional_batched(tpl, es, BatchPlan((16,), final_mode="exhaustive", threshold=tau), 1,
+                                         SamplerContext(hypersamples=8, dtype="complex128"))
+    for k, recs in zip(es, got):
+        mops, finals = bridge.merged_ops(c, k.realized)
+        p = O.conditional_marginal(mops, finals, (16,), 1, "")
+        want = np.flatnonzero(p >= tau)
+        assert [int(r.bitstring, 2) for r in recs] == want.tolist()
+        assert max(abs(r.prob - p[int(r.bitstring, 2)]) for r in recs) <= 1e-11
+    # two stages: one chosen 2-bit prefix per error set, then a 2^14 harvest conditioned on it
+    got2 = sample_nonproportional_batched(tpl, es, BatchPlan((2, 14), final_mode="exhaustive", threshold=1e-4), 4,
+                                          SamplerContext(hypersamples=8, dtype="complex128"))
+    for k, recs in zip(es, got2):
+        assert recs and len({r.bitstring[:2] for r in recs}) == 1
+        mops, finals = bridge.merged_ops(c, k.realized)
+        cond = O.conditional_marginal(mops, finals, (2, 14), 2, recs[0].bitstring[:2])
+        assert [int(r.bitstring[2:], 2) for r in recs] == np.flatnonzero(cond >= 1e-4).tolist()
+        assert max(abs(r.prob - cond[int(r.bitstring[2:], 2)]) for r in recs) <= 1e-11
