@@ -75,6 +75,11 @@ def build_workload(name: str, args):
         c, _ = workloads.qaoa(12, 2, p=1e-3, seed=4)
         sizes = (5, 5, 2)
         dflt = dict(sets=2_000, shots=10_000, dtype="complex128", label="cfg4 twin: 12-qubit QAOA p=2, 3-regular")
+    elif name == "harvest24":
+        # data-harvesting showcase for --mode nonproportional: 24-qubit HEA depth 4, final batch of 20 qubits
+        c, _ = workloads.hea(24, 4, gamma=0.0, p=0.01, seed=3)
+        sizes = (4, 20)
+        dflt = dict(sets=64, shots=1, dtype="complex64", label="24-qubit HEA depth 4, 2q depolarizing 0.01, final batch 20 qubits")
     elif name == "cfg5":
         c, _ = workloads.random40(40, 400, seed=5)
         sizes = (10, 6, 6, 6, 6, 6)  # best of a sweep; 6-qubit stages keep the descent tree in shared memory
@@ -171,7 +176,7 @@ def cpu_sample_size(name: str):
     """(error sets, shots per set) of the bounded CPU sample: about 10-30 s of
     host work for the whole pool."""
     return {"cfg1": (64, 1000), "cfg2": (None, 24), "cfg3": (None, 1), "cfg4": (None, 8),
-            "cfg5": (None, 20), "cfg3s": (64, 1), "cfg4s": (None, 50)}[name]
+            "cfg5": (None, 20), "cfg3s": (64, 1), "cfg4s": (None, 50), "harvest24": (None, 1)}[name]
 
 
 # --------------------------------------------------------------------------
@@ -362,7 +367,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfg3s", "cfg4s"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfg3s", "cfg4s", "harvest24"])
     ap.add_argument("--sets", type=int, default=0, help="error sets PER GPU")
     ap.add_argument("--shots", type=int, default=0, help="shots per error set")
     ap.add_argument("--plan", default="", help="comma-separated batch sizes")
