@@ -590,8 +590,8 @@ static void launch_sampler(cudaStream_t st, SampleArgs& a, int sm_count) {
   if (a.np_mode == 2 && nb * 12 > 160 * 1024) {
     // exhaustive harvest of a population vector beyond shared memory: streamed from global memory
     if (a.b > 30) throw Failure(PTSBE_ECAPACITY, "exhaustive harvest supports final batches of at most 30 qubits");
-    const unsigned grid = (unsigned)std::min<uint64_t>(a.n_items, (uint64_t)sm_count * 8);
-    harvest_big_kernel<<<grid, SAMPLE_THREADS, 0, st>>>(a);
+    const unsigned grid = (unsigned)std::min<uint64_t>(a.n_items, (uint64_t)sm_count * 2);
+    harvest_big_kernel<<<grid, HB_THREADS, 0, st>>>(a);
     g_launches++;
     CK(cudaGetLastError());
     return;

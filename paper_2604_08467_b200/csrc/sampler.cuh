@@ -351,13 +351,14 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) nonprop_kernel(const SampleArg
 // streams the 2^b reals twice: mass / minimum, then ordered threshold compaction in tiles of
 // HB_TILE entries (each thread owns HB_PER consecutive entries of a tile, a block scan gives its
 // output position).  Purely bandwidth-bound: 2 x 2^b x sizeof(real) read, 16 B per harvested record.
+constexpr int HB_THREADS = 1024;  // one big CTA per item: 32 warps of loads in flight on its SM
 constexpr int HB_PER = 8;
-constexpr int HB_TILE = SAMPLE_THREADS * HB_PER;
+constexpr int HB_TILE = HB_THREADS * HB_PER;
 
-__global__ void __launch_bounds__(SAMPLE_THREADS) harvest_big_kernel(const SampleArgs a) {
+__global__ void __launch_bounds__(HB_THREADS) harvest_big_kernel(const SampleArgs a) {
   const uint64_t nb = 1ull << a.b;
   __shared__ uint32_t ws32[33];
-  __shared__ double redmin[SAMPLE_THREADS / 32], redsum[SAMPLE_THREADS / 32];
+  __shared__ double redmin[HB_THREADS / 32], redsum[HB_THREADS / 32];
   __shared__ uint32_t s_base;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (uint64_t it = blockIdx.x; it < a.n_items; it += gridDim.x) {
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) harvest_big_kernel(const Sampl
     const double* pdb = reinterpret_cast<const double*>(a.probs) + it * nb;
     auto at = [&](uint64_t k) -> double { return a.is_f32 ? (double)pf[k] : pdb[k]; };
     double rawmin = 1e300, csum = 0.0;
-    for (uint64_t k = tid; k < nb; k += SAMPLE_THREADS) {
+    for (uint64_t k = tid; k < nb; k += HB_THREADS) {
       double v = at(k);
       rawmin = fmin(rawmin, v);
       csum += v > 0.0 ? v : 0.0;
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) harvest_big_kernel(const Sampl
     __syncthreads();
     rawmin = redmin[0]; csum = redsum[0];
 #pragma unroll
-    for (int w = 1; w < SAMPLE_THREADS / 32; ++w) { rawmin = fmin(rawmin, redmin[w]); csum += redsum[w]; }
+    for (int w = 1; w < HB_THREADS / 32; ++w) { rawmin = fmin(rawmin, redmin[w]); csum += redsum[w]; }
     const double ms = a.mass ? a.mass[it] : csum, mn = a.minv ? a.minv[it] : rawmin;
     uint32_t bad = 0;
     {

@@ -512,3 +512,18 @@ def test_nonproportional_exhaustive_large_final_batch():
         cond = O.conditional_marginal(mops, finals, (2, 14), 2, recs[0].bitstring[:2])
         assert [int(r.bitstring[2:], 2) for r in recs] == np.flatnonzero(cond >= 1e-4).tolist()
         assert max(abs(r.prob - cond[int(r.bitstring[2:], 2)]) for r in recs) <= 1e-11
+
+
+def test_batch_time_curve_rows():
+    """Device counterpart of the reference's bench.batch_time_curve (bench.py:287-331):
+    one row per feasible b with the reference's keys; est_cost grows with b."""
+    from paper_2604_08467_b200.bench_tools import batch_time_curve
+    from paper_2604_08467_b200.circuits import random_circuit
+
+    c = random_circuit(10, 40, rng=np.random.default_rng(3))
+    rows = batch_time_curve(c, [2, 5, 10, 12], hypersamples=4, reps=2, batch=64)
+    assert [r["b"] for r in rows] == [2, 5, 10]
+    for r in rows:
+        assert {"b", "stage_seconds", "per_qubit_seconds", "path_seconds", "est_cost", "reps"} <= set(r)
+        assert r["stage_seconds"] > 0 and r["per_qubit_seconds"] == pytest.approx(r["stage_seconds"] / r["b"])
+    assert rows[-1]["est_cost"] > rows[0]["est_cost"]
