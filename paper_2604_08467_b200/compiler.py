@@ -35,7 +35,7 @@ MEMO_NONE = 0xFFFF         # "operand is not produced by a step of this program"
 MEMO_MIN_STEPS = 48        # class-0 programs at least this long get a variant-0 memo
 LO_TABLE_MAX = 1024          # entries in the per-lane (low) gather table of a step
 SMEM_BYTES = 52 * 1024       # shared-memory arena of a CTA-per-item program: 4 CTAs per SM stay resident
-WARP_ARENA_BYTES = 6 * 1024  # beyond this a warp-per-item mapping starves occupancy
+WARP_ARENA_BYTES = 16 * 1024  # beyond this a warp-per-item mapping starves occupancy (8 warps x 16 KB = 2 CTAs per SM)
 
 
 @dataclass
@@ -367,7 +367,7 @@ def compile_stage(
         # sizing of the on-chip arena: try everything on chip, spill the big buffers otherwise
         max_out = max([nodes[nid].size for nid in mine], default=1)
         peak = _place(nodes, mine, rec_off, lambda x: storage_of(x)[0], fast_cap=None)[1]
-        if max_out <= 512 and peak * elem_bytes <= WARP_ARENA_BYTES:
+        if max_out <= 1024 and peak * elem_bytes <= WARP_ARENA_BYTES:
             # sub-warp groups: GS lanes per item, 32 / GS items per warp in lockstep.  Pick the
             # group size with the fewest issued warp-instructions per item (rough model of
             # csrc/executor.cuh: per step ~80, per output ~10, per multiply-add ~8).
