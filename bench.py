@@ -378,6 +378,8 @@ def main():
     ap.add_argument("--cpu-shots", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--device-presample", action="store_true",
+                    help="draw the error sets on the device (ptsbe_batch_presample) for the device-timed leg")
     ap.add_argument("--mode", default="proportional", choices=["proportional", "nonproportional"],
                     help="nonproportional: data-harvesting mode (reference engine.py:527-576), SURVEY 8f #1")
     ap.add_argument("--nonfinal-shots", type=int, default=1)
@@ -433,7 +435,13 @@ def main():
     pipe = DevicePipeline(tpl, BatchPlan(sizes), tables, ctx, shots_per_set=float(shots))
     plan_s = time.perf_counter() - t0
     dp = pipe.device_plan
-    batch = dp.upload(kraus, shots_arr, ids)
+    if args.device_presample:
+        # error sets [first, first + sets) drawn on the device from the channel probabilities
+        site_probs = [[pr for _, pr in g.noise.outcomes()] for g in c.gates]
+        batch = dp.presample(site_probs, sets, first, shots, args.seed)
+        kraus = batch.kraus(sets, len(c.gates))  # the host-buffer leg below replays the same error sets
+    else:
+        batch = dp.upload(kraus, shots_arr, ids)
 
     def sync_all():
         torch.cuda.synchronize()
@@ -615,6 +623,7 @@ def main():
             "dtype": "c64 (f32 FMA)" if dtype == "complex64" else "c128 (f64 FMA)", "data": "synthetic",
             "config": {"workload": label, "plan": list(sizes), "error_sets_per_gpu": sets, "shots_per_set": shots,
                        "gates": len(c.gates), "hypersamples": args.hypersamples, "plan_s": round(plan_s, 3),
+                       "error_sets_from": "device pre-sampling" if args.device_presample else "host matrix",
                        "l2": "per-step working set (work lists, hoisted records, population vectors) exceeds the 126 MB L2"
                              if total_shots_local * 8 > 126e6 else "working set below L2 size (small workload)",
                        "parallelism": f"error sets sharded over {world} GPU(s), weak scaling"},

@@ -222,6 +222,17 @@ int ptsbe_sample_nonproportional(ptsbe_plan* plan, const uint8_t* kraus_idx, con
 typedef struct ptsbe_batch ptsbe_batch;
 int ptsbe_batch_upload(ptsbe_plan* plan, const uint8_t* kraus_idx, const uint32_t* shots,
                        const uint32_t* eset_ids, uint64_t n_sets, ptsbe_batch** out);
+/* replaces: presample_errors / draw_realization (engine.py:232-281) for a uniform allocation of
+ * shots_per_set shots: the Kraus-index matrix of error sets [first_id, first_id + n_sets) is drawn ON THE
+ * DEVICE from the per-site outcome distributions and becomes a resident batch (no uint8[E][g] upload).
+ *   site_off [g + 1], site_cdf [site_off[g]]: inclusive cumulative outcome probabilities per site
+ *   (outcome 0 = no error, same order as the variant tables of the plan).
+ *   uniform of (error set id, site): Philox counter (site, id, 'PRES', 0), key = seed. */
+int ptsbe_batch_presample(ptsbe_plan* plan, const double* site_cdf, const uint32_t* site_off,
+                          uint64_t n_sets, uint32_t first_id, uint32_t shots_per_set, uint64_t seed,
+                          ptsbe_batch** out);
+/* copy the Kraus-index matrix [n_sets][g] of a resident batch to the host (caller-allocated) */
+int ptsbe_batch_kraus(ptsbe_batch* batch, uint8_t* out_host);
 int ptsbe_batch_run(ptsbe_batch* batch, uint64_t seed, uint64_t* n_records,
                     ptsbe_run_stats* stats);
 /* copy the histogram of the last run to the host (library-allocated) */

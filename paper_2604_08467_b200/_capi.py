@@ -28,7 +28,7 @@ EXPORTS = (
     "ptsbe_sample", "ptsbe_batch_upload", "ptsbe_batch_run", "ptsbe_batch_fetch",
     "ptsbe_batch_destroy", "ptsbe_histogram_merge", "ptsbe_plan_greedy", "ptsbe_free",
     "ptsbe_batch_histogram_dev", "ptsbe_histogram_merge_dev", "ptsbe_free_dev",
-    "ptsbe_measure_fma_peak", "ptsbe_sample_nonproportional",
+    "ptsbe_measure_fma_peak", "ptsbe_sample_nonproportional", "ptsbe_batch_presample", "ptsbe_batch_kraus",
 )
 
 
@@ -96,6 +96,8 @@ def load() -> ctypes.CDLL:
                                                  ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P),
                                                  ctypes.POINTER(P), ctypes.POINTER(U64), ctypes.POINTER(RunStats)]
     lib.ptsbe_batch_upload.argtypes = [P, P, P, P, U64, ctypes.POINTER(P)]
+    lib.ptsbe_batch_presample.argtypes = [P, P, P, U64, U32, U32, U64, ctypes.POINTER(P)]
+    lib.ptsbe_batch_kraus.argtypes = [P, P]
     lib.ptsbe_batch_run.argtypes = [P, U64, ctypes.POINTER(U64), ctypes.POINTER(RunStats)]
     lib.ptsbe_batch_fetch.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(U64)]
     lib.ptsbe_batch_destroy.argtypes = [P]
@@ -194,6 +196,8 @@ class ResidentBatch:
     def __init__(self, plan: "DevicePlan", kraus_idx, shots, eset_ids):
         self.plan = plan
         self._h = ctypes.c_void_p()
+        if kraus_idx is None:  # filled in by DevicePlan.presample
+            return
         kraus_idx = np.ascontiguousarray(kraus_idx, dtype=np.uint8)
         shots = np.ascontiguousarray(shots, dtype=np.uint32)
         ids = None if eset_ids is None else np.ascontiguousarray(eset_ids, dtype=np.uint32)
@@ -205,6 +209,12 @@ class ResidentBatch:
         n = ctypes.c_uint64()
         check(load().ptsbe_batch_run(self._h, seed & (2**64 - 1), ctypes.byref(n), ctypes.byref(st)))
         return int(n.value), st
+
+    def kraus(self, n_sets: int, g: int) -> np.ndarray:
+        """Kraus-index matrix [n_sets, g] of this batch (device-side pre-sampling: what was drawn)."""
+        out = np.empty((n_sets, g), dtype=np.uint8)
+        check(load().ptsbe_batch_kraus(self._h, _ptr(out)))
+        return out
 
     def fetch(self) -> tuple[np.ndarray, np.ndarray]:
         k, c, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
@@ -306,6 +316,18 @@ class DevicePlan:
         counts = _take(c, n.value, np.uint64)
         probs = _take(pr, n.value, np.float64)
         return keys, esets, counts, (probs if final_mode == "exhaustive" else None), st
+
+    def presample(self, site_probs, n_sets: int, first_id: int, shots_per_set: int, seed: int) -> ResidentBatch:
+        """Resident batch whose error sets [first_id, first_id + n_sets) are drawn on the device from
+        the per-site outcome probabilities `site_probs` (list of sequences, outcome 0 = no error)."""
+        off = np.zeros(len(site_probs) + 1, dtype=np.uint32)
+        off[1:] = np.cumsum([len(p) for p in site_probs])
+        cdf = np.concatenate([np.cumsum(np.asarray(p, dtype=np.float64)) for p in site_probs]) if len(site_probs) \
+            else np.zeros(0, np.float64)
+        bt = ResidentBatch(self, None, None, None)
+        check(load().ptsbe_batch_presample(self._h, _ptr(np.ascontiguousarray(cdf)), _ptr(off), int(n_sets),
+                                           int(first_id), int(shots_per_set), seed & (2**64 - 1), ctypes.byref(bt._h)))
+        return bt
 
     def upload(self, kraus_idx, shots, eset_ids=None) -> ResidentBatch:
         return ResidentBatch(self, kraus_idx, shots, eset_ids)

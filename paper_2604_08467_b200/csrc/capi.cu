@@ -1608,6 +1608,57 @@ int ptsbe_batch_upload(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t*
   });
 }
 
+int ptsbe_batch_presample(ptsbe_plan* pl, const double* site_cdf, const uint32_t* site_off,
+                          uint64_t n_sets, uint32_t first_id, uint32_t shots_per_set, uint64_t seed,
+                          ptsbe_batch** out) {
+  return guarded([&] {
+    if (!pl || !out || !site_cdf || !site_off) throw Failure(PTSBE_EINVAL, "null argument");
+    if (n_sets < 1 || n_sets >= (1ull << 32)) throw Failure(PTSBE_EINVAL, "need 1 .. 2^32 error sets");
+    if (shots_per_set < 1) throw Failure(PTSBE_EINVAL, "proportional sampling needs m >= 1");
+    if (site_off[0] != 0) throw Failure(PTSBE_EINVAL, "site_off must start at 0");
+    for (uint32_t s = 0; s < pl->g; ++s)
+      if (site_off[s + 1] <= site_off[s] || site_off[s + 1] - site_off[s] > 255)
+        throw Failure(PTSBE_EINVAL, "every site needs 1 .. 255 outcomes");
+    CK(cudaSetDevice(pl->device));
+    std::unique_ptr<ptsbe_batch> bt(new ptsbe_batch);
+    bt->plan = pl;
+    bt->n_sets = n_sets;
+    {
+      std::lock_guard<std::mutex> lock(pl->mu);
+      bt->ws_tmp_own = pl->take_workspace();
+      bt->ws_out_own = pl->take_workspace();
+    }
+    bt->shots_host.assign(n_sets, shots_per_set);
+    bt->total_shots = n_sets * (uint64_t)shots_per_set;
+    cudaStream_t st = pl->stream;
+    const uint32_t n_out = site_off[pl->g];
+    bt->kraus.alloc(std::max<size_t>(16, n_sets * pl->g), st);
+    bt->shots.alloc(n_sets * 4, st);
+    bt->ids.alloc(n_sets * 4, st);
+    DevBuf cdf((size_t)n_out * 8, st), off(((size_t)pl->g + 1) * 4, st);
+    CK(cudaMemcpyAsync(cdf.p, site_cdf, (size_t)n_out * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(off.p, site_off, ((size_t)pl->g + 1) * 4, cudaMemcpyHostToDevice, st));
+    fill_u32_kernel<<<cdiv(n_sets, 256), 256, 0, st>>>(bt->shots.as<uint32_t>(), (uint32_t)n_sets, shots_per_set);
+    iota_kernel<<<cdiv(n_sets, 256), 256, 0, st>>>(bt->ids.as<uint32_t>(), (uint32_t)n_sets, first_id);
+    if (pl->g)
+      presample_kernel<<<cdiv(n_sets * pl->g, 256), 256, 0, st>>>(
+          cdf.as<double>(), off.as<uint32_t>(), pl->g, n_sets, first_id, (uint32_t)seed, (uint32_t)(seed >> 32),
+          bt->kraus.as<uint8_t>());
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    *out = bt.release();
+  });
+}
+
+int ptsbe_batch_kraus(ptsbe_batch* bt, uint8_t* out_host) {
+  return guarded([&] {
+    if (!bt || !out_host) throw Failure(PTSBE_EINVAL, "null argument");
+    CK(cudaSetDevice(bt->plan->device));
+    CK(cudaMemcpyAsync(out_host, bt->kraus.p, bt->n_sets * bt->plan->g, cudaMemcpyDeviceToHost, bt->plan->stream));
+    CK(cudaStreamSynchronize(bt->plan->stream));
+  });
+}
+
 int ptsbe_batch_run(ptsbe_batch* bt, uint64_t seed, uint64_t* n_records, ptsbe_run_stats* stats) {
   return guarded([&] {
     if (!bt) throw Failure(PTSBE_EINVAL, "null batch");

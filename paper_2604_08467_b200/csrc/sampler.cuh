@@ -638,4 +638,29 @@ __global__ void iota_kernel(uint32_t* p, uint32_t n, uint32_t add) {
   if (i < n) p[i] = i + add;
 }
 
+// Pre-trajectory sampling on the device (reference draw_realization / presample_errors,
+// engine.py:232-281): one Kraus/Pauli index per (error set, gate site), drawn from the
+// site's outcome distribution with a counter-based uniform -- Philox counter
+// (site, GLOBAL error-set id, 'PRES', 0), key = seed -- so an error set's realisation does not
+// depend on the batch, the rank or the order it is generated in.  site_cdf holds, per site, the
+// inclusive cumulative probabilities of its outcomes (index 0 = no error).
+constexpr uint32_t PRESAMPLE_TAG = 0x50524553u;  // "PRES"
+
+__global__ void presample_kernel(const double* __restrict__ site_cdf, const uint32_t* __restrict__ site_off,
+                                 uint32_t g, uint64_t n_sets, uint32_t first_id, uint32_t k0, uint32_t k1,
+                                 uint8_t* __restrict__ out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_sets * g) return;
+  const uint32_t e = (uint32_t)(i / g), s = (uint32_t)(i - (uint64_t)e * g);
+  const uint32_t a = site_off[s], b = site_off[s + 1];
+  uint32_t idx = 0;
+  if (b - a > 1) {
+    const Philox4 x = philox4x32_10(s, first_id + e, PRESAMPLE_TAG, 0u, k0, k1);
+    const uint64_t x64 = ((uint64_t)x.v[1] << 32) | x.v[0];
+    const double u = (double)(x64 >> 11) * (1.0 / 9007199254740992.0);
+    while (idx + 1 < b - a && site_cdf[a + idx] <= u) ++idx;
+  }
+  out[i] = (uint8_t)idx;
+}
+
 }  // namespace ptsbe

@@ -527,3 +527,47 @@ def test_batch_time_curve_rows():
         assert {"b", "stage_seconds", "per_qubit_seconds", "path_seconds", "est_cost", "reps"} <= set(r)
         assert r["stage_seconds"] > 0 and r["per_qubit_seconds"] == pytest.approx(r["stage_seconds"] / r["b"])
     assert rows[-1]["est_cost"] > rows[0]["est_cost"]
+
+
+def test_device_presampling_matches_counter_oracle_and_upload_path():
+    """Pre-trajectory sampling on the device (reference engine.py:232-281): the
+    Kraus-index matrix equals the oracle's counter-based draw bit for bit, does not depend on
+    how the id range is split, follows the channel probabilities, and a run over the
+    device-sampled batch equals a run over the same matrix uploaded from the host."""
+    from paper_2604_08467_b200.engine import DevicePipeline, VariantTables
+
+    c, _ = workloads.hea(10, 3, gamma=0.08, p=0.1, seed=4)
+    tpl = CircuitNetwork.from_circuit(c)
+    tables = VariantTables.from_channels(tpl)
+    site_probs = [[pr for _, pr in g.noise.outcomes()] for g in c.gates]
+    sets, seed = 5000, 12345
+    ctx = SamplerContext(hypersamples=4, dtype="complex128")
+    pipe = DevicePipeline(tpl, BatchPlan((5, 5)), tables, ctx, shots_per_set=20.0)
+    try:
+        dp = pipe.device_plan
+        bt = dp.presample(site_probs, sets, 100, 20, seed)
+        got = bt.kraus(sets, len(c.gates))
+        want = O.presample_counter(site_probs, sets, 100, seed)
+        np.testing.assert_array_equal(got, want)
+        # split-independence: the second half generated on its own
+        half = dp.presample(site_probs, sets // 2, 100 + sets // 2, 20, seed)
+        np.testing.assert_array_equal(half.kraus(sets // 2, len(c.gates)), want[sets // 2:])
+        half.close()
+        # distribution: frequency of "some error" per site within 5 sigma of 1 - p0
+        for s, probs in enumerate(site_probs):
+            p_err = 1.0 - probs[0]
+            f_err = float(np.mean(got[:, s] != 0))
+            assert abs(f_err - p_err) <= 5 * np.sqrt(max(p_err * (1 - p_err), 1e-9) / sets) + 1e-12
+        # same records as the host-upload path
+        n1, _ = bt.run(7)
+        k1, c1 = bt.fetch()
+        up = dp.upload(want, np.full(sets, 20, np.uint32), np.arange(100, 100 + sets, dtype=np.uint32))
+        n2, _ = up.run(7)
+        k2, c2 = up.fetch()
+        assert n1 == n2
+        np.testing.assert_array_equal(k1, k2)
+        np.testing.assert_array_equal(c1, c2)
+        bt.close()
+        up.close()
+    finally:
+        pipe.close()

@@ -150,3 +150,21 @@ def test_golden_nonproportional_records(golden_cases):
                     assert abs(p - q) <= 1e-12
             n_records += len(got)
     assert n_records >= 1000
+
+
+def test_presample_counter_follows_channel_probabilities():
+    """Counter-based pre-trajectory draw (device: presample_kernel): per site the
+    outcome frequencies follow the channel's distribution (engine.py:232-244), the
+    stream is keyed by (site, global error-set id) only."""
+    from paper_2604_08467_b200 import workloads
+
+    c, _ = workloads.hea(6, 2, gamma=0.1, p=0.2, seed=1)
+    site_probs = [[pr for _, pr in g.noise.outcomes()] for g in c.gates]
+    sets = 20000
+    m = O.presample_counter(site_probs, sets, 0, 99)
+    for s, probs in enumerate(site_probs):
+        freq = np.bincount(m[:, s], minlength=len(probs)) / sets
+        sigma = np.sqrt(np.maximum(np.asarray(probs) * (1 - np.asarray(probs)), 1e-9) / sets)
+        assert np.all(np.abs(freq - np.asarray(probs)) <= 5 * sigma + 1e-12)
+    np.testing.assert_array_equal(O.presample_counter(site_probs, 100, 500, 99), m[500:600])
+    assert not np.array_equal(O.presample_counter(site_probs, 100, 0, 100), m[:100])
