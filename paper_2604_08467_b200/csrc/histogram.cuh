@@ -95,6 +95,23 @@ inline void reduce_by_key(const uint64_t* keys, uint64_t stride, uint32_t words,
   g_launches++;
   uint32_t* pin = perm_a.as<uint32_t>();
   uint32_t* pout = perm_b.as<uint32_t>();
+  DevBuf sorted_counts;
+  if (words == 1 && counts32 && key_bits >= 1) {
+    // one key word: sort the (key, count) pairs themselves; everything downstream then reads
+    // sorted arrays through the identity permutation (coalesced) instead of gathering through one
+    const int used = (int)std::min<uint32_t>(key_bits, 64);
+    sorted_counts.alloc(n * 4, st);
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, kout.as<uint64_t>(), counts32,
+                                       sorted_counts.as<uint32_t>(), (int)n, 64 - used, 64, st));
+    DevBuf tmp(tmp_bytes, st);
+    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys, kout.as<uint64_t>(), counts32,
+                                       sorted_counts.as<uint32_t>(), (int)n, 64 - used, 64, st));
+    g_launches += 1 + (used + 7) / 8 * 2;
+    keys = kout.as<uint64_t>();
+    stride = n;
+    counts32 = sorted_counts.as<uint32_t>();
+  } else
   for (int w = (int)words - 1; w >= 0; --w) {
     // bits used in word w: qubits [64w, min(64w+64, key_bits)) occupy the top of the word
     const int used = (int)key_bits - 64 * w >= 64 ? 64 : (int)key_bits - 64 * w;
