@@ -104,6 +104,9 @@ def run_ptsbe_sharded(c, config, errorsets, *, group=None, cache=None):
 
     from . import engine
 
+    if config.mode != "ptsbe-proportional":
+        raise NotImplementedError("the sharded run gathers count histograms; the non-proportional mode "
+                                  "(records with probability tags) runs per rank and is merged with merge_records")
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     device = config.device
     lo, hi = shard_bounds([k.m for k in errorsets], world)[rank]
