@@ -571,3 +571,52 @@ def test_device_presampling_matches_counter_oracle_and_upload_path():
         up.close()
     finally:
         pipe.close()
+
+
+def test_cfg2_full_circuit_size_independent_properties():
+    """BASELINE config 2 at full circuit size (30-qubit HEA depth 6, 447 sites, plan 9/6/7/8,
+    complex64, every production kernel: memo + tiled class-0 pass, lane interpreter, fused
+    descent, Hermitian packing), on a batch small enough for a test: (a) every shot of every
+    unflagged error set is sampled, (b) records are sorted and unique per error set, (c) the
+    empirical distribution of the first 9 measured bits matches the exact complex128 stage-1
+    marginal of that error set (TVD at 10^4 shots), (d) results do not depend on how the error
+    sets are grouped into calls."""
+    from paper_2604_08467_b200.engine import DevicePipeline, VariantTables
+
+    c, _ = workloads.hea(30, 6, gamma=0.01, p=0.01, seed=2)
+    sizes = (9, 6, 7, 8)
+    tpl = CircuitNetwork.from_circuit(c)
+    tables = VariantTables.from_channels(tpl)
+    sets, shots = 12, 10_000
+    kraus = workloads.presample_matrix(c, sets, np.random.default_rng(6))
+    kraus[:, :] = np.where(np.arange(len(c.gates))[None, :] < 60, 0, kraus)  # no K1 on |0>: nothing flagged
+    ids = np.arange(sets, dtype=np.uint32)
+    ctx = SamplerContext(hypersamples=16, dtype="complex64")
+    pipe = DevicePipeline(tpl, BatchPlan(sizes), tables, ctx, shots_per_set=float(shots))
+    try:
+        dp = pipe.device_plan
+        keys, esets, counts, st = dp.sample(kraus, np.full(sets, shots, np.uint32), ids, 11, merged=False)
+        assert int(st.flagged_sets) == 0 and int(counts.sum()) == sets * shots
+        for e in range(sets):
+            ke = keys[esets == e, 0]
+            assert np.all(np.diff(ke.astype(np.uint64)) > 0)  # sorted, unique
+        # (d) grouping independence: two calls of 6 error sets
+        k2a, e2a, c2a, _ = dp.sample(kraus[:6], np.full(6, shots, np.uint32), ids[:6], 11, merged=False)
+        k2b, e2b, c2b, _ = dp.sample(kraus[6:], np.full(6, shots, np.uint32), ids[6:], 11, merged=False)
+        np.testing.assert_array_equal(np.concatenate([k2a, k2b]), keys)
+        np.testing.assert_array_equal(np.concatenate([c2a, c2b]), counts)
+    finally:
+        pipe.close()
+    # (c) stage-1 marginal of three error sets in complex128 through the marginals entry point
+    es = workloads.errorsets_from_matrix(c, kraus[:3], shots)
+    # (unnormalised: a realised K1 gives the trajectory a weight far below the reference's absolute
+    # 1e-12 mass floor, which the normalising form of this call enforces like the reference does)
+    exact, mass = conditional_marginals_batched(tpl, es, BatchPlan(sizes), 1, ["", "", ""],
+                                                SamplerContext(hypersamples=16, dtype="complex128"),
+                                                normalize=False, return_mass=True)
+    exact = exact / mass[:, None]
+    for e in range(3):
+        sel = esets == e
+        first9 = (keys[sel, 0] >> np.uint64(64 - 9)).astype(np.int64)
+        emp = np.bincount(first9, weights=counts[sel].astype(np.float64), minlength=512) / shots
+        assert 0.5 * np.abs(emp - exact[e]).sum() <= 0.12  # 512 bins, 10^4 shots: sampling noise ~0.09
