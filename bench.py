@@ -9,7 +9,8 @@ shapes.
 A step = one pass of the hot path (stored-path contraction + non-degenerate
 sampling + local histogram) over one batch of pre-sampled error sets.  Weak
 scaling: every GPU gets `--sets` error sets; with N > 1 each step ends with
-the NCCL gather + merge of the per-rank histograms.  Planning/compilation is
+the NCCL exchange of the per-rank histograms by key range (all_to_all) and the
+merge of every rank's slice.  Planning/compilation is
 excluded from the timed region, as the reference excludes path planning from
 its loop time (reference bench.py:5-8, engine.py:895-901).
 
@@ -412,7 +413,7 @@ def main():
 
     from paper_2604_08467_b200 import _capi
     from paper_2604_08467_b200.engine import BatchPlan, CircuitNetwork, DevicePipeline, SamplerContext, VariantTables
-    from paper_2604_08467_b200.partition import gather_histograms, merge_on_device
+    from paper_2604_08467_b200.partition import exchange_histograms_by_key_range, merge_on_device
 
     if _capi.device_count() < 1:
         raise SystemExit("bench.py needs a CUDA device: libptsbe_b200 has no CPU fallback")
@@ -461,7 +462,8 @@ def main():
                 torch.zeros(0, dtype=torch.int64, device=f"cuda:{local_rank}")
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            gather_histograms(kt, ct, merge=lambda a, b: merge_on_device(a, b, local_rank))
+            # final exchange: every rank receives and merges only its key range of the global histogram
+            exchange_histograms_by_key_range(kt, ct, merge=lambda a, b: merge_on_device(a, b, local_rank))
             e1.record()
             torch.cuda.synchronize()
             ms += e0.elapsed_time(e1)
@@ -534,7 +536,7 @@ def main():
             if world > 1:
                 kt = torch.from_numpy(keys.view(np.int64)).to(f"cuda:{local_rank}")
                 ct = torch.from_numpy(counts.view(np.int64)).to(f"cuda:{local_rank}")
-                kk, cc = gather_histograms(kt, ct, merge=lambda a, b: merge_on_device(a, b, local_rank))
+                kk, cc = exchange_histograms_by_key_range(kt, ct, merge=lambda a, b: merge_on_device(a, b, local_rank))
                 cc.cpu()
         sync_all()
         te = torch.tensor([(time.perf_counter() - w0)], dtype=torch.float64, device=f"cuda:{local_rank}")
@@ -626,7 +628,8 @@ def main():
                        "error_sets_from": "device pre-sampling" if args.device_presample else "host matrix",
                        "l2": "per-step working set (work lists, hoisted records, population vectors) exceeds the 126 MB L2"
                              if total_shots_local * 8 > 126e6 else "working set below L2 size (small workload)",
-                       "parallelism": f"error sets sharded over {world} GPU(s), weak scaling"},
+                       "parallelism": f"error sets sharded over {world} GPU(s), weak scaling; no traffic while sampling, "
+                                      "final NCCL exchange of the histogram by key range (all_to_all) + per-rank merge"},
             "clocks": clocks,
             "e2e": e2e,
             "gpu_launches": int(sum(int(s.gpu_launches) for s in stats)),

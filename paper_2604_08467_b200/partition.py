@@ -74,6 +74,45 @@ def gather_histograms(keys, counts, *, group=None, merge: Optional[Callable] = N
     return k, c
 
 
+def exchange_histograms_by_key_range(keys, counts, *, group=None, merge: Optional[Callable] = None):
+    """Final exchange for LARGE histograms: instead of every rank receiving and merging
+    everything (`gather_histograms`), the key space is cut into `world` equal ranges of the
+    first key word and rank r receives, from every rank, only the records whose key falls into
+    range r (one all_to_all of the split sizes, one all_to_all of the rows), then merges its
+    slice.  The global histogram is the concatenation of the ranks' slices in rank order, each
+    sorted by key; merge work and memory per rank are 1 / world of the gathered form.
+
+    `keys` [R_r, words] (u64 bit patterns as int64) must be sorted by key, as every merged
+    per-rank histogram is.  Returns this rank's (keys, counts) slice."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    words = keys.shape[1]
+    n = keys.shape[0]
+    # destination rank = floor(key0 / 2^64 * world), on the top 32 bits of the first word
+    if n:
+        top = torch.bitwise_and(torch.bitwise_right_shift(keys[:, 0], 32), 0xFFFFFFFF)
+        dest = torch.bitwise_right_shift(top * world, 32)
+        send = torch.bincount(dest, minlength=world).to(torch.int64)
+    else:
+        send = torch.zeros(world, dtype=torch.int64, device=keys.device)
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send, group=group)
+    send_l, recv_l = [int(v) for v in send.tolist()], [int(v) for v in recv.tolist()]
+    rows = torch.empty((n, words + 1), dtype=torch.int64, device=keys.device)
+    if n:
+        rows[:, :words] = keys
+        rows[:, words] = counts
+    got = torch.empty((sum(recv_l), words + 1), dtype=torch.int64, device=keys.device)
+    # sorted input: the records for rank r are one contiguous block, blocks in rank order
+    dist.all_to_all_single(got, rows, output_split_sizes=recv_l, input_split_sizes=send_l, group=group)
+    k, c = got[:, :words].contiguous(), got[:, words].contiguous()
+    if merge is not None and k.shape[0]:
+        k, c = merge(k, c)
+    return k, c
+
+
 def merge_on_device(keys, counts, device: int):
     """Sort + reduce-by-key of gathered rows with the library's device kernels.
     Inputs/outputs are int64 cuda tensors holding u64 bit patterns."""

@@ -54,8 +54,12 @@ def _worker(rank, world, port, case_json, out_dir):
 
     k, cnt = gather_histograms(keys, counts, merge=merge)
     got = list(zip(unpack_keys(k.numpy().view(np.uint64), c.n), cnt.tolist()))
+    # key-range exchange: every rank ends with a disjoint, merged slice of the same histogram
+    from paper_2604_08467_b200.partition import exchange_histograms_by_key_range
+    ks, cs = exchange_histograms_by_key_range(keys, counts, merge=merge)
+    mine = list(zip(unpack_keys(ks.numpy().view(np.uint64), c.n), cs.tolist()))
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fp:
-        json.dump({"hist": got, "shard": [lo, hi]}, fp)
+        json.dump({"hist": got, "shard": [lo, hi], "slice": mine}, fp)
     dist.destroy_process_group()
 
 
@@ -66,11 +70,13 @@ def test_sharded_histogram_equals_single_process(golden_cases, tmp_path, name, w
     case = golden_cases[name]
     want = O.merge_histograms([[tuple(r) for r in h] for h in case["histograms"]])
     mp.spawn(_worker, args=(world, _free_port(), json.dumps(case), str(tmp_path)), nprocs=world, join=True)
-    shards = []
+    shards, slices = [], []
     for r in range(world):
         doc = json.load(open(tmp_path / f"rank{r}.json"))
         assert [tuple(x) for x in doc["hist"]] == want
         shards.append(tuple(doc["shard"]))
+        slices += [tuple(x) for x in doc["slice"]]
+    assert slices == want  # slices in rank order = the merged histogram, sorted by key
     assert shards[0][0] == 0 and shards[-1][1] == len(case["errorsets"])
     assert all(a[1] == b[0] for a, b in zip(shards, shards[1:]))
 
