@@ -1706,6 +1706,38 @@ void ptsbe_batch_destroy(ptsbe_batch* bt) {
   delete bt;
 }
 
+// Per-error-set records of a run -> host buffers of the C-ABI layout (keys [n][words] u64, counts u64,
+// error-set position u32, optional probability tags).  Layout conversion runs on the device and the
+// copies land in recycled page-locked buffers, like the merged histogram.
+static void fetch_per_set(ptsbe_plan* pl, const RunOutput& out, bool with_probs, uint64_t** keys,
+                          uint32_t** rec_eset, uint64_t** counts, double** probs, uint64_t* n_records) {
+  cudaStream_t st = pl->stream;
+  const uint32_t words = pl->words;
+  const uint64_t nr = out.n, cap = std::max<uint64_t>(nr, 1);
+  uint64_t* k = (uint64_t*)g_host_pool.get(cap * 8 * words);
+  uint64_t* c = (uint64_t*)g_host_pool.get(cap * 8);
+  uint32_t* es = (uint32_t*)g_host_pool.get(cap * 4);
+  double* pr = probs ? (double*)g_host_pool.get(cap * 8) : nullptr;
+  if (!k || !c || !es || (probs && !pr)) throw Failure(PTSBE_ECAPACITY, "host allocation of the records failed");
+  if (nr) {
+    DevBuf aos(nr * 8 * words, st), c64(nr * 8, st);
+    untranspose_keys_kernel<<<cdiv(nr * words, 256), 256, 0, st>>>(out.keys.as<uint64_t>(), aos.as<uint64_t>(), nr, words);
+    widen_counts_kernel<<<cdiv(nr, 256), 256, 0, st>>>(out.counts.as<uint32_t>(), c64.as<uint64_t>(), nr);
+    g_launches += 2;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(k, aos.p, nr * 8 * words, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(c, c64.p, nr * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(es, out.eset.p, nr * 4, cudaMemcpyDeviceToHost, st));
+    if (pr && with_probs) CK(cudaMemcpyAsync(pr, out.probs.p, nr * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (pr && !with_probs)
+      for (uint64_t i = 0; i < nr; ++i) pr[i] = -1.0;  // no tag in direct mode
+  }
+  *keys = k; *counts = c; *n_records = nr;
+  if (rec_eset) *rec_eset = es; else ptsbe_free(es);
+  if (probs) *probs = pr;
+}
+
 int ptsbe_sample(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t* shots,
                  const uint32_t* eset_ids, uint64_t n_sets, uint64_t seed, int merged,
                  uint64_t** keys, uint32_t** rec_eset, uint64_t** counts, uint64_t* n_records,
@@ -1734,24 +1766,8 @@ int ptsbe_sample(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t* shots
       fetch_merged(bt, keys, counts, n_records);
       if (rec_eset) *rec_eset = nullptr;
     } else {
-      const uint64_t nr = bt->per_set.n;
-      std::vector<uint64_t> soa(std::max<uint64_t>(nr, 1) * words);
-      std::vector<uint32_t> c32(std::max<uint64_t>(nr, 1));
-      uint64_t* k = (uint64_t*)malloc(std::max<uint64_t>(nr, 1) * 8 * words);
-      uint64_t* c = (uint64_t*)malloc(std::max<uint64_t>(nr, 1) * 8);
-      uint32_t* es = (uint32_t*)malloc(std::max<uint64_t>(nr, 1) * 4);
-      if (nr) {
-        CK(cudaMemcpyAsync(soa.data(), bt->per_set.keys.p, nr * 8 * words, cudaMemcpyDeviceToHost, pl->stream));
-        CK(cudaMemcpyAsync(c32.data(), bt->per_set.counts.p, nr * 4, cudaMemcpyDeviceToHost, pl->stream));
-        CK(cudaMemcpyAsync(es, bt->per_set.eset.p, nr * 4, cudaMemcpyDeviceToHost, pl->stream));
-        CK(cudaStreamSynchronize(pl->stream));
-      }
-      for (uint64_t i = 0; i < nr; ++i) {
-        for (uint32_t w = 0; w < words; ++w) k[i * words + w] = soa[(uint64_t)w * nr + i];
-        c[i] = c32[i];
-      }
-      *keys = k; *counts = c; *n_records = nr;
-      if (rec_eset) *rec_eset = es; else free(es);
+      WorkspaceScope tmp_scope(&bt->ws_tmp());
+      fetch_per_set(pl, bt->per_set, false, keys, rec_eset, counts, nullptr, n_records);
     }
     CK(cudaEventRecord(e3, pl->stream));
     CK(cudaStreamSynchronize(pl->stream));
@@ -1827,27 +1843,11 @@ int ptsbe_sample_nonproportional(ptsbe_plan* pl, const uint8_t* kraus_idx, const
         stats->first_flag_stage = (uint32_t)((fl.first >> 8) & 0xff);
         stats->first_flagged_id = (int64_t)(fl.first >> 16);
       }
+      {
+        WorkspaceScope tmp_scope(ws_tmp.get());
+        fetch_per_set(pl, out, final_mode == 0, keys, rec_eset, counts, probs, n_records);
+      }
       const uint64_t nr = out.n;
-      std::vector<uint64_t> soa(std::max<uint64_t>(nr, 1) * words);
-      std::vector<uint32_t> c32(std::max<uint64_t>(nr, 1));
-      uint64_t* k = (uint64_t*)malloc(std::max<uint64_t>(nr, 1) * 8 * words);
-      uint64_t* c = (uint64_t*)malloc(std::max<uint64_t>(nr, 1) * 8);
-      uint32_t* es = (uint32_t*)malloc(std::max<uint64_t>(nr, 1) * 4);
-      double* pr = (double*)malloc(std::max<uint64_t>(nr, 1) * 8);
-      if (!k || !c || !es || !pr) throw Failure(PTSBE_ECAPACITY, "host allocation of the records failed");
-      if (nr) {
-        CK(cudaMemcpyAsync(soa.data(), out.keys.p, nr * 8 * words, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(c32.data(), out.counts.p, nr * 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(es, out.eset.p, nr * 4, cudaMemcpyDeviceToHost, st));
-        if (final_mode == 0) CK(cudaMemcpyAsync(pr, out.probs.p, nr * 8, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-      }
-      for (uint64_t i = 0; i < nr; ++i) {
-        for (uint32_t w = 0; w < words; ++w) k[i * words + w] = soa[(uint64_t)w * nr + i];
-        c[i] = c32[i];
-        if (final_mode != 0) pr[i] = -1.0;  // no tag in direct mode
-      }
-      *keys = k; *counts = c; *rec_eset = es; *probs = pr; *n_records = nr;
       stats->n_records = nr;
       stats->gpu_launches = g_launches;
     }

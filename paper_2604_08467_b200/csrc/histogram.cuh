@@ -76,6 +76,18 @@ __global__ void transpose_keys_kernel(const uint64_t* in, uint64_t* out, uint64_
   out[w * n + r] = in[i];
 }
 
+// SoA [words][n] -> row-major [n][words]
+__global__ void untranspose_keys_kernel(const uint64_t* in, uint64_t* out, uint64_t n, uint32_t words) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * words) return;
+  const uint64_t r = i / words, w = i - r * words;
+  out[i] = in[w * n + r];
+}
+__global__ void widen_counts_kernel(const uint32_t* in, uint64_t* out, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i];
+}
+
 struct Histogram {
   DevBuf keys;    // [n][words] row-major
   DevBuf counts;  // [n] u64
