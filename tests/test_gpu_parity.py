@@ -620,3 +620,29 @@ def test_cfg2_full_circuit_size_independent_properties():
         first9 = (keys[sel, 0] >> np.uint64(64 - 9)).astype(np.int64)
         emp = np.bincount(first9, weights=counts[sel].astype(np.float64), minlength=512) / shots
         assert 0.5 * np.abs(emp - exact[e]).sum() <= 0.12  # 512 bins, 10^4 shots: sampling noise ~0.09
+
+
+def test_cfg2_full_circuit_complex64_marginals_within_1e5_of_complex128():
+    """North-star tolerance at BASELINE size: conditional marginals of the 30-qubit HEA depth-6
+    circuit (447 sites) in complex64 within 1e-5 relative of complex128, every stage of the
+    9/6/7/8 plan, on prefixes that a proportional run actually visits."""
+    c, _ = workloads.hea(30, 6, gamma=0.01, p=0.01, seed=2)
+    sizes = (9, 6, 7, 8)
+    tpl = CircuitNetwork.from_circuit(c)
+    kraus = workloads.presample_matrix(c, 6, np.random.default_rng(6))
+    kraus[:, :60] = 0
+    es = workloads.errorsets_from_matrix(c, kraus, 100)
+    per = sample_proportional_batched(tpl, es, BatchPlan(sizes), 3, SamplerContext(hypersamples=16, dtype="complex128"))
+    for j in (1, 2, 3, 4):
+        off = sum(sizes[:j - 1])
+        pf = [recs[len(recs) // 2].bitstring[:off] for recs in per]
+        hi, mh = conditional_marginals_batched(tpl, es, BatchPlan(sizes), j, pf,
+                                               SamplerContext(hypersamples=16, dtype="complex128"),
+                                               normalize=False, return_mass=True)
+        lo, ml = conditional_marginals_batched(tpl, es, BatchPlan(sizes), j, pf,
+                                               SamplerContext(hypersamples=16, dtype="complex64"),
+                                               normalize=False, return_mass=True)
+        a, b = hi / mh[:, None], lo / ml[:, None]
+        err = np.max(np.abs(a - b), axis=1) / np.max(a, axis=1)
+        assert err.max() <= 1e-5, (j, err.max())
+        assert np.max(np.abs(ml / mh - 1.0)) <= 1e-5
