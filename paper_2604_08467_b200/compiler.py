@@ -21,6 +21,7 @@ whose class is j-1 are recomputed for every stage-j work item.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -35,6 +36,8 @@ MEMO_NONE = 0xFFFF         # "operand is not produced by a step of this program"
 MEMO_MIN_STEPS = 48        # class-0 programs at least this long get a variant-0 memo
 LO_TABLE_MAX = 1024          # entries in the per-lane (low) gather table of a step
 SMEM_BYTES = 52 * 1024       # shared-memory arena of a CTA-per-item program: 4 CTAs per SM stay resident
+SMALL_ARENA_BYTES = 6 * 1024   # up to here the lane count is chosen by issued instructions alone
+BIG_ARENA_LANES = 32  # measured on cfg5 (8: 155.8, 16: 150.4, 32: 148.4 ms per step)
 WARP_ARENA_BYTES = 16 * 1024  # beyond this a warp-per-item mapping starves occupancy (8 warps x 16 KB = 2 CTAs per SM)
 
 
@@ -383,6 +386,10 @@ def compile_stage(
                     total += 80 + -(-nd.size // gs) * (10 + 8 * kn)
                 return total * gs / 32.0
             threads = min((8, 16, 32), key=per_item)
+            if peak * elem_bytes > SMALL_ARENA_BYTES:
+                # big arenas leave room for few groups per SM: latency per step, not issued
+                # instructions, decides -- spread the item over more lanes
+                threads = int(os.environ.get("PTSBE_BIG_GS", BIG_ARENA_LANES))
             fast_cap = peak
         else:
             # CTA per item.  Large steps run as 4 x 4 register tiles (separable form), so 256
