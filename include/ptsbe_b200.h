@@ -68,6 +68,7 @@ enum { PTSBE_C64 = 0, PTSBE_C128 = 1 };
  *          nB, (qubit, stride) x nB]: operand bases advance by stride when the measured bit
  *          of that qubit is 1 (the operand is a slice of a stored tensor, never materialised)
  *          bit 4: the step always runs (it writes a record or the result);
+ *          bit 5 / 6: the offsets of operand A / B do not depend on the output index (loA, hiA all 0);
  *          a_prod / b_prod: index of the step of this program that produces operand A / B
  *          (0xFFFF: a leaf or an earlier pass), a_memo / b_memo / own_memo: offsets of the
  *          operands' and the step's own variant-0 value in the program's memo (memo_elems > 0)

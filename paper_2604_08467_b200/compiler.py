@@ -531,6 +531,12 @@ def compile_stage(
             if is_always:
                 conj_flags |= 16
                 always_steps.append(len(step_rows))
+            # operand offsets that do not depend on the output index (a fully contracted operand, e.g.
+            # the vector of a vector-matrix step): the lane interpreter loads it once per step
+            if not select and not lo_a.any() and not hi_a.any():
+                conj_flags |= 32
+            if not select and not lo_b.any() and not hi_b.any():
+                conj_flags |= 64
             step_index[nid] = len(step_rows)
             memo_off[nid] = memo_top
             step_sites.append(deps)

@@ -10,7 +10,7 @@
 // (served from the program image in shared memory as broadcasts), only operand
 // loads and the multiply-adds are per-lane work, and the item's intermediates
 // live in a private slice of a warp-interleaved shared-memory arena
-// (element e of lane t at [e * 33 + t]: conflict-free for "same element, all
+// (element e of lane t at [e * 40 + t]: conflict-free for "same element, all
 // lanes" as well as for "same item, different elements").
 //
 // lane_descent_kernel additionally keeps the item's last intermediate on chip:
@@ -34,7 +34,9 @@ namespace ptsbe {
 
 constexpr int LN_THREADS = 256;
 constexpr int LN_WARPS = LN_THREADS / 32;
-constexpr int LN_AST = 33;          // arena element stride (in elements) between consecutive indices
+constexpr int LN_AST = 40;          // arena row pitch in elements: lane t of element e at [e * 40 + t].  Pitch = 8
+                                    // (mod 16) puts the elements a 4-lane group reads for one item, and the items of
+                                    // the 8 groups of a warp, on disjoint bank pairs (33 gave 4-way conflicts)
 constexpr int LN_MAX_LEVELS = 16;   // ancestors kept per lane
 constexpr int LN_GS = 4;            // lanes per (item, draw) in the descent phase of the fused kernel
 constexpr int LN_NG = 32 / LN_GS;   // such groups per warp
@@ -210,6 +212,23 @@ __device__ __forceinline__ void lane_step_fixed(const LaneStep& t, const LaneOp<
   uint32_t ka[KN], kb[KN];
 #pragma unroll
   for (int k = 0; k < KN; ++k) { ka[k] = t.kA[k] * A.stride; kb[k] = t.kB[k] * B.stride; }
+  if ((t.flags & 32u) && KN <= 8) {
+    // A does not depend on the output index (vector-matrix step): its KN elements are loaded once
+    C av[KN];
+#pragma unroll
+    for (int k = 0; k < KN; ++k) av[k] = A.p[ka[k]];
+    for (uint32_t ch = 0, c = 0; ch < t.hi_n; ++ch) {
+      const uint32_t hb = t.hi_n > 1 ? t.hiB[ch] : 0u;
+      for (uint32_t cl = 0; cl < t.lo_n; ++cl, ++c) {
+        const C* pb = B.p + (t.loB[cl] + hb) * B.stride;
+        C acc; acc.x = 0; acc.y = 0;
+#pragma unroll
+        for (int k = 0; k < KN; ++k) cmac_s<FA, FB>(acc, av[k], pb[kb[k]]);
+        if (store) O[c * o_stride] = acc;
+      }
+    }
+    return;
+  }
   for (uint32_t ch = 0, c = 0; ch < t.hi_n; ++ch) {
     const uint32_t ha = t.hi_n > 1 ? t.hiA[ch] : 0u, hb = t.hi_n > 1 ? t.hiB[ch] : 0u;
     for (uint32_t cl = 0; cl < t.lo_n; ++cl, ++c) {
