@@ -229,6 +229,23 @@ __device__ __forceinline__ void lane_step_fixed(const LaneStep& t, const LaneOp<
     }
     return;
   }
+  if ((t.flags & 64u) && KN <= 8) {
+    // same with the roles swapped (matrix-vector step)
+    C bv[KN];
+#pragma unroll
+    for (int k = 0; k < KN; ++k) bv[k] = B.p[kb[k]];
+    for (uint32_t ch = 0, c = 0; ch < t.hi_n; ++ch) {
+      const uint32_t ha = t.hi_n > 1 ? t.hiA[ch] : 0u;
+      for (uint32_t cl = 0; cl < t.lo_n; ++cl, ++c) {
+        const C* pa = A.p + (t.loA[cl] + ha) * A.stride;
+        C acc; acc.x = 0; acc.y = 0;
+#pragma unroll
+        for (int k = 0; k < KN; ++k) cmac_s<FA, FB>(acc, pa[ka[k]], bv[k]);
+        if (store) O[c * o_stride] = acc;
+      }
+    }
+    return;
+  }
   for (uint32_t ch = 0, c = 0; ch < t.hi_n; ++ch) {
     const uint32_t ha = t.hi_n > 1 ? t.hiA[ch] : 0u, hb = t.hi_n > 1 ? t.hiB[ch] : 0u;
     for (uint32_t cl = 0; cl < t.lo_n; ++cl, ++c) {
