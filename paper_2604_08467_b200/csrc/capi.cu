@@ -910,6 +910,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       log.end();
       stats->marg_launches[j - 1]++;
       SampleArgs sa;
+      memset(&sa, 0, sizeof sa);
       sa.probs = probs.p;
       sa.mult = cur.mult.as<uint32_t>();
       sa.slot_off = cur.slot_off.as<uint32_t>();
@@ -936,6 +937,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       sa.neg_abs = pl->neg_abs;
       sa.neg_rel = pl->neg_rel;
       sa.np_mode = 0;
+      sa.np_floor_bits = pl->dtype == PTSBE_C64 ? 17 : 40;
       sa.child_mult = 0;
       sa.threshold = 0.0;
       sa.slot_prob = nullptr;
@@ -1521,6 +1523,7 @@ int ptsbe_sample_stage(uint32_t b, uint32_t stage, uint64_t seed, uint64_t n_ite
       CK(cudaMemsetAsync(flag.as<unsigned char>() + 8, 0, 8, st));
       exclusive_scan<uint32_t, uint32_t>(dm.as<uint32_t>(), so.as<uint32_t>(), n_items, nullptr, st);
       SampleArgs sa;
+      memset(&sa, 0, sizeof sa);
       memset(&sa, 0, sizeof sa);
       sa.probs = dp.p;
       sa.mult = dm.as<uint32_t>();

@@ -73,6 +73,7 @@ struct SampleArgs {
   uint32_t child_mult;      // multiplicity handed to every emitted child (slot_count)
   double threshold;         // harvest: conditional probability an outcome must reach
   double* slot_prob;        // harvest: conditional probability of each emitted outcome
+  uint32_t np_floor_bits;   // choice: weights below max >> np_floor_bits count as zero probability
 };
 
 constexpr int SAMPLE_THREADS = 128;
@@ -293,9 +294,15 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) nonprop_kernel(const SampleArg
     int ex;
     frexp(mx, &ex);
     const int shift = (62 - (int)a.b) - ex;
+    // Outcomes whose weight is below 2^-np_floor_bits of the row maximum are rounding noise of an
+    // exactly-zero probability (the reference tests probs > 0.0, engine.py:550, and then fails on the
+    // noise child with a vanishing-mass error at the next stage -- a rounding-dependent accident):
+    // they are not eligible.  40 bits for complex128, 17 for complex64.
+    const uint64_t wfloor = ((uint64_t)ldexp(mx, shift)) >> a.np_floor_bits;
     uint64_t local = 0;
     for (uint32_t k = k0; k < k0 + per && k < nb; ++k) {
-      const uint64_t w = (uint64_t)ldexp(pd[k], shift);
+      uint64_t w = (uint64_t)ldexp(pd[k], shift);
+      if (w < wfloor) w = 0;
       local += w;
       cdf[k] = w;
     }
