@@ -206,7 +206,8 @@ int ptsbe_sample(ptsbe_plan* plan, const uint8_t* kraus_idx, const uint32_t* sho
 
 /* replaces: sample_nonproportional per error set (engine.py:527-576), the data-harvesting mode.
  *   Every non-final stage branches each prefix into up to `nonfinal_shots` DISTINCT children
- *   (weighted choice without replacement, engine.py:549-556); the final stage emits, per prefix,
+ *   (weighted choice without replacement, engine.py:549-556; outcomes below 2^-40 (c128) / 2^-17 (c64)
+ *   of the row maximum count as zero probability); the final stage emits, per prefix,
  *   final_mode 0: every outcome whose conditional probability reaches `threshold`, count 1, tagged
  *                 with that probability in probs[] (engine.py:562-568),
  *   final_mode 1: a multinomial split of `direct_count` shots, probs[] = -1 (engine.py:569-574).
