@@ -45,6 +45,19 @@ def test_no_cpu_fallback():
 
     with pytest.raises(DeviceError):
         contract_pair(Tensor([Index(0, 2)], [1, 0]), Tensor([Index(0, 2)], [1, 0]))
+    # the widened rows (non-proportional sampler, run_ptsbe in both modes) have no CPU path either
+    from paper_2604_08467_b200 import workloads
+    from paper_2604_08467_b200.engine import (BatchPlan, CircuitNetwork, ErrorSet, RunConfig, run_ptsbe,
+                                              sample_nonproportional)
+
+    c, sizes = workloads.ghz(4, p=0.1)
+    k = ErrorSet(0, tuple("I" * len(g.targets) for g in c.gates), 1)
+    with pytest.raises(DeviceError):
+        sample_nonproportional(CircuitNetwork.from_circuit(c), k, BatchPlan(sizes), np.random.default_rng(0))
+    for mode in ("ptsbe-proportional", "ptsbe-nonproportional"):
+        with pytest.raises(DeviceError):
+            run_ptsbe(c, RunConfig(n=4, g=len(c.gates), mode=mode, batch_sizes=sizes, error_sets=2, total_shots=4,
+                                   hypersamples=2))
 
 
 def test_product_does_not_import_oracle():
