@@ -195,7 +195,7 @@ __device__ __forceinline__ void tiled_step(const C* __restrict__ A, const C* __r
 // TILED   : (with MEMO) large steps run in their separable form with register tiles; costs
 //           registers, so only programs dominated by such steps use it
 template <typename R, int GS, bool MEMO, bool TILED = false>
-__global__ void __launch_bounds__(TILED ? 512 : 256, TILED ? 1 : 5) exec_kernel(const ExecArgs a) {
+__global__ void __launch_bounds__(256, TILED ? 3 : 5) exec_kernel(const ExecArgs a) {
   using C = typename CxT<R>::type;
   constexpr bool WARP = GS > 0;
   constexpr int GSD = GS > 0 ? GS : 1;
