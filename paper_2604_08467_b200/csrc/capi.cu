@@ -992,7 +992,11 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       ea.words = words;
       ea.offset = pl->offsets[j - 1];
       ea.b = b;
-      expand_kernel<<<cdiv(Un, T), T, 0, st>>>(ea);
+      // few children per parent (late stages): parent-side scatter; otherwise child-side binary search
+      if (words <= 4 && (uint64_t)Un <= 4ull * U)
+        expand_scatter_kernel<<<cdiv(U, T), T, 0, st>>>(ea, nnz.as<uint32_t>());
+      else
+        expand_kernel<<<cdiv(Un, T), T, 0, st>>>(ea);
       g_launches++;
       if (np_exhaustive && j == f) {
         out.probs.alloc((size_t)Un * 8, ws_out);

@@ -624,6 +624,38 @@ __global__ void expand_kernel(const ExpandArgs a) {
   }
 }
 
+// Same result as expand_kernel, driven from the parent side: one thread per parent writes its
+// (few) children.  Late stages have 1-2 children per parent, where the per-child binary search over
+// tens of millions of scan entries (24 dependent loads) costs more than everything else in the
+// compaction; early stages (hundreds of children per parent) keep the child-side kernel.
+__global__ void expand_scatter_kernel(const ExpandArgs a, const uint32_t* __restrict__ nnz) {
+  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= a.p_n) return;
+  const uint32_t n = nnz[w];
+  if (n == 0) return;
+  const uint32_t base = a.child_base[w], slot0 = a.p_slot_off[w], es = a.p_eset[w];
+  uint64_t pv[4];
+  const uint32_t words = min(a.words, 4u);
+  for (uint32_t wd = 0; wd < words; ++wd) pv[wd] = a.p_prefix[(size_t)wd * a.p_n + w];
+  for (uint32_t k = 0; k < n; ++k) {
+    const uint32_t c = base + k;
+    const uint32_t idx = a.slot_index[slot0 + k];
+    a.c_eset[c] = es;
+    a.c_parent[c] = w;
+    a.c_mult[c] = a.slot_count[slot0 + k];
+    for (uint32_t wd = 0; wd < words; ++wd) {
+      uint64_t v = pv[wd];
+      const int q0 = (int)wd * 64, q1 = q0 + 64;
+      const int s = max(q0, (int)a.offset), e = min(q1, (int)(a.offset + a.b));
+      for (int q = s; q < e; ++q) {
+        const uint64_t bit = (idx >> (a.b - 1 - (q - a.offset))) & 1u;
+        v |= bit << (63 - (q - q0));
+      }
+      a.c_prefix[(size_t)wd * a.c_n + c] = v;
+    }
+  }
+}
+
 // rank of an item inside its error set = index - first index of that error set
 __global__ void segment_start_kernel(const uint32_t* eset, uint32_t n, uint32_t* seg_start) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
