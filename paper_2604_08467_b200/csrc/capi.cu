@@ -1803,7 +1803,7 @@ int ptsbe_sample_nonproportional(ptsbe_plan* pl, const uint8_t* kraus_idx, const
     std::lock_guard<std::mutex> lock(pl->mu);
     CK(cudaSetDevice(pl->device));
     cudaStream_t st = pl->stream;
-    const uint32_t f = pl->f, words = pl->words;
+    const uint32_t f = pl->f;
     NonpropParams np{nonfinal_shots, final_mode, direct_count, threshold};
     // slots any stage can need: items_j <= n_sets * nonfinal^(j-1), each with its multiplicity
     double bound = 0, items = (double)n_sets;
