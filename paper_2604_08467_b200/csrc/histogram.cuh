@@ -88,6 +88,102 @@ __global__ void widen_counts_kernel(const uint32_t* in, uint64_t* out, uint64_t 
   if (i < n) out[i] = in[i];
 }
 
+// ---- one-word keys, already sorted together with their u32 counts ----------------------------
+// The segment heads, the head scan and the u64 count scan are done tile by tile straight from the
+// sorted (key, count) arrays: one reduce pass, a scan of the per-tile totals, one emit pass.
+constexpr int HT_THREADS = 256;
+constexpr int HT_ITEMS = 8;
+constexpr int HT_TILE = HT_THREADS * HT_ITEMS;
+
+__device__ __forceinline__ void hist_tile_load(const uint64_t* __restrict__ keys,
+                                               const uint32_t* __restrict__ counts, uint64_t base,
+                                               uint64_t n, uint64_t (&k)[HT_ITEMS],
+                                               uint32_t (&c)[HT_ITEMS], uint64_t& prev) {
+  if (base + HT_ITEMS <= n) {
+    const ulonglong2* kp = reinterpret_cast<const ulonglong2*>(keys + base);
+    const uint4* cp = reinterpret_cast<const uint4*>(counts + base);
+#pragma unroll
+    for (int i = 0; i < HT_ITEMS / 2; ++i) { const ulonglong2 v = kp[i]; k[2 * i] = v.x; k[2 * i + 1] = v.y; }
+#pragma unroll
+    for (int i = 0; i < HT_ITEMS / 4; ++i) {
+      const uint4 v = cp[i];
+      c[4 * i] = v.x; c[4 * i + 1] = v.y; c[4 * i + 2] = v.z; c[4 * i + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < HT_ITEMS; ++i) {
+      k[i] = base + i < n ? keys[base + i] : 0;
+      c[i] = base + i < n ? counts[base + i] : 0;
+    }
+  }
+  prev = (base && base < n) ? keys[base - 1] : 0;
+}
+
+// is item i of this thread (global index base + i) the first record of its key?
+__device__ __forceinline__ uint32_t hist_is_head(const uint64_t (&k)[HT_ITEMS], uint64_t prev,
+                                                 uint64_t base, uint64_t n, int i) {
+  if (base + i >= n) return 0;
+  if (base + i == 0) return 1;
+  return k[i] != (i ? k[i - 1] : prev);
+}
+
+__global__ void __launch_bounds__(HT_THREADS)
+hist_tile_reduce_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ counts,
+                        uint64_t n, uint32_t* __restrict__ tile_heads,
+                        uint64_t* __restrict__ tile_sums) {
+  __shared__ uint32_t wh[HT_THREADS / 32];
+  __shared__ uint64_t wsum[HT_THREADS / 32];
+  const uint64_t base = (uint64_t)blockIdx.x * HT_TILE + (uint64_t)threadIdx.x * HT_ITEMS;
+  uint64_t k[HT_ITEMS], prev;
+  uint32_t c[HT_ITEMS];
+  hist_tile_load(keys, counts, base, n, k, c, prev);
+  uint32_t heads = 0;
+  uint64_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < HT_ITEMS; ++i) { heads += hist_is_head(k, prev, base, n, i); sum += c[i]; }
+#pragma unroll
+  for (int d = 16; d; d >>= 1) {
+    heads += __shfl_xor_sync(0xffffffffu, heads, d);
+    sum += __shfl_xor_sync(0xffffffffu, sum, d);
+  }
+  if ((threadIdx.x & 31) == 0) { wh[threadIdx.x >> 5] = heads; wsum[threadIdx.x >> 5] = sum; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t h = 0;
+    uint64_t t = 0;
+#pragma unroll
+    for (int w = 0; w < HT_THREADS / 32; ++w) { h += wh[w]; t += wsum[w]; }
+    tile_heads[blockIdx.x] = h;
+    tile_sums[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(HT_THREADS)
+hist_tile_emit_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ counts,
+                      uint64_t n, const uint32_t* __restrict__ tile_head_off,
+                      const uint64_t* __restrict__ tile_sum_off, uint64_t* __restrict__ out_keys,
+                      uint64_t* __restrict__ seg_begin) {
+  __shared__ uint32_t ws32[33];
+  __shared__ uint64_t ws64[33];
+  const uint64_t base = (uint64_t)blockIdx.x * HT_TILE + (uint64_t)threadIdx.x * HT_ITEMS;
+  uint64_t k[HT_ITEMS], prev;
+  uint32_t c[HT_ITEMS];
+  hist_tile_load(keys, counts, base, n, k, c, prev);
+  uint32_t h[HT_ITEMS], heads = 0;
+  uint64_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < HT_ITEMS; ++i) { h[i] = hist_is_head(k, prev, base, n, i); heads += h[i]; sum += c[i]; }
+  uint32_t th;
+  uint64_t ts;
+  uint32_t row = block_exclusive<uint32_t>(heads, ws32, &th) + tile_head_off[blockIdx.x];
+  uint64_t run = block_exclusive<uint64_t>(sum, ws64, &ts) + tile_sum_off[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < HT_ITEMS; ++i) {
+    if (h[i]) { out_keys[row] = k[i]; seg_begin[row] = run; ++row; }
+    run += c[i];
+  }
+}
+
 struct Histogram {
   DevBuf keys;    // [n][words] row-major
   DevBuf counts;  // [n] u64
@@ -102,11 +198,7 @@ inline void reduce_by_key(const uint64_t* keys, uint64_t stride, uint32_t words,
   if (n == 0) { out.keys.alloc(0, st); out.counts.alloc(0, st); return; }
   if (n >= (1ull << 32)) throw Failure(PTSBE_ECAPACITY, "more than 2^32 records in one reduce");
   const unsigned T = 256, G = cdiv(n, T);
-  DevBuf perm_a(n * 4, st), perm_b(n * 4, st), kin(n * 8, st), kout(n * 8, st);
-  iota_kernel<<<G, T, 0, st>>>(perm_a.as<uint32_t>(), (uint32_t)n, 0);
-  g_launches++;
-  uint32_t* pin = perm_a.as<uint32_t>();
-  uint32_t* pout = perm_b.as<uint32_t>();
+  DevBuf kout(n * 8, st);
   DevBuf sorted_counts;
   if (words == 1 && counts32 && key_bits >= 1) {
     // one key word: sort the (key, count) pairs themselves; everything downstream then reads
@@ -120,10 +212,34 @@ inline void reduce_by_key(const uint64_t* keys, uint64_t stride, uint32_t words,
     CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys, kout.as<uint64_t>(), counts32,
                                        sorted_counts.as<uint32_t>(), (int)n, 64 - used, 64, st));
     g_launches += 1 + (used + 7) / 8 * 2;
-    keys = kout.as<uint64_t>();
-    stride = n;
-    counts32 = sorted_counts.as<uint32_t>();
-  } else
+    const uint64_t* sk = kout.as<uint64_t>();
+    const uint32_t* sc = sorted_counts.as<uint32_t>();
+    const unsigned tiles = (unsigned)cdiv(n, (uint64_t)HT_TILE);
+    DevBuf th(tiles * 4, st), tho(tiles * 4, st), ts(tiles * 8, st), tso(tiles * 8, st), tot(16, st);
+    hist_tile_reduce_kernel<<<tiles, HT_THREADS, 0, st>>>(sk, sc, n, th.as<uint32_t>(), ts.as<uint64_t>());
+    g_launches++;
+    exclusive_scan<uint32_t, uint32_t>(th.as<uint32_t>(), tho.as<uint32_t>(), tiles, tot.as<uint32_t>(), st);
+    exclusive_scan<uint64_t, uint64_t>(ts.as<uint64_t>(), tso.as<uint64_t>(), tiles, tot.as<uint64_t>() + 1, st);
+    struct { uint32_t heads; uint32_t pad; uint64_t total; } h;
+    CK(cudaMemcpyAsync(&h, tot.p, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    out.n = h.heads;
+    out.keys.alloc((size_t)out.n * 8, st);
+    out.counts.alloc((size_t)out.n * 8, st);
+    DevBuf seg(out.n * 8, st);
+    hist_tile_emit_kernel<<<tiles, HT_THREADS, 0, st>>>(sk, sc, n, tho.as<uint32_t>(), tso.as<uint64_t>(),
+                                                        out.keys.as<uint64_t>(), seg.as<uint64_t>());
+    segment_counts_kernel<<<cdiv(out.n, T), T, 0, st>>>(seg.as<uint64_t>(), h.total, out.n,
+                                                        out.counts.as<uint64_t>());
+    g_launches += 2;
+    CK(cudaGetLastError());
+    return;
+  }
+  DevBuf perm_a(n * 4, st), perm_b(n * 4, st), kin(n * 8, st);
+  iota_kernel<<<G, T, 0, st>>>(perm_a.as<uint32_t>(), (uint32_t)n, 0);
+  g_launches++;
+  uint32_t* pin = perm_a.as<uint32_t>();
+  uint32_t* pout = perm_b.as<uint32_t>();
   for (int w = (int)words - 1; w >= 0; --w) {
     // bits used in word w: qubits [64w, min(64w+64, key_bits)) occupy the top of the word
     const int used = (int)key_bits - 64 * w >= 64 ? 64 : (int)key_bits - 64 * w;
