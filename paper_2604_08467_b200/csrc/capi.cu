@@ -561,25 +561,26 @@ static void launch_project(ptsbe_plan* pl, const Program& pr, const void* v, uin
   a.N = pr.d.out_elems;
   a.rec_stride = rec_stride;
   a.m_off = pr.d.result_ref;
-  const uint64_t tiles = (uint64_t)cdiv(n, PJ_TI) * cdiv(a.N, PJ_TN);
-  const size_t smem_f = 2 * (size_t)ProjK<float>::KC * (PJ_TI + PJ_TN) * sizeof(float2);    // two-deep ring
-  const size_t smem_d = 2 * (size_t)ProjK<double>::KC * (PJ_TI + PJ_TN) * sizeof(double2);
-  static int per_sm_f = 0, per_sm_d = 0;
-  if (!per_sm_f) {
-    CK(cudaFuncSetAttribute(project_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
-    CK(cudaFuncSetAttribute(project_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_d, project_kernel<double>, PJ_THREADS, smem_d));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_f, project_kernel<float>, PJ_THREADS, smem_f));
-    per_sm_f = std::max(per_sm_f, 1);
-    per_sm_d = std::max(per_sm_d, 1);
+  // column tile: 64 when the whole row fits (no dead columns), else 128
+  const int narrow = a.N <= 64;
+  const uint32_t tn = narrow ? 64 : PJ_TN;
+  const uint64_t tiles = (uint64_t)cdiv(n, PJ_TI) * cdiv(a.N, tn);
+  const bool f32 = pl->dtype == PTSBE_C64;
+  const size_t smem = f32 ? 2 * (size_t)ProjK<float>::KC * (PJ_TI + tn) * sizeof(float2)    // two-deep ring
+                          : 2 * (size_t)ProjK<double>::KC * (PJ_TI + tn) * sizeof(double2);
+  using Kern = void (*)(const ProjectArgs);
+  static const Kern kern[2][2] = {{project_kernel<double, PJ_TN>, project_kernel<double, 64>},
+                                  {project_kernel<float, PJ_TN>, project_kernel<float, 64>}};
+  static int per_sm[2][2] = {{0, 0}, {0, 0}};
+  int& occ = per_sm[f32][narrow];
+  const Kern k = kern[f32][narrow];
+  if (!occ) {
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, PJ_THREADS, smem));
+    occ = std::max(occ, 1);
   }
-  if (pl->dtype == PTSBE_C64) {
-    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)pl->sm_count * per_sm_f);
-    project_kernel<float><<<grid, PJ_THREADS, smem_f, pl->stream>>>(a);
-  } else {
-    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)pl->sm_count * per_sm_d);
-    project_kernel<double><<<grid, PJ_THREADS, smem_d, pl->stream>>>(a);
-  }
+  const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)pl->sm_count * occ);
+  k<<<grid, PJ_THREADS, smem, pl->stream>>>(a);
   g_launches++;
   CK(cudaGetLastError());
 }

@@ -207,6 +207,23 @@ def test_descent_sampler_bit_exact_vs_oracle_complex128(monkeypatch):
     assert dict(ctx.stats.stage_events) == events
 
 
+@pytest.mark.parametrize("sets,shots", [(3, 5000), (12, 600), (150, 12)])
+def test_projection_tiles_spanning_error_sets_bit_exact(monkeypatch, sets, shots):
+    """Dense projection (csrc/project.cuh) with the descent sampler off: 64-item tiles holding
+    one error set, a few runs of error sets (computed once per run) and more than eight of them
+    (per-item path) all give the oracle's records (reference engine.py:442-450, 513-523)."""
+    monkeypatch.setenv("PTSBE_DESCENT", "0")
+    c, tpl, es = _hea_case(12, 4, sets, shots, 21, gamma=0.0)  # unitary errors only: no impossible sets
+    sizes = (4, 4, 4)
+    ctx = SamplerContext(hypersamples=8, dtype="complex128")
+    per_set = sample_proportional_batched(tpl, es, BatchPlan(sizes), 13, ctx)
+    assert not ctx.stats.descent_events
+    ops, finals = bridge.template_of(c)
+    _, want, events = O.run_proportional(ops, finals, sizes, bridge.oracle_errorsets(c, es), 13)
+    assert [[(r.bitstring, r.count) for r in recs] for recs in per_set] == want
+    assert dict(ctx.stats.stage_events) == events
+
+
 @pytest.mark.parametrize("dtype", ["complex128", "complex64"])
 def test_descent_sampler_agrees_with_flat_sampler(monkeypatch, dtype):
     """Descent on vs off on a 16-qubit HEA (D = 64 cut): identical records in
