@@ -43,10 +43,32 @@ __device__ __forceinline__ T block_exclusive(T v, T* warp_sums, T* total) {
   return r;
 }
 
+// per-tile sums only (first pass of a multi-tile scan: nothing but the totals is written)
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(SCAN_THREADS)
-scan_tile_kernel(const TI* __restrict__ in, TO* __restrict__ out, TO* __restrict__ tile_sums,
-                 uint64_t n) {
+scan_reduce_kernel(const TI* __restrict__ in, TO* __restrict__ tile_sums, uint64_t n) {
+  __shared__ TO ws[SCAN_THREADS / 32];
+  const uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_ITEMS;
+  TO local = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; ++i) local += (base + i < n) ? (TO)in[base + i] : TO(0);
+#pragma unroll
+  for (int d = 16; d; d >>= 1) local += __shfl_xor_sync(0xffffffffu, local, d);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    TO t = 0;
+#pragma unroll
+    for (int w = 0; w < SCAN_THREADS / 32; ++w) t += ws[w];
+    tile_sums[blockIdx.x] = t;
+  }
+}
+
+// scan of one tile, shifted by the tile's offset when given; writes the tile total when asked
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(SCAN_THREADS)
+scan_tile_kernel(const TI* in, TO* out, TO* __restrict__ tile_sums,
+                 const TO* __restrict__ tile_offsets, uint64_t n) {
   __shared__ TO ws[33];
   const uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_ITEMS;
   TO v[SCAN_ITEMS];
@@ -58,22 +80,13 @@ scan_tile_kernel(const TI* __restrict__ in, TO* __restrict__ out, TO* __restrict
   }
   TO total;
   TO run = block_exclusive<TO>(local, ws, &total);
+  if (tile_offsets) run += tile_offsets[blockIdx.x];
 #pragma unroll
   for (int i = 0; i < SCAN_ITEMS; ++i) {
     if (base + i < n) out[base + i] = run;
     run += v[i];
   }
   if (threadIdx.x == 0 && tile_sums) tile_sums[blockIdx.x] = total;
-}
-
-template <typename TO>
-__global__ void __launch_bounds__(SCAN_THREADS)
-scan_add_kernel(TO* __restrict__ out, const TO* __restrict__ tile_offsets, uint64_t n) {
-  const uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_ITEMS;
-  const TO off = tile_offsets[blockIdx.x];
-#pragma unroll
-  for (int i = 0; i < SCAN_ITEMS; ++i)
-    if (base + i < n) out[base + i] += off;
 }
 
 template <typename TO>
@@ -93,15 +106,18 @@ void exclusive_scan(const TI* in, TO* out, uint64_t n, TO* total_dev, cudaStream
     return;
   }
   const uint64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-  DevBuf sums(tiles * sizeof(TO), st), offs(tiles * sizeof(TO), st);
-  scan_tile_kernel<TI, TO><<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, out, sums.as<TO>(), n);
-  g_launches++;
+  DevBuf sums(tiles * sizeof(TO), st);
   if (tiles > 1) {
+    // reduce, scan the tile totals, scan every tile from its offset: 12 bytes per u32 element
+    DevBuf offs(tiles * sizeof(TO), st);
+    scan_reduce_kernel<TI, TO><<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, sums.as<TO>(), n);
     exclusive_scan<TO, TO>(sums.as<TO>(), offs.as<TO>(), tiles, total_dev, st);
-    scan_add_kernel<TO><<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(out, offs.as<TO>(), n);
+    scan_tile_kernel<TI, TO><<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, out, nullptr, offs.as<TO>(), n);
+    g_launches += 2;
+  } else {
+    scan_tile_kernel<TI, TO><<<1, SCAN_THREADS, 0, st>>>(in, out, sums.as<TO>(), nullptr, n);
     g_launches++;
-  } else if (total_dev) {
-    CK(cudaMemcpyAsync(total_dev, sums.p, sizeof(TO), cudaMemcpyDeviceToDevice, st));
+    if (total_dev) CK(cudaMemcpyAsync(total_dev, sums.p, sizeof(TO), cudaMemcpyDeviceToDevice, st));
   }
   CK(cudaGetLastError());
 }
