@@ -417,12 +417,25 @@ def test_many_error_sets_single_shot_descent():
     kraus = workloads.presample_matrix(c, sets, np.random.default_rng(2))
     ctx = SamplerContext(hypersamples=8, dtype="complex64")
     pipe = DevicePipeline(tpl, BatchPlan((8, 8, 1)), tables, ctx, shots_per_set=1.0)
+    ids = np.arange(sets, dtype=np.uint32)
     try:
-        keys, _, counts, st = pipe.device_plan.sample(kraus, np.ones(sets, np.uint32), np.arange(sets, dtype=np.uint32), 3)
+        keys, _, counts, st = pipe.device_plan.sample(kraus, np.ones(sets, np.uint32), ids, 3)
+        keys, counts = np.array(keys), np.array(counts)
+        halves = []
+        for lo, hi in ((0, 30_001), (30_001, sets)):  # streams are keyed by the global id: halves add up
+            k, _, c, _ = pipe.device_plan.sample(kraus[lo:hi], np.ones(hi - lo, np.uint32), ids[lo:hi], 3)
+            halves.append((np.array(k), np.array(c)))
     finally:
         pipe.close()
     assert int(counts.sum()) + 0 == sets - 0 * int(st.flagged_sets)
     assert int(st.flagged_sets) == 0
+    # few distinct keys, 70 000 records: segments of equal keys span many 2048-record tiles of the
+    # one-word histogram tail; output strictly increasing, and equal to the generic (u64-count,
+    # permutation-based) merge of the two halves
+    assert np.all(keys[1:, 0] > keys[:-1, 0])
+    from paper_2604_08467_b200 import _capi
+    mk, mc = _capi.histogram_merge(np.concatenate([h[0] for h in halves]), np.concatenate([h[1] for h in halves]))
+    assert np.array_equal(mk, keys) and np.array_equal(mc.astype(np.uint64), counts.astype(np.uint64))
 
 
 def _nonprop_runs():
