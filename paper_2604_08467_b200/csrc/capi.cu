@@ -535,9 +535,16 @@ static void launch_tree_build(ptsbe_plan* pl, const Program& pr, const void* rec
   t.b = b;
   t.dpad = dpad;
   t.n_sets = n_sets;
-  const dim3 grid(n_sets, cdiv(((uint64_t)dpad) << b, 256));  // error sets on x: up to 2^31 - 1
-  if (pl->dtype == PTSBE_C64) tree_build_kernel<float><<<grid, 256, 0, pl->stream>>>(t);
-  else tree_build_kernel<double><<<grid, 256, 0, pl->stream>>>(t);
+  static const bool reduce_tree = env_size("PTSBE_TREE_REDUCE", 1) != 0;
+  if (b <= (uint32_t)TB_MAX_B && reduce_tree) {
+    const dim3 grid(n_sets, cdiv(dpad, (uint32_t)TB_ROWS));
+    if (pl->dtype == PTSBE_C64) tree_reduce_kernel<float><<<grid, TB_ROWS * 32, 0, pl->stream>>>(t);
+    else tree_reduce_kernel<double><<<grid, TB_ROWS * 32, 0, pl->stream>>>(t);
+  } else {
+    const dim3 grid(n_sets, cdiv(((uint64_t)dpad) << b, 256));  // error sets on x: up to 2^31 - 1
+    if (pl->dtype == PTSBE_C64) tree_build_kernel<float><<<grid, 256, 0, pl->stream>>>(t);
+    else tree_build_kernel<double><<<grid, 256, 0, pl->stream>>>(t);
+  }
   g_launches++;
   CK(cudaGetLastError());
 }

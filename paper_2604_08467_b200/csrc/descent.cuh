@@ -73,6 +73,58 @@ __global__ void tree_build_kernel(const TreeArgs a) {
   *out = s;
 }
 
+// Same table for b <= TB_MAX_B, built as a reduction tree: a CTA owns TB_ROWS consecutive d of one
+// error set, warp w reads row M[d0 + w][0 .. N) once (coalesced), sums pairs level by level in
+// shared memory (double), and the CTA writes every node's TB_ROWS consecutive d as one 32/64-byte
+// piece.  tree_build_kernel above reads each row b/2 + 1 times with a stride of N between lanes.
+constexpr int TB_ROWS = 4;
+constexpr int TB_MAX_B = 8;
+
+template <typename R>
+__global__ void __launch_bounds__(TB_ROWS * 32) tree_reduce_kernel(const TreeArgs a) {
+  using C = typename CxT<R>::type;
+  __shared__ double2 nodes[TB_ROWS][2 << TB_MAX_B];  // level k (blocks of 2^k columns) at off_k + q
+  const uint32_t N = 1u << a.b;
+  const uint32_t e = blockIdx.x, d0 = blockIdx.y * TB_ROWS;
+  const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t d = d0 + w;
+  double2* nd = nodes[w];
+  if (d < a.D) {
+    const C* M = reinterpret_cast<const C*>(a.rec0) + (size_t)e * a.rec_stride + a.m_off + (size_t)d * N;
+    for (uint32_t c = lane; c < N; c += 32) { const C m = M[c]; nd[c] = make_double2((double)m.x, (double)m.y); }
+  } else {
+    for (uint32_t c = lane; c < N; c += 32) nd[c] = make_double2(0.0, 0.0);
+  }
+  __syncwarp();
+  uint32_t off = 0;
+  for (uint32_t k = 1; k <= a.b; ++k) {
+    const uint32_t prev = off, n_prev = N >> (k - 1);
+    off += n_prev;
+    for (uint32_t q = lane; q < (n_prev >> 1); q += 32) {
+      const double2 l = nd[prev + 2 * q], r = nd[prev + 2 * q + 1];
+      nd[off + q] = make_double2(l.x + r.x, l.y + r.y);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // node idx: 0 = all columns = level b, q 0; idx = 2^(t-1) + parent -> level b - t, q = 2 * parent
+  C* out = reinterpret_cast<C*>(a.tree) + (size_t)e * N * a.dpad + d0;
+  for (uint32_t i = threadIdx.x; i < N * TB_ROWS; i += TB_ROWS * 32) {
+    const uint32_t idx = i / TB_ROWS, dd = i % TB_ROWS;
+    if (d0 + dd >= a.dpad) continue;
+    uint32_t k = a.b, q = 0;
+    if (idx) {
+      const uint32_t t = 32 - __clz(idx);
+      k = a.b - t;
+      q = 2 * (idx - (1u << (t - 1)));
+    }
+    const uint32_t lvl = 2 * N - (2 * N >> k);  // off_k = N + N/2 + ... = 2N (1 - 2^-k)
+    const double2 v = nodes[dd][lvl + q];
+    C o; o.x = (R)v.x; o.y = (R)v.y;
+    out[(size_t)idx * a.dpad + dd] = o;
+  }
+}
+
 struct DescentArgs {
   const void* v;            // [items of this launch][dpad] complex, row per item, zero padded
   const void* tree;         // [error sets][N][dpad] complex
