@@ -705,6 +705,38 @@ __global__ void dedup_kernel(const DedupArgs a) {
   if (m < 2 || m > LN_DEDUP_SERIAL) return;
   uint32_t* idx = a.slot_index + a.slot_off[item];
   uint32_t* cnt = a.slot_count + a.slot_off[item];
+  if (m <= 8) {
+    // the common case: all draws in registers (one round of independent loads), 19-comparator
+    // odd-even merge network, run-length merge straight from the registers
+    uint32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = (uint32_t)i < m ? idx[i] : 0xFFFFFFFFu;
+#define PTSBE_CE(i, j) { const uint32_t lo = min(v[i], v[j]), hi = max(v[i], v[j]); v[i] = lo; v[j] = hi; }
+    PTSBE_CE(0, 1) PTSBE_CE(2, 3) PTSBE_CE(4, 5) PTSBE_CE(6, 7)
+    PTSBE_CE(0, 2) PTSBE_CE(1, 3) PTSBE_CE(4, 6) PTSBE_CE(5, 7)
+    PTSBE_CE(1, 2) PTSBE_CE(5, 6)
+    PTSBE_CE(0, 4) PTSBE_CE(1, 5) PTSBE_CE(2, 6) PTSBE_CE(3, 7)
+    PTSBE_CE(2, 4) PTSBE_CE(3, 5)
+    PTSBE_CE(1, 2) PTSBE_CE(3, 4) PTSBE_CE(5, 6)
+#undef PTSBE_CE
+    uint32_t out = 0, run = 1;
+#pragma unroll
+    for (int i = 1; i <= 8; ++i) {
+      if ((uint32_t)i <= m) {
+        const bool same = (uint32_t)i < m && v[i < 8 ? i : 7] == v[i - 1];
+        if (same) {
+          ++run;
+        } else {
+          idx[out] = v[i - 1];
+          cnt[out] = run;
+          ++out;
+          run = 1;
+        }
+      }
+    }
+    a.nnz[item] = out;
+    return;
+  }
   for (uint32_t i = 1; i < m; ++i) {
     const uint32_t x = idx[i];
     uint32_t j = i;
