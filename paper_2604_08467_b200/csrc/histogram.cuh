@@ -95,15 +95,25 @@ constexpr int HT_THREADS = 256;
 constexpr int HT_ITEMS = 8;
 constexpr int HT_TILE = HT_THREADS * HT_ITEMS;
 
-__device__ __forceinline__ void hist_tile_load(const uint64_t* __restrict__ keys,
+template <typename K>
+__device__ __forceinline__ void hist_tile_load(const K* __restrict__ keys,
                                                const uint32_t* __restrict__ counts, uint64_t base,
-                                               uint64_t n, uint64_t (&k)[HT_ITEMS],
-                                               uint32_t (&c)[HT_ITEMS], uint64_t& prev) {
+                                               uint64_t n, K (&k)[HT_ITEMS],
+                                               uint32_t (&c)[HT_ITEMS], K& prev) {
   if (base + HT_ITEMS <= n) {
-    const ulonglong2* kp = reinterpret_cast<const ulonglong2*>(keys + base);
-    const uint4* cp = reinterpret_cast<const uint4*>(counts + base);
+    if constexpr (sizeof(K) == 8) {
+      const ulonglong2* kp = reinterpret_cast<const ulonglong2*>(keys + base);
 #pragma unroll
-    for (int i = 0; i < HT_ITEMS / 2; ++i) { const ulonglong2 v = kp[i]; k[2 * i] = v.x; k[2 * i + 1] = v.y; }
+      for (int i = 0; i < HT_ITEMS / 2; ++i) { const ulonglong2 v = kp[i]; k[2 * i] = v.x; k[2 * i + 1] = v.y; }
+    } else {
+      const uint4* kp = reinterpret_cast<const uint4*>(keys + base);
+#pragma unroll
+      for (int i = 0; i < HT_ITEMS / 4; ++i) {
+        const uint4 v = kp[i];
+        k[4 * i] = v.x; k[4 * i + 1] = v.y; k[4 * i + 2] = v.z; k[4 * i + 3] = v.w;
+      }
+    }
+    const uint4* cp = reinterpret_cast<const uint4*>(counts + base);
 #pragma unroll
     for (int i = 0; i < HT_ITEMS / 4; ++i) {
       const uint4 v = cp[i];
@@ -112,29 +122,31 @@ __device__ __forceinline__ void hist_tile_load(const uint64_t* __restrict__ keys
   } else {
 #pragma unroll
     for (int i = 0; i < HT_ITEMS; ++i) {
-      k[i] = base + i < n ? keys[base + i] : 0;
+      k[i] = base + i < n ? keys[base + i] : K(0);
       c[i] = base + i < n ? counts[base + i] : 0;
     }
   }
-  prev = (base && base < n) ? keys[base - 1] : 0;
+  prev = (base && base < n) ? keys[base - 1] : K(0);
 }
 
 // is item i of this thread (global index base + i) the first record of its key?
-__device__ __forceinline__ uint32_t hist_is_head(const uint64_t (&k)[HT_ITEMS], uint64_t prev,
+template <typename K>
+__device__ __forceinline__ uint32_t hist_is_head(const K (&k)[HT_ITEMS], K prev,
                                                  uint64_t base, uint64_t n, int i) {
   if (base + i >= n) return 0;
   if (base + i == 0) return 1;
   return k[i] != (i ? k[i - 1] : prev);
 }
 
+template <typename K>
 __global__ void __launch_bounds__(HT_THREADS)
-hist_tile_reduce_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ counts,
+hist_tile_reduce_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ counts,
                         uint64_t n, uint32_t* __restrict__ tile_heads,
                         uint64_t* __restrict__ tile_sums) {
   __shared__ uint32_t wh[HT_THREADS / 32];
   __shared__ uint64_t wsum[HT_THREADS / 32];
   const uint64_t base = (uint64_t)blockIdx.x * HT_TILE + (uint64_t)threadIdx.x * HT_ITEMS;
-  uint64_t k[HT_ITEMS], prev;
+  K k[HT_ITEMS], prev;
   uint32_t c[HT_ITEMS];
   hist_tile_load(keys, counts, base, n, k, c, prev);
   uint32_t heads = 0;
@@ -158,15 +170,25 @@ hist_tile_reduce_kernel(const uint64_t* __restrict__ keys, const uint32_t* __res
   }
 }
 
+// 32-bit keys are the top halves of the packed bitstrings (key_bits <= 32)
+__device__ __forceinline__ uint64_t hist_widen(uint64_t k) { return k; }
+__device__ __forceinline__ uint64_t hist_widen(uint32_t k) { return (uint64_t)k << 32; }
+
+__global__ void narrow_keys_kernel(const uint64_t* __restrict__ in, uint32_t* __restrict__ out, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (uint32_t)(in[i] >> 32);
+}
+
+template <typename K>
 __global__ void __launch_bounds__(HT_THREADS)
-hist_tile_emit_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ counts,
+hist_tile_emit_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ counts,
                       uint64_t n, const uint32_t* __restrict__ tile_head_off,
                       const uint64_t* __restrict__ tile_sum_off, uint64_t* __restrict__ out_keys,
                       uint64_t* __restrict__ seg_begin) {
   __shared__ uint32_t ws32[33];
   __shared__ uint64_t ws64[33];
   const uint64_t base = (uint64_t)blockIdx.x * HT_TILE + (uint64_t)threadIdx.x * HT_ITEMS;
-  uint64_t k[HT_ITEMS], prev;
+  K k[HT_ITEMS], prev;
   uint32_t c[HT_ITEMS];
   hist_tile_load(keys, counts, base, n, k, c, prev);
   uint32_t h[HT_ITEMS], heads = 0;
@@ -179,7 +201,7 @@ hist_tile_emit_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restr
   uint64_t run = block_exclusive<uint64_t>(sum, ws64, &ts) + tile_sum_off[blockIdx.x];
 #pragma unroll
   for (int i = 0; i < HT_ITEMS; ++i) {
-    if (h[i]) { out_keys[row] = k[i]; seg_begin[row] = run; ++row; }
+    if (h[i]) { out_keys[row] = hist_widen(k[i]); seg_begin[row] = run; ++row; }
     run += c[i];
   }
 }
@@ -190,6 +212,31 @@ struct Histogram {
   uint64_t n = 0;
 };
 
+// heads, head scan, u64 count scan and emission for sorted (key, count) pairs of one key word
+template <typename K>
+inline void sorted_pairs_tail(const K* sk, const uint32_t* sc, uint64_t n, Histogram& out, cudaStream_t st) {
+  const unsigned T = 256;
+  const unsigned tiles = (unsigned)cdiv(n, (uint64_t)HT_TILE);
+  DevBuf th(tiles * 4, st), tho(tiles * 4, st), ts(tiles * 8, st), tso(tiles * 8, st), tot(16, st);
+  hist_tile_reduce_kernel<K><<<tiles, HT_THREADS, 0, st>>>(sk, sc, n, th.as<uint32_t>(), ts.as<uint64_t>());
+  g_launches++;
+  exclusive_scan<uint32_t, uint32_t>(th.as<uint32_t>(), tho.as<uint32_t>(), tiles, tot.as<uint32_t>(), st);
+  exclusive_scan<uint64_t, uint64_t>(ts.as<uint64_t>(), tso.as<uint64_t>(), tiles, tot.as<uint64_t>() + 1, st);
+  struct { uint32_t heads; uint32_t pad; uint64_t total; } h;
+  CK(cudaMemcpyAsync(&h, tot.p, 16, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  out.n = h.heads;
+  out.keys.alloc((size_t)out.n * 8, st);
+  out.counts.alloc((size_t)out.n * 8, st);
+  DevBuf seg(out.n * 8, st);
+  hist_tile_emit_kernel<K><<<tiles, HT_THREADS, 0, st>>>(sk, sc, n, tho.as<uint32_t>(), tso.as<uint64_t>(),
+                                                         out.keys.as<uint64_t>(), seg.as<uint64_t>());
+  segment_counts_kernel<<<cdiv(out.n, T), T, 0, st>>>(seg.as<uint64_t>(), h.total, out.n,
+                                                      out.counts.as<uint64_t>());
+  g_launches += 2;
+  CK(cudaGetLastError());
+}
+
 // keys: SoA [words][stride] u64 on device; counts u32 (counts64 == nullptr) or u64.
 inline void reduce_by_key(const uint64_t* keys, uint64_t stride, uint32_t words,
                           const uint32_t* counts32, const uint64_t* counts64, uint64_t n,
@@ -198,44 +245,39 @@ inline void reduce_by_key(const uint64_t* keys, uint64_t stride, uint32_t words,
   if (n == 0) { out.keys.alloc(0, st); out.counts.alloc(0, st); return; }
   if (n >= (1ull << 32)) throw Failure(PTSBE_ECAPACITY, "more than 2^32 records in one reduce");
   const unsigned T = 256, G = cdiv(n, T);
-  DevBuf kout(n * 8, st);
+  DevBuf kout;
   DevBuf sorted_counts;
   if (words == 1 && counts32 && key_bits >= 1) {
-    // one key word: sort the (key, count) pairs themselves; everything downstream then reads
-    // sorted arrays through the identity permutation (coalesced) instead of gathering through one
+    // one key word: sort the (key, count) pairs themselves, then reduce tile by tile from the
+    // sorted arrays.  Keys of at most 32 bits are sorted as u32 (8 instead of 12 bytes per pair
+    // and radix pass).
     const int used = (int)std::min<uint32_t>(key_bits, 64);
     sorted_counts.alloc(n * 4, st);
     size_t tmp_bytes = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, kout.as<uint64_t>(), counts32,
-                                       sorted_counts.as<uint32_t>(), (int)n, 64 - used, 64, st));
-    DevBuf tmp(tmp_bytes, st);
-    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys, kout.as<uint64_t>(), counts32,
-                                       sorted_counts.as<uint32_t>(), (int)n, 64 - used, 64, st));
-    g_launches += 1 + (used + 7) / 8 * 2;
-    const uint64_t* sk = kout.as<uint64_t>();
-    const uint32_t* sc = sorted_counts.as<uint32_t>();
-    const unsigned tiles = (unsigned)cdiv(n, (uint64_t)HT_TILE);
-    DevBuf th(tiles * 4, st), tho(tiles * 4, st), ts(tiles * 8, st), tso(tiles * 8, st), tot(16, st);
-    hist_tile_reduce_kernel<<<tiles, HT_THREADS, 0, st>>>(sk, sc, n, th.as<uint32_t>(), ts.as<uint64_t>());
-    g_launches++;
-    exclusive_scan<uint32_t, uint32_t>(th.as<uint32_t>(), tho.as<uint32_t>(), tiles, tot.as<uint32_t>(), st);
-    exclusive_scan<uint64_t, uint64_t>(ts.as<uint64_t>(), tso.as<uint64_t>(), tiles, tot.as<uint64_t>() + 1, st);
-    struct { uint32_t heads; uint32_t pad; uint64_t total; } h;
-    CK(cudaMemcpyAsync(&h, tot.p, 16, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    out.n = h.heads;
-    out.keys.alloc((size_t)out.n * 8, st);
-    out.counts.alloc((size_t)out.n * 8, st);
-    DevBuf seg(out.n * 8, st);
-    hist_tile_emit_kernel<<<tiles, HT_THREADS, 0, st>>>(sk, sc, n, tho.as<uint32_t>(), tso.as<uint64_t>(),
-                                                        out.keys.as<uint64_t>(), seg.as<uint64_t>());
-    segment_counts_kernel<<<cdiv(out.n, T), T, 0, st>>>(seg.as<uint64_t>(), h.total, out.n,
-                                                        out.counts.as<uint64_t>());
-    g_launches += 2;
-    CK(cudaGetLastError());
+    if (used <= 32) {
+      DevBuf k32(n * 4, st), k32s(n * 4, st);
+      narrow_keys_kernel<<<G, T, 0, st>>>(keys, k32.as<uint32_t>(), n);
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k32.as<uint32_t>(), k32s.as<uint32_t>(), counts32,
+                                         sorted_counts.as<uint32_t>(), (int)n, 32 - used, 32, st));
+      DevBuf tmp(tmp_bytes, st);
+      CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, k32.as<uint32_t>(), k32s.as<uint32_t>(), counts32,
+                                         sorted_counts.as<uint32_t>(), (int)n, 32 - used, 32, st));
+      g_launches += 2 + (used + 7) / 8 * 2;
+      sorted_pairs_tail<uint32_t>(k32s.as<uint32_t>(), sorted_counts.as<uint32_t>(), n, out, st);
+    } else {
+      kout.alloc(n * 8, st);
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, kout.as<uint64_t>(), counts32,
+                                         sorted_counts.as<uint32_t>(), (int)n, 64 - used, 64, st));
+      DevBuf tmp(tmp_bytes, st);
+      CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys, kout.as<uint64_t>(), counts32,
+                                         sorted_counts.as<uint32_t>(), (int)n, 64 - used, 64, st));
+      g_launches += 1 + (used + 7) / 8 * 2;
+      sorted_pairs_tail<uint64_t>(kout.as<uint64_t>(), sorted_counts.as<uint32_t>(), n, out, st);
+    }
     return;
   }
   DevBuf perm_a(n * 4, st), perm_b(n * 4, st), kin(n * 8, st);
+  kout.alloc(n * 8, st);
   iota_kernel<<<G, T, 0, st>>>(perm_a.as<uint32_t>(), (uint32_t)n, 0);
   g_launches++;
   uint32_t* pin = perm_a.as<uint32_t>();
