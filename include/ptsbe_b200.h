@@ -122,6 +122,17 @@ typedef struct {
    * prefixes entering stage p+1 (p = j-1 is the marginal pass itself) */
   const ptsbe_program_desc* programs; /* stage-major, f*(f+1)/2 entries */
   uint64_t max_intermediate;          /* ceiling, informational (checked at compile time) */
+  /* Mean shots per error set of the WHOLE job (all ranks, all calls), or 0.  When > 0 the choice
+   * between the flat sampler and the per-qubit descent is made per stage from this number and the
+   * stage offset alone -- expected shots per work item = hint / min(hint, 2^offset_j) -- so it does
+   * not depend on how error sets are grouped into calls, chunks or ranks (determinism contract of
+   * the reference, tests/test_engine.py:455-463).  0: decided per chunk from its actual work list. */
+  double shots_per_set_hint;
+  /* [n_sites] number of operator variants (Kraus indices 0..v-1) of every gate site in this plan's
+   * tables, or NULL.  When given, every Kraus-index matrix handed to the plan is checked on the
+   * device and an out-of-range index (e.g. error sets encoded against other tables) is refused
+   * with PTSBE_EINVAL instead of gathering outside the operand pool. */
+  const uint8_t* site_variants;
 } ptsbe_plan_desc;
 
 typedef struct ptsbe_plan ptsbe_plan;

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import weakref
 from typing import Optional
 
 import numpy as np
@@ -196,29 +197,33 @@ class ResidentBatch:
     def __init__(self, plan: "DevicePlan", kraus_idx, shots, eset_ids):
         self.plan = plan
         self._h = ctypes.c_void_p()
+        plan._batches.add(self)  # the C batch holds a raw plan pointer: the plan closes us before it dies
         if kraus_idx is None:  # filled in by DevicePlan.presample
             return
-        kraus_idx = np.ascontiguousarray(kraus_idx, dtype=np.uint8)
-        shots = np.ascontiguousarray(shots, dtype=np.uint32)
-        ids = None if eset_ids is None else np.ascontiguousarray(eset_ids, dtype=np.uint32)
+        kraus_idx, shots, ids = plan._check_inputs(kraus_idx, shots, eset_ids)
         check(load().ptsbe_batch_upload(plan._h, _ptr(kraus_idx), _ptr(shots), _ptr(ids),
                                         shots.size, ctypes.byref(self._h)))
+
+    def _live(self):
+        if not self._h:
+            raise DeviceError("this resident batch was closed (with its plan)")
+        return self._h
 
     def run(self, seed: int) -> tuple[int, RunStats]:
         st = RunStats()
         n = ctypes.c_uint64()
-        check(load().ptsbe_batch_run(self._h, seed & (2**64 - 1), ctypes.byref(n), ctypes.byref(st)))
+        check(load().ptsbe_batch_run(self._live(), seed & (2**64 - 1), ctypes.byref(n), ctypes.byref(st)))
         return int(n.value), st
 
     def kraus(self, n_sets: int, g: int) -> np.ndarray:
         """Kraus-index matrix [n_sets, g] of this batch (device-side pre-sampling: what was drawn)."""
         out = np.empty((n_sets, g), dtype=np.uint8)
-        check(load().ptsbe_batch_kraus(self._h, _ptr(out)))
+        check(load().ptsbe_batch_kraus(self._live(), _ptr(out)))
         return out
 
     def fetch(self) -> tuple[np.ndarray, np.ndarray]:
         k, c, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
-        check(load().ptsbe_batch_fetch(self._h, ctypes.byref(k), ctypes.byref(c), ctypes.byref(n)))
+        check(load().ptsbe_batch_fetch(self._live(), ctypes.byref(k), ctypes.byref(c), ctypes.byref(n)))
         w = self.plan.words
         return _take(k, n.value * w, np.uint64).reshape(-1, w), _take(c, n.value, np.uint64)
 
@@ -226,7 +231,7 @@ class ResidentBatch:
         """Histogram of the last run as borrowed device buffers (keys [R, words],
         counts [R]); valid until the next run or close()."""
         k, c, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
-        check(load().ptsbe_batch_histogram_dev(self._h, ctypes.byref(k), ctypes.byref(c), ctypes.byref(n)))
+        check(load().ptsbe_batch_histogram_dev(self._live(), ctypes.byref(k), ctypes.byref(c), ctypes.byref(n)))
         return (DeviceArray(k.value, (n.value, self.plan.words), owner=self),
                 DeviceArray(c.value, (n.value,), owner=self))
 
@@ -251,11 +256,15 @@ class DevicePlan:
         self.words = max(1, (compiled.n_qubits + 63) // 64)
         self.n_sites = compiled.n_sites
         self._h = ctypes.c_void_p()
+        self._batches = weakref.WeakSet()
         desc = compiled.descriptor()
         check(lib.ptsbe_plan_create(ctypes.byref(desc), device, ctypes.byref(self._h)))
 
     def close(self):
         if self._h:
+            # batches first: ptsbe_batch_destroy dereferences its plan (stream, workspace cache, mutex)
+            for bt in list(self._batches):
+                bt.close()
             load().ptsbe_plan_destroy(self._h)
             self._h = ctypes.c_void_p()
 
@@ -265,11 +274,34 @@ class DevicePlan:
         except Exception:
             pass
 
+    def _check_inputs(self, kraus_idx, shots, eset_ids):
+        """Shapes and dtypes of the flat arrays the C ABI copies from (it trusts its sizes)."""
+        if not self._h:
+            raise DeviceError("this device plan was closed")
+        kraus_idx = np.ascontiguousarray(kraus_idx, dtype=np.uint8)
+        if kraus_idx.ndim != 2 or kraus_idx.shape[1] != self.n_sites:
+            raise ValueError(f"kraus_idx must be [n_sets, {self.n_sites}] (one column per gate site), "
+                             f"got {kraus_idx.shape}")
+        n_sets = kraus_idx.shape[0]
+        if shots is not None:
+            shots = np.ascontiguousarray(shots, dtype=np.uint32)
+            if shots.shape != (n_sets,):
+                raise ValueError(f"shots must have one entry per error set ({n_sets}), got shape {shots.shape}")
+        ids = None
+        if eset_ids is not None:
+            ids = np.ascontiguousarray(eset_ids, dtype=np.uint32)
+            if ids.shape != (n_sets,):
+                raise ValueError(f"eset_ids must have one entry per error set ({n_sets}), got shape {ids.shape}")
+        return kraus_idx, shots, ids
+
     def marginals(self, stage: int, kraus_idx: np.ndarray, prefixes: np.ndarray):
         """(probs [W, 2^b] float64 unnormalised+clamped, mass [W], min [W])."""
-        kraus_idx = np.ascontiguousarray(kraus_idx, dtype=np.uint8)
+        kraus_idx, _, _ = self._check_inputs(kraus_idx, None, None)
         w = kraus_idx.shape[0]
-        prefixes = np.ascontiguousarray(prefixes, dtype=np.uint64).reshape(w, self.words)
+        prefixes = np.ascontiguousarray(prefixes, dtype=np.uint64)
+        if prefixes.size != w * self.words:
+            raise ValueError(f"prefixes must be [{w}, {self.words}] u64, got {prefixes.shape}")
+        prefixes = prefixes.reshape(w, self.words)
         nb = 1 << self.compiled.sizes[stage - 1]
         probs = np.empty((w, nb), dtype=np.float64)
         mass = np.empty(w, dtype=np.float64)
@@ -284,9 +316,7 @@ class DevicePlan:
     def sample(self, kraus_idx, shots, eset_ids, seed: int, merged: bool = True):
         """Host-buffer entry point: returns (keys [R, words] u64, eset [R] or None,
         counts [R] u64, RunStats)."""
-        kraus_idx = np.ascontiguousarray(kraus_idx, dtype=np.uint8)
-        shots = np.ascontiguousarray(shots, dtype=np.uint32)
-        ids = None if eset_ids is None else np.ascontiguousarray(eset_ids, dtype=np.uint32)
+        kraus_idx, shots, ids = self._check_inputs(kraus_idx, shots, eset_ids)
         k, e, c, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()
         st = RunStats()
         check(load().ptsbe_sample(self._h, _ptr(kraus_idx), _ptr(shots), _ptr(ids), shots.size,
@@ -301,8 +331,7 @@ class DevicePlan:
                                threshold: float, direct_count: int):
         """Non-proportional sampling (engine.py:527-576) of every error set in one device run:
         returns (keys [R, words] u64, eset position [R], counts [R], probs [R] or None, RunStats)."""
-        kraus_idx = np.ascontiguousarray(kraus_idx, dtype=np.uint8)
-        ids = None if eset_ids is None else np.ascontiguousarray(eset_ids, dtype=np.uint32)
+        kraus_idx, _, ids = self._check_inputs(kraus_idx, None, eset_ids)
         if final_mode not in ("exhaustive", "direct"):
             raise ValueError(f"final_mode must be 'exhaustive' or 'direct', got {final_mode!r}")
         k, e, c, pr, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_uint64()

@@ -708,6 +708,8 @@ class PlanDesc(ctypes.Structure):
         ("pool_elems", ctypes.c_uint64),
         ("programs", ctypes.c_void_p),
         ("max_intermediate", ctypes.c_uint64),
+        ("shots_per_set_hint", ctypes.c_double),
+        ("site_variants", ctypes.c_void_p),
     ]
 
 
@@ -722,6 +724,8 @@ class CompiledPlan:
     pool: np.ndarray
     programs: list  # stage-major flat list of Program
     max_intermediate: int
+    shots_per_set_hint: float = 0.0
+    site_variants: Optional[np.ndarray] = None  # [n_sites] u8: variants per gate site (index validation)
     _keep: list = field(default_factory=list)
 
     def descriptor(self) -> PlanDesc:
@@ -747,6 +751,12 @@ class CompiledPlan:
         sizes = np.asarray(self.sizes, dtype=np.uint32)
         pool = np.ascontiguousarray(self.pool)
         keep += [arr, sizes, pool]
+        sv = None
+        if self.site_variants is not None and self.n_sites:
+            sv = np.ascontiguousarray(self.site_variants, dtype=np.uint8)
+            if sv.size != self.n_sites:
+                raise ValueError("site_variants must have one entry per gate site")
+            keep.append(sv)
         self._keep = keep
         return PlanDesc(
             0 if self.dtype == "complex64" else 1,
@@ -758,4 +768,6 @@ class CompiledPlan:
             pool.size,
             ctypes.addressof(arr),
             self.max_intermediate,
+            float(self.shots_per_set_hint),
+            sv.ctypes.data if sv is not None else None,
         )

@@ -8,8 +8,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <map>
 #include <memory>
 #include <mutex>
+#include <set>
+#include <tuple>
 
 #include "common.cuh"
 #include "descent.cuh"
@@ -63,6 +66,9 @@ struct ptsbe_plan {
   uint32_t lane = 1;                   // lane-per-item interpreter / fused descent (lane.cuh)
   uint32_t descent = 1;                // per-qubit descent sampler for low-multiplicity stages
   double descent_mult = 4.0;           // ... used when shots / unique prefixes of the stage <= this
+  // per stage: 1 descent, 0 flat, -1 decide per chunk (no shots_per_set_hint in the descriptor)
+  std::vector<int> stage_descent;
+  DevBuf site_variants;                // [g] u8 variants per site, or empty (no index validation)
   uint64_t chunk_shots = 1ull << 26;
   size_t ext_budget = 48ull << 30;
   double vanish = 1e-12, neg_abs = -1e-12, neg_rel = 0.0, vanish_stage1 = 1e-30;
@@ -132,6 +138,36 @@ struct HostPool {
   }
 };
 static HostPool g_host_pool;
+
+// cudaFuncSetAttribute and occupancy are PER DEVICE: plans may live on several GPUs of one process,
+// so the opt-in to > 48 KB of dynamic shared memory and the occupancy figures are remembered per
+// (device, kernel[, shared-memory size]) under a lock, never in a process-wide flag.
+static void opt_in_smem(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({dev, fn})) return;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert({dev, fn});
+}
+
+static int cached_occupancy(const void* fn, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, size_t>, int> memo;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_tuple(dev, fn, smem);
+  auto it = memo.find(key);
+  if (it != memo.end()) return it->second;
+  int nb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem));
+  nb = std::max(nb, 1);
+  memo[key] = nb;
+  return nb;
+}
 
 static size_t env_size(const char* name, size_t dflt) {
   const char* v = getenv(name);
@@ -427,14 +463,8 @@ static DescentShape descent_shape(const ptsbe_plan* pl, uint32_t D, uint32_t b) 
 
 template <typename R, int NCH>
 static void launch_descent_t(ptsbe_plan* pl, const DescentArgs& a, size_t smem) {
-  static int per_sm = 0;
-  static size_t per_sm_smem = 0;
-  if (!per_sm || per_sm_smem != smem) {
-    CK(cudaFuncSetAttribute(descent_kernel<R, NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, descent_kernel<R, NCH>, DS_THREADS, smem));
-    per_sm = std::max(per_sm, 1);
-    per_sm_smem = smem;
-  }
+  opt_in_smem((const void*)descent_kernel<R, NCH>, 200 * 1024);
+  const int per_sm = cached_occupancy((const void*)descent_kernel<R, NCH>, DS_THREADS, smem);
   const uint64_t tiles = cdiv(a.n_items, DS_TILE);
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)pl->sm_count * per_sm));
   descent_kernel<R, NCH><<<grid, DS_THREADS, smem, pl->stream>>>(a);
@@ -578,14 +608,9 @@ static void launch_project(ptsbe_plan* pl, const Program& pr, const void* v, uin
   using Kern = void (*)(const ProjectArgs);
   static const Kern kern[2][2] = {{project_kernel<double, PJ_TN>, project_kernel<double, 64>},
                                   {project_kernel<float, PJ_TN>, project_kernel<float, 64>}};
-  static int per_sm[2][2] = {{0, 0}, {0, 0}};
-  int& occ = per_sm[f32][narrow];
   const Kern k = kern[f32][narrow];
-  if (!occ) {
-    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, PJ_THREADS, smem));
-    occ = std::max(occ, 1);
-  }
+  opt_in_smem((const void*)k, 110 * 1024);
+  const int occ = cached_occupancy((const void*)k, PJ_THREADS, smem);
   const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)pl->sm_count * occ);
   k<<<grid, PJ_THREADS, smem, pl->stream>>>(a);
   g_launches++;
@@ -605,20 +630,12 @@ static void launch_sampler(cudaStream_t st, SampleArgs& a, int sm_count) {
     return;
   }
   if (a.b > 14) throw Failure(PTSBE_ECAPACITY, "sampler supports stage batches of at most 14 qubits");
-  static bool attr_set = false;
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(sample_group_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(sample_group_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(sample_group_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr_set = true;
-  }
+  opt_in_smem((const void*)sample_kernel, 200 * 1024);
+  opt_in_smem((const void*)sample_group_kernel<8>, 200 * 1024);
+  opt_in_smem((const void*)sample_group_kernel<16>, 200 * 1024);
+  opt_in_smem((const void*)sample_group_kernel<32>, 200 * 1024);
   if (a.np_mode) {
-    static bool np_attr = false;
-    if (!np_attr) {
-      CK(cudaFuncSetAttribute(nonprop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      np_attr = true;
-    }
+    opt_in_smem((const void*)nonprop_kernel, 200 * 1024);
     const unsigned grid = (unsigned)std::min<uint64_t>(a.n_items, (uint64_t)sm_count * 16);
     nonprop_kernel<<<grid, SAMPLE_THREADS, nb * 12, st>>>(a);
     g_launches++;
@@ -762,7 +779,9 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     // Stages whose work items carry few shots each are sampled by per-qubit descent over the
     // error set's conditional-marginal tree (descent.cuh) instead of project + sample.
     DescentShape dsh;
-    if (proj && pl->descent && j > 1 && U && (double)chunk_shots <= pl->descent_mult * (double)U &&
+    const int hint = pl->stage_descent[j - 1];
+    const bool few_shots = hint >= 0 ? hint == 1 : (double)chunk_shots <= pl->descent_mult * (double)U;
+    if (proj && pl->descent && j > 1 && U && few_shots &&
         (!npp || (j == f && !np_exhaustive)))  // choice without replacement / harvest need the full vector
       dsh = descent_shape(pl, progs[j - 1].d.proj_d, b);
     if (dsh.nch) {
@@ -1073,6 +1092,65 @@ struct ptsbe_batch {
 
 namespace ptsbe {
 
+// Kraus indices must address a variant the plan's tables hold (reference merge_errors raises on an
+// unknown label, engine.py:300-312; here an out-of-range index would gather outside the pool).
+__global__ void check_kraus_kernel(const uint8_t* kraus, const uint8_t* variants, uint64_t n, uint32_t g,
+                                   unsigned long long* first_bad) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    if (kraus[i] >= variants[i % g]) atomicMin(first_bad, (unsigned long long)i);
+}
+
+static void check_kraus(ptsbe_plan* pl, const uint8_t* kraus_dev, uint64_t n_sets) {
+  if (!pl->site_variants.p || !pl->g || !n_sets) return;
+  cudaStream_t st = pl->stream;
+  DevBuf bad(8, st);
+  CK(cudaMemsetAsync(bad.p, 0xff, 8, st));
+  const uint64_t n = n_sets * pl->g;
+  const unsigned grid = (unsigned)std::min<uint64_t>(cdiv(n, 256), (uint64_t)pl->sm_count * 8);
+  check_kraus_kernel<<<grid, 256, 0, st>>>(kraus_dev, pl->site_variants.as<uint8_t>(), n, pl->g,
+                                           bad.as<unsigned long long>());
+  g_launches++;
+  CK(cudaGetLastError());
+  unsigned long long first = 0;
+  CK(cudaMemcpyAsync(&first, bad.p, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (first != ~0ull)
+    throw Failure(PTSBE_EINVAL, "Kraus index out of range: error set row " + std::to_string(first / pl->g) +
+                                    ", site " + std::to_string(first % pl->g) +
+                                    " addresses a variant this plan's tables do not hold");
+}
+
+// Joins per-chunk record lists (level f+1 of run_chunk) into one: keys [words][n] SoA, counts,
+// error-set rows offset by the chunk's first set, probability tags when every chunk carries them.
+static void concat_outputs(std::vector<RunOutput>& outs, const std::vector<uint64_t>& first_set,
+                           uint32_t words, RunOutput& all, cudaStream_t st) {
+  uint64_t total = 0;
+  bool tags = true;
+  for (auto& o : outs) { total += o.n; tags = tags && (o.n == 0 || o.probs.p != nullptr); }
+  all = RunOutput();
+  all.n = total;
+  if (!total) return;
+  all.keys.alloc(total * 8 * words, st);
+  all.counts.alloc(total * 4, st);
+  all.eset.alloc(total * 4, st);
+  if (tags) all.probs.alloc(total * 8, st);
+  uint64_t off = 0;
+  for (size_t c = 0; c < outs.size(); ++c) {
+    RunOutput& o = outs[c];
+    if (!o.n) continue;
+    for (uint32_t w = 0; w < words; ++w)
+      CK(cudaMemcpyAsync(all.keys.as<uint64_t>() + (uint64_t)w * total + off,
+                         o.keys.as<uint64_t>() + (uint64_t)w * o.n, o.n * 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(all.counts.as<uint32_t>() + off, o.counts.p, o.n * 4, cudaMemcpyDeviceToDevice, st));
+    add_offset_u32_kernel<<<cdiv(o.n, 256), 256, 0, st>>>(o.eset.as<uint32_t>(), all.eset.as<uint32_t>() + off,
+                                                          o.n, (uint32_t)first_set[c]);
+    g_launches++;
+    CK(cudaGetLastError());
+    if (tags) CK(cudaMemcpyAsync(all.probs.as<double>() + off, o.probs.p, o.n * 8, cudaMemcpyDeviceToDevice, st));
+    off += o.n;
+  }
+}
+
 static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stats* stats) {
   ptsbe_plan* pl = bt->plan;
   cudaStream_t st = pl->stream;
@@ -1178,9 +1256,16 @@ static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stat
     }
     stats->n_records = bt->merged.n;
   } else {
-    if (chunks.size() != 1)
-      throw Failure(PTSBE_ECAPACITY, "per-error-set output needs the batch to fit one chunk");
-    bt->per_set = std::move(outs[0]);
+    if (chunks.size() == 1) {
+      bt->per_set = std::move(outs[0]);
+    } else {
+      // concatenate the chunks' records: keys are SoA with the record count as stride, error-set rows
+      // are relative to the chunk's first set (the reference's per-set API has no size limit,
+      // engine.py:493-524)
+      std::vector<uint64_t> first_set;
+      for (auto& ch : chunks) first_set.push_back(ch.first);
+      concat_outputs(outs, first_set, words, bt->per_set, st);
+    }
     bt->have_per_set = true;
     stats->n_records = bt->per_set.n;
   }
@@ -1305,11 +1390,25 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     if (const char* dm = getenv("PTSBE_DESCENT_MULT")) if (*dm) pl->descent_mult = atof(dm);
     pl->chunk_shots = env_size("PTSBE_CHUNK_SHOTS", pl->chunk_shots);
     pl->ext_budget = env_size("PTSBE_EXT_BYTES", pl->ext_budget);
+    // sampler choice per stage from plan-level quantities only (grouping / sharding independent)
+    for (uint32_t j = 0; j < d->n_stages; ++j) {
+      int h = -1;
+      if (d->shots_per_set_hint > 0.0) {
+        const double m = d->shots_per_set_hint;
+        const double prefixes = pl->offsets[j] >= 62 ? m : std::min(m, std::ldexp(1.0, (int)pl->offsets[j]));
+        h = m / std::max(prefixes, 1.0) <= pl->descent_mult ? 1 : 0;
+      }
+      pl->stage_descent.push_back(h);
+    }
     const bool use_memo = env_size("PTSBE_MEMO", 1) != 0;  // variant-0 memo of class-0 programs
     cudaStream_t st = pl->stream;
     pl->pool.alloc(std::max<size_t>(16, d->pool_elems * pl->elem), st);
     if (d->pool_elems)
       CK(cudaMemcpyAsync(pl->pool.p, d->pool, d->pool_elems * pl->elem, cudaMemcpyHostToDevice, st));
+    if (d->site_variants && d->n_sites) {
+      pl->site_variants.alloc(d->n_sites, st);
+      CK(cudaMemcpyAsync(pl->site_variants.p, d->site_variants, d->n_sites, cudaMemcpyHostToDevice, st));
+    }
     size_t k = 0;
     pl->programs.resize(d->n_stages);
     for (uint32_t j = 1; j <= d->n_stages; ++j) {
@@ -1416,6 +1515,7 @@ int ptsbe_marginals(ptsbe_plan* pl, uint32_t stage, const uint8_t* kraus_idx,
       if (pl->g)
         CK(cudaMemcpyAsync(kraus.p, kraus_idx + c0 * pl->g, (size_t)W * pl->g,
                            cudaMemcpyHostToDevice, st));
+      check_kraus(pl, kraus.as<uint8_t>(), W);
       // prefixes arrive item-major [W][words]; the device wants [words][W]
       std::vector<uint64_t> soa((size_t)W * words);
       for (uint32_t i = 0; i < W; ++i)
@@ -1619,6 +1719,10 @@ int ptsbe_batch_upload(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t*
       iota_kernel<<<cdiv(n_sets, 256), 256, 0, st>>>(bt->ids.as<uint32_t>(), (uint32_t)n_sets, 0);
     }
     CK(cudaStreamSynchronize(st));
+    {
+      std::lock_guard<std::mutex> lock(pl->mu);
+      check_kraus(pl, bt->kraus.as<uint8_t>(), n_sets);
+    }
     *out = bt.release();
   });
 }
@@ -1813,14 +1917,17 @@ int ptsbe_sample_nonproportional(ptsbe_plan* pl, const uint8_t* kraus_idx, const
     cudaStream_t st = pl->stream;
     const uint32_t f = pl->f;
     NonpropParams np{nonfinal_shots, final_mode, direct_count, threshold};
-    // slots any stage can need: items_j <= n_sets * nonfinal^(j-1), each with its multiplicity
-    double bound = 0, items = (double)n_sets;
+    // slots any stage can need PER ERROR SET: items_j <= nonfinal^(j-1), each with its multiplicity;
+    // error sets are processed in chunks whose slot count stays below the chunk bound
+    double per_set = 0, items = 1.0;
     for (uint32_t j = 1; j <= f; ++j) {
       const double mult = j < f ? nonfinal_shots : (final_mode == 0 ? std::ldexp(1.0, (int)pl->sizes[f - 1]) : direct_count);
-      bound = std::max(bound, items * mult);
+      per_set = std::max(per_set, items * mult);
       items *= nonfinal_shots;
     }
-    if (bound >= 2147483648.0) throw Failure(PTSBE_ECAPACITY, "non-proportional run needs more than 2^31 child slots");
+    if (per_set >= 2147483648.0) throw Failure(PTSBE_ECAPACITY, "one error set needs more than 2^31 child slots");
+    const double chunk_cap = std::min<double>(2147483647.0, (double)pl->chunk_shots);
+    const uint64_t sets_per_chunk = std::max<uint64_t>(1, (uint64_t)(chunk_cap / per_set));
     memset(stats, 0, sizeof *stats);
     stats->first_flagged_id = -1;
     g_launches = 0;
@@ -1835,15 +1942,29 @@ int ptsbe_sample_nonproportional(ptsbe_plan* pl, const uint8_t* kraus_idx, const
       else { iota_kernel<<<cdiv(n_sets, 256), 256, 0, st>>>(ids.as<uint32_t>(), (uint32_t)n_sets, 0); g_launches++; }
       CK(cudaMemsetAsync(flag.p, 0xff, 8, st));
       CK(cudaMemsetAsync(flag.as<unsigned char>() + 8, 0, 8, st));
+      check_kraus(pl, kraus.as<uint8_t>(), n_sets);
       RunOutput out;
       cudaEvent_t e0, e1;
       CK(cudaEventCreate(&e0));
       CK(cudaEventCreate(&e1));
       CK(cudaEventRecord(e0, st));
       {
-        WorkspaceScope chunk_scope(ws_tmp.get());
-        run_chunk(pl, kraus.as<uint8_t>(), nullptr, ids.as<uint32_t>(), (uint32_t)n_sets, (uint64_t)bound, seed, out,
-                  stats, flag.as<unsigned long long>(), flag.as<uint32_t>() + 2, *ws_out, &np);
+        std::vector<RunOutput> outs;
+        std::vector<uint64_t> first_set;
+        for (uint64_t e = 0; e < n_sets; e += sets_per_chunk) {
+          const uint64_t cnt = std::min<uint64_t>(sets_per_chunk, n_sets - e);
+          outs.emplace_back();
+          first_set.push_back(e);
+          WorkspaceScope chunk_scope(ws_tmp.get());
+          const Workspace::Mark mark = ws_tmp->mark();
+          run_chunk(pl, kraus.as<uint8_t>() + e * pl->g, nullptr, ids.as<uint32_t>() + e, (uint32_t)cnt,
+                    (uint64_t)(per_set * (double)cnt), seed, outs.back(), stats, flag.as<unsigned long long>(),
+                    flag.as<uint32_t>() + 2, *ws_out, &np);
+          ws_tmp->rewind(mark);  // run_chunk returns with the stream drained
+        }
+        stats->n_chunks = (uint32_t)outs.size();
+        if (outs.size() == 1) out = std::move(outs[0]);
+        else concat_outputs(outs, first_set, pl->words, out, st);
       }
       CK(cudaEventRecord(e1, st));
       struct { unsigned long long first; uint32_t count; uint32_t pad; } fl;

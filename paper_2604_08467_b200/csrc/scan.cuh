@@ -127,6 +127,12 @@ __global__ void fill_u32_kernel(uint32_t* out, uint32_t n, uint32_t value) {
   if (i < n) out[i] = value;
 }
 
+// out[i] = in[i] + offset (error-set rows of a later chunk -> rows of the whole batch)
+__global__ void add_offset_u32_kernel(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t offset) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i] + offset;
+}
+
 // probability tag of child c: slot (slot_off[parent] + position of c among its parent's children)
 __global__ void gather_prob_kernel(const uint32_t* c_parent, const uint32_t* child_base,
                                    const uint32_t* p_slot_off, const double* slot_prob, double* out,

@@ -641,6 +641,8 @@ class DevicePipeline:
         self.compiled = CompiledPlan(
             dtype=ctx.dtype, n_qubits=plan.n, n_sites=tables.n_sites, sizes=plan.sizes,
             pool=pool.finish(ctx.dtype), programs=programs, max_intermediate=ctx.max_intermediate,
+            shots_per_set_hint=float(shots_per_set),
+            site_variants=np.asarray([min(d.shape[0], 255) for d in tables.data], dtype=np.uint8),
         )
         # upload=False: compile only (plan inspection; CPU-side tests of the compiler)
         self.device_plan = _capi.DevicePlan(self.compiled, ctx.device) if upload else None
@@ -1039,13 +1041,19 @@ class RunResult:
 
 
 def run_ptsbe(c: Circuit, config: RunConfig, cache: Optional[PathCache] = None,
-              errorsets: Optional[Sequence[ErrorSet]] = None, _keep_packed: bool = False) -> RunResult:
+              errorsets: Optional[Sequence[ErrorSet]] = None, _keep_packed: bool = False,
+              _shard: Optional[tuple] = None) -> RunResult:
     """Optimised proportional pipeline on the device (engine.py:832-929):
     pre-sample error sets on the host (same rng stream as the reference), plan
     one path per stage on the error-free template (plan events = f, or 0 with a
     warm cache), then ONE batched device run over all error sets, histogram
     merged on the device.  `errorsets` overrides the pre-sampling (the
-    north-star API: pre-sampled error sets in, histogram out)."""
+    north-star API: pre-sampled error sets in, histogram out).
+
+    `_shard=(lo, hi)` (partition.run_ptsbe_sharded): everything that shapes the
+    arithmetic -- variant tables, light cone, planner weights, stored paths,
+    sampler choice per stage -- is built from the FULL error-set list, exactly
+    as in a single-process run; only error sets [lo, hi) are sampled here."""
     if config.mode not in ("ptsbe-proportional", "ptsbe-nonproportional"):
         raise ValueError(f"run_ptsbe handles optimized modes only, got {config.mode!r}")
     nonprop = config.mode == "ptsbe-nonproportional"
@@ -1074,6 +1082,10 @@ def run_ptsbe(c: Circuit, config: RunConfig, cache: Optional[PathCache] = None,
     pipe = DevicePipeline(template, plan, tables, ctx,
                           shots_per_set=float(plan.nonfinal_shots) if nonprop else float(shots.mean()))
     plan_s = time.perf_counter() - t0
+    all_sets = errorsets
+    if _shard is not None:
+        errorsets = list(errorsets[_shard[0]:_shard[1]])
+        shots = shots[_shard[0]:_shard[1]]
     try:
         ctx.check_deadline()
         kraus_idx = tables.encode(errorsets)

@@ -6,8 +6,11 @@ The reference has no distributed layer; what it pins is the determinism
 contract under sharding -- results are independent of how error sets are
 spread over lanes (/root/reference/pkg/tests/test_engine.py:455-463, per
 error-set RNG streams keyed by k.id, engine.py:889).  The device sampler keys
-its Philox streams by (seed, GLOBAL error-set id, stage, prefix rank), so the
-merged histogram is bit-identical for any world size.
+its Philox streams by (seed, GLOBAL error-set id, stage, prefix rank), and
+`run_ptsbe_sharded` builds everything that shapes the arithmetic (variant
+tables, light cone, planner weights, stored paths, per-stage sampler choice)
+from the full error-set list on every rank, so the merged histogram does not
+depend on the world size (GPU test: tests/test_gpu_sharded.py).
 
 `merge_records` across ranks (engine.py:815-829) = all_gather of lengths,
 padded all_gather of (key words, count) rows, sort + reduce-by-key on the
@@ -133,51 +136,178 @@ def merge_on_device(keys, counts, device: int):
     return k, c
 
 
+def _collective_device(group, device: int) -> str:
+    """Where tensors must live for the group's backend: NCCL moves device memory over
+    NVLink, gloo (CPU tests; several ranks sharing one GPU) moves host memory."""
+    import torch.distributed as dist
+
+    return f"cuda:{device}" if dist.get_backend(group) == "nccl" else "cpu"
+
+
+def _merge_for(where: str, device: int):
+    """reduce-by-key of gathered rows on the GPU: device pointers for cuda tensors, the
+    host-buffer entry point (H2D + D2H inside) for cpu tensors."""
+    if where != "cpu":
+        return lambda a, b: merge_on_device(a, b, device)
+
+    def merge_host(k, c):
+        import torch
+
+        from . import _capi
+
+        ok, oc = _capi.histogram_merge(k.numpy().view(np.uint64), c.numpy().view(np.uint64), device)
+        return (torch.from_numpy(np.ascontiguousarray(ok).view(np.int64)),
+                torch.from_numpy(np.ascontiguousarray(oc).view(np.int64)))
+
+    return merge_host
+
+
 def run_ptsbe_sharded(c, config, errorsets, *, group=None, cache=None):
     """`run_ptsbe` with the error sets block-partitioned over the ranks of the
     (already initialised) process group; every rank returns the same merged
     `RunResult.records`.  Counters (`contract_events`, `stage_events`) are
-    summed over ranks; `timings["device_loop_s"]` is the max over ranks."""
+    summed over ranks; `timings["device_loop_s"]` is the max over ranks.
+
+    Determinism under sharding (reference tests/test_engine.py:455-463): every
+    rank builds the variant tables, the light cone, the planner weights, the
+    stored paths and the per-stage sampler choice from the FULL error-set list
+    and the global mean shot count -- exactly what a single-process run builds --
+    and only the error sets it samples differ.  The RNG streams are keyed by the
+    global error-set id, so the merged histogram does not depend on the world
+    size.  The per-rank histogram never leaves the device before the exchange
+    (`ptsbe_batch_histogram_dev`); a failing error set is reported on every rank
+    (the ranks agree on the failure before anyone raises, so none is left
+    waiting in a collective)."""
+    import time
+
     import torch
     import torch.distributed as dist
 
     from . import engine
+    from .errors import STATUS_TO_ERROR, SimulationError
 
-    if config.mode != "ptsbe-proportional":
-        raise NotImplementedError("the sharded run gathers count histograms; the non-proportional mode "
-                                  "(records with probability tags) runs per rank and is merged with merge_records")
+    if config.mode not in ("ptsbe-proportional", "ptsbe-nonproportional"):
+        raise ValueError(f"run_ptsbe_sharded handles optimized modes only, got {config.mode!r}")
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     device = config.device
-    lo, hi = shard_bounds([k.m for k in errorsets], world)[rank]
+    where = _collective_device(group, device)
     plan = config.plan()
-    if hi > lo:
-        local = engine.run_ptsbe(c, config, cache=cache, errorsets=errorsets[lo:hi], _keep_packed=True)
-    else:  # more ranks than error sets: this rank only takes part in the gather
-        words = max(1, (plan.n + 63) // 64)
-        local = engine.RunResult(
-            mode=config.mode, records=[], unique_shots=0, total_count=0,
-            timings={"generate_s": 0.0, "plan_s": 0.0, "loop_s": 0.0, "aggregate_s": 0.0, "path_s": 0.0,
-                     "contract_s": 0.0, "device_loop_s": 0.0, "h2d_s": 0.0, "d2h_s": 0.0, "gpu_launches": 0},
-            plan_events=0, contract_events=0, stage_events={}, stage_seconds={}, config=config.to_dict(),
-            seed=config.seed, shot_allocations=[], packed_keys=np.zeros((0, words), np.uint64),
-            packed_counts=np.zeros(0, np.uint64))
-    keys = torch.from_numpy(local.packed_keys.view(np.int64)).to(f"cuda:{device}")
-    counts = torch.from_numpy(local.packed_counts.view(np.int64)).to(f"cuda:{device}")
-    k, cnt = gather_histograms(keys, counts, group=group, merge=lambda a, b: merge_on_device(a, b, device))
-    records = [engine.ShotRecord(bitstring=s, count=int(v)) for s, v in
-               zip(engine.unpack_keys(k.cpu().numpy().view(np.uint64), plan.n), cnt.cpu().tolist())]
-    # counters: sum over ranks; device time: max over ranks
+    if plan.n != c.n:
+        raise ValueError(f"plan covers {plan.n} qubits, circuit has {c.n}")
+    errorsets = list(errorsets)
+    lo, hi = shard_bounds([k.m for k in errorsets], world)[rank]
     f = plan.f
-    vec = torch.tensor([local.contract_events] + [local.stage_events.get(j, 0) for j in range(1, f + 1)],
-                       dtype=torch.int64, device=f"cuda:{device}")
-    dist.all_reduce(vec, group=group)
-    tmax = torch.tensor([local.timings["device_loop_s"]], dtype=torch.float64, device=f"cuda:{device}")
-    dist.all_reduce(tmax, op=dist.ReduceOp.MAX, group=group)
-    local.records = records
-    local.unique_shots = len(records)
-    local.total_count = sum(r.count for r in records)
-    local.contract_events = int(vec[0].item())
-    local.stage_events = {j: int(vec[j].item()) for j in range(1, f + 1)}
-    local.timings["device_loop_s"] = float(tmax.item())
-    local.shot_allocations = [int(k.m) for k in errorsets]
-    return local
+
+    def agree_on_failure(exc):
+        """(kind, error-set id) of the failure with the smallest id over all ranks, or None."""
+        code = 0
+        eid = 2**62
+        if exc is not None:
+            code = next((k for k, v in STATUS_TO_ERROR.items() if isinstance(exc, v) and type(exc) is v), 1)
+            eid = getattr(exc, "eset_id", 2**62 - 1)
+        t = torch.tensor([eid, code], dtype=torch.int64, device=where)
+        rows = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(rows, t, group=group)
+        bad = sorted((int(r[0]), int(r[1])) for r in rows if int(r[1]))
+        return bad[0] if bad else None
+
+    if config.mode == "ptsbe-nonproportional":
+        # records carry probability tags: per-rank merged records travel as objects, then merge_records
+        # (engine.py:815-829; counts summed, a tag survives only if all contributors agree)
+        err, local = None, None
+        try:
+            if hi > lo:
+                local = engine.run_ptsbe(c, config, cache=cache, errorsets=errorsets, _shard=(lo, hi))
+        except SimulationError as exc:
+            err = exc
+        bad = agree_on_failure(err)
+        if bad is not None:
+            raise err if err is not None else SimulationError(f"error set {bad[0]}: failed on another rank")
+        parts = [None] * world
+        dist.all_gather_object(parts, None if local is None else
+                               (local.records, local.contract_events, local.stage_events,
+                                local.timings["device_loop_s"]), group=group)
+        parts = [p for p in parts if p is not None]
+        records = engine.merge_records([p[0] for p in parts])
+        stage_events = {j: sum(p[2].get(j, 0) for p in parts) for j in range(1, f + 1)}
+        return engine.RunResult(
+            mode=config.mode, records=records, unique_shots=len(records),
+            total_count=sum(r.count for r in records),
+            timings=dict(local.timings, device_loop_s=max(p[3] for p in parts)) if local is not None
+            else {"device_loop_s": max(p[3] for p in parts)},
+            plan_events=local.plan_events if local is not None else 0,
+            contract_events=sum(p[1] for p in parts), stage_events=stage_events,
+            stage_seconds=local.stage_seconds if local is not None else {}, config=config.to_dict(),
+            seed=config.seed, shot_allocations=[int(k.m) for k in errorsets])
+
+    ctx = engine.SamplerContext(
+        cache=cache if cache is not None else engine.PathCache(), hypersamples=config.hypersamples,
+        planner_seed=config.seed, max_intermediate=config.max_intermediate,
+        deadline=(time.perf_counter() + config.timeout_s) if config.timeout_s else None,
+        dtype=config.dtype, device=device)
+    t0 = time.perf_counter()
+    template = engine.CircuitNetwork.from_circuit(c)
+    tables = engine.VariantTables.from_errorsets(template, errorsets)
+    shots_all = np.asarray([k.m for k in errorsets], dtype=np.uint32)
+    if shots_all.min() < 1:
+        raise ValueError("proportional sampling needs m >= 1")
+    pipe = engine.DevicePipeline(template, plan, tables, ctx, shots_per_set=float(shots_all.mean()))
+    plan_s = time.perf_counter() - t0
+    words = max(1, (plan.n + 63) // 64)
+    batch, st, err = None, None, None
+    try:
+        t0 = time.perf_counter()
+        if hi > lo:
+            mine = errorsets[lo:hi]
+            batch = pipe.device_plan.upload(tables.encode(mine), shots_all[lo:hi],
+                                            np.asarray([k.id for k in mine], dtype=np.uint32))
+            n_rec, st = batch.run(config.seed)
+            try:
+                engine._raise_flagged(st)
+            except SimulationError as exc:
+                exc.eset_id = int(st.first_flagged_id)
+                err = exc
+        bad = agree_on_failure(err)
+        if bad is not None:
+            exc_cls = STATUS_TO_ERROR.get(bad[1], SimulationError)
+            raise err if (err is not None and int(st.first_flagged_id) == bad[0]) else \
+                exc_cls(f"error set {bad[0]}: flagged on another rank")
+        if batch is not None and n_rec:
+            dk, dc = batch.histogram_dev()
+            keys = torch.as_tensor(dk, device=f"cuda:{device}").view(torch.int64)
+            counts = torch.as_tensor(dc, device=f"cuda:{device}").view(torch.int64)
+            if where == "cpu":
+                keys, counts = keys.cpu(), counts.cpu()
+        else:
+            keys = torch.zeros((0, words), dtype=torch.int64, device=where)
+            counts = torch.zeros(0, dtype=torch.int64, device=where)
+        k, cnt = gather_histograms(keys, counts, group=group, merge=_merge_for(where, device))
+        loop_s = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        records = [engine.ShotRecord(bitstring=s, count=int(v)) for s, v in
+                   zip(engine.unpack_keys(k.cpu().numpy().view(np.uint64), plan.n), cnt.cpu().tolist())]
+        aggregate_s = time.perf_counter() - t0
+        # counters: sum over ranks; device time: max over ranks
+        ev = [int(st.stage_events[j]) if st is not None else 0 for j in range(f)]
+        vec = torch.tensor([sum(ev)] + ev, dtype=torch.int64, device=where)
+        dist.all_reduce(vec, group=group)
+        tmax = torch.tensor([st.loop_ms * 1e-3 if st is not None else 0.0], dtype=torch.float64, device=where)
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX, group=group)
+    finally:
+        if batch is not None:
+            batch.close()
+        pipe.close()
+    if st is not None:
+        engine._account(ctx.stats, st, f)
+    return engine.RunResult(
+        mode=config.mode, records=records, unique_shots=len(records),
+        total_count=sum(r.count for r in records),
+        timings={"generate_s": 0.0, "plan_s": plan_s, "loop_s": loop_s, "aggregate_s": aggregate_s,
+                 "path_s": ctx.stats.path_seconds, "contract_s": ctx.stats.contract_seconds,
+                 "device_loop_s": float(tmax.item()),
+                 "h2d_s": (st.h2d_ms * 1e-3) if st is not None else 0.0, "d2h_s": 0.0,
+                 "gpu_launches": int(st.gpu_launches) if st is not None else 0},
+        plan_events=ctx.stats.plan_events, contract_events=int(vec[0].item()),
+        stage_events={j: int(vec[j].item()) for j in range(1, f + 1)},
+        stage_seconds=dict(sorted(ctx.stats.stage_seconds.items())),
+        config=config.to_dict(), seed=config.seed, shot_allocations=[int(k.m) for k in errorsets])
