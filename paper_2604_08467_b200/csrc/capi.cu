@@ -1478,6 +1478,7 @@ void ptsbe_plan_destroy(ptsbe_plan* pl) {
   cudaStreamSynchronize(pl->stream);
   pl->ws_cache.clear();
   pl->pool.release();
+  pl->site_variants.release();  // every stream-ordered buffer goes before its stream does
   for (auto& s : pl->programs)
     for (auto& p : s) {
       p.leaves.release(); p.steps.release(); p.tables.release();

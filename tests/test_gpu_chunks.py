@@ -37,8 +37,8 @@ def _pipe(c, sizes, shots, chunk_shots=None, dtype="complex128", **plan_kw):
 
 def _cases():
     c1, _ = workloads.hea(10, 3, gamma=0.05, p=0.08, seed=3)      # one-word keys
-    c2, _ = workloads.surface_code(3, 8, p=0.02)                  # 9 + 8*8 = 73 qubits: two-word keys
-    return [("hea10", c1, (4, 3, 3)), ("surface73", c2, tuple([8] * 9 + [1]))]
+    c2, _ = workloads.random40(70, 260, seed=7)                   # 70 qubits: two-word keys
+    return [("hea10", c1, (4, 3, 3)), ("random70", c2, (10, 8, 8, 8, 8, 8, 8, 6, 6))]
 
 
 @pytest.mark.parametrize("which", [0, 1])
