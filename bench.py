@@ -210,7 +210,8 @@ def parity_check(c, sizes, seed: int, cpu: dict, procs: int, device: int, hypers
             want[e] = rec
     tpl = CircuitNetwork.from_circuit(c)
     ctx = SamplerContext(hypersamples=hypersamples, planner_seed=seed, dtype="complex128", device=device)
-    pipe = DevicePipeline(tpl, BatchPlan(sizes), VariantTables.from_channels(tpl), ctx, shots_per_set=float(shots))
+    pipe = DevicePipeline(tpl, BatchPlan(sizes), VariantTables.from_channels(tpl), ctx, shots_per_set=float(shots),
+                          calibrate=True)
     try:
         keys, esets, counts, st = pipe.device_plan.sample(rows, np.full(n, shots, np.uint32), ids, seed, merged=False)
     finally:
@@ -592,7 +593,7 @@ def main():
     tpl = CircuitNetwork.from_circuit(c)
     tables = VariantTables.from_channels(tpl)
     ctx = SamplerContext(hypersamples=args.hypersamples, planner_seed=args.seed, dtype=dtype, device=dev)
-    pipe = DevicePipeline(tpl, BatchPlan(sizes), tables, ctx, shots_per_set=float(shots))
+    pipe = DevicePipeline(tpl, BatchPlan(sizes), tables, ctx, shots_per_set=float(shots), calibrate=True)
     plan_s = time.perf_counter() - t0
     dp = pipe.device_plan
     if args.device_presample:
@@ -732,7 +733,7 @@ def main():
     c128_leg = None
     if dtype == "complex64" and world == 1 and not args.no_c128:
         ctx2 = SamplerContext(hypersamples=args.hypersamples, planner_seed=args.seed, dtype="complex128", device=dev)
-        pipe2 = DevicePipeline(tpl, BatchPlan(sizes), tables, ctx2, shots_per_set=float(shots))
+        pipe2 = DevicePipeline(tpl, BatchPlan(sizes), tables, ctx2, shots_per_set=float(shots), calibrate=True)
         b2 = pipe2.device_plan.upload(kraus, shots_arr, ids)
         b2.run(args.seed - 1)
         ms2, k2 = 0.0, min(args.steps, 2)
@@ -829,6 +830,7 @@ def main():
                        "error_sets_per_gpu": sets if args.scaling == "weak" else None,
                        "error_sets_total": sets_global, "shots_per_set": shots, "backend": backend if world > 1 else None,
                        "gates": len(c.gates), "hypersamples": args.hypersamples, "plan_s": round(plan_s, 3),
+                       "stage_samplers": ["descent" if k else "flat" for k in pipe.stage_samplers.tolist()],
                        "error_sets_from": "device pre-sampling" if args.device_presample else "host matrix",
                        "l2": "per-step working set (work lists, hoisted records, population vectors) exceeds the 126 MB L2"
                              if total_shots_local * 8 > 126e6 else "working set below L2 size (small workload)",

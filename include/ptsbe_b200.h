@@ -122,12 +122,6 @@ typedef struct {
    * prefixes entering stage p+1 (p = j-1 is the marginal pass itself) */
   const ptsbe_program_desc* programs; /* stage-major, f*(f+1)/2 entries */
   uint64_t max_intermediate;          /* ceiling, informational (checked at compile time) */
-  /* Mean shots per error set of the WHOLE job (all ranks, all calls), or 0.  When > 0 the choice
-   * between the flat sampler and the per-qubit descent is made per stage from this number and the
-   * stage offset alone -- expected shots per work item = hint / min(hint, 2^offset_j) -- so it does
-   * not depend on how error sets are grouped into calls, chunks or ranks (determinism contract of
-   * the reference, tests/test_engine.py:455-463).  0: decided per chunk from its actual work list. */
-  double shots_per_set_hint;
   /* [n_sites] number of operator variants (Kraus indices 0..v-1) of every gate site in this plan's
    * tables, or NULL.  When given, every Kraus-index matrix handed to the plan is checked on the
    * device and an out-of-range index (e.g. error sets encoded against other tables) is refused
@@ -175,6 +169,14 @@ const char* ptsbe_version(void);
  * (engine.py:864-879 warm loop; planner.py:343-442 PathCache) */
 int ptsbe_plan_create(const ptsbe_plan_desc* desc, int device, ptsbe_plan** out);
 void ptsbe_plan_destroy(ptsbe_plan* plan);
+
+/* Per-stage choice between the two samplers of rng.multinomial's categorical draw
+ * (engine.py:519): kinds[j] = 0 flat inverse-CDF sampler over the 2^b population vector,
+ * 1 per-qubit descent (few shots per work item), -1 decide per chunk from its work list (default).
+ * A fixed choice makes complex64 results independent of how error sets are grouped into calls,
+ * chunks and ranks (determinism under sharding, reference tests/test_engine.py:455-463): the host
+ * derives it once per plan from a pilot run of the error-free circuit. */
+int ptsbe_plan_set_stage_samplers(ptsbe_plan* plan, const int32_t* kinds, uint32_t n_stages);
 
 /* replaces: conditional_marginal / _contract_marginal for a batch of W work
  * items of one stage (engine.py:417-477).

@@ -30,6 +30,7 @@ EXPORTS = (
     "ptsbe_batch_destroy", "ptsbe_histogram_merge", "ptsbe_plan_greedy", "ptsbe_free",
     "ptsbe_batch_histogram_dev", "ptsbe_histogram_merge_dev", "ptsbe_free_dev",
     "ptsbe_measure_fma_peak", "ptsbe_sample_nonproportional", "ptsbe_batch_presample", "ptsbe_batch_kraus",
+    "ptsbe_plan_set_stage_samplers",
 )
 
 
@@ -86,6 +87,7 @@ def load() -> ctypes.CDLL:
     lib.ptsbe_plan_create.argtypes = [ctypes.POINTER(PlanDesc), I, ctypes.POINTER(P)]
     lib.ptsbe_plan_destroy.argtypes = [P]
     lib.ptsbe_plan_destroy.restype = None
+    lib.ptsbe_plan_set_stage_samplers.argtypes = [P, P, U32]
     lib.ptsbe_marginals.argtypes = [P, U32, P, P, U64, P, P, P]
     lib.ptsbe_execute_raw.argtypes = [P, P]
     lib.ptsbe_sample_stage.argtypes = [U32, U32, U64, U64, P, P, P, P,
@@ -273,6 +275,11 @@ class DevicePlan:
             self.close()
         except Exception:
             pass
+
+    def set_stage_samplers(self, kinds) -> None:
+        """Fix the sampler of every stage: 0 flat, 1 per-qubit descent, -1 per-chunk choice."""
+        kinds = np.ascontiguousarray(kinds, dtype=np.int32)
+        check(load().ptsbe_plan_set_stage_samplers(self._h, _ptr(kinds), kinds.size))
 
     def _check_inputs(self, kraus_idx, shots, eset_ids):
         """Shapes and dtypes of the flat arrays the C ABI copies from (it trusts its sizes)."""

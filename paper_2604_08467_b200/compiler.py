@@ -708,7 +708,6 @@ class PlanDesc(ctypes.Structure):
         ("pool_elems", ctypes.c_uint64),
         ("programs", ctypes.c_void_p),
         ("max_intermediate", ctypes.c_uint64),
-        ("shots_per_set_hint", ctypes.c_double),
         ("site_variants", ctypes.c_void_p),
     ]
 
@@ -724,7 +723,6 @@ class CompiledPlan:
     pool: np.ndarray
     programs: list  # stage-major flat list of Program
     max_intermediate: int
-    shots_per_set_hint: float = 0.0
     site_variants: Optional[np.ndarray] = None  # [n_sites] u8: variants per gate site (index validation)
     _keep: list = field(default_factory=list)
 
@@ -768,6 +766,5 @@ class CompiledPlan:
             pool.size,
             ctypes.addressof(arr),
             self.max_intermediate,
-            float(self.shots_per_set_hint),
             sv.ctypes.data if sv is not None else None,
         )

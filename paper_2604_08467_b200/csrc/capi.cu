@@ -66,7 +66,7 @@ struct ptsbe_plan {
   uint32_t lane = 1;                   // lane-per-item interpreter / fused descent (lane.cuh)
   uint32_t descent = 1;                // per-qubit descent sampler for low-multiplicity stages
   double descent_mult = 4.0;           // ... used when shots / unique prefixes of the stage <= this
-  // per stage: 1 descent, 0 flat, -1 decide per chunk (no shots_per_set_hint in the descriptor)
+  // per stage: 1 descent, 0 flat, -1 decide per chunk (ptsbe_plan_set_stage_samplers)
   std::vector<int> stage_descent;
   DevBuf site_variants;                // [g] u8 variants per site, or empty (no index validation)
   uint64_t chunk_shots = 1ull << 26;
@@ -1390,16 +1390,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     if (const char* dm = getenv("PTSBE_DESCENT_MULT")) if (*dm) pl->descent_mult = atof(dm);
     pl->chunk_shots = env_size("PTSBE_CHUNK_SHOTS", pl->chunk_shots);
     pl->ext_budget = env_size("PTSBE_EXT_BYTES", pl->ext_budget);
-    // sampler choice per stage from plan-level quantities only (grouping / sharding independent)
-    for (uint32_t j = 0; j < d->n_stages; ++j) {
-      int h = -1;
-      if (d->shots_per_set_hint > 0.0) {
-        const double m = d->shots_per_set_hint;
-        const double prefixes = pl->offsets[j] >= 62 ? m : std::min(m, std::ldexp(1.0, (int)pl->offsets[j]));
-        h = m / std::max(prefixes, 1.0) <= pl->descent_mult ? 1 : 0;
-      }
-      pl->stage_descent.push_back(h);
-    }
+    pl->stage_descent.assign(d->n_stages, -1);
     const bool use_memo = env_size("PTSBE_MEMO", 1) != 0;  // variant-0 memo of class-0 programs
     cudaStream_t st = pl->stream;
     pl->pool.alloc(std::max<size_t>(16, d->pool_elems * pl->elem), st);
@@ -1487,6 +1478,18 @@ void ptsbe_plan_destroy(ptsbe_plan* pl) {
   cudaStreamSynchronize(pl->stream);
   cudaStreamDestroy(pl->stream);
   delete pl;
+}
+
+int ptsbe_plan_set_stage_samplers(ptsbe_plan* pl, const int32_t* kinds, uint32_t n_stages) {
+  return guarded([&] {
+    if (!pl || !kinds) throw Failure(PTSBE_EINVAL, "null argument");
+    if (n_stages != pl->f) throw Failure(PTSBE_EINVAL, "one sampler kind per stage expected");
+    std::lock_guard<std::mutex> lock(pl->mu);
+    for (uint32_t j = 0; j < n_stages; ++j) {
+      if (kinds[j] < -1 || kinds[j] > 1) throw Failure(PTSBE_EINVAL, "sampler kind must be -1 (auto), 0 (flat) or 1 (descent)");
+      pl->stage_descent[j] = kinds[j];
+    }
+  });
 }
 
 int ptsbe_marginals(ptsbe_plan* pl, uint32_t stage, const uint8_t* kraus_idx,

@@ -598,7 +598,7 @@ class DevicePipeline:
 
     def __init__(self, cnet: CircuitNetwork, plan: BatchPlan, tables: VariantTables,
                  ctx: SamplerContext, stages: Optional[Sequence[int]] = None,
-                 shots_per_set: float = 1.0, upload: bool = True):
+                 shots_per_set: float = 1.0, upload: bool = True, calibrate: bool = False):
         from . import _capi
 
         if plan.n != cnet.n:
@@ -641,11 +641,38 @@ class DevicePipeline:
         self.compiled = CompiledPlan(
             dtype=ctx.dtype, n_qubits=plan.n, n_sites=tables.n_sites, sizes=plan.sizes,
             pool=pool.finish(ctx.dtype), programs=programs, max_intermediate=ctx.max_intermediate,
-            shots_per_set_hint=float(shots_per_set),
             site_variants=np.asarray([min(d.shape[0], 255) for d in tables.data], dtype=np.uint8),
         )
         # upload=False: compile only (plan inspection; CPU-side tests of the compiler)
         self.device_plan = _capi.DevicePlan(self.compiled, ctx.device) if upload else None
+        self.stage_samplers = None
+        if calibrate and self.device_plan is not None and stages is None:
+            self.calibrate_samplers(shots_per_set)
+
+    def calibrate_samplers(self, shots_per_set: float) -> None:
+        """Pilot run that fixes the sampler of every stage for the life of the plan.  The device
+        has two samplers for the categorical draws of engine.py:519 -- flat inverse CDF over the 2^b
+        populations, per-qubit descent -- and the better one depends on the shots a work item
+        carries.  Choosing per chunk from the chunk's own work list would make complex64 results
+        depend on how error sets are grouped into calls, chunks and ranks; instead ONE error set
+        (the error-free circuit, the job's mean shots, fixed seed, flat sampler) is run here and
+        stage j gets the descent iff shots / unique prefixes entering it is at most DESCENT_MULT.
+        Same circuit + plan + shots => same choice on every rank and in every call."""
+        import os
+
+        m = int(min(max(round(shots_per_set), 1), 1 << 17))
+        f = self.plan.f
+        dp = self.device_plan
+        dp.set_stage_samplers(np.zeros(f, np.int32))
+        _, _, _, st = dp.sample(np.zeros((1, self.tables.n_sites), np.uint8), np.asarray([m], np.uint32),
+                                np.zeros(1, np.uint32), 0x5EED, merged=True)
+        mult = float(os.environ.get("PTSBE_DESCENT_MULT") or 4.0)
+        kinds = np.zeros(f, np.int32)
+        for j in range(1, f):
+            u = int(st.stage_events[j])
+            kinds[j] = 1 if (u and m <= mult * u) else 0
+        dp.set_stage_samplers(kinds)
+        self.stage_samplers = kinds
 
     def close(self):
         if self.device_plan is not None:
@@ -819,7 +846,7 @@ def sample_proportional_batched(
     ctx.check_deadline()
     tables = VariantTables.from_errorsets(template, errorsets)
     shots = np.asarray([k.m for k in errorsets], dtype=np.uint32)
-    pipe = DevicePipeline(template, plan, tables, ctx, shots_per_set=float(shots.mean()))
+    pipe = DevicePipeline(template, plan, tables, ctx, shots_per_set=float(shots.mean()), calibrate=True)
     try:
         keys, esets, counts, st = pipe.device_plan.sample(
             tables.encode(errorsets), shots, np.asarray([k.id for k in errorsets], dtype=np.uint32),
@@ -1080,7 +1107,8 @@ def run_ptsbe(c: Circuit, config: RunConfig, cache: Optional[PathCache] = None,
     if not nonprop and shots.min() < 1:
         raise ValueError("proportional sampling needs m >= 1")
     pipe = DevicePipeline(template, plan, tables, ctx,
-                          shots_per_set=float(plan.nonfinal_shots) if nonprop else float(shots.mean()))
+                          shots_per_set=float(plan.nonfinal_shots) if nonprop else float(shots.mean()),
+                          calibrate=not nonprop)
     plan_s = time.perf_counter() - t0
     all_sets = errorsets
     if _shard is not None:

@@ -251,7 +251,7 @@ def run_ptsbe_sharded(c, config, errorsets, *, group=None, cache=None):
     shots_all = np.asarray([k.m for k in errorsets], dtype=np.uint32)
     if shots_all.min() < 1:
         raise ValueError("proportional sampling needs m >= 1")
-    pipe = engine.DevicePipeline(template, plan, tables, ctx, shots_per_set=float(shots_all.mean()))
+    pipe = engine.DevicePipeline(template, plan, tables, ctx, shots_per_set=float(shots_all.mean()), calibrate=True)
     plan_s = time.perf_counter() - t0
     words = max(1, (plan.n + 63) // 64)
     batch, st, err = None, None, None
