@@ -62,11 +62,16 @@ def build_workload(name: str, args):
         c, sizes = workloads.ghz(12, p=0.01)
         dflt = dict(sets=64, shots=1000, dtype="complex64", label="cfg1: 12-qubit GHZ, depolarizing 0.01")
     elif name == "cfg3":
-        c, sizes = workloads.surface_code(5, 3, p=1e-3)
+        c, sizes = workloads.surface_code(5, 3, p=1e-3, order="ancilla_first")
         dflt = dict(sets=100_000, shots=1, dtype="complex64", label="cfg3: surface code d=5, 3 rounds, p=1e-3")
     elif name == "cfg4":
         c, sizes = workloads.qaoa(50, 2, p=1e-3, seed=4)
         dflt = dict(sets=10_000, shots=10_000, dtype="complex128", label="cfg4: 50-qubit QAOA p=2, 3-regular")
+    elif name == "cfg3r1":
+        # largest member of the cfg3 family that exact dense contraction reaches: the d = 5 lattice, one round
+        # (49 qubits, ancilla blocks first); DESIGN.md section 6b has the width study of 2 and 3 rounds
+        c, sizes = workloads.surface_code(5, 1, p=1e-3, order="ancilla_first")
+        dflt = dict(sets=100_000, shots=1, dtype="complex64", label="cfg3 at one round: surface code d=5, 1 round, p=1e-3 (49 qubits)")
     elif name == "cfg3s":
         # the full-size cfg3 / cfg4 networks exceed the 2^26-entry intermediate ceiling (the reference's own
         # execute_path raises ResourceLimitError for them too); these are the largest twins that plan
@@ -234,7 +239,7 @@ def cpu_sample_size(name: str):
     """(error sets, shots per set) of the bounded CPU sample: about 10-30 s of
     host work for the whole pool."""
     return {"cfg1": (64, 1000), "cfg2": (None, 48), "cfg3": (None, 1), "cfg4": (None, 8),
-            "cfg5": (None, 40), "cfg3s": (64, 1), "cfg4s": (None, 50), "harvest24": (None, 1)}[name]
+            "cfg5": (None, 40), "cfg3r1": (None, 1), "cfg3s": (64, 1), "cfg4s": (None, 50), "harvest24": (None, 1)}[name]
 
 
 # --------------------------------------------------------------------------
@@ -486,7 +491,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfg3s", "cfg4s", "harvest24"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfg3r1", "cfg3s", "cfg4s", "harvest24"])
     ap.add_argument("--sets", type=int, default=0, help="error sets PER GPU")
     ap.add_argument("--shots", type=int, default=0, help="shots per error set")
     ap.add_argument("--plan", default="", help="comma-separated batch sizes")

@@ -300,6 +300,15 @@ int ptsbe_measure_fma_peak(int device, double* fp32_tflops, double* fp64_tflops)
 
 void ptsbe_free(void* p);
 
+/* Test / measurement probe of the dense projection step P[i][c] = Re(sum_d v_i[d] M_e(i)[d][c])
+ * (the last np.tensordot of execute_path, tensor.py:190-216, engine.py:442-445) on raw complex64
+ * arrays: v [n_items][D], m [n_sets][D][N], eset [n_items] sorted error-set rows; out [n_items][N].
+ * use_tc = 1: tcgen05 / TMEM / TMA kernel (csrc/project_tc.cuh), 0: FP32 FMA kernel (csrc/project.cuh).
+ * kernel_ms: device time of one launch (average of reps), prep_ms: building the B images (tc only). */
+int ptsbe_project_probe(int device, uint32_t D, uint32_t N, uint64_t n_items, uint32_t n_sets,
+                        const uint32_t* eset, const float* v, const float* m, int use_tc, float* out,
+                        int reps, float* kernel_ms, float* prep_ms);
+
 #ifdef __cplusplus
 }
 #endif

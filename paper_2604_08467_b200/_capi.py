@@ -30,7 +30,7 @@ EXPORTS = (
     "ptsbe_batch_destroy", "ptsbe_histogram_merge", "ptsbe_plan_greedy", "ptsbe_free",
     "ptsbe_batch_histogram_dev", "ptsbe_histogram_merge_dev", "ptsbe_free_dev",
     "ptsbe_measure_fma_peak", "ptsbe_sample_nonproportional", "ptsbe_batch_presample", "ptsbe_batch_kraus",
-    "ptsbe_plan_set_stage_samplers",
+    "ptsbe_plan_set_stage_samplers", "ptsbe_project_probe",
 )
 
 
@@ -117,6 +117,8 @@ def load() -> ctypes.CDLL:
     lib.ptsbe_free_dev.argtypes = [P]
     lib.ptsbe_free_dev.restype = None
     lib.ptsbe_measure_fma_peak.argtypes = [I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    lib.ptsbe_project_probe.argtypes = [I, U32, U32, U64, U32, P, P, P, I, P, I,
+                                        ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
     _lib = lib
     return lib
 
@@ -415,6 +417,23 @@ def histogram_merge_dev(keys_ptr: int, counts_ptr: int, n: int, words: int, devi
     check(load().ptsbe_histogram_merge_dev(keys_ptr, counts_ptr, n, words, device, ctypes.byref(ok),
                                            ctypes.byref(oc), ctypes.byref(m)))
     return (DeviceArray(ok.value, (m.value, words), owned=True), DeviceArray(oc.value, (m.value,), owned=True))
+
+
+def project_probe(v: np.ndarray, m: np.ndarray, eset: np.ndarray, use_tc: bool, reps: int = 1, device: int = 0):
+    """Dense projection step on raw complex64 arrays (ptsbe_project_probe): v [items, D], m [sets, D, N],
+    eset [items] sorted rows into m.  Returns (P [items, N] float32, kernel ms per launch, B-image prep ms)."""
+    v = np.ascontiguousarray(v, dtype=np.complex64)
+    m = np.ascontiguousarray(m, dtype=np.complex64)
+    eset = np.ascontiguousarray(eset, dtype=np.uint32)
+    n, d = v.shape
+    sets, d2, nn = m.shape
+    if d2 != d or eset.shape != (n,) or (n and int(eset.max()) >= sets):
+        raise ValueError("inconsistent shapes for the projection probe")
+    out = np.empty((n, nn), dtype=np.float32)
+    km, pm = ctypes.c_float(), ctypes.c_float()
+    check(load().ptsbe_project_probe(device, d, nn, n, sets, _ptr(eset), _ptr(v), _ptr(m), 1 if use_tc else 0,
+                                     _ptr(out), int(reps), ctypes.byref(km), ctypes.byref(pm)))
+    return out, float(km.value), float(pm.value)
 
 
 def measure_fma_peak(device: int = 0) -> tuple:

@@ -20,6 +20,7 @@
 #include "histogram.cuh"
 #include "lane.cuh"
 #include "project.cuh"
+#include "project_tc.cuh"
 #include "sampler.cuh"
 #include "scan.cuh"
 
@@ -64,6 +65,7 @@ struct ptsbe_plan {
   size_t probs_budget = 256ull << 20;  // bytes of marginal buffer per sub-batch
   size_t vec_budget = 512ull << 20;    // bytes of per-item vectors per sub-batch (descent stages)
   uint32_t lane = 1;                   // lane-per-item interpreter / fused descent (lane.cuh)
+  uint32_t tc_project = 1;             // complex64 projection on tcgen05 tensor cores (project_tc.cuh)
   uint32_t descent = 1;                // per-qubit descent sampler for low-multiplicity stages
   double descent_mult = 4.0;           // ... used when shots / unique prefixes of the stage <= this
   // per stage: 1 descent, 0 flat, -1 decide per chunk (ptsbe_plan_set_stage_samplers)
@@ -617,6 +619,98 @@ static void launch_project(ptsbe_plan* pl, const Program& pr, const void* v, uin
   CK(cudaGetLastError());
 }
 
+// ---- tensor-core projection (project_tc.cuh) ----
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link against libcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return (EncodeTiledFn)p;
+  }();
+  if (!fn) throw Failure(PTSBE_EDEVICE, "cuTensorMapEncodeTiled is not available from this driver");
+  return fn;
+}
+
+// fp32 matrix [rows][k_floats] with row pitch `pitch_bytes`, tiles of box_rows x 32 floats, 128-byte swizzle
+static CUtensorMap tc_map_2d(const void* ptr, uint64_t k_floats, uint64_t rows, uint64_t pitch_bytes, uint32_t box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {k_floats, rows};
+  const cuuint64_t strides[1] = {pitch_bytes};
+  const cuuint32_t box[2] = {(cuuint32_t)TC_BK, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult rc = encode_tiled_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box,
+                                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) throw Failure(PTSBE_EDEVICE, "cuTensorMapEncodeTiled failed (" + std::to_string((int)rc) + ")");
+  return m;
+}
+
+struct TcShape {
+  uint32_t K = 0, kb = 0, stages = 0, tmem_cols = 0;
+  size_t smem = 0;
+  bool ok = false;
+};
+
+// K = 2 D padded to a multiple of 32 floats; ring depth from the shared memory one SM has
+static TcShape tc_shape(uint32_t D, uint32_t N) {
+  TcShape t;
+  if (N < 32 || N > 256 || (N & (N - 1)) || D < 1) return t;
+  t.K = (2 * D + TC_BK - 1) / TC_BK * TC_BK;
+  t.kb = t.K / TC_BK;
+  const size_t stage = 2 * (size_t)TC_A_BYTES + 2 * (size_t)N * TC_BK * 4;
+  const size_t fixed = 1024 + 4 * 32 * 33 * 4 + (3 * TC_MAX_STAGES + 4) * 8 + 16;
+  t.stages = (uint32_t)std::min<size_t>(TC_MAX_STAGES, (220 * 1024 - fixed) / stage);
+  if (t.stages < 2) return t;
+  t.smem = fixed + t.stages * stage;
+  t.tmem_cols = 32;
+  while (t.tmem_cols < 2 * N) t.tmem_cols <<= 1;
+  t.ok = true;
+  return t;
+}
+
+// hi / lo K-major images of B_e for every error set of the chunk (once per stage)
+static void launch_tc_prep(ptsbe_plan* pl, const void* rec0, uint32_t rec_stride, uint32_t m_off, uint32_t n_sets,
+                           uint32_t D, uint32_t N, const TcShape& t, float* b_hi, float* b_lo) {
+  TcPrepArgs a;
+  a.rec0 = reinterpret_cast<const float2*>(rec0);
+  a.b_hi = b_hi;
+  a.b_lo = b_lo;
+  a.n_sets = n_sets; a.D = D; a.N = N; a.K = t.K; a.rec_stride = rec_stride; a.m_off = m_off;
+  tc_prep_b_kernel<<<dim3(n_sets, cdiv(N, 32)), 256, 0, pl->stream>>>(a);
+  g_launches++;
+  CK(cudaGetLastError());
+}
+
+// P = A . B_e on the tensor cores for the work items [first, first + n) of a level; vrows: one row of
+// t.K / 2 complex64 per item (zero padded), out [n][N] fp32
+static void launch_project_tc(ptsbe_plan* pl, const TcShape& t, const void* vrows, const float* b_hi, const float* b_lo,
+                              uint32_t n_sets, const uint32_t* eset, uint32_t first, uint32_t n, uint32_t N, void* out) {
+  if (n == 0) return;
+  const CUtensorMap ma = tc_map_2d(vrows, t.K, n, (uint64_t)t.K * 4, TC_BM);
+  const CUtensorMap mh = tc_map_2d(b_hi, t.K, (uint64_t)n_sets * N, (uint64_t)t.K * 4, N);
+  const CUtensorMap ml = tc_map_2d(b_lo, t.K, (uint64_t)n_sets * N, (uint64_t)t.K * 4, N);
+  TcProjectArgs a;
+  a.eset = eset;
+  a.out = reinterpret_cast<float*>(out);
+  a.first_item = first;
+  a.n_items = n;
+  a.N = N;
+  a.kb = t.kb;
+  a.stages = t.stages;
+  a.tmem_cols = t.tmem_cols;
+  opt_in_smem((const void*)project_tc_kernel, 227 * 1024);
+  const unsigned grid = (unsigned)std::min<uint64_t>(cdiv(n, TC_BM), (uint64_t)pl->sm_count);
+  project_tc_kernel<<<grid, TC_THREADS, t.smem, pl->stream>>>(ma, mh, ml, a);
+  g_launches++;
+  CK(cudaGetLastError());
+}
+
 static void launch_sampler(cudaStream_t st, SampleArgs& a, int sm_count) {
   if (a.n_items == 0) return;
   const size_t nb = 1ull << a.b;
@@ -919,11 +1013,35 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     uint32_t B = (uint32_t)std::max<size_t>(1, std::min<size_t>(U, pl->probs_budget / (nb * real)));
     DevBuf probs((size_t)B * nb * real, st), mass((size_t)B * 8, st), minv((size_t)B * 8, st);
     DevBuf vbuf;
-    if (proj) vbuf.alloc((size_t)vec_pitch(B) * progs[j - 1].d.proj_d * pl->elem, st);
+    // complex64 projections with long runs of items per error set go to the tensor cores
+    // (project_tc.cuh): v as one row per item, B_e images built once per error set for this stage
+    TcShape tcs;
+    if (proj && pl->tc_project && pl->dtype == PTSBE_C64 && (uint64_t)U >= 64ull * ne)
+      tcs = tc_shape(progs[j - 1].d.proj_d, nb);
+    DevBuf tc_bhi, tc_blo;
+    if (tcs.ok) {
+      vbuf.alloc((size_t)B * tcs.K * 4, st);
+      if (tcs.K != 2 * progs[j - 1].d.proj_d) CK(cudaMemsetAsync(vbuf.p, 0, (size_t)B * tcs.K * 4, st));
+      tc_bhi.alloc((size_t)ne * nb * tcs.K * 4, st);
+      tc_blo.alloc((size_t)ne * nb * tcs.K * 4, st);
+      log.begin(&stats->project_ms[j - 1]);
+      launch_tc_prep(pl, table[1].ext, table[1].ext_rec, progs[j - 1].d.result_ref, ne, progs[j - 1].d.proj_d, nb, tcs,
+                     tc_bhi.as<float>(), tc_blo.as<float>());
+      log.end();
+    } else if (proj) {
+      vbuf.alloc((size_t)vec_pitch(B) * progs[j - 1].d.proj_d * pl->elem, st);
+    }
     for (uint32_t s0 = 0; s0 < U; s0 += B) {
       const uint32_t nbatch = std::min(B, U - s0);
       log.begin(&stats->marg_ms[j - 1]);
-      if (proj) {
+      if (tcs.ok) {
+        launch_exec_any(pl, progs[j - 1], EXEC_VECTOR, table_dev.as<LevelDev>(), kraus_dev, s0,
+                        nbatch, vbuf.p, nullptr, nullptr, 0, tcs.K / 2);
+        log.end();
+        log.begin(&stats->project_ms[j - 1]);
+        launch_project_tc(pl, tcs, vbuf.p, tc_bhi.as<float>(), tc_blo.as<float>(), ne, cur.eset.as<uint32_t>(), s0,
+                          nbatch, nb, probs.p);
+      } else if (proj) {
         launch_exec_any(pl, progs[j - 1], EXEC_VECTOR, table_dev.as<LevelDev>(), kraus_dev, s0,
                         nbatch, vbuf.p, nullptr, nullptr, vec_pitch(nbatch));
         log.end();
@@ -1386,6 +1504,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     pl->probs_budget = env_size("PTSBE_PROBS_BYTES", pl->probs_budget);
     pl->vec_budget = env_size("PTSBE_VEC_BYTES", pl->vec_budget);
     pl->descent = (uint32_t)env_size("PTSBE_DESCENT", pl->descent);
+    pl->tc_project = (uint32_t)env_size("PTSBE_TC_PROJECT", pl->tc_project);
     pl->lane = (uint32_t)env_size("PTSBE_LANE", pl->lane);
     if (const char* dm = getenv("PTSBE_DESCENT_MULT")) if (*dm) pl->descent_mult = atof(dm);
     pl->chunk_shots = env_size("PTSBE_CHUNK_SHOTS", pl->chunk_shots);
@@ -1993,6 +2112,80 @@ int ptsbe_sample_nonproportional(ptsbe_plan* pl, const uint8_t* kraus_idx, const
     }
     pl->give_workspace(std::move(ws_tmp));
     pl->give_workspace(std::move(ws_out));
+  });
+}
+
+int ptsbe_project_probe(int device, uint32_t D, uint32_t N, uint64_t n_items, uint32_t n_sets,
+                        const uint32_t* eset, const float* v, const float* m, int use_tc, float* out,
+                        int reps, float* kernel_ms, float* prep_ms) {
+  return guarded([&] {
+    if (!eset || !v || !m || !out || !n_items || !n_sets) throw Failure(PTSBE_EINVAL, "null or empty argument");
+    if (ptsbe_device_count() <= device) throw Failure(PTSBE_EDEVICE, "no CUDA device: libptsbe_b200 has no CPU fallback");
+    CK(cudaSetDevice(device));
+    ptsbe_plan pl;
+    pl.device = device;
+    pl.dtype = PTSBE_C64;
+    pl.elem = 8;
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    pl.sm_count = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&pl.stream, cudaStreamNonBlocking));
+    cudaStream_t st = pl.stream;
+    const uint32_t n = (uint32_t)n_items;
+    cudaEvent_t e0, e1, e2;
+    CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1)); CK(cudaEventCreate(&e2));
+    {
+      DevBuf es((size_t)n * 4, st), rec((size_t)n_sets * D * N * 8, st), po((size_t)n * N * 4, st);
+      CK(cudaMemcpyAsync(es.p, eset, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(rec.p, m, (size_t)n_sets * D * N * 8, cudaMemcpyHostToDevice, st));
+      CK(cudaMemsetAsync(po.p, 0xff, (size_t)n * N * 4, st));
+      Program pr;
+      memset(&pr.d, 0, sizeof pr.d);
+      pr.d.proj_d = D;
+      pr.d.out_elems = N;
+      pr.d.result_ref = 0;
+      float pm = 0, km = 0;
+      if (use_tc) {
+        const TcShape t = tc_shape(D, N);
+        if (!t.ok) throw Failure(PTSBE_EINVAL, "tensor-core projection needs N = 32 .. 256 (power of two)");
+        DevBuf vr((size_t)n * t.K * 4, st), bh((size_t)n_sets * N * t.K * 4, st), bl((size_t)n_sets * N * t.K * 4, st);
+        CK(cudaMemsetAsync(vr.p, 0, (size_t)n * t.K * 4, st));
+        CK(cudaMemcpy2DAsync(vr.p, (size_t)t.K * 4, v, (size_t)D * 8, (size_t)D * 8, n, cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(e0, st));
+        launch_tc_prep(&pl, rec.p, D * N, 0, n_sets, D, N, t, bh.as<float>(), bl.as<float>());
+        CK(cudaEventRecord(e1, st));
+        for (int r = 0; r < std::max(reps, 1); ++r)
+          launch_project_tc(&pl, t, vr.p, bh.as<float>(), bl.as<float>(), n_sets, es.as<uint32_t>(), 0, n, N, po.p);
+        CK(cudaEventRecord(e2, st));
+        CK(cudaStreamSynchronize(st));
+        CK(cudaEventElapsedTime(&pm, e0, e1));
+        CK(cudaEventElapsedTime(&km, e1, e2));
+      } else {
+        const uint32_t pitch = vec_pitch(n);
+        std::vector<float> vt((size_t)D * pitch * 2, 0.f);
+        for (uint32_t i = 0; i < n; ++i)
+          for (uint32_t d = 0; d < D; ++d) {
+            vt[((size_t)d * pitch + i) * 2] = v[((size_t)i * D + d) * 2];
+            vt[((size_t)d * pitch + i) * 2 + 1] = v[((size_t)i * D + d) * 2 + 1];
+          }
+        DevBuf vd(vt.size() * 4, st);
+        CK(cudaMemcpyAsync(vd.p, vt.data(), vt.size() * 4, cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(e1, st));
+        for (int r = 0; r < std::max(reps, 1); ++r)
+          launch_project(&pl, pr, vd.p, pitch, rec.p, D * N, es.as<uint32_t>(), 0, n, po.p);
+        CK(cudaEventRecord(e2, st));
+        CK(cudaStreamSynchronize(st));
+        CK(cudaEventElapsedTime(&km, e1, e2));
+      }
+      CK(cudaMemcpyAsync(out, po.p, (size_t)n * N * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (kernel_ms) *kernel_ms = km / std::max(reps, 1);
+      if (prep_ms) *prep_ms = pm;
+    }
+    cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
+    CK(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    pl.stream = nullptr;
   });
 }
 

@@ -43,13 +43,18 @@ def hea(n: int = 30, depth: int = 6, gamma: float = 0.01, p: float = 0.01, seed:
     return Circuit(n, tuple(gates)), _even(n, 10)
 
 
-def surface_code(d: int = 5, rounds: int = 3, p: float = 1e-3) -> tuple:
+def surface_code(d: int = 5, rounds: int = 3, p: float = 1e-3, order: str = "data_first", batch: int = 8) -> tuple:
     """cfg3: rotated surface code memory-Z experiment, circuit-level noise,
     deferred measurement with a fresh ancilla per stabiliser per round:
-    n = d^2 + rounds * (d^2 - 1) qubits.  Data qubits first, then ancillas
-    round by round.  X-type ancillas: H, 4 (or 2) CX ancilla->data, H;
-    Z-type: CX data->ancilla.  Two-qubit depolarizing p after every CX,
-    single-qubit depolarizing p after every H."""
+    n = d^2 + rounds * (d^2 - 1) qubits.  X-type ancillas: H, 4 (or 2) CX
+    ancilla->data, H; Z-type: CX data->ancilla.  Two-qubit depolarizing p after
+    every CX, single-qubit depolarizing p after every H.
+
+    order="data_first" (the golden twins): data qubits 0..d^2-1, then ancillas
+    round by round, batches of `batch` qubits.  order="ancilla_first" (SURVEY
+    8d: per-round ancilla blocks, data last): round-1 ancillas, round-2
+    ancillas, ..., data; batches never straddle a round, so the unitary light
+    cone of the stages of round r stops at round r."""
     data = {(r, c): r * d + c for r in range(d) for c in range(d)}
     stabs = []  # (type, [data qubits])
     for r in range(-1, d):
@@ -80,8 +85,18 @@ def surface_code(d: int = 5, rounds: int = 3, p: float = 1e-3) -> tuple:
             else:
                 for q in members:
                     gates.append(Gate("CX", (q, anc), None, NoiseChannel("depolarizing", p)))
-    sizes = _even(n, 8)
-    return Circuit(n, tuple(gates)), sizes
+    if order == "data_first":
+        return Circuit(n, tuple(gates)), _even(n, batch)
+    if order != "ancilla_first":
+        raise ValueError(f"unknown qubit order {order!r}")
+    n_data, n_anc = d * d, len(stabs)
+    pos = {q: rounds * n_anc + q for q in range(n_data)}
+    pos.update({n_data + k: k for k in range(rounds * n_anc)})
+    gates = [Gate(g.kind, tuple(pos[q] for q in g.targets), g.angle, g.noise) for g in gates]
+    sizes = []
+    for block in [n_anc] * rounds + [n_data]:
+        sizes += list(_even(block, batch))
+    return Circuit(n, tuple(gates)), tuple(sizes)
 
 
 def qaoa(n: int = 50, layers: int = 2, p: float = 1e-3, seed: int = 4) -> tuple:
