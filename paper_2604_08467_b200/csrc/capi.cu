@@ -19,6 +19,7 @@
 #include "executor.cuh"
 #include "histogram.cuh"
 #include "lane.cuh"
+#include "lane_x.cuh"
 #include "project.cuh"
 #include "project_tc.cuh"
 #include "sampler.cuh"
@@ -45,6 +46,11 @@ struct Program {
   bool herm = false;
   std::vector<uint32_t> herm_map_host;
   DevBuf herm_map;
+  // ... with x of herm_dx in {2, 4, 8} complex entries: lane-per-draw kernel (lane_x.cuh) over tree columns in
+  // canonical order; herm_canon[s] = position | sign << 31 of packed slot s
+  uint32_t herm_dx = 0;
+  std::vector<uint32_t> herm_canon_host;
+  DevBuf herm_canon;
 };
 
 }  // namespace ptsbe
@@ -66,6 +72,7 @@ struct ptsbe_plan {
   size_t vec_budget = 512ull << 20;    // bytes of per-item vectors per sub-batch (descent stages)
   uint32_t lane = 1;                   // lane-per-item interpreter / fused descent (lane.cuh)
   uint32_t tc_project = 1;             // complex64 projection on tcgen05 tensor cores (project_tc.cuh)
+  uint32_t lane_x = 1;                 // lane-per-draw fused descent for Hermitian cuts (lane_x.cuh)
   uint32_t descent = 1;                // per-qubit descent sampler for low-multiplicity stages
   double descent_mult = 4.0;           // ... used when shots / unique prefixes of the stage <= this
   // per stage: 1 descent, 0 flat, -1 decide per chunk (ptsbe_plan_set_stage_samplers)
@@ -383,6 +390,39 @@ static void classify_lane(const ptsbe_plan* pl, Program& pr) {
       pr.herm = pr.herm_map_host.size() == D;
       if (!pr.herm) pr.herm_map_host.clear();
     }
+    // canonical order of lane_x.cuh: x has DX entries at element offsets 0 .. DX-1 of the operand
+    pr.herm_dx = 0;
+    pr.herm_canon_host.clear();
+    uint32_t dx = 0;
+    for (uint32_t k : {4u, 8u}) if (k * k == D) dx = k;  // packed rows of exactly D reals (herm_shape pads below 16)
+    if (pr.herm && dx && pl->dtype == PTSBE_C64) {
+      bool fine = true;
+      std::vector<uint32_t> canon(D, 0), hit(D, 0);
+      for (uint32_t s2 = 0; fine && s2 < D; ++s2) {
+        const uint32_t m = pr.herm_map_host[s2];
+        const uint32_t c = m & 0xfffu, c2 = (m >> 12) & 0xfffu, kind = m >> 24;
+        uint32_t p = ab[c].first, q = ab[c].second;
+        if ((flags & 3u) == 1u) std::swap(p, q);  // v_c = conj(x_a) x_b = x_b conj(x_a)
+        if (p >= dx || q >= dx || (c == c2) != (p == q)) { fine = false; break; }
+        uint32_t pos, neg = 0;
+        if (p == q) {
+          pos = p;
+        } else {
+          const uint32_t lo = std::min(p, q), hi = std::max(p, q);
+          uint32_t idx = 0;
+          for (uint32_t z = 0; z < lo; ++z) idx += dx - 1 - z;
+          idx += hi - lo - 1;
+          pos = dx + 2 * idx + (kind ? 1u : 0u);
+          neg = (kind == 1 && p > q) ? 1u : 0u;
+        }
+        if (pos >= D || hit[pos]++) { fine = false; break; }
+        canon[s2] = pos | (neg << 31);
+      }
+      if (fine) {
+        pr.herm_dx = dx;
+        pr.herm_canon_host = canon;
+      }
+    }
   }
 }
 
@@ -493,7 +533,7 @@ static void launch_lane_descent_t(ptsbe_plan* pl, Program& pr, LaneDescentArgs& 
   const LaneLayout L = lane_layout(a.l.e.n_steps, a.l.n_leaves, a.l.n_table_words, a.l.n_levels,
                                    a.l.e.arena_fast, a.l.e.words, (uint32_t)sizeof(C));
   const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4) +
-                      (((size_t)(LN_GS * NCH + 1) * sizeof(CH)) << a.d.b);
+                      (((size_t)(LN_GS * NCH + (NCH >= 2 ? 0 : 1)) * sizeof(CH)) << a.d.b);
   if (smem > 200 * 1024) throw Failure(PTSBE_ERESOURCE, "fused descent needs more shared memory than one SM has");
   if (pr.lane_blocks_per_sm == 0) {
     CK(cudaFuncSetAttribute(lane_descent_kernel<R, NCH, HERM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -514,19 +554,47 @@ static void launch_lane_descent_t(ptsbe_plan* pl, Program& pr, LaneDescentArgs& 
   CK(cudaGetLastError());
 }
 
+template <int DX>
+static void launch_lane_descent_x(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a) {
+  const LaneLayout L = lane_layout(a.l.e.n_steps, a.l.n_leaves, a.l.n_table_words, a.l.n_levels,
+                                   a.l.e.arena_fast, a.l.e.words, (uint32_t)sizeof(float2));
+  constexpr size_t NQ = DX * DX / 4 > 0 ? DX * DX / 4 : 1;
+  const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4) + (((NQ + 1) * 16) << a.d.b);
+  if (smem > 200 * 1024) throw Failure(PTSBE_ERESOURCE, "fused descent needs more shared memory than one SM has");
+  opt_in_smem((const void*)lane_descent_x_kernel<DX>, 200 * 1024);
+  const int per_sm = cached_occupancy((const void*)lane_descent_x_kernel<DX>, LN_THREADS, smem);
+  const uint64_t ctas = (uint64_t)pl->sm_count * per_sm;
+  uint64_t tile = a.d.n_items / (ctas * 4) / LN_THREADS * LN_THREADS;
+  tile = std::min<uint64_t>(2048, std::max<uint64_t>(LN_THREADS, tile));
+  a.tile = (uint32_t)tile;
+  const uint64_t tiles = cdiv(a.d.n_items, tile);
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, ctas));
+  lane_descent_x_kernel<DX><<<grid, LN_THREADS, smem, pl->stream>>>(a);
+  g_launches++;
+  CK(cudaGetLastError());
+}
+
 static bool lane_descent_fits(const ptsbe_plan* pl, const Program& pr, const DescentShape& sh, uint32_t b) {
   const uint32_t elem = (uint32_t)pl->elem;
   const LaneLayout L = lane_layout(pr.d.n_steps, pr.d.n_leaves, pr.d.n_table_words, pl->f + 2,
                                    pr.d.arena_fast_elems, pl->words, elem);
   // sh is the 8-lane shape of descent.cuh; the fused kernel spreads the same padded column over LN_GS lanes
   const uint32_t nch_f = sh.nch * (DS_GS / LN_GS);
-  const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4) + (((size_t)(LN_GS * nch_f + 1) * 16) << b);
+  const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4) + (((size_t)(LN_GS * nch_f + (nch_f >= 2 ? 0 : 1)) * 16) << b);
   return nch_f <= 8 && smem <= 200 * 1024;
 }
 
 static void launch_lane_descent(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a, const DescentShape& sh) {
   if (a.d.n_items == 0) return;
   const bool f32 = pl->dtype == PTSBE_C64;
+  if (a.herm_map && f32 && pr.herm_dx && pl->lane_x) {
+    // x (x) conj(x) with a small x: one lane per draw over canonically packed columns (lane_x.cuh)
+    switch (pr.herm_dx) {
+      case 4: launch_lane_descent_x<4>(pl, pr, a); return;
+      case 8: launch_lane_descent_x<8>(pl, pr, a); return;
+      default: break;
+    }
+  }
   if (a.herm_map) {
     switch (sh.nch) {
       case 1: f32 ? launch_lane_descent_t<float, 1, true>(pl, pr, a) : launch_lane_descent_t<double, 1, true>(pl, pr, a); break;
@@ -898,6 +966,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
           hp.tree = tree.p;
           hp.packed = htree.p;
           hp.map = prj.herm_map.as<uint32_t>();
+          hp.canon = (prj.herm_dx && pl->lane_x) ? prj.herm_canon.as<uint32_t>() : nullptr;
           hp.D = prj.d.proj_d;
           hp.dpad_c = dsh.dpad;
           hp.dpad_r = hsh.dpad;
@@ -1505,6 +1574,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     pl->vec_budget = env_size("PTSBE_VEC_BYTES", pl->vec_budget);
     pl->descent = (uint32_t)env_size("PTSBE_DESCENT", pl->descent);
     pl->tc_project = (uint32_t)env_size("PTSBE_TC_PROJECT", pl->tc_project);
+    pl->lane_x = (uint32_t)env_size("PTSBE_LANE_X", pl->lane_x);
     pl->lane = (uint32_t)env_size("PTSBE_LANE", pl->lane);
     if (const char* dm = getenv("PTSBE_DESCENT_MULT")) if (*dm) pl->descent_mult = atof(dm);
     pl->chunk_shots = env_size("PTSBE_CHUNK_SHOTS", pl->chunk_shots);
@@ -1547,6 +1617,11 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
                              cudaMemcpyHostToDevice, st));
         classify_lane(pl.get(), pr);
         if (pr.herm && env_size("PTSBE_HERM", 1)) {
+          if (pr.herm_dx) {
+            pr.herm_canon.alloc(pr.herm_canon_host.size() * 4, st);
+            CK(cudaMemcpyAsync(pr.herm_canon.p, pr.herm_canon_host.data(), pr.herm_canon_host.size() * 4,
+                               cudaMemcpyHostToDevice, st));
+          }
           pr.herm_map.alloc(pr.herm_map_host.size() * 4, st);
           CK(cudaMemcpyAsync(pr.herm_map.p, pr.herm_map_host.data(), pr.herm_map_host.size() * 4,
                              cudaMemcpyHostToDevice, st));
@@ -1592,7 +1667,7 @@ void ptsbe_plan_destroy(ptsbe_plan* pl) {
   for (auto& s : pl->programs)
     for (auto& p : s) {
       p.leaves.release(); p.steps.release(); p.tables.release();
-      p.memo_ptr.release(); p.memo_idx.release(); p.memo.release(); p.herm_map.release();
+      p.memo_ptr.release(); p.memo_idx.release(); p.memo.release(); p.herm_map.release(); p.herm_canon.release();
     }
   cudaStreamSynchronize(pl->stream);
   cudaStreamDestroy(pl->stream);

@@ -406,6 +406,8 @@ struct HermPackArgs {
   const void* tree;         // [sets][N][dpad_c] complex columns (tree_build_kernel)
   void* packed;             // [sets][N][dpad_r] reals
   const uint32_t* map;      // [D] c | c' << 12 | kind << 24
+  const uint32_t* canon;    // null, or [D]: slot s is stored at position canon[s] & 0xffff, negated if bit 31 is
+                            // set (canonical order of lane_x.cuh)
   uint32_t D, dpad_c, dpad_r, b;
 };
 
@@ -418,6 +420,7 @@ __global__ void herm_pack_kernel(const HermPackArgs a) {
   if (x >= N * a.dpad_r) return;
   const uint32_t node = x / a.dpad_r, s = x % a.dpad_r;
   R out = R(0);
+  uint32_t dst = s;
   if (s < a.D) {
     const uint32_t m = __ldg(a.map + s);
     const uint32_t c = m & 0xfffu, c2 = (m >> 12) & 0xfffu, kind = m >> 24;
@@ -425,8 +428,13 @@ __global__ void herm_pack_kernel(const HermPackArgs a) {
     const C u = col[c], w = col[c2];
     if (kind == 0) out = (c == c2) ? u.x : u.x + w.x;
     else if (kind == 1) out = -(u.y - w.y);
+    if (a.canon) {
+      const uint32_t cm = __ldg(a.canon + s);
+      dst = cm & 0xffffu;
+      if (cm >> 31) out = -out;
+    }
   }
-  reinterpret_cast<R*>(a.packed)[((size_t)e * N + node) * a.dpad_r + s] = out;
+  reinterpret_cast<R*>(a.packed)[((size_t)e * N + node) * a.dpad_r + dst] = out;
 }
 
 template <typename R, int NCH, bool HERM>
@@ -435,7 +443,13 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
   using CH = typename DsChunk<R>::type;
   constexpr int CPC = HERM ? 2 * DsChunk<R>::CPC : DsChunk<R>::CPC;  // vector elements per 16-byte chunk
   constexpr uint32_t COL = LN_GS * NCH;
-  constexpr uint32_t COLP = COL + 1;  // shared-memory row pitch: one chunk of padding staggers the rows over the banks
+  // Shared-memory row pitch of the tree table.  A 4-lane group reads 64 contiguous bytes (16 banks) of its
+  // node's row per chunk; the 8 groups of a warp read 8 different rows.  With an even chunk count the rows are
+  // unpadded (every row starts at bank 0, chunk i covers the bank half i & 1) and the groups walk the chunks in
+  // an order rotated by their parity (ROT below): at every step four groups hit each half -> 4 wavefronts per
+  // 512-byte warp access, the minimum, for ANY combination of rows.  (One chunk of padding, the previous
+  // layout, left ~1.5x the ideal wavefronts on this load, the largest shared-memory consumer of the kernel.)
+  constexpr uint32_t COLP = NCH >= 2 ? COL : COL + 1;
   extern __shared__ __align__(16) unsigned char ln_smem[];
   const ExecArgs& e = a.l.e;
   const DescentArgs& d = a.d;
@@ -456,6 +470,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
   const int tid = threadIdx.x, lane32 = tid & 31, warp = tid >> 5;
   const int lane = tid & (LN_GS - 1), grp = lane32 / LN_GS;                    // LN_GS-lane groups
   const unsigned gmask = ((1u << LN_GS) - 1u) << (LN_GS * grp);
+  const int ROT = NCH >= 2 ? (grp & 1) : 0;  // register slot i of v holds logical chunk i ^ ROT
   const uint32_t wbase = warp * 32;
   const CH* TREE = reinterpret_cast<const CH*>(d.tree);
   uint32_t loaded = 0xffffffffu;
@@ -472,7 +487,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
   uint32_t vim = 0;  // HERM: bit k set -> slot k takes the imaginary part
 #pragma unroll
   for (int k = 0; k < NCH * CPC; ++k) {
-    uint32_t c = CPC * ((k / CPC) * LN_GS + lane) + (k % CPC);
+    uint32_t c = CPC * (((k / CPC) ^ ROT) * LN_GS + lane) + (k % CPC);
     bool ok = fast_last && c < last.out_n;
     if constexpr (HERM) {
       if (ok) {
@@ -501,7 +516,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
           cmac(x[k], p, q);
         }
       } else {
-        const uint32_t c = CPC * ((k / CPC) * LN_GS + lane) + (k % CPC);
+        const uint32_t c = CPC * (((k / CPC) ^ ROT) * LN_GS + lane) + (k % CPC);
         if (c < last.out_n) x[k] = lane_element<R>(last, A, B, c);
       }
     }
@@ -523,20 +538,31 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
       }
     }
   };
+  // One partial sum per chunk (independent FMA chains), pairs of chunks added first: a + b is commutative, so
+  // the result does not depend on the group's chunk order (ROT) -- an item's draws are the same whichever
+  // group of whichever warp serves it.
   auto dot = [&](const CH (&v)[NCH], const CH* col) -> R {
-    R acc = R(0);
+    R part[NCH];
 #pragma unroll
     for (int i = 0; i < NCH; ++i) {
-      const CH m = col[i * LN_GS + lane];
+      const CH m = col[(i ^ ROT) * LN_GS + lane];
+      R acc;
       if constexpr (HERM) {
-        acc = fma(v[i].x, m.x, acc); acc = fma(v[i].y, m.y, acc);
+        acc = v[i].x * m.x; acc = fma(v[i].y, m.y, acc);
         if constexpr (CPC == 4) { acc = fma(v[i].z, m.z, acc); acc = fma(v[i].w, m.w, acc); }
       } else if constexpr (CPC == 2) {
-        acc = fma(v[i].x, m.x, acc); acc = fma(-v[i].y, m.y, acc);
+        acc = v[i].x * m.x; acc = fma(-v[i].y, m.y, acc);
         acc = fma(v[i].z, m.z, acc); acc = fma(-v[i].w, m.w, acc);
       } else {
-        acc = fma(v[i].x, m.x, acc); acc = fma(-v[i].y, m.y, acc);
+        acc = v[i].x * m.x; acc = fma(-v[i].y, m.y, acc);
       }
+      part[i] = acc;
+    }
+    R acc = part[0];
+    if constexpr (NCH >= 2) {
+      acc += part[1];
+#pragma unroll
+      for (int i = 2; i < NCH; i += 2) acc += part[i] + part[i + 1];
     }
 #pragma unroll
     for (int s = LN_GS / 2; s > 0; s >>= 1) acc += __shfl_xor_sync(gmask, acc, s, LN_GS);

@@ -1,0 +1,227 @@
+// Fused per-item steps + per-qubit descent, ONE LANE PER DRAW (complex64, Hermitian cut).
+//
+// lane_descent_kernel (lane.cuh) serves a draw with a 4-lane group: the item's projection vector v is
+// rebuilt per draw through the generic gather tables of the program's last step (32 shared-memory
+// loads per lane), every tree level costs 4 chunk loads, 16 FMAs and 2 shuffles per lane, and a warp has 8
+// draws in flight.  When the cut vector is x (x) conj(x) with x of DX complex entries (the ket and bra
+// halves of the cut are mirror images: every projection-form stage of cfg2), the probability of a tree
+// node is the Hermitian form  p = x^H H_node x  and needs, in packed real form (lane.cuh HERM),
+//     w = { |x_p|^2 ; Re(x_p conj x_q), Im(x_p conj x_q)  for p < q }      (DX^2 reals, this order)
+// Here one lane owns one (item, draw): it loads x (DX shared-memory loads), forms w in REGISTERS with
+// compile-time indices, and walks the tree with DX^2 / 4 16-byte row loads and DX^2 FMAs per level -- no
+// gather tables, no shuffles, 32 draws in flight per warp.  The tree columns are packed in the canonical
+// order above by herm_pack_kernel (Program::herm_canon gives position and sign of every packed slot).
+// Same Philox counters, guards, slot layout and dedup as lane_descent_kernel; replaces, like it,
+// rng.multinomial of reference engine.py:519 plus the marginal contraction of engine.py:417-450 for the
+// stage's per-item steps.
+#pragma once
+#include "lane.cuh"
+
+namespace ptsbe {
+
+template <int DX>
+__global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_x_kernel(const LaneDescentArgs a) {
+  using R = float;
+  using C = float2;
+  constexpr int D = DX * DX;                       // reals per packed column
+  constexpr int NQ = D / 4 > 0 ? D / 4 : 1;        // 16-byte chunks per column
+  constexpr uint32_t PITCH = NQ + 1;               // one chunk of padding staggers the rows over the banks
+  extern __shared__ __align__(16) unsigned char ln_smem[];
+  const ExecArgs& e = a.l.e;
+  const DescentArgs& d = a.d;
+  const LaneLayout L = lane_layout(e.n_steps, a.l.n_leaves, a.l.n_table_words, a.l.n_levels, e.arena_fast, e.words,
+                                   (uint32_t)sizeof(C));
+  const LaneCtx<R> cx = lane_setup<R>(a.l, ln_smem, L);
+  const uint32_t N = 1u << d.b;
+  double* mass_s = reinterpret_cast<double*>(ln_smem + L.end);                 // [LN_THREADS]
+  uint32_t* cum_s = reinterpret_cast<uint32_t*>(mass_s + LN_THREADS);          // [LN_THREADS]
+  uint32_t* slot0_s = cum_s + LN_THREADS;
+  uint32_t* eset_s = slot0_s + LN_THREADS;
+  uint32_t* bad_s = eset_s + LN_THREADS;
+  uint32_t* rank_s = bad_s + LN_THREADS;
+  uint32_t* gid_s = rank_s + LN_THREADS;
+  float4* table = reinterpret_cast<float4*>(gid_s + LN_THREADS);               // [N][PITCH]
+  __shared__ uint32_t s_end;
+  const int tid = threadIdx.x, lane32 = tid & 31, warp = tid >> 5;
+  const uint32_t wbase = warp * 32;
+  const float4* TREE = reinterpret_cast<const float4*>(d.tree);
+  uint32_t loaded = 0xffffffffu;
+  __syncthreads();  // program image complete
+  const LaneStep last = lane_decode(cx.steps, cx.tables, e.n_steps - 1);
+
+  // packed Hermitian vector of the item in warp slot i, in registers
+  auto load_w = [&](uint32_t i, float (&w)[D < 4 ? 4 : D]) {
+    const uint32_t slot = wbase + i;
+    LaneOp<C> A, B;
+    lane_operands<R>(cx, last, slot, eset_s[slot], A, B);
+    float xr[DX], xi[DX];
+#pragma unroll
+    for (int p = 0; p < DX; ++p) {
+      const C x = A.p[p * A.stride];
+      xr[p] = x.x;
+      xi[p] = x.y;
+    }
+#pragma unroll
+    for (int p = 0; p < DX; ++p) w[p] = fmaf(xr[p], xr[p], xi[p] * xi[p]);
+    int k = DX;
+#pragma unroll
+    for (int p = 0; p < DX; ++p)
+#pragma unroll
+      for (int q = p + 1; q < DX; ++q) {
+        w[k++] = fmaf(xr[p], xr[q], xi[p] * xi[q]);    // Re(x_p conj x_q)
+        w[k++] = fmaf(xi[p], xr[q], -xr[p] * xi[q]);   // Im(x_p conj x_q)
+      }
+#pragma unroll
+    for (int z = D; z < 4; ++z) w[z] = 0.f;
+  };
+  // four independent accumulators, added in a fixed order: the value does not depend on the lane
+  auto dot = [&](const float (&w)[D < 4 ? 4 : D], const float4* row) -> R {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const float4 m = row[q];
+      float s = acc[q & 3];
+      s = fmaf(w[4 * q], m.x, s);
+      s = fmaf(w[4 * q + 1], m.y, s);
+      s = fmaf(w[4 * q + 2], m.z, s);
+      s = fmaf(w[4 * q + 3], m.w, s);
+      acc[q & 3] = s;
+    }
+    return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  };
+
+  const uint32_t n_tiles = (d.n_items + a.tile - 1) / a.tile;
+  const uint32_t tiles_per = (n_tiles + gridDim.x - 1) / gridDim.x;
+  const uint32_t tile_end = min(n_tiles, (blockIdx.x + 1) * tiles_per);
+  __syncthreads();
+  for (uint32_t tile = blockIdx.x * tiles_per; tile < tile_end; ++tile) {
+    const uint32_t t1 = min(d.n_items, (tile + 1) * a.tile);
+    uint32_t pos = tile * a.tile;
+    while (pos < t1) {
+      // ---- the run of items [pos, end) that share error set er ----
+      const uint32_t er = d.eset[d.first_item + pos];
+      if (tid == 0) s_end = t1;
+      __syncthreads();
+      for (uint32_t i = pos + 1 + tid; i < t1; i += LN_THREADS)
+        if (d.eset[d.first_item + i] != er) { atomicMin(&s_end, i); break; }
+      if (er != loaded) {
+        const float4* src = TREE + (size_t)er * N * NQ;
+        for (uint32_t x = tid; x < N * NQ; x += LN_THREADS) table[(x / NQ) * PITCH + (x % NQ)] = __ldg(src + x);
+        loaded = er;
+      }
+      __syncthreads();
+      const uint32_t end = s_end;
+      const double floor_mass = d.vanish * d.set_mass[er];
+
+      for (uint32_t w0 = pos + wbase; w0 < end; w0 += LN_THREADS) {
+        // ---- phase A: this lane's item, every step but the last ----
+        const uint32_t it = w0 + lane32;
+        const bool live = it < end;
+        const uint32_t item = d.first_item + (live ? it : end - 1);
+        const uint32_t es_row = lane_item_context<R>(a.l, cx, ln_smem, L, item);
+        eset_s[tid] = es_row;
+        __syncwarp();
+        lane_run<R>(cx, 0, e.n_steps - 1, es_row, nullptr, false);
+        const uint32_t m = live ? d.mult[item] : 0u;
+        slot0_s[tid] = d.slot_off[item];
+        rank_s[tid] = d.rank[item];
+        gid_s[tid] = d.eset_id[item];
+        bad_s[tid] = 0;
+        // draws 1.. of the items that carry more than one shot: inclusive scan of (m - 1)
+        uint32_t incl = m > 1 ? m - 1 : 0u;
+#pragma unroll
+        for (int s = 1; s < 32; s <<= 1) {
+          const uint32_t o = __shfl_up_sync(0xffffffffu, incl, s);
+          if (lane32 >= s) incl += o;
+        }
+        cum_s[tid] = incl;
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        __syncwarp();
+        // ---- phase B: one (item, draw) per lane and round.  Round 0: the warp's items, mass (guards of
+        // reference engine.py:445-450, 475-476) and draw 0; later rounds: 32 of the remaining draws each ----
+        const uint32_t n_live = min(32u, end - w0);
+        const uint32_t rounds = 1 + (total + 31) / 32;
+        for (uint32_t rd = 0; rd < rounds; ++rd) {
+          const bool first = rd == 0;  // warp-uniform
+          bool active;
+          uint32_t i, t;
+          if (first) {
+            active = (uint32_t)lane32 < n_live;
+            i = active ? (uint32_t)lane32 : n_live - 1;
+            t = 0;
+          } else {
+            const uint32_t d0 = (rd - 1) * 32 + lane32;
+            active = d0 < total;
+            const uint32_t dr = active ? d0 : total - 1;
+            uint32_t lo = 0, hi = 31;  // smallest i with cum[i] > dr
+            while (lo < hi) {
+              const uint32_t mid = (lo + hi) >> 1;
+              if (cum_s[wbase + mid] > dr) hi = mid; else lo = mid + 1;
+            }
+            i = lo;
+            t = 1 + dr - (i ? cum_s[wbase + i - 1] : 0u);
+          }
+          float w[D < 4 ? 4 : D];
+          load_w(i, w);
+          uint32_t bad = 0;
+          R mass;
+          if (first) {
+            mass = dot(w, table);
+            if (!((double)mass >= floor_mass) || !(mass > R(0))) bad = PTSBE_EIMPOSSIBLE;
+          } else {
+            mass = (R)mass_s[wbase + i];
+            bad = bad_s[wbase + i] == PTSBE_EIMPOSSIBLE ? PTSBE_EIMPOSSIBLE : 0u;
+          }
+          uint32_t node = 0;
+          if (!bad) {
+            // inverse-CDF walk down the tree of conditional marginals: same uniform, same decisions as
+            // lane_descent_kernel
+            const R tol = (R)(d.neg_abs - d.neg_rel * (double)mass);
+            const Philox4 x = philox4x32_10(t, rank_s[wbase + i], d.stage, gid_s[wbase + i], d.k0, d.k1);
+            const uint64_t x64 = ((uint64_t)x.v[1] << 32) | x.v[0];
+            R p = mass;
+            R r = (R)((double)(x64 >> 11) * (1.0 / 9007199254740992.0)) * mass;  // u in [0, 1)
+            if (!(r < mass)) r = nextafterf(mass, 0.0f);                          // u rounded up to 1.0f
+            for (uint32_t lvl = 1; lvl <= d.b; ++lvl) {
+              R pl = dot(w, table + (size_t)((1u << (lvl - 1)) + node) * PITCH);
+              if (pl < tol || p - pl < tol) bad = PTSBE_ENUMERIC;
+              pl = fminf(fmaxf(pl, R(0)), p);
+              if (r < pl) { node = 2 * node; p = pl; }
+              else { node = 2 * node + 1; r -= pl; p -= pl; }
+            }
+          }
+          if (active) {
+            if (first) mass_s[wbase + i] = (double)mass;
+            if (bad) {
+              bad_s[wbase + i] = bad;
+            } else {
+              const uint32_t sl = slot0_s[wbase + i] + t;
+              d.slot_index[sl] = node;
+              d.slot_count[sl] = 1;
+            }
+          }
+          if (first) __syncwarp();  // masses and flags visible to the later rounds
+        }
+        __syncwarp();
+        // ---- per item: number of raw children, flags, hand-over of long draw lists ----
+        if (live) {
+          const uint32_t bad = bad_s[tid];
+          if (bad) {
+            d.nnz[item] = 0;
+            atomicMin(d.flag, ((unsigned long long)d.eset_id[item] << 16) |
+                                  ((unsigned long long)(d.stage & 0xff) << 8) | bad);
+            atomicAdd(d.flag_count, 1u);
+          } else {
+            d.nnz[item] = m;
+            if (m > LN_DEDUP_SERIAL) a.big_list[atomicAdd(a.big_count, 1u)] = item;
+          }
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      pos = end;
+    }
+  }
+}
+
+}  // namespace ptsbe
