@@ -231,9 +231,21 @@ def compile_stage(
     elem_bytes: int,
     ceiling: Optional[int] = None,
     mirror: Optional[Sequence[int]] = None,
+    fold_from: Optional[int] = None,
+    consumer_layout: bool = False,
 ) -> tuple[list[Program], tuple]:
     """Compile one stage network + stored path into `n_passes` programs.
     Returns (programs, result label order).
+
+    `fold_from` (optional, >= 1): classes fold_from .. n_passes - 2 are not hoisted; their nodes are
+    evaluated by the marginal pass together with the per-item class (the caller asks for this when
+    those classes have about as many distinct instances as there are work items, so a hoist pass
+    would save no arithmetic and cost a launch plus a record round trip through HBM).  The
+    programs of the folded passes are empty.
+
+    `consumer_layout`: store every record in the order its latest consumer reads it (see "record
+    layout" below).  Off by default: measured on cfg2, contiguous per-item
+    blocks at power-of-two strides are what a lane-per-item kernel reads worst.
 
     `mirror[k]` (optional) names the operand whose value is the complex
     conjugate of operand k under a relabelling (the bra copy of a ket operand,
@@ -253,6 +265,8 @@ def compile_stage(
         )
     for nd in nodes:
         nd.pass_ = min(nd.cls, top)
+        if fold_from is not None and fold_from >= 1 and nd.pass_ >= fold_from:
+            nd.pass_ = top
     if root >= n_leaves:
         rootn.pass_ = top  # the finished record is always produced by the marginal pass
 
@@ -360,6 +374,38 @@ def compile_stage(
     if proj is not None:
         rec_off[proj[0]] = 0  # v is the output record of the marginal pass
         rec_size[top] = nodes[proj[0]].size
+
+    # record layout ------------------------------------------------------------
+    # A record is read by tens of millions of per-item steps and written once per instance of its
+    # own class, so it is stored in the order its consumer of the latest pass reads it: labels that
+    # the consumer slices away with prefix bits first, then the contracted labels, then the
+    # surviving ones in the consumer's output order.  The operand of one work item (e.g. the 8 x 8
+    # transfer matrix selected by the bits of the previous stage) is then ONE contiguous block with
+    # the output index fastest, instead of a gather over the whole record.  Only the label order
+    # of the stored tensor changes; every table below is derived from label -> stride maps.
+    for R in (list(rec_off) if consumer_layout else ()):
+        if R == root or (proj is not None and R in proj):
+            continue
+        later = [c for c in consumers.get(R, ()) if nodes[c].pass_ > nodes[R].pass_]
+        if not later:
+            continue
+        nd = nodes[max(later, key=lambda c: (nodes[c].pass_, c))]
+        for ch, other in ((nd.a, nd.b), (nd.b, nd.a)):
+            x = ch
+            while x in view and x not in virt:
+                x = view[x][0]
+            if x != R or x in virt:
+                continue
+            op_labels = nodes[ch].labels
+            others = set(nodes[other].labels)
+            shared = [lb for lb in op_labels if lb in others]
+            surv = [lb for lb in nd.labels if lb in op_labels and lb not in others]
+            surv += [lb for lb in op_labels if lb not in others and lb not in surv]
+            sliced = [lb for lb in nodes[R].labels if lb not in op_labels]
+            order = sliced + shared + surv
+            if sorted(map(str, order)) == sorted(map(str, nodes[R].labels)) and len(set(order)) == len(order):
+                _relabel(nodes, virt, view, R, tuple(order))
+            break
 
     programs: list[Program] = []
     result_kind, result_ref = 0, 0
@@ -594,6 +640,25 @@ def compile_stage(
             )
         )
     return programs, tuple(open_order)
+
+
+def _relabel(nodes, virt, view, nid, new_labels):
+    """Store node `nid` with its labels in the order `new_labels`.  Nodes whose label order is tied
+    to it position by position follow: slice views of it (child order minus the sliced label) and
+    conjugate twins (mirror labels in the same positions)."""
+    old = nodes[nid].labels
+    if tuple(new_labels) == tuple(old):
+        return
+    perm = [old.index(lb) for lb in new_labels]
+    dims = nodes[nid].dims
+    nodes[nid].labels = tuple(new_labels)
+    nodes[nid].dims = tuple(dims[k] for k in perm)
+    for v, twin in virt.items():
+        if twin == nid:
+            _relabel(nodes, virt, view, v, tuple(nodes[v].labels[k] for k in perm))
+    for w, (child, lb, _) in view.items():
+        if child == nid:
+            _relabel(nodes, virt, view, w, tuple(x for x in new_labels if x != lb))
 
 
 def _place(nodes, mine, rec_off, real_of, fast_cap):

@@ -41,6 +41,9 @@ struct Program {
   // lane_fused: additionally its last step alone produces the projection vector
   bool lane_ok = false, lane_fused = false;
   int lane_blocks_per_sm = 0;
+  // class-0 hoist program that can run one thread per error set with a global-memory arena (lane.cuh BIG)
+  bool lane_big_ok = false;
+  int lane_big_blocks_per_sm = 0;
   bool tiled = false;  // most multiply-adds sit in large separable steps: register-tiled kernel variant
   // projection vector is x (x) conj(x): Hermitian-packed tree columns (lane.cuh HERM)
   bool herm = false;
@@ -51,6 +54,8 @@ struct Program {
   uint32_t herm_dx = 0;
   std::vector<uint32_t> herm_canon_host;
   DevBuf herm_canon;
+  // ... and every step before the outer product is a vector-matrix product over a record (lane_x.cuh CHAIN)
+  bool lane_chain = false;
 };
 
 }  // namespace ptsbe
@@ -73,6 +78,10 @@ struct ptsbe_plan {
   uint32_t lane = 1;                   // lane-per-item interpreter / fused descent (lane.cuh)
   uint32_t tc_project = 1;             // complex64 projection on tcgen05 tensor cores (project_tc.cuh)
   uint32_t lane_x = 1;                 // lane-per-draw fused descent for Hermitian cuts (lane_x.cuh)
+  uint32_t lane_chain = 0;             // ... with the vector-matrix chain served by lane groups (lane_x.cuh CHAIN);
+                                       // pays only with PTSBE_RECORD_LAYOUT=1
+  uint32_t lane_big_min = 16384;       // class-0 hoists over at least this many error sets run one thread per
+                                       // error set with a global-memory arena (lane.cuh BIG)
   uint32_t descent = 1;                // per-qubit descent sampler for low-multiplicity stages
   double descent_mult = 4.0;           // ... used when shots / unique prefixes of the stage <= this
   // per stage: 1 descent, 0 flat, -1 decide per chunk (ptsbe_plan_set_stage_samplers)
@@ -339,6 +348,17 @@ static void launch_exec_any(ptsbe_plan* pl, Program& pr, uint32_t mode, const Le
 static void classify_lane(const ptsbe_plan* pl, Program& pr) {
   const ptsbe_program_desc& d = pr.d;
   pr.lane_ok = pr.lane_fused = false;
+  pr.lane_big_ok = false;
+  if (d.n_steps && d.steps && d.level == 1 && d.threads_per_item <= 32 && !d.arena_spill_elems && !d.memo_elems &&
+      !d.proj_d && d.arena_fast_elems > 48 && pl->f + 2 <= (uint32_t)LN_MAX_LEVELS) {
+    const LaneLayout Lb = lane_layout(d.n_steps, d.n_leaves, 0, pl->f + 2, 0, pl->words, (uint32_t)pl->elem);
+    uint64_t serial = 0;
+    for (uint32_t s = 0; s < d.n_steps; ++s) {
+      const uint32_t* st = d.steps + (size_t)s * STEP_WORDS;
+      serial += (uint64_t)st[6] * std::max<uint32_t>(st[7], 1);
+    }
+    pr.lane_big_ok = Lb.end <= 100 * 1024 && serial <= (1u << 18);
+  }
   if (!d.n_steps || !d.steps || d.threads_per_item > 32 || d.arena_spill_elems || d.arena_fast_elems > 48 ||
       d.memo_elems || d.level + 1 > (uint32_t)LN_MAX_LEVELS || pl->f + 2 > (uint32_t)LN_MAX_LEVELS)
     return;
@@ -424,6 +444,35 @@ static void classify_lane(const ptsbe_plan* pl, Program& pr) {
       }
     }
   }
+  // chain form (lane_x.cuh CHAIN): steps 0 .. n-2 are x_s = x_{s-1} . T_s with T_s a block of a record
+  // (an earlier pass of this stage) sliced by prefix bits, x_0 a record of an earlier pass
+  pr.lane_chain = false;
+  if (pr.herm_dx && d.n_steps >= 2 && d.n_steps - 1 <= (uint32_t)LN_CHAIN_MAX && d.tables) {
+    const uint32_t dx = pr.herm_dx;
+    bool ok = last[0] == 0;
+    uint32_t prev_out = 0;
+    for (uint32_t s = 0; ok && s + 1 < d.n_steps; ++s) {
+      const uint32_t* st = d.steps + (size_t)s * STEP_WORDS;
+      const uint32_t fl = st[11], kn = st[7], lo_n = st[8], hi_n = st[9];
+      const bool vec_a = (fl & 32u) != 0, vec_b = (fl & 64u) != 0;
+      if (vec_a == vec_b || (fl & 4u) || st[4] != 0 || st[6] != dx || lo_n != dx || hi_n != 1 || kn < 1 || kn > 8) { ok = false; break; }
+      const uint32_t* t = d.tables + st[10];
+      const uint32_t *kA = t + 2 * lo_n + 2 * hi_n, *kB = kA + kn, *dyn = kB + kn;
+      const uint32_t vk = vec_a ? st[0] : st[2], vr = vec_a ? st[1] : st[3], mk = vec_a ? st[2] : st[0];
+      const uint32_t* kV = vec_a ? kA : kB;
+      for (uint32_t k = 0; k < kn; ++k) if (kV[k] != k) ok = false;
+      if (fl & 8u) {  // no prefix-bit slicing on the vector side
+        const uint32_t na = dyn[0], nb = dyn[1 + 2 * na];
+        if ((vec_a ? na : nb) != 0) ok = false;
+      }
+      if (mk < 2 || mk - 1 > d.level) ok = false;   // the matrix comes from a record
+      if (s == 0) { if (vk < 2 || vk - 1 > d.level) ok = false; }
+      else if (vk != 0 || vr != prev_out || kn != dx) ok = false;
+      prev_out = st[5];
+    }
+    if (ok && last[1] != prev_out) ok = false;  // the outer product is taken of the chain's result
+    pr.lane_chain = ok;
+  }
 }
 
 template <typename R>
@@ -477,9 +526,34 @@ static void launch_lane(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelD
   CK(cudaGetLastError());
 }
 
+// class-0 hoist over a large batch of error sets: one thread per error set, arena in global memory
+template <typename R>
+static void launch_lane_big(ptsbe_plan* pl, Program& pr, const LevelDev* levels_dev, const uint8_t* kraus_dev,
+                            uint32_t n_items, void* out) {
+  using C = typename CxT<R>::type;
+  if (n_items == 0) return;
+  LaneArgs a = lane_args<R>(pl, pr, EXEC_HOIST, levels_dev, kraus_dev, 0, n_items, out, 0);
+  const LaneLayout L = lane_layout(a.e.n_steps, a.n_leaves, 0, a.n_levels, 0, a.e.words, (uint32_t)sizeof(C));
+  opt_in_smem((const void*)exec_lane_kernel<R, true>, 200 * 1024);
+  if (pr.lane_big_blocks_per_sm == 0)
+    pr.lane_big_blocks_per_sm = cached_occupancy((const void*)exec_lane_kernel<R, true>, LN_THREADS, L.end);
+  const uint64_t need = cdiv(n_items, LN_THREADS);
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)pl->sm_count * pr.lane_big_blocks_per_sm));
+  DevBuf arena((size_t)grid * LN_WARPS * pr.d.arena_fast_elems * 32 * sizeof(C), pl->stream);
+  a.e.spill = arena.p;
+  exec_lane_kernel<R, true><<<grid, LN_THREADS, L.end, pl->stream>>>(a);
+  g_launches++;
+  CK(cudaGetLastError());
+}
+
 // hoist pass of a per-prefix program: lane-per-item when the program qualifies
 static void launch_hoist(ptsbe_plan* pl, Program& pr, const LevelDev* lv, const uint8_t* kraus,
                          uint32_t n, void* out) {
+  if (pr.lane_big_ok && pl->lane && n >= pl->lane_big_min) {
+    if (pl->dtype == PTSBE_C64) launch_lane_big<float>(pl, pr, lv, kraus, n, out);
+    else launch_lane_big<double>(pl, pr, lv, kraus, n, out);
+    return;
+  }
   if (pr.lane_ok && pl->lane) {
     if (pl->dtype == PTSBE_C64) launch_lane<float>(pl, pr, EXEC_HOIST, lv, kraus, 0, n, out, 0);
     else launch_lane<double>(pl, pr, EXEC_HOIST, lv, kraus, 0, n, out, 0);
@@ -554,22 +628,25 @@ static void launch_lane_descent_t(ptsbe_plan* pl, Program& pr, LaneDescentArgs& 
   CK(cudaGetLastError());
 }
 
-template <int DX>
+template <int DX, bool CHAIN>
 static void launch_lane_descent_x(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a) {
+  // CHAIN keeps the intermediate vectors in registers: the arena holds only x (DX entries per item)
+  if (CHAIN) a.l.e.arena_fast = DX;
   const LaneLayout L = lane_layout(a.l.e.n_steps, a.l.n_leaves, a.l.n_table_words, a.l.n_levels,
                                    a.l.e.arena_fast, a.l.e.words, (uint32_t)sizeof(float2));
   constexpr size_t NQ = DX * DX / 4 > 0 ? DX * DX / 4 : 1;
-  const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4) + (((NQ + 1) * 16) << a.d.b);
+  const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4 + (CHAIN ? LN_CHAIN_MAX * 4 : 0)) +
+                      (((NQ + 1) * 16) << a.d.b);
   if (smem > 200 * 1024) throw Failure(PTSBE_ERESOURCE, "fused descent needs more shared memory than one SM has");
-  opt_in_smem((const void*)lane_descent_x_kernel<DX>, 200 * 1024);
-  const int per_sm = cached_occupancy((const void*)lane_descent_x_kernel<DX>, LN_THREADS, smem);
+  opt_in_smem((const void*)lane_descent_x_kernel<DX, CHAIN>, 200 * 1024);
+  const int per_sm = cached_occupancy((const void*)lane_descent_x_kernel<DX, CHAIN>, LN_THREADS, smem);
   const uint64_t ctas = (uint64_t)pl->sm_count * per_sm;
   uint64_t tile = a.d.n_items / (ctas * 4) / LN_THREADS * LN_THREADS;
   tile = std::min<uint64_t>(2048, std::max<uint64_t>(LN_THREADS, tile));
   a.tile = (uint32_t)tile;
   const uint64_t tiles = cdiv(a.d.n_items, tile);
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, ctas));
-  lane_descent_x_kernel<DX><<<grid, LN_THREADS, smem, pl->stream>>>(a);
+  lane_descent_x_kernel<DX, CHAIN><<<grid, LN_THREADS, smem, pl->stream>>>(a);
   g_launches++;
   CK(cudaGetLastError());
 }
@@ -589,9 +666,10 @@ static void launch_lane_descent(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a,
   const bool f32 = pl->dtype == PTSBE_C64;
   if (a.herm_map && f32 && pr.herm_dx && pl->lane_x) {
     // x (x) conj(x) with a small x: one lane per draw over canonically packed columns (lane_x.cuh)
+    const bool chain = pr.lane_chain && pl->lane_chain;
     switch (pr.herm_dx) {
-      case 4: launch_lane_descent_x<4>(pl, pr, a); return;
-      case 8: launch_lane_descent_x<8>(pl, pr, a); return;
+      case 4: chain ? launch_lane_descent_x<4, true>(pl, pr, a) : launch_lane_descent_x<4, false>(pl, pr, a); return;
+      case 8: chain ? launch_lane_descent_x<8, true>(pl, pr, a) : launch_lane_descent_x<8, false>(pl, pr, a); return;
       default: break;
     }
   }
@@ -1575,6 +1653,8 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     pl->descent = (uint32_t)env_size("PTSBE_DESCENT", pl->descent);
     pl->tc_project = (uint32_t)env_size("PTSBE_TC_PROJECT", pl->tc_project);
     pl->lane_x = (uint32_t)env_size("PTSBE_LANE_X", pl->lane_x);
+    pl->lane_chain = (uint32_t)env_size("PTSBE_LANE_CHAIN", pl->lane_chain);
+    pl->lane_big_min = (uint32_t)env_size("PTSBE_LANE_BIG_MIN", pl->lane_big_min);
     pl->lane = (uint32_t)env_size("PTSBE_LANE", pl->lane);
     if (const char* dm = getenv("PTSBE_DESCENT_MULT")) if (*dm) pl->descent_mult = atof(dm);
     pl->chunk_shots = env_size("PTSBE_CHUNK_SHOTS", pl->chunk_shots);

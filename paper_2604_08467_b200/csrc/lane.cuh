@@ -89,6 +89,7 @@ struct LaneCtx {
   const C* pool;
   const uint8_t* kraus;
   uint32_t g, arena_fast;
+  uint32_t ast;             // arena row pitch: LN_AST (shared memory) or 32 (global arena, BIG)
 
   __device__ __forceinline__ uint32_t bit(uint32_t q, uint32_t slot) const {
     return (uint32_t)((pfx[(q >> 6) * LN_THREADS + slot] >> (63 - (q & 63))) & 1ull);
@@ -97,8 +98,8 @@ struct LaneCtx {
   __device__ __forceinline__ LaneOp<C> resolve(uint32_t kind, uint32_t ref, uint32_t slot, uint32_t eset) const {
     LaneOp<C> o;
     if (kind == 0) {
-      o.p = arena_w + ref * LN_AST + (slot & 31);
-      o.stride = LN_AST;
+      o.p = arena_w + ref * ast + (slot & 31);
+      o.stride = ast;
       return o;
     }
     o.stride = 1;
@@ -277,10 +278,12 @@ struct LaneArgs {
 
 // Loads the program image and the level table into shared memory (all threads), returns the context.
 template <typename R>
-__device__ __forceinline__ LaneCtx<R> lane_setup(const LaneArgs& a, unsigned char* smem, const LaneLayout& L) {
+__device__ __forceinline__ LaneCtx<R> lane_setup(const LaneArgs& a, unsigned char* smem, const LaneLayout& L,
+                                                 bool big = false) {
   using C = typename CxT<R>::type;
   uint32_t* img = reinterpret_cast<uint32_t*>(smem);
-  const uint32_t ns = a.e.n_steps * STEP_WORDS, nl = a.n_leaves * LEAF_WORDS, nt = a.n_table_words;
+  // big: the gather tables stay in global memory (warp-uniform reads, L1-resident) and the arena is global
+  const uint32_t ns = a.e.n_steps * STEP_WORDS, nl = a.n_leaves * LEAF_WORDS, nt = big ? 0u : a.n_table_words;
   for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) img[L.steps_off / 4 + i] = __ldg(a.e.steps + i);
   for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) img[L.leaves_off / 4 + i] = __ldg(a.e.leaves + i);
   for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) img[L.tables_off / 4 + i] = __ldg(a.e.tables + i);
@@ -290,10 +293,13 @@ __device__ __forceinline__ LaneCtx<R> lane_setup(const LaneArgs& a, unsigned cha
   LaneCtx<R> cx;
   cx.steps = img + L.steps_off / 4;
   cx.leaves = img + L.leaves_off / 4;
-  cx.tables = img + L.tables_off / 4;
+  cx.tables = big ? a.e.tables : img + L.tables_off / 4;
   cx.levels = reinterpret_cast<const LevelDev*>(smem + L.levels_off);
-  cx.arena_w = reinterpret_cast<C*>(smem + L.arena_off) +
-               (size_t)(threadIdx.x >> 5) * (a.e.arena_fast ? a.e.arena_fast : 1) * LN_AST;
+  cx.ast = big ? 32u : (uint32_t)LN_AST;
+  cx.arena_w = big ? reinterpret_cast<C*>(a.e.spill) +
+                         ((size_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5)) * a.e.arena_fast * 32
+                   : reinterpret_cast<C*>(smem + L.arena_off) +
+                         (size_t)(threadIdx.x >> 5) * (a.e.arena_fast ? a.e.arena_fast : 1) * LN_AST;
   cx.anc = reinterpret_cast<const uint32_t*>(smem + L.anc_off);
   cx.pfx = reinterpret_cast<const uint64_t*>(smem + L.pfx_off);
   cx.pool = reinterpret_cast<const C*>(a.e.pool);
@@ -334,8 +340,8 @@ __device__ __forceinline__ void lane_run(const LaneCtx<R>& cx, uint32_t s0, uint
     LaneOp<C> A, B;
     lane_operands<R>(cx, t, slot, eset, A, B);
     const bool to_arena = t.s1.x == 0;
-    C* O = to_arena ? cx.arena_w + t.s1.y * LN_AST + ls : rec + t.s1.y;
-    const uint32_t o_stride = to_arena ? LN_AST : 1u;
+    C* O = to_arena ? cx.arena_w + t.s1.y * cx.ast + ls : rec + t.s1.y;
+    const uint32_t o_stride = to_arena ? cx.ast : 1u;
     const bool store = to_arena || live;
     if (t.flags & 4u) {
       for (uint32_t c = 0; c < t.out_n; ++c) {
@@ -362,13 +368,18 @@ __device__ __forceinline__ void lane_run(const LaneCtx<R>& cx, uint32_t s0, uint
 // ---------------------------------------------------------------------------
 // standalone: hoist passes p >= 1 and vector rows, one thread per work item
 // ---------------------------------------------------------------------------
-template <typename R>
+// BIG: class-0 programs of hundreds of steps over arenas of kilobytes (cfg5: 320-560 steps, 650-1600
+// elements) when the batch holds tens of thousands of error sets.  A group of lanes per item spends ~100
+// issued instructions per step on decoding for a handful of multiply-adds; with one thread per error set the
+// decode is shared by 32 items and the arena moves to global memory, interleaved [element][lane] so that every
+// access of a warp is one or two full cache lines (a.e.spill: [resident warps][arena_fast][32]).
+template <typename R, bool BIG = false>
 __global__ void __launch_bounds__(LN_THREADS) exec_lane_kernel(const LaneArgs a) {
   using C = typename CxT<R>::type;
   extern __shared__ __align__(16) unsigned char ln_smem[];
-  const LaneLayout L = lane_layout(a.e.n_steps, a.n_leaves, a.n_table_words, a.n_levels, a.e.arena_fast,
-                                   a.e.words, (uint32_t)sizeof(C));
-  const LaneCtx<R> cx = lane_setup<R>(a, ln_smem, L);
+  const LaneLayout L = lane_layout(a.e.n_steps, a.n_leaves, BIG ? 0u : a.n_table_words, a.n_levels,
+                                   BIG ? 0u : a.e.arena_fast, a.e.words, (uint32_t)sizeof(C));
+  const LaneCtx<R> cx = lane_setup<R>(a, ln_smem, L, BIG);
   __syncthreads();
   const uint32_t per_round = gridDim.x * LN_THREADS;
   const uint32_t rounds = (a.e.n_items + per_round - 1) / per_round;

@@ -14,12 +14,23 @@
 // Same Philox counters, guards, slot layout and dedup as lane_descent_kernel; replaces, like it,
 // rng.multinomial of reference engine.py:519 plus the marginal contraction of engine.py:417-450 for the
 // stage's per-item steps.
+//
+// CHAIN: the per-item steps before the outer product are a chain of vector-matrix products
+//     x_1 = r . T_1[bits],  x_2 = x_1 . T_2[bits],  ...      (r: record of an earlier pass, T_s: transfer
+// matrices sliced out of the error set's class-0 record by prefix bits -- the matrix-product-state form the
+// cut planner produces).  A lane that owns an item would read its own DX x DX matrix: 32 lanes, 32 different
+// matrices, every load instruction touching 32 cache lines.  Here a group of DX lanes serves one item, lane c
+// computes component c of the product from rows that the group reads as contiguous blocks (the compiler stores
+// records in consumer order: [slicing bits][contracted][surviving]), the intermediate vectors stay in registers
+// and only x is handed to the draw phase through shared memory.  Same multiply-add order as lane_run.
 #pragma once
 #include "lane.cuh"
 
 namespace ptsbe {
 
-template <int DX>
+constexpr int LN_CHAIN_MAX = 4;  // vector-matrix steps a CHAIN kernel accepts
+
+template <int DX, bool CHAIN>
 __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_x_kernel(const LaneDescentArgs a) {
   using R = float;
   using C = float2;
@@ -40,7 +51,8 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_x_kernel(const Lan
   uint32_t* bad_s = eset_s + LN_THREADS;
   uint32_t* rank_s = bad_s + LN_THREADS;
   uint32_t* gid_s = rank_s + LN_THREADS;
-  float4* table = reinterpret_cast<float4*>(gid_s + LN_THREADS);               // [N][PITCH]
+  uint32_t* dyn_s = gid_s + LN_THREADS;                                        // CHAIN: [LN_CHAIN_MAX][LN_THREADS]
+  float4* table = reinterpret_cast<float4*>(dyn_s + (CHAIN ? LN_CHAIN_MAX * LN_THREADS : 0));  // [N][PITCH]
   __shared__ uint32_t s_end;
   const int tid = threadIdx.x, lane32 = tid & 31, warp = tid >> 5;
   const uint32_t wbase = warp * 32;
@@ -53,7 +65,12 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_x_kernel(const Lan
   auto load_w = [&](uint32_t i, float (&w)[D < 4 ? 4 : D]) {
     const uint32_t slot = wbase + i;
     LaneOp<C> A, B;
-    lane_operands<R>(cx, last, slot, eset_s[slot], A, B);
+    if constexpr (CHAIN) {
+      A.p = cx.arena_w + i;  // x of the item in warp slot i: element p at [p * LN_AST + i]
+      A.stride = LN_AST;
+    } else {
+      lane_operands<R>(cx, last, slot, eset_s[slot], A, B);
+    }
     float xr[DX], xi[DX];
 #pragma unroll
     for (int p = 0; p < DX; ++p) {
@@ -120,8 +137,86 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_x_kernel(const Lan
         const uint32_t item = d.first_item + (live ? it : end - 1);
         const uint32_t es_row = lane_item_context<R>(a.l, cx, ln_smem, L, item);
         eset_s[tid] = es_row;
-        __syncwarp();
-        lane_run<R>(cx, 0, e.n_steps - 1, es_row, nullptr, false);
+        if constexpr (CHAIN) {
+          // per item: offset of its transfer matrix inside the record, step by step (prefix-bit slicing)
+          for (uint32_t s = 0; s + 1 < e.n_steps; ++s) {
+            const LaneStep t = lane_decode(cx.steps, cx.tables, s);
+            uint32_t add_a = 0, add_b = 0;
+            if (t.flags & 8u) {
+              const uint32_t* dt = t.dyn;
+              const uint32_t na = dt[0];
+              for (uint32_t z = 0; z < na; ++z)
+                if (cx.bit(dt[1 + 2 * z], tid)) add_a += dt[2 + 2 * z];
+              dt += 1 + 2 * na;
+              const uint32_t nb = dt[0];
+              for (uint32_t z = 0; z < nb; ++z)
+                if (cx.bit(dt[1 + 2 * z], tid)) add_b += dt[2 + 2 * z];
+            }
+            dyn_s[s * LN_THREADS + tid] = (t.flags & 32u) ? add_b : add_a;
+          }
+          __syncwarp();
+          // DX lanes per item, 32 / DX items per round: lane c owns component c
+          constexpr int G = 32 / DX;
+          const uint32_t grp = lane32 / DX, c = lane32 % DX;
+          for (uint32_t sub = 0; sub < (uint32_t)DX; ++sub) {
+            const uint32_t i = sub * G + grp, slot = wbase + i;
+            C vec[8], acc;
+            acc.x = acc.y = 0.f;
+            for (uint32_t s = 0; s + 1 < e.n_steps; ++s) {
+              const LaneStep t = lane_decode(cx.steps, cx.tables, s);
+              const bool vec_a = (t.flags & 32u) != 0;  // which operand is the vector
+              const uint32_t mk = vec_a ? t.s0.z : t.s0.x, mr = vec_a ? t.s0.w : t.s0.y;
+              const uint32_t* lo_m = vec_a ? t.loB : t.loA;
+              const uint32_t* k_m = vec_a ? t.kB : t.kA;
+              const bool cj_v = vec_a ? (t.flags & 1u) : (t.flags & 2u);
+              const bool cj_m = vec_a ? (t.flags & 2u) : (t.flags & 1u);
+              if (s == 0) {
+                const uint32_t vk = vec_a ? t.s0.x : t.s0.z, vr = vec_a ? t.s0.y : t.s0.w;
+                const LevelDev& lv = cx.levels[vk - 1];
+                const C* vp = reinterpret_cast<const C*>(lv.ext) + (size_t)cx.anc[(vk - 1) * LN_THREADS + slot] * lv.ext_rec + vr;
+                if (!((vr | lv.ext_rec) & 1u)) {
+                  const float4* vp4 = reinterpret_cast<const float4*>(vp);
+#pragma unroll
+                  for (int k = 0; k < 4; ++k)
+                    if (2 * k < (int)t.kn) {
+                      const float4 q = __ldg(vp4 + k);
+                      vec[2 * k].x = q.x; vec[2 * k].y = q.y; vec[2 * k + 1].x = q.z; vec[2 * k + 1].y = q.w;
+                    }
+                } else {
+#pragma unroll
+                  for (int k = 0; k < 8; ++k)
+                    if (k < (int)t.kn) vec[k] = __ldg(vp + k);
+                }
+              } else {
+                // the previous product, gathered from the group's lanes
+#pragma unroll
+                for (int k = 0; k < DX; ++k) {
+                  vec[k].x = __shfl_sync(0xffffffffu, acc.x, grp * DX + k);
+                  vec[k].y = __shfl_sync(0xffffffffu, acc.y, grp * DX + k);
+                }
+              }
+              const LevelDev& lm = cx.levels[mk - 1];
+              const C* mp = reinterpret_cast<const C*>(lm.ext) + (size_t)cx.anc[(mk - 1) * LN_THREADS + slot] * lm.ext_rec +
+                            mr + dyn_s[s * LN_THREADS + slot] + lo_m[c];
+              acc.x = acc.y = 0.f;
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (k < (int)t.kn) {
+                  C m = __ldg(mp + k_m[k]);
+                  C v = vec[k];
+                  if (cj_m) m.y = -m.y;
+                  if (cj_v) v.y = -v.y;
+                  if (vec_a) cmac_s<false, false>(acc, v, m);
+                  else cmac_s<false, false>(acc, m, v);
+                }
+            }
+            cx.arena_w[c * LN_AST + i] = acc;
+          }
+          __syncwarp();
+        } else {
+          __syncwarp();
+          lane_run<R>(cx, 0, e.n_steps - 1, es_row, nullptr, false);
+        }
         const uint32_t m = live ? d.mult[item] : 0u;
         slot0_s[tid] = d.slot_off[item];
         rank_s[tid] = d.rank[item];

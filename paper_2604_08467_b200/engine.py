@@ -23,6 +23,7 @@ compatibility and raise NotImplementedError when called.
 from __future__ import annotations
 
 import json
+import os
 import math
 import time
 from dataclasses import dataclass, field
@@ -592,6 +593,25 @@ def _size_cap_log2(dtype: str) -> float:
     return 13.0 if dtype == "complex64" else 12.0
 
 
+def _fold_from(weights: Sequence[float]) -> Optional[int]:
+    """First prefix-dependent class that is NOT worth a hoist pass of its own: a class with at
+    least half as many distinct instances as the stage has work items (late stages of a spread-out
+    distribution, where nearly every shot is its own prefix) saves no arithmetic by being hoisted
+    and costs a launch plus a record round trip; compiler.compile_stage evaluates it with the
+    per-item class instead.  PTSBE_FOLD: 0 (default) = never, 1 = only the class just below the
+    per-item one, 2 = every qualifying class.  Off by default: with the kernels of this round the
+    folded programs run slower than hoist pass + fused kernel (DESIGN.md section 7 has the A/B).  Decided from the plan-level weights only, so every
+    rank and every chunk of a run compiles the same programs."""
+    mode = int(os.environ.get("PTSBE_FOLD", "0"))
+    top = len(weights) - 1
+    if mode <= 0 or top < 2:
+        return None
+    c = top
+    while c - 1 >= 1 and weights[c - 1] >= 0.5 * weights[top] and (mode >= 2 or c == top):
+        c -= 1
+    return c if c < top else None
+
+
 class DevicePipeline:
     """Plans (once), compiles and owns the device plan of one
     (circuit structure, batch plan, variant tables) triple."""
@@ -635,7 +655,9 @@ class DevicePipeline:
                 ctx.stats.path_seconds += time.perf_counter() - t0
             self.paths[j] = path
             progs, _ = compiler.compile_stage(ops, path.steps, opens, j, pool, elem,
-                                              ceiling=ctx.max_intermediate, mirror=mirror)
+                                              ceiling=ctx.max_intermediate, mirror=mirror,
+                                              fold_from=_fold_from(weights),
+                                              consumer_layout=os.environ.get("PTSBE_RECORD_LAYOUT", "0") == "1")
             self.stage_flops[j] = [p.flops for p in progs]
             programs += progs
         self.compiled = CompiledPlan(

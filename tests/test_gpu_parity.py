@@ -16,7 +16,7 @@ from paper_2604_08467_b200 import _capi, workloads
 from paper_2604_08467_b200.engine import (
     BatchPlan, CircuitNetwork, ErrorSet, RunConfig, SamplerContext, conditional_marginal,
     conditional_marginals_batched, merge_records, run_ptsbe, sample_proportional,
-    sample_proportional_batched, ShotRecord, presample_errors,
+    sample_proportional_batched, ShotRecord, presample_errors, DevicePipeline, VariantTables,
 )
 from paper_2604_08467_b200.errors import ImpossiblePrefixError
 from paper_2604_08467_b200.planner import PathCache
@@ -404,6 +404,38 @@ def test_lane_per_item_kernels_agree_with_group_kernels(monkeypatch, dtype):
             da, db = {r.bitstring: r.count for r in a}, {r.bitstring: r.count for r in b}
             tvd = 0.5 * sum(abs(da.get(s, 0) - db.get(s, 0)) for s in set(da) | set(db)) / k.m
             assert tvd <= 0.02
+
+
+@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+def test_thread_per_error_set_hoist_equals_group_executor(monkeypatch, dtype):
+    """Class-0 hoist passes over large batches run one thread per error set with the
+    arena in global memory (csrc/lane.cuh BIG) instead of a lane group per error set
+    (csrc/executor.cuh).  Same multiply-add order, so the records are identical in
+    both dtypes; complex128 also equals the oracle (reference engine.py:361-450)."""
+    c, sizes = workloads.random40(14, 70, seed=3)
+    sizes = (5, 5, 4)
+    tpl = CircuitNetwork.from_circuit(c)
+    es = presample_errors(c, 40, "uniform", shots_per_set=50, rng=np.random.default_rng(8))
+
+    def run(big):
+        monkeypatch.setenv("PTSBE_LANE_BIG_MIN", "1" if big else "4000000000")
+        ctx = SamplerContext(hypersamples=8, dtype=dtype)
+        tables = VariantTables.from_channels(tpl)
+        pipe = DevicePipeline(tpl, BatchPlan(sizes), tables, ctx, shots_per_set=50.0)
+        qualifying = [p for p in pipe.compiled.programs if p.level == 1 and p.threads <= 32 and p.arena_fast > 48
+                      and not p.memo_elems and not p.proj_d and len(p.steps)]
+        pipe.close()
+        out = sample_proportional_batched(tpl, es, BatchPlan(sizes), 5, ctx)
+        return [[(r.bitstring, r.count) for r in recs] for recs in out], len(qualifying)
+
+    big, n_q = run(True)
+    group, _ = run(False)
+    assert n_q >= 1, "no class-0 program of this case qualifies for the thread-per-error-set kernel"
+    assert big == group
+    if dtype == "complex128":
+        ops, finals = bridge.template_of(c)
+        _, want, _ = O.run_proportional(ops, finals, sizes, bridge.oracle_errorsets(c, es), 5)
+        assert big == want
 
 
 def test_many_error_sets_single_shot_descent():
