@@ -528,11 +528,17 @@ static void launch_lane(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelD
 
 // class-0 hoist over a large batch of error sets: one thread per error set, arena in global memory
 template <typename R>
-static void launch_lane_big(ptsbe_plan* pl, Program& pr, const LevelDev* levels_dev, const uint8_t* kraus_dev,
-                            uint32_t n_items, void* out) {
+static void launch_lane_big(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelDev* levels_dev,
+                            const uint8_t* kraus_dev, uint32_t first, uint32_t n_items, void* out,
+                            double* mass = nullptr, double* minv = nullptr) {
   using C = typename CxT<R>::type;
   if (n_items == 0) return;
-  LaneArgs a = lane_args<R>(pl, pr, EXEC_HOIST, levels_dev, kraus_dev, 0, n_items, out, 0);
+  LaneArgs a = lane_args<R>(pl, pr, mode, levels_dev, kraus_dev, first, n_items, out, 0);
+  a.e.out_mass = mass;
+  a.e.out_min = minv;
+  a.e.result_kind = pr.d.result_kind;
+  a.e.result_ref = pr.d.result_ref;
+  a.e.item_bytes = pr.d.threads_per_item;  // MARGINAL: the mass is folded the way that many lanes would (lane.cuh)
   const LaneLayout L = lane_layout(a.e.n_steps, a.n_leaves, 0, a.n_levels, 0, a.e.words, (uint32_t)sizeof(C));
   opt_in_smem((const void*)exec_lane_kernel<R, true>, 200 * 1024);
   if (pr.lane_big_blocks_per_sm == 0)
@@ -550,8 +556,8 @@ static void launch_lane_big(ptsbe_plan* pl, Program& pr, const LevelDev* levels_
 static void launch_hoist(ptsbe_plan* pl, Program& pr, const LevelDev* lv, const uint8_t* kraus,
                          uint32_t n, void* out) {
   if (pr.lane_big_ok && pl->lane && n >= pl->lane_big_min) {
-    if (pl->dtype == PTSBE_C64) launch_lane_big<float>(pl, pr, lv, kraus, n, out);
-    else launch_lane_big<double>(pl, pr, lv, kraus, n, out);
+    if (pl->dtype == PTSBE_C64) launch_lane_big<float>(pl, pr, EXEC_HOIST, lv, kraus, 0, n, out);
+    else launch_lane_big<double>(pl, pr, EXEC_HOIST, lv, kraus, 0, n, out);
     return;
   }
   if (pr.lane_ok && pl->lane) {
@@ -1195,6 +1201,14 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
         log.begin(&stats->project_ms[j - 1]);
         launch_project(pl, progs[j - 1], vbuf.p, vec_pitch(nbatch), table[1].ext, table[1].ext_rec,
                        cur.eset.as<uint32_t>(), s0, nbatch, probs.p);
+      } else if (j == 1 && progs[0].lane_big_ok && progs[0].d.result_kind == 0 && pl->lane && U >= pl->lane_big_min) {
+        // stage 1 over a large batch of error sets: one thread per error set (lane.cuh BIG)
+        if (pl->dtype == PTSBE_C64)
+          launch_lane_big<float>(pl, progs[0], EXEC_MARGINAL, table_dev.as<LevelDev>(), kraus_dev, s0, nbatch,
+                                 probs.p, mass.as<double>(), minv.as<double>());
+        else
+          launch_lane_big<double>(pl, progs[0], EXEC_MARGINAL, table_dev.as<LevelDev>(), kraus_dev, s0, nbatch,
+                                  probs.p, mass.as<double>(), minv.as<double>());
       } else {
         launch_exec_any(pl, progs[j - 1], EXEC_MARGINAL, table_dev.as<LevelDev>(), kraus_dev, s0,
                         nbatch, probs.p, mass.as<double>(), minv.as<double>());
@@ -1440,25 +1454,36 @@ static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stat
   // chunk the error sets: bounded shots (slot arrays) and bounded hoist records
   std::vector<std::pair<uint64_t, uint64_t>> chunks;  // (first set, count)
   {
+    // hoist-record bound of a chunk of `cnt` error sets with `sh` shots: records of pass p exist for
+    // every level-(p+1) item
+    std::vector<double> fan(pl->f + 1);
+    for (uint32_t p = 0; p <= pl->f; ++p) fan[p] = std::pow(2.0, std::min<uint32_t>(pl->offsets[std::min(p, pl->f - 1)], 60));
+    auto ext_bytes_of = [&](uint64_t sh, uint64_t cnt) {
+      size_t worst = 0;
+      for (uint32_t j = 1; j <= pl->f; ++j) {
+        size_t here = 0;
+        for (uint32_t p = 0; p + 1 < j; ++p) {
+          const double cap_items = std::min<double>((double)sh, (double)cnt * fan[p]);
+          here += (size_t)(cap_items * pl->programs[j - 1][p].d.out_elems * pl->elem);
+        }
+        worst = std::max(worst, here);
+      }
+      return worst;
+    };
     uint64_t e = 0;
+    // the whole batch fits one chunk (the usual case): no walk over the error sets, which costs
+    // milliseconds of idle GPU at 10^5 sets
+    if (bt->n_sets && bt->total_shots <= pl->chunk_shots && bt->total_shots < (1ull << 32) &&
+        ext_bytes_of(bt->total_shots, bt->n_sets) <= pl->ext_budget) {
+      chunks.push_back({0, bt->n_sets});
+      e = bt->n_sets;
+    }
     while (e < bt->n_sets) {
       uint64_t cnt = 0, sh = 0;
       while (e + cnt < bt->n_sets) {
         const uint64_t s = bt->shots_host[e + cnt];
         if (cnt && sh + s > pl->chunk_shots) break;
-        // hoist-record bound: records of pass p exist for every level-(p+1) item
-        size_t ext_bytes = 0;
-        for (uint32_t j = 1; j <= pl->f; ++j) {
-          size_t here = 0;
-          for (uint32_t p = 0; p + 1 < j; ++p) {
-            const double cap_items = std::min<double>(
-                (double)(sh + s),
-                (double)(cnt + 1) * std::pow(2.0, std::min<uint32_t>(pl->offsets[p], 60)));
-            here += (size_t)(cap_items * pl->programs[j - 1][p].d.out_elems * pl->elem);
-          }
-          ext_bytes = std::max(ext_bytes, here);
-        }
-        if (cnt && ext_bytes > pl->ext_budget) break;
+        if (cnt && ext_bytes_of(sh + s, cnt + 1) > pl->ext_budget) break;
         sh += s;
         ++cnt;
       }

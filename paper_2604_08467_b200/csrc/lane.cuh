@@ -368,6 +368,39 @@ __device__ __forceinline__ void lane_run(const LaneCtx<R>& cx, uint32_t s0, uint
 // ---------------------------------------------------------------------------
 // standalone: hoist passes p >= 1 and vector rows, one thread per work item
 // ---------------------------------------------------------------------------
+// Marginal epilogue of a lane-owned item (reference engine.py:445-450: real part, minimum before
+// clamping, clamp, mass), bit-compatible with the GS-lane epilogue of exec_kernel: that one gives lane t
+// the elements c = t (mod GS), sums them in double in increasing c and folds the GS partial sums with
+// xor-butterflies of distance GS/2 .. 1.  Here one thread keeps the GS partial sums itself and folds
+// them in the same tree, so the mass does not depend on which kernel served the error set.
+template <typename R, int GS>
+__device__ __forceinline__ void lane_marginal_epilogue(const typename CxT<R>::type* res, uint32_t res_stride,
+                                                       uint32_t n, R* o, bool live, double& mass, double& mn_out) {
+  double part[GS];
+#pragma unroll
+  for (int t = 0; t < GS; ++t) part[t] = 0.0;
+  double mn = 1e300;
+  for (uint32_t c0 = 0; c0 < n; c0 += GS) {
+#pragma unroll
+    for (int t = 0; t < GS; ++t) {
+      const uint32_t c = c0 + t;
+      if (c < n) {
+        R v = res[(size_t)c * res_stride].x;
+        mn = fmin(mn, (double)v);
+        v = v > R(0) ? v : R(0);
+        part[t] += (double)v;
+        if (live) o[c] = v;
+      }
+    }
+  }
+#pragma unroll
+  for (int d = GS / 2; d > 0; d >>= 1)
+#pragma unroll
+    for (int t = 0; t < d; ++t) part[t] += part[t + d];
+  mass = part[0];
+  mn_out = mn;
+}
+
 // BIG: class-0 programs of hundreds of steps over arenas of kilobytes (cfg5: 320-560 steps, 650-1600
 // elements) when the batch holds tens of thousands of error sets.  A group of lanes per item spends ~100
 // issued instructions per step on decoding for a handful of multiply-adds; with one thread per error set the
@@ -393,6 +426,20 @@ __global__ void __launch_bounds__(LN_THREADS) exec_lane_kernel(const LaneArgs a)
     C* rec = a.e.mode == EXEC_VECTOR ? reinterpret_cast<C*>(a.e.out) + (size_t)it * a.e.vec_row
                                      : reinterpret_cast<C*>(a.e.out) + (size_t)item * a.e.out_elems;
     lane_run<R>(cx, 0, a.e.n_steps, eset, rec, live);
+    if constexpr (BIG) {
+      if (a.e.mode == EXEC_MARGINAL) {
+        // stage-1 marginal pass: the root sits in this lane's arena slice
+        const C* res = cx.arena_w + (size_t)a.e.result_ref * 32 + (threadIdx.x & 31);
+        R* o = reinterpret_cast<R*>(a.e.out) + (size_t)it * a.e.out_elems;
+        double mass, mn;
+        switch (a.e.item_bytes) {  // lanes per item of the group kernel this one stands in for
+          case 8: lane_marginal_epilogue<R, 8>(res, 32, a.e.out_elems, o, live, mass, mn); break;
+          case 16: lane_marginal_epilogue<R, 16>(res, 32, a.e.out_elems, o, live, mass, mn); break;
+          default: lane_marginal_epilogue<R, 32>(res, 32, a.e.out_elems, o, live, mass, mn); break;
+        }
+        if (live) { a.e.out_mass[it] = mass; a.e.out_min[it] = mn; }
+      }
+    }
   }
 }
 
