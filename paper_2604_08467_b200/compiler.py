@@ -233,6 +233,7 @@ def compile_stage(
     mirror: Optional[Sequence[int]] = None,
     fold_from: Optional[int] = None,
     consumer_layout: bool = False,
+    step_order: str = "dfs",
 ) -> tuple[list[Program], tuple]:
     """Compile one stage network + stored path into `n_passes` programs.
     Returns (programs, result label order).
@@ -242,6 +243,12 @@ def compile_stage(
     those classes have about as many distinct instances as there are work items, so a hoist pass
     would save no arithmetic and cost a launch plus a record round trip through HBM).  The
     programs of the folded passes are empty.
+
+    `step_order`: "dfs" (default) replays the steps of a pass depth first, the child with the larger
+    live footprint first (Sethi-Ullman), instead of in stored-path order ("path").  Every node is
+    still the contraction of the same two children, so every value is bit-identical; what changes is
+    how long intermediates stay alive, i.e. the arena a work item needs (shared memory per item for
+    the group kernels, cache footprint for the thread-per-error-set kernel).
 
     `consumer_layout`: store every record in the order its latest consumer reads it (see "record
     layout" below).  Off by default: measured on cfg2, contiguous per-item
@@ -413,6 +420,8 @@ def compile_stage(
         mine = [nid for nid in range(n_leaves, len(nodes)) if nodes[nid].pass_ == p and nid not in virt and nid not in view]
         if proj is not None and p == top:
             mine = [nid for nid in mine if nid != root]
+        if step_order == "dfs":
+            mine = _depth_first(nodes, mine, rec_off, lambda x: storage_of(x)[0])
         # sizing of the on-chip arena: try everything on chip, spill the big buffers otherwise
         max_out = max([nodes[nid].size for nid in mine], default=1)
         peak = _place(nodes, mine, rec_off, lambda x: storage_of(x)[0], fast_cap=None)[1]
@@ -659,6 +668,62 @@ def _relabel(nodes, virt, view, nid, new_labels):
     for w, (child, lb, _) in view.items():
         if child == nid:
             _relabel(nodes, virt, view, w, tuple(x for x in new_labels if x != lb))
+
+
+def _depth_first(nodes, mine, rec_off, real_of):
+    """Topological order of the nodes of one pass that keeps few intermediates alive: post-order
+    over the pass's forest, at every node the operand whose evaluation needs the larger arena first
+    (its result then waits alone while the smaller sibling is evaluated).  Record outputs do not
+    occupy the arena.  Nodes with several consumers (conjugate twins make the tree a DAG) are
+    evaluated at their first use."""
+    mine_set = set(mine)
+
+    def deps(nid):
+        out = []
+        for ch in (nodes[nid].a, nodes[nid].b):
+            ch = real_of(ch)
+            if ch in mine_set and ch not in out:
+                out.append(ch)
+        return out
+
+    # need[n]: arena elements the evaluation of n's subtree peaks at; hold[n]: what stays afterwards
+    need: dict[int, int] = {}
+    order_of: dict[int, list] = {}
+    for nid in mine:  # stored-path order is topological
+        ds = deps(nid)
+        hold = 0 if nid in rec_off else nodes[nid].size
+        held = lambda d: 0 if d in rec_off else nodes[d].size
+        # evaluating children in order c1, c2: peak = max(need[c1], held(c1) + need[c2], held(c1) + held(c2) + hold)
+        ds.sort(key=lambda d: need[d] - held(d), reverse=True)
+        peak, carried = 0, 0
+        for d in ds:
+            peak = max(peak, carried + need[d])
+            carried += held(d)
+        need[nid] = max(peak, carried + hold)
+        order_of[nid] = ds
+    consumed = set()
+    for nid in mine:
+        consumed.update(order_of[nid])
+    out: list[int] = []
+    seen: set[int] = set()
+    for r in mine:
+        if r in consumed:
+            continue
+        stack = [(r, 0)]
+        while stack:
+            nid, k = stack.pop()
+            if nid in seen:
+                continue
+            ds = order_of[nid]
+            if k < len(ds):
+                stack.append((nid, k + 1))
+                if ds[k] not in seen:
+                    stack.append((ds[k], 0))
+            else:
+                seen.add(nid)
+                out.append(nid)
+    assert len(out) == len(mine), "depth-first order lost nodes"
+    return out
 
 
 def _place(nodes, mine, rec_off, real_of, fast_cap):

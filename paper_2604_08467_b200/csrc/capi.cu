@@ -80,6 +80,10 @@ struct ptsbe_plan {
   uint32_t lane_x = 1;                 // lane-per-draw fused descent for Hermitian cuts (lane_x.cuh)
   uint32_t lane_chain = 0;             // ... with the vector-matrix chain served by lane groups (lane_x.cuh CHAIN);
                                        // pays only with PTSBE_RECORD_LAYOUT=1
+  uint32_t warp_runs = 1;              // fused descent: a private tree table per warp when error sets bring ...
+  uint32_t warp_run_len = 512;         // ... fewer than this many work items each on average (lane.cuh warp_runs)
+  uint32_t stage_image = 1;            // lane-group class-0 programs keep their image in shared memory ...
+  uint32_t stage_image_max = 4096;     // ... for batches of at most this many error sets (executor.cuh STAGED)
   uint32_t lane_big_min = 16384;       // class-0 hoists over at least this many error sets run one thread per
                                        // error set with a global-memory arena (lane.cuh BIG)
   uint32_t descent = 1;                // per-qubit descent sampler for low-multiplicity stages
@@ -199,6 +203,7 @@ struct ExecLaunch {
   size_t smem;
   uint32_t item_bytes;
   uint32_t groups_per_block;
+  bool staged = false;  // lane-group program with its image in shared memory (executor.cuh STAGED)
 };
 
 template <typename R>
@@ -211,9 +216,15 @@ static ExecLaunch configure_exec(ptsbe_plan* pl, Program& pr, uint32_t n_items) 
   L.item_bytes = (uint32_t)ib;
   const uint32_t gs = d.threads_per_item;  // 8 / 16 / 32: sub-warp groups; larger: one CTA per item
   const bool warp = gs <= 32;
+  // class-0 lane-group programs over small batches are bound by the latency of their dependent
+  // program reads: keep the image in shared memory when it fits beside the groups' arenas
+  const size_t image = (((size_t)d.n_steps * STEP_WORDS + (size_t)d.n_leaves * LEAF_WORDS + d.n_table_words) * 4 + 15) & ~size_t(15);
+  L.staged = warp && pl->stage_image && d.level == 1 && d.n_steps >= 32 && image <= 120 * 1024 &&
+             n_items <= pl->stage_image_max && ib * (32 / gs) + 1024 + image <= 200 * 1024;
   if (warp) {
     uint32_t block = 256;
-    while (block > 32 && ib * (block / gs) + 1024 > 200 * 1024) block >>= 1;
+    const size_t extra = L.staged ? image : 0;
+    while (block > 32 && ib * (block / gs) + 1024 + extra > 200 * 1024) block >>= 1;
     L.groups_per_block = block / gs;
     L.block = block;
   } else {
@@ -230,21 +241,32 @@ static ExecLaunch configure_exec(ptsbe_plan* pl, Program& pr, uint32_t n_items) 
     L.smem += (size_t)L.desc_cap * STEP_WORDS * 4;
     if (memo) L.smem += (size_t)L.desc_cap * 2 * sizeof(void*);  // pre-resolved leaf operands
   }
+  if (L.staged) {  // the image follows the groups and the reduction scratch
+    L.desc_off = (uint32_t)L.smem;
+    L.smem += image;
+  }
   if (L.smem > 227 * 1024)
     throw Failure(PTSBE_ERESOURCE, "stage program needs more shared memory than one SM has");
-  void (*kern)(ExecArgs) = gs == 8    ? exec_kernel<R, 8, false>
-                           : gs == 16 ? exec_kernel<R, 16, false>
-                           : gs == 32 ? exec_kernel<R, 32, false>
+  void (*kern)(ExecArgs) = gs == 8    ? (L.staged ? exec_kernel<R, 8, false, false, true> : exec_kernel<R, 8, false>)
+                           : gs == 16 ? (L.staged ? exec_kernel<R, 16, false, false, true> : exec_kernel<R, 16, false>)
+                           : gs == 32 ? (L.staged ? exec_kernel<R, 32, false, false, true> : exec_kernel<R, 32, false>)
                            : memo     ? (pr.tiled ? exec_kernel<R, 0, true, true> : exec_kernel<R, 0, true>)
                                       : exec_kernel<R, 0, false>;
-  if (pr.blocks_per_sm == 0) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, (int)L.block, L.smem));
-    pr.blocks_per_sm = std::max(nb, 1);
+  int per_sm;
+  if (L.staged) {
+    opt_in_smem((const void*)kern, 227 * 1024);
+    per_sm = cached_occupancy((const void*)kern, (int)L.block, L.smem);
+  } else {
+    if (pr.blocks_per_sm == 0) {
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      int nb = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, (int)L.block, L.smem));
+      pr.blocks_per_sm = std::max(nb, 1);
+    }
+    per_sm = pr.blocks_per_sm;
   }
   const uint64_t need = (n_items + L.groups_per_block - 1) / L.groups_per_block;
-  const uint64_t cap = (uint64_t)pl->sm_count * pr.blocks_per_sm;
+  const uint64_t cap = (uint64_t)pl->sm_count * per_sm;
   L.grid = (unsigned)std::max<uint64_t>(1, std::min(need, cap));
   return L;
 }
@@ -323,8 +345,13 @@ static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelD
   a.memo_ptr = pr.memo_ptr.as<uint32_t>();
   a.memo_idx = pr.memo_idx.as<uint32_t>();
   a.n_memo_sites = pr.d.n_memo_sites;
+  a.n_leaves = pr.d.n_leaves;
+  a.n_table_words = pr.d.n_table_words;
   const uint32_t gs = pr.d.threads_per_item;
-  if (gs == 8) exec_kernel<R, 8, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  if (L.staged && gs == 8) exec_kernel<R, 8, false, false, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  else if (L.staged && gs == 16) exec_kernel<R, 16, false, false, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  else if (L.staged && gs == 32) exec_kernel<R, 32, false, false, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  else if (gs == 8) exec_kernel<R, 8, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
   else if (gs == 16) exec_kernel<R, 16, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
   else if (gs == 32) exec_kernel<R, 32, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
   else if (memo && pr.tiled) exec_kernel<R, 0, true, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
@@ -607,23 +634,23 @@ static void launch_descent(ptsbe_plan* pl, const DescentArgs& a, const DescentSh
 }
 
 template <typename R, int NCH, bool HERM>
-static void launch_lane_descent_t(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a) {
+static void launch_lane_descent_t(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a, uint32_t n_sets) {
   using C = typename CxT<R>::type;
   using CH = typename DsChunk<R>::type;
   const LaneLayout L = lane_layout(a.l.e.n_steps, a.l.n_leaves, a.l.n_table_words, a.l.n_levels,
                                    a.l.e.arena_fast, a.l.e.words, (uint32_t)sizeof(C));
-  const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4) +
-                      (((size_t)(LN_GS * NCH + (NCH >= 2 ? 0 : 1)) * sizeof(CH)) << a.d.b);
+  const size_t table = ((size_t)(LN_GS * NCH + (NCH >= 2 ? 0 : 1)) * sizeof(CH)) << a.d.b;
+  const size_t fixed = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4);
+  // short runs of items per error set: a private table per warp, no CTA barriers (lane.cuh warp_runs)
+  a.warp_runs = pl->warp_runs && a.d.n_items < (uint64_t)pl->warp_run_len * n_sets &&
+                fixed + table * LN_WARPS <= 110 * 1024;
+  const size_t smem = fixed + table * (a.warp_runs ? LN_WARPS : 1);
   if (smem > 200 * 1024) throw Failure(PTSBE_ERESOURCE, "fused descent needs more shared memory than one SM has");
-  if (pr.lane_blocks_per_sm == 0) {
-    CK(cudaFuncSetAttribute(lane_descent_kernel<R, NCH, HERM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    int nb = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lane_descent_kernel<R, NCH, HERM>, LN_THREADS, smem));
-    pr.lane_blocks_per_sm = std::max(nb, 1);
-  }
+  opt_in_smem((const void*)lane_descent_kernel<R, NCH, HERM>, 200 * 1024);
+  const int per_sm = cached_occupancy((const void*)lane_descent_kernel<R, NCH, HERM>, LN_THREADS, smem);
   // tiles: long enough to amortise the CTA barriers around an error-set run, short enough that
   // every resident CTA gets several
-  const uint64_t ctas = (uint64_t)pl->sm_count * pr.lane_blocks_per_sm;
+  const uint64_t ctas = (uint64_t)pl->sm_count * per_sm;
   uint64_t tile = a.d.n_items / (ctas * 4) / LN_THREADS * LN_THREADS;
   tile = std::min<uint64_t>(2048, std::max<uint64_t>(LN_THREADS, tile));
   a.tile = (uint32_t)tile;
@@ -635,14 +662,17 @@ static void launch_lane_descent_t(ptsbe_plan* pl, Program& pr, LaneDescentArgs& 
 }
 
 template <int DX, bool CHAIN>
-static void launch_lane_descent_x(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a) {
+static void launch_lane_descent_x(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a, uint32_t n_sets) {
   // CHAIN keeps the intermediate vectors in registers: the arena holds only x (DX entries per item)
   if (CHAIN) a.l.e.arena_fast = DX;
   const LaneLayout L = lane_layout(a.l.e.n_steps, a.l.n_leaves, a.l.n_table_words, a.l.n_levels,
                                    a.l.e.arena_fast, a.l.e.words, (uint32_t)sizeof(float2));
   constexpr size_t NQ = DX * DX / 4 > 0 ? DX * DX / 4 : 1;
-  const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4 + (CHAIN ? LN_CHAIN_MAX * 4 : 0)) +
-                      (((NQ + 1) * 16) << a.d.b);
+  const size_t table = ((NQ + 1) * 16) << a.d.b;
+  const size_t fixed = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4 + (CHAIN ? LN_CHAIN_MAX * 4 : 0));
+  a.warp_runs = pl->warp_runs && a.d.n_items < (uint64_t)pl->warp_run_len * n_sets &&
+                fixed + table * LN_WARPS <= 110 * 1024;
+  const size_t smem = fixed + table * (a.warp_runs ? LN_WARPS : 1);
   if (smem > 200 * 1024) throw Failure(PTSBE_ERESOURCE, "fused descent needs more shared memory than one SM has");
   opt_in_smem((const void*)lane_descent_x_kernel<DX, CHAIN>, 200 * 1024);
   const int per_sm = cached_occupancy((const void*)lane_descent_x_kernel<DX, CHAIN>, LN_THREADS, smem);
@@ -667,33 +697,34 @@ static bool lane_descent_fits(const ptsbe_plan* pl, const Program& pr, const Des
   return nch_f <= 8 && smem <= 200 * 1024;
 }
 
-static void launch_lane_descent(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a, const DescentShape& sh) {
+static void launch_lane_descent(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a, const DescentShape& sh,
+                                uint32_t n_sets) {
   if (a.d.n_items == 0) return;
   const bool f32 = pl->dtype == PTSBE_C64;
   if (a.herm_map && f32 && pr.herm_dx && pl->lane_x) {
     // x (x) conj(x) with a small x: one lane per draw over canonically packed columns (lane_x.cuh)
     const bool chain = pr.lane_chain && pl->lane_chain;
     switch (pr.herm_dx) {
-      case 4: chain ? launch_lane_descent_x<4, true>(pl, pr, a) : launch_lane_descent_x<4, false>(pl, pr, a); return;
-      case 8: chain ? launch_lane_descent_x<8, true>(pl, pr, a) : launch_lane_descent_x<8, false>(pl, pr, a); return;
+      case 4: chain ? launch_lane_descent_x<4, true>(pl, pr, a, n_sets) : launch_lane_descent_x<4, false>(pl, pr, a, n_sets); return;
+      case 8: chain ? launch_lane_descent_x<8, true>(pl, pr, a, n_sets) : launch_lane_descent_x<8, false>(pl, pr, a, n_sets); return;
       default: break;
     }
   }
   if (a.herm_map) {
     switch (sh.nch) {
-      case 1: f32 ? launch_lane_descent_t<float, 1, true>(pl, pr, a) : launch_lane_descent_t<double, 1, true>(pl, pr, a); break;
-      case 2: f32 ? launch_lane_descent_t<float, 2, true>(pl, pr, a) : launch_lane_descent_t<double, 2, true>(pl, pr, a); break;
-      case 4: f32 ? launch_lane_descent_t<float, 4, true>(pl, pr, a) : launch_lane_descent_t<double, 4, true>(pl, pr, a); break;
-      case 8: f32 ? launch_lane_descent_t<float, 8, true>(pl, pr, a) : launch_lane_descent_t<double, 8, true>(pl, pr, a); break;
+      case 1: f32 ? launch_lane_descent_t<float, 1, true>(pl, pr, a, n_sets) : launch_lane_descent_t<double, 1, true>(pl, pr, a, n_sets); break;
+      case 2: f32 ? launch_lane_descent_t<float, 2, true>(pl, pr, a, n_sets) : launch_lane_descent_t<double, 2, true>(pl, pr, a, n_sets); break;
+      case 4: f32 ? launch_lane_descent_t<float, 4, true>(pl, pr, a, n_sets) : launch_lane_descent_t<double, 4, true>(pl, pr, a, n_sets); break;
+      case 8: f32 ? launch_lane_descent_t<float, 8, true>(pl, pr, a, n_sets) : launch_lane_descent_t<double, 8, true>(pl, pr, a, n_sets); break;
       default: throw Failure(PTSBE_EINVAL, "descent sampler: unsupported vector length");
     }
     return;
   }
   switch (sh.nch) {
-    case 1: f32 ? launch_lane_descent_t<float, 1, false>(pl, pr, a) : launch_lane_descent_t<double, 1, false>(pl, pr, a); break;
-    case 2: f32 ? launch_lane_descent_t<float, 2, false>(pl, pr, a) : launch_lane_descent_t<double, 2, false>(pl, pr, a); break;
-    case 4: f32 ? launch_lane_descent_t<float, 4, false>(pl, pr, a) : launch_lane_descent_t<double, 4, false>(pl, pr, a); break;
-    case 8: f32 ? launch_lane_descent_t<float, 8, false>(pl, pr, a) : launch_lane_descent_t<double, 8, false>(pl, pr, a); break;
+    case 1: f32 ? launch_lane_descent_t<float, 1, false>(pl, pr, a, n_sets) : launch_lane_descent_t<double, 1, false>(pl, pr, a, n_sets); break;
+    case 2: f32 ? launch_lane_descent_t<float, 2, false>(pl, pr, a, n_sets) : launch_lane_descent_t<double, 2, false>(pl, pr, a, n_sets); break;
+    case 4: f32 ? launch_lane_descent_t<float, 4, false>(pl, pr, a, n_sets) : launch_lane_descent_t<double, 4, false>(pl, pr, a, n_sets); break;
+    case 8: f32 ? launch_lane_descent_t<float, 8, false>(pl, pr, a, n_sets) : launch_lane_descent_t<double, 8, false>(pl, pr, a, n_sets); break;
     default: throw Failure(PTSBE_EINVAL, "descent sampler: unsupported vector length");
   }
 }
@@ -1103,7 +1134,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
         log.begin(&stats->descent_ms[j - 1]);
         DescentShape fsh = dsh;  // chunks per lane of the fused kernel's LN_GS-lane groups
         fsh.nch = dsh.nch * (DS_GS / LN_GS);
-        launch_lane_descent(pl, prj, fa, hsh.nch ? hsh : fsh);
+        launch_lane_descent(pl, prj, fa, hsh.nch ? hsh : fsh, ne);
         DedupArgs dd;
         dd.slot_off = da.slot_off;
         dd.slot_index = da.slot_index;
@@ -1680,6 +1711,10 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     pl->lane_x = (uint32_t)env_size("PTSBE_LANE_X", pl->lane_x);
     pl->lane_chain = (uint32_t)env_size("PTSBE_LANE_CHAIN", pl->lane_chain);
     pl->lane_big_min = (uint32_t)env_size("PTSBE_LANE_BIG_MIN", pl->lane_big_min);
+    pl->stage_image = (uint32_t)env_size("PTSBE_STAGE_IMAGE", pl->stage_image);
+    pl->warp_runs = (uint32_t)env_size("PTSBE_WARP_RUNS", pl->warp_runs);
+    pl->warp_run_len = (uint32_t)env_size("PTSBE_WARP_RUN_LEN", pl->warp_run_len);
+    pl->stage_image_max = (uint32_t)env_size("PTSBE_STAGE_IMAGE_MAX", pl->stage_image_max);
     pl->lane = (uint32_t)env_size("PTSBE_LANE", pl->lane);
     if (const char* dm = getenv("PTSBE_DESCENT_MULT")) if (*dm) pl->descent_mult = atof(dm);
     pl->chunk_shots = env_size("PTSBE_CHUNK_SHOTS", pl->chunk_shots);

@@ -79,6 +79,7 @@ struct ExecArgs {
   // of dependent loads otherwise: descriptor -> table -> operand)
   uint32_t desc_off;   // byte offset of the staging area from the dynamic shared-memory base
   uint32_t desc_cap;   // steps it holds (0: none)
+  uint32_t n_leaves, n_table_words;  // STAGED: the whole program image goes to the staging area
 };
 
 constexpr uint32_t DESC_CAP = 192;  // staged step descriptors per CTA (x 80 bytes)
@@ -99,6 +100,13 @@ __device__ __forceinline__ void cmac(C& acc, const C a, const C b) {
   acc.y = fma(a.y, b.x, acc.y);
 }
 
+// program words (steps, leaves, gather tables): read-only global memory, or -- STAGED -- the copy a CTA
+// keeps in shared memory (generic pointer, so no ld.global.nc)
+template <bool STAGED>
+__device__ __forceinline__ uint32_t ldt(const uint32_t* p) { return STAGED ? *p : __ldg(p); }
+template <bool STAGED>
+__device__ __forceinline__ uint4 ldt4(const uint4* p) { return STAGED ? *p : __ldg(p); }
+
 struct StepTables {
   const uint32_t *loA, *loB, *hiA, *hiB, *kA, *kB;
   uint32_t out_n, lo_n, hi_n;
@@ -113,13 +121,13 @@ __device__ __forceinline__ C ld_conj(const C* p, bool flip) {
 }
 
 // inner product over KN shared labels with the k-offsets held in registers
-template <typename C, int KN>
+template <typename C, int KN, bool STAGED = false>
 __device__ __forceinline__ void step_fixed_k(const C* __restrict__ A, const C* __restrict__ B, C* O,
                                              size_t o_stride, const StepTables& t, int tid,
                                              int gsize, bool store) {
   uint32_t ka[KN], kb[KN];
 #pragma unroll
-  for (int k = 0; k < KN; ++k) { ka[k] = __ldg(t.kA + k); kb[k] = __ldg(t.kB + k); }
+  for (int k = 0; k < KN; ++k) { ka[k] = ldt<STAGED>(t.kA + k); kb[k] = ldt<STAGED>(t.kB + k); }
   const int sh = 31 - __clz(t.lo_n);
   const bool pow2 = (t.lo_n & (t.lo_n - 1)) == 0;
   const bool fa = t.conj & 1, fb = t.conj & 2;
@@ -127,8 +135,8 @@ __device__ __forceinline__ void step_fixed_k(const C* __restrict__ A, const C* _
     uint32_t cl, ch;
     if (pow2) { cl = c & (t.lo_n - 1); ch = c >> sh; }
     else { ch = c / t.lo_n; cl = c - ch * t.lo_n; }
-    uint32_t a0 = __ldg(t.loA + cl), b0 = __ldg(t.loB + cl);
-    if (t.hi_n > 1) { a0 += __ldg(t.hiA + ch); b0 += __ldg(t.hiB + ch); }
+    uint32_t a0 = ldt<STAGED>(t.loA + cl), b0 = ldt<STAGED>(t.loB + cl);
+    if (t.hi_n > 1) { a0 += ldt<STAGED>(t.hiA + ch); b0 += ldt<STAGED>(t.hiB + ch); }
     C acc; acc.x = 0; acc.y = 0;
 #pragma unroll
     for (int k = 0; k < KN; ++k) cmac(acc, ld_conj(A + a0 + ka[k], fa), ld_conj(B + b0 + kb[k], fb));
@@ -194,7 +202,11 @@ __device__ __forceinline__ void tiled_step(const C* __restrict__ A, const C* __r
 //           memo that was computed once per plan.
 // TILED   : (with MEMO) large steps run in their separable form with register tiles; costs
 //           registers, so only programs dominated by such steps use it
-template <typename R, int GS, bool MEMO, bool TILED = false>
+// STAGED  : (GS > 0 only) the program image -- steps, leaves, gather tables -- is copied to shared memory
+//           once per CTA.  A step of a lane-group program is a chain of dependent reads (descriptor ->
+//           tables -> leaf row -> Kraus index -> operand); from global memory that chain costs ~2000
+//           cycles per step, which is all there is when a batch holds few error sets (cfg5 at E <= 10^4).
+template <typename R, int GS, bool MEMO, bool TILED = false, bool STAGED = false>
 __global__ void __launch_bounds__(256, TILED ? 3 : 5) exec_kernel(const ExecArgs a) {
   using C = typename CxT<R>::type;
   constexpr bool WARP = GS > 0;
@@ -227,6 +239,20 @@ __global__ void __launch_bounds__(256, TILED ? 3 : 5) exec_kernel(const ExecArgs
   uint32_t* desc_s = reinterpret_cast<uint32_t*>(smem_raw + a.desc_off);
   const C** pre_s = reinterpret_cast<const C**>(smem_raw + a.desc_off + (size_t)a.desc_cap * STEP_WORDS * 4);
   uint32_t n_staged = 0;
+  const uint32_t* steps_p = a.steps;
+  const uint32_t* leaves_p = a.leaves;
+  const uint32_t* tables_p = a.tables;
+  if constexpr (STAGED) {
+    uint32_t* img = reinterpret_cast<uint32_t*>(smem_raw + a.desc_off);
+    const uint32_t ns = a.n_steps * STEP_WORDS, nl = a.n_leaves * LEAF_WORDS, nt = a.n_table_words;
+    for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) img[i] = __ldg(a.steps + i);
+    for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) img[ns + i] = __ldg(a.leaves + i);
+    for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) img[ns + nl + i] = __ldg(a.tables + i);
+    __syncthreads();
+    steps_p = img;
+    leaves_p = img + ns;
+    tables_p = img + ns + nl;
+  }
   if (!WARP && !MEMO && a.desc_cap) {
     // same step list for every item: staged once
     n_staged = min(a.n_steps, a.desc_cap);
@@ -328,13 +354,13 @@ __global__ void __launch_bounds__(256, TILED ? 3 : 5) exec_kernel(const ExecArgs
 
     // measured bit selected by a prefix-projector leaf (slice steps read the bit, not the vector)
     auto leaf_bit = [&](uint32_t ref) -> uint32_t {
-      const uint4 lf = __ldg(reinterpret_cast<const uint4*>(a.leaves) + ref);
+      const uint4 lf = ldt4<STAGED>(reinterpret_cast<const uint4*>(leaves_p) + ref);
       return (uint32_t)((pfx[lf.w >> 6] >> (63 - (lf.w & 63))) & 1ull);
     };
     auto resolve = [&](uint32_t kind, uint32_t ref) -> const C* {
       if (kind == 0) return ref < a.arena_fast ? arena + ref : spill + (ref - a.arena_fast);
       if (kind == 1) {
-        const uint4 lf = __ldg(reinterpret_cast<const uint4*>(a.leaves) + ref);
+        const uint4 lf = ldt4<STAGED>(reinterpret_cast<const uint4*>(leaves_p) + ref);
         uint32_t v = 0;
         if (lf.z == 1) v = __ldg(sel + lf.w);
         else if (lf.z == 2) v = (uint32_t)((pfx[lf.w >> 6] >> (63 - (lf.w & 63))) & 1ull);
@@ -364,10 +390,10 @@ __global__ void __launch_bounds__(256, TILED ? 3 : 5) exec_kernel(const ExecArgs
           if (TILED && nd[17]) prefetch_l1(a.tables + nd[16]);
         }
       } else {
-        const uint4* st4 = reinterpret_cast<const uint4*>(a.steps + (size_t)s * STEP_WORDS);
-        s0 = __ldg(st4); s1 = __ldg(st4 + 1); s2 = __ldg(st4 + 2);
-        if (MEMO) s3 = __ldg(st4 + 3);
-        if (TILED) s4 = __ldg(st4 + 4);
+        const uint4* st4 = reinterpret_cast<const uint4*>(steps_p + (size_t)s * STEP_WORDS);
+        s0 = ldt4<STAGED>(st4); s1 = ldt4<STAGED>(st4 + 1); s2 = ldt4<STAGED>(st4 + 2);
+        if (MEMO) s3 = ldt4<STAGED>(st4 + 3);
+        if (TILED) s4 = ldt4<STAGED>(st4 + 4);
       }
       const bool slice = (s2.w & 4u) != 0;
       const C* A = nullptr;
@@ -410,7 +436,7 @@ __global__ void __launch_bounds__(256, TILED ? 3 : 5) exec_kernel(const ExecArgs
       t.hi_n = s2.y;
       t.conj = s2.w;
       const uint32_t kn = s1.w;
-      t.loA = a.tables + s2.z;
+      t.loA = tables_p + s2.z;
       t.loB = t.loA + t.lo_n;
       t.hiA = t.loB + t.lo_n;
       t.hiB = t.hiA + t.hi_n;
@@ -420,16 +446,16 @@ __global__ void __launch_bounds__(256, TILED ? 3 : 5) exec_kernel(const ExecArgs
         // slice views: the operand is T[.., bit(q), ..] of a stored tensor -- add bit * stride
         // per sliced leg to the base instead of materialising the slice
         const uint32_t* dt = t.kB + kn;
-        const uint32_t na = __ldg(dt);
+        const uint32_t na = ldt<STAGED>(dt);
         for (uint32_t i = 0; i < na; ++i) {
-          const uint32_t q = __ldg(dt + 1 + 2 * i);
-          if ((pfx[q >> 6] >> (63 - (q & 63))) & 1ull) A += __ldg(dt + 2 + 2 * i);
+          const uint32_t q = ldt<STAGED>(dt + 1 + 2 * i);
+          if ((pfx[q >> 6] >> (63 - (q & 63))) & 1ull) A += ldt<STAGED>(dt + 2 + 2 * i);
         }
         dt += 1 + 2 * na;
-        const uint32_t nb = __ldg(dt);
+        const uint32_t nb = ldt<STAGED>(dt);
         for (uint32_t i = 0; i < nb; ++i) {
-          const uint32_t q = __ldg(dt + 1 + 2 * i);
-          if ((pfx[q >> 6] >> (63 - (q & 63))) & 1ull) B += __ldg(dt + 2 + 2 * i);
+          const uint32_t q = ldt<STAGED>(dt + 1 + 2 * i);
+          if ((pfx[q >> 6] >> (63 - (q & 63))) & 1ull) B += ldt<STAGED>(dt + 2 + 2 * i);
         }
       }
       if (MEMO && copy_memo) {
@@ -448,7 +474,7 @@ __global__ void __launch_bounds__(256, TILED ? 3 : 5) exec_kernel(const ExecArgs
       } else if (slice) {
         // B is the basis vector e_x of a measured bit, contracted over its only label:
         // out[c] = A[a0(c) + kA[x]] -- a gather, no multiply-adds
-        const uint32_t k0 = __ldg(t.kA), k1 = __ldg(t.kA + 1);
+        const uint32_t k0 = ldt<STAGED>(t.kA), k1 = ldt<STAGED>(t.kA + 1);
         const uint32_t off = leaf_bit(s0.w) ? k1 : k0;
         const bool pow2 = (t.lo_n & (t.lo_n - 1)) == 0;
         const int sh = 31 - __clz(t.lo_n);
@@ -457,17 +483,17 @@ __global__ void __launch_bounds__(256, TILED ? 3 : 5) exec_kernel(const ExecArgs
           uint32_t cl, ch;
           if (pow2) { cl = c & (t.lo_n - 1); ch = c >> sh; }
           else { ch = c / t.lo_n; cl = c - ch * t.lo_n; }
-          uint32_t a0 = __ldg(t.loA + cl);
-          if (t.hi_n > 1) a0 += __ldg(t.hiA + ch);
+          uint32_t a0 = ldt<STAGED>(t.loA + cl);
+          if (t.hi_n > 1) a0 += ldt<STAGED>(t.hiA + ch);
           const C v = ld_conj(A + a0 + off, fa);
           if (store) O[(size_t)c * o_stride] = v;
         }
       } else
       switch (kn) {
-        case 1: step_fixed_k<C, 1>(A, B, O, o_stride, t, tid, gsize, store); break;
-        case 2: step_fixed_k<C, 2>(A, B, O, o_stride, t, tid, gsize, store); break;
-        case 4: step_fixed_k<C, 4>(A, B, O, o_stride, t, tid, gsize, store); break;
-        case 8: step_fixed_k<C, 8>(A, B, O, o_stride, t, tid, gsize, store); break;
+        case 1: step_fixed_k<C, 1, STAGED>(A, B, O, o_stride, t, tid, gsize, store); break;
+        case 2: step_fixed_k<C, 2, STAGED>(A, B, O, o_stride, t, tid, gsize, store); break;
+        case 4: step_fixed_k<C, 4, STAGED>(A, B, O, o_stride, t, tid, gsize, store); break;
+        case 8: step_fixed_k<C, 8, STAGED>(A, B, O, o_stride, t, tid, gsize, store); break;
         default: {
           const bool pow2 = (t.lo_n & (t.lo_n - 1)) == 0;
           const int sh = 31 - __clz(t.lo_n);
@@ -476,11 +502,11 @@ __global__ void __launch_bounds__(256, TILED ? 3 : 5) exec_kernel(const ExecArgs
             uint32_t cl, ch;
             if (pow2) { cl = c & (t.lo_n - 1); ch = c >> sh; }
             else { ch = c / t.lo_n; cl = c - ch * t.lo_n; }
-            uint32_t a0 = __ldg(t.loA + cl), b0 = __ldg(t.loB + cl);
-            if (t.hi_n > 1) { a0 += __ldg(t.hiA + ch); b0 += __ldg(t.hiB + ch); }
+            uint32_t a0 = ldt<STAGED>(t.loA + cl), b0 = ldt<STAGED>(t.loB + cl);
+            if (t.hi_n > 1) { a0 += ldt<STAGED>(t.hiA + ch); b0 += ldt<STAGED>(t.hiB + ch); }
             C acc; acc.x = 0; acc.y = 0;
             for (uint32_t k = 0; k < kn; ++k)
-              cmac(acc, ld_conj(A + a0 + __ldg(t.kA + k), fa), ld_conj(B + b0 + __ldg(t.kB + k), fb));
+              cmac(acc, ld_conj(A + a0 + ldt<STAGED>(t.kA + k), fa), ld_conj(B + b0 + ldt<STAGED>(t.kB + k), fb));
             if (store) O[(size_t)c * o_stride] = acc;
           }
         }

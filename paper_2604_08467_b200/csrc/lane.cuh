@@ -452,6 +452,9 @@ struct LaneDescentArgs {
   uint32_t* big_list;       // items with more than LN_DEDUP_SERIAL draws (merged by dedup_big_kernel)
   uint32_t* big_count;
   uint32_t tile;            // consecutive items a CTA takes at a time (multiple of LN_THREADS)
+  uint32_t warp_runs;       // non-zero: every warp walks its own share of the tile with a private copy of the
+                            // tree table (short runs of items per error set: cfg5 has <= 100), instead of the
+                            // CTA serving one error set at a time between two barriers
   const uint32_t* herm_map; // HERM: [D] real slot -> c | c' << 12 | kind << 24 (kind 0: Re v_c, 1: Im v_c)
 };
 
@@ -523,9 +526,10 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
   uint32_t* bad_s = eset_s + LN_THREADS;                                       // [LN_THREADS]
   uint32_t* rank_s = bad_s + LN_THREADS;                                       // [LN_THREADS]
   uint32_t* gid_s = rank_s + LN_THREADS;                                       // [LN_THREADS]
-  CH* table = reinterpret_cast<CH*>(gid_s + LN_THREADS);                       // [N][COLP]
-  __shared__ uint32_t s_end;
   const int tid = threadIdx.x, lane32 = tid & 31, warp = tid >> 5;
+  const bool WR = a.warp_runs != 0;
+  CH* table = reinterpret_cast<CH*>(gid_s + LN_THREADS) + (WR ? (size_t)warp * N * COLP : 0);  // [N][COLP]
+  __shared__ uint32_t s_end;
   const int lane = tid & (LN_GS - 1), grp = lane32 / LN_GS;                    // LN_GS-lane groups
   const unsigned gmask = ((1u << LN_GS) - 1u) << (LN_GS * grp);
   const int ROT = NCH >= 2 ? (grp & 1) : 0;  // register slot i of v holds logical chunk i ^ ROT
@@ -632,25 +636,45 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
   const uint32_t tile_end = min(n_tiles, (blockIdx.x + 1) * tiles_per);
   __syncthreads();
   for (uint32_t tile = blockIdx.x * tiles_per; tile < tile_end; ++tile) {
-    const uint32_t t1 = min(d.n_items, (tile + 1) * a.tile);
+    uint32_t t1 = min(d.n_items, (tile + 1) * a.tile);
     uint32_t pos = tile * a.tile;
+    if (WR) {  // this warp's share of the tile
+      const uint32_t per = ((t1 - pos + LN_WARPS - 1) / LN_WARPS + 31) & ~31u;
+      pos = min(t1, pos + warp * per);
+      t1 = min(t1, pos + per);
+    }
     while (pos < t1) {
       // ---- the run of items [pos, end) that share error set er ----
       const uint32_t er = d.eset[d.first_item + pos];
-      if (tid == 0) s_end = t1;
-      __syncthreads();
-      for (uint32_t i = pos + 1 + tid; i < t1; i += LN_THREADS)
-        if (d.eset[d.first_item + i] != er) { atomicMin(&s_end, i); break; }
-      if (er != loaded) {
-        const CH* src = TREE + (size_t)er * N * COL;
-        for (uint32_t x = tid; x < N * COL; x += LN_THREADS) table[(x / COL) * COLP + (x % COL)] = __ldg(src + x);
-        loaded = er;
+      uint32_t end = t1;
+      if (WR) {
+        for (uint32_t i0 = pos + 1; i0 < t1; i0 += 32) {
+          const uint32_t i = i0 + lane32;
+          const unsigned differs = __ballot_sync(0xffffffffu, i < t1 && d.eset[d.first_item + i] != er);
+          if (differs) { end = i0 + __ffs(differs) - 1; break; }
+        }
+        if (er != loaded) {
+          const CH* src = TREE + (size_t)er * N * COL;
+          for (uint32_t x = lane32; x < N * COL; x += 32) table[(x / COL) * COLP + (x % COL)] = __ldg(src + x);
+          loaded = er;
+        }
+        __syncwarp();
+      } else {
+        if (tid == 0) s_end = t1;
+        __syncthreads();
+        for (uint32_t i = pos + 1 + tid; i < t1; i += LN_THREADS)
+          if (d.eset[d.first_item + i] != er) { atomicMin(&s_end, i); break; }
+        if (er != loaded) {
+          const CH* src = TREE + (size_t)er * N * COL;
+          for (uint32_t x = tid; x < N * COL; x += LN_THREADS) table[(x / COL) * COLP + (x % COL)] = __ldg(src + x);
+          loaded = er;
+        }
+        __syncthreads();
+        end = s_end;
       }
-      __syncthreads();
-      const uint32_t end = s_end;
       const double floor_mass = d.vanish * d.set_mass[er];
 
-      for (uint32_t w0 = pos + wbase; w0 < end; w0 += LN_THREADS) {
+      for (uint32_t w0 = pos + (WR ? 0u : wbase); w0 < end; w0 += (WR ? 32u : (uint32_t)LN_THREADS)) {
         // ---- phase A: this lane's item, every step but the last ----
         const uint32_t it = w0 + lane32;
         const bool live = it < end;
@@ -761,7 +785,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneD
         }
         __syncwarp();
       }
-      __syncthreads();
+      if (WR) __syncwarp(); else __syncthreads();
       pos = end;
     }
   }

@@ -52,9 +52,11 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_x_kernel(const Lan
   uint32_t* rank_s = bad_s + LN_THREADS;
   uint32_t* gid_s = rank_s + LN_THREADS;
   uint32_t* dyn_s = gid_s + LN_THREADS;                                        // CHAIN: [LN_CHAIN_MAX][LN_THREADS]
-  float4* table = reinterpret_cast<float4*>(dyn_s + (CHAIN ? LN_CHAIN_MAX * LN_THREADS : 0));  // [N][PITCH]
-  __shared__ uint32_t s_end;
   const int tid = threadIdx.x, lane32 = tid & 31, warp = tid >> 5;
+  const bool WR = a.warp_runs != 0;  // every warp walks its own runs with a private table (lane.cuh)
+  float4* table = reinterpret_cast<float4*>(dyn_s + (CHAIN ? LN_CHAIN_MAX * LN_THREADS : 0)) +
+                  (WR ? (size_t)warp * N * PITCH : 0);  // [N][PITCH]
+  __shared__ uint32_t s_end;
   const uint32_t wbase = warp * 32;
   const float4* TREE = reinterpret_cast<const float4*>(d.tree);
   uint32_t loaded = 0xffffffffu;
@@ -112,25 +114,45 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_x_kernel(const Lan
   const uint32_t tile_end = min(n_tiles, (blockIdx.x + 1) * tiles_per);
   __syncthreads();
   for (uint32_t tile = blockIdx.x * tiles_per; tile < tile_end; ++tile) {
-    const uint32_t t1 = min(d.n_items, (tile + 1) * a.tile);
+    uint32_t t1 = min(d.n_items, (tile + 1) * a.tile);
     uint32_t pos = tile * a.tile;
+    if (WR) {  // this warp's share of the tile
+      const uint32_t per = ((t1 - pos + LN_WARPS - 1) / LN_WARPS + 31) & ~31u;
+      pos = min(t1, pos + warp * per);
+      t1 = min(t1, pos + per);
+    }
     while (pos < t1) {
       // ---- the run of items [pos, end) that share error set er ----
       const uint32_t er = d.eset[d.first_item + pos];
-      if (tid == 0) s_end = t1;
-      __syncthreads();
-      for (uint32_t i = pos + 1 + tid; i < t1; i += LN_THREADS)
-        if (d.eset[d.first_item + i] != er) { atomicMin(&s_end, i); break; }
-      if (er != loaded) {
-        const float4* src = TREE + (size_t)er * N * NQ;
-        for (uint32_t x = tid; x < N * NQ; x += LN_THREADS) table[(x / NQ) * PITCH + (x % NQ)] = __ldg(src + x);
-        loaded = er;
+      uint32_t end = t1;
+      if (WR) {
+        for (uint32_t i0 = pos + 1; i0 < t1; i0 += 32) {
+          const uint32_t i = i0 + lane32;
+          const unsigned differs = __ballot_sync(0xffffffffu, i < t1 && d.eset[d.first_item + i] != er);
+          if (differs) { end = i0 + __ffs(differs) - 1; break; }
+        }
+        if (er != loaded) {
+          const float4* src = TREE + (size_t)er * N * NQ;
+          for (uint32_t x = lane32; x < N * NQ; x += 32) table[(x / NQ) * PITCH + (x % NQ)] = __ldg(src + x);
+          loaded = er;
+        }
+        __syncwarp();
+      } else {
+        if (tid == 0) s_end = t1;
+        __syncthreads();
+        for (uint32_t i = pos + 1 + tid; i < t1; i += LN_THREADS)
+          if (d.eset[d.first_item + i] != er) { atomicMin(&s_end, i); break; }
+        if (er != loaded) {
+          const float4* src = TREE + (size_t)er * N * NQ;
+          for (uint32_t x = tid; x < N * NQ; x += LN_THREADS) table[(x / NQ) * PITCH + (x % NQ)] = __ldg(src + x);
+          loaded = er;
+        }
+        __syncthreads();
+        end = s_end;
       }
-      __syncthreads();
-      const uint32_t end = s_end;
       const double floor_mass = d.vanish * d.set_mass[er];
 
-      for (uint32_t w0 = pos + wbase; w0 < end; w0 += LN_THREADS) {
+      for (uint32_t w0 = pos + (WR ? 0u : wbase); w0 < end; w0 += (WR ? 32u : (uint32_t)LN_THREADS)) {
         // ---- phase A: this lane's item, every step but the last ----
         const uint32_t it = w0 + lane32;
         const bool live = it < end;
@@ -313,7 +335,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_x_kernel(const Lan
         }
         __syncwarp();
       }
-      __syncthreads();
+      if (WR) __syncwarp(); else __syncthreads();
       pos = end;
     }
   }
