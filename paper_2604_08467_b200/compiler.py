@@ -232,7 +232,7 @@ def compile_stage(
     ceiling: Optional[int] = None,
     mirror: Optional[Sequence[int]] = None,
     fold_from: Optional[int] = None,
-    consumer_layout: bool = False,
+    consumer_layout: int = 0,
     step_order: str = "dfs",
 ) -> tuple[list[Program], tuple]:
     """Compile one stage network + stored path into `n_passes` programs.
@@ -250,9 +250,14 @@ def compile_stage(
     how long intermediates stay alive, i.e. the arena a work item needs (shared memory per item for
     the group kernels, cache footprint for the thread-per-error-set kernel).
 
-    `consumer_layout`: store every record in the order its latest consumer reads it (see "record
-    layout" below).  Off by default: measured on cfg2, contiguous per-item
-    blocks at power-of-two strides are what a lane-per-item kernel reads worst.
+    `consumer_layout`: order in which a record (a tensor handed to a later pass) is stored, chosen
+    from the step of the latest pass that reads it (see "record layout" below).  0: as the path
+    produced it; 1: [slicing bits][contracted][surviving] -- the block one work item reads is
+    contiguous, which suits kernels that serve an item with a group of lanes; 2 (the engine's
+    default): [contracted][surviving][slicing bits] -- element (k, c) of the blocks of ALL prefixes
+    is contiguous, so the 32 work items a warp of a lane-per-item kernel serves, which differ in
+    the slicing bits only, touch a few cache lines per load instead of up to 32.  Measured on cfg2
+    (DESIGN.md section 7): 40.8 ms per step with 0, 50.1 with 1, 37.6 with 2.
 
     `mirror[k]` (optional) names the operand whose value is the complex
     conjugate of operand k under a relabelling (the bra copy of a ket operand,
@@ -409,7 +414,10 @@ def compile_stage(
             surv = [lb for lb in nd.labels if lb in op_labels and lb not in others]
             surv += [lb for lb in op_labels if lb not in others and lb not in surv]
             sliced = [lb for lb in nodes[R].labels if lb not in op_labels]
-            order = sliced + shared + surv
+            # 1: the per-item block contiguous (lane groups read it as rows); 2: the slicing bits fastest, so
+            # the 32 items a warp of a lane-per-item kernel serves find element (k, c) of their 32 different
+            # blocks within a few cache lines
+            order = sliced + shared + surv if consumer_layout == 1 else shared + surv + sliced
             if sorted(map(str, order)) == sorted(map(str, nodes[R].labels)) and len(set(order)) == len(order):
                 _relabel(nodes, virt, view, R, tuple(order))
             break

@@ -657,7 +657,7 @@ class DevicePipeline:
             progs, _ = compiler.compile_stage(ops, path.steps, opens, j, pool, elem,
                                               ceiling=ctx.max_intermediate, mirror=mirror,
                                               fold_from=_fold_from(weights),
-                                              consumer_layout=os.environ.get("PTSBE_RECORD_LAYOUT", "0") == "1")
+                                              consumer_layout=int(os.environ.get("PTSBE_RECORD_LAYOUT", "2")))
             self.stage_flops[j] = [p.flops for p in progs]
             programs += progs
         self.compiled = CompiledPlan(
