@@ -80,6 +80,8 @@ struct ptsbe_plan {
   uint32_t lane_x = 1;                 // lane-per-draw fused descent for Hermitian cuts (lane_x.cuh)
   uint32_t lane_chain = 0;             // ... with the vector-matrix chain served by lane groups (lane_x.cuh CHAIN);
                                        // pays only with PTSBE_RECORD_LAYOUT=1
+  uint32_t tiled_plain = 1;            // CTA-per-item programs without a memo (per-prefix passes of the dense
+                                       // regime, cfg3r1) also run their large steps with register tiles
   uint32_t warp_runs = 1;              // fused descent: a private tree table per warp when error sets bring ...
   uint32_t warp_run_len = 512;         // ... fewer than this many work items each on average (lane.cuh warp_runs)
   uint32_t stage_image = 1;            // lane-group class-0 programs keep their image in shared memory ...
@@ -251,7 +253,7 @@ static ExecLaunch configure_exec(ptsbe_plan* pl, Program& pr, uint32_t n_items) 
                            : gs == 16 ? (L.staged ? exec_kernel<R, 16, false, false, true> : exec_kernel<R, 16, false>)
                            : gs == 32 ? (L.staged ? exec_kernel<R, 32, false, false, true> : exec_kernel<R, 32, false>)
                            : memo     ? (pr.tiled ? exec_kernel<R, 0, true, true> : exec_kernel<R, 0, true>)
-                                      : exec_kernel<R, 0, false>;
+                                      : (pr.tiled && pl->tiled_plain ? exec_kernel<R, 0, false, true> : exec_kernel<R, 0, false>);
   int per_sm;
   if (L.staged) {
     opt_in_smem((const void*)kern, 227 * 1024);
@@ -356,6 +358,7 @@ static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelD
   else if (gs == 32) exec_kernel<R, 32, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
   else if (memo && pr.tiled) exec_kernel<R, 0, true, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
   else if (memo) exec_kernel<R, 0, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  else if (pr.tiled && pl->tiled_plain) exec_kernel<R, 0, false, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
   else exec_kernel<R, 0, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
   g_launches++;
   CK(cudaGetLastError());
@@ -665,8 +668,9 @@ template <int DX, bool CHAIN>
 static void launch_lane_descent_x(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a, uint32_t n_sets) {
   // CHAIN keeps the intermediate vectors in registers: the arena holds only x (DX entries per item)
   if (CHAIN) a.l.e.arena_fast = DX;
+  a.l.ast = 32;  // one lane per item and per draw: every lane stays inside its own arena slice
   const LaneLayout L = lane_layout(a.l.e.n_steps, a.l.n_leaves, a.l.n_table_words, a.l.n_levels,
-                                   a.l.e.arena_fast, a.l.e.words, (uint32_t)sizeof(float2));
+                                   a.l.e.arena_fast, a.l.e.words, (uint32_t)sizeof(float2), a.l.ast);
   constexpr size_t NQ = DX * DX / 4 > 0 ? DX * DX / 4 : 1;
   const size_t table = ((NQ + 1) * 16) << a.d.b;
   const size_t fixed = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4 + (CHAIN ? LN_CHAIN_MAX * 4 : 0));
@@ -1713,6 +1717,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     pl->lane_big_min = (uint32_t)env_size("PTSBE_LANE_BIG_MIN", pl->lane_big_min);
     pl->stage_image = (uint32_t)env_size("PTSBE_STAGE_IMAGE", pl->stage_image);
     pl->warp_runs = (uint32_t)env_size("PTSBE_WARP_RUNS", pl->warp_runs);
+    pl->tiled_plain = (uint32_t)env_size("PTSBE_TILED_PLAIN", pl->tiled_plain);
     pl->warp_run_len = (uint32_t)env_size("PTSBE_WARP_RUN_LEN", pl->warp_run_len);
     pl->stage_image_max = (uint32_t)env_size("PTSBE_STAGE_IMAGE_MAX", pl->stage_image_max);
     pl->lane = (uint32_t)env_size("PTSBE_LANE", pl->lane);

@@ -49,7 +49,7 @@ struct LaneLayout {
 
 __host__ __device__ inline LaneLayout lane_layout(uint32_t n_steps, uint32_t n_leaves, uint32_t n_table_words,
                                                   uint32_t n_levels, uint32_t arena_elems, uint32_t words,
-                                                  uint32_t elem_bytes) {
+                                                  uint32_t elem_bytes, uint32_t ast = LN_AST) {
   LaneLayout L;
   uint32_t o = 0;
   L.steps_off = o;  o += n_steps * STEP_WORDS * 4;
@@ -58,7 +58,7 @@ __host__ __device__ inline LaneLayout lane_layout(uint32_t n_steps, uint32_t n_l
   o = (o + 15) & ~15u;
   L.levels_off = o; o += n_levels * (uint32_t)sizeof(LevelDev);
   o = (o + 15) & ~15u;
-  L.arena_off = o;  o += LN_WARPS * (arena_elems ? arena_elems : 1) * LN_AST * elem_bytes;
+  L.arena_off = o;  o += LN_WARPS * (arena_elems ? arena_elems : 1) * ast * elem_bytes;
   o = (o + 15) & ~15u;
   L.anc_off = o;    o += n_levels * LN_THREADS * 4;
   o = (o + 15) & ~15u;
@@ -207,7 +207,7 @@ __device__ __forceinline__ typename CxT<R>::type lane_element(
 }
 
 // all outputs of a step with KN contracted entries: k-offsets in registers, conjugation folded
-template <typename C, int KN, bool FA, bool FB>
+template <typename C, int KN, bool FA, bool FB, int U = 1>
 __device__ __forceinline__ void lane_step_fixed(const LaneStep& t, const LaneOp<C>& A, const LaneOp<C>& B, C* O,
                                                 uint32_t o_stride, bool store) {
   uint32_t ka[KN], kb[KN];
@@ -247,6 +247,33 @@ __device__ __forceinline__ void lane_step_fixed(const LaneStep& t, const LaneOp<
     }
     return;
   }
+  if constexpr (U > 1 && KN * U <= 16) {
+    // U outputs at a time: all their operand loads are issued before the first multiply-add, so a thread
+    // that waits on global memory (BIG: the arena is not in shared memory) has 2 * KN * U loads in flight
+    // instead of 2 * KN.  Every output is still sum_k in the same order.
+    for (uint32_t ch = 0, c = 0; ch < t.hi_n; ++ch) {
+      const uint32_t ha = t.hi_n > 1 ? t.hiA[ch] : 0u, hb = t.hi_n > 1 ? t.hiB[ch] : 0u;
+      for (uint32_t cl = 0; cl < t.lo_n; cl += U, c += U) {
+        C av[U][KN], bv[U][KN];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t cu = min(cl + u, t.lo_n - 1);
+          const C* pa = A.p + (t.loA[cu] + ha) * A.stride;
+          const C* pb = B.p + (t.loB[cu] + hb) * B.stride;
+#pragma unroll
+          for (int k = 0; k < KN; ++k) { av[u][k] = pa[ka[k]]; bv[u][k] = pb[kb[k]]; }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          C acc; acc.x = 0; acc.y = 0;
+#pragma unroll
+          for (int k = 0; k < KN; ++k) cmac_s<FA, FB>(acc, av[u][k], bv[u][k]);
+          if (store && cl + u < t.lo_n) O[(c + u) * o_stride] = acc;
+        }
+      }
+    }
+    return;
+  }
   for (uint32_t ch = 0, c = 0; ch < t.hi_n; ++ch) {
     const uint32_t ha = t.hi_n > 1 ? t.hiA[ch] : 0u, hb = t.hi_n > 1 ? t.hiB[ch] : 0u;
     for (uint32_t cl = 0; cl < t.lo_n; ++cl, ++c) {
@@ -260,20 +287,22 @@ __device__ __forceinline__ void lane_step_fixed(const LaneStep& t, const LaneOp<
   }
 }
 
-template <typename C, int KN>
+template <typename C, int KN, int U = 1>
 __device__ __forceinline__ void lane_step_kn(const LaneStep& t, const LaneOp<C>& A, const LaneOp<C>& B, C* O,
                                              uint32_t o_stride, bool store) {
   switch (t.flags & 3u) {
-    case 0: lane_step_fixed<C, KN, false, false>(t, A, B, O, o_stride, store); break;
-    case 1: lane_step_fixed<C, KN, true, false>(t, A, B, O, o_stride, store); break;
-    case 2: lane_step_fixed<C, KN, false, true>(t, A, B, O, o_stride, store); break;
-    default: lane_step_fixed<C, KN, true, true>(t, A, B, O, o_stride, store); break;
+    case 0: lane_step_fixed<C, KN, false, false, U>(t, A, B, O, o_stride, store); break;
+    case 1: lane_step_fixed<C, KN, true, false, U>(t, A, B, O, o_stride, store); break;
+    case 2: lane_step_fixed<C, KN, false, true, U>(t, A, B, O, o_stride, store); break;
+    default: lane_step_fixed<C, KN, true, true, U>(t, A, B, O, o_stride, store); break;
   }
 }
 
 struct LaneArgs {
   ExecArgs e;               // program, lists, output (HOIST record or VECTOR row per item)
   uint32_t n_leaves, n_table_words, n_levels;
+  uint32_t ast;             // arena row pitch in elements; 0: LN_AST.  Kernels whose lanes only ever touch their
+                            // own item's slice (lane_x.cuh) run with 32: a fifth less shared memory
 };
 
 // Loads the program image and the level table into shared memory (all threads), returns the context.
@@ -295,11 +324,11 @@ __device__ __forceinline__ LaneCtx<R> lane_setup(const LaneArgs& a, unsigned cha
   cx.leaves = img + L.leaves_off / 4;
   cx.tables = big ? a.e.tables : img + L.tables_off / 4;
   cx.levels = reinterpret_cast<const LevelDev*>(smem + L.levels_off);
-  cx.ast = big ? 32u : (uint32_t)LN_AST;
+  cx.ast = big ? 32u : (a.ast ? a.ast : (uint32_t)LN_AST);
   cx.arena_w = big ? reinterpret_cast<C*>(a.e.spill) +
                          ((size_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5)) * a.e.arena_fast * 32
                    : reinterpret_cast<C*>(smem + L.arena_off) +
-                         (size_t)(threadIdx.x >> 5) * (a.e.arena_fast ? a.e.arena_fast : 1) * LN_AST;
+                         (size_t)(threadIdx.x >> 5) * (a.e.arena_fast ? a.e.arena_fast : 1) * cx.ast;
   cx.anc = reinterpret_cast<const uint32_t*>(smem + L.anc_off);
   cx.pfx = reinterpret_cast<const uint64_t*>(smem + L.pfx_off);
   cx.pool = reinterpret_cast<const C*>(a.e.pool);
@@ -330,7 +359,7 @@ __device__ __forceinline__ uint32_t lane_item_context(const LaneArgs& a, const L
 
 // Runs steps [s0, s1) for the item of this thread.  Outputs of kind 0 go to the private arena;
 // outputs of kind 1 to `rec` (this item's record / vector row) when `live`.
-template <typename R>
+template <typename R, int U = 1>
 __device__ __forceinline__ void lane_run(const LaneCtx<R>& cx, uint32_t s0, uint32_t s1, uint32_t eset,
                                          typename CxT<R>::type* rec, bool live) {
   using C = typename CxT<R>::type;
@@ -350,10 +379,10 @@ __device__ __forceinline__ void lane_run(const LaneCtx<R>& cx, uint32_t s0, uint
       }
     } else {
       switch (t.kn) {
-        case 1: lane_step_kn<C, 1>(t, A, B, O, o_stride, store); break;
-        case 2: lane_step_kn<C, 2>(t, A, B, O, o_stride, store); break;
-        case 4: lane_step_kn<C, 4>(t, A, B, O, o_stride, store); break;
-        case 8: lane_step_kn<C, 8>(t, A, B, O, o_stride, store); break;
+        case 1: lane_step_kn<C, 1, U>(t, A, B, O, o_stride, store); break;
+        case 2: lane_step_kn<C, 2, U>(t, A, B, O, o_stride, store); break;
+        case 4: lane_step_kn<C, 4, U>(t, A, B, O, o_stride, store); break;
+        case 8: lane_step_kn<C, 8, U>(t, A, B, O, o_stride, store); break;
         case 16: lane_step_kn<C, 16>(t, A, B, O, o_stride, store); break;
         default:
           for (uint32_t c = 0; c < t.out_n; ++c) {
@@ -425,7 +454,7 @@ __global__ void __launch_bounds__(LN_THREADS) exec_lane_kernel(const LaneArgs a)
     __syncwarp();
     C* rec = a.e.mode == EXEC_VECTOR ? reinterpret_cast<C*>(a.e.out) + (size_t)it * a.e.vec_row
                                      : reinterpret_cast<C*>(a.e.out) + (size_t)item * a.e.out_elems;
-    lane_run<R>(cx, 0, a.e.n_steps, eset, rec, live);
+    lane_run<R>(cx, 0, a.e.n_steps, eset, rec, live);  // U > 1 (outputs in flight) measured slower: registers
     if constexpr (BIG) {
       if (a.e.mode == EXEC_MARGINAL) {
         // stage-1 marginal pass: the root sits in this lane's arena slice

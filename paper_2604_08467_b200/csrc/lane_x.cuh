@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_x_kernel(const Lan
   const ExecArgs& e = a.l.e;
   const DescentArgs& d = a.d;
   const LaneLayout L = lane_layout(e.n_steps, a.l.n_leaves, a.l.n_table_words, a.l.n_levels, e.arena_fast, e.words,
-                                   (uint32_t)sizeof(C));
+                                   (uint32_t)sizeof(C), a.l.ast ? a.l.ast : (uint32_t)LN_AST);
   const LaneCtx<R> cx = lane_setup<R>(a.l, ln_smem, L);
   const uint32_t N = 1u << d.b;
   double* mass_s = reinterpret_cast<double*>(ln_smem + L.end);                 // [LN_THREADS]
@@ -68,8 +68,8 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_x_kernel(const Lan
     const uint32_t slot = wbase + i;
     LaneOp<C> A, B;
     if constexpr (CHAIN) {
-      A.p = cx.arena_w + i;  // x of the item in warp slot i: element p at [p * LN_AST + i]
-      A.stride = LN_AST;
+      A.p = cx.arena_w + i;  // x of the item in warp slot i: element p at [p * ast + i]
+      A.stride = cx.ast;
     } else {
       lane_operands<R>(cx, last, slot, eset_s[slot], A, B);
     }
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_x_kernel(const Lan
                   else cmac_s<false, false>(acc, m, v);
                 }
             }
-            cx.arena_w[c * LN_AST + i] = acc;
+            cx.arena_w[c * cx.ast + i] = acc;
           }
           __syncwarp();
         } else {
