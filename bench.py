@@ -771,8 +771,8 @@ def main():
             launches_j = sum(int(s.marg_launches[j]) for s in stats)
             d_items = sum(int(s.descent_items[j]) for s in stats)
             if pr.proj_d and d_items and marg[j] == 0.0:
-                # fused lane_descent_kernel (csrc/lane.cuh): per-item steps (thread per item) + per-qubit
-                # descent (8 lanes per draw); v never leaves the SM.  HBM traffic of one work item: its
+                # fused descent kernels (csrc/lane.cuh, lane_x.cuh): per-item steps (thread per item) + per-qubit
+                # descent (4 lanes or 1 lane per draw); v never leaves the SM.  HBM traffic of one work item: its
                 # list entry (eset, parent, mult, slot_off, rank, id, prefix words), one (index, count)
                 # pair per draw, nnz; plus, amortised, every record of an earlier pass and every tree
                 # column once per launch.
@@ -784,8 +784,13 @@ def main():
                 tree_bytes = float(sets * args.steps) * pr.proj_d * elem * (1 << b_j)
                 per_item = 24 + 8 * words + 4 + 8.0 * shots_j / max(d_items, 1) + (rec_bytes + tree_bytes) / max(d_items, 1)
                 flops_item = 8.0 * pr.flops * (1.0 + shots_j / max(d_items, 1)) + 4.0 * pr.proj_d * (b_j + 1) * shots_j / max(d_items, 1)
-                cands.append((desc[j], f"lane_descent_kernel (per-item steps + per-qubit descent fused, D={pr.proj_d}, b={b_j}), stage {j + 1}",
-                              d_items, launches_j, per_item, flops_item, "lane_descent_kernel"))
+                # Hermitian cuts with 4 or 8 complex entries in complex64 are served by lane_descent_x_kernel
+                # (csrc/lane_x.cuh: one lane per draw), everything else by lane_descent_kernel (4 lanes per draw)
+                herm_x = dtype == "complex64" and pr.proj_d in (16, 64)
+                kname = "lane_descent_x_kernel" if herm_x else "lane_descent_kernel"
+                cands.append((desc[j], f"{kname} (per-item steps + per-qubit descent fused, D={pr.proj_d}, b={b_j}), stage {j + 1}, "
+                                       "incl. the per-error-set tree tables and the dedup of raw draws",
+                              d_items, launches_j, per_item, flops_item, kname))
             elif pr.proj_d and d_items:
                 # per-item steps, vector written as one row per item
                 cands.append((marg[j], f"exec_kernel (per-item steps -> v[{pr.proj_d}]), stage {j + 1}", n_items, launches_j,
