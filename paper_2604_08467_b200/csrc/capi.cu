@@ -80,6 +80,8 @@ struct ptsbe_plan {
   uint32_t lane_x = 1;                 // lane-per-draw fused descent for Hermitian cuts (lane_x.cuh)
   uint32_t lane_chain = 0;             // ... with the vector-matrix chain served by lane groups (lane_x.cuh CHAIN);
                                        // pays only with PTSBE_RECORD_LAYOUT=1
+  uint32_t tc_steps = 0;               // opt-in (slower): large separable steps of CTA-per-item programs on tcgen05
+                                       // tensor cores (executor.cuh tc_step, TF32 x3)
   uint32_t tiled_plain = 1;            // CTA-per-item programs without a memo (per-prefix passes of the dense
                                        // regime, cfg3r1) also run their large steps with register tiles
   uint32_t warp_runs = 1;              // fused descent: a private tree table per warp when error sets bring ...
@@ -206,7 +208,22 @@ struct ExecLaunch {
   uint32_t item_bytes;
   uint32_t groups_per_block;
   bool staged = false;  // lane-group program with its image in shared memory (executor.cuh STAGED)
+  bool tc = false;      // large separable steps on the tensor cores (executor.cuh TC)
+  uint32_t tc_off = 0;
+  void (*kern)(ExecArgs) = nullptr;
 };
+
+template <typename R>
+static void (*pick_exec_kernel(uint32_t gs, bool memo, bool tiled, bool staged, bool tc))(ExecArgs) {
+  if (gs == 8) return staged ? exec_kernel<R, 8, false, false, true> : exec_kernel<R, 8, false>;
+  if (gs == 16) return staged ? exec_kernel<R, 16, false, false, true> : exec_kernel<R, 16, false>;
+  if (gs == 32) return staged ? exec_kernel<R, 32, false, false, true> : exec_kernel<R, 32, false>;
+  if constexpr (sizeof(R) == 4) {
+    if (tc && tiled) return memo ? exec_kernel<R, 0, true, true, false, true> : exec_kernel<R, 0, false, true, false, true>;
+  }
+  if (memo) return tiled ? exec_kernel<R, 0, true, true> : exec_kernel<R, 0, true>;
+  return tiled ? exec_kernel<R, 0, false, true> : exec_kernel<R, 0, false>;
+}
 
 template <typename R>
 static ExecLaunch configure_exec(ptsbe_plan* pl, Program& pr, uint32_t n_items) {
@@ -247,13 +264,16 @@ static ExecLaunch configure_exec(ptsbe_plan* pl, Program& pr, uint32_t n_items) 
     L.desc_off = (uint32_t)L.smem;
     L.smem += image;
   }
+  const bool tiled = pr.tiled && (memo || pl->tiled_plain);
+  L.tc = !warp && tiled && pl->tc_steps && sizeof(R) == 4;
+  if (L.tc) {  // operand tiles, mbarrier and TMEM slot of the tensor-core steps
+    L.tc_off = (uint32_t)L.smem;
+    L.smem += TCS_BYTES;
+  }
   if (L.smem > 227 * 1024)
     throw Failure(PTSBE_ERESOURCE, "stage program needs more shared memory than one SM has");
-  void (*kern)(ExecArgs) = gs == 8    ? (L.staged ? exec_kernel<R, 8, false, false, true> : exec_kernel<R, 8, false>)
-                           : gs == 16 ? (L.staged ? exec_kernel<R, 16, false, false, true> : exec_kernel<R, 16, false>)
-                           : gs == 32 ? (L.staged ? exec_kernel<R, 32, false, false, true> : exec_kernel<R, 32, false>)
-                           : memo     ? (pr.tiled ? exec_kernel<R, 0, true, true> : exec_kernel<R, 0, true>)
-                                      : (pr.tiled && pl->tiled_plain ? exec_kernel<R, 0, false, true> : exec_kernel<R, 0, false>);
+  void (*kern)(ExecArgs) = pick_exec_kernel<R>(gs, memo, tiled, L.staged, L.tc);
+  L.kern = kern;
   int per_sm;
   if (L.staged) {
     opt_in_smem((const void*)kern, 227 * 1024);
@@ -349,17 +369,8 @@ static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelD
   a.n_memo_sites = pr.d.n_memo_sites;
   a.n_leaves = pr.d.n_leaves;
   a.n_table_words = pr.d.n_table_words;
-  const uint32_t gs = pr.d.threads_per_item;
-  if (L.staged && gs == 8) exec_kernel<R, 8, false, false, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
-  else if (L.staged && gs == 16) exec_kernel<R, 16, false, false, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
-  else if (L.staged && gs == 32) exec_kernel<R, 32, false, false, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
-  else if (gs == 8) exec_kernel<R, 8, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
-  else if (gs == 16) exec_kernel<R, 16, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
-  else if (gs == 32) exec_kernel<R, 32, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
-  else if (memo && pr.tiled) exec_kernel<R, 0, true, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
-  else if (memo) exec_kernel<R, 0, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
-  else if (pr.tiled && pl->tiled_plain) exec_kernel<R, 0, false, true><<<L.grid, L.block, L.smem, pl->stream>>>(a);
-  else exec_kernel<R, 0, false><<<L.grid, L.block, L.smem, pl->stream>>>(a);
+  a.tc_off = L.tc_off;
+  L.kern<<<L.grid, L.block, L.smem, pl->stream>>>(a);
   g_launches++;
   CK(cudaGetLastError());
 }
@@ -1718,6 +1729,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     pl->stage_image = (uint32_t)env_size("PTSBE_STAGE_IMAGE", pl->stage_image);
     pl->warp_runs = (uint32_t)env_size("PTSBE_WARP_RUNS", pl->warp_runs);
     pl->tiled_plain = (uint32_t)env_size("PTSBE_TILED_PLAIN", pl->tiled_plain);
+    pl->tc_steps = (uint32_t)env_size("PTSBE_TC_STEPS", pl->tc_steps);
     pl->warp_run_len = (uint32_t)env_size("PTSBE_WARP_RUN_LEN", pl->warp_run_len);
     pl->stage_image_max = (uint32_t)env_size("PTSBE_STAGE_IMAGE_MAX", pl->stage_image_max);
     pl->lane = (uint32_t)env_size("PTSBE_LANE", pl->lane);

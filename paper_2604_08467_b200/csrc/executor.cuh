@@ -16,6 +16,7 @@
 // _contract_marginal (engine.py:442-450).
 #pragma once
 #include "common.cuh"
+#include "project_tc.cuh"  // tcgen05 / mbarrier PTX wrappers, TF32 split
 
 namespace ptsbe {
 
@@ -80,6 +81,7 @@ struct ExecArgs {
   uint32_t desc_off;   // byte offset of the staging area from the dynamic shared-memory base
   uint32_t desc_cap;   // steps it holds (0: none)
   uint32_t n_leaves, n_table_words;  // STAGED: the whole program image goes to the staging area
+  uint32_t tc_off;     // TC: byte offset of the tensor-core tiles (TCS_BYTES) from the dynamic shared-memory base
 };
 
 constexpr uint32_t DESC_CAP = 192;  // staged step descriptors per CTA (x 80 bytes)
@@ -194,6 +196,154 @@ __device__ __forceinline__ void tiled_step(const C* __restrict__ A, const C* __r
   }
 }
 
+// ---------------------------------------------------------------------------
+// Large separable steps on the 5th-generation tensor cores (complex64, CTA-per-item programs).
+//
+// The same step as tiled_step -- out[oA[a] + oB[b]] = sum_k A[aOff[a] + kA[k]] * B[bOff[b] + kB[k]], the
+// np.tensordot of reference tensor.py:190-216 -- written as a REAL product D[M x 2N] = A'[M x 2K] B'[2N x 2K]^T:
+//     A'[a][2k] = Re A, A'[a][2k+1] = Im A;   B'[2b][2k] = Re B, B'[2b][2k+1] = -Im B  (real part of out),
+//                                             B'[2b+1][2k] = Im B, B'[2b+1][2k+1] = Re B (imaginary part),
+// so a row of D is the row of complex outputs, interleaved.  Operands are gather-addressed per error set, so
+// there is no TMA: all 256 threads gather, split x = hi + lo on the TF32 mantissa (project_tc.cuh) and store
+// 16-byte chunks into K-major tiles with the 128-byte swizzle the UMMA descriptors of project_tc.cuh expect
+// (chunk j of row r at (r / 8) * 1024 + (r % 8) * 128 + ((j ^ (r % 8)) * 16)); one thread issues
+// tcgen05.mma.kind::tf32 (M = 128, N' <= 64, K = 8) for hi*hi + hi*lo, the A tile is overwritten with its lo
+// part for lo*hi (one A buffer: shared memory decides how many CTAs stay resident), the accumulator lives in
+// TMEM and comes back with tcgen05.ld, thread = output row.  3 x TF32 keeps ~2^-21 per product.
+constexpr uint32_t TCS_A_BYTES = 128 * 128;      // 128 rows x 32 floats
+constexpr uint32_t TCS_NP = 64;                  // real output columns per pass (32 complex)
+constexpr uint32_t TCS_B_BYTES = TCS_NP * 128;
+constexpr uint32_t TCS_BYTES = TCS_A_BYTES + 2 * TCS_B_BYTES + 1024 /* alignment */ + 64 /* mbarrier, TMEM slot */;
+constexpr uint32_t TCS_TMEM_COLS = 64;
+
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct TcStepCtx {
+  unsigned char* tiles;   // 1024-byte aligned: A | B_hi | B_lo
+  uint32_t bar;           // shared-memory address of the mbarrier (count 1)
+  uint32_t tmem;          // TMEM base of this CTA's TCS_TMEM_COLS columns
+  uint32_t phase;         // parity of the next barrier completion (uniform over the CTA)
+};
+
+__device__ __forceinline__ uint32_t tcs_swz(uint32_t r, uint32_t j) {
+  return (r >> 3) * 1024u + (r & 7u) * 128u + ((j ^ (r & 7u)) << 4);
+}
+
+// CTA-wide; every thread of the 256 must call it (barriers inside)
+__device__ __forceinline__ void tc_step(TcStepCtx& cx, const float2* __restrict__ A, const float2* __restrict__ B,
+                                        float2* O, const uint32_t* __restrict__ g, uint32_t M, uint32_t N,
+                                        const uint32_t* __restrict__ kA, const uint32_t* __restrict__ kB, uint32_t kn,
+                                        bool fa, bool fb, int tid, bool store) {
+  const uint32_t *aOff = g, *bOff = g + M, *oA = g + M + N, *oB = g + 2 * M + N;
+  unsigned char* a_tile = cx.tiles;
+  unsigned char* bh_tile = cx.tiles + TCS_A_BYTES;
+  unsigned char* bl_tile = bh_tile + TCS_B_BYTES;
+  const uint32_t a_s = tc_smem(a_tile), bh_s = tc_smem(bh_tile), bl_s = tc_smem(bl_tile);
+  const uint32_t kblocks = (kn + 15) / 16;
+  const int warp = tid >> 5, lane = tid & 31;
+  for (uint32_t m0 = 0; m0 < M; m0 += 128) {
+    for (uint32_t n0 = 0; n0 < N; n0 += TCS_NP / 2) {
+      const uint32_t np = min(TCS_NP / 2, N - n0);                 // complex columns of this pass
+      const uint32_t nprime = max(16u, 2u * ((np + 7u) & ~7u));    // UMMA N: multiple of 16
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((nprime >> 3) << 17) | ((128u >> 4) << 24);
+      for (uint32_t kb = 0; kb < kblocks; ++kb) {
+        // ---- gather + split: A (hi to the tile, lo kept in registers), B (hi and lo tiles) ----
+        float4 alo[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t idx = tid + 256 * i, r = idx >> 3, j = idx & 7, k0 = kb * 16 + 2 * j;
+          const uint32_t row = m0 + r;
+          float2 x0 = make_float2(0.f, 0.f), x1 = x0;
+          if (row < M) {
+            const uint32_t ao = __ldg(aOff + row);
+            if (k0 < kn) x0 = A[ao + __ldg(kA + k0)];
+            if (k0 + 1 < kn) x1 = A[ao + __ldg(kA + k0 + 1)];
+          }
+          if (fa) { x0.y = -x0.y; x1.y = -x1.y; }
+          float4 h, l;
+          tc_split(x0.x, h.x, l.x); tc_split(x0.y, h.y, l.y); tc_split(x1.x, h.z, l.z); tc_split(x1.y, h.w, l.w);
+          *reinterpret_cast<float4*>(a_tile + tcs_swz(r, j)) = h;
+          alo[i] = l;
+        }
+        for (uint32_t idx = tid; idx < nprime * 8; idx += 256) {
+          const uint32_t r = idx >> 3, j = idx & 7, k0 = kb * 16 + 2 * j, b = r >> 1;
+          float2 y0 = make_float2(0.f, 0.f), y1 = y0;
+          if (b < np) {
+            const uint32_t bo = __ldg(bOff + n0 + b);
+            if (k0 < kn) y0 = B[bo + __ldg(kB + k0)];
+            if (k0 + 1 < kn) y1 = B[bo + __ldg(kB + k0 + 1)];
+          }
+          if (fb) { y0.y = -y0.y; y1.y = -y1.y; }
+          float4 v;
+          if (r & 1u) v = make_float4(y0.y, y0.x, y1.y, y1.x);      // imaginary part of the output
+          else v = make_float4(y0.x, -y0.y, y1.x, -y1.y);           // real part
+          float4 h, l;
+          tc_split(v.x, h.x, l.x); tc_split(v.y, h.y, l.y); tc_split(v.z, h.z, l.z); tc_split(v.w, h.w, l.w);
+          *reinterpret_cast<float4*>(bh_tile + tcs_swz(r, j)) = h;
+          *reinterpret_cast<float4*>(bl_tile + tcs_swz(r, j)) = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
+        __syncthreads();
+        const uint32_t ksteps = min(4u, (2u * kn - kb * 32u + 7u) / 8u);
+        if (tid == 0) {
+          tc_fence_after();
+          for (uint32_t k = 0; k < ksteps; ++k) {
+            tc_mma_tf32(cx.tmem, tc_desc(a_s + k * 32), tc_desc(bh_s + k * 32), idesc, (kb | k) ? 1u : 0u);
+            tc_mma_tf32(cx.tmem, tc_desc(a_s + k * 32), tc_desc(bl_s + k * 32), idesc, 1u);
+          }
+          tc_commit(cx.bar);
+        }
+        mbar_wait(cx.bar, cx.phase);
+        cx.phase ^= 1u;
+        // ---- A_lo over the same buffer, times B_hi ----
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t idx = tid + 256 * i;
+          *reinterpret_cast<float4*>(a_tile + tcs_swz(idx >> 3, idx & 7)) = alo[i];
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+          tc_fence_after();
+          for (uint32_t k = 0; k < ksteps; ++k)
+            tc_mma_tf32(cx.tmem, tc_desc(a_s + k * 32), tc_desc(bh_s + k * 32), idesc, 1u);
+          tc_commit(cx.bar);
+        }
+        mbar_wait(cx.bar, cx.phase);
+        cx.phase ^= 1u;
+      }
+      // ---- accumulator -> registers -> out: thread = row (TMEM lane), warps 0-3 = lane quadrants ----
+      tc_fence_after();
+      if (warp < 4) {
+        const uint32_t row = m0 + 32 * warp + lane;
+        const uint32_t oa = row < M ? __ldg(oA + row) : 0u;
+        for (uint32_t c0 = 0; c0 < nprime; c0 += 16) {
+          uint32_t r[16];
+          tc_ld16(cx.tmem + ((32u * warp) << 16) + c0, r);
+          if (store && row < M) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const uint32_t b = c0 / 2 + q;
+              if (b < np) O[oa + __ldg(oB + n0 + b)] = make_float2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncthreads();  // accumulator and tiles free for the next pass; outputs visible to the CTA
+    }
+  }
+}
+
 // GS > 0 : sub-warp mapping, GS lanes per item, 32 / GS items per warp, __syncwarp between steps
 // GS == 0: one CTA per item, __syncthreads between steps
 // MEMO    : (GS == 0 only) class-0 program with a variant-0 memo.  UPV leaves every tensor of the
@@ -206,8 +356,9 @@ __device__ __forceinline__ void tiled_step(const C* __restrict__ A, const C* __r
 //           once per CTA.  A step of a lane-group program is a chain of dependent reads (descriptor ->
 //           tables -> leaf row -> Kraus index -> operand); from global memory that chain costs ~2000
 //           cycles per step, which is all there is when a batch holds few error sets (cfg5 at E <= 10^4).
-template <typename R, int GS, bool MEMO, bool TILED = false, bool STAGED = false>
-__global__ void __launch_bounds__(256, TILED ? 3 : 5) exec_kernel(const ExecArgs a) {
+// TC      : (GS == 0, TILED, complex64) large separable steps on the tensor cores (tc_step above)
+template <typename R, int GS, bool MEMO, bool TILED = false, bool STAGED = false, bool TC = false>
+__global__ void __launch_bounds__(256, TILED ? (TC ? 2 : 3) : 5) exec_kernel(const ExecArgs a) {
   using C = typename CxT<R>::type;
   constexpr bool WARP = GS > 0;
   constexpr int GSD = GS > 0 ? GS : 1;
@@ -258,6 +409,30 @@ __global__ void __launch_bounds__(256, TILED ? 3 : 5) exec_kernel(const ExecArgs
     n_staged = min(a.n_steps, a.desc_cap);
     for (uint32_t i = threadIdx.x; i < n_staged * STEP_WORDS; i += blockDim.x) desc_s[i] = __ldg(a.steps + i);
     __syncthreads();
+  }
+
+  TcStepCtx tcx;
+  tcx.tiles = nullptr; tcx.bar = 0; tcx.tmem = 0; tcx.phase = 0;
+  if constexpr (TC) {
+    unsigned char* raw = smem_raw + a.tc_off;
+    tcx.tiles = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(tcx.tiles + TCS_A_BYTES + 2 * TCS_B_BYTES);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+    tcx.bar = tc_smem(bar);
+    if (threadIdx.x == 0) {
+      mbar_init(tcx.bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (threadIdx.x < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_smem(slot)),
+                   "r"(TCS_TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    tcx.tmem = *slot;
   }
 
   auto group_sync = [&]() {
@@ -462,6 +637,13 @@ __global__ void __launch_bounds__(256, TILED ? 3 : 5) exec_kernel(const ExecArgs
         const C* src = memo + own_memo;
         for (uint32_t c = tid; c < t.out_n; c += gsize)
           if (store) O[(size_t)c * o_stride] = src[c];
+      } else if (TC && TILED && o_stride == 1 && s4.y >= 64 && s4.z >= 4 && kn >= 4 &&
+                 (uint64_t)s4.y * s4.z * kn >= 16384) {
+        // large step on the tensor cores
+        if constexpr (TC)
+          tc_step(tcx, reinterpret_cast<const float2*>(A), reinterpret_cast<const float2*>(B),
+                  reinterpret_cast<float2*>(O), a.tables + s4.x, s4.y, s4.z, t.kA, t.kB, kn, (t.conj & 1u) != 0,
+                  (t.conj & 2u) != 0, tid, store);
       } else if (TILED && o_stride == 1 && s4.y != 0) {
         // large step: separable form with register tiles
         const uint32_t* gt = a.tables + s4.x;
@@ -553,6 +735,14 @@ __global__ void __launch_bounds__(256, TILED ? 3 : 5) exec_kernel(const ExecArgs
       }
     }
     group_sync();
+  }
+  if constexpr (TC) {
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tcx.tmem), "r"(TCS_TMEM_COLS) : "memory");
+    }
   }
 }
 

@@ -161,3 +161,46 @@ def test_fullsize_records_bit_exact_vs_vendored_reference(name):
             assert [(strings[i], int(counts[i])) for i in sel] == [tuple(r) for r in ref["records"][e]], (name, e)
     finally:
         pipe.close()
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3r1"])
+def test_tensor_core_steps_keep_complex64_within_tolerance(monkeypatch, name):
+    """Opt-in tcgen05 path for the large separable steps of CTA-per-item programs
+    (csrc/executor.cuh tc_step: TF32 x3 split, accumulators in TMEM; PTSBE_TC_STEPS=1): the
+    complex64 conditional marginals of every stage stay within 1e-5 of the complex128 device
+    marginals (which the tests above hold to the oracle at 1e-11) -- the arithmetic being replaced is
+    the np.tensordot of reference tensor.py:190-216."""
+    c, sizes, shots = _workload(name)
+    sets = 3 if name == "cfg2" else 2
+    rows = _error_rows(name, c, sets)
+    ids = np.arange(sets, dtype=np.uint32)
+    tpl = CircuitNetwork.from_circuit(c)
+    tables = VariantTables.from_channels(tpl)
+    plan = BatchPlan(sizes)
+    p128 = DevicePipeline(tpl, plan, tables, SamplerContext(hypersamples=16, dtype="complex128"), shots_per_set=float(shots))
+    monkeypatch.setenv("PTSBE_TC_STEPS", "1")
+    p64 = DevicePipeline(tpl, plan, tables, SamplerContext(hypersamples=16, dtype="complex64"), shots_per_set=float(shots))
+    try:
+        keys, esets, counts, st = p128.device_plan.sample(rows, np.full(sets, shots, np.uint32), ids, 5, merged=False)
+        strings = unpack_keys(keys, plan.n)
+        tiled = 0
+        for j in range(1, plan.f + 1):
+            off = plan.offset(j)
+            work = []
+            for e in range(sets):
+                seen = sorted({strings[i][:off] for i in np.flatnonzero(esets == e)})
+                for pfx in (seen[:1] + seen[-1:]) if off else [""]:
+                    work.append((e, pfx))
+            kr = rows[[e for e, _ in work]]
+            pf = pack_prefixes([p for _, p in work], plan.n)
+            ref, ref_m, _ = p128.device_plan.marginals(j, kr, pf)
+            got, got_m, _ = p64.device_plan.marginals(j, kr, pf)
+            ref = ref / ref_m[:, None]
+            err = np.max(np.abs(got / got_m[:, None] - ref), axis=1) / np.max(ref, axis=1)
+            assert err.max() <= 1e-5, (name, j, err.max())
+            assert np.max(np.abs(got_m / ref_m - 1.0)) <= 1e-4, (name, j)
+            tiled += sum(1 for p in p64.programs_of(j) if p.threads > 32 and p.flops >= 1.5e5)
+        assert tiled >= 1, "no program of this case has steps large enough for the tensor-core path"
+    finally:
+        p128.close()
+        p64.close()
