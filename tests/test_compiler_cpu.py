@@ -235,3 +235,56 @@ def test_separable_form_tables_match_the_gather_tables():
             np.testing.assert_array_equal(b_plain[out], b_gemm)
             checked += 1
     assert checked >= 1
+
+
+@pytest.mark.parametrize("layout,fold", [("0", "0"), ("1", "0"), ("2", "2"), ("1", "2")])
+@pytest.mark.parametrize("name", ["random10x40", "hea8", "surface_d3_r1"])
+def test_record_layout_and_hoist_folding_do_not_change_values(monkeypatch, golden_cases, name, layout, fold):
+    """The compiler may store a record in any label order (consumer layout 0 / 1 / 2) and may evaluate
+    a prefix class with the per-item class instead of in a hoist pass of its own (fold): the programs
+    must still reproduce the reference's golden marginals (reference engine.py:361-450)."""
+    monkeypatch.setenv("PTSBE_RECORD_LAYOUT", layout)
+    monkeypatch.setenv("PTSBE_FOLD", fold)
+    case = golden_cases[name]
+    pipe, tables, es = _pipeline(case, hypersamples=8)
+    idx = tables.encode(es)
+    for row in case["marginals"]:
+        j = row["stage"]
+        bits = [int(ch) for ch in row["prefix"]] + [0] * (pipe.plan.n - len(row["prefix"]))
+        rec = emulator.run_stage(pipe.programs_of(j), pipe.compiled.pool, idx[row["eset"]], bits)
+        probs = np.clip(rec.real, 0, None)
+        np.testing.assert_allclose(probs / probs.sum(), np.asarray(row["probs"]), rtol=0, atol=1e-11)
+
+
+def test_depth_first_step_order_is_topological_and_shrinks_arenas(golden_cases):
+    """compile_stage replays the steps of a pass depth first (larger live footprint first): same nodes,
+    same values, a smaller or equal arena than in stored-path order."""
+    case = golden_cases["random10x40"]
+    c, sizes, es = case_objects(case)
+    tpl = CircuitNetwork.from_circuit(c)
+    tables = VariantTables.from_errorsets(tpl, es)
+    from paper_2604_08467_b200.engine import stage_operands
+    from paper_2604_08467_b200.planner import plan_stage
+    from paper_2604_08467_b200.compiler import SEL_PREFIX, Pool, compile_stage
+    plan = BatchPlan(sizes)
+    total = {"dfs": 0, "path": 0}
+    for j in range(1, plan.f + 1):
+        ops, opens, mirror = stage_operands(tpl, plan, j, tables, split=True)
+        path = plan_stage([o.labels for o in ops], [o.dims for o in ops], [o.cls for o in ops],
+                          [o.sel_kind == SEL_PREFIX for o in ops], opens, [1.0] + [100.0] * (j - 1), 26.0, 26.0,
+                          op_mirror=mirror, hypersamples=4, rng=np.random.default_rng(3))
+        progs = {}
+        for order in ("dfs", "path"):
+            progs[order], _ = compile_stage(ops, path.steps, opens, j, Pool(), 16, mirror=mirror, step_order=order)
+            total[order] += sum(p.arena_fast + p.arena_spill for p in progs[order])
+        for a, b in zip(progs["dfs"], progs["path"]):
+            assert len(a.steps) == len(b.steps) and a.flops == b.flops and a.out_elems == b.out_elems
+            # every operand of a step is a leaf, a record or the output of an EARLIER step of the program
+            produced = set()
+            for st in a.steps:
+                for kind, ref in ((int(st[0]), int(st[1])), (int(st[2]), int(st[3]))):
+                    if kind == 0:
+                        assert any(lo <= ref < hi for lo, hi in produced), "arena operand read before it is written"
+                if int(st[4]) == 0:
+                    produced.add((int(st[5]), int(st[5]) + int(st[6])))
+    assert total["dfs"] <= total["path"]

@@ -438,6 +438,35 @@ def test_thread_per_error_set_hoist_equals_group_executor(monkeypatch, dtype):
         assert big == want
 
 
+@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+def test_warp_private_descent_tables_and_staged_image_equal_the_cta_paths(monkeypatch, dtype):
+    """Short runs of work items per error set: the fused descent kernels give every warp its own
+    copy of the tree table (csrc/lane.cuh warp_runs) and lane-group class-0 programs keep their
+    image in shared memory (csrc/executor.cuh STAGED).  Both are scheduling choices: the records
+    equal those of the one-error-set-per-CTA kernels with the image in global memory, in both
+    dtypes, and the oracle's in complex128 (reference engine.py:493-524)."""
+    c, _ = workloads.random40(14, 70, seed=3)
+    sizes = (5, 5, 4)
+    tpl = CircuitNetwork.from_circuit(c)
+    es = presample_errors(c, 300, "uniform", shots_per_set=20, rng=np.random.default_rng(12))
+
+    def run(on):
+        monkeypatch.setenv("PTSBE_WARP_RUNS", "1" if on else "0")
+        monkeypatch.setenv("PTSBE_STAGE_IMAGE", "1" if on else "0")
+        monkeypatch.setenv("PTSBE_DESCENT_MULT", "1e18")
+        ctx = SamplerContext(hypersamples=8, dtype=dtype)
+        out = sample_proportional_batched(tpl, es, BatchPlan(sizes), 23, ctx)
+        assert sum(ctx.stats.descent_events.values()) > 0
+        return [[(r.bitstring, r.count) for r in recs] for recs in out]
+
+    fast, plain = run(True), run(False)
+    assert fast == plain
+    if dtype == "complex128":
+        ops, finals = bridge.template_of(c)
+        _, want, _ = O.run_proportional(ops, finals, sizes, bridge.oracle_errorsets(c, es), 23)
+        assert fast == want
+
+
 def test_many_error_sets_single_shot_descent():
     """More error sets than a grid dimension holds (tree_build puts them on
     grid.x), one shot each: every shot is sampled and the histogram total is exact."""
