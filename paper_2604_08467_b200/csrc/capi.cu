@@ -80,6 +80,8 @@ struct ptsbe_plan {
   uint32_t lane_x = 1;                 // lane-per-draw fused descent for Hermitian cuts (lane_x.cuh)
   uint32_t lane_chain = 0;             // ... with the vector-matrix chain served by lane groups (lane_x.cuh CHAIN);
                                        // pays only with PTSBE_RECORD_LAYOUT=1
+  uint32_t tile_min = 128;             // CTA-per-item programs: 4 x 4 register tiles for separable steps with at
+                                       // least this many tiles, 2 x 2 below (keeps the CTA busy on mid-size steps)
   uint32_t tc_steps = 0;               // opt-in (slower): large separable steps of CTA-per-item programs on tcgen05
                                        // tensor cores (executor.cuh tc_step, TF32 x3)
   uint32_t tiled_plain = 1;            // CTA-per-item programs without a memo (per-prefix passes of the dense
@@ -370,6 +372,7 @@ static void launch_exec(ptsbe_plan* pl, Program& pr, uint32_t mode, const LevelD
   a.n_leaves = pr.d.n_leaves;
   a.n_table_words = pr.d.n_table_words;
   a.tc_off = L.tc_off;
+  a.tile_min = pl->tile_min;
   L.kern<<<L.grid, L.block, L.smem, pl->stream>>>(a);
   g_launches++;
   CK(cudaGetLastError());
@@ -1730,6 +1733,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     pl->warp_runs = (uint32_t)env_size("PTSBE_WARP_RUNS", pl->warp_runs);
     pl->tiled_plain = (uint32_t)env_size("PTSBE_TILED_PLAIN", pl->tiled_plain);
     pl->tc_steps = (uint32_t)env_size("PTSBE_TC_STEPS", pl->tc_steps);
+    pl->tile_min = (uint32_t)env_size("PTSBE_TILE_MIN", pl->tile_min);
     pl->warp_run_len = (uint32_t)env_size("PTSBE_WARP_RUN_LEN", pl->warp_run_len);
     pl->stage_image_max = (uint32_t)env_size("PTSBE_STAGE_IMAGE_MAX", pl->stage_image_max);
     pl->lane = (uint32_t)env_size("PTSBE_LANE", pl->lane);

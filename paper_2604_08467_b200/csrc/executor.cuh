@@ -81,6 +81,7 @@ struct ExecArgs {
   uint32_t desc_off;   // byte offset of the staging area from the dynamic shared-memory base
   uint32_t desc_cap;   // steps it holds (0: none)
   uint32_t n_leaves, n_table_words;  // STAGED: the whole program image goes to the staging area
+  uint32_t tile_min;   // TILED: 4 x 4 register tiles for steps with at least this many of them, 2 x 2 below
   uint32_t tc_off;     // TC: byte offset of the tensor-core tiles (TCS_BYTES) from the dynamic shared-memory base
 };
 
@@ -151,12 +152,11 @@ __device__ __forceinline__ void step_fixed_k(const C* __restrict__ A, const C* _
 // feeds TN (or TM) multiply-adds instead of one; neighbouring threads share the tile row (their A
 // loads are shared-memory broadcasts).  The k order of every output is that of the plain form,
 // so the values are bit-identical.
-template <typename C, bool FA, bool FB>
+template <typename C, bool FA, bool FB, int TM = 4, int TN = 4>
 __device__ __forceinline__ void tiled_step(const C* __restrict__ A, const C* __restrict__ B, C* O,
                                            const uint32_t* __restrict__ g, uint32_t M, uint32_t N,
                                            const uint32_t* __restrict__ kA, const uint32_t* __restrict__ kB,
                                            uint32_t kn, int tid, int nthreads, bool store) {
-  constexpr int TM = 4, TN = 4;
   const uint32_t *aOff = g, *bOff = g + M, *oA = g + M + N, *oB = g + 2 * M + N;
   const uint32_t tn = (N + TN - 1) / TN, tm = (M + TM - 1) / TM;
   for (uint32_t tile = tid; tile < tm * tn; tile += nthreads) {
@@ -647,11 +647,22 @@ __global__ void __launch_bounds__(256, TILED ? (TC ? 2 : 3) : 5) exec_kernel(con
       } else if (TILED && o_stride == 1 && s4.y != 0) {
         // large step: separable form with register tiles
         const uint32_t* gt = a.tables + s4.x;
-        switch (t.conj & 3u) {
-          case 0: tiled_step<C, false, false>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
-          case 1: tiled_step<C, true, false>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
-          case 2: tiled_step<C, false, true>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
-          default: tiled_step<C, true, true>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
+        // 4 x 4 tiles when they keep most of the CTA busy; steps of a few hundred outputs (2-32 k MACs, K up
+        // to 64) would otherwise run on one or two warps while the rest waits at the barrier: 2 x 2 tiles
+        if (((s4.y + 3) / 4) * ((s4.z + 3) / 4) >= a.tile_min) {
+          switch (t.conj & 3u) {
+            case 0: tiled_step<C, false, false>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
+            case 1: tiled_step<C, true, false>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
+            case 2: tiled_step<C, false, true>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
+            default: tiled_step<C, true, true>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
+          }
+        } else {
+          switch (t.conj & 3u) {
+            case 0: tiled_step<C, false, false, 2, 2>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
+            case 1: tiled_step<C, true, false, 2, 2>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
+            case 2: tiled_step<C, false, true, 2, 2>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
+            default: tiled_step<C, true, true, 2, 2>(A, B, O, gt, s4.y, s4.z, t.kA, t.kB, kn, tid, gsize, store); break;
+          }
         }
       } else if (slice) {
         // B is the basis vector e_x of a measured bit, contracted over its only label:
