@@ -97,6 +97,10 @@ struct ptsbe_plan {
   // per stage: 1 descent, 0 flat, -1 decide per chunk (ptsbe_plan_set_stage_samplers)
   std::vector<int> stage_descent;
   DevBuf site_variants;                // [g] u8 variants per site, or empty (no index validation)
+  // small batches: the class-0 passes of stages 2..f depend on the error sets only, so they are launched up front
+  // on side streams and overlap each other and stage 1 (none of them fills the GPU); see run_chunk
+  uint32_t prelaunch = 1, prelaunch_max = 4096;
+  std::vector<cudaStream_t> side;
   uint64_t chunk_shots = 1ull << 26;
   size_t ext_budget = 48ull << 30;
   double vanish = 1e-12, neg_abs = -1e-12, neg_rel = 0.0, vanish_stage1 = 1e-30;
@@ -1038,6 +1042,58 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
   CK(cudaEventRecord(ev[0], st));
   EventLog log(st);
 
+  // ---- small batches: class-0 passes of stages 2..f up front, on side streams ----
+  // They read the Kraus rows and the (trivial) level-1 list only.  At a few thousand error sets none of them
+  // fills the GPU and each is a chain of hundreds of dependent steps, so run back to back they are most of the
+  // step (cfg5 at E = 100: 2.0 of 3.0 ms); concurrently they cost the longest one.
+  struct SideGuard {  // no side-stream work may outlive the chunk's workspace
+    ptsbe_plan* pl; bool on = false;
+    ~SideGuard() { if (on) for (cudaStream_t q : pl->side) cudaStreamSynchronize(q); }
+  } side_guard{pl};
+  std::vector<DevBuf> ext0(f + 1);
+  std::vector<cudaEvent_t> ev0(f + 1, nullptr);
+  DevBuf table0_dev;
+  if (pl->prelaunch && f >= 2 && ne <= pl->prelaunch_max) {
+    // one level table per stage: a class-0 step may read its OWN pass's record (a node that feeds both a later
+    // step of the pass and a later pass lives in the record), so level 1 must point at that stage's records
+    std::vector<LevelDev> t0((size_t)(f + 1) * (f + 2));
+    memset(t0.data(), 0, sizeof(LevelDev) * t0.size());
+    for (uint32_t j = 2; j <= f; ++j) {
+      Program& p0 = pl->programs[j - 1][0];
+      if (!p0.d.n_steps || !p0.d.out_elems) continue;
+      ext0[j].alloc((size_t)ne * p0.d.out_elems * pl->elem, st);
+      LevelDev& e1 = t0[(size_t)j * (f + 2) + 1];
+      e1.eset = lv[1].eset.as<uint32_t>();
+      e1.parent = lv[1].parent.as<uint32_t>();
+      e1.prefix = lv[1].prefix.as<uint64_t>();
+      e1.n = ne;
+      e1.ext = ext0[j].p;
+      e1.ext_rec = p0.d.out_elems;
+    }
+    table0_dev.alloc(t0.size() * sizeof(LevelDev), st);
+    CK(cudaMemcpyAsync(table0_dev.p, t0.data(), sizeof(LevelDev) * t0.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // t0 is a local; level 1 is ready for the side streams
+    while (pl->side.size() < f) {
+      cudaStream_t q;
+      CK(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
+      pl->side.push_back(q);
+    }
+    side_guard.on = true;
+    for (uint32_t j = 2; j <= f; ++j) {
+      Program& p0 = pl->programs[j - 1][0];
+      if (!p0.d.n_steps || !p0.d.out_elems) continue;
+      // the variant-0 memo is built once per plan, on the plan's own stream
+      if (p0.d.memo_elems && p0.d.threads_per_item > 32 && !p0.memo_ready) {
+        if (pl->dtype == PTSBE_C64) build_memo<float>(pl, p0); else build_memo<double>(pl, p0);
+      }
+      struct Swap { ptsbe_plan* pl; cudaStream_t keep; ~Swap() { pl->stream = keep; } } swap{pl, pl->stream};
+      pl->stream = pl->side[j - 1];
+      launch_hoist(pl, p0, table0_dev.as<LevelDev>() + (size_t)j * (f + 2), kraus_dev, ne, ext0[j].p);
+      CK(cudaEventCreateWithFlags(&ev0[j], cudaEventDisableTiming));
+      CK(cudaEventRecord(ev0[j], pl->stream));
+    }
+  }
+
   for (uint32_t j = 1; j <= f; ++j) {
     Level& cur = lv[j];
     const uint32_t U = cur.n, b = pl->sizes[j - 1], nb = 1u << b;
@@ -1053,7 +1109,8 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       table[l].ext = nullptr;
       table[l].ext_rec = 0;
       if (l < j && progs[l - 1].d.out_elems && progs[l - 1].d.n_steps) {
-        ext[l - 1].alloc((size_t)lv[l].n * progs[l - 1].d.out_elems * pl->elem, st);
+        if (l == 1 && ev0[j]) ext[0] = std::move(ext0[j]);  // written by the pre-launched class-0 pass
+        else ext[l - 1].alloc((size_t)lv[l].n * progs[l - 1].d.out_elems * pl->elem, st);
         table[l].ext = ext[l - 1].p;
         table[l].ext_rec = progs[l - 1].d.out_elems;
       }
@@ -1063,6 +1120,10 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     // hoist passes: everything that does not depend on the newest prefix bits
     for (uint32_t p = 0; p + 1 < j; ++p) {
       if (!progs[p].d.n_steps) continue;
+      if (p == 0 && ev0[j]) {  // pre-launched on a side stream: wait for it here
+        CK(cudaStreamWaitEvent(st, ev0[j], 0));
+        continue;
+      }
       log.begin(&stats->hoist_ms[j - 1]);
       launch_hoist(pl, progs[p], table_dev.as<LevelDev>(), kraus_dev, lv[p + 1].n, ext[p].p);
       log.end();
@@ -1391,6 +1452,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     stats->stage_ms[j - 1] += ms;
   }
   for (auto& e : ev) cudaEventDestroy(e);
+  for (auto& e : ev0) if (e) cudaEventDestroy(e);
   Level& fin = lv[f + 1];
   out.n = fin.n;
   out.eset = std::move(fin.eset);
@@ -1734,6 +1796,8 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     pl->tiled_plain = (uint32_t)env_size("PTSBE_TILED_PLAIN", pl->tiled_plain);
     pl->tc_steps = (uint32_t)env_size("PTSBE_TC_STEPS", pl->tc_steps);
     pl->tile_min = (uint32_t)env_size("PTSBE_TILE_MIN", pl->tile_min);
+    pl->prelaunch = (uint32_t)env_size("PTSBE_PRELAUNCH", pl->prelaunch);
+    pl->prelaunch_max = (uint32_t)env_size("PTSBE_PRELAUNCH_MAX", pl->prelaunch_max);
     pl->warp_run_len = (uint32_t)env_size("PTSBE_WARP_RUN_LEN", pl->warp_run_len);
     pl->stage_image_max = (uint32_t)env_size("PTSBE_STAGE_IMAGE_MAX", pl->stage_image_max);
     pl->lane = (uint32_t)env_size("PTSBE_LANE", pl->lane);
@@ -1831,6 +1895,7 @@ void ptsbe_plan_destroy(ptsbe_plan* pl) {
       p.memo_ptr.release(); p.memo_idx.release(); p.memo.release(); p.herm_map.release(); p.herm_canon.release();
     }
   cudaStreamSynchronize(pl->stream);
+  for (cudaStream_t q : pl->side) { cudaStreamSynchronize(q); cudaStreamDestroy(q); }
   cudaStreamDestroy(pl->stream);
   delete pl;
 }
