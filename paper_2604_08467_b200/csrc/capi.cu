@@ -82,6 +82,7 @@ struct ptsbe_plan {
                                        // pays only with PTSBE_RECORD_LAYOUT=1
   uint32_t tile_min = 128;             // CTA-per-item programs: 4 x 4 register tiles for separable steps with at
                                        // least this many tiles, 2 x 2 below (keeps the CTA busy on mid-size steps)
+  uint32_t tree_herm = 1;              // small descent tables: trees + Hermitian packing in one kernel
   uint32_t tc_steps = 0;               // opt-in (slower): large separable steps of CTA-per-item programs on tcgen05
                                        // tensor cores (executor.cuh tc_step, TF32 x3)
   uint32_t tiled_plain = 1;            // CTA-per-item programs without a memo (per-prefix passes of the dense
@@ -1142,17 +1143,49 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       dsh = descent_shape(pl, progs[j - 1].d.proj_d, b);
     if (dsh.nch) {
       const Program& pr = progs[j - 1];
-      DevBuf tree(((size_t)ne * dsh.dpad * pl->elem) << b, st);
-      log.begin(&stats->descent_ms[j - 1]);
-      launch_tree_build(pl, pr, table[1].ext, table[1].ext_rec, ne, b, dsh.dpad, tree.p);
-      log.end();
       Program& prj = progs[j - 1];
       const bool fused = pl->lane && prj.lane_fused && lane_descent_fits(pl, prj, dsh, b);
       // Hermitian-packed columns (v = x (x) conj(x)): half the table, half the work per tree level
       DescentShape hsh;
-      DevBuf htree;
-      if (fused && prj.herm) {
-        hsh = herm_shape(pl, prj.d.proj_d);
+      DevBuf htree, tree;
+      if (fused && prj.herm) hsh = herm_shape(pl, prj.d.proj_d);
+      // small tables: trees and packing in one kernel, a warp per error set (lane.cuh tree_herm_kernel)
+      const size_t th_warp = (size_t)2 * nb * sizeof(double2) + (size_t)prj.d.proj_d * nb * pl->elem;
+      const bool tree_herm = fused && prj.herm && hsh.nch && pl->tree_herm && b <= (uint32_t)TB_MAX_B &&
+                             (size_t)prj.d.proj_d * nb * pl->elem <= 16 * 1024;
+      if (tree_herm) {
+        const size_t real = pl->elem / 2;
+        htree.alloc(((size_t)ne * hsh.dpad * real) << b, st);
+        TreeHermArgs th;
+        th.rec0 = table[1].ext;
+        th.packed = htree.p;
+        th.map = prj.herm_map.as<uint32_t>();
+        th.canon = (prj.herm_dx && pl->lane_x) ? prj.herm_canon.as<uint32_t>() : nullptr;
+        th.rec_stride = table[1].ext_rec;
+        th.m_off = pr.d.result_ref;
+        th.D = prj.d.proj_d;
+        th.b = b;
+        th.dpad_r = hsh.dpad;
+        th.n_sets = ne;
+        const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(ne, (uint32_t)TH_WARPS), (uint64_t)pl->sm_count * 8));
+        log.begin(&stats->descent_ms[j - 1]);
+        if (pl->dtype == PTSBE_C64) {
+          opt_in_smem((const void*)tree_herm_kernel<float>, 200 * 1024);
+          tree_herm_kernel<float><<<grid, TH_WARPS * 32, th_warp * TH_WARPS, st>>>(th);
+        } else {
+          opt_in_smem((const void*)tree_herm_kernel<double>, 200 * 1024);
+          tree_herm_kernel<double><<<grid, TH_WARPS * 32, th_warp * TH_WARPS, st>>>(th);
+        }
+        g_launches++;
+        CK(cudaGetLastError());
+        log.end();
+      } else {
+        tree.alloc(((size_t)ne * dsh.dpad * pl->elem) << b, st);
+        log.begin(&stats->descent_ms[j - 1]);
+        launch_tree_build(pl, pr, table[1].ext, table[1].ext_rec, ne, b, dsh.dpad, tree.p);
+        log.end();
+      }
+      if (fused && prj.herm && !tree_herm) {
         if (hsh.nch) {
           const size_t real = pl->elem / 2;
           htree.alloc(((size_t)ne * hsh.dpad * real) << b, st);
@@ -1795,6 +1828,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     pl->warp_runs = (uint32_t)env_size("PTSBE_WARP_RUNS", pl->warp_runs);
     pl->tiled_plain = (uint32_t)env_size("PTSBE_TILED_PLAIN", pl->tiled_plain);
     pl->tc_steps = (uint32_t)env_size("PTSBE_TC_STEPS", pl->tc_steps);
+    pl->tree_herm = (uint32_t)env_size("PTSBE_TREE_HERM", pl->tree_herm);
     pl->tile_min = (uint32_t)env_size("PTSBE_TILE_MIN", pl->tile_min);
     pl->prelaunch = (uint32_t)env_size("PTSBE_PRELAUNCH", pl->prelaunch);
     pl->prelaunch_max = (uint32_t)env_size("PTSBE_PRELAUNCH_MAX", pl->prelaunch_max);

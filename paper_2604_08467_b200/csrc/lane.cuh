@@ -527,6 +527,82 @@ __global__ void herm_pack_kernel(const HermPackArgs a) {
   reinterpret_cast<R*>(a.packed)[((size_t)e * N + node) * a.dpad_r + dst] = out;
 }
 
+// tree_reduce_kernel + herm_pack_kernel in one pass for small tables (cfg5: 64 nodes x 16 reals per error set,
+// 10^5 error sets per stage, ~100 work items each): a warp owns an error set, reduces the D rows of M one after
+// the other (pairwise sums in double, as tree_reduce_kernel) into a [D][N] table of rounded node values in
+// shared memory and writes the packed columns coalesced.  The two-kernel path launched 4 x 10^5 CTAs of 128
+// threads for the trees, wrote them to HBM and read them back: 7.4 of cfg5's 54 ms per step.  Same values.
+struct TreeHermArgs {
+  const void* rec0;         // pass-0 records [error sets][rec_stride] complex
+  void* packed;             // out: [sets][N][dpad_r] reals
+  const uint32_t* map;      // [D] c | c' << 12 | kind << 24
+  const uint32_t* canon;    // null or [D] (HermPackArgs)
+  uint32_t rec_stride, m_off, D, b, dpad_r, n_sets;
+};
+constexpr int TH_WARPS = 4;
+
+template <typename R>
+__global__ void __launch_bounds__(TH_WARPS * 32) tree_herm_kernel(const TreeHermArgs a) {
+  using C = typename CxT<R>::type;
+  extern __shared__ __align__(16) unsigned char th_smem[];
+  const uint32_t N = 1u << a.b;
+  const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t per_warp = (size_t)2 * N * sizeof(double2) + (size_t)a.D * N * sizeof(C);
+  double2* nd = reinterpret_cast<double2*>(th_smem + w * per_warp);   // reduction tree of one row
+  C* tr = reinterpret_cast<C*>(nd + 2 * N);                           // [D][N] node values, rounded
+  for (uint32_t e = blockIdx.x * TH_WARPS + w; e < a.n_sets; e += gridDim.x * TH_WARPS) {
+    const C* M0 = reinterpret_cast<const C*>(a.rec0) + (size_t)e * a.rec_stride + a.m_off;
+    for (uint32_t d = 0; d < a.D; ++d) {
+      const C* M = M0 + (size_t)d * N;
+      for (uint32_t c = lane; c < N; c += 32) { const C m = M[c]; nd[c] = make_double2((double)m.x, (double)m.y); }
+      __syncwarp();
+      uint32_t off = 0;
+      for (uint32_t k = 1; k <= a.b; ++k) {
+        const uint32_t prev = off, n_prev = N >> (k - 1);
+        off += n_prev;
+        for (uint32_t q = lane; q < (n_prev >> 1); q += 32) {
+          const double2 l = nd[prev + 2 * q], r = nd[prev + 2 * q + 1];
+          nd[off + q] = make_double2(l.x + r.x, l.y + r.y);
+        }
+        __syncwarp();
+      }
+      // node idx: 0 = all columns = level b, q 0; idx = 2^(t-1) + parent -> level b - t, q = 2 * parent
+      for (uint32_t idx = lane; idx < N; idx += 32) {
+        uint32_t k = a.b, q = 0;
+        if (idx) {
+          const uint32_t t = 32 - __clz(idx);
+          k = a.b - t;
+          q = 2 * (idx - (1u << (t - 1)));
+        }
+        const double2 v = nd[2 * N - (2 * N >> k) + q];
+        C o; o.x = (R)v.x; o.y = (R)v.y;
+        tr[d * N + idx] = o;
+      }
+      __syncwarp();
+    }
+    R* out = reinterpret_cast<R*>(a.packed) + (size_t)e * N * a.dpad_r;
+    for (uint32_t x = lane; x < N * a.dpad_r; x += 32) {
+      const uint32_t node = x / a.dpad_r, sl = x % a.dpad_r;
+      R val = R(0);
+      uint32_t dst = sl;
+      if (sl < a.D) {
+        const uint32_t m = __ldg(a.map + sl);
+        const uint32_t c = m & 0xfffu, c2 = (m >> 12) & 0xfffu, kind = m >> 24;
+        const C u = tr[c * N + node], v2 = tr[c2 * N + node];
+        if (kind == 0) val = (c == c2) ? u.x : u.x + v2.x;
+        else if (kind == 1) val = -(u.y - v2.y);
+        if (a.canon) {
+          const uint32_t cm = __ldg(a.canon + sl);
+          dst = cm & 0xffffu;
+          if (cm >> 31) val = -val;
+        }
+      }
+      out[(size_t)node * a.dpad_r + dst] = val;
+    }
+    __syncwarp();
+  }
+}
+
 template <typename R, int NCH, bool HERM>
 __global__ void __launch_bounds__(LN_THREADS, 2) lane_descent_kernel(const LaneDescentArgs a) {
   using C = typename CxT<R>::type;
