@@ -98,9 +98,10 @@ struct ptsbe_plan {
   // per stage: 1 descent, 0 flat, -1 decide per chunk (ptsbe_plan_set_stage_samplers)
   std::vector<int> stage_descent;
   DevBuf site_variants;                // [g] u8 variants per site, or empty (no index validation)
-  // small batches: the class-0 passes of stages 2..f depend on the error sets only, so they are launched up front
-  // on side streams and overlap each other and stage 1 (none of them fills the GPU); see run_chunk
-  uint32_t prelaunch = 1, prelaunch_max = 4096;
+  // the class-0 passes of stages 2..f depend on the error sets only, so they are launched up front on side
+  // streams and overlap each other and stage 1; see run_chunk (measured a gain at every batch size: the passes
+  // are latency-bound, small batches because they do not fill the GPU, large ones because they wait on L2)
+  uint32_t prelaunch = 1, prelaunch_max = 0xffffffffu;
   std::vector<cudaStream_t> side;
   uint64_t chunk_shots = 1ull << 26;
   size_t ext_budget = 48ull << 30;
@@ -1043,10 +1044,11 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
   CK(cudaEventRecord(ev[0], st));
   EventLog log(st);
 
-  // ---- small batches: class-0 passes of stages 2..f up front, on side streams ----
+  // ---- class-0 passes of stages 2..f up front, on side streams ----
   // They read the Kraus rows and the (trivial) level-1 list only.  At a few thousand error sets none of them
   // fills the GPU and each is a chain of hundreds of dependent steps, so run back to back they are most of the
-  // step (cfg5 at E = 100: 2.0 of 3.0 ms); concurrently they cost the longest one.
+  // step (cfg5 at E = 100: 2.0 of 3.0 ms); concurrently they cost the longest one.  Large batches gain less
+  // (cfg5 at 10^5 sets 52.7 -> 50.7 ms, cfg2 37.1 -> 36.5 ms): the kernels wait on L2 and barriers.
   struct SideGuard {  // no side-stream work may outlive the chunk's workspace
     ptsbe_plan* pl; bool on = false;
     ~SideGuard() { if (on) for (cudaStream_t q : pl->side) cudaStreamSynchronize(q); }
