@@ -988,6 +988,66 @@ struct RunOutput {
 };
 
 // Runs error sets [e0, e0+ne) of a resident batch through all stages.
+// Per-error-set tables of the descent sampler for one stage: column sums over the binary tree of the batch
+// qubits (tree), Hermitian-packed (htree) when the fused kernel takes them that way.  Depends on the class-0
+// records only.
+static void build_descent_tables(ptsbe_plan* pl, Program& prj, const void* rec0, uint32_t rec_stride, uint32_t ne,
+                                 uint32_t b, const DescentShape& dsh, const DescentShape& hsh, bool fused,
+                                 DevBuf& tree, DevBuf& htree) {
+  cudaStream_t st = pl->stream;
+  const uint32_t nb = 1u << b;
+  // small tables: trees and packing in one kernel, a warp per error set (lane.cuh tree_herm_kernel)
+  const size_t th_warp = (size_t)2 * nb * sizeof(double2) + (size_t)prj.d.proj_d * nb * pl->elem;
+  const bool tree_herm = fused && prj.herm && hsh.nch && pl->tree_herm && b <= (uint32_t)TB_MAX_B &&
+                         (size_t)prj.d.proj_d * nb * pl->elem <= 16 * 1024;
+  if (tree_herm) {
+    const size_t real = pl->elem / 2;
+    htree.alloc(((size_t)ne * hsh.dpad * real) << b, st);
+    TreeHermArgs th;
+    th.rec0 = rec0;
+    th.packed = htree.p;
+    th.map = prj.herm_map.as<uint32_t>();
+    th.canon = (prj.herm_dx && pl->lane_x) ? prj.herm_canon.as<uint32_t>() : nullptr;
+    th.rec_stride = rec_stride;
+    th.m_off = prj.d.result_ref;
+    th.D = prj.d.proj_d;
+    th.b = b;
+    th.dpad_r = hsh.dpad;
+    th.n_sets = ne;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(ne, (uint32_t)TH_WARPS), (uint64_t)pl->sm_count * 8));
+    if (pl->dtype == PTSBE_C64) {
+      opt_in_smem((const void*)tree_herm_kernel<float>, 200 * 1024);
+      tree_herm_kernel<float><<<grid, TH_WARPS * 32, th_warp * TH_WARPS, st>>>(th);
+    } else {
+      opt_in_smem((const void*)tree_herm_kernel<double>, 200 * 1024);
+      tree_herm_kernel<double><<<grid, TH_WARPS * 32, th_warp * TH_WARPS, st>>>(th);
+    }
+    g_launches++;
+    CK(cudaGetLastError());
+    return;
+  }
+  tree.alloc(((size_t)ne * dsh.dpad * pl->elem) << b, st);
+  launch_tree_build(pl, prj, rec0, rec_stride, ne, b, dsh.dpad, tree.p);
+  if (fused && prj.herm && hsh.nch) {
+    const size_t real = pl->elem / 2;
+    htree.alloc(((size_t)ne * hsh.dpad * real) << b, st);
+    HermPackArgs hp;
+    hp.tree = tree.p;
+    hp.packed = htree.p;
+    hp.map = prj.herm_map.as<uint32_t>();
+    hp.canon = (prj.herm_dx && pl->lane_x) ? prj.herm_canon.as<uint32_t>() : nullptr;
+    hp.D = prj.d.proj_d;
+    hp.dpad_c = dsh.dpad;
+    hp.dpad_r = hsh.dpad;
+    hp.b = b;
+    const dim3 grid(ne, cdiv(((uint64_t)hsh.dpad) << b, 256));
+    if (pl->dtype == PTSBE_C64) herm_pack_kernel<float><<<grid, 256, 0, st>>>(hp);
+    else herm_pack_kernel<double><<<grid, 256, 0, st>>>(hp);
+    g_launches++;
+    CK(cudaGetLastError());
+  }
+}
+
 static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* shots_dev,
                       const uint32_t* ids_dev, uint32_t ne, uint64_t chunk_shots, uint64_t seed,
                       RunOutput& out, ptsbe_run_stats* stats, unsigned long long* flag_dev,
@@ -1055,6 +1115,8 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
   } side_guard{pl};
   std::vector<DevBuf> ext0(f + 1);
   std::vector<cudaEvent_t> ev0(f + 1, nullptr);
+  struct PreTab { DevBuf tree, htree; bool done = false; };
+  std::vector<PreTab> pre_tab(f + 1);
   DevBuf table0_dev;
   if (pl->prelaunch && f >= 2 && ne <= pl->prelaunch_max) {
     // one level table per stage: a class-0 step may read its OWN pass's record (a node that feeds both a later
@@ -1092,6 +1154,20 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       struct Swap { ptsbe_plan* pl; cudaStream_t keep; ~Swap() { pl->stream = keep; } } swap{pl, pl->stream};
       pl->stream = pl->side[j - 1];
       launch_hoist(pl, p0, table0_dev.as<LevelDev>() + (size_t)j * (f + 2), kraus_dev, ne, ext0[j].p);
+      // the descent tables of the stage depend on these records only: same side stream, when the plan has
+      // fixed the stage's sampler (the per-chunk choice needs the stage's work-list size)
+      Program& pj = pl->programs[j - 1][j - 1];
+      if (pl->descent && pl->stage_descent[j - 1] == 1 && pj.d.result_kind == 3 && (!npp || (j == f && !np_exhaustive))) {
+        const uint32_t bj = pl->sizes[j - 1];
+        const DescentShape dsh = descent_shape(pl, pj.d.proj_d, bj);
+        if (dsh.nch) {
+          const bool fused = pl->lane && pj.lane_fused && lane_descent_fits(pl, pj, dsh, bj);
+          DescentShape hsh;
+          if (fused && pj.herm) hsh = herm_shape(pl, pj.d.proj_d);
+          build_descent_tables(pl, pj, ext0[j].p, p0.d.out_elems, ne, bj, dsh, hsh, fused, pre_tab[j].tree, pre_tab[j].htree);
+          pre_tab[j].done = true;
+        }
+      }
       CK(cudaEventCreateWithFlags(&ev0[j], cudaEventDisableTiming));
       CK(cudaEventRecord(ev0[j], pl->stream));
     }
@@ -1147,67 +1223,18 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       const Program& pr = progs[j - 1];
       Program& prj = progs[j - 1];
       const bool fused = pl->lane && prj.lane_fused && lane_descent_fits(pl, prj, dsh, b);
-      // Hermitian-packed columns (v = x (x) conj(x)): half the table, half the work per tree level
+      // tree of conditional marginals per error set (Hermitian-packed when v = x (x) conj(x)); built up front
+      // on the stage's side stream when the plan fixed the sampler (pre_tab), here otherwise
       DescentShape hsh;
       DevBuf htree, tree;
       if (fused && prj.herm) hsh = herm_shape(pl, prj.d.proj_d);
-      // small tables: trees and packing in one kernel, a warp per error set (lane.cuh tree_herm_kernel)
-      const size_t th_warp = (size_t)2 * nb * sizeof(double2) + (size_t)prj.d.proj_d * nb * pl->elem;
-      const bool tree_herm = fused && prj.herm && hsh.nch && pl->tree_herm && b <= (uint32_t)TB_MAX_B &&
-                             (size_t)prj.d.proj_d * nb * pl->elem <= 16 * 1024;
-      if (tree_herm) {
-        const size_t real = pl->elem / 2;
-        htree.alloc(((size_t)ne * hsh.dpad * real) << b, st);
-        TreeHermArgs th;
-        th.rec0 = table[1].ext;
-        th.packed = htree.p;
-        th.map = prj.herm_map.as<uint32_t>();
-        th.canon = (prj.herm_dx && pl->lane_x) ? prj.herm_canon.as<uint32_t>() : nullptr;
-        th.rec_stride = table[1].ext_rec;
-        th.m_off = pr.d.result_ref;
-        th.D = prj.d.proj_d;
-        th.b = b;
-        th.dpad_r = hsh.dpad;
-        th.n_sets = ne;
-        const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(cdiv(ne, (uint32_t)TH_WARPS), (uint64_t)pl->sm_count * 8));
-        log.begin(&stats->descent_ms[j - 1]);
-        if (pl->dtype == PTSBE_C64) {
-          opt_in_smem((const void*)tree_herm_kernel<float>, 200 * 1024);
-          tree_herm_kernel<float><<<grid, TH_WARPS * 32, th_warp * TH_WARPS, st>>>(th);
-        } else {
-          opt_in_smem((const void*)tree_herm_kernel<double>, 200 * 1024);
-          tree_herm_kernel<double><<<grid, TH_WARPS * 32, th_warp * TH_WARPS, st>>>(th);
-        }
-        g_launches++;
-        CK(cudaGetLastError());
-        log.end();
+      if (pre_tab[j].done) {
+        htree = std::move(pre_tab[j].htree);
+        tree = std::move(pre_tab[j].tree);
       } else {
-        tree.alloc(((size_t)ne * dsh.dpad * pl->elem) << b, st);
         log.begin(&stats->descent_ms[j - 1]);
-        launch_tree_build(pl, pr, table[1].ext, table[1].ext_rec, ne, b, dsh.dpad, tree.p);
+        build_descent_tables(pl, prj, table[1].ext, table[1].ext_rec, ne, b, dsh, hsh, fused, tree, htree);
         log.end();
-      }
-      if (fused && prj.herm && !tree_herm) {
-        if (hsh.nch) {
-          const size_t real = pl->elem / 2;
-          htree.alloc(((size_t)ne * hsh.dpad * real) << b, st);
-          HermPackArgs hp;
-          hp.tree = tree.p;
-          hp.packed = htree.p;
-          hp.map = prj.herm_map.as<uint32_t>();
-          hp.canon = (prj.herm_dx && pl->lane_x) ? prj.herm_canon.as<uint32_t>() : nullptr;
-          hp.D = prj.d.proj_d;
-          hp.dpad_c = dsh.dpad;
-          hp.dpad_r = hsh.dpad;
-          hp.b = b;
-          const dim3 grid(ne, cdiv(((uint64_t)hsh.dpad) << b, 256));
-          log.begin(&stats->descent_ms[j - 1]);
-          if (pl->dtype == PTSBE_C64) herm_pack_kernel<float><<<grid, 256, 0, st>>>(hp);
-          else herm_pack_kernel<double><<<grid, 256, 0, st>>>(hp);
-          g_launches++;
-          CK(cudaGetLastError());
-          log.end();
-        }
       }
       if (fused) {
         // per-item steps and descent in one kernel: v never leaves the SM; raw per-draw outcomes
