@@ -1104,74 +1104,98 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
   CK(cudaEventRecord(ev[0], st));
   EventLog log(st);
 
-  // ---- class-0 passes of stages 2..f up front, on side streams ----
-  // They read the Kraus rows and the (trivial) level-1 list only.  At a few thousand error sets none of them
-  // fills the GPU and each is a chain of hundreds of dependent steps, so run back to back they are most of the
-  // step (cfg5 at E = 100: 2.0 of 3.0 ms); concurrently they cost the longest one.  Large batches gain less
-  // (cfg5 at 10^5 sets 52.7 -> 50.7 ms, cfg2 37.1 -> 36.5 ms): the kernels wait on L2 and barriers.
+  // ---- hoist passes run as early as their inputs exist, on one side stream per stage ----
+  // Pass p of stage j needs the level-(p+1) work list (complete when stage p has been sampled) and the records
+  // of the passes below it of the same stage -- nothing of stages p+1 .. j-1.  So as soon as level L is
+  // built, pass L-1 of EVERY later stage is launched on that stage's side stream (class-0 passes, L = 1, before
+  // stage 1 starts, together with the stage's descent tables when the plan fixed the sampler), and the main
+  // stream waits for a stage's side stream where the stage begins.  The passes are latency-bound -- small
+  // batches because no pass fills the GPU (cfg5 at E = 100: 2.96 -> 1.3 ms per step), large ones because they
+  // wait on L2 and barriers (cfg5 at 10^5 sets 52.7 -> 48 ms, cfg2 37.1 -> 35.9 ms) -- so they overlap well.
   struct SideGuard {  // no side-stream work may outlive the chunk's workspace
     ptsbe_plan* pl; bool on = false;
     ~SideGuard() { if (on) for (cudaStream_t q : pl->side) cudaStreamSynchronize(q); }
   } side_guard{pl};
-  std::vector<DevBuf> ext0(f + 1);
-  std::vector<cudaEvent_t> ev0(f + 1, nullptr);
+  struct EventBag {
+    std::vector<cudaEvent_t> v;
+    cudaEvent_t make() { cudaEvent_t e; CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); v.push_back(e); return e; }
+    ~EventBag() { for (cudaEvent_t e : v) cudaEventDestroy(e); }
+  } events;
+  std::vector<std::vector<DevBuf>> sext(f + 1);           // [stage][pass] records of the hoist passes
+  std::vector<std::vector<LevelDev>> stab(f + 1);         // [stage] level table as the stage's passes see it
+  std::vector<DevBuf> stab_dev(f + 1);
+  std::vector<cudaEvent_t> sev(f + 1, nullptr);           // last work queued on the stage's side stream
+  std::vector<uint32_t> passes_done(f + 1, 0);            // leading passes of the stage already launched
   struct PreTab { DevBuf tree, htree; bool done = false; };
   std::vector<PreTab> pre_tab(f + 1);
-  DevBuf table0_dev;
-  if (pl->prelaunch && f >= 2 && ne <= pl->prelaunch_max) {
-    // one level table per stage: a class-0 step may read its OWN pass's record (a node that feeds both a later
-    // step of the pass and a later pass lives in the record), so level 1 must point at that stage's records
-    std::vector<LevelDev> t0((size_t)(f + 1) * (f + 2));
-    memset(t0.data(), 0, sizeof(LevelDev) * t0.size());
-    for (uint32_t j = 2; j <= f; ++j) {
-      Program& p0 = pl->programs[j - 1][0];
-      if (!p0.d.n_steps || !p0.d.out_elems) continue;
-      ext0[j].alloc((size_t)ne * p0.d.out_elems * pl->elem, st);
-      LevelDev& e1 = t0[(size_t)j * (f + 2) + 1];
-      e1.eset = lv[1].eset.as<uint32_t>();
-      e1.parent = lv[1].parent.as<uint32_t>();
-      e1.prefix = lv[1].prefix.as<uint64_t>();
-      e1.n = ne;
-      e1.ext = ext0[j].p;
-      e1.ext_rec = p0.d.out_elems;
-    }
-    table0_dev.alloc(t0.size() * sizeof(LevelDev), st);
-    CK(cudaMemcpyAsync(table0_dev.p, t0.data(), sizeof(LevelDev) * t0.size(), cudaMemcpyHostToDevice, st));
-    CK(cudaStreamSynchronize(st));  // t0 is a local; level 1 is ready for the side streams
+  for (uint32_t j = 1; j <= f; ++j) {
+    sext[j].resize(j);
+    stab[j].assign(f + 2, LevelDev{});
+    memset(stab[j].data(), 0, sizeof(LevelDev) * (f + 2));
+  }
+  const bool eager = pl->prelaunch && f >= 2 && ne <= pl->prelaunch_max;
+  if (eager) {
     while (pl->side.size() < f) {
       cudaStream_t q;
       CK(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
       pl->side.push_back(q);
     }
     side_guard.on = true;
-    for (uint32_t j = 2; j <= f; ++j) {
-      Program& p0 = pl->programs[j - 1][0];
-      if (!p0.d.n_steps || !p0.d.out_elems) continue;
-      // the variant-0 memo is built once per plan, on the plan's own stream
-      if (p0.d.memo_elems && p0.d.threads_per_item > 32 && !p0.memo_ready) {
-        if (pl->dtype == PTSBE_C64) build_memo<float>(pl, p0); else build_memo<double>(pl, p0);
+    for (uint32_t j = 2; j <= f; ++j) stab_dev[j].alloc((f + 2) * sizeof(LevelDev), st);
+  }
+  // level L is complete on the main stream: launch pass L-1 of the stages L+1 .. f
+  auto eager_hoists = [&](uint32_t L) {
+    if (!eager || L + 1 > f) return;
+    const uint32_t p = L - 1;
+    for (uint32_t j = L + 1; j <= f; ++j) {  // records and table rows first (allocations on the main stream)
+      Program& pp = pl->programs[j - 1][p];
+      LevelDev& row = stab[j][L];
+      row.eset = lv[L].eset.as<uint32_t>();
+      row.parent = lv[L].parent.as<uint32_t>();
+      row.prefix = lv[L].prefix.as<uint64_t>();
+      row.n = lv[L].n;
+      if (pp.d.n_steps && pp.d.out_elems) {
+        sext[j][p].alloc((size_t)lv[L].n * pp.d.out_elems * pl->elem, st);
+        row.ext = sext[j][p].p;        // a step may read its OWN pass's record, so the row points at it already
+        row.ext_rec = pp.d.out_elems;
+        // the variant-0 memo is built once per plan, on the plan's own stream
+        if (p == 0 && pp.d.memo_elems && pp.d.threads_per_item > 32 && !pp.memo_ready) {
+          if (pl->dtype == PTSBE_C64) build_memo<float>(pl, pp); else build_memo<double>(pl, pp);
+        }
       }
+      passes_done[j] = L;
+    }
+    cudaEvent_t ready = events.make();
+    CK(cudaEventRecord(ready, st));
+    for (uint32_t j = L + 1; j <= f; ++j) {
+      Program& pp = pl->programs[j - 1][p];
+      if (!(pp.d.n_steps && pp.d.out_elems)) continue;
       struct Swap { ptsbe_plan* pl; cudaStream_t keep; ~Swap() { pl->stream = keep; } } swap{pl, pl->stream};
       pl->stream = pl->side[j - 1];
-      launch_hoist(pl, p0, table0_dev.as<LevelDev>() + (size_t)j * (f + 2), kraus_dev, ne, ext0[j].p);
-      // the descent tables of the stage depend on these records only: same side stream, when the plan has
-      // fixed the stage's sampler (the per-chunk choice needs the stage's work-list size)
+      CK(cudaStreamWaitEvent(pl->stream, ready, 0));
+      CK(cudaMemcpyAsync(stab_dev[j].p, stab[j].data(), sizeof(LevelDev) * (f + 2), cudaMemcpyHostToDevice, pl->stream));
+      launch_hoist(pl, pp, stab_dev[j].as<LevelDev>(), kraus_dev, lv[L].n, sext[j][p].p);
+      // the descent tables of the stage depend on the class-0 records only: same side stream, when the plan
+      // has fixed the stage's sampler (the per-chunk choice needs the stage's work-list size)
       Program& pj = pl->programs[j - 1][j - 1];
-      if (pl->descent && pl->stage_descent[j - 1] == 1 && pj.d.result_kind == 3 && (!npp || (j == f && !np_exhaustive))) {
+      if (p == 0 && pl->descent && pl->stage_descent[j - 1] == 1 && pj.d.result_kind == 3 &&
+          (!npp || (j == f && !np_exhaustive))) {
         const uint32_t bj = pl->sizes[j - 1];
         const DescentShape dsh = descent_shape(pl, pj.d.proj_d, bj);
         if (dsh.nch) {
           const bool fused = pl->lane && pj.lane_fused && lane_descent_fits(pl, pj, dsh, bj);
           DescentShape hsh;
           if (fused && pj.herm) hsh = herm_shape(pl, pj.d.proj_d);
-          build_descent_tables(pl, pj, ext0[j].p, p0.d.out_elems, ne, bj, dsh, hsh, fused, pre_tab[j].tree, pre_tab[j].htree);
+          build_descent_tables(pl, pj, sext[j][0].p, pp.d.out_elems, ne, bj, dsh, hsh, fused, pre_tab[j].tree, pre_tab[j].htree);
           pre_tab[j].done = true;
         }
       }
-      CK(cudaEventCreateWithFlags(&ev0[j], cudaEventDisableTiming));
-      CK(cudaEventRecord(ev0[j], pl->stream));
+      sev[j] = events.make();
+      CK(cudaEventRecord(sev[j], pl->stream));
     }
-  }
+  };
+  CK(cudaStreamSynchronize(st));  // level 1 is complete
+  eager_hoists(1);
 
   for (uint32_t j = 1; j <= f; ++j) {
     Level& cur = lv[j];
@@ -1179,7 +1203,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     stats->stage_events[j - 1] += U;
     auto& progs = pl->programs[j - 1];
     // level table for this stage
-    std::vector<DevBuf> ext(j);
+    std::vector<DevBuf>& ext = sext[j];
     for (uint32_t l = 1; l <= j; ++l) {
       table[l].eset = lv[l].eset.as<uint32_t>();
       table[l].parent = lv[l].parent.as<uint32_t>();
@@ -1188,21 +1212,19 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       table[l].ext = nullptr;
       table[l].ext_rec = 0;
       if (l < j && progs[l - 1].d.out_elems && progs[l - 1].d.n_steps) {
-        if (l == 1 && ev0[j]) ext[0] = std::move(ext0[j]);  // written by the pre-launched class-0 pass
-        else ext[l - 1].alloc((size_t)lv[l].n * progs[l - 1].d.out_elems * pl->elem, st);
+        // passes below passes_done[j] were launched early on the stage's side stream, records included
+        if (l - 1 >= passes_done[j]) ext[l - 1].alloc((size_t)lv[l].n * progs[l - 1].d.out_elems * pl->elem, st);
         table[l].ext = ext[l - 1].p;
         table[l].ext_rec = progs[l - 1].d.out_elems;
       }
     }
     CK(cudaMemcpyAsync(table_dev.p, table.data(), sizeof(LevelDev) * (f + 2),
                        cudaMemcpyHostToDevice, st));
+    if (sev[j]) CK(cudaStreamWaitEvent(st, sev[j], 0));  // the stage's early passes (and descent tables)
     // hoist passes: everything that does not depend on the newest prefix bits
     for (uint32_t p = 0; p + 1 < j; ++p) {
       if (!progs[p].d.n_steps) continue;
-      if (p == 0 && ev0[j]) {  // pre-launched on a side stream: wait for it here
-        CK(cudaStreamWaitEvent(st, ev0[j], 0));
-        continue;
-      }
+      if (p < passes_done[j]) continue;  // launched early
       log.begin(&stats->hoist_ms[j - 1]);
       launch_hoist(pl, progs[p], table_dev.as<LevelDev>(), kraus_dev, lv[p + 1].n, ext[p].p);
       log.end();
@@ -1500,6 +1522,8 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     CK(cudaGetLastError());
     log.end();
     CK(cudaEventRecord(ev[j], st));
+    eager_hoists(j + 1);  // level j+1 is complete: its hoist passes of all later stages can start
+    for (auto& buf : sext[j]) buf.release();
     // parents' per-stage arrays are no longer needed (lists stay for ancestor lookups)
     cur.mult.release();
     cur.slot_off.release();
@@ -1514,7 +1538,6 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     stats->stage_ms[j - 1] += ms;
   }
   for (auto& e : ev) cudaEventDestroy(e);
-  for (auto& e : ev0) if (e) cudaEventDestroy(e);
   Level& fin = lv[f + 1];
   out.n = fin.n;
   out.eset = std::move(fin.eset);
