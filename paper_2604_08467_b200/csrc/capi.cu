@@ -82,6 +82,7 @@ struct ptsbe_plan {
                                        // pays only with PTSBE_RECORD_LAYOUT=1
   uint32_t tile_min = 128;             // CTA-per-item programs: 4 x 4 register tiles for separable steps with at
                                        // least this many tiles, 2 x 2 below (keeps the CTA busy on mid-size steps)
+  uint32_t descent_tile_max = 2048;    // fused descent: most consecutive work items a CTA takes at a time
   uint32_t tree_herm = 1;              // small descent tables: trees + Hermitian packing in one kernel
   uint32_t tc_steps = 0;               // opt-in (slower): large separable steps of CTA-per-item programs on tcgen05
                                        // tensor cores (executor.cuh tc_step, TF32 x3)
@@ -675,7 +676,7 @@ static void launch_lane_descent_t(ptsbe_plan* pl, Program& pr, LaneDescentArgs& 
   // every resident CTA gets several
   const uint64_t ctas = (uint64_t)pl->sm_count * per_sm;
   uint64_t tile = a.d.n_items / (ctas * 4) / LN_THREADS * LN_THREADS;
-  tile = std::min<uint64_t>(2048, std::max<uint64_t>(LN_THREADS, tile));
+  tile = std::min<uint64_t>(pl->descent_tile_max, std::max<uint64_t>(LN_THREADS, tile));
   a.tile = (uint32_t)tile;
   const uint64_t tiles = cdiv(a.d.n_items, tile);
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, ctas));
@@ -702,7 +703,7 @@ static void launch_lane_descent_x(ptsbe_plan* pl, Program& pr, LaneDescentArgs& 
   const int per_sm = cached_occupancy((const void*)lane_descent_x_kernel<DX, CHAIN>, LN_THREADS, smem);
   const uint64_t ctas = (uint64_t)pl->sm_count * per_sm;
   uint64_t tile = a.d.n_items / (ctas * 4) / LN_THREADS * LN_THREADS;
-  tile = std::min<uint64_t>(2048, std::max<uint64_t>(LN_THREADS, tile));
+  tile = std::min<uint64_t>(pl->descent_tile_max, std::max<uint64_t>(LN_THREADS, tile));
   a.tile = (uint32_t)tile;
   const uint64_t tiles = cdiv(a.d.n_items, tile);
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, ctas));
@@ -1881,6 +1882,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     pl->tiled_plain = (uint32_t)env_size("PTSBE_TILED_PLAIN", pl->tiled_plain);
     pl->tc_steps = (uint32_t)env_size("PTSBE_TC_STEPS", pl->tc_steps);
     pl->tree_herm = (uint32_t)env_size("PTSBE_TREE_HERM", pl->tree_herm);
+    pl->descent_tile_max = (uint32_t)env_size("PTSBE_DESCENT_TILE_MAX", pl->descent_tile_max);
     pl->tile_min = (uint32_t)env_size("PTSBE_TILE_MIN", pl->tile_min);
     pl->prelaunch = (uint32_t)env_size("PTSBE_PRELAUNCH", pl->prelaunch);
     pl->prelaunch_max = (uint32_t)env_size("PTSBE_PRELAUNCH_MAX", pl->prelaunch_max);
