@@ -103,6 +103,7 @@ struct ptsbe_plan {
   // streams and overlap each other and stage 1; see run_chunk (measured a gain at every batch size: the passes
   // are latency-bound, small batches because they do not fill the GPU, large ones because they wait on L2)
   uint32_t prelaunch = 1, prelaunch_max = 0xffffffffu;
+  uint32_t side_priority = 1;
   std::vector<cudaStream_t> side;
   uint64_t chunk_shots = 1ull << 26;
   size_t ext_budget = 48ull << 30;
@@ -1137,8 +1138,13 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
   const bool eager = pl->prelaunch && f >= 2 && ne <= pl->prelaunch_max;
   if (eager) {
     while (pl->side.size() < f) {
+      // the side stream of an earlier stage outranks those of later stages (and the plan's own stream outranks
+      // them all): what the pipeline needs next is scheduled first, the rest fills the gaps
       cudaStream_t q;
-      CK(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
+      int lo = 0, hi = 0;  // numerically lower = higher priority
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      const int prio = pl->side_priority ? std::min(lo, hi + 1 + (int)pl->side.size()) : lo;
+      CK(cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, prio));
       pl->side.push_back(q);
     }
     side_guard.on = true;
@@ -1862,7 +1868,12 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     }
     if (off != d->n_qubits) throw Failure(PTSBE_EINVAL, "stage sizes do not sum to n_qubits");
     if (d->dtype == PTSBE_C64) { pl->neg_abs = -1e-12; pl->neg_rel = 1e-4; }
-    CK(cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking));
+    {
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      pl->side_priority = (uint32_t)env_size("PTSBE_SIDE_PRIORITY", 1);
+      CK(cudaStreamCreateWithPriority(&pl->stream, cudaStreamNonBlocking, pl->side_priority ? hi : lo));
+    }
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device));
     pl->sm_count = prop.multiProcessorCount;
