@@ -467,6 +467,34 @@ def test_warp_private_descent_tables_and_staged_image_equal_the_cta_paths(monkey
         assert fast == want
 
 
+@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+def test_early_hoist_passes_fused_tables_and_tile_shapes_do_not_change_records(monkeypatch, dtype):
+    """Scheduling choices of the run loop and of the CTA executor: hoist passes launched on side
+    streams as soon as their level exists (PTSBE_PRELAUNCH), descent tables built by the fused
+    tree + packing kernel (PTSBE_TREE_HERM), 2 x 2 instead of 4 x 4 register tiles for mid-size steps
+    (PTSBE_TILE_MIN).  None of them may change a record; complex128 must still equal the oracle
+    (reference engine.py:493-524)."""
+    c, tpl, es = _hea_case(14, 4, 24, 300, 5, gamma=0.0)
+    sizes = (5, 5, 4)
+
+    def run(on):
+        monkeypatch.setenv("PTSBE_PRELAUNCH", "1" if on else "0")
+        monkeypatch.setenv("PTSBE_TREE_HERM", "1" if on else "0")
+        monkeypatch.setenv("PTSBE_TILE_MIN", "128" if on else "0")
+        monkeypatch.setenv("PTSBE_DESCENT_MULT", "1e18")
+        ctx = SamplerContext(hypersamples=8, dtype=dtype)
+        out = sample_proportional_batched(tpl, es, BatchPlan(sizes), 41, ctx)
+        return [[(r.bitstring, r.count) for r in recs] for recs in out], dict(ctx.stats.stage_events)
+
+    fast, ev1 = run(True)
+    plain, ev0 = run(False)
+    assert fast == plain and ev1 == ev0
+    if dtype == "complex128":
+        ops, finals = bridge.template_of(c)
+        _, want, events = O.run_proportional(ops, finals, sizes, bridge.oracle_errorsets(c, es), 41)
+        assert fast == want and ev1 == events
+
+
 def test_many_error_sets_single_shot_descent():
     """More error sets than a grid dimension holds (tree_build puts them on
     grid.x), one shot each: every shot is sampled and the histogram total is exact."""
