@@ -82,6 +82,7 @@ struct ptsbe_plan {
                                        // pays only with PTSBE_RECORD_LAYOUT=1
   uint32_t tile_min = 128;             // CTA-per-item programs: 4 x 4 register tiles for separable steps with at
                                        // least this many tiles, 2 x 2 below (keeps the CTA busy on mid-size steps)
+  uint32_t lane_tiny = 16;             // lane interpreter: steps of <= this many multiply-adds use the generic loop
   uint32_t descent_tile_max = 2048;    // fused descent: most consecutive work items a CTA takes at a time
   uint32_t tree_herm = 1;              // small descent tables: trees + Hermitian packing in one kernel
   uint32_t tc_steps = 0;               // opt-in (slower): large separable steps of CTA-per-item programs on tcgen05
@@ -553,6 +554,7 @@ static LaneArgs lane_args(ptsbe_plan* pl, Program& pr, uint32_t mode, const Leve
   a.n_leaves = pr.d.n_leaves;
   a.n_table_words = pr.d.n_table_words;
   a.n_levels = pl->f + 2;
+  a.tiny = pl->lane_tiny;
   return a;
 }
 
@@ -1893,6 +1895,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     pl->tiled_plain = (uint32_t)env_size("PTSBE_TILED_PLAIN", pl->tiled_plain);
     pl->tc_steps = (uint32_t)env_size("PTSBE_TC_STEPS", pl->tc_steps);
     pl->tree_herm = (uint32_t)env_size("PTSBE_TREE_HERM", pl->tree_herm);
+    pl->lane_tiny = (uint32_t)env_size("PTSBE_LANE_TINY", pl->lane_tiny);
     pl->descent_tile_max = (uint32_t)env_size("PTSBE_DESCENT_TILE_MAX", pl->descent_tile_max);
     pl->tile_min = (uint32_t)env_size("PTSBE_TILE_MIN", pl->tile_min);
     pl->prelaunch = (uint32_t)env_size("PTSBE_PRELAUNCH", pl->prelaunch);

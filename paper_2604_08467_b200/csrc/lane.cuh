@@ -90,6 +90,7 @@ struct LaneCtx {
   const uint8_t* kraus;
   uint32_t g, arena_fast;
   uint32_t ast;             // arena row pitch: LN_AST (shared memory) or 32 (global arena, BIG)
+  uint32_t tiny;            // steps with out_n * kn <= tiny (and kn <= 4) take the compact generic loop
 
   __device__ __forceinline__ uint32_t bit(uint32_t q, uint32_t slot) const {
     return (uint32_t)((pfx[(q >> 6) * LN_THREADS + slot] >> (63 - (q & 63))) & 1ull);
@@ -301,6 +302,9 @@ __device__ __forceinline__ void lane_step_kn(const LaneStep& t, const LaneOp<C>&
 struct LaneArgs {
   ExecArgs e;               // program, lists, output (HOIST record or VECTOR row per item)
   uint32_t n_leaves, n_table_words, n_levels;
+  uint32_t tiny;            // steps of at most this many multiply-adds (kn <= 4) run through the compact generic loop
+                            // instead of their unrolled variant: programs of many tiny steps (cfg5) otherwise stall
+                            // on instruction fetch across the interpreter's 60 specialised loops
   uint32_t ast;             // arena row pitch in elements; 0: LN_AST.  Kernels whose lanes only ever touch their
                             // own item's slice (lane_x.cuh) run with 32: a fifth less shared memory
 };
@@ -325,6 +329,7 @@ __device__ __forceinline__ LaneCtx<R> lane_setup(const LaneArgs& a, unsigned cha
   cx.tables = big ? a.e.tables : img + L.tables_off / 4;
   cx.levels = reinterpret_cast<const LevelDev*>(smem + L.levels_off);
   cx.ast = big ? 32u : (a.ast ? a.ast : (uint32_t)LN_AST);
+  cx.tiny = a.tiny;
   cx.arena_w = big ? reinterpret_cast<C*>(a.e.spill) +
                          ((size_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5)) * a.e.arena_fast * 32
                    : reinterpret_cast<C*>(smem + L.arena_off) +
@@ -373,6 +378,11 @@ __device__ __forceinline__ void lane_run(const LaneCtx<R>& cx, uint32_t s0, uint
     const uint32_t o_stride = to_arena ? cx.ast : 1u;
     const bool store = to_arena || live;
     if (t.flags & 4u) {
+      for (uint32_t c = 0; c < t.out_n; ++c) {
+        const C v = lane_element<R>(t, A, B, c);
+        if (store) O[c * o_stride] = v;
+      }
+    } else if (t.kn <= 4 && t.out_n * t.kn <= cx.tiny) {
       for (uint32_t c = 0; c < t.out_n; ++c) {
         const C v = lane_element<R>(t, A, B, c);
         if (store) O[c * o_stride] = v;
