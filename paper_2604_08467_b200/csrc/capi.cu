@@ -593,6 +593,7 @@ static void launch_lane_big(ptsbe_plan* pl, Program& pr, uint32_t mode, const Le
   a.e.result_kind = pr.d.result_kind;
   a.e.result_ref = pr.d.result_ref;
   a.e.item_bytes = pr.d.threads_per_item;  // MARGINAL: the mass is folded the way that many lanes would (lane.cuh)
+  a.tiny = 0;  // hundreds of steps per item: the unrolled variants pay here (measured: 20.5 against 22.6 ms on cfg5)
   const LaneLayout L = lane_layout(a.e.n_steps, a.n_leaves, 0, a.n_levels, 0, a.e.words, (uint32_t)sizeof(C));
   opt_in_smem((const void*)exec_lane_kernel<R, true>, 200 * 1024);
   if (pr.lane_big_blocks_per_sm == 0)
