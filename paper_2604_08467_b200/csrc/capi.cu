@@ -44,6 +44,7 @@ struct Program {
   // class-0 hoist program that can run one thread per error set with a global-memory arena (lane.cuh BIG)
   bool lane_big_ok = false;
   int lane_big_blocks_per_sm = 0;
+  double macs = 0;  // complex multiply-adds of one execution (sum over steps of outputs x contracted entries)
   bool tiled = false;  // most multiply-adds sit in large separable steps: register-tiled kernel variant
   // projection vector is x (x) conj(x): Hermitian-packed tree columns (lane.cuh HERM)
   bool herm = false;
@@ -105,6 +106,7 @@ struct ptsbe_plan {
   // are latency-bound, small batches because they do not fill the GPU, large ones because they wait on L2)
   uint32_t prelaunch = 1, prelaunch_max = 0xffffffffu;
   uint32_t side_priority = 1;
+  double eager_work_max = 8e9;         // complex multiply-adds per launch above which a hoist pass is not run early
   std::vector<cudaStream_t> side;
   uint64_t chunk_shots = 1ull << 26;
   size_t ext_budget = 48ull << 30;
@@ -993,6 +995,16 @@ struct RunOutput {
 };
 
 // Runs error sets [e0, e0+ne) of a resident batch through all stages.
+// A chunk is "dense" when some hoist pass has enough work to fill the GPU by itself (see run_chunk)
+static bool chunk_is_dense(const ptsbe_plan* pl, uint64_t n_sets, uint64_t shots) {
+  for (uint32_t j = 2; j <= pl->f; ++j)
+    for (uint32_t p = 0; p + 1 < j; ++p) {
+      const double items = std::min<double>((double)shots, (double)n_sets * std::pow(2.0, std::min<uint32_t>(pl->offsets[p], 60)));
+      if (items * pl->programs[j - 1][p].macs > pl->eager_work_max) return true;
+    }
+  return false;
+}
+
 // Per-error-set tables of the descent sampler for one stage: column sums over the binary tree of the batch
 // qubits (tree), Hermitian-packed (htree) when the fused kernel takes them that way.  Depends on the class-0
 // records only.
@@ -1131,6 +1143,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
   std::vector<DevBuf> stab_dev(f + 1);
   std::vector<cudaEvent_t> sev(f + 1, nullptr);           // last work queued on the stage's side stream
   std::vector<uint32_t> passes_done(f + 1, 0);            // leading passes of the stage already launched
+  std::vector<char> eager_off(f + 1, 0);                  // the stage has a pass that fills the GPU by itself
   struct PreTab { DevBuf tree, htree; bool done = false; };
   std::vector<PreTab> pre_tab(f + 1);
   for (uint32_t j = 1; j <= f; ++j) {
@@ -1138,7 +1151,12 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     stab[j].assign(f + 2, LevelDev{});
     memset(stab[j].data(), 0, sizeof(LevelDev) * (f + 2));
   }
-  const bool eager = pl->prelaunch && f >= 2 && ne <= pl->prelaunch_max;
+  // Dense regime (cfg3r1: hoist passes of 10^6-10^7 multiply-adds per item): every pass fills the GPU by itself
+  // and running light passes beside them only takes SMs away (7.8 s against 7.2 s per 10^5 error sets), so a
+  // chunk with any such pass runs everything in order.  Items of pass p are bounded by the chunk's shots and by
+  // error sets x 2^(qubits measured before stage p+1).
+  const bool dense = chunk_is_dense(pl, ne, chunk_shots);
+  const bool eager = pl->prelaunch && f >= 2 && ne <= pl->prelaunch_max && !dense;
   if (eager) {
     while (pl->side.size() < f) {
       // the side stream of an earlier stage outranks those of later stages (and the plan's own stream outranks
@@ -1159,6 +1177,10 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     const uint32_t p = L - 1;
     for (uint32_t j = L + 1; j <= f; ++j) {  // records and table rows first (allocations on the main stream)
       Program& pp = pl->programs[j - 1][p];
+      // a pass with enough work to fill the GPU gains nothing from running beside others (dense regime, cfg3r1:
+      // 808 ms with every pass early against 741 ms in order); it and the later passes of its stage stay in order
+      if ((double)lv[L].n * pp.macs > pl->eager_work_max) eager_off[j] = 1;
+      if (eager_off[j]) continue;
       LevelDev& row = stab[j][L];
       row.eset = lv[L].eset.as<uint32_t>();
       row.parent = lv[L].parent.as<uint32_t>();
@@ -1179,7 +1201,7 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     CK(cudaEventRecord(ready, st));
     for (uint32_t j = L + 1; j <= f; ++j) {
       Program& pp = pl->programs[j - 1][p];
-      if (!(pp.d.n_steps && pp.d.out_elems)) continue;
+      if (eager_off[j] || !(pp.d.n_steps && pp.d.out_elems)) continue;
       struct Swap { ptsbe_plan* pl; cudaStream_t keep; ~Swap() { pl->stream = keep; } } swap{pl, pl->stream};
       pl->stream = pl->side[j - 1];
       CK(cudaStreamWaitEvent(pl->stream, ready, 0));
@@ -1664,6 +1686,9 @@ static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stat
     // every level-(p+1) item
     std::vector<double> fan(pl->f + 1);
     for (uint32_t p = 0; p <= pl->f; ++p) fan[p] = std::pow(2.0, std::min<uint32_t>(pl->offsets[std::min(p, pl->f - 1)], 60));
+    // early hoist passes keep the records of all stages alive at once (decided for the whole batch: the walk
+    // below runs once per error set)
+    const bool sum_stages = pl->prelaunch && !chunk_is_dense(pl, bt->n_sets, bt->total_shots);
     auto ext_bytes_of = [&](uint64_t sh, uint64_t cnt) {
       size_t worst = 0;
       for (uint32_t j = 1; j <= pl->f; ++j) {
@@ -1672,7 +1697,8 @@ static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stat
           const double cap_items = std::min<double>((double)sh, (double)cnt * fan[p]);
           here += (size_t)(cap_items * pl->programs[j - 1][p].d.out_elems * pl->elem);
         }
-        worst = std::max(worst, here);
+        // early hoist passes (run_chunk) keep the records of ALL stages alive at once
+        worst = sum_stages ? worst + here : std::max(worst, here);
       }
       return worst;
     };
@@ -1901,6 +1927,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     pl->tile_min = (uint32_t)env_size("PTSBE_TILE_MIN", pl->tile_min);
     pl->prelaunch = (uint32_t)env_size("PTSBE_PRELAUNCH", pl->prelaunch);
     pl->prelaunch_max = (uint32_t)env_size("PTSBE_PRELAUNCH_MAX", pl->prelaunch_max);
+    if (const char* v = getenv("PTSBE_EAGER_WORK_MAX")) pl->eager_work_max = atof(v);
     pl->warp_run_len = (uint32_t)env_size("PTSBE_WARP_RUN_LEN", pl->warp_run_len);
     pl->stage_image_max = (uint32_t)env_size("PTSBE_STAGE_IMAGE_MAX", pl->stage_image_max);
     pl->lane = (uint32_t)env_size("PTSBE_LANE", pl->lane);
@@ -1965,6 +1992,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
             if (stw[17]) big += macs;
           }
           pr.tiled = big >= 1.5e5 && big >= 0.5 * all;
+          pr.macs = all;
         }
         if (pr.d.memo_elems) {
           if (!pr.d.memo_ptr || !pr.d.memo_idx || pr.d.n_memo_sites > pl->g || pr.d.n_steps >= 0xFFFF)
