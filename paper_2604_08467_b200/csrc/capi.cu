@@ -626,7 +626,7 @@ static void launch_hoist(ptsbe_plan* pl, Program& pr, const LevelDev* lv, const 
 }
 
 // ---- per-qubit descent sampler (descent.cuh) ----
-struct DescentShape { uint32_t nch = 0, dpad = 0; size_t smem = 0; };
+struct DescentShape { uint32_t nch = 0, dpad = 0; size_t smem = 0; bool fits = false; };
 
 static DescentShape descent_shape(const ptsbe_plan* pl, uint32_t D, uint32_t b) {
   DescentShape s;
@@ -636,7 +636,7 @@ static DescentShape descent_shape(const ptsbe_plan* pl, uint32_t D, uint32_t b) 
   if (!s.nch || b > 12) { s.nch = 0; return s; }
   s.dpad = DS_GS * s.nch * cpc;
   s.smem = ((size_t)s.dpad * pl->elem + (size_t)DS_GROUPS * 4) << b;
-  if (s.smem > 160 * 1024) s.nch = 0;
+  s.fits = s.smem <= 160 * 1024;  // the stand-alone kernel's table; the fused Hermitian kernel packs it in half
   return s;
 }
 
@@ -726,6 +726,39 @@ static bool lane_descent_fits(const ptsbe_plan* pl, const Program& pr, const Des
   const uint32_t nch_f = sh.nch * (DS_GS / LN_GS);
   const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4) + (((size_t)(LN_GS * nch_f + (nch_f >= 2 ? 0 : 1)) * 16) << b);
   return nch_f <= 8 && smem <= 200 * 1024;
+}
+
+// descent shape of the Hermitian-packed form: D reals per column
+static DescentShape herm_shape(const ptsbe_plan* pl, uint32_t D);
+
+// the fused kernel over Hermitian-packed columns (table of D reals per node)
+static bool lane_descent_fits_packed(const ptsbe_plan* pl, const Program& pr, const DescentShape& hsh, uint32_t b) {
+  if (!hsh.nch) return false;
+  const LaneLayout L = lane_layout(pr.d.n_steps, pr.d.n_leaves, pr.d.n_table_words, pl->f + 2,
+                                   pr.d.arena_fast_elems, pl->words, (uint32_t)pl->elem);
+  const size_t smem = (size_t)L.end + (size_t)LN_THREADS * (8 + 6 * 4) +
+                      (((size_t)(LN_GS * hsh.nch + (hsh.nch >= 2 ? 0 : 1)) * 16) << b);
+  return smem <= 200 * 1024;
+}
+
+// How a projection-form stage is sampled by descent: fused per-item steps + descent (packed table when the cut
+// vector is Hermitian, which also fits where the unpacked table does not: complex128 at D = 64, b = 8), the
+// stand-alone kernel, or not at all (ok == false: project + flat sampler).
+struct DescentChoice { DescentShape dsh, hsh; bool fused = false, ok = false; };
+static DescentChoice choose_descent(const ptsbe_plan* pl, const Program& prj, uint32_t b) {
+  DescentChoice c;
+  c.dsh = descent_shape(pl, prj.d.proj_d, b);
+  if (!c.dsh.nch) return c;
+  if (pl->lane && prj.lane_fused) {
+    if (prj.herm) {
+      c.hsh = herm_shape(pl, prj.d.proj_d);
+      c.fused = lane_descent_fits_packed(pl, prj, c.hsh, b);
+      if (!c.fused) c.hsh = DescentShape();
+    }
+    if (!c.fused) c.fused = lane_descent_fits(pl, prj, c.dsh, b);
+  }
+  c.ok = c.fused || c.dsh.fits;
+  return c;
 }
 
 static void launch_lane_descent(ptsbe_plan* pl, Program& pr, LaneDescentArgs& a, const DescentShape& sh,
@@ -1213,12 +1246,9 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       if (p == 0 && pl->descent && pl->stage_descent[j - 1] == 1 && pj.d.result_kind == 3 &&
           (!npp || (j == f && !np_exhaustive))) {
         const uint32_t bj = pl->sizes[j - 1];
-        const DescentShape dsh = descent_shape(pl, pj.d.proj_d, bj);
-        if (dsh.nch) {
-          const bool fused = pl->lane && pj.lane_fused && lane_descent_fits(pl, pj, dsh, bj);
-          DescentShape hsh;
-          if (fused && pj.herm) hsh = herm_shape(pl, pj.d.proj_d);
-          build_descent_tables(pl, pj, sext[j][0].p, pp.d.out_elems, ne, bj, dsh, hsh, fused, pre_tab[j].tree, pre_tab[j].htree);
+        const DescentChoice dc = choose_descent(pl, pj, bj);
+        if (dc.ok) {
+          build_descent_tables(pl, pj, sext[j][0].p, pp.d.out_elems, ne, bj, dc.dsh, dc.hsh, dc.fused, pre_tab[j].tree, pre_tab[j].htree);
           pre_tab[j].done = true;
         }
       }
@@ -1267,21 +1297,21 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
     DevBuf nnz((size_t)U * 4, st);
     // Stages whose work items carry few shots each are sampled by per-qubit descent over the
     // error set's conditional-marginal tree (descent.cuh) instead of project + sample.
-    DescentShape dsh;
+    DescentChoice dc;
     const int hint = pl->stage_descent[j - 1];
     const bool few_shots = hint >= 0 ? hint == 1 : (double)chunk_shots <= pl->descent_mult * (double)U;
     if (proj && pl->descent && j > 1 && U && few_shots &&
         (!npp || (j == f && !np_exhaustive)))  // choice without replacement / harvest need the full vector
-      dsh = descent_shape(pl, progs[j - 1].d.proj_d, b);
-    if (dsh.nch) {
+      dc = choose_descent(pl, progs[j - 1], b);
+    if (dc.ok) {
+      const DescentShape& dsh = dc.dsh;
       const Program& pr = progs[j - 1];
       Program& prj = progs[j - 1];
-      const bool fused = pl->lane && prj.lane_fused && lane_descent_fits(pl, prj, dsh, b);
+      const bool fused = dc.fused;
       // tree of conditional marginals per error set (Hermitian-packed when v = x (x) conj(x)); built up front
       // on the stage's side stream when the plan fixed the sampler (pre_tab), here otherwise
-      DescentShape hsh;
+      const DescentShape& hsh = dc.hsh;
       DevBuf htree, tree;
-      if (fused && prj.herm) hsh = herm_shape(pl, prj.d.proj_d);
       if (pre_tab[j].done) {
         htree = std::move(pre_tab[j].htree);
         tree = std::move(pre_tab[j].tree);
