@@ -94,8 +94,10 @@ struct ptsbe_plan {
   uint32_t warp_run_len = 512;         // ... fewer than this many work items each on average (lane.cuh warp_runs)
   uint32_t stage_image = 1;            // lane-group class-0 programs keep their image in shared memory ...
   uint32_t stage_image_max = 4096;     // ... for batches of at most this many error sets (executor.cuh STAGED)
-  uint32_t lane_big_min = 16384;       // class-0 hoists over at least this many error sets run one thread per
-                                       // error set with a global-memory arena (lane.cuh BIG)
+  uint32_t lane_big_min = 3072;        // class-0 hoists over at least this many error sets run one thread per
+                                       // error set with a global-memory arena (lane.cuh BIG).  With the passes of all
+                                       // stages concurrent on side streams the crossover against the lane-group
+                                       // kernel sits near 3000 error sets on cfg5 (16384 when they ran one by one)
   uint32_t descent = 1;                // per-qubit descent sampler for low-multiplicity stages
   double descent_mult = 4.0;           // ... used when shots / unique prefixes of the stage <= this
   // per stage: 1 descent, 0 flat, -1 decide per chunk (ptsbe_plan_set_stage_samplers)
