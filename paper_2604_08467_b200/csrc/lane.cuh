@@ -591,8 +591,9 @@ __global__ void __launch_bounds__(TH_WARPS * 32) tree_herm_kernel(const TreeHerm
       __syncwarp();
     }
     R* out = reinterpret_cast<R*>(a.packed) + (size_t)e * N * a.dpad_r;
+    const uint32_t dsh = 31 - __clz(a.dpad_r);  // dpad_r = lanes x chunks x reals per chunk: a power of two
     for (uint32_t x = lane; x < N * a.dpad_r; x += 32) {
-      const uint32_t node = x / a.dpad_r, sl = x % a.dpad_r;
+      const uint32_t node = x >> dsh, sl = x & (a.dpad_r - 1);
       R val = R(0);
       uint32_t dst = sl;
       if (sl < a.D) {
