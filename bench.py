@@ -325,6 +325,9 @@ def reference_arm(args):
         s_sets = args.cpu_sets
     if args.cpu_shots:
         s_shots = args.cpu_shots
+    elif args.steps > 5 and not (s_sets == sets and s_shots == shots):
+        # a step is a bounded sample (~18 s for cfg2 at the default size): keep K steps within a few minutes
+        s_shots = max(4, s_shots * 5 // args.steps)
     cache_json = None
     for _ in range(min(args.warmup, 1)):
         w = cpu_leg(c, sizes, args.seed, min(s_sets, cores), max(1, s_shots // 4), cores)
