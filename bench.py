@@ -822,11 +822,14 @@ def main():
         top_ms, top_name, items, launches, item_bytes, item_flops = top[:6]
         # DRAM bytes per work item measured by ncu --set full for this kernel, read from profiles/ncu_traffic.json
         ncu_item_traffic, traffic_src = None, None
+        lsu_view = None
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if len(top) > 6 and os.path.exists(tpath):
             ent = json.load(open(tpath)).get(top[6], {}).get(f"{args.workload}:{dtype}")
             if ent:
                 ncu_item_traffic, traffic_src = float(ent["dram_bytes_per_item"]), ent["source"]
+                if "lsu_wavefronts_pct_of_peak" in ent:
+                    lsu_view = {"frac": float(ent["lsu_wavefronts_pct_of_peak"]) / 100.0, "source": ent["lsu_source"]}
         hbm_peak, peak_src = peaks()
         t_s = top_ms * 1e-3
         achieved = items * item_bytes / t_s / 1e9 if t_s > 0 else 0.0
@@ -878,6 +881,8 @@ def main():
                 "launch_ms": top_ms / max(launches, 1), "share_of_step": top_ms / max(timed_ms, 1e-9),
                 "fma": {"achieved_tflops": tflops, "peak_tflops": fma_peak, "frac": tflops / fma_peak if fma_peak else None,
                         "flops_per_item": item_flops, "peak_source": "ptsbe_measure_fma_peak (independent FMA chains, this run)"},
+                # the unit the kernel actually saturates, from the committed ncu capture (not measured in this run)
+                "lsu_pipe": lsu_view,
             },
             "cpu_baseline": cpu,
             "parity": parity,
