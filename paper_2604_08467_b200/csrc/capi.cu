@@ -1164,10 +1164,6 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
   // stream waits for a stage's side stream where the stage begins.  The passes are latency-bound -- small
   // batches because no pass fills the GPU (cfg5 at E = 100: 2.96 -> 1.3 ms per step), large ones because they
   // wait on L2 and barriers (cfg5 at 10^5 sets 52.7 -> 48 ms, cfg2 37.1 -> 35.9 ms) -- so they overlap well.
-  struct SideGuard {  // no side-stream work may outlive the chunk's workspace
-    ptsbe_plan* pl; bool on = false;
-    ~SideGuard() { if (on) for (cudaStream_t q : pl->side) cudaStreamSynchronize(q); }
-  } side_guard{pl};
   struct EventBag {
     std::vector<cudaEvent_t> v;
     cudaEvent_t make() { cudaEvent_t e; CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); v.push_back(e); return e; }
@@ -1181,6 +1177,10 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
   std::vector<char> eager_off(f + 1, 0);                  // the stage has a pass that fills the GPU by itself
   struct PreTab { DevBuf tree, htree; bool done = false; };
   std::vector<PreTab> pre_tab(f + 1);
+  struct SideGuard {  // declared after the buffers, so destroyed before them: no side-stream work outlives the
+    ptsbe_plan* pl; bool on = false;  // chunk's records, tables or workspace, on any exit path
+    ~SideGuard() { if (on) for (cudaStream_t q : pl->side) cudaStreamSynchronize(q); }
+  } side_guard{pl};
   for (uint32_t j = 1; j <= f; ++j) {
     sext[j].resize(j);
     stab[j].assign(f + 2, LevelDev{});
