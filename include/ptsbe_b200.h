@@ -217,6 +217,16 @@ int ptsbe_sample(ptsbe_plan* plan, const uint8_t* kraus_idx, const uint32_t* sho
                  uint64_t** keys, uint32_t** rec_eset, uint64_t** counts,
                  uint64_t* n_records, ptsbe_run_stats* stats);
 
+/* ptsbe_sample(merged != 0) with the histogram returned as records [n_records][2] uint32
+ * (key, count), sorted by key: same run, same RNG streams, half the device-to-host bytes.
+ * key = the high 32 bits of ptsbe_sample's key word (qubit q at bit 31 - q).
+ * For plans that measure at most 32 qubits and calls of fewer than 2^32 shots in total
+ * (PTSBE_EINVAL otherwise).  replaces: the same fan-out + merge_records (engine.py:885-906, 815-829)
+ * for callers that fill RunResult.records from narrow integers. */
+int ptsbe_sample_packed(ptsbe_plan* plan, const uint8_t* kraus_idx, const uint32_t* shots,
+                        const uint32_t* eset_ids, uint64_t n_sets, uint64_t seed,
+                        uint32_t** records, uint64_t* n_records, ptsbe_run_stats* stats);
+
 /* replaces: sample_nonproportional per error set (engine.py:527-576), the data-harvesting mode.
  *   Every non-final stage branches each prefix into up to `nonfinal_shots` DISTINCT children
  *   (weighted choice without replacement, engine.py:549-556; outcomes below 2^-40 (c128) / 2^-17 (c64)

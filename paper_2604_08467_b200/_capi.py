@@ -30,7 +30,7 @@ EXPORTS = (
     "ptsbe_batch_destroy", "ptsbe_histogram_merge", "ptsbe_plan_greedy", "ptsbe_free",
     "ptsbe_batch_histogram_dev", "ptsbe_histogram_merge_dev", "ptsbe_free_dev",
     "ptsbe_measure_fma_peak", "ptsbe_sample_nonproportional", "ptsbe_batch_presample", "ptsbe_batch_kraus",
-    "ptsbe_plan_set_stage_samplers", "ptsbe_project_probe",
+    "ptsbe_plan_set_stage_samplers", "ptsbe_project_probe", "ptsbe_sample_packed",
 )
 
 
@@ -95,6 +95,8 @@ def load() -> ctypes.CDLL:
                                        ctypes.POINTER(U64), I]
     lib.ptsbe_sample.argtypes = [P, P, P, P, U64, U64, I, ctypes.POINTER(P), ctypes.POINTER(P),
                                  ctypes.POINTER(P), ctypes.POINTER(U64), ctypes.POINTER(RunStats)]
+    lib.ptsbe_sample_packed.argtypes = [P, P, P, P, U64, U64, ctypes.POINTER(P), ctypes.POINTER(U64),
+                                        ctypes.POINTER(RunStats)]
     lib.ptsbe_sample_nonproportional.argtypes = [P, P, P, U64, U64, U32, U32, ctypes.c_double, U32,
                                                  ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P),
                                                  ctypes.POINTER(P), ctypes.POINTER(U64), ctypes.POINTER(RunStats)]
@@ -335,6 +337,18 @@ class DevicePlan:
         counts = _take(c, n.value, np.uint64)
         esets = None if merged else _take(e, n.value, np.uint32)
         return keys, esets, counts, st
+
+    def sample_packed(self, kraus_idx, shots, eset_ids, seed: int):
+        """`sample(merged=True)` with the histogram as one [R, 2] uint32 array of (key, count) rows
+        (ptsbe_sample_packed: at most 32 measured qubits, fewer than 2^32 shots per call): half the
+        device-to-host bytes; key = high half of `sample`'s key word (qubit q at bit 31 - q).
+        Returns (records, RunStats)."""
+        kraus_idx, shots, ids = self._check_inputs(kraus_idx, shots, eset_ids)
+        r, n = ctypes.c_void_p(), ctypes.c_uint64()
+        st = RunStats()
+        check(load().ptsbe_sample_packed(self._h, _ptr(kraus_idx), _ptr(shots), _ptr(ids), shots.size,
+                                         seed & (2**64 - 1), ctypes.byref(r), ctypes.byref(n), ctypes.byref(st)))
+        return _take(r, n.value * 2, np.uint32).reshape(-1, 2), st
 
     def sample_nonproportional(self, kraus_idx, eset_ids, seed: int, nonfinal_shots: int, final_mode: str,
                                threshold: float, direct_count: int):

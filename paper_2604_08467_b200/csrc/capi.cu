@@ -2391,6 +2391,37 @@ static void fetch_merged(ptsbe_batch* bt, uint64_t** keys, uint64_t** counts, ui
   *n = nr;
 }
 
+// Merged histogram as [n][2] u32 (high half of the key word, count): plans of at most 32 measured qubits and runs of fewer
+// than 2^32 shots need 8 bytes per record on the PCIe link instead of 16.
+__global__ void pack_records_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ counts,
+                                    uint2* __restrict__ out, uint64_t n) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = make_uint2((uint32_t)(keys[i] >> 32), (uint32_t)counts[i]);  // qubit q at bit 31 - q
+}
+
+static void fetch_packed(ptsbe_batch* bt, uint32_t** records, uint64_t* n) {
+  ptsbe_plan* pl = bt->plan;
+  if (pl->words != 1 || pl->n > 32) throw Failure(PTSBE_EINVAL, "packed records need at most 32 measured qubits");
+  if (bt->total_shots >= (1ull << 32)) throw Failure(PTSBE_EINVAL, "packed records need fewer than 2^32 shots per call");
+  const uint64_t nr = bt->merged.n;
+  uint32_t* r = (uint32_t*)g_host_pool.get(std::max<uint64_t>(nr, 1) * 8);
+  if (!r) throw Failure(PTSBE_ECAPACITY, "host allocation of the histogram failed");
+  if (nr) {
+    WorkspaceScope tmp_scope(&bt->ws_tmp());
+    const Workspace::Mark mark = bt->ws_tmp().mark();
+    DevBuf packed(nr * 8, pl->stream);
+    pack_records_kernel<<<cdiv(nr, 256), 256, 0, pl->stream>>>(bt->merged.keys.as<uint64_t>(), bt->merged.counts.as<uint64_t>(),
+                                                               packed.as<uint2>(), nr);
+    g_launches++;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(r, packed.p, nr * 8, cudaMemcpyDeviceToHost, pl->stream));
+    CK(cudaStreamSynchronize(pl->stream));
+    bt->ws_tmp().rewind(mark);
+  }
+  *records = r;
+  *n = nr;
+}
+
 int ptsbe_batch_fetch(ptsbe_batch* bt, uint64_t** keys, uint64_t** counts, uint64_t* n_records) {
   return guarded([&] {
     if (!bt) throw Failure(PTSBE_EINVAL, "null batch");
@@ -2444,10 +2475,10 @@ static void fetch_per_set(ptsbe_plan* pl, const RunOutput& out, bool with_probs,
   if (probs) *probs = pr;
 }
 
-int ptsbe_sample(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t* shots,
-                 const uint32_t* eset_ids, uint64_t n_sets, uint64_t seed, int merged,
-                 uint64_t** keys, uint32_t** rec_eset, uint64_t** counts, uint64_t* n_records,
-                 ptsbe_run_stats* stats) {
+static int sample_host(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t* shots,
+                       const uint32_t* eset_ids, uint64_t n_sets, uint64_t seed, int merged,
+                       uint64_t** keys, uint32_t** rec_eset, uint64_t** counts, uint32_t** packed,
+                       uint64_t* n_records, ptsbe_run_stats* stats) {
   ptsbe_batch* bt = nullptr;
   ptsbe_run_stats local;
   if (!stats) stats = &local;
@@ -2468,7 +2499,9 @@ int ptsbe_sample(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t* shots
     run_batch(bt, seed, merged, stats);
     CK(cudaEventRecord(e2, pl->stream));
     const uint32_t words = pl->words;
-    if (merged) {
+    if (packed) {
+      fetch_packed(bt, packed, n_records);
+    } else if (merged) {
       fetch_merged(bt, keys, counts, n_records);
       if (rec_eset) *rec_eset = nullptr;
     } else {
@@ -2480,11 +2513,31 @@ int ptsbe_sample(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t* shots
     CK(cudaEventElapsedTime(&stats->h2d_ms, e0, e1));
     CK(cudaEventElapsedTime(&stats->d2h_ms, e2, e3));
     stats->h2d_bytes = n_sets * pl->g + n_sets * 4 * (eset_ids ? 2 : 1);
-    stats->d2h_bytes = *n_records * (8ull * words + (merged ? 8 : 8));
+    stats->d2h_bytes = packed ? *n_records * 8ull : *n_records * (8ull * words + (merged ? 8 : 12));
   });
   ptsbe_batch_destroy(bt);
   if (e0) { cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2); cudaEventDestroy(e3); }
   return rc;
+}
+
+int ptsbe_sample(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t* shots,
+                 const uint32_t* eset_ids, uint64_t n_sets, uint64_t seed, int merged,
+                 uint64_t** keys, uint32_t** rec_eset, uint64_t** counts, uint64_t* n_records,
+                 ptsbe_run_stats* stats) {
+  return sample_host(pl, kraus_idx, shots, eset_ids, n_sets, seed, merged, keys, rec_eset, counts, nullptr,
+                     n_records, stats);
+}
+
+int ptsbe_sample_packed(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t* shots,
+                        const uint32_t* eset_ids, uint64_t n_sets, uint64_t seed,
+                        uint32_t** records, uint64_t* n_records, ptsbe_run_stats* stats) {
+  const int pre = guarded([&] {
+    if (!pl || !records || !n_records) throw Failure(PTSBE_EINVAL, "null argument");
+    if (pl->words != 1 || pl->n > 32) throw Failure(PTSBE_EINVAL, "packed records need at most 32 measured qubits");
+  });
+  if (pre) return pre;
+  return sample_host(pl, kraus_idx, shots, eset_ids, n_sets, seed, 1, nullptr, nullptr, nullptr, records,
+                     n_records, stats);
 }
 
 int ptsbe_sample_nonproportional(ptsbe_plan* pl, const uint8_t* kraus_idx, const uint32_t* eset_ids,

@@ -1144,6 +1144,10 @@ def run_ptsbe(c: Circuit, config: RunConfig, cache: Optional[PathCache] = None,
         if nonprop:
             keys, esets, counts, probs, st = pipe.device_plan.sample_nonproportional(
                 kraus_idx, ids, config.seed, plan.nonfinal_shots, plan.final_mode, plan.threshold, plan.direct_count)
+        elif plan.n <= 32 and int(np.asarray(shots, dtype=np.uint64).sum()) < 2**32:
+            # (key, count) rows as two u32: half the bytes on the PCIe link, same records
+            rec, st = pipe.device_plan.sample_packed(kraus_idx, shots, ids, config.seed)
+            keys, counts = rec[:, :1].astype(np.uint64) << np.uint64(32), rec[:, 1]
         else:
             keys, _, counts, st = pipe.device_plan.sample(kraus_idx, shots, ids, config.seed, merged=True)
         loop_s = time.perf_counter() - t0

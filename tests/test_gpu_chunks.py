@@ -68,6 +68,39 @@ def test_multi_chunk_outputs_equal_single_chunk(which):
         many.close()
 
 
+@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+def test_packed_records_equal_the_wide_histogram(dtype):
+    """ptsbe_sample_packed: the merged histogram as (key, count) rows of two u32 -- the same records as
+    ptsbe_sample(merged), single- and multi-chunk; refused for plans of more than 32 measured qubits."""
+    name, c, sizes = _cases()[0]
+    sets, shots, seed = 23, 60, 5
+    rows = workloads.presample_matrix(c, sets, np.random.default_rng(8))
+    sh = np.full(sets, shots, np.uint32)
+    sh[::5] = 7
+    ids = (np.arange(sets, dtype=np.uint32) * 3 + 11)
+    one, many = _pipe(c, sizes, shots, dtype=dtype), _pipe(c, sizes, shots, chunk_shots=150, dtype=dtype)
+    try:
+        k, _, cnt, s0 = one.device_plan.sample(rows, sh, ids, seed, merged=True)
+        for pipe in (one, many):
+            rec, st = pipe.device_plan.sample_packed(rows, sh, ids, seed)
+            assert rec.dtype == np.uint32 and rec.shape == (k.shape[0], 2)
+            np.testing.assert_array_equal(rec[:, 0].astype(np.uint64) << np.uint64(32), k[:, 0])
+            np.testing.assert_array_equal(rec[:, 1].astype(np.uint64), cnt)
+            assert int(st.d2h_bytes) == 8 * rec.shape[0] and int(s0.d2h_bytes) == 16 * rec.shape[0]
+            assert int(st.n_records) == rec.shape[0]
+    finally:
+        one.close()
+        many.close()
+    _, c2, sizes2 = _cases()[1]
+    wide = _pipe(c2, sizes2, 4)
+    try:
+        rows2 = workloads.presample_matrix(c2, 2, np.random.default_rng(1))
+        with pytest.raises(ValueError, match="32 measured qubits"):
+            wide.device_plan.sample_packed(rows2, np.full(2, 4, np.uint32), None, 1)
+    finally:
+        wide.close()
+
+
 @pytest.mark.parametrize("final_mode", ["exhaustive", "direct"])
 def test_nonproportional_multi_chunk_equals_single_chunk(final_mode):
     c, _ = workloads.hea(10, 3, gamma=0.05, p=0.08, seed=3)
