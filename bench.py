@@ -830,7 +830,12 @@ def main():
                               n_items, launches_j, pr.proj_d * elem + pr.out_elems * real + m_bytes,
                               4.0 * pr.proj_d * pr.out_elems))
             else:
-                cands.append((marg[j], f"exec_kernel (marginal pass), stage {j + 1}", n_items, launches_j,
+                # from 3072 error sets on, a stage-1 pass of a lane-sized program runs one thread per error set
+                # (exec_lane_kernel<R, 1>, capi.cu lane_big_min), below that the CTA / lane-group kernels
+                mname = "exec_lane_kernel (one thread per error set)" if (j == 0 and sets >= 3072 and pr.threads <= 32) \
+                    else "exec_kernel"
+                cands.append((marg[j], f"{mname} (marginal pass; its span also holds the concurrent up-front passes "
+                                       f"of later stages), stage {j + 1}", n_items, launches_j,
                               pr.ext_read_elems * elem + 8 + 8 * words + pr.out_elems * real + 16, 8.0 * pr.flops))
         top = max(cands, key=lambda x: x[0])
         top_ms, top_name, items, launches, item_bytes, item_flops = top[:6]

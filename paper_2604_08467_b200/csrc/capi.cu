@@ -94,6 +94,7 @@ struct ptsbe_plan {
   uint32_t warp_run_len = 512;         // ... fewer than this many work items each on average (lane.cuh warp_runs)
   uint32_t stage_image = 1;            // lane-group class-0 programs keep their image in shared memory ...
   uint32_t stage_image_max = 4096;     // ... for batches of at most this many error sets (executor.cuh STAGED)
+  bool raw_final = true;               // PTSBE_RAW_FINAL=0: per-item merge of the final stage's draws even for merged output
   uint32_t lane_big_min = 3072;        // class-0 hoists over at least this many error sets run one thread per
                                        // error set with a global-memory arena (lane.cuh BIG).  With the passes of all
                                        // stages concurrent on side streams the crossover against the lane-group
@@ -1027,6 +1028,7 @@ struct RunOutput {
   // final records of one chunk, device resident (level f+1): eset rows, keys, counts
   DevBuf eset, keys, counts;
   uint64_t n = 0;
+  bool unit_counts = false;  // every record is one raw draw (count 1): the merge may sort keys alone
 };
 
 // Runs error sets [e0, e0+ne) of a resident batch through all stages.
@@ -1103,7 +1105,8 @@ static void build_descent_tables(ptsbe_plan* pl, Program& prj, const void* rec0,
 static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* shots_dev,
                       const uint32_t* ids_dev, uint32_t ne, uint64_t chunk_shots, uint64_t seed,
                       RunOutput& out, ptsbe_run_stats* stats, unsigned long long* flag_dev,
-                      uint32_t* flag_count_dev, Workspace& ws_out, const NonpropParams* npp = nullptr) {
+                      uint32_t* flag_count_dev, Workspace& ws_out, const NonpropParams* npp = nullptr,
+                      bool merged_out = false) {
   cudaStream_t st = pl->stream;
   const uint32_t f = pl->f, words = pl->words;
   const bool np_exhaustive = npp && npp->final_mode == 0;
@@ -1362,6 +1365,12 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
         DescentShape fsh = dsh;  // chunks per lane of the fused kernel's LN_GS-lane groups
         fsh.nch = dsh.nch * (DS_GS / LN_GS);
         launch_lane_descent(pl, prj, fa, hsh.nch ? hsh : fsh, ne);
+        // Final stage of a run whose records are merged over error sets anyway: the raw draws (count 1 each,
+        // nnz = multiplicity) go to the histogram as they are -- the descent sampler is chosen for stages with
+        // about one draw per item, so the per-item merge removes next to nothing and the sort can then move
+        // keys alone (merge_records of reference engine.py:815-829 sums equal bitstrings either way).
+        const bool raw_final = merged_out && j == f && !npp && pl->raw_final;
+        if (raw_final) out.unit_counts = true;
         DedupArgs dd;
         dd.slot_off = da.slot_off;
         dd.slot_index = da.slot_index;
@@ -1372,9 +1381,11 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
         dd.first_item = 0;
         dd.n_items = U;
         dd.b = b;
-        dedup_kernel<<<cdiv(U, 256), 256, 0, st>>>(dd);
-        dedup_big_kernel<<<pl->sm_count, 256, sizeof(uint32_t) << b, st>>>(dd);
-        g_launches += 2;
+        if (!raw_final) {
+          dedup_kernel<<<cdiv(U, 256), 256, 0, st>>>(dd);
+          dedup_big_kernel<<<pl->sm_count, 256, sizeof(uint32_t) << b, st>>>(dd);
+          g_launches += 2;
+        }
         CK(cudaGetLastError());
         log.end();
         stats->marg_launches[j - 1]++;
@@ -1769,7 +1780,7 @@ static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stat
       const Workspace::Mark mark = bt->ws_tmp().mark();
       run_chunk(pl, bt->kraus.as<uint8_t>() + e * pl->g, bt->shots.as<uint32_t>() + e,
                 bt->ids.as<uint32_t>() + e, (uint32_t)cnt, sh, seed, outs[c], stats,
-                flag.as<unsigned long long>(), flag.as<uint32_t>() + 2, bt->ws_out());
+                flag.as<unsigned long long>(), flag.as<uint32_t>() + 2, bt->ws_out(), nullptr, merged != 0);
       bt->ws_tmp().rewind(mark);  // run_chunk returns with the stream drained
     }
     total_rec += outs[c].n;
@@ -1791,7 +1802,7 @@ static void run_batch(ptsbe_batch* bt, uint64_t seed, int merged, ptsbe_run_stat
   if (merged) {
     if (chunks.size() == 1) {
       reduce_by_key(outs[0].keys.as<uint64_t>(), outs[0].n, words, outs[0].counts.as<uint32_t>(),
-                    nullptr, outs[0].n, pl->n, bt->merged, st);
+                    nullptr, outs[0].n, pl->n, bt->merged, st, outs[0].unit_counts);
     } else {
       // concatenate chunk records (SoA with common stride), then reduce
       DevBuf keys(total_rec * 8 * words, st), counts(total_rec * 4, st);
@@ -1949,6 +1960,7 @@ int ptsbe_plan_create(const ptsbe_plan_desc* d, int device, ptsbe_plan** out) {
     pl->lane_x = (uint32_t)env_size("PTSBE_LANE_X", pl->lane_x);
     pl->lane_chain = (uint32_t)env_size("PTSBE_LANE_CHAIN", pl->lane_chain);
     pl->lane_big_min = (uint32_t)env_size("PTSBE_LANE_BIG_MIN", pl->lane_big_min);
+    pl->raw_final = env_size("PTSBE_RAW_FINAL", 1) != 0;
     pl->stage_image = (uint32_t)env_size("PTSBE_STAGE_IMAGE", pl->stage_image);
     pl->warp_runs = (uint32_t)env_size("PTSBE_WARP_RUNS", pl->warp_runs);
     pl->tiled_plain = (uint32_t)env_size("PTSBE_TILED_PLAIN", pl->tiled_plain);

@@ -113,17 +113,22 @@ __device__ __forceinline__ void hist_tile_load(const K* __restrict__ keys,
         k[4 * i] = v.x; k[4 * i + 1] = v.y; k[4 * i + 2] = v.z; k[4 * i + 3] = v.w;
       }
     }
-    const uint4* cp = reinterpret_cast<const uint4*>(counts + base);
+    if (counts) {
+      const uint4* cp = reinterpret_cast<const uint4*>(counts + base);
 #pragma unroll
-    for (int i = 0; i < HT_ITEMS / 4; ++i) {
-      const uint4 v = cp[i];
-      c[4 * i] = v.x; c[4 * i + 1] = v.y; c[4 * i + 2] = v.z; c[4 * i + 3] = v.w;
+      for (int i = 0; i < HT_ITEMS / 4; ++i) {
+        const uint4 v = cp[i];
+        c[4 * i] = v.x; c[4 * i + 1] = v.y; c[4 * i + 2] = v.z; c[4 * i + 3] = v.w;
+      }
+    } else {  // records of one raw draw each
+#pragma unroll
+      for (int i = 0; i < HT_ITEMS; ++i) c[i] = 1;
     }
   } else {
 #pragma unroll
     for (int i = 0; i < HT_ITEMS; ++i) {
       k[i] = base + i < n ? keys[base + i] : K(0);
-      c[i] = base + i < n ? counts[base + i] : 0;
+      c[i] = base + i < n ? (counts ? counts[base + i] : 1u) : 0;
     }
   }
   prev = (base && base < n) ? keys[base - 1] : K(0);
@@ -240,7 +245,7 @@ inline void sorted_pairs_tail(const K* sk, const uint32_t* sc, uint64_t n, Histo
 // keys: SoA [words][stride] u64 on device; counts u32 (counts64 == nullptr) or u64.
 inline void reduce_by_key(const uint64_t* keys, uint64_t stride, uint32_t words,
                           const uint32_t* counts32, const uint64_t* counts64, uint64_t n,
-                          uint32_t key_bits, Histogram& out, cudaStream_t st) {
+                          uint32_t key_bits, Histogram& out, cudaStream_t st, bool unit_counts = false) {
   out.n = 0;
   if (n == 0) { out.keys.alloc(0, st); out.counts.alloc(0, st); return; }
   if (n >= (1ull << 32)) throw Failure(PTSBE_ECAPACITY, "more than 2^32 records in one reduce");
@@ -252,8 +257,31 @@ inline void reduce_by_key(const uint64_t* keys, uint64_t stride, uint32_t words,
     // sorted arrays.  Keys of at most 32 bits are sorted as u32 (8 instead of 12 bytes per pair
     // and radix pass).
     const int used = (int)std::min<uint32_t>(key_bits, 64);
-    sorted_counts.alloc(n * 4, st);
     size_t tmp_bytes = 0;
+    if (unit_counts) {
+      // every count is 1 (raw draws of a final descent stage): the sort moves keys alone and the tail
+      // counts run lengths
+      if (used <= 32) {
+        DevBuf k32(n * 4, st), k32s(n * 4, st);
+        narrow_keys_kernel<<<G, T, 0, st>>>(keys, k32.as<uint32_t>(), n);
+        CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, k32.as<uint32_t>(), k32s.as<uint32_t>(), (int)n,
+                                          32 - used, 32, st));
+        DevBuf tmp(tmp_bytes, st);
+        CK(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, k32.as<uint32_t>(), k32s.as<uint32_t>(), (int)n,
+                                          32 - used, 32, st));
+        g_launches += 2 + (used + 7) / 8 * 2;
+        sorted_pairs_tail<uint32_t>(k32s.as<uint32_t>(), nullptr, n, out, st);
+      } else {
+        kout.alloc(n * 8, st);
+        CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, kout.as<uint64_t>(), (int)n, 64 - used, 64, st));
+        DevBuf tmp(tmp_bytes, st);
+        CK(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, keys, kout.as<uint64_t>(), (int)n, 64 - used, 64, st));
+        g_launches += 1 + (used + 7) / 8 * 2;
+        sorted_pairs_tail<uint64_t>(kout.as<uint64_t>(), nullptr, n, out, st);
+      }
+      return;
+    }
+    sorted_counts.alloc(n * 4, st);
     if (used <= 32) {
       DevBuf k32(n * 4, st), k32s(n * 4, st);
       narrow_keys_kernel<<<G, T, 0, st>>>(keys, k32.as<uint32_t>(), n);

@@ -495,6 +495,40 @@ def test_early_hoist_passes_fused_tables_and_tile_shapes_do_not_change_records(m
         assert fast == want and ev1 == events
 
 
+@pytest.mark.parametrize("dtype", ["complex128", "complex64"])
+def test_raw_final_draws_give_the_same_merged_histogram(monkeypatch, dtype):
+    """Merged output of a run whose final stage is sampled by the fused descent kernels: the raw draws go to
+    the histogram sort as records of count 1 (no per-item merge; keys-only radix sort; csrc/capi.cu raw_final).
+    merge_records (reference engine.py:815-829) sums equal bitstrings either way: the merged histogram equals
+    the one built with the per-item merge, the merge of the per-error-set records, and the oracle's in
+    complex128.  20 shots over 16 final outcomes per prefix: many duplicate draws per work item."""
+    c, _ = workloads.random40(14, 70, seed=3)
+    sizes = (5, 5, 4)
+    tpl = CircuitNetwork.from_circuit(c)
+    es = presample_errors(c, 300, "uniform", shots_per_set=20, rng=np.random.default_rng(12))
+    monkeypatch.setenv("PTSBE_DESCENT_MULT", "1e18")
+    cfg = RunConfig(n=c.n, g=len(c.gates), batch_sizes=sizes, seed=23, hypersamples=8, dtype=dtype,
+                    error_sets=len(es), total_shots=sum(k.m for k in es))
+
+    def run(raw):
+        monkeypatch.setenv("PTSBE_RAW_FINAL", "1" if raw else "0")
+        res = run_ptsbe(c, cfg, errorsets=es)
+        assert res.total_count == sum(k.m for k in es)
+        return [(r.bitstring, r.count) for r in res.records]
+
+    raw, merged_per_item = run(True), run(False)
+    assert raw == merged_per_item
+    ctx = SamplerContext(hypersamples=8, dtype=dtype)
+    per_set = sample_proportional_batched(tpl, es, BatchPlan(sizes), 23, ctx)
+    assert sum(ctx.stats.descent_events.values()) > 0
+    assert raw == [(r.bitstring, r.count) for r in merge_records(per_set)]
+    assert max(n for _, n in raw) > 1
+    if dtype == "complex128":
+        ops, finals = bridge.template_of(c)
+        _, want, _ = O.run_proportional(ops, finals, sizes, bridge.oracle_errorsets(c, es), 23)
+        assert raw == O.merge_histograms(want)
+
+
 def test_many_error_sets_single_shot_descent():
     """More error sets than a grid dimension holds (tree_build puts them on
     grid.x), one shot each: every shot is sampled and the histogram total is exact."""
