@@ -1122,7 +1122,6 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
   std::vector<LevelDev> table(f + 2);
   memset(table.data(), 0, sizeof(LevelDev) * table.size());
   DevBuf table_dev((f + 2) * sizeof(LevelDev), st);
-  DevBuf seg_start((size_t)ne * 4, st);
   DevBuf slot_index(chunk_shots * 4, st), slot_count(chunk_shots * 4, st);
   DevBuf scal(16, st);
   DevBuf set_mass((size_t)ne * 8, st);  // stage-1 mass (trajectory weight) of every error set
@@ -1567,6 +1566,16 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       ea.words = words;
       ea.offset = pl->offsets[j - 1];
       ea.b = b;
+      ea.p_rank = ea.p_gid = nullptr;
+      ea.c_rank = ea.c_gid = nullptr;
+      if (j < f) {  // rank and global id of the children, written by the expansion itself
+        nx.rank.alloc((size_t)Un * 4, st);
+        nx.gid.alloc((size_t)Un * 4, st);
+        ea.p_rank = cur.rank.as<uint32_t>();
+        ea.p_gid = cur.gid.as<uint32_t>();
+        ea.c_rank = nx.rank.as<uint32_t>();
+        ea.c_gid = nx.gid.as<uint32_t>();
+      }
       // few children per parent (late stages): parent-side scatter; otherwise child-side binary search
       if (words <= 4 && (uint64_t)Un <= 4ull * U)
         expand_scatter_kernel<<<cdiv(U, T), T, 0, st>>>(ea, nnz.as<uint32_t>());
@@ -1582,16 +1591,8 @@ static void run_chunk(ptsbe_plan* pl, const uint8_t* kraus_dev, const uint32_t* 
       }
       if (j < f) {
         nx.slot_off.alloc((size_t)Un * 4, st);
-        nx.rank.alloc((size_t)Un * 4, st);
-        nx.gid.alloc((size_t)Un * 4, st);
         exclusive_scan<uint32_t, uint32_t>(nx.mult.as<uint32_t>(), nx.slot_off.as<uint32_t>(), Un,
                                            nullptr, st);
-        segment_start_kernel<<<cdiv(Un, T), T, 0, st>>>(nx.eset.as<uint32_t>(), Un,
-                                                        seg_start.as<uint32_t>());
-        rank_kernel<<<cdiv(Un, T), T, 0, st>>>(nx.eset.as<uint32_t>(), seg_start.as<uint32_t>(),
-                                               ids_dev, Un, nx.rank.as<uint32_t>(),
-                                               nx.gid.as<uint32_t>());
-        g_launches += 2;
       }
     }
     CK(cudaGetLastError());

@@ -595,6 +595,10 @@ struct ExpandArgs {
   // child level
   uint32_t* c_eset; uint32_t* c_parent; uint64_t* c_prefix; uint32_t* c_mult; uint32_t c_n;
   uint32_t words, offset, b;  // child prefix = parent prefix with b bits appended at qubit `offset`
+  // Philox counters of the children (null at the final stage): rank = position inside the error set's run of
+  // items, gid = global error-set id.  Items of one error set are contiguous at every level, so parent w's first
+  // sibling is w - p_rank[w] and the error set's first child is child_base[w - p_rank[w]].
+  const uint32_t* p_rank; const uint32_t* p_gid; uint32_t* c_rank; uint32_t* c_gid;
 };
 
 __global__ void expand_kernel(const ExpandArgs a) {
@@ -611,6 +615,10 @@ __global__ void expand_kernel(const ExpandArgs a) {
   a.c_eset[c] = a.p_eset[w];
   a.c_parent[c] = w;
   a.c_mult[c] = a.slot_count[slot];
+  if (a.c_rank) {
+    a.c_rank[c] = c - a.child_base[w - a.p_rank[w]];
+    a.c_gid[c] = a.p_gid[w];
+  }
   // qubit q -> word q/64, bit 63-(q%64); first batch qubit = MSB of idx (engine.py:489-490)
   for (uint32_t wd = 0; wd < a.words; ++wd) {
     uint64_t v = a.p_prefix[(size_t)wd * a.p_n + w];
@@ -637,12 +645,21 @@ __global__ void expand_scatter_kernel(const ExpandArgs a, const uint32_t* __rest
   uint64_t pv[4];
   const uint32_t words = min(a.words, 4u);
   for (uint32_t wd = 0; wd < words; ++wd) pv[wd] = a.p_prefix[(size_t)wd * a.p_n + w];
+  uint32_t rank0 = 0, gid = 0;
+  if (a.c_rank) {
+    rank0 = base - a.child_base[w - a.p_rank[w]];
+    gid = a.p_gid[w];
+  }
   for (uint32_t k = 0; k < n; ++k) {
     const uint32_t c = base + k;
     const uint32_t idx = a.slot_index[slot0 + k];
     a.c_eset[c] = es;
     a.c_parent[c] = w;
     a.c_mult[c] = a.slot_count[slot0 + k];
+    if (a.c_rank) {
+      a.c_rank[c] = rank0 + k;
+      a.c_gid[c] = gid;
+    }
     for (uint32_t wd = 0; wd < words; ++wd) {
       uint64_t v = pv[wd];
       const int q0 = (int)wd * 64, q1 = q0 + 64;
@@ -656,21 +673,6 @@ __global__ void expand_scatter_kernel(const ExpandArgs a, const uint32_t* __rest
   }
 }
 
-// rank of an item inside its error set = index - first index of that error set
-__global__ void segment_start_kernel(const uint32_t* eset, uint32_t n, uint32_t* seg_start) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  if (i == 0 || eset[i] != eset[i - 1]) seg_start[eset[i]] = i;
-}
-__global__ void rank_kernel(const uint32_t* eset, const uint32_t* seg_start,
-                            const uint32_t* global_id, uint32_t n, uint32_t* rank,
-                            uint32_t* gid) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t e = eset[i];
-  rank[i] = i - seg_start[e];
-  gid[i] = global_id[e];
-}
 
 __global__ void iota_kernel(uint32_t* p, uint32_t n, uint32_t add) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
